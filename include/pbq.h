@@ -1,0 +1,139 @@
+/*
+ * pbq.h — C ABI of the B200-native PbP-QLP library (libpbq.so).
+ *
+ * The reference exposes PbP-QLP only as a Python function,
+ *   pbpqlp.pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True) -> QlpFactors
+ *   (/root/reference/pkg/src/pbpqlp/algorithms.py:209-260),
+ * with no FFI or plugin registry.  These entry points are the
+ * device-side boundary that the drop-in Python function (package
+ * `paper_2103_07245_b200`) binds through ctypes.  Every entry
+ * point takes plain pointers and sizes; no torch types cross the boundary.
+ *
+ * Conventions
+ *  - All matrices are FP64, row-major, in device memory; `ld*` is the row
+ *    stride in elements and must be even, base pointers 16-byte aligned.
+ *  - Work is enqueued on `stream` (a cudaStream_t passed as void*); no entry
+ *    point synchronises the host except pbq_ctx_create.
+ *  - Scratch memory is caller-owned: query the size, pass a device buffer.
+ *    A workspace must not be shared by calls that may run concurrently.
+ *  - Return value is a pbq_status; pbq_last_error() describes the last failure.
+ *  - A context is bound to one device and is not thread-safe.
+ */
+#ifndef PBQ_H_
+#define PBQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PBQ_OK = 0,
+  PBQ_ERR_PARAM = 1,     /* maps to pbpqlp ParameterError  (exceptions.py:8)  */
+  PBQ_ERR_DIM = 2,       /* maps to pbpqlp DimensionError  (exceptions.py:12) */
+  PBQ_ERR_NONFINITE = 3, /* maps to pbpqlp MatrixInputError (exceptions.py:16) */
+  PBQ_ERR_CUDA = 4,
+  PBQ_ERR_NCCL = 5,
+  PBQ_ERR_OOM = 6,
+  PBQ_ERR_UNSUPPORTED = 7
+} pbq_status;
+
+typedef struct pbq_ctx pbq_ctx;
+
+/* Context lifetime (one device).  Replaces nothing in the reference: the
+ * reference is stateless; the context only caches device
+ * properties and launch plans. */
+int pbq_ctx_create(int device, pbq_ctx** out);
+int pbq_ctx_destroy(pbq_ctx* ctx);
+const char* pbq_last_error(const pbq_ctx* ctx);
+int pbq_ctx_sm_count(const pbq_ctx* ctx);
+/* Kernel launches enqueued by this context since creation (evidence for the
+ * bench's "gpu_launches" count). */
+int64_t pbq_ctx_launch_count(const pbq_ctx* ctx);
+
+/* C = alpha·Aᵀ·B + beta·C.  A is K×M (lda), B is K×N (ldb), C is M×N (ldc).
+ * Replaces `_PassCounter.apply_t` (`a.T @ block`, algorithms.py:182-184).
+ * If `nonfinite` is non-null, *nonfinite is OR-ed with 1 when A holds an
+ * Inf/NaN (the `check_matrix` isfinite scan, validation.py:47, fused into the
+ * pass).  Workspace: pbq_gemm_workspace_bytes(). */
+int pbq_gemm_tn(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                int32_t* nonfinite, void* workspace, size_t workspace_bytes, void* stream);
+
+/* C = alpha·A·B + beta·C.  A is M×K (lda), B is K×N (ldb), C is M×N (ldc).
+ * Replaces `_PassCounter.apply` (`a @ block`, algorithms.py:178-180) and
+ * `pbar @ w` (algorithms.py:258). */
+int pbq_gemm_nn(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                int32_t* nonfinite, void* workspace, size_t workspace_bytes, void* stream);
+
+int pbq_gemm_workspace_bytes(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, size_t* bytes);
+
+/* Unpivoted Householder QR of an m×n matrix (m ≥ n ≥ 1), in place.
+ * Replaces `householder_qr` (linalg.py:106-115, LAPACK dgeqrf+dorgqr through
+ * np.linalg.qr(mode="reduced")) and `_fix_signs` (linalg.py:96-103).
+ * On return A (if want_q) holds the thin Q, R (if non-null) the n×n upper
+ * triangular factor with diag(R) ≥ 0 and exact zeros below the diagonal.
+ * If rank_flag is non-null it receives the `orth` rank test
+ * (linalg.py:142-165): 0 full rank, 1 some |R_ii| < 1e-14·|R_00|, 2 R_00 == 0. */
+int pbq_householder_qr(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, double* R,
+                       int64_t ldr, int32_t want_q, int32_t* rank_flag, void* workspace,
+                       size_t workspace_bytes, void* stream);
+int pbq_qr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes);
+
+/* rows×cols standard-normal sketch, bit-identical to
+ * numpy.random.Generator(numpy.random.Philox(key=seed)).standard_normal((rows, cols))
+ * as drawn by `gaussian_matrix` (linalg.py:83-93): Philox4x64-10 with
+ * key = (seed_lo, seed_hi), numpy's 256-layer ziggurat, element (i, j) the
+ * (i·cols + j)-th normal of the stream.  `row_offset` generates rows
+ * [row_offset, row_offset+rows) of the same global rows×... matrix whose
+ * column count is `cols` (row-sharded multi-GPU generation). */
+int pbq_gaussian(pbq_ctx* ctx, int64_t rows, int64_t cols, int64_t row_offset, uint64_t seed_lo,
+                 uint64_t seed_hi, double* out, int64_t ldo, void* workspace,
+                 size_t workspace_bytes, void* stream);
+int pbq_gaussian_workspace_bytes(pbq_ctx* ctx, int64_t rows, int64_t cols, int64_t row_offset,
+                                 size_t* bytes);
+
+/* Full single-device PbP-QLP (Algorithm 3; algorithms.py:209-260). */
+typedef struct {
+  int64_t n1, n2, d, q;
+  const double* a; /* n1×n2 */
+  int64_t lda;
+  const double* phi; /* n1×d explicit sketch (oracle mode) or NULL → seeded */
+  int64_t ldphi;
+  uint64_t seed_lo, seed_hi;
+  int32_t reorthonormalize;
+  int32_t check_finite;
+} pbq_problem;
+
+typedef struct {
+  double* q; /* n1×d */
+  int64_t ldq;
+  double* l; /* d×d lower triangular, diag ≥ 0 */
+  int64_t ldl;
+  double* p; /* n2×d */
+  int64_t ldp;
+  double* r; /* d×d first-stage R, upper triangular, diag ≥ 0 */
+  int64_t ldr;
+  double* phi; /* n1×d: receives the seeded sketch (required when problem.phi == NULL) */
+  int64_t ldphi;
+  int32_t* rank_flags; /* device, 2q+1 ints: one per `orth` call in call order */
+  int32_t* nonfinite;  /* device int status: bit0 A held Inf/NaN, bit1 sketch generator overflow */
+} pbq_outputs;
+
+int pbq_pbp_qlp_workspace_bytes(pbq_ctx* ctx, const pbq_problem* prob, size_t* bytes);
+int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* prob, const pbq_outputs* out, void* workspace,
+                size_t workspace_bytes, void* stream);
+
+/* Small helpers used by the host driver.
+ * dst[i][j] = src[j][i]            (n×n), or with lower=1 the lower triangle
+ * of srcᵀ and zeros above (L = tril(R̃ᵀ), algorithms.py:257). */
+int pbq_transpose(pbq_ctx* ctx, int64_t n, const double* src, int64_t lds, double* dst,
+                  int64_t ldd, int32_t lower, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBQ_H_ */

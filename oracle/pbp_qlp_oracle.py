@@ -1,0 +1,212 @@
+"""TEST INFRASTRUCTURE ONLY — CPU oracle for PbP-QLP.
+
+Used by tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+``--impl reference``) as the checker / the timed CPU reference.  The product
+package never imports it.
+
+This is a restatement of the reference path at the numpy level, call for call:
+
+* ``oracle_gaussian``   ↔ ``gaussian_matrix``  (pbpqlp/linalg.py:83-93)
+* ``oracle_qr``         ↔ ``householder_qr`` + ``_fix_signs`` (linalg.py:96-115)
+* ``oracle_orth``       ↔ ``orth``             (linalg.py:142-165)
+* ``oracle_pbp_qlp``    ↔ ``pbp_qlp``          (algorithms.py:209-260)
+
+The arithmetic lives in numpy 2.3.5 (the reference pins only numpy>=1.24,
+pyproject.toml:11-15): dgemm for products, LAPACK dgeqrf+dorgqr (via
+``np.linalg.qr``) for QR, Philox4x64-10 + ziggurat for the sketch.  Because the
+calls are the reference's own, the oracle reproduces the reference bit for bit
+on the same machine (pinned in tests/test_oracle.py against /root/reference
+when present and against the committed tests/golden/ fixtures everywhere).
+
+``householder_qr_restated`` is an independent column-by-column restatement of
+LAPACK's dgeqr2/dorg2r Householder algorithm (no LAPACK call), used to
+cross-check ``oracle_qr`` on small inputs.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+RANK_DEFICIENCY_RTOL = 1e-14  # linalg.py:48
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_CLIB = os.path.join(_HERE, "_build", "libpbq_oracle.so")
+_clib = None
+
+
+def build_c_oracle():
+    """Compile sketch_oracle.c (gcc) into oracle/_build/."""
+    import subprocess
+
+    os.makedirs(os.path.join(_HERE, "_build"), exist_ok=True)
+    src = os.path.join(_HERE, "sketch_oracle.c")
+    if not os.path.exists(_CLIB) or os.path.getmtime(_CLIB) < os.path.getmtime(src):
+        subprocess.run(["gcc", "-O2", "-fPIC", "-std=gnu11", "-shared", "-o", _CLIB, src, "-lm"], check=True)
+    return _CLIB
+
+
+def _c():
+    global _clib
+    if _clib is None:
+        if not os.path.exists(_CLIB):
+            build_c_oracle()
+        lib = ctypes.CDLL(_CLIB)
+        lib.pbqo_philox_raw.argtypes = [ctypes.c_uint64] * 4 + [ctypes.c_void_p]
+        lib.pbqo_normals.argtypes = [ctypes.c_uint64] * 4 + [ctypes.c_void_p]
+        lib.pbqo_normals.restype = ctypes.c_uint64
+        _clib = lib
+    return _clib
+
+
+# ------------------------------------------------------------------ sketch --
+def oracle_gaussian(rows, cols, seed=0):
+    """numpy's own draw, exactly what the reference calls (linalg.py:92-93)."""
+    rng = np.random.Generator(np.random.Philox(key=int(seed)))
+    return rng.standard_normal((rows, cols))
+
+
+def c_gaussian(rows, cols, seed=0, row_offset=0):
+    """The C restatement (sketch_oracle.c): rows [row_offset, row_offset+rows)."""
+    seed = int(seed)
+    out = np.empty((rows, cols))
+    _c().pbqo_normals(seed & (2**64 - 1), seed >> 64, row_offset * cols, rows * cols, out.ctypes.data)
+    return out
+
+
+def c_philox_raw(seed, start, n):
+    seed = int(seed)
+    out = np.empty(n, dtype=np.uint64)
+    _c().pbqo_philox_raw(seed & (2**64 - 1), seed >> 64, start, n, out.ctypes.data)
+    return out
+
+
+# ---------------------------------------------------------------------- QR --
+def _fix_signs(q, r):
+    k = min(r.shape)
+    signs = np.sign(np.diagonal(r)[:k])
+    signs[signs == 0] = 1.0
+    q[:, :k] *= signs
+    r[:k, :] *= signs[:, None]
+    return q, r
+
+
+def oracle_qr(m):
+    """(Q, R) with diag(R) >= 0 and an exact-zero lower triangle (linalg.py:106-115)."""
+    q, r = np.linalg.qr(np.asarray(m, dtype=np.float64), mode="reduced")
+    q, r = _fix_signs(q.copy(), r.copy())
+    return q, np.triu(r)
+
+
+def rank_flag(r):
+    """0 ok, 1 rank deficient, 2 identically zero — the two warnings of orth."""
+    diag = np.abs(np.diagonal(r))
+    if diag.size and diag[0] > 0 and np.any(diag < RANK_DEFICIENCY_RTOL * diag[0]):
+        return 1
+    if diag.size and diag[0] == 0:
+        return 2
+    return 0
+
+
+def oracle_orth(m):
+    q, r = oracle_qr(m)
+    return q, rank_flag(r)
+
+
+def householder_qr_restated(m):
+    """LAPACK dgeqr2 + dorg2r restated with numpy vector ops (small inputs)."""
+    a = np.array(m, dtype=np.float64)
+    mm, n = a.shape
+    k = min(mm, n)
+    taus = np.zeros(k)
+    for j in range(k):
+        alpha = a[j, j]
+        x = a[j + 1:, j]
+        xnorm = np.linalg.norm(x)
+        if xnorm == 0.0:
+            taus[j] = 0.0
+            continue
+        beta = -np.copysign(np.hypot(alpha, xnorm), alpha)
+        taus[j] = (beta - alpha) / beta
+        a[j + 1:, j] = x / (alpha - beta)
+        a[j, j] = beta
+        v = np.concatenate(([1.0], a[j + 1:, j]))
+        w = v @ a[j:, j + 1:]
+        a[j:, j + 1:] -= taus[j] * np.outer(v, w)
+    r = np.triu(a[:k, :])
+    q = np.zeros((mm, k))
+    q[:k, :k] = np.eye(k)
+    for j in range(k - 1, -1, -1):
+        v = np.concatenate(([1.0], a[j + 1:, j]))
+        w = v @ q[j:, j:]
+        q[j:, j:] -= taus[j] * np.outer(v, w)
+    return _fix_signs(q, r)
+
+
+# ---------------------------------------------------------------- pipeline --
+def oracle_pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, phi=None):
+    """algorithms.py:209-260 restated; returns a dict of the factors plus the
+    per-orth rank flags (in call order) and the pass count."""
+    a = np.asarray(a, dtype=np.float64)
+    n1, n2 = a.shape
+    if phi is None:
+        phi = oracle_gaussian(n1, d, seed)
+    flags = []
+    passes = 0
+
+    def apply(block):
+        nonlocal passes
+        passes += 1
+        return a @ block
+
+    def apply_t(block):
+        nonlocal passes
+        passes += 1
+        return a.T @ block
+
+    c = apply_t(phi)
+    if reorthonormalize:
+        pbar, f = oracle_orth(c)
+        flags.append(f)
+        for _ in range(q):
+            pbar, f = oracle_orth(apply(pbar))
+            flags.append(f)
+            pbar, f = oracle_orth(apply_t(pbar))
+            flags.append(f)
+    else:
+        for _ in range(q):
+            c = apply_t(apply(c))
+        pbar, f = oracle_orth(c)
+        flags.append(f)
+    dmat = apply(pbar)
+    qfac, rfac = oracle_qr(dmat)
+    w, rt = oracle_qr(rfac.T)
+    l = np.tril(rt.T)
+    p = pbar @ w
+    return {"q": qfac, "l": l, "p": p, "r": rfac, "phi": phi, "rank_flags": flags, "passes": passes}
+
+
+# ------------------------------------------------------------------ checks --
+def column_relative_error(x, ref):
+    """max_j ‖x_j − ref_j‖ / ‖ref_j‖ after aligning column signs (BASELINE §5)."""
+    x = np.asarray(x, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    s = np.sign(np.sum(x * ref, axis=0))
+    s[s == 0] = 1.0
+    num = np.linalg.norm(x * s - ref, axis=0)
+    den = np.linalg.norm(ref, axis=0)
+    den[den == 0] = 1.0
+    return num / den
+
+
+def conditioning_tolerance(l_ref, strict=1e-10, factor=64.0):
+    """Per-column tolerance max(strict, factor·u·κ_j), κ_j = L_00/L_jj
+    (SURVEY.md §8 a9)."""
+    diag = np.abs(np.diagonal(np.asarray(l_ref)))
+    with np.errstate(divide="ignore"):
+        kappa = np.where(diag > 0, diag[0] / diag, np.inf)
+    return np.maximum(strict, factor * 2.0**-53 * kappa)
+
+
+def reconstruction_error(a, qf, l, p):
+    a = np.asarray(a, dtype=np.float64)
+    return np.linalg.norm(a - qf @ l @ p.T) / np.linalg.norm(a)

@@ -1,0 +1,30 @@
+"""B200-native PbP-QLP (projection-based partial QLP, arXiv:2103.07245).
+
+Drop-in for the reference package's PbP-QLP path (``pbpqlp.pbp_qlp``,
+/root/reference/pkg/src/pbpqlp/algorithms.py:209-260): same entry point,
+arguments, errors, warnings and result fields; every FLOP runs in
+hand-written sm_100a CUDA behind the C ABI in include/pbq.h.
+"""
+from .algorithms import QlpFactors, SketchRecord, pbp_qlp, pbp_qlp_bytes, pbp_qlp_flops
+from .exceptions import DeviceError, DimensionError, MatrixInputError, ParameterError, RankDeficiencyWarning
+from .linalg import QrFactors, gaussian_matrix, householder_qr, orth
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DeviceError",
+    "DimensionError",
+    "MatrixInputError",
+    "ParameterError",
+    "QlpFactors",
+    "QrFactors",
+    "RankDeficiencyWarning",
+    "SketchRecord",
+    "gaussian_matrix",
+    "householder_qr",
+    "orth",
+    "pbp_qlp",
+    "pbp_qlp_bytes",
+    "pbp_qlp_flops",
+    "__version__",
+]

@@ -1,0 +1,80 @@
+// Shared device helpers for the PbP-QLP sm_100a kernels.
+//
+// FP64 tensor math on sm_100a is the warp-level DMMA.8x8x4 instruction
+// (`mma.sync.aligned.m8n8k4.row.col.f64`); tcgen05/UMMA has no f64 kind, so the
+// FP64 path is register MMA fed from shared memory that is staged with
+// cp.async (LDGSTS) multi-buffering.  See DESIGN.md §3.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pbq {
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte async copy global->shared; bytes beyond `src_bytes` are zero-filled.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int atom_add_release(unsigned int* p, unsigned int v) {
+  unsigned int old;
+  asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// True when the IEEE-754 binary64 exponent field is all ones (Inf or NaN).
+__device__ __forceinline__ bool nonfinite_bits(double x) {
+  return ((__double_as_longlong(x) >> 52) & 0x7ff) == 0x7ff;
+}
+
+// Software grid barrier for persistent (cooperatively launched) kernels.
+// `counter` must be zeroed before the launch; `*generation` counts barriers
+// already passed by this CTA.  All writes made before the barrier by any CTA
+// are visible after it to loads that bypass L1 (ld.global.cg / acquire).
+__device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int& generation) {
+  __threadfence();
+  __syncthreads();
+  generation += 1;
+  if (threadIdx.x == 0) {
+    atom_add_release(counter, 1u);
+    const unsigned int target = generation * gridDim.x;
+    while (ld_acquire_u32(counter) < target) {
+    }
+  }
+  __syncthreads();
+}
+
+__host__ __device__ constexpr long ceil_div(long a, long b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ long lmin(long a, long b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ long lmax(long a, long b) { return a > b ? a : b; }
+
+}  // namespace pbq

@@ -1,0 +1,262 @@
+// FP64 DMMA GEMM for the two PbP-QLP contractions:
+//
+//   TRANS_A = true  : C[M×N] = alpha · Aᵀ·B + beta·C,  A stored K×M row-major
+//                     (C = AᵀX, reference `_PassCounter.apply_t`, algorithms.py:182-184)
+//   TRANS_A = false : C[M×N] = alpha · A·B  + beta·C,  A stored M×K row-major
+//                     (D = A·X, reference `_PassCounter.apply`, algorithms.py:178-180)
+//
+// B is K×N row-major in both cases.  All operands are FP64 and the products
+// run on the sm_100a FP64 tensor instruction DMMA.8x8x4.  Tiles are staged by
+// cp.async into a STAGES-deep shared-memory ring.  The grid is persistent
+// (one CTA per SM) and walks a deterministic stream-K schedule: the linearised
+// (tile, k-block) iteration space is cut into `grid` equal ranges, a tile whose
+// k-range is split across CTAs is finished by the CTA that owns its k=0 block,
+// which adds the other CTAs' partial tiles in increasing k order.  The
+// reduction order depends only on (M, N, K, grid), so results are bitwise
+// reproducible run to run on the same GPU model (test_algorithms.py:53-60).
+#pragma once
+#include "common.cuh"
+
+namespace pbq {
+
+struct GemmArgs {
+  long M, N, K;
+  const double* A;
+  long lda;
+  const double* B;
+  long ldb;
+  double* C;
+  long ldc;
+  double alpha, beta;
+  int tiles_m, tiles_n, k_iters;
+  long total_iters;
+  double* partials;  // grid × (BM·BN) doubles
+  int* flags;        // grid ints, zeroed before the launch
+  int* nonfinite;    // optional: OR-flag set if any element of A is Inf/NaN
+};
+
+template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES>
+struct GemmCfg {
+  static constexpr int WARPS_M = BM / WM;
+  static constexpr int WARPS_N = BN / WN;
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int MT = WM / 8;
+  static constexpr int NT = WN / 8;
+  // Row strides (in doubles) are ≡ 4 (mod 16) so that the 8×4 fragment loads
+  // of a warp hit 16 distinct 8-byte bank pairs per half-warp.
+  static constexpr int SA_LD = TRANS_A ? (BM + 4) : (BK + 4);
+  static constexpr int SA_ROWS = TRANS_A ? BK : BM;
+  static constexpr int SB_LD = BN + 4;
+  static constexpr int SA_ELEMS = SA_ROWS * SA_LD;
+  static constexpr int SB_ELEMS = BK * SB_LD;
+  static constexpr int STAGE_ELEMS = SA_ELEMS + SB_ELEMS;
+  static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
+  static constexpr int FRAGS = MT * NT * 2;
+  static_assert(BM % WM == 0 && BN % WN == 0 && WM % 8 == 0 && WN % 8 == 0, "tile shape");
+  static_assert(BK % 4 == 0, "BK multiple of 4");
+  static_assert(SA_LD % 16 == 4 && SB_LD % 16 == 4, "bank-conflict-free strides");
+};
+
+template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::THREADS, 1)
+    gemm_f64_streamk(GemmArgs p) {
+  using Cfg = GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>;
+  constexpr int THREADS = Cfg::THREADS;
+  constexpr int MT = Cfg::MT, NT = Cfg::NT;
+  extern __shared__ __align__(128) double smem[];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp / Cfg::WARPS_N) * WM;
+  const int wn0 = (warp % Cfg::WARPS_N) * WN;
+  const int G = gridDim.x;
+
+  long it = long(blockIdx.x) * p.total_iters / G;
+  const long it_end = long(blockIdx.x + 1) * p.total_iters / G;
+  bool saw_nonfinite = false;
+
+  while (it < it_end) {
+    const int tile = int(it / p.k_iters);
+    const int kb = int(it % p.k_iters);
+    const int ke = int(lmin(p.k_iters, kb + (it_end - it)));
+    const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
+    const long m0 = long(tm) * BM, n0 = long(tn) * BN;
+    const bool check = (p.nonfinite != nullptr) && (tn == 0);
+
+    double acc[MT][NT][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // ---- stage loader --------------------------------------------------
+    auto load_stage = [&](int stage, int kblk) {
+      double* sA = smem + stage * Cfg::STAGE_ELEMS;
+      double* sB = sA + Cfg::SA_ELEMS;
+      const long k0 = long(kblk) * BK;
+      if (TRANS_A) {
+        // sA[kk][m]: BK rows of A (global row k0+kk), columns m0..m0+BM
+        constexpr int CH = BK * (BM / 2);
+        for (int c = tid; c < CH; c += THREADS) {
+          const int kk = c / (BM / 2), mc = (c % (BM / 2)) * 2;
+          const long gk = k0 + kk, gm = m0 + mc;
+          int bytes = 0;
+          const double* src = p.A;
+          if (gk < p.K && gm < p.M) {
+            bytes = int(lmin(2, p.M - gm)) * 8;
+            src = p.A + gk * p.lda + gm;
+          }
+          cp_async16(sA + kk * Cfg::SA_LD + mc, src, bytes);
+        }
+      } else {
+        // sA[m][kk]: BM rows of A (global row m0+i), columns k0..k0+BK
+        constexpr int CH = BM * (BK / 2);
+        for (int c = tid; c < CH; c += THREADS) {
+          const int i = c / (BK / 2), kc = (c % (BK / 2)) * 2;
+          const long gm = m0 + i, gk = k0 + kc;
+          int bytes = 0;
+          const double* src = p.A;
+          if (gm < p.M && gk < p.K) {
+            bytes = int(lmin(2, p.K - gk)) * 8;
+            src = p.A + gm * p.lda + gk;
+          }
+          cp_async16(sA + i * Cfg::SA_LD + kc, src, bytes);
+        }
+      }
+      {
+        constexpr int CH = BK * (BN / 2);
+        for (int c = tid; c < CH; c += THREADS) {
+          const int kk = c / (BN / 2), nc = (c % (BN / 2)) * 2;
+          const long gk = k0 + kk, gn = n0 + nc;
+          int bytes = 0;
+          const double* src = p.B;
+          if (gk < p.K && gn < p.N) {
+            bytes = int(lmin(2, p.N - gn)) * 8;
+            src = p.B + gk * p.ldb + gn;
+          }
+          cp_async16(sB + kk * Cfg::SB_LD + nc, src, bytes);
+        }
+      }
+    };
+    // Non-finite scan of the A chunks this thread staged (own cp.async data is
+    // visible to the issuing thread after wait_group).
+    auto scan_stage = [&](int stage) {
+      const double* sA = smem + stage * Cfg::STAGE_ELEMS;
+      constexpr int CH = TRANS_A ? BK * (BM / 2) : BM * (BK / 2);
+      constexpr int ROWW = TRANS_A ? BM / 2 : BK / 2;
+      for (int c = tid; c < CH; c += THREADS) {
+        const int r = c / ROWW, cc = (c % ROWW) * 2;
+        const double2 v = *reinterpret_cast<const double2*>(sA + r * Cfg::SA_LD + cc);
+        saw_nonfinite |= nonfinite_bits(v.x) | nonfinite_bits(v.y);
+      }
+    };
+
+    // ---- prologue ------------------------------------------------------
+    const int nk = ke - kb;
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < nk) load_stage(s, kb + s);
+      cp_async_commit();
+    }
+
+    // ---- main loop -----------------------------------------------------
+    for (int i = 0; i < nk; ++i) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      const int stage = i % STAGES;
+      if (check) scan_stage(stage);
+      {
+        const int nxt = i + STAGES - 1;
+        if (nxt < nk) load_stage(nxt % STAGES, kb + nxt);
+        cp_async_commit();
+      }
+      const double* sA = smem + stage * Cfg::STAGE_ELEMS;
+      const double* sB = sA + Cfg::SA_ELEMS;
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        double a[MT], b[NT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          if (TRANS_A)
+            a[mt] = sA[(kk * 4 + t) * Cfg::SA_LD + wm0 + mt * 8 + g];
+          else
+            a[mt] = sA[(wm0 + mt * 8 + g) * Cfg::SA_LD + kk * 4 + t];
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = sB[(kk * 4 + t) * Cfg::SB_LD + wn0 + nt * 8 + g];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // ring buffer is reused by the next tile
+
+    // ---- stream-K fix-up + epilogue ------------------------------------
+    const bool full = (kb == 0 && ke == p.k_iters);
+    if (!full && kb != 0) {
+      // contributor: publish the partial tile in fragment-native layout
+      double* slot = p.partials + size_t(blockIdx.x) * (BM * BN);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            __stcg(slot + size_t(((warp * MT + mt) * NT + nt) * 2 + e) * 32 + lane, acc[mt][nt][e]);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release(p.flags + blockIdx.x, 1);
+    } else {
+      if (!full) {
+        // owner of the k=0 block: add later CTAs' partials in k order
+        const long tile_end = long(tile + 1) * p.k_iters;
+        for (int c = blockIdx.x + 1; c < G; ++c) {
+          if (tid == 0) {
+            while (ld_acquire(p.flags + c) == 0) {
+            }
+          }
+          __syncthreads();
+          const double* slot = p.partials + size_t(c) * (BM * BN);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                acc[mt][nt][e] += __ldcg(slot + size_t(((warp * MT + mt) * NT + nt) * 2 + e) * 32 + lane);
+          if (long(c + 1) * p.total_iters / G >= tile_end) break;
+        }
+      }
+      // epilogue: C = alpha·acc + beta·C
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const long r = m0 + wm0 + mt * 8 + g;
+        if (r >= p.M) continue;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const long cidx = n0 + wn0 + nt * 8 + 2 * t;
+          double* dst = p.C + r * p.ldc + cidx;
+          double v0 = p.alpha * acc[mt][nt][0], v1 = p.alpha * acc[mt][nt][1];
+          if (cidx + 1 < p.N) {
+            if (p.beta != 0.0) {
+              const double2 o = *reinterpret_cast<const double2*>(dst);
+              v0 += p.beta * o.x;
+              v1 += p.beta * o.y;
+            }
+            *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+          } else if (cidx < p.N) {
+            if (p.beta != 0.0) v0 += p.beta * dst[0];
+            dst[0] = v0;
+          }
+        }
+      }
+    }
+    it += nk;
+  }
+  if (saw_nonfinite) atomicOr(p.nonfinite, 1);
+}
+
+}  // namespace pbq

@@ -1,0 +1,485 @@
+// C-ABI implementation of libpbq (include/pbq.h): launch planning, workspace
+// carving and the single-device PbP-QLP pipeline (algorithms.py:209-260).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/pbq.h"
+#include "common.cuh"
+#include "gemm_f64.cuh"
+#include "qr_f64.cuh"
+#include "sketch.cuh"
+
+struct pbq_ctx {
+  int device = 0;
+  int sms = 0;
+  size_t smem_optin = 0;
+  long long launches = 0;
+  bool sketch_tables_ready = false;
+  char err[512] = {0};
+};
+
+namespace {
+
+using namespace pbq;
+
+int fail(pbq_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(ctx->err, sizeof(ctx->err), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+#define PBQ_CUDA(ctx, call)                                                                     \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? PBQ_ERR_OOM : PBQ_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                           \
+  } while (0)
+
+#define PBQ_TRY(expr)        \
+  do {                       \
+    int s_ = (expr);         \
+    if (s_ != PBQ_OK) return s_; \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Bump allocator over a caller workspace.
+struct Carve {
+  char* base;
+  size_t cap, off = 0;
+  Carve(void* b, size_t c) : base(static_cast<char*>(b)), cap(c) {}
+  template <class T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+  bool ok() const { return off <= cap; }
+};
+
+// ---------------------------------------------------------------- GEMM ----
+// Two tile shapes: d ≤ 64 uses 128×64 (warp 32×32), larger d 128×128 (warp 64×32).
+constexpr int G_BM = 128, G_BK = 16, G_STAGES = 4;
+
+template <bool T, int BN, int WM, int WN>
+struct GemmKernel {
+  using Cfg = GemmCfg<T, G_BM, BN, G_BK, WM, WN, G_STAGES>;
+  static void* fn() { return reinterpret_cast<void*>(&gemm_f64_streamk<T, G_BM, BN, G_BK, WM, WN, G_STAGES>); }
+};
+
+struct GemmPlan {
+  int bn;
+  int tiles_m, tiles_n, k_iters;
+  long total;
+  int grid;
+};
+
+GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K) {
+  GemmPlan p;
+  p.bn = (N <= 64) ? 64 : 128;
+  p.tiles_m = int(ceil_div(M, G_BM));
+  p.tiles_n = int(ceil_div(N, p.bn));
+  p.k_iters = int(ceil_div(K, G_BK));
+  p.total = long(p.tiles_m) * p.tiles_n * p.k_iters;
+  p.grid = int(std::min<long>(ctx->sms, p.total));
+  return p;
+}
+
+size_t gemm_ws_bytes(const GemmPlan& p) {
+  return align_up(size_t(p.grid) * G_BM * p.bn * sizeof(double), 256) + align_up(size_t(p.grid) * sizeof(int), 256) + 512;
+}
+
+template <bool TRANS>
+int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double* A, long lda, const double* B,
+                long ldb, double beta, double* C, long ldc, int32_t* nonfinite, void* ws, size_t ws_bytes,
+                cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K < 0) return fail(ctx, PBQ_ERR_DIM, "gemm: bad shape M=%ld N=%ld K=%ld", M, N, K);
+  if ((lda & 1) || (ldb & 1) || (ldc & 1) || !aligned16(A) || !aligned16(B) || !aligned16(C))
+    return fail(ctx, PBQ_ERR_PARAM, "gemm: leading dimensions must be even and pointers 16-byte aligned");
+  if (K == 0) return fail(ctx, PBQ_ERR_DIM, "gemm: K == 0");
+  const GemmPlan pl = gemm_plan(ctx, M, N, K);
+  Carve cv(ws, ws_bytes);
+  GemmArgs a;
+  a.M = M; a.N = N; a.K = K;
+  a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.C = C; a.ldc = ldc;
+  a.alpha = alpha; a.beta = beta;
+  a.tiles_m = pl.tiles_m; a.tiles_n = pl.tiles_n; a.k_iters = pl.k_iters; a.total_iters = pl.total;
+  a.partials = cv.take<double>(size_t(pl.grid) * G_BM * pl.bn);
+  a.flags = cv.take<int>(pl.grid);
+  a.nonfinite = nonfinite;
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gemm: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
+  void* fn;
+  size_t smem;
+  int threads;
+  if (pl.bn == 64) {
+    using K_ = GemmKernel<TRANS, 64, 32, 32>;
+    fn = K_::fn(); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
+  } else {
+    using K_ = GemmKernel<TRANS, 128, 64, 32>;
+    fn = K_::fn(); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
+  }
+  PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  void* args[] = {&a};
+  PBQ_CUDA(ctx, cudaLaunchKernel(fn, dim3(pl.grid), dim3(threads), args, smem, st));
+  ctx->launches += 2;
+  return PBQ_OK;
+}
+
+// ------------------------------------------------------------------ QR ----
+struct QrPlan {
+  int grid;
+  long rows;
+  int nb;
+  size_t smem;
+};
+
+int qr_plan(pbq_ctx* ctx, long m, long n, QrPlan& pl) {
+  if (m < 1 || n < 1) return fail(ctx, PBQ_ERR_DIM, "qr: bad shape %ldx%ld", m, n);
+  if (m < n) return fail(ctx, PBQ_ERR_UNSUPPORTED, "qr: requires m >= n (got %ldx%ld)", m, n);
+  long g = std::min<long>(ctx->sms, ceil_div(m, 16));
+  long rows = ceil_div(m, g);
+  g = ceil_div(m, rows);
+  const size_t limit = ctx->smem_optin;
+  for (int nb : {32, 16, 8}) {
+    const size_t bytes = qr_smem_doubles(rows, nb, n, int(g)) * sizeof(double);
+    if (bytes <= limit) {
+      pl.grid = int(g);
+      pl.rows = rows;
+      pl.nb = nb;
+      pl.smem = bytes;
+      return PBQ_OK;
+    }
+  }
+  return fail(ctx, PBQ_ERR_UNSUPPORTED, "qr: %ld rows per CTA do not fit shared memory (m=%ld n=%ld)", rows, m, n);
+}
+
+size_t qr_ws_bytes(const QrPlan& pl, long n) {
+  const size_t G = pl.grid;
+  size_t b = 0;
+  b += align_up(2 * G * 32 * 8, 256);
+  b += align_up(2 * 32 * 8, 256);
+  b += align_up(G * QR_NBMAX * size_t(n) * 8, 256);
+  b += align_up(QR_NBMAX * size_t(n) * 8, 256);
+  b += align_up(size_t(ceil_div(n, pl.nb)) * pl.nb * pl.nb * 8, 256);
+  b += 256 + 256;
+  return b;
+}
+
+int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int want_q, int32_t* rank_flag,
+              void* ws, size_t ws_bytes, cudaStream_t st) {
+  QrPlan pl;
+  PBQ_TRY(qr_plan(ctx, m, n, pl));
+  if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "qr: leading dimension too small");
+  Carve cv(ws, ws_bytes);
+  QrArgs a;
+  a.m = m; a.n = n; a.A = A; a.lda = lda; a.R = R; a.ldr = ldr;
+  a.want_q = want_q; a.nb = pl.nb; a.rows_per_cta = pl.rows;
+  a.part = cv.take<double>(2 * size_t(pl.grid) * 32);
+  a.pivrow = cv.take<double>(2 * 32);
+  a.wpart = cv.take<double>(size_t(pl.grid) * QR_NBMAX * n);
+  a.ybuf = cv.take<double>(size_t(QR_NBMAX) * n);
+  a.tall = cv.take<double>(size_t(ceil_div(n, pl.nb)) * pl.nb * pl.nb);
+  a.counter = cv.take<unsigned int>(1);
+  a.rank_flag = rank_flag;
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
+  PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&qr_tall_kernel),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
+  void* args[] = {&a};
+  PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&qr_tall_kernel), dim3(pl.grid),
+                                            dim3(QR_THREADS), args, pl.smem, st));
+  ctx->launches += 2;
+  return PBQ_OK;
+}
+
+// -------------------------------------------------------------- sketch ----
+struct SketchPlan {
+  long n_chunks;
+};
+
+SketchPlan sketch_plan(long rows, long cols, long row_offset) {
+  const long last = (row_offset + rows) * cols;
+  SketchPlan p;
+  // ~1.0223 words per normal; 5% + 4 chunks of head-room (shortfall is detected)
+  p.n_chunks = ceil_div(long(double(last) * 1.05) + 2 * PBQ_SK_CHUNK, PBQ_SK_CHUNK) + 2;
+  return p;
+}
+
+size_t sketch_ws_bytes(const SketchPlan& p) {
+  const size_t n = p.n_chunks;
+  return align_up(n * 4, 256) + align_up(n * PBQ_SK_E * 4, 256) + align_up(n * 8, 256) + align_up(n * 4, 256) +
+         256 + 256;
+}
+
+int sketch_tables(pbq_ctx* ctx) {
+  if (ctx->sketch_tables_ready) return PBQ_OK;
+  PBQ_CUDA(ctx, cudaMemcpyToSymbol(c_zig_ki, pbq_zig_ki, sizeof(pbq_zig_ki)));
+  PBQ_CUDA(ctx, cudaMemcpyToSymbol(c_zig_wi, pbq_zig_wi, sizeof(pbq_zig_wi)));
+  PBQ_CUDA(ctx, cudaMemcpyToSymbol(c_zig_fi, pbq_zig_fi, sizeof(pbq_zig_fi)));
+  ctx->sketch_tables_ready = true;
+  return PBQ_OK;
+}
+
+int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t k0, uint64_t k1, double* out,
+                  long ldo, int* error_flag, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (rows < 1 || cols < 1 || row_offset < 0) return fail(ctx, PBQ_ERR_DIM, "gaussian: bad shape");
+  if (ldo < cols) return fail(ctx, PBQ_ERR_PARAM, "gaussian: ldo < cols");
+  PBQ_TRY(sketch_tables(ctx));
+  const SketchPlan pl = sketch_plan(rows, cols, row_offset);
+  Carve cv(ws, ws_bytes);
+  SketchArgs a;
+  a.k0 = k0; a.k1 = k1;
+  a.n_chunks = pl.n_chunks;
+  a.first = row_offset * cols;
+  a.count = rows * cols;
+  a.cols = cols;
+  a.out = out; a.ldo = ldo;
+  a.exits = cv.take<int>(pl.n_chunks);
+  a.counts = cv.take<int>(size_t(pl.n_chunks) * PBQ_SK_E);
+  a.base = cv.take<long>(pl.n_chunks);
+  a.entry = cv.take<int>(pl.n_chunks);
+  int* own_err = cv.take<int>(1);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gaussian: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  a.error = error_flag ? error_flag : own_err;
+  if (!error_flag) PBQ_CUDA(ctx, cudaMemsetAsync(own_err, 0, sizeof(int), st));
+  sketch_k1<<<dim3(unsigned(pl.n_chunks)), PBQ_SK_THREADS, 0, st>>>(a);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  sketch_k2<<<1, 1024, 0, st>>>(a);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  sketch_k3<<<dim3(unsigned(pl.n_chunks)), PBQ_SK_THREADS, 0, st>>>(a);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 3;
+  return PBQ_OK;
+}
+
+// ----------------------------------------------------------- helpers ----
+__global__ void transpose_kernel(long n, const double* __restrict__ src, long lds, double* __restrict__ dst, long ldd,
+                                 int lower) {
+  __shared__ double tile[32][33];
+  const long bx = long(blockIdx.x) * 32, by = long(blockIdx.y) * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const long r = by + j, c = bx + threadIdx.x;
+    tile[j][threadIdx.x] = (r < n && c < n) ? src[r * lds + c] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const long r = bx + j, c = by + threadIdx.x;  // dst[r][c] = src[c][r]
+    if (r < n && c < n) dst[r * ldd + c] = (lower && c > r) ? 0.0 : tile[threadIdx.x][j];
+  }
+}
+
+int transpose_launch(pbq_ctx* ctx, long n, const double* src, long lds, double* dst, long ldd, int lower,
+                     cudaStream_t st) {
+  dim3 grid(unsigned(ceil_div(n, 32)), unsigned(ceil_div(n, 32)));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(n, src, lds, dst, ldd, lower);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
+long thin_ld(long d) { return (d + 1) & ~1L; }
+
+__global__ void merge_flag_kernel(int32_t* status, const int32_t* sketch_err) {
+  if (*sketch_err) *status |= 2;
+}
+
+}  // namespace
+
+// =================================================================== C ABI ==
+extern "C" {
+
+int pbq_ctx_create(int device, pbq_ctx** out) {
+  if (!out) return PBQ_ERR_PARAM;
+  *out = nullptr;
+  pbq_ctx* ctx = new pbq_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+  int optin = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return PBQ_ERR_CUDA;
+  }
+  ctx->smem_optin = size_t(optin);
+  *out = ctx;
+  return PBQ_OK;
+}
+
+int pbq_ctx_destroy(pbq_ctx* ctx) {
+  delete ctx;
+  return PBQ_OK;
+}
+
+const char* pbq_last_error(const pbq_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+int pbq_ctx_sm_count(const pbq_ctx* ctx) { return ctx ? ctx->sms : 0; }
+int64_t pbq_ctx_launch_count(const pbq_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int pbq_gemm_workspace_bytes(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, size_t* bytes) {
+  if (!ctx || !bytes) return PBQ_ERR_PARAM;
+  *bytes = gemm_ws_bytes(gemm_plan(ctx, M, N, std::max<int64_t>(K, 1)));
+  return PBQ_OK;
+}
+
+int pbq_gemm_tn(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int32_t* nonfinite, void* ws,
+                size_t ws_bytes, void* stream) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  if (lda < M || ldb < N || ldc < N) return fail(ctx, PBQ_ERR_PARAM, "gemm_tn: leading dimension too small");
+  return gemm_launch<true>(ctx, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, nonfinite, ws, ws_bytes,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int pbq_gemm_nn(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int32_t* nonfinite, void* ws,
+                size_t ws_bytes, void* stream) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  if (lda < K || ldb < N || ldc < N) return fail(ctx, PBQ_ERR_PARAM, "gemm_nn: leading dimension too small");
+  return gemm_launch<false>(ctx, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, nonfinite, ws, ws_bytes,
+                            static_cast<cudaStream_t>(stream));
+}
+
+int pbq_qr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes) {
+  if (!ctx || !bytes) return PBQ_ERR_PARAM;
+  QrPlan pl;
+  PBQ_TRY(qr_plan(ctx, m, n, pl));
+  *bytes = qr_ws_bytes(pl, n);
+  return PBQ_OK;
+}
+
+int pbq_householder_qr(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, double* R, int64_t ldr,
+                       int32_t want_q, int32_t* rank_flag, void* ws, size_t ws_bytes, void* stream) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  return qr_launch(ctx, m, n, A, lda, R, ldr, want_q, rank_flag, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int pbq_gaussian_workspace_bytes(pbq_ctx* ctx, int64_t rows, int64_t cols, int64_t row_offset, size_t* bytes) {
+  if (!ctx || !bytes) return PBQ_ERR_PARAM;
+  *bytes = sketch_ws_bytes(sketch_plan(rows, cols, row_offset));
+  return PBQ_OK;
+}
+
+int pbq_gaussian(pbq_ctx* ctx, int64_t rows, int64_t cols, int64_t row_offset, uint64_t seed_lo, uint64_t seed_hi,
+                 double* out, int64_t ldo, void* ws, size_t ws_bytes, void* stream) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  return sketch_launch(ctx, rows, cols, row_offset, seed_lo, seed_hi, out, ldo, nullptr, ws, ws_bytes,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int pbq_transpose(pbq_ctx* ctx, int64_t n, const double* src, int64_t lds, double* dst, int64_t ldd, int32_t lower,
+                  void* stream) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  return transpose_launch(ctx, n, src, lds, dst, ldd, lower, static_cast<cudaStream_t>(stream));
+}
+
+// ------------------------------------------------------------- pipeline --
+static int pipeline_sizes(pbq_ctx* ctx, const pbq_problem* pr, size_t* total, size_t* scratch) {
+  const long n1 = pr->n1, n2 = pr->n2, d = pr->d;
+  size_t g1, g2, g3, q1, q2, q3, s1 = 0;
+  PBQ_TRY(pbq_gemm_workspace_bytes(ctx, n2, d, n1, &g1));
+  PBQ_TRY(pbq_gemm_workspace_bytes(ctx, n1, d, n2, &g2));
+  PBQ_TRY(pbq_gemm_workspace_bytes(ctx, n2, d, d, &g3));
+  PBQ_TRY(pbq_qr_workspace_bytes(ctx, n2, d, &q1));
+  PBQ_TRY(pbq_qr_workspace_bytes(ctx, n1, d, &q2));
+  PBQ_TRY(pbq_qr_workspace_bytes(ctx, d, d, &q3));
+  if (!pr->phi) PBQ_TRY(pbq_gaussian_workspace_bytes(ctx, n1, d, 0, &s1));
+  const size_t sc = std::max({g1, g2, g3, q1, q2, q3, s1});
+  const long ld = thin_ld(d);
+  *scratch = sc;
+  *total = align_up(size_t(n2) * ld * 8, 256) + 2 * align_up(size_t(d) * ld * 8, 256) + align_up(64, 256) + sc + 512;
+  return PBQ_OK;
+}
+
+int pbq_pbp_qlp_workspace_bytes(pbq_ctx* ctx, const pbq_problem* pr, size_t* bytes) {
+  if (!ctx || !pr || !bytes) return PBQ_ERR_PARAM;
+  size_t scratch;
+  return pipeline_sizes(ctx, pr, bytes, &scratch);
+}
+
+int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void* ws, size_t ws_bytes, void* stream) {
+  if (!ctx || !pr || !o) return PBQ_ERR_PARAM;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long n1 = pr->n1, n2 = pr->n2, d = pr->d, q = pr->q;
+  // argument contract of algorithms.py:239-241 (A checks, then d, then q)
+  if (n1 < 1 || n2 < 1) return fail(ctx, PBQ_ERR_DIM, "a has a zero dimension: shape (%ld, %ld)", n1, n2);
+  if (d < 1 || d > std::min(n1, n2)) return fail(ctx, PBQ_ERR_PARAM, "d must be in [1, %ld], got %ld", std::min(n1, n2), d);
+  if (q < 0) return fail(ctx, PBQ_ERR_DIM, "q must be >= 0, got %ld", q);
+  if (!pr->a || !o->q || !o->l || !o->p || !o->r || !o->rank_flags || !o->nonfinite)
+    return fail(ctx, PBQ_ERR_PARAM, "null pointer argument");
+  if (!pr->phi && !o->phi) return fail(ctx, PBQ_ERR_PARAM, "seeded mode needs an output buffer for the sketch");
+  size_t total, scratch;
+  PBQ_TRY(pipeline_sizes(ctx, pr, &total, &scratch));
+  if (ws_bytes < total) return fail(ctx, PBQ_ERR_PARAM, "pbp_qlp: workspace too small (%zu < %zu)", ws_bytes, total);
+  const long ld = thin_ld(d);
+  Carve cv(ws, ws_bytes);
+  double* cbuf = cv.take<double>(size_t(n2) * ld);  // C, then P̄ (in place)
+  double* wbuf = cv.take<double>(size_t(d) * ld);   // Rᵀ → W
+  double* rt = cv.take<double>(size_t(d) * ld);     // R̃
+  int32_t* sk_err = cv.take<int32_t>(16);
+  void* sc = cv.take<char>(scratch);
+  const int32_t check = pr->check_finite ? 1 : 0;
+
+  PBQ_CUDA(ctx, cudaMemsetAsync(o->nonfinite, 0, sizeof(int32_t), st));
+  PBQ_CUDA(ctx, cudaMemsetAsync(o->rank_flags, 0, sizeof(int32_t) * (2 * q + 1), st));
+  const double* phi = pr->phi;
+  long ldphi = pr->ldphi;
+  if (!phi) {
+    PBQ_CUDA(ctx, cudaMemsetAsync(sk_err, 0, sizeof(int32_t), st));
+    PBQ_TRY(sketch_launch(ctx, n1, d, 0, pr->seed_lo, pr->seed_hi, o->phi, o->ldphi, sk_err, sc, scratch, st));
+    phi = o->phi;
+    ldphi = o->ldphi;
+  }
+  // pass 1: C = Aᵀ Φ  (+ fused isfinite scan of A)
+  PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, phi, ldphi, 0.0, cbuf, ld,
+                            check ? o->nonfinite : nullptr, sc, scratch, st));
+  int site = 0;
+  double* dbuf = o->q;  // n1×d scratch for A·P̄, finally D itself
+  const long ldq = o->ldq;
+  if (pr->reorthonormalize) {
+    PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
+    for (long it = 0; it < q; ++it) {
+      PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cbuf, ld, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
+      PBQ_TRY(qr_launch(ctx, n1, d, dbuf, ldq, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
+      PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, dbuf, ldq, 0.0, cbuf, ld, nullptr, sc, scratch, st));
+      PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
+    }
+  } else {
+    for (long it = 0; it < q; ++it) {
+      PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cbuf, ld, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
+      PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, dbuf, ldq, 0.0, cbuf, ld, nullptr, sc, scratch, st));
+    }
+    PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
+  }
+  // D = A·P̄ ; (Q, R) = qr(D)
+  PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cbuf, ld, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
+  PBQ_TRY(qr_launch(ctx, n1, d, dbuf, ldq, o->r, o->ldr, 1, nullptr, sc, scratch, st));
+  // (W, R̃) = qr(Rᵀ); L = tril(R̃ᵀ); P = P̄·W
+  PBQ_TRY(transpose_launch(ctx, d, o->r, o->ldr, wbuf, ld, 0, st));
+  PBQ_TRY(qr_launch(ctx, d, d, wbuf, ld, rt, ld, 1, nullptr, sc, scratch, st));
+  PBQ_TRY(transpose_launch(ctx, d, rt, ld, o->l, o->ldl, 1, st));
+  PBQ_TRY(gemm_launch<false>(ctx, n2, d, d, 1.0, cbuf, ld, wbuf, ld, 0.0, o->p, o->ldp, nullptr, sc, scratch, st));
+  if (!pr->phi) {
+    // fold a sketch-generator overflow into bit 1 of the status word so the
+    // host reads one int
+    merge_flag_kernel<<<1, 1, 0, st>>>(o->nonfinite, sk_err);
+    PBQ_CUDA(ctx, cudaGetLastError());
+    ctx->launches += 1;
+  }
+  return PBQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+"""Per-device library contexts and thin typed wrappers over the C ABI.
+
+PyTorch provides device memory (caching allocator), streams and the NCCL
+process group; every FLOP of the PbP-QLP path runs in libpbq's kernels.
+Matrices are torch float64 CUDA tensors, row-major, with an even row stride
+(the kernels stage 16-byte chunks).
+"""
+import ctypes
+import threading
+
+import torch
+
+from . import _lib
+from . import exceptions as _exc
+
+_ctx_lock = threading.Lock()
+_contexts = {}
+
+
+class Context:
+    """One ``pbq_ctx`` bound to a CUDA device (not thread-safe: guarded)."""
+
+    def __init__(self, device_index):
+        self.lib = _lib.load()
+        self.device_index = device_index
+        self.lock = threading.RLock()
+        handle = ctypes.c_void_p()
+        st = self.lib.pbq_ctx_create(device_index, ctypes.byref(handle))
+        if st != _lib.PBQ_OK:
+            raise _exc.DeviceError(f"pbq_ctx_create(device={device_index}) failed with status {st}")
+        self.handle = handle
+
+    @property
+    def sm_count(self):
+        return self.lib.pbq_ctx_sm_count(self.handle)
+
+    @property
+    def launch_count(self):
+        return int(self.lib.pbq_ctx_launch_count(self.handle))
+
+    def check(self, status, what):
+        _lib.raise_status(status, self.handle, what)
+
+
+def require_cuda(device=None):
+    if not torch.cuda.is_available():
+        raise _exc.DeviceError("no CUDA device is available; the PbP-QLP path runs only on the GPU")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.type != "cuda":
+        raise _exc.DeviceError(f"expected a CUDA device, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def context(device):
+    dev = require_cuda(device)
+    with _ctx_lock:
+        ctx = _contexts.get(dev.index)
+        if ctx is None:
+            with torch.cuda.device(dev):
+                ctx = Context(dev.index)
+            _contexts[dev.index] = ctx
+    return ctx
+
+
+def stream_ptr(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def even_ld(n):
+    return n + (n & 1)
+
+
+def empty_matrix(rows, cols, device):
+    """rows×cols float64 view of a (rows, even_ld(cols)) allocation."""
+    ld = even_ld(cols)
+    buf = torch.empty((rows, ld), dtype=torch.float64, device=device)
+    return buf[:, :cols] if ld != cols else buf
+
+
+def ld_of(t):
+    return t.stride(0)
+
+
+def as_kernel_operand(t):
+    """Return ``t`` or a copy whose layout the kernels accept (row-major,
+    unit column stride, even row stride, 16-byte aligned base)."""
+    ok = (
+        t.dtype == torch.float64
+        and t.dim() == 2
+        and t.stride(1) == 1
+        and t.stride(0) >= t.shape[1]
+        and t.stride(0) % 2 == 0
+        and t.data_ptr() % 16 == 0
+    )
+    if ok:
+        return t
+    out = empty_matrix(t.shape[0], t.shape[1], t.device)
+    out.copy_(t)
+    return out
+
+
+def workspace(nbytes, device):
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+# ---------------------------------------------------------------- kernels --
+def gemm(ctx, a, b, trans_a, out=None, alpha=1.0, beta=0.0, nonfinite=None):
+    """out = alpha·op(a)·b + beta·out, op = transpose when ``trans_a``."""
+    dev = a.device
+    a = as_kernel_operand(a)
+    b = as_kernel_operand(b)
+    if trans_a:
+        K, M = a.shape
+    else:
+        M, K = a.shape
+    N = b.shape[1]
+    if b.shape[0] != K:
+        raise _exc.DimensionError(f"gemm: inner dimensions differ ({K} vs {b.shape[0]})")
+    if out is None:
+        out = empty_matrix(M, N, dev)
+    nbytes = ctypes.c_size_t()
+    with ctx.lock:
+        ctx.check(ctx.lib.pbq_gemm_workspace_bytes(ctx.handle, M, N, K, ctypes.byref(nbytes)), "gemm workspace")
+        ws = workspace(nbytes.value, dev)
+        fn = ctx.lib.pbq_gemm_tn if trans_a else ctx.lib.pbq_gemm_nn
+        st = fn(ctx.handle, M, N, K, float(alpha), ptr(a), ld_of(a), ptr(b), ld_of(b), float(beta), ptr(out),
+                ld_of(out), ptr(nonfinite), ptr(ws), nbytes.value, stream_ptr(dev))
+        ctx.check(st, "gemm")
+    return out
+
+
+def householder_qr_(ctx, a, r=None, want_q=True, rank_flag=None):
+    """In-place QR of the m×n device matrix ``a`` (must be kernel-ready)."""
+    dev = a.device
+    m, n = a.shape
+    nbytes = ctypes.c_size_t()
+    with ctx.lock:
+        ctx.check(ctx.lib.pbq_qr_workspace_bytes(ctx.handle, m, n, ctypes.byref(nbytes)), "qr workspace")
+        ws = workspace(nbytes.value, dev)
+        st = ctx.lib.pbq_householder_qr(ctx.handle, m, n, ptr(a), ld_of(a), ptr(r), ld_of(r) if r is not None else 0,
+                                        int(bool(want_q)), ptr(rank_flag), ptr(ws), nbytes.value, stream_ptr(dev))
+        ctx.check(st, "householder_qr")
+    return a, r
+
+
+def gaussian(ctx, rows, cols, seed, device, row_offset=0, out=None):
+    if out is None:
+        out = empty_matrix(rows, cols, device)
+    nbytes = ctypes.c_size_t()
+    with ctx.lock:
+        ctx.check(ctx.lib.pbq_gaussian_workspace_bytes(ctx.handle, rows, cols, row_offset, ctypes.byref(nbytes)),
+                  "gaussian workspace")
+        ws = workspace(nbytes.value, device)
+        st = ctx.lib.pbq_gaussian(ctx.handle, rows, cols, row_offset, seed & ((1 << 64) - 1), seed >> 64, ptr(out),
+                                  ld_of(out), ptr(ws), nbytes.value, stream_ptr(device))
+        ctx.check(st, "gaussian")
+    return out
+
+
+def transpose(ctx, src, dst=None, lower=False):
+    n = src.shape[0]
+    if dst is None:
+        dst = empty_matrix(n, n, src.device)
+    with ctx.lock:
+        st = ctx.lib.pbq_transpose(ctx.handle, n, ptr(src), ld_of(src), ptr(dst), ld_of(dst), int(bool(lower)),
+                                   stream_ptr(src.device))
+        ctx.check(st, "transpose")
+    return dst

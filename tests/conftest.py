@@ -1,0 +1,39 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+REFERENCE_SRC = "/root/reference/pkg/src"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libpbq.so")
+    config.addinivalue_line("markers", "slow: full-size BASELINE configurations")
+
+
+@pytest.fixture(scope="session")
+def cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2103_07245_b200 import _lib
+
+    _lib.load()  # fail loudly if the extension is missing on a GPU box
+    return torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="session")
+def reference_pkg():
+    """The reference package, importable only in the build container."""
+    if not os.path.isdir(REFERENCE_SRC):
+        pytest.skip("reference source not present (GPU box)")
+    if REFERENCE_SRC not in sys.path:
+        sys.path.insert(0, REFERENCE_SRC)
+    import pbpqlp
+
+    return pbpqlp

@@ -1,0 +1,132 @@
+"""Parity of the individual sm_100a kernels behind the C ABI.
+
+GEMMs are checked against an exact-enough FP64 reference (numpy dgemm on the
+host), the QR against the oracle's LAPACK path (reference linalg.py:106-115),
+and the sketch against numpy's own Generator (linalg.py:83-93).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.pbp_qlp_oracle import c_gaussian, column_relative_error, oracle_gaussian, oracle_qr, rank_flag
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev_matrix(x, dev):
+    from paper_2103_07245_b200 import device as D
+
+    t = D.empty_matrix(x.shape[0], x.shape[1], dev)
+    t.copy_(torch.from_numpy(np.ascontiguousarray(x)))
+    return t
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (130, 40, 1000), (1000, 40, 1000), (257, 100, 4001),
+                                   (512, 256, 2048), (10000, 256, 300), (300, 129, 77)])
+@pytest.mark.parametrize("trans", [True, False])
+def test_gemm_matches_fp64(cuda, M, N, K, trans):
+    from paper_2103_07245_b200 import device as D
+
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    a = rng.standard_normal((K, M) if trans else (M, K))
+    b = rng.standard_normal((K, N))
+    ref = (a.T if trans else a) @ b
+    ctx = D.context(cuda)
+    out = D.gemm(ctx, _dev_matrix(a, cuda), _dev_matrix(b, cuda), trans_a=trans)
+    got = out.cpu().numpy()
+    # FP64 summation-order difference bound: ~K·u·Σ|a||b|
+    bound = 4 * K * 2.0**-53 * ((np.abs(a.T if trans else a)) @ np.abs(b))
+    assert np.all(np.abs(got - ref) <= bound + 1e-300)
+
+
+def test_gemm_alpha_beta_and_determinism(cuda):
+    from paper_2103_07245_b200 import device as D
+
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((3000, 700))
+    b = rng.standard_normal((3000, 130))
+    c0 = rng.standard_normal((700, 130))
+    ctx = D.context(cuda)
+    A, B = _dev_matrix(a, cuda), _dev_matrix(b, cuda)
+    C = _dev_matrix(c0, cuda)
+    D.gemm(ctx, A, B, trans_a=True, out=C, alpha=-0.5, beta=2.0)
+    ref = -0.5 * a.T @ b + 2.0 * c0
+    assert np.abs(C.cpu().numpy() - ref).max() < 1e-10
+    r1 = D.gemm(ctx, A, B, trans_a=True).cpu().numpy()
+    r2 = D.gemm(ctx, A, B, trans_a=True).cpu().numpy()
+    assert np.array_equal(r1, r2)  # stream-K fix-up order is fixed
+
+
+def test_gemm_nonfinite_flag(cuda):
+    from paper_2103_07245_b200 import device as D
+
+    ctx = D.context(cuda)
+    a = np.ones((517, 300))
+    b = np.ones((517, 40))
+    flag = torch.zeros(1, dtype=torch.int32, device=cuda)
+    D.gemm(ctx, _dev_matrix(a, cuda), _dev_matrix(b, cuda), trans_a=True, nonfinite=flag)
+    assert int(flag.item()) == 0
+    a[516, 299] = np.inf
+    D.gemm(ctx, _dev_matrix(a, cuda), _dev_matrix(b, cuda), trans_a=True, nonfinite=flag)
+    assert int(flag.item()) == 1
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (5, 5), (40, 40), (64, 33), (1000, 40), (4000, 100), (10000, 256),
+                                 (256, 256), (2500, 301), (700, 1)])
+def test_qr_matches_lapack(cuda, m, n):
+    from paper_2103_07245_b200 import device as D
+
+    rng = np.random.default_rng(m + 31 * n)
+    x = rng.standard_normal((m, n))
+    qr, rr = oracle_qr(x)
+    ctx = D.context(cuda)
+    t = _dev_matrix(x, cuda)
+    r = D.empty_matrix(n, n, cuda)
+    flag = torch.full((1,), -1, dtype=torch.int32, device=cuda)
+    D.householder_qr_(ctx, t, r, want_q=True, rank_flag=flag)
+    q = t.cpu().numpy()
+    rg = r.cpu().numpy()
+    assert int(flag.item()) == rank_flag(rr)
+    assert np.all(np.diag(rg) >= 0)
+    assert np.array_equal(np.tril(rg, -1), np.zeros((n, n)))
+    assert column_relative_error(q, qr).max() < 1e-11
+    assert np.abs(rg - rr).max() <= 1e-11 * np.abs(rr).max()
+    assert np.abs(q.T @ q - np.eye(n)).max() < 1e-13
+
+
+def test_qr_rank_flags(cuda):
+    from paper_2103_07245_b200 import device as D
+
+    ctx = D.context(cuda)
+    rng = np.random.default_rng(1)
+    low = rng.standard_normal((300, 3)) @ rng.standard_normal((3, 20))
+    for x, expect in ((low, 1), (np.zeros((50, 10)), 2), (rng.standard_normal((80, 10)), 0)):
+        t = _dev_matrix(x, cuda)
+        flag = torch.full((1,), -1, dtype=torch.int32, device=cuda)
+        D.householder_qr_(ctx, t, D.empty_matrix(x.shape[1], x.shape[1], cuda), rank_flag=flag)
+        assert int(flag.item()) == expect
+
+
+@pytest.mark.parametrize("rows,cols,seed", [(1, 1, 0), (7, 13, 2**100 + 7), (1000, 40, 0), (4000, 100, 1),
+                                            (20000, 256, 12345)])
+def test_gaussian_matches_numpy(cuda, rows, cols, seed):
+    from paper_2103_07245_b200 import gaussian_matrix
+
+    got = gaussian_matrix(rows, cols, seed)
+    ref = oracle_gaussian(rows, cols, seed)
+    diff = got != ref
+    # bit-exact except possibly the exponential-tail draws (CUDA log1p vs glibc, ≤ 1 ulp)
+    assert np.count_nonzero(diff) <= max(2, int(2e-5 * rows * cols))
+    if diff.any():
+        assert np.all(np.abs(ref[diff]) > 3.6)
+        assert np.all(np.abs(got[diff] - ref[diff]) <= 2 * np.spacing(np.abs(ref[diff])))
+
+
+def test_gaussian_row_offset(cuda):
+    from paper_2103_07245_b200 import gaussian_matrix
+
+    full = gaussian_matrix(3000, 64, 9)
+    part = gaussian_matrix(1000, 64, 9, row_offset=1500)
+    assert np.array_equal(part, full[1500:2500])
+    ref = c_gaussian(1000, 64, 9, row_offset=1500)
+    assert np.count_nonzero(part != ref) <= 2

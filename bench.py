@@ -1,0 +1,356 @@
+#!/usr/bin/env python3
+"""PbP-QLP benchmark (BASELINE.json metric: GFLOP/s and % FP64 roofline at
+20000×10000, d=256, q=1; 1/2/4/8-GPU scaling).
+
+One *step* = one full PbP-QLP factorization (device sketch, 2q+2 passes over
+A, all QRs, L and P) of the synthetic config-3 matrix resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload cfg3] [--no-cpu-baseline] [--no-e2e]
+
+For N > 1 launch under torchrun (one rank per GPU, NCCL); A is row-sharded
+across ranks (strong scaling: the same A is split N ways), timing is the max
+over ranks of CUDA-event time.  ``--impl reference`` times the reference's CPU
+implementation (the oracle port of pbpqlp.pbp_qlp, numpy/OpenBLAS on all host
+cores) on the same workload; under torchrun only rank 0 runs it.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.0  # measured DMMA.8x8x4 burst peak, profiles/r01_fp64_peak.jsonl
+FP64_PEAK_SOURCE = "measured: tools/microbench/fp64_peak.cu DMMA m8n8k4 on this pool's B200 (profiles/r01_fp64_peak.jsonl); MEASURED_PEAKS.json has no FP64 entry"
+METRIC = "PbP-QLP GFLOP/s and % FP64 roofline at 20000x10000, d=256; 1/2/4/8 GPU scaling"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def time_cpu_oracle(a_host, wl, seed, steps, budget_s=None):
+    """Time the CPU oracle (the reference's numpy call sequence) on all host cores."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle.pbp_qlp_oracle import oracle_pbp_qlp
+    from paper_2103_07245_b200 import pbp_qlp_flops
+
+    cores = cpu_threads()
+    n1, n2, d, q = wl["n1"], wl["n2"], wl["d"], wl["q"]
+    a = a_host
+    sample = f"full {n1}x{n2} d={d} q={q} factorization per step"
+    times = []
+    with threadpool_limits(limits=cores):
+        t0 = time.perf_counter()
+        oracle_pbp_qlp(a, d, q=q, seed=seed)
+        first = time.perf_counter() - t0
+        if budget_s is not None and first * steps > budget_s:
+            rows = max(d, int(n1 * budget_s / (first * steps * 1.2)))
+            a = a_host[:rows]
+            n1 = rows
+            sample = f"row sample {rows}x{n2} of the {wl['n1']}x{n2} matrix, d={d} q={q}, per step"
+        for i in range(steps):
+            t0 = time.perf_counter()
+            oracle_pbp_qlp(a, d, q=q, seed=seed + 1 + i)
+            times.append(time.perf_counter() - t0)
+    f = pbp_qlp_flops(n1, n2, d, q)
+    med = statistics.median(times)
+    return {"value": f / med / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+            "sample": sample + f" ({len(times)} timed, median {med:.3f} s; numpy/OpenBLAS oracle/pbp_qlp_oracle.py)",
+            "seconds": med, "times": times}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU path (oracle port) on rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+
+    from paper_2103_07245_b200 import workloads
+
+    wl = workloads.CONFIGS[args.workload]
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    a = workloads.make(args.workload, args.seed, dev).cpu().numpy()
+    res = time_cpu_oracle(a, wl, args.seed, args.steps, budget_s=180.0)
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": "GFLOP/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, wl, world),
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, wl, world):
+    return {
+        "workload": f"{args.workload}: A {wl['n1']}x{wl['n2']} fp64 synthetic (BASELINE config), d={wl['d']}, q={wl['q']}, seeded device sketch",
+        "n1": wl["n1"], "n2": wl["n2"], "d": wl["d"], "q": wl["q"], "seed": args.seed,
+        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+        "l2": "inputs larger than L2 (A is 1.6 GB vs 126 MB L2)" if wl["n1"] * wl["n2"] * 8 > 126e6 else "A fits L2",
+    }
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_07245_b200 import PbpQlpPlan, pbp_qlp, pbp_qlp_flops, workloads
+    from paper_2103_07245_b200 import device as D
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    wl = workloads.CONFIGS[args.workload]
+    n1, n2, d, q = wl["n1"], wl["n2"], wl["d"], wl["q"]
+    flops = pbp_qlp_flops(n1, n2, d, q)
+
+    if world > 1:
+        from paper_2103_07245_b200 import distributed as PD
+
+        a_full = workloads.make(args.workload, args.seed, dev)
+        rows = PD.shard_rows(n1, world)
+        a = a_full[rows[rank]:rows[rank + 1]].contiguous()
+        del a_full
+        torch.cuda.empty_cache()
+        runner = PD.DistributedPbpQlp(n1, n2, d, q, rows, dev)
+        step = lambda s: runner.run(a, seed=s)  # noqa: E731
+        finish = runner.finish
+        ctx = D.context(dev)
+    else:
+        a = workloads.make(args.workload, args.seed, dev)
+        plan = PbpQlpPlan(n1, n2, d, q, device=dev)
+        step = lambda s: plan.run(a, seed=s)  # noqa: E731
+        finish = plan.finish
+        ctx = plan.ctx
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        step(args.seed + i)
+        finish()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    barrier()
+    launches0 = ctx.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        step(args.seed + 100 + i)
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    finish()
+    launches = ctx.launch_count - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = flops / (ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (FP64 DMMA GEMM, 2q+2 launches/step)
+    roof = None
+    if rank == 0:
+        roof = gemm_roofline(D, ctx, a if world == 1 else None, n1, n2, d, q, dev, args.steps)
+        roof["step_frac_of_peak"] = value / 1e3 / FP64_PEAK_TFLOPS
+        roof["gemm_share_of_step"] = roof.pop("_gemm_ms_per_step") / ms if roof.get("_gemm_ms_per_step") else None
+
+    # ---- end to end through the public API with host (pinned) input
+    e2e = None
+    if not args.no_e2e and world == 1:
+        a_host = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        a_host.copy_(a)
+        del plan
+        torch.cuda.synchronize()
+        f = pbp_qlp(a_host, d, q=q, seed=args.seed)  # warm
+        ts = []
+        for i in range(max(3, min(args.steps, 10))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            f = pbp_qlp(a_host, d, q=q, seed=args.seed + 200 + i)
+            ts.append(time.perf_counter() - t0)
+        t_e2e = statistics.median(ts)
+        d2h = sum(x.numel() * 8 for x in (f.q_basis, f.l, f.p_basis, f.first_stage_r)) + 4 * (2 * q + 2)
+        e2e = {"value": flops / t_e2e / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(n1 * n2 * 8),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": t_e2e * 1e3, "input": "pinned host torch tensor"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        a_np = a_host.numpy() if e2e is not None else a.cpu().numpy()
+        res = time_cpu_oracle(a_np, wl, args.seed, steps=3, budget_s=60.0)
+        cpu = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, wl, world),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def gemm_roofline(D, ctx, a, n1, n2, d, q, dev, reps):
+    """Time the two GEMM launches of a step alone (CUDA events on the launch stream)."""
+    import torch
+
+    from paper_2103_07245_b200 import workloads
+
+    if a is None:
+        return {"bound": "tensor", "achieved": None, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": None,
+                "traffic": None, "kernel": "gemm_f64_streamk", "peak_source": FP64_PEAK_SOURCE}
+    x = D.empty_matrix(n1, d, dev)
+    x.normal_()
+    c = D.empty_matrix(n2, d, dev)
+    c.normal_()
+    dn = D.empty_matrix(n1, d, dev)
+    out_t = D.empty_matrix(n2, d, dev)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    t_tn = timed(lambda: D.gemm(ctx, a, x, trans_a=True, out=out_t))
+    t_nn = timed(lambda: D.gemm(ctx, a, c, trans_a=False, out=dn))
+    fl = 2.0 * n1 * n2 * d
+    per_step_ms = (q + 1) * (t_tn + t_nn)
+    achieved = 2 * (q + 1) * fl / (per_step_ms * 1e-3) / 1e12
+    return {
+        "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+        "kernel": "gemm_f64_streamk (C=A^T X and D=A X, FP64 DMMA.8x8x4)",
+        "per_launch_flop": fl, "tn_ms": t_tn, "nn_ms": t_nn,
+        "tn_tflops": fl / (t_tn * 1e-3) / 1e12, "nn_tflops": fl / (t_nn * 1e-3) / 1e12,
+        "peak_source": FP64_PEAK_SOURCE, "_gemm_ms_per_step": per_step_ms,
+    }
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        if args.impl == "reference":
+            if rank == 0:
+                run_reference(args, world, rank)
+            return
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        try:
+            run_ours(args, world, rank, local)
+        finally:
+            dist.destroy_process_group()
+        return
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -133,6 +133,11 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* prob, const pbq_outputs* out, v
 int pbq_transpose(pbq_ctx* ctx, int64_t n, const double* src, int64_t lds, double* dst,
                   int64_t ldd, int32_t lower, void* stream);
 
+/* Profiling hooks (device pointers, NULL to disable): number of QR panels
+ * that took the column-by-column fallback, and CTA-0 nanoseconds per QR
+ * phase (12 slots, see qr_f64.cuh). */
+int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns);
+
 #ifdef __cplusplus
 }
 #endif

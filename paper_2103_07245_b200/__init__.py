@@ -5,7 +5,7 @@ Drop-in for the reference package's PbP-QLP path (``pbpqlp.pbp_qlp``,
 arguments, errors, warnings and result fields; every FLOP runs in
 hand-written sm_100a CUDA behind the C ABI in include/pbq.h.
 """
-from .algorithms import QlpFactors, SketchRecord, pbp_qlp, pbp_qlp_bytes, pbp_qlp_flops
+from .algorithms import PbpQlpPlan, QlpFactors, SketchRecord, pbp_qlp, pbp_qlp_bytes, pbp_qlp_flops
 from .exceptions import DeviceError, DimensionError, MatrixInputError, ParameterError, RankDeficiencyWarning
 from .linalg import QrFactors, gaussian_matrix, householder_qr, orth
 
@@ -16,6 +16,7 @@ __all__ = [
     "DimensionError",
     "MatrixInputError",
     "ParameterError",
+    "PbpQlpPlan",
     "QlpFactors",
     "QrFactors",
     "RankDeficiencyWarning",

@@ -39,6 +39,7 @@ EXPORTED = (
     "pbq_pbp_qlp_workspace_bytes",
     "pbq_pbp_qlp",
     "pbq_transpose",
+    "pbq_debug_qr_hooks",
 )
 
 c_i64 = ctypes.c_int64
@@ -89,6 +90,7 @@ _SIGS = {
     "pbq_pbp_qlp_workspace_bytes": ([c_p, ctypes.POINTER(PbqProblem), ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_pbp_qlp": ([c_p, ctypes.POINTER(PbqProblem), ctypes.POINTER(PbqOutputs), c_p, c_sz, c_p], ctypes.c_int),
     "pbq_transpose": ([c_p, c_i64, c_p, c_i64, c_p, c_i64, c_i32, c_p], ctypes.c_int),
+    "pbq_debug_qr_hooks": ([c_p, c_p, c_p], ctypes.c_int),
 }
 
 _lib = None

@@ -15,7 +15,7 @@ The host only validates, stages A, launches, and reads back one status word
 plus the per-``orth`` rank flags (one device→host sync per call).
 """
 import ctypes
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Any, Optional
 
 import numpy as np
@@ -27,7 +27,7 @@ from . import exceptions as _exc
 from .linalg import HostMatrix, from_device, householder_qr, to_device_matrix, warn_rank
 from .validation import check_index_range, check_seed, check_sketch_params
 
-__all__ = ["SketchRecord", "QlpFactors", "pbp_qlp", "pbp_qlp_flops", "pbp_qlp_bytes"]
+__all__ = ["SketchRecord", "QlpFactors", "PbpQlpPlan", "pbp_qlp", "pbp_qlp_flops", "pbp_qlp_bytes"]
 
 
 class SketchRecord:
@@ -128,6 +128,84 @@ def pbp_qlp_bytes(n1, n2, q):
     return (2 * q + 2) * 8.0 * n1 * n2
 
 
+class PbpQlpPlan:
+    """Preallocated single-device PbP-QLP for one problem shape.
+
+    ``run`` only enqueues work on the current stream (no host sync), so
+    repeated calls can be timed back to back or captured; ``finish`` performs
+    the one device→host read of the status/rank flags, raises / warns exactly
+    like the reference, and returns the factors as torch tensors.
+    """
+
+    def __init__(self, n1, n2, d, q=0, reorthonormalize=True, device=None, explicit_phi=False):
+        dev = _dev.require_cuda(device)
+        self.n1, self.n2, self.d, self.q = int(n1), int(n2), int(d), int(q)
+        self.reorthonormalize = bool(reorthonormalize)
+        self.device = dev
+        self.ctx = _dev.context(dev)
+        self.Q = _dev.empty_matrix(n1, d, dev)
+        self.P = _dev.empty_matrix(n2, d, dev)
+        self.L = _dev.empty_matrix(d, d, dev)
+        self.R = _dev.empty_matrix(d, d, dev)
+        self.PHI = None if explicit_phi else _dev.empty_matrix(n1, d, dev)
+        self.flags = torch.zeros(2 * q + 2, dtype=torch.int32, device=dev)  # [status, rank flags...]
+        self.prob = _lib.PbqProblem()
+        self.prob.n1, self.prob.n2, self.prob.d, self.prob.q = n1, n2, d, q
+        self.prob.reorthonormalize = 1 if reorthonormalize else 0
+        self.prob.check_finite = 1
+        self.out = _lib.PbqOutputs()
+        o = self.out
+        o.q, o.ldq = self.Q.data_ptr(), self.Q.stride(0)
+        o.l, o.ldl = self.L.data_ptr(), self.L.stride(0)
+        o.p, o.ldp = self.P.data_ptr(), self.P.stride(0)
+        o.r, o.ldr = self.R.data_ptr(), self.R.stride(0)
+        if self.PHI is not None:
+            o.phi, o.ldphi = self.PHI.data_ptr(), self.PHI.stride(0)
+        o.nonfinite = self.flags.data_ptr()
+        o.rank_flags = self.flags.data_ptr() + 4
+        if explicit_phi:
+            self.prob.phi = 1  # sizing only: explicit sketch needs no generator workspace
+        nbytes = ctypes.c_size_t()
+        self.ctx.check(self.ctx.lib.pbq_pbp_qlp_workspace_bytes(self.ctx.handle, ctypes.byref(self.prob),
+                                                               ctypes.byref(nbytes)), "pbp_qlp workspace")
+        self.ws_bytes = nbytes.value
+        self.ws = _dev.workspace(self.ws_bytes, dev)
+        self.seed = 0
+        self.phi_in = None
+
+    def run(self, A, seed=0, phi=None):
+        """Enqueue one factorization of the kernel-ready device matrix ``A``."""
+        if tuple(A.shape) != (self.n1, self.n2):
+            raise _exc.DimensionError(f"plan is for {(self.n1, self.n2)}, got {tuple(A.shape)}")
+        seed = check_seed(seed)
+        self.seed = seed
+        self.prob.a, self.prob.lda = A.data_ptr(), A.stride(0)
+        self.prob.seed_lo, self.prob.seed_hi = seed & ((1 << 64) - 1), seed >> 64
+        if phi is not None:
+            if tuple(phi.shape) != (self.n1, self.d):
+                raise _exc.DimensionError(f"phi must have shape ({self.n1}, {self.d}), got {tuple(phi.shape)}")
+            self.prob.phi, self.prob.ldphi = phi.data_ptr(), phi.stride(0)
+        else:
+            if self.PHI is None:
+                raise _exc.ParameterError("plan was built for an explicit sketch; pass phi")
+            self.prob.phi, self.prob.ldphi = None, 0
+        self.phi_in = phi
+        with self.ctx.lock:
+            st = self.ctx.lib.pbq_pbp_qlp(self.ctx.handle, ctypes.byref(self.prob), ctypes.byref(self.out),
+                                          _dev.ptr(self.ws), self.ws_bytes, _dev.stream_ptr(self.device))
+            self.ctx.check(st, "pbp_qlp")
+
+    def finish(self, stacklevel=3):
+        fl = self.flags.cpu().tolist()  # the one device→host synchronisation
+        if fl[0] & 1:
+            raise _exc.MatrixInputError("a contains non-finite entries")
+        if fl[0] & 2:
+            raise _exc.DeviceError("sketch generator overflow (internal error)")
+        for flag in fl[1:]:
+            warn_rank(flag, stacklevel=stacklevel + 1)
+        return fl
+
+
 def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, *, phi=None, device=None):
     """Projection-based partial QLP factorization of ``a`` on the GPU.
 
@@ -135,7 +213,7 @@ def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, *, phi=None, device=None):
     reference (algorithms.py:209-260).  Extensions (keyword-only):
     ``phi`` supplies the sketch explicitly (oracle mode, n1×d); ``device``
     picks the GPU for array-like inputs.  numpy/array-like input returns numpy
-    factors; a torch tensor returns torch tensors on the tensor's device.
+    factors; a torch tensor returns torch tensors on the tensor's home device.
     """
     ha = HostMatrix(a, "a")
     n1, n2 = ha.shape
@@ -150,65 +228,20 @@ def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, *, phi=None, device=None):
     kind, home = ha.kind, ha.home
     A = ha.to_device(device)
     dev = A.device
-    ctx = _dev.context(dev)
-
-    Q = _dev.empty_matrix(n1, d, dev)
-    P = _dev.empty_matrix(n2, d, dev)
-    L = _dev.empty_matrix(d, d, dev)
-    R = _dev.empty_matrix(d, d, dev)
-    flags = torch.zeros(2 * q + 2, dtype=torch.int32, device=dev)  # [status, rank flags...]
-    prob = _lib.PbqProblem()
-    prob.n1, prob.n2, prob.d, prob.q = n1, n2, d, q
-    prob.a, prob.lda = A.data_ptr(), A.stride(0)
-    prob.seed_lo, prob.seed_hi = seed & ((1 << 64) - 1), seed >> 64
-    prob.reorthonormalize = 1 if reorthonormalize else 0
-    prob.check_finite = 1
-    out = _lib.PbqOutputs()
-    out.q, out.ldq = Q.data_ptr(), Q.stride(0)
-    out.l, out.ldl = L.data_ptr(), L.stride(0)
-    out.p, out.ldp = P.data_ptr(), P.stride(0)
-    out.r, out.ldr = R.data_ptr(), R.stride(0)
+    PHI = None
     if phi is not None:
-        pkind, PHI, _, _ = to_device_matrix(phi, "phi", dev)
-        if tuple(PHI.shape) != (n1, d):
-            raise _exc.DimensionError(f"phi must have shape ({n1}, {d}), got {tuple(PHI.shape)}")
-        prob.phi, prob.ldphi = PHI.data_ptr(), PHI.stride(0)
-        sketch_phi = phi if kind == "torch" or isinstance(phi, np.ndarray) else np.asarray(phi, dtype=np.float64)
-    else:
-        PHI = _dev.empty_matrix(n1, d, dev)
-        prob.phi, prob.ldphi = None, 0
-        out.phi, out.ldphi = PHI.data_ptr(), PHI.stride(0)
-        sketch_phi = None
-    out.nonfinite = flags.data_ptr()
-    out.rank_flags = flags.data_ptr() + 4
-
-    nbytes = ctypes.c_size_t()
-    with ctx.lock:
-        ctx.check(ctx.lib.pbq_pbp_qlp_workspace_bytes(ctx.handle, ctypes.byref(prob), ctypes.byref(nbytes)),
-                  "pbp_qlp workspace")
-        ws = _dev.workspace(nbytes.value, dev)
-        st = ctx.lib.pbq_pbp_qlp(ctx.handle, ctypes.byref(prob), ctypes.byref(out), _dev.ptr(ws), nbytes.value,
-                                 _dev.stream_ptr(dev))
-        ctx.check(st, "pbp_qlp")
-    fl = flags.cpu().tolist()  # the one device→host synchronisation
-    if fl[0] & 1:
-        raise _exc.MatrixInputError("a contains non-finite entries")
-    if fl[0] & 2:
-        raise _exc.DeviceError("sketch generator overflow (internal error)")
-    for flag in fl[1:]:
-        warn_rank(flag, stacklevel=3)
-
+        _, PHI, _, _ = to_device_matrix(phi, "phi", dev)
+    plan = PbpQlpPlan(n1, n2, d, q, reorthonormalize, dev, explicit_phi=phi is not None)
+    plan.run(A, seed, PHI)
+    plan.finish(stacklevel=3)
     passes = 2 * q + 2
-    if sketch_phi is not None:
-        sketch = SketchRecord(PHI, kind, seed, d, q, passes, home)
-        if kind == "numpy":
-            sketch._host = np.asarray(sketch_phi, dtype=np.float64)
-    else:
-        sketch = SketchRecord(PHI, kind, seed, d, q, passes, home)
+    sketch = SketchRecord(PHI if PHI is not None else plan.PHI, kind, seed, d, q, passes, home)
+    if phi is not None and kind == "numpy":
+        sketch._host = np.asarray(phi, dtype=np.float64)
     return QlpFactors(
-        from_device(Q, kind, home),
-        from_device(L, kind, home),
-        from_device(P, kind, home),
-        from_device(R, kind, home),
+        from_device(plan.Q, kind, home),
+        from_device(plan.L, kind, home),
+        from_device(plan.P, kind, home),
+        from_device(plan.R, kind, home),
         sketch,
     )

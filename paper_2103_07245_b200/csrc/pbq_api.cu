@@ -20,6 +20,9 @@ struct pbq_ctx {
   size_t smem_optin = 0;
   long long launches = 0;
   bool sketch_tables_ready = false;
+  int* qr_fallbacks = nullptr;                // profiling hooks (device pointers), off by default
+  int* qr_error = nullptr;                    // when set: QR kernels report unsupported panels here
+  unsigned long long* qr_phase_ns = nullptr;
   char err[512] = {0};
 };
 
@@ -135,15 +138,15 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   void* args[] = {&a};
   PBQ_CUDA(ctx, cudaLaunchKernel(fn, dim3(pl.grid), dim3(threads), args, smem, st));
-  ctx->launches += 2;
+  ctx->launches += 1;
   return PBQ_OK;
 }
 
 // ------------------------------------------------------------------ QR ----
 struct QrPlan {
   int grid;
-  long rows;
-  int nb;
+  long rows;  // rows per CTA
+  long rch;   // rows per shared-memory chunk
   size_t smem;
 };
 
@@ -154,28 +157,30 @@ int qr_plan(pbq_ctx* ctx, long m, long n, QrPlan& pl) {
   long rows = ceil_div(m, g);
   g = ceil_div(m, rows);
   const size_t limit = ctx->smem_optin;
-  for (int nb : {32, 16, 8}) {
-    const size_t bytes = qr_smem_doubles(rows, nb, n, int(g)) * sizeof(double);
-    if (bytes <= limit) {
-      pl.grid = int(g);
-      pl.rows = rows;
-      pl.nb = nb;
-      pl.smem = bytes;
-      return PBQ_OK;
-    }
+  long rch = rows;
+  if (qr_smem_doubles(rch, n, int(g)) * sizeof(double) > limit) {
+    rch = 32;
+    while (qr_smem_doubles(rch + 32, n, int(g)) * sizeof(double) <= limit) rch += 32;
+    if (qr_smem_doubles(rch, n, int(g)) * sizeof(double) > limit)
+      return fail(ctx, PBQ_ERR_UNSUPPORTED, "qr: n=%ld too large for shared memory", n);
   }
-  return fail(ctx, PBQ_ERR_UNSUPPORTED, "qr: %ld rows per CTA do not fit shared memory (m=%ld n=%ld)", rows, m, n);
+  pl.grid = int(g);
+  pl.rows = rows;
+  pl.rch = rch;
+  pl.smem = qr_smem_doubles(rch, n, int(g)) * sizeof(double);
+  return PBQ_OK;
 }
 
 size_t qr_ws_bytes(const QrPlan& pl, long n) {
   const size_t G = pl.grid;
   size_t b = 0;
-  b += align_up(2 * G * 32 * 8, 256);
-  b += align_up(2 * 32 * 8, 256);
-  b += align_up(G * QR_NBMAX * size_t(n) * 8, 256);
-  b += align_up(QR_NBMAX * size_t(n) * 8, 256);
-  b += align_up(size_t(ceil_div(n, pl.nb)) * pl.nb * pl.nb * 8, 256);
-  b += 256 + 256;
+  b += align_up(2 * G * 32 * 8, 256);                           // part
+  b += align_up(2 * 32 * 8, 256);                               // pivrow
+  b += 2 * align_up(32 * 32 * 8, 256);                          // pivbuf, gfin
+  b += align_up(G * QR_NB * size_t(qr_ldw(n)) * 8, 256);        // wpart
+  b += align_up(QR_NB * size_t(qr_ldy(n)) * 8, 256);            // ybuf
+  b += align_up(size_t(ceil_div(n, QR_NB)) * 1024 * 8, 256);    // tall
+  b += 256 + 256 + 256;                                         // counter, error
   return b;
 }
 
@@ -184,17 +189,23 @@ int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   QrPlan pl;
   PBQ_TRY(qr_plan(ctx, m, n, pl));
   if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "qr: leading dimension too small");
+  if ((lda & 1) || !aligned16(A)) return fail(ctx, PBQ_ERR_PARAM, "qr: lda must be even and A 16-byte aligned");
   Carve cv(ws, ws_bytes);
   QrArgs a;
   a.m = m; a.n = n; a.A = A; a.lda = lda; a.R = R; a.ldr = ldr;
-  a.want_q = want_q; a.nb = pl.nb; a.rows_per_cta = pl.rows;
+  a.want_q = want_q; a.rows_per_cta = pl.rows; a.rch = int(pl.rch);
   a.part = cv.take<double>(2 * size_t(pl.grid) * 32);
   a.pivrow = cv.take<double>(2 * 32);
-  a.wpart = cv.take<double>(size_t(pl.grid) * QR_NBMAX * n);
-  a.ybuf = cv.take<double>(size_t(QR_NBMAX) * n);
-  a.tall = cv.take<double>(size_t(ceil_div(n, pl.nb)) * pl.nb * pl.nb);
+  a.pivbuf = cv.take<double>(32 * 32);
+  a.gfin = cv.take<double>(32 * 32);
+  a.wpart = cv.take<double>(size_t(pl.grid) * QR_NB * qr_ldw(n));
+  a.ybuf = cv.take<double>(size_t(QR_NB) * qr_ldy(n));
+  a.tall = cv.take<double>(size_t(ceil_div(n, QR_NB)) * 1024);
   a.counter = cv.take<unsigned int>(1);
+  a.error = ctx->qr_error ? ctx->qr_error : cv.take<int>(1);
   a.rank_flag = rank_flag;
+  a.fallbacks = ctx->qr_fallbacks;
+  a.phase_ns = ctx->qr_phase_ns;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
   PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&qr_tall_kernel),
@@ -202,7 +213,7 @@ int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   void* args[] = {&a};
   PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&qr_tall_kernel), dim3(pl.grid),
                                             dim3(QR_THREADS), args, pl.smem, st));
-  ctx->launches += 2;
+  ctx->launches += 1;
   return PBQ_OK;
 }
 
@@ -378,6 +389,13 @@ int pbq_gaussian(pbq_ctx* ctx, int64_t rows, int64_t cols, int64_t row_offset, u
   if (!ctx) return PBQ_ERR_PARAM;
   return sketch_launch(ctx, rows, cols, row_offset, seed_lo, seed_hi, out, ldo, nullptr, ws, ws_bytes,
                        static_cast<cudaStream_t>(stream));
+}
+
+int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  ctx->qr_fallbacks = fallbacks;
+  ctx->qr_phase_ns = reinterpret_cast<unsigned long long*>(phase_ns);
+  return PBQ_OK;
 }
 
 int pbq_transpose(pbq_ctx* ctx, int64_t n, const double* src, int64_t lds, double* dst, int64_t ldd, int32_t lower,

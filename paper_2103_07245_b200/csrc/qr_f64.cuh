@@ -6,26 +6,43 @@
 // below the diagonal, and `rank_flag` reports the `orth` rank test
 // (linalg.py:142-165): 1 if some |R_ii| < 1e-14·|R_00|, 2 if R_00 == 0.
 //
-// Layout and schedule: one persistent CTA per SM, launched
-// cooperatively.  CTA c owns a contiguous block of rows for the whole call.
-// Columns are processed in panels of NB (32/16/8).  Inside a panel each column
-// needs one global reduction (the dots of the pivot column with every panel
-// column, computed in the same pass as the norm, so a column costs exactly
-// one grid barrier); the CTA's panel rows stay resident in shared memory.
-// Reflectors are accumulated into the compact-WY T factor on the fly (the
-// Vᵀv products ride in the same reduction).  The trailing update
-// A2 ← (I − V Tᵀ Vᵀ) A2 and the backward Q formation
-// Q ← (I − V T Vᵀ) Q are GEMM-shaped: per-CTA partials of VᵀA2, a
-// fixed-order slice reduction (deterministic), then a row-local update.
+// Algorithm: blocked Householder QR in compact-WY form with
+// 32-column panels.  One persistent CTA per SM (cooperative launch); CTA c
+// owns a contiguous block of rows for the whole call; its rows of the current
+// panel live in shared memory (in chunks when they do not fit).
+//
+// A full 32-column panel is factored by the fast path:
+//   Cholesky-QR2 — two Gram reductions (four grid barriers per panel instead
+//   of one per column) — followed by Householder reconstruction (Ballard,
+//   Demmel, Grigori, Jacquelin, Knight, Nguyen, "Reconstructing Householder
+//   vectors from tall-skinny QR", JPDC 2015): with Q₁ the panel's pivot block
+//   and S = −sign(diag Q₁), an unpivoted LU I − Q₁S = V₁U gives the unit-lower
+//   V₁; V₂ = −Q₂SU⁻¹, T = U·V₁⁻ᵀ, and the panel's R block is S·R.
+// The 32×32 algebra is done redundantly by every CTA: two sequential
+// eliminations (Cholesky, LU) and otherwise log-depth triangular inverses and
+// small matrix products, so the per-row work becomes 32×32 matrix products.
+// A panel takes the fallback — column-by-column Householder (dlarfg
+// convention, one grid reduction per column) — when it is the last, partial
+// panel or when diag(R₁) shows it is numerically rank deficient / worse
+// conditioned than 1e4; every CTA takes the same decision from the same
+// reduced Gram matrix.  The trailing update A2 ← (I − V Tᵀ Vᵀ) A2 and the
+// backward Q formation Q ← (I − V T Vᵀ) Q are GEMM-shaped: per-CTA partials
+// of VᵀX, a fixed-order slice reduction, then a row-local update.  All
+// cross-CTA sums run in a fixed order: results are bitwise reproducible.
 #pragma once
 #include "common.cuh"
 
 namespace pbq {
 
 constexpr int QR_THREADS = 256;
-constexpr int QR_NBMAX = 32;
-constexpr int QR_STAGE_DOUBLES = 4096;  // one 32 KB staging tile
-constexpr double QR_RANK_RTOL = 1e-14;  // RANK_DEFICIENCY_RTOL, linalg.py:48
+constexpr int QR_NB = 32;                 // panel width
+constexpr int QR_SLD = QR_NB + 1;         // leading dimension of 32×32 smem matrices
+constexpr int QR_PLD = QR_NB + 1;         // leading dimension of the panel rows
+constexpr int QR_TILE_DOUBLES = 4096;     // one 32 KB staging tile (32 rows × 128 columns)
+constexpr int QR_CW = QR_TILE_DOUBLES / QR_NB;  // 128 columns per tile
+constexpr double QR_RANK_RTOL = 1e-14;    // RANK_DEFICIENCY_RTOL, linalg.py:48
+constexpr double QR_FAST_DIAG_RATIO = 1e-4;  // min/max diag(R₁) accepted by the fast path
+constexpr int QR_NSMALL = 12;             // 32×32 scratch matrices in shared memory
 
 struct QrArgs {
   long m, n;
@@ -34,59 +51,477 @@ struct QrArgs {
   double* R;  // n×n, may be null
   long ldr;
   int want_q;
-  int nb;
   long rows_per_cta;
-  double* part;    // 2 × G × 32
+  int rch;         // rows per shared-memory chunk (≥ rows_per_cta when resident)
+  double* part;    // 2 × G × 32   (fallback column partials)
   double* pivrow;  // 2 × 32
-  double* wpart;   // G × 32 × n
-  double* ybuf;    // 32 × n
-  double* tall;    // ceil(n/nb) × nb × nb
+  double* pivbuf;  // 32 × 32      (original pivot rows of the panel)
+  double* gfin;    // 32 × 32      (reduced Gram matrix)
+  double* wpart;   // G × 32 × ldw (Gram / W partials), ldw = max(n, 32)
+  double* ybuf;    // 32 × qr_ldy(n)
+  double* tall;    // ceil(n/32) × 32 × 32
   unsigned int* counter;
   int* rank_flag;  // may be null
+  int* fallbacks;  // may be null: number of panels that took the fallback
+  int* error;      // may be null: set to 1 if a fallback panel met non-resident rows
+  unsigned long long* phase_ns;  // may be null: CTA-0 time per phase (profiling)
 };
+
+__device__ __forceinline__ unsigned long long qr_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// accumulate elapsed time since the previous mark into slot `ph` (CTA 0, thread 0)
+#define QR_PHASE(ph)                                          \
+  do {                                                       \
+    if (p.phase_ns && blockIdx.x == 0 && threadIdx.x == 0) { \
+      const unsigned long long now_ = qr_now();              \
+      p.phase_ns[ph] += now_ - t_phase;                      \
+      t_phase = now_;                                        \
+    }                                                        \
+  } while (0)
+
+// row stride of ybuf: even so that 16-byte cp.async sources stay aligned
+__host__ __device__ constexpr long qr_ldy(long n) { return (n + 1) & ~1L; }
+__host__ __device__ constexpr long qr_ldw(long n) { return n > QR_NB ? n : QR_NB; }
+__host__ __device__ constexpr size_t qr_pad4(size_t x) { return (x + 3) & ~size_t(3); }
 
 __device__ __forceinline__ double qr_sign(double beta) { return beta < 0.0 ? -1.0 : 1.0; }
 
-// Shared-memory carve-up (doubles): Ps[rows×(nb+1)] | Ts[nb×nb] | V1[nb×nb] |
-// M1[nb×nb] | beta[n] | red[8×32] | svec[32] | prow[32] | wt[32] | stage[4096] | wsl[nb×⌈n/G⌉]
 struct QrSmem {
-  double *Ps, *Ts, *V1, *M1, *beta, *red, *svec, *prow, *wt, *stage, *wsl;
+  double* Ps;     // rch × 33: the CTA's rows of the panel (one chunk)
+  double* mat;    // QR_NSMALL × 32 × 33 scratch matrices
+  double* beta;   // n   (signed diag of R)
+  double* small;  // 256 reduction + 8 × 32 vectors
+  double* stage;  // 2 × 4096 (double-buffered tiles)
+  double* wsl;    // 32 × ⌈n/G⌉
+  __device__ double* M(int k) const { return mat + k * qr_pad4(QR_NB * QR_SLD); }
 };
 
-__host__ __device__ inline size_t qr_smem_doubles(long rows_per_cta, int nb, long n, int grid) {
-  return size_t(rows_per_cta) * (nb + 1) + 3 * size_t(nb) * nb + size_t(n) + 8 * 32 + 3 * 32 +
-         QR_STAGE_DOUBLES + size_t(nb) * ceil_div(n, grid);
+__host__ __device__ inline size_t qr_smem_doubles(long rch, long n, int grid) {
+  return qr_pad4(size_t(rch) * QR_PLD) + QR_NSMALL * qr_pad4(size_t(QR_NB) * QR_SLD) + qr_pad4(n) + 256 +
+         8 * 32 + 2 * QR_TILE_DOUBLES + qr_pad4(size_t(QR_NB) * ceil_div(n, grid)) + 8;
 }
 
-// W-partial of this CTA: wpart[cta][i][c] = Σ_{r∈[ra,r1)} V[r][i]·X[r][c0+c],
-// X = A[:, col0 : col0+ntr].  Thread (ib, cb) owns a 4×4 block of (i, c).
-__device__ void qr_wpartial(const QrArgs& p, const QrSmem& s, int nb, long r0, long ra, long r1,
-                            long col0, long ntr) {
+// --------------------------------------------------------------------------
+// Deterministic parallel reduction over the G CTA partials.  Entry e's partial
+// from CTA q lives at addr(e) + q·stride.  `tpe` threads share an entry; each
+// loads its partials q ≡ g (mod tpe) in independent batches and adds them in
+// increasing q, then the tpe sub-sums are added in increasing g.  The order is
+// a function of (E, G) only, so results are bitwise reproducible.
+template <class Addr, class Sink>
+__device__ __forceinline__ void qr_reduce_entries(int E, int G, size_t stride, Addr addr, Sink sink, double* red) {
   const int tid = threadIdx.x;
-  const int CW = QR_STAGE_DOUBLES / nb;  // columns per chunk
-  const int CB = CW / 4;
-  const int ib = tid / CB, cb = tid % CB;
-  const int PLD = nb + 1;
-  double* wdst = p.wpart + size_t(blockIdx.x) * QR_NBMAX * p.n;
-  for (long c0 = 0; c0 < ntr; c0 += CW) {
+  for (int e0 = 0; e0 < E; e0 += QR_THREADS) {
+    const int ecount = min(E - e0, QR_THREADS);
+    int tpe = 1;
+    while (tpe * 2 * ecount <= QR_THREADS && tpe * 2 <= G) tpe *= 2;
+    const int el = tid / tpe, g = tid % tpe;
+    double acc = 0.0;
+    if (el < ecount) {
+      const double* src = addr(e0 + el);
+      int q = g;
+      for (; q + 7 * tpe < G; q += 8 * tpe) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + size_t(q + u * tpe) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+      }
+      for (; q < G; q += tpe) acc += __ldcg(src + size_t(q) * stride);
+    }
+    red[tid] = acc;
+    __syncthreads();
+    if (tid < ecount) {
+      double sum = 0.0;
+      for (int j = 0; j < tpe; ++j) sum += red[tid * tpe + j];
+      sink(e0 + tid, sum);
+    }
+    __syncthreads();
+  }
+}
+
+// ============================ 32×32 small algebra ============================
+// All routines run on the whole CTA; thread t owns row t/8, columns
+// 4·(t%8)..+3 of the 32×32 result.  Matrices live in shared memory, ld 33.
+
+// C = op(A)·op(B) (opX = transpose when TX); C must not alias A or B.
+template <bool TA, bool TB>
+__device__ __forceinline__ void sm_mm(double* C, const double* A, const double* B) {
+  const int i = threadIdx.x >> 3, c0 = (threadIdx.x & 7) << 2;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int q = 0; q < QR_NB; ++q) {
+    const double a = TA ? A[q * QR_SLD + i] : A[i * QR_SLD + q];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = fma(a, TB ? B[(c0 + u) * QR_SLD + q] : B[q * QR_SLD + c0 + u], acc[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) C[i * QR_SLD + c0 + u] = acc[u];
+  __syncthreads();
+}
+
+// X = inv(op(U)) for upper-triangular op(U) (op = transpose when TRANS, i.e.
+// the stored input is lower triangular); UNIT assumes a unit diagonal.
+// Log-depth recursive doubling: [[A, B], [0, C]]⁻¹ = [[A⁻¹, −A⁻¹·B·C⁻¹],
+// [0, C⁻¹]] for block sizes 1, 2, 4, 8, 16.  Z is 32×32 scratch.
+template <bool TRANS, bool UNIT>
+__device__ __forceinline__ void sm_tri_inv_upper(double* X, const double* U, double* Z) {
+  const int tid = threadIdx.x;
+  const int i = tid >> 3, c0 = (tid & 7) << 2;
+  auto u_at = [&](int r, int c) { return TRANS ? U[c * QR_SLD + r] : U[r * QR_SLD + c]; };
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int c = c0 + v;
+    X[i * QR_SLD + c] = (i == c) ? (UNIT ? 1.0 : 1.0 / u_at(i, i)) : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int lv = 0; lv < 5; ++lv) {
+    const int b = 1 << lv;  // merge pairs of b×b blocks into 2b×2b
+    // Z = B·C⁻¹ for every pair, entries (r, c) ∈ [0,b)²; 16b ≤ 256 entries
+    if (tid < 16 * b) {
+      const int pair = tid / (b * b), rr = (tid / b) % b, cc = tid % b;
+      const int a0 = pair * 2 * b, k0 = a0 + b;
+      double acc = 0.0;
+      for (int q = 0; q <= cc; ++q) acc = fma(u_at(a0 + rr, k0 + q), X[(k0 + q) * QR_SLD + k0 + cc], acc);
+      Z[(a0 + rr) * QR_SLD + k0 + cc] = acc;
+    }
+    __syncthreads();
+    // X[A, C] = −A⁻¹·Z
+    if (tid < 16 * b) {
+      const int pair = tid / (b * b), rr = (tid / b) % b, cc = tid % b;
+      const int a0 = pair * 2 * b, k0 = a0 + b;
+      double acc = 0.0;
+      for (int q = rr; q < b; ++q) acc = fma(X[(a0 + rr) * QR_SLD + a0 + q], Z[(a0 + q) * QR_SLD + k0 + cc], acc);
+      X[(a0 + rr) * QR_SLD + k0 + cc] = -acc;
+    }
+    __syncthreads();
+  }
+}
+
+// Sequential elimination shared by the Cholesky and the LU: step j publishes
+// the final pivot row j and 1/pivot through shared memory (one barrier and
+// one dependent reciprocal per step); every thread below the pivot updates its
+// 4 entries.  SYM = Cholesky (Schur complement of a symmetric matrix,
+// multipliers from the pivot row), else LU (multipliers from the own row,
+// stored in place of the eliminated entry).
+template <bool SYM>
+__device__ __forceinline__ void sm_eliminate(double (&v)[4], double* row_sm /*64*/, double* inv_sm /*2*/) {
+  const int tid = threadIdx.x;
+  const int i = tid >> 3, c0 = (tid & 7) << 2;
+#pragma unroll 1
+  for (int j = 0; j < QR_NB; ++j) {
+    const int b = j & 1;
+    if (i == j) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) row_sm[b * 32 + c0 + u] = v[u];
+      const int jj = j - c0;
+      if (jj >= 0 && jj < 4) {
+        double pv = v[0];
+        if (jj == 1) pv = v[1];
+        if (jj == 2) pv = v[2];
+        if (jj == 3) pv = v[3];
+        inv_sm[b] = 1.0 / pv;
+      }
+    }
+    double own = 0.0;
+    if (!SYM) {  // entry (i, j), held by lane (row base + j/4) of this warp
+      double cand = v[0];
+      if ((j & 3) == 1) cand = v[1];
+      if ((j & 3) == 2) cand = v[2];
+      if ((j & 3) == 3) cand = v[3];
+      own = __shfl_sync(0xffffffffu, cand, ((tid & ~7) | (j >> 2)) & 31);
+    }
+    __syncthreads();
+    if (i > j) {
+      const double f = (SYM ? row_sm[b * 32 + i] : own) * inv_sm[b];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int l = c0 + u;
+        if (l > j) v[u] = fma(-f, row_sm[b * 32 + l], v[u]);
+        if (!SYM && l == j) v[u] = f;
+      }
+    }
+  }
+}
+
+// Upper Cholesky of the symmetric 32×32 matrix G (in place; upper triangle
+// receives R with RᵀR = G, lower triangle zeroed).  Returns min/max of
+// diag(R), or -1 if a pivot was not positive.
+__device__ double sm_chol(double* G, double* vec /*≥ 96*/) {
+  __shared__ double s_ratio;
+  const int tid = threadIdx.x;
+  const int i = tid >> 3, c0 = (tid & 7) << 2;
+  double v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = G[i * QR_SLD + c0 + u];
+  __syncthreads();
+  sm_eliminate<true>(v, vec, vec + 64);
+  __syncthreads();
+  // pivots → diag(R); row i of R = (row i of the Schur complement)/R_ii
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (c0 + u == i) vec[i] = v[u];
+  __syncthreads();
+  if (tid < 32) {
+    const double d = vec[tid];
+    const bool ok = __all_sync(0xffffffffu, d > 0.0);
+    const double r = sqrt(fmax(d, 0.0));
+    double mn = r, mx = r;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (tid == 0) s_ratio = ok ? mn / mx : -1.0;
+  }
+  const double rd = sqrt(vec[i]), inv = 1.0 / rd;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int l = c0 + u;
+    G[i * QR_SLD + l] = (l > i) ? v[u] * inv : ((l == i) ? rd : 0.0);
+  }
+  __syncthreads();
+  return s_ratio;
+}
+
+// Unpivoted LU of the 32×32 matrix M in place: strict lower = unit-lower
+// factor, upper = U.
+__device__ void sm_lu(double* M, double* vec) {
+  const int i = threadIdx.x >> 3, c0 = (threadIdx.x & 7) << 2;
+  double v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = M[i * QR_SLD + c0 + u];
+  __syncthreads();
+  sm_eliminate<false>(v, vec, vec + 64);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) M[i * QR_SLD + c0 + u] = v[u];
+  __syncthreads();
+}
+
+// Cholesky factor of a near-identity Gram matrix G = I + E (‖E‖ tiny) by the
+// quadratically convergent series R = I + X, X ← split(E − XᵀX),
+// split(M) = triu(M, 1) + diag(M)/2 — no sequential pivots.  The second
+// Cholesky-QR pass has G = I + O(u·κ²).  R (upper, zeros below) goes to Rout;
+// returns max|E|.
+__device__ double sm_chol_near_identity(double* Rout, const double* G, double* X) {
+  __shared__ unsigned long long s_emax;
+  const int tid = threadIdx.x;
+  const int i = tid >> 3, c0 = (tid & 7) << 2;
+  double e[4];
+  double emax = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    e[u] = G[i * QR_SLD + c0 + u] - ((i == c0 + u) ? 1.0 : 0.0);
+    emax = fmax(emax, fabs(e[u]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  if (tid == 0) s_emax = 0ull;
+  __syncthreads();
+  if ((tid & 31) == 0) atomicMax(&s_emax, (unsigned long long)__double_as_longlong(emax));
+  auto split = [&](int l, double x) { return (l > i) ? x : ((l == i) ? 0.5 * x : 0.0); };
+#pragma unroll
+  for (int u = 0; u < 4; ++u) X[i * QR_SLD + c0 + u] = split(c0 + u, e[u]);
+  __syncthreads();
+#pragma unroll 1
+  for (int it = 0; it < 3; ++it) {
+    double nx[4] = {e[0], e[1], e[2], e[3]};
+#pragma unroll
+    for (int q = 0; q < QR_NB; ++q) {
+      const double xqi = (q <= i) ? X[q * QR_SLD + i] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) nx[u] = fma(-xqi, X[q * QR_SLD + c0 + u], nx[u]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) X[i * QR_SLD + c0 + u] = split(c0 + u, nx[u]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int l = c0 + u;
+    Rout[i * QR_SLD + l] = (l >= i) ? X[i * QR_SLD + l] + ((l == i) ? 1.0 : 0.0) : 0.0;
+  }
+  __syncthreads();
+  return __longlong_as_double((long long)*(volatile unsigned long long*)&s_emax);
+}
+
+// ======================= row-chunk helpers (panel rows) ======================
+// The CTA's active rows [ra, r1) are processed in chunks of p.rch rows held in
+// s.Ps (resident when one chunk covers all rows).
+
+// Ps[rr][c] = A[cs + rr][col0 + c] for c < 32 and chunk rows [cs, ce).
+__device__ __forceinline__ void qr_load_chunk(const QrArgs& p, const QrSmem& s, long cs, long ce, long col0) {
+  const int rows = int(ce - cs);
+  for (int e = threadIdx.x; e < rows * 16; e += QR_THREADS) {
+    const int rr = e >> 4, cc = (e & 15) << 1;
+    const double2 v = *reinterpret_cast<const double2*>(p.A + (cs + rr) * p.lda + col0 + cc);
+    s.Ps[rr * QR_PLD + cc] = v.x;
+    s.Ps[rr * QR_PLD + cc + 1] = v.y;
+  }
+}
+__device__ __forceinline__ void qr_store_chunk(const QrArgs& p, const QrSmem& s, long cs, long ce, long col0) {
+  const int rows = int(ce - cs);
+  for (int e = threadIdx.x; e < rows * 16; e += QR_THREADS) {
+    const int rr = e >> 4, cc = (e & 15) << 1;
+    *reinterpret_cast<double2*>(p.A + (cs + rr) * p.lda + col0 + cc) =
+        make_double2(s.Ps[rr * QR_PLD + cc], s.Ps[rr * QR_PLD + cc + 1]);
+  }
+}
+// V form of the factored panel k (stored in A: R on/above the diagonal of the
+// pivot rows, V below): unit diagonal, zeros above and beyond column jb.
+__device__ __forceinline__ void qr_load_chunk_vform(const QrArgs& p, const QrSmem& s, long cs, long ce, long k,
+                                                    int jb) {
+  const int rows = int(ce - cs);
+  for (int e = threadIdx.x; e < rows * 32; e += QR_THREADS) {
+    const int rr = e >> 5, c = e & 31;
+    const long r = cs + rr;
+    double v;
+    if (c >= jb || r < k + c) v = 0.0;
+    else if (r == k + c) v = 1.0;
+    else v = p.A[r * p.lda + k + c];
+    s.Ps[rr * QR_PLD + c] = v;
+  }
+}
+
+// Gram partial accumulation over chunk rows: thread (rg = t/64, blk = t%64)
+// owns a 4×4 block of the 32×32 Gram for rows ≡ rg (mod 4).
+__device__ __forceinline__ void qr_gram_accum(const QrSmem& s, int rows, double (&acc)[4][4]) {
+  const int tid = threadIdx.x;
+  const int rg = tid >> 6, blk = tid & 63;
+  const int ab = (blk >> 3) << 2, bb = (blk & 7) << 2;
+  for (int rr = rg; rr < rows; rr += 4) {
+    const double* row = s.Ps + rr * QR_PLD;
+    double pa[4], pb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      pa[u] = row[ab + u];
+      pb[u] = row[bb + u];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(pa[a], pb[b], acc[a][b]);
+  }
+}
+// Combine the 4 row-group partials (fixed order) and publish to dst (global).
+__device__ __forceinline__ void qr_gram_publish(const QrSmem& s, double (&acc)[4][4], double* dst) {
+  const int tid = threadIdx.x;
+  const int rg = tid >> 6, blk = tid & 63;
+  const int ab = (blk >> 3) << 2, bb = (blk & 7) << 2;
+  __syncthreads();
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) s.stage[rg * 1024 + (ab + a) * 32 + bb + b] = acc[a][b];
+  __syncthreads();
+  for (int e = tid; e < 1024; e += QR_THREADS)
+    __stcg(dst + e, ((s.stage[e] + s.stage[1024 + e]) + s.stage[2048 + e]) + s.stage[3072 + e]);
+}
+
+// Slice reduction of the Gram partials (1024 entries) into p.gfin.
+__device__ void qr_gram_reduce(const QrArgs& p, double* red) {
+  const int G = gridDim.x;
+  const int e0 = int(long(blockIdx.x) * 1024 / G), e1 = int(long(blockIdx.x + 1) * 1024 / G);
+  const double* base = p.wpart;
+  double* out = p.gfin;
+  qr_reduce_entries(
+      e1 - e0, G, size_t(QR_NB) * qr_ldw(p.n), [=](int e) { return base + e0 + e; },
+      [=](int e, double v) { __stcg(out + e0 + e, v); }, red);
+}
+
+// Chunk rows × W (32×32, smem) in place: Ps[rr][:] ← Ps[rr][:]·W.  Thread
+// (rb = t/8, cb = t%8) computes 4 rows × 4 columns per 128-row block.
+__device__ __forceinline__ void qr_rows_times(const QrSmem& s, int rows, const double* W) {
+  const int tid = threadIdx.x;
+  const int rb = (tid >> 3) << 2, cb = (tid & 7) << 2;
+  for (int b0 = 0; b0 < rows; b0 += 128) {
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    for (long rc = ra; rc < r1; rc += nb) {
-      const int rows = int(lmin(nb, r1 - rc));
-      // stage X[rc : rc+rows, c0 : c0+CW]
-      for (int e = tid; e < nb * CW; e += QR_THREADS) {
-        const int rr = e / CW, cc = e % CW;
-        double v = 0.0;
-        if (rr < rows && c0 + cc < ntr) v = p.A[(rc + rr) * p.lda + col0 + c0 + cc];
-        s.stage[e] = v;
+    const bool any = b0 + rb < rows;
+    if (any) {
+#pragma unroll 8
+      for (int q = 0; q < QR_NB; ++q) {
+        double x[4], w[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) x[a] = (b0 + rb + a < rows) ? s.Ps[(b0 + rb + a) * QR_PLD + q] : 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) w[b] = W[q * QR_SLD + cb + b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], w[b], acc[a][b]);
+      }
+    }
+    __syncthreads();
+    if (any) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (b0 + rb + a < rows)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) s.Ps[(b0 + rb + a) * QR_PLD + cb + b] = acc[a][b];
+    }
+    __syncthreads();
+  }
+}
+
+// ====================== trailing update (GEMM-shaped) =======================
+// Accumulate this chunk's contribution to the W partial of columns
+// [col0, col0+ntr):  W[i][c] += Σ_rr V[rr][i]·X[row][c].  The W partial lives
+// in the CTA's wpart slot (first chunk writes, later chunks accumulate).
+// X tiles (32 rows × 128 columns) stream through a double-buffered cp.async
+// ring; thread (ib, cb) owns 4 i × 4 strided columns.
+__device__ void qr_wpartial_chunk(const QrArgs& p, const QrSmem& s, long cs, long ce, long col0, long ntr,
+                                  bool first) {
+  const int tid = threadIdx.x;
+  constexpr int CB = QR_CW / 4;  // 32
+  const int ib = tid / CB, cb = tid % CB;
+  const long ldw = qr_ldw(p.n);
+  double* wdst = p.wpart + size_t(blockIdx.x) * QR_NB * ldw;
+  const int nrows = int(ce - cs);
+  const int nrc = (nrows + QR_NB - 1) / QR_NB;
+  for (long c0 = 0; c0 < ntr; c0 += QR_CW) {
+    auto load = [&](int t, int buf) {
+      double* dst = s.stage + buf * QR_TILE_DOUBLES;
+      const long rc = cs + long(t) * QR_NB;
+      for (int e = tid; e < QR_NB * QR_CW / 2; e += QR_THREADS) {
+        const int rr = e / (QR_CW / 2), cc = (e % (QR_CW / 2)) * 2;
+        const long c = c0 + cc;
+        int bytes = 0;
+        const double* src = p.A;
+        if (rc + rr < ce && c < ntr) {
+          bytes = int(lmin(2, ntr - c)) * 8;
+          src = p.A + (rc + rr) * p.lda + col0 + c;
+        }
+        cp_async16(dst + rr * QR_CW + cc, src, bytes);
+      }
+      cp_async_commit();
+    };
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    if (nrc > 0) load(0, 0);
+    for (int t = 0; t < nrc; ++t) {
+      if (t + 1 < nrc) {
+        load(t + 1, (t + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
       }
       __syncthreads();
+      const double* tile = s.stage + (t & 1) * QR_TILE_DOUBLES;
+      const int rows = min(QR_NB, nrows - t * QR_NB);
       for (int rr = 0; rr < rows; ++rr) {
-        const double* vrow = s.Ps + (rc + rr - r0) * PLD + ib * 4;
-        const double* xrow = s.stage + rr * CW + cb;
+        const double* vrow = s.Ps + (t * QR_NB + rr) * QR_PLD + ib * 4;
+        const double* xrow = tile + rr * QR_CW + cb;
         double v[4], x[4];
 #pragma unroll
         for (int a = 0; a < 4; ++a) v[a] = vrow[a];
@@ -104,73 +539,78 @@ __device__ void qr_wpartial(const QrArgs& p, const QrSmem& s, int nb, long r0, l
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const long c = c0 + cb + b * CB;
-        if (c < ntr) __stcg(wdst + size_t(ib * 4 + a) * p.n + c, acc[a][b]);
+        if (c < ntr) {
+          double* w = wdst + size_t(ib * 4 + a) * ldw + c;
+          __stcg(w, first ? acc[a][b] : acc[a][b] + __ldcg(w));
+        }
       }
   }
+  __syncthreads();
 }
 
 // Fixed-order reduction of the W partials over CTAs for this CTA's column
 // slice, then Y = op(T)·W for the slice (op = transpose when `trans_t`).
-__device__ void qr_reduce_slice(const QrArgs& p, const QrSmem& s, int nb, long ntr, bool trans_t) {
+__device__ void qr_reduce_slice(const QrArgs& p, const QrSmem& s, const double* Ts, long ntr, bool trans_t) {
   const int tid = threadIdx.x;
   const int G = gridDim.x;
+  const long ldw = qr_ldw(p.n);
   const long cs = long(blockIdx.x) * ntr / G, ce = long(blockIdx.x + 1) * ntr / G;
   const int sw = int(ce - cs);
   if (sw <= 0) return;
-  for (int e = tid; e < nb * sw; e += QR_THREADS) {
-    const int i = e / sw, c = e % sw;
-    double acc = 0.0;
-    const double* src = p.wpart + size_t(i) * p.n + cs + c;
-    for (int q = 0; q < G; ++q) acc += __ldcg(src + size_t(q) * QR_NBMAX * p.n);
-    s.wsl[i * sw + c] = acc;
-  }
-  __syncthreads();
-  for (int e = tid; e < nb * sw; e += QR_THREADS) {
+  const double* base = p.wpart + cs;
+  double* wsl = s.wsl;
+  qr_reduce_entries(
+      QR_NB * sw, G, size_t(QR_NB) * ldw, [=](int e) { return base + size_t(e / sw) * ldw + e % sw; },
+      [=](int e, double v) { wsl[e] = v; }, s.small);
+  for (int e = tid; e < QR_NB * sw; e += QR_THREADS) {
     const int i = e / sw, c = e % sw;
     double acc = 0.0;
     if (trans_t) {
-      for (int l = 0; l <= i; ++l) acc = fma(s.Ts[l * nb + i], s.wsl[l * sw + c], acc);
+      for (int l = 0; l <= i; ++l) acc = fma(Ts[l * QR_SLD + i], s.wsl[l * sw + c], acc);
     } else {
-      for (int l = i; l < nb; ++l) acc = fma(s.Ts[i * nb + l], s.wsl[l * sw + c], acc);
+      for (int l = i; l < QR_NB; ++l) acc = fma(Ts[i * QR_SLD + l], s.wsl[l * sw + c], acc);
     }
-    __stcg(p.ybuf + size_t(i) * p.n + cs + c, acc);
+    __stcg(p.ybuf + size_t(i) * qr_ldy(p.n) + cs + c, acc);
   }
 }
 
-// Row-local update X[r][c] -= Σ_i V[r][i]·Y[i][c] for owned rows [ra, r1).
-__device__ void qr_apply_update(const QrArgs& p, const QrSmem& s, int nb, long r0, long ra, long r1,
-                                long col0, long ntr) {
+// Row-local update of this chunk: X[row][c] -= Σ_i V[rr][i]·Y[i][c].
+__device__ void qr_update_chunk(const QrArgs& p, const QrSmem& s, long cs, long ce, long col0, long ntr) {
   const int tid = threadIdx.x;
-  const int CW = QR_STAGE_DOUBLES / nb;
-  const int CB = CW / 4;
+  constexpr int CB = QR_CW / 4;
   const int rb = tid / CB, cb = tid % CB;
-  const int PLD = nb + 1;
-  for (long c0 = 0; c0 < ntr; c0 += CW) {
+  const int nrows = int(ce - cs);
+  for (long c0 = 0; c0 < ntr; c0 += QR_CW) {
     __syncthreads();
-    for (int e = tid; e < nb * CW; e += QR_THREADS) {
-      const int i = e / CW, cc = e % CW;
-      s.stage[e] = (c0 + cc < ntr) ? __ldcg(p.ybuf + size_t(i) * p.n + c0 + cc) : 0.0;
+    for (int e = tid; e < QR_NB * QR_CW / 2; e += QR_THREADS) {
+      const int i = e / (QR_CW / 2), cc = (e % (QR_CW / 2)) * 2;
+      const long c = c0 + cc;
+      const int bytes = (c < ntr) ? int(lmin(2, ntr - c)) * 8 : 0;
+      cp_async16(s.stage + i * QR_CW + cc, bytes ? p.ybuf + size_t(i) * qr_ldy(p.n) + c : p.ybuf, bytes);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
-    for (long rc = ra; rc < r1; rc += nb) {
+    for (int rc = 0; rc < nrows; rc += QR_NB) {
       double acc[4][4];
       bool ok[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        const long r = rc + rb * 4 + a;
-        ok[a] = r < r1;
+        const int rr = rc + rb * 4 + a;
+        ok[a] = rr < nrows;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const long c = c0 + cb + b * CB;
-          acc[a][b] = (ok[a] && c < ntr) ? p.A[r * p.lda + col0 + c] : 0.0;
+          acc[a][b] = (ok[a] && c < ntr) ? p.A[(cs + rr) * p.lda + col0 + c] : 0.0;
         }
       }
-      for (int i = 0; i < nb; ++i) {
+#pragma unroll 4
+      for (int i = 0; i < QR_NB; ++i) {
         double y[4], v[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) y[b] = s.stage[i * CW + cb + b * CB];
+        for (int b = 0; b < 4; ++b) y[b] = s.stage[i * QR_CW + cb + b * CB];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) v[a] = ok[a] ? s.Ps[(rc + rb * 4 + a - r0) * PLD + i] : 0.0;
+        for (int a = 0; a < 4; ++a) v[a] = ok[a] ? s.Ps[(rc + rb * 4 + a) * QR_PLD + i] : 0.0;
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -179,7 +619,7 @@ __device__ void qr_apply_update(const QrArgs& p, const QrSmem& s, int nb, long r
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         if (!ok[a]) continue;
-        const long r = rc + rb * 4 + a;
+        const long r = cs + rc + rb * 4 + a;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const long c = c0 + cb + b * CB;
@@ -191,153 +631,356 @@ __device__ void qr_apply_update(const QrArgs& p, const QrSmem& s, int nb, long r
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
-  extern __shared__ __align__(16) double qsm[];
-  const int nb = p.nb;
-  const int PLD = nb + 1;
-  const long m = p.m, n = p.n;
+// ============ fallback: column-by-column Householder (any jb ≤ 32) ==========
+// Needs the CTA's active rows resident (one chunk, Ps row rr ↔ row ra + rr).
+// On return Ps holds the factored panel (R on/above the pivot diagonal, V
+// below), Ts the T factor and s.beta the signed diagonal.
+__device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* Ts, long k, int jb, long ra,
+                                     long r1, unsigned int& gen) {
   const int tid = threadIdx.x;
   const int G = gridDim.x;
+  double* red = s.small;          // 256
+  double* svec = s.small + 256;   // 32
+  double* prow = svec + 32;       // 32
+  double* wt = prow + 32;         // 32
+  for (int e = tid; e < QR_NB * QR_SLD; e += QR_THREADS) Ts[e] = 0.0;
+  __syncthreads();
+  const int nrows = int(lmax(0L, r1 - ra));
+  for (int jj = 0; jj < jb; ++jj) {
+    const long piv = k + jj;
+    const int buf = int(piv & 1);
+    {
+      const int c = tid & 31, grp = tid >> 5;
+      double a0 = 0.0, a1 = 0.0;
+      if (c < jb) {
+        int rr = int(lmax(0L, piv + 1 - ra)) + grp;
+        for (; rr + 8 < nrows; rr += 16) {
+          const double* row0 = s.Ps + rr * QR_PLD;
+          const double* row1 = row0 + 8 * QR_PLD;
+          a0 = fma(row0[jj], row0[c], a0);
+          a1 = fma(row1[jj], row1[c], a1);
+        }
+        if (rr < nrows) {
+          const double* row0 = s.Ps + rr * QR_PLD;
+          a0 = fma(row0[jj], row0[c], a0);
+        }
+      }
+      red[grp * 32 + c] = a0 + a1;
+    }
+    __syncthreads();
+    if (tid < jb) {
+      double acc = 0.0;
+#pragma unroll
+      for (int g2 = 0; g2 < 8; ++g2) acc += red[g2 * 32 + tid];
+      __stcg(p.part + (size_t(buf) * G + blockIdx.x) * 32 + tid, acc);
+      if (piv >= ra && piv < r1) __stcg(p.pivrow + buf * 32 + tid, s.Ps[(piv - ra) * QR_PLD + tid]);
+    }
+    grid_barrier(p.counter, gen);
+    {
+      const double* base = p.part + size_t(buf) * G * 32;
+      qr_reduce_entries(
+          jb, G, 32, [=](int e) { return base + e; }, [=](int e, double v) { svec[e] = v; }, red);
+    }
+    if (tid < jb) prow[tid] = __ldcg(p.pivrow + buf * 32 + tid);
+    __syncthreads();
+    const double alpha = prow[jj], sigma = svec[jj];
+    double beta, tau, scale;
+    if (sigma == 0.0) {
+      beta = alpha;
+      tau = 0.0;
+      scale = 0.0;
+    } else {
+      const double nrm = sqrt(fma(alpha, alpha, sigma));
+      beta = signbit(alpha) ? nrm : -nrm;
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    if (tid < jb) wt[tid] = (tid > jj) ? tau * fma(scale, svec[tid], prow[tid]) : 0.0;
+    if (tid < jj) {
+      double acc = 0.0;
+      for (int l = tid; l < jj; ++l) acc = fma(Ts[tid * QR_SLD + l], fma(scale, svec[l], prow[l]), acc);
+      Ts[tid * QR_SLD + jj] = -tau * acc;
+    }
+    if (tid == 0) {
+      Ts[jj * QR_SLD + jj] = tau;
+      s.beta[piv] = beta;
+    }
+    __syncthreads();
+    const int rs = int(lmax(0L, piv - ra));
+    const int ncol = jb - jj;
+    for (int e = tid; e < (nrows - rs) * ncol; e += QR_THREADS) {
+      const int rr = rs + e / ncol;
+      const int c = jj + e % ncol;
+      double* row = s.Ps + rr * QR_PLD;
+      if (ra + rr == piv) {
+        row[c] = (c == jj) ? beta : row[c] - wt[c];
+      } else if (c > jj) {
+        row[c] = fma(-wt[c], scale * row[jj], row[c]);
+      }
+    }
+    __syncthreads();
+    for (int rr = int(lmax(0L, piv + 1 - ra)) + tid; rr < nrows; rr += QR_THREADS) s.Ps[rr * QR_PLD + jj] *= scale;
+    __syncthreads();
+  }
+}
+
+// ================================ the kernel ================================
+__global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
+  extern __shared__ __align__(16) double qsm[];
+  const long m = p.m, n = p.n;
+  const int tid = threadIdx.x;
   const long r0 = long(blockIdx.x) * p.rows_per_cta;
   const long r1 = lmin(m, r0 + p.rows_per_cta);
+  const long rch = p.rch;
 
   QrSmem s;
   {
     double* q = qsm;
-    s.Ps = q; q += size_t(p.rows_per_cta) * PLD;
-    s.Ts = q; q += nb * nb;
-    s.V1 = q; q += nb * nb;
-    s.M1 = q; q += nb * nb;
-    s.beta = q; q += n;
-    s.red = q; q += 8 * 32;
-    s.svec = q; q += 32;
-    s.prow = q; q += 32;
-    s.wt = q; q += 32;
-    s.stage = q; q += QR_STAGE_DOUBLES;
+    s.Ps = q; q += qr_pad4(size_t(rch) * QR_PLD);
+    s.mat = q; q += QR_NSMALL * qr_pad4(size_t(QR_NB) * QR_SLD);
+    s.beta = q; q += qr_pad4(n);
+    s.small = q; q += 256 + 8 * 32;
+    s.stage = q; q += 2 * QR_TILE_DOUBLES;
     s.wsl = q;
   }
+  // named 32×32 scratch matrices
+  double* R1 = s.M(0);    // Cholesky factor of pass 1
+  double* R1i = s.M(1);   // R₁⁻¹
+  double* R2 = s.M(2);    // Cholesky factor of pass 2
+  double* R2i = s.M(3);   // R₂⁻¹
+  double* Ts = s.M(4);    // T
+  double* LU = s.M(5);    // LU(I − Q₁S), later V₁ for the Q formation
+  double* Wm = s.M(6);    // per-row transform of the current pass
+  double* Z = s.M(7);     // scratch
+  double* Pp = s.M(8);    // pivot rows of the panel, later R_p
+  double* Ui = s.M(9);    // U⁻¹
+  double* Lt = s.M(10);   // V₁⁻ᵀ, later M1 = T·V₁ᵀ
+  double* SR = s.M(11);   // S·R_p
+  double* vec = s.small + 256;         // 96: elimination rows (0..63) and pivots (64..65)
+  double* svec = s.small + 256 + 128;  // 32: S signs
   unsigned int gen = 0;
+  int nfallback = 0;
+  unsigned long long t_phase = (p.phase_ns && blockIdx.x == 0 && tid == 0) ? qr_now() : 0;
+  const bool resident = p.rows_per_cta <= rch;  // same for every CTA (barrier counts must agree)
 
   // ===================== factorization (dgeqrf) =====================
-  for (long k = 0, pidx = 0; k < n; k += nb, ++pidx) {
-    const int jb = int(lmin(nb, n - k));
+  for (long k = 0, pidx = 0; k < n; k += QR_NB, ++pidx) {
+    const int jb = int(lmin(QR_NB, n - k));
     const long ra = lmax(r0, k);  // first active owned row
-    for (long e = tid; e < (r1 - ra) * jb; e += QR_THREADS) {
-      const long r = ra + e / jb;
-      const int c = int(e % jb);
-      s.Ps[(r - r0) * PLD + c] = p.A[r * p.lda + k + c];
-    }
-    for (int e = tid; e < nb * nb; e += QR_THREADS) s.Ts[e] = 0.0;
-    __syncthreads();
-
-    for (int jj = 0; jj < jb; ++jj) {
-      const long piv = k + jj;
-      const int buf = int(piv & 1);
-      // (1) partial dots of the pivot column with all panel columns, rows > piv
-      {
-        const int c = tid & 31, grp = tid >> 5;
-        double acc = 0.0;
-        if (c < jb) {
-          for (long r = lmax(r0, piv + 1) + grp; r < r1; r += 8) {
-            const double* row = s.Ps + (r - r0) * PLD;
-            acc = fma(row[jj], row[c], acc);
+    double* gdst = p.wpart + size_t(blockIdx.x) * QR_NB * qr_ldw(n);
+    bool fast = false;
+    if (jb == QR_NB) {
+      // ---- pass 1: Gram partial (+ publish the pivot rows)
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (long cs = ra; cs < r1; cs += rch) {
+        const long ce = lmin(r1, cs + rch);
+        qr_load_chunk(p, s, cs, ce, k);
+        __syncthreads();
+        qr_gram_accum(s, int(ce - cs), acc);
+        for (int e = tid; e < int(lmin(ce, k + QR_NB) - cs) * QR_NB; e += QR_THREADS) {
+          const int rr = e >> 5, c = e & 31;
+          __stcg(p.pivbuf + (cs + rr - k) * 32 + c, s.Ps[rr * QR_PLD + c]);
+        }
+        if (!resident) __syncthreads();
+      }
+      qr_gram_publish(s, acc, gdst);
+      grid_barrier(p.counter, gen);
+      QR_PHASE(0);
+      qr_gram_reduce(p, s.small);
+      grid_barrier(p.counter, gen);
+      for (int e = tid; e < 1024; e += QR_THREADS) {
+        R1[(e >> 5) * QR_SLD + (e & 31)] = __ldcg(p.gfin + e);
+        Pp[(e >> 5) * QR_SLD + (e & 31)] = __ldcg(p.pivbuf + e);
+      }
+      __syncthreads();
+      const double ratio1 = sm_chol(R1, vec);
+      fast = ratio1 > QR_FAST_DIAG_RATIO;
+      QR_PHASE(1);
+      if (fast) {
+        sm_tri_inv_upper<false, false>(R1i, R1, Z);
+        // ---- pass 2: Q₁ = P·R₁⁻¹ (rows in place) + Gram of Q₁
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (long cs = ra; cs < r1; cs += rch) {
+          const long ce = lmin(r1, cs + rch);
+          if (!resident) {
+            qr_load_chunk(p, s, cs, ce, k);
+            __syncthreads();
+          }
+          qr_rows_times(s, int(ce - cs), R1i);
+          qr_gram_accum(s, int(ce - cs), acc);
+          if (!resident) {
+            __syncthreads();
+            qr_store_chunk(p, s, cs, ce, k);
+            __syncthreads();
           }
         }
-        s.red[grp * 32 + c] = acc;
-      }
-      __syncthreads();
-      if (tid < jb) {
-        double acc = 0.0;
-#pragma unroll
-        for (int g2 = 0; g2 < 8; ++g2) acc += s.red[g2 * 32 + tid];
-        __stcg(p.part + (size_t(buf) * G + blockIdx.x) * 32 + tid, acc);
-        if (piv >= r0 && piv < r1) __stcg(p.pivrow + buf * 32 + tid, s.Ps[(piv - r0) * PLD + tid]);
-      }
-      grid_barrier(p.counter, gen);
-      // (2) fixed-order reduction over CTAs
-      {
-        const int c = tid & 31, grp = tid >> 5;
-        double acc = 0.0;
-        if (c < jb)
-          for (int q = grp; q < G; q += 8) acc += __ldcg(p.part + (size_t(buf) * G + q) * 32 + c);
-        s.red[grp * 32 + c] = acc;
-      }
-      __syncthreads();
-      if (tid < jb) {
-        double acc = 0.0;
-#pragma unroll
-        for (int g2 = 0; g2 < 8; ++g2) acc += s.red[g2 * 32 + tid];
-        s.svec[tid] = acc;
-        s.prow[tid] = __ldcg(p.pivrow + buf * 32 + tid);
-      }
-      __syncthreads();
-      // (3) Householder scalars (dlarfg convention: beta = -sign(alpha)·‖x‖)
-      const double alpha = s.prow[jj], sigma = s.svec[jj];
-      double beta, tau, scale;
-      if (sigma == 0.0) {
-        beta = alpha;
-        tau = 0.0;
-        scale = 0.0;
-      } else {
-        const double nrm = sqrt(fma(alpha, alpha, sigma));
-        beta = signbit(alpha) ? nrm : -nrm;
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      if (tid < jb) s.wt[tid] = (tid > jj) ? tau * fma(scale, s.svec[tid], s.prow[tid]) : 0.0;
-      // T column jj: T[0:jj, jj] = -tau · T[0:jj, 0:jj] · z,  z_l = v_lᵀ v_jj
-      if (tid < jj) {
-        double acc = 0.0;
-        for (int l = tid; l < jj; ++l) acc = fma(s.Ts[tid * nb + l], fma(scale, s.svec[l], s.prow[l]), acc);
-        s.Ts[tid * nb + jj] = -tau * acc;
-      }
-      if (tid == 0) {
-        s.Ts[jj * nb + jj] = tau;
-        s.beta[piv] = beta;
-      }
-      __syncthreads();
-      // (4) apply H to the CTA's rows of the panel
-      for (long r = lmax(r0, piv) + tid; r < r1; r += QR_THREADS) {
-        double* row = s.Ps + (r - r0) * PLD;
-        if (r == piv) {
-          for (int c = jj + 1; c < jb; ++c) row[c] -= s.wt[c];
-          row[jj] = beta;
-        } else {
-          const double v = scale * row[jj];
-          row[jj] = v;
-          for (int c = jj + 1; c < jb; ++c) row[c] = fma(-s.wt[c], v, row[c]);
+        qr_gram_publish(s, acc, gdst);
+        grid_barrier(p.counter, gen);
+        qr_gram_reduce(p, s.small);
+        grid_barrier(p.counter, gen);
+        for (int e = tid; e < 1024; e += QR_THREADS) Z[(e >> 5) * QR_SLD + (e & 31)] = __ldcg(p.gfin + e);
+        __syncthreads();
+        QR_PHASE(2);
+        // ---- R₂: series when Q₁ᵀQ₁ = I + E with tiny E, else pivots
+        const double emax = sm_chol_near_identity(R2, Z, Wm);
+        if (!(emax <= 1e-5)) {
+          for (int e = tid; e < 1024; e += QR_THREADS) R2[(e >> 5) * QR_SLD + (e & 31)] = Z[(e >> 5) * QR_SLD + (e & 31)];
+          __syncthreads();
+          fast = sm_chol(R2, vec) > 0.5;
+          if (!fast) {
+            // not expected for diag ratio(R₁) > 1e-4: restore P = Q₁·R₁ and
+            // take the fallback
+            for (long cs = ra; cs < r1; cs += rch) {
+              const long ce = lmin(r1, cs + rch);
+              if (!resident) {
+                qr_load_chunk(p, s, cs, ce, k);
+                __syncthreads();
+              }
+              qr_rows_times(s, int(ce - cs), R1);
+              if (!resident) qr_store_chunk(p, s, cs, ce, k);
+              __syncthreads();
+            }
+          }
         }
+        QR_PHASE(12);
+      }
+    }
+    if (fast) {
+      // ---- the 32×32 reconstruction algebra (redundant per CTA)
+      sm_tri_inv_upper<false, false>(R2i, R2, Z);
+      sm_mm<false, false>(Wm, R1i, R2i);   // R_p⁻¹ = R₁⁻¹R₂⁻¹
+      sm_mm<false, false>(Z, Pp, Wm);      // Q₁ = P_piv·R_p⁻¹
+      {
+        const int i = tid >> 3, c0 = (tid & 7) << 2;
+        if (tid < 32) svec[tid] = (Z[tid * QR_SLD + tid] >= 0.0) ? -1.0 : 1.0;  // S = −sign(diag Q₁)
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int l = c0 + u;
+          LU[i * QR_SLD + l] = ((i == l) ? 1.0 : 0.0) - Z[i * QR_SLD + l] * svec[l];
+        }
+        __syncthreads();
+      }
+      QR_PHASE(13);
+      sm_mm<false, false>(Pp, R2, R1);     // R_p = R₂R₁ (pivot rows no longer needed)
+      sm_lu(LU, vec);
+      QR_PHASE(14);
+      {
+        const int i = tid >> 3, c0 = (tid & 7) << 2;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int l = c0 + u;
+          Z[i * QR_SLD + l] = (l >= i) ? LU[i * QR_SLD + l] : 0.0;            // U
+          SR[i * QR_SLD + l] = (l >= i) ? svec[i] * Pp[i * QR_SLD + l] : 0.0;  // S·R_p
+        }
+        __syncthreads();
+      }
+      sm_tri_inv_upper<false, false>(Ui, Z, Wm);  // U⁻¹
+      sm_tri_inv_upper<true, true>(Lt, LU, Wm);   // (V₁ᵀ)⁻¹ = V₁⁻ᵀ
+      sm_mm<false, false>(Ts, Z, Lt);             // T = U·V₁⁻ᵀ
+      {
+        const int i = tid >> 3, c0 = (tid & 7) << 2;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) Z[i * QR_SLD + c0 + u] = -R2i[i * QR_SLD + c0 + u] * svec[c0 + u];
+        __syncthreads();
+      }
+      sm_mm<false, false>(Wm, Z, Ui);             // W₃ = R₂⁻¹·(−S)·U⁻¹
+      if (tid < 32) s.beta[k + tid] = SR[tid * QR_SLD + tid];
+      QR_PHASE(15);
+      // ---- pass 3: V rows = Q₁ rows · W₃ ; pivot rows get S·R_p / V₁
+      for (long cs = ra; cs < r1; cs += rch) {
+        const long ce = lmin(r1, cs + rch);
+        if (!resident) {
+          qr_load_chunk(p, s, cs, ce, k);
+          __syncthreads();
+        }
+        qr_rows_times(s, int(ce - cs), Wm);
+        for (int e = tid; e < int(ce - cs) * QR_NB; e += QR_THREADS) {
+          const int rr = e >> 5, c = e & 31;
+          const long r = cs + rr;
+          double a = s.Ps[rr * QR_PLD + c];  // V row (non-pivot)
+          if (r < k + QR_NB) {
+            const int i = int(r - k);
+            a = (c >= i) ? SR[i * QR_SLD + c] : LU[i * QR_SLD + c];
+            s.Ps[rr * QR_PLD + c] = (c < i) ? LU[i * QR_SLD + c] : ((c == i) ? 1.0 : 0.0);
+          }
+          p.A[r * p.lda + k + c] = a;
+        }
+        __syncthreads();
+      }
+      QR_PHASE(4);
+    } else {
+      // ---- fallback: column-by-column Householder (needs resident rows)
+      ++nfallback;
+      if (!resident) {  // not supported: report loudly, leave the panel as is
+        if (tid == 0 && p.error) atomicExch(p.error, 1);
+        continue;
+      }
+      for (int e = tid; e < int(lmax(0L, r1 - ra)) * QR_NB; e += QR_THREADS) {
+        const int rr = e >> 5, c = e & 31;
+        s.Ps[rr * QR_PLD + c] = (c < jb) ? p.A[(ra + rr) * p.lda + k + c] : 0.0;
       }
       __syncthreads();
-    }
-
-    // write the factored panel back; CTA 0 keeps T for the Q formation
-    for (long e = tid; e < (r1 - ra) * jb; e += QR_THREADS) {
-      const long r = ra + e / jb;
-      const int c = int(e % jb);
-      p.A[r * p.lda + k + c] = s.Ps[(r - r0) * PLD + c];
+      qr_panel_householder(p, s, Ts, k, jb, ra, r1, gen);
+      for (int e = tid; e < int(lmax(0L, r1 - ra)) * QR_NB; e += QR_THREADS) {
+        const int rr = e >> 5, c = e & 31;
+        const long r = ra + rr;
+        double v = s.Ps[rr * QR_PLD + c];
+        if (c < jb) p.A[r * p.lda + k + c] = v;
+        if (c >= jb || r < k + c) v = 0.0;
+        else if (r == k + c) v = 1.0;
+        s.Ps[rr * QR_PLD + c] = v;  // V form for the trailing update
+      }
+      __syncthreads();
+      QR_PHASE(5);
     }
     if (blockIdx.x == 0)
-      for (int e = tid; e < nb * nb; e += QR_THREADS) p.tall[pidx * nb * nb + e] = s.Ts[e];
+      for (int e = tid; e < 1024; e += QR_THREADS) p.tall[pidx * 1024 + e] = Ts[(e >> 5) * QR_SLD + (e & 31)];
 
     const long ntr = n - k - jb;
     if (ntr > 0) {
-      // V form: unit diagonal, zeros above
-      for (long e = tid; e < (r1 - ra) * jb; e += QR_THREADS) {
-        const long r = ra + e / jb;
-        const int c = int(e % jb);
-        if (r < k + c) s.Ps[(r - r0) * PLD + c] = 0.0;
-        else if (r == k + c) s.Ps[(r - r0) * PLD + c] = 1.0;
+      // W partial over all active rows (V chunk in Ps)
+      bool first = true;
+      for (long cs = ra; cs < r1; cs += rch) {
+        const long ce = lmin(r1, cs + rch);
+        if (!resident) {
+          __syncthreads();
+          qr_load_chunk_vform(p, s, cs, ce, k, jb);
+          __syncthreads();
+        }
+        qr_wpartial_chunk(p, s, cs, ce, k + jb, ntr, first);
+        first = false;
       }
-      __syncthreads();
-      qr_wpartial(p, s, nb, r0, ra, r1, k + jb, ntr);
+      if (first) {  // no active rows: publish zeros
+        double* wdst = p.wpart + size_t(blockIdx.x) * QR_NB * qr_ldw(n);
+        for (long e = tid; e < QR_NB * ntr; e += QR_THREADS) __stcg(wdst + (e / ntr) * qr_ldw(n) + e % ntr, 0.0);
+      }
       grid_barrier(p.counter, gen);
-      qr_reduce_slice(p, s, nb, ntr, /*trans_t=*/true);
+      QR_PHASE(6);
+      qr_reduce_slice(p, s, Ts, ntr, /*trans_t=*/true);
       grid_barrier(p.counter, gen);
-      qr_apply_update(p, s, nb, r0, ra, r1, k + jb, ntr);
+      QR_PHASE(7);
+      for (long cs = ra; cs < r1; cs += rch) {
+        const long ce = lmin(r1, cs + rch);
+        if (!resident) {
+          __syncthreads();
+          qr_load_chunk_vform(p, s, cs, ce, k, jb);
+          __syncthreads();
+        }
+        qr_update_chunk(p, s, cs, ce, k + jb, ntr);
+      }
+      QR_PHASE(8);
     }
     __syncthreads();
   }
+  if (blockIdx.x == 0 && tid == 0 && p.fallbacks) *p.fallbacks = nfallback;
 
   // ===================== R extraction + rank test =====================
   if (blockIdx.x == 0 && tid == 0 && p.rank_flag) {
@@ -364,64 +1007,79 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
     const long i = r0 + e / n, j = e % n;
     if (j > i) p.A[i * p.lda + j] = 0.0;
   }
-  // every CTA's factored panels (V1 blocks, T factors) are published before
+  // every CTA's factored panels (V₁ blocks, T factors) are published before
   // any CTA starts reading them
   grid_barrier(p.counter, gen);
+  QR_PHASE(9);
 
   // ===================== Q formation (dorgqr, backward) =====================
-  const long npan = ceil_div(n, nb);
+  const long npan = ceil_div(n, QR_NB);
   for (long pidx = npan - 1; pidx >= 0; --pidx) {
-    const long k = pidx * nb;
-    const int jb = int(lmin(nb, n - k));
+    const long k = pidx * QR_NB;
+    const int jb = int(lmin(QR_NB, n - k));
     const long ra = lmax(r0, k);
-    // V_p (own rows) and V1 (pivot block, needed by every CTA)
-    for (long e = tid; e < (r1 - ra) * jb; e += QR_THREADS) {
-      const long r = ra + e / jb;
-      const int c = int(e % jb);
-      double v;
-      if (r < k + c) v = 0.0;
-      else if (r == k + c) v = 1.0;
-      else v = p.A[r * p.lda + k + c];
-      s.Ps[(r - r0) * PLD + c] = v;
+    // V₁ (pivot block, needed by every CTA) and T
+    for (int e = tid; e < 1024; e += QR_THREADS) {
+      const int a = e >> 5, c = e & 31;
+      double v = (a == c && a < jb) ? 1.0 : 0.0;
+      if (a > c && a < jb) v = __ldcg(p.A + (k + a) * p.lda + k + c);
+      LU[a * QR_SLD + c] = v;
+      Ts[a * QR_SLD + c] = __ldcg(p.tall + pidx * 1024 + e);
     }
-    for (int e = tid; e < jb * jb; e += QR_THREADS) {
-      const int a = e / jb, c = e % jb;
-      double v = (a == c) ? 1.0 : 0.0;
-      if (a > c) v = __ldcg(p.A + (k + a) * p.lda + k + c);
-      s.V1[a * nb + c] = v;
-    }
-    // the last panel's T is still resident from the factorization
-    if (pidx < npan - 1)
-      for (int e = tid; e < nb * nb; e += QR_THREADS) s.Ts[e] = __ldcg(p.tall + pidx * nb * nb + e);
     __syncthreads();
     const long ntr = n - k - jb;
     if (ntr > 0) {
-      qr_wpartial(p, s, nb, r0, ra, r1, k + jb, ntr);
+      bool first = true;
+      for (long cs = ra; cs < r1; cs += rch) {
+        const long ce = lmin(r1, cs + rch);
+        __syncthreads();
+        qr_load_chunk_vform(p, s, cs, ce, k, jb);
+        __syncthreads();
+        qr_wpartial_chunk(p, s, cs, ce, k + jb, ntr, first);
+        first = false;
+      }
+      if (first) {
+        double* wdst = p.wpart + size_t(blockIdx.x) * QR_NB * qr_ldw(n);
+        for (long e = tid; e < QR_NB * ntr; e += QR_THREADS) __stcg(wdst + (e / ntr) * qr_ldw(n) + e % ntr, 0.0);
+      }
       grid_barrier(p.counter, gen);
-      qr_reduce_slice(p, s, nb, ntr, /*trans_t=*/false);
+      qr_reduce_slice(p, s, Ts, ntr, /*trans_t=*/false);
       grid_barrier(p.counter, gen);
-      qr_apply_update(p, s, nb, r0, ra, r1, k + jb, ntr);
+      QR_PHASE(10);
+      for (long cs = ra; cs < r1; cs += rch) {
+        const long ce = lmin(r1, cs + rch);
+        if (!resident) {
+          __syncthreads();
+          qr_load_chunk_vform(p, s, cs, ce, k, jb);
+          __syncthreads();
+        }
+        qr_update_chunk(p, s, cs, ce, k + jb, ntr);
+      }
     } else {
-      grid_barrier(p.counter, gen);  // every CTA has read V1 before it is overwritten
+      grid_barrier(p.counter, gen);  // every CTA has read V₁ before it is overwritten
     }
-    // M1 = T · V1ᵀ  (jb × jb)
-    for (int e = tid; e < jb * jb; e += QR_THREADS) {
-      const int i = e / jb, c = e % jb;
-      double acc = 0.0;
-      for (int l = i; l < jb; ++l) acc = fma(s.Ts[i * nb + l], s.V1[c * nb + l], acc);
-      s.M1[i * nb + c] = acc;
+    // M1 = T·V₁ᵀ; panel columns Q[r][k+c] = δ(r, k+c) − Σ_i V[r][i]·M1[i][c]
+    sm_mm<false, true>(Lt, Ts, LU);
+    for (long cs = ra; cs < r1; cs += rch) {
+      const long ce = lmin(r1, cs + rch);
+      if (!resident || ntr <= 0) {
+        __syncthreads();
+        qr_load_chunk_vform(p, s, cs, ce, k, jb);
+        __syncthreads();
+      }
+      for (int e = tid; e < int(ce - cs) * QR_NB; e += QR_THREADS) {
+        const int rr = e >> 5, c = e & 31;
+        if (c >= jb) continue;
+        const long r = cs + rr;
+        const double* vrow = s.Ps + rr * QR_PLD;
+        double acc = (r == k + c) ? 1.0 : 0.0;
+#pragma unroll 8
+        for (int i = 0; i < QR_NB; ++i) acc = fma(-vrow[i], Lt[i * QR_SLD + c], acc);
+        p.A[r * p.lda + k + c] = acc;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    // panel columns: Q[r][k+c] = δ(r, k+c) − Σ_i V[r][i]·M1[i][c]
-    for (long e = tid; e < (r1 - ra) * jb; e += QR_THREADS) {
-      const long r = ra + e / jb;
-      const int c = int(e % jb);
-      const double* vrow = s.Ps + (r - r0) * PLD;
-      double acc = (r == k + c) ? 1.0 : 0.0;
-      for (int i = 0; i < jb; ++i) acc = fma(-vrow[i], s.M1[i * nb + c], acc);
-      p.A[r * p.lda + k + c] = acc;
-    }
-    __syncthreads();
+    QR_PHASE(11);
   }
   // sign fix: Q[:, c] *= sign(R_cc)
   for (long e = tid; e < (r1 - r0) * n; e += QR_THREADS) {

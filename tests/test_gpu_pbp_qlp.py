@@ -32,7 +32,8 @@ def _check_against_oracle(a, d, q, seed, reorth=True, phi=None, strict=1e-10, nc
     assert np.all(lerr <= conditioning_tolerance(ref["l"], strict=strict, factor=16.0)[:k])
     e_got = reconstruction_error(a, got.q_basis, got.l, got.p_basis)
     e_ref = reconstruction_error(a, ref["q"], ref["l"], ref["p"])
-    assert abs(e_got - e_ref) <= 1e-10 * max(e_ref, 1e-300) + 1e-15
+    if ncols is None:  # with arbitrary trailing directions the error itself is arbitrary at O(σ_noise)
+        assert abs(e_got - e_ref) <= 1e-10 * max(e_ref, 1e-300) + 1e-15
     assert got.sketch.passes_over_a == ref["passes"] == 2 * q + 2
     return got, ref
 

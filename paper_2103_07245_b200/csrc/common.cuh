@@ -51,6 +51,17 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   return v;
 }
 
+// Reciprocal for dependency chains: MUFU approximation + two Newton steps
+// (~1 ulp; ~70 cycles instead of ~250 for an IEEE division on sm_100a).
+__device__ __forceinline__ double fast_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
 // True when the IEEE-754 binary64 exponent field is all ones (Inf or NaN).
 __device__ __forceinline__ bool nonfinite_bits(double x) {
   return ((__double_as_longlong(x) >> 52) & 0x7ff) == 0x7ff;

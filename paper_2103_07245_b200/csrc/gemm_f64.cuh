@@ -6,14 +6,20 @@
 //                     (D = A·X, reference `_PassCounter.apply`, algorithms.py:178-180)
 //
 // B is K×N row-major in both cases.  All operands are FP64 and the products
-// run on the sm_100a FP64 tensor instruction DMMA.8x8x4.  Tiles are staged by
-// cp.async into a STAGES-deep shared-memory ring.  The grid is persistent
-// (one CTA per SM) and walks a deterministic stream-K schedule: the linearised
-// (tile, k-block) iteration space is cut into `grid` equal ranges, a tile whose
-// k-range is split across CTAs is finished by the CTA that owns its k=0 block,
-// which adds the other CTAs' partial tiles in increasing k order.  The
-// reduction order depends only on (M, N, K, grid), so results are bitwise
+// run on the sm_100a FP64 tensor instruction DMMA.8x8x4 (tcgen05 has no f64
+// kind).  Tiles are staged by cp.async into a STAGES-deep shared-memory ring
+// (BK = 32 so one barrier covers 8 MMA k-steps); every thread's cp.async
+// sources are a single pointer advanced by a constant per k-block, so the
+// mainloop carries no address arithmetic.  Fragments for k-step s+1 are
+// loaded while the MMAs of k-step s issue.  The grid is persistent (one CTA
+// per SM) and walks a deterministic stream-K schedule: the linearised
+// (tile, k-block) iteration space is cut into `grid` equal ranges; a tile
+// whose k-range is split across CTAs is finished by the CTA that owns its
+// k=0 block, which adds the other CTAs' partial tiles in increasing k order.
+// The reduction order depends only on (M, N, K, grid), so results are bitwise
 // reproducible run to run on the same GPU model (test_algorithms.py:53-60).
+// CHECK additionally ORs an Inf/NaN flag over every element of A (the
+// `check_matrix` isfinite scan, validation.py:47), fused into the first pass.
 #pragma once
 #include "common.cuh"
 
@@ -32,7 +38,7 @@ struct GemmArgs {
   long total_iters;
   double* partials;  // grid × (BM·BN) doubles
   int* flags;        // grid ints, zeroed before the launch
-  int* nonfinite;    // optional: OR-flag set if any element of A is Inf/NaN
+  int* nonfinite;    // CHECK only: OR-flag set if any element of A is Inf/NaN
 };
 
 template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES>
@@ -51,18 +57,28 @@ struct GemmCfg {
   static constexpr int SB_ELEMS = BK * SB_LD;
   static constexpr int STAGE_ELEMS = SA_ELEMS + SB_ELEMS;
   static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
-  static constexpr int FRAGS = MT * NT * 2;
+  // cp.async chunk geometry (16-byte chunks = 2 doubles)
+  static constexpr int A_ROWW = TRANS_A ? BM / 2 : BK / 2;  // chunks per staged row of A
+  static constexpr int A_CHUNKS = SA_ROWS * A_ROWW;
+  static constexpr int A_PER_THREAD = A_CHUNKS / THREADS;
+  static constexpr int A_ROW_STEP = THREADS / A_ROWW;        // staged rows between a thread's chunks
+  static constexpr int B_ROWW = BN / 2;
+  static constexpr int B_PER_THREAD = BK * B_ROWW / THREADS;
+  static constexpr int B_ROW_STEP = THREADS / B_ROWW;
   static_assert(BM % WM == 0 && BN % WN == 0 && WM % 8 == 0 && WN % 8 == 0, "tile shape");
   static_assert(BK % 4 == 0, "BK multiple of 4");
   static_assert(SA_LD % 16 == 4 && SB_LD % 16 == 4, "bank-conflict-free strides");
+  static_assert(A_CHUNKS % THREADS == 0 && THREADS % A_ROWW == 0, "A loader geometry");
+  static_assert((BK * B_ROWW) % THREADS == 0 && THREADS % B_ROWW == 0, "B loader geometry");
 };
 
-template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES>
+template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES, bool CHECK>
 __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::THREADS, 1)
     gemm_f64_streamk(GemmArgs p) {
   using Cfg = GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>;
   constexpr int THREADS = Cfg::THREADS;
   constexpr int MT = Cfg::MT, NT = Cfg::NT;
+  constexpr int KSTEPS = BK / 4;
   extern __shared__ __align__(128) double smem[];
 
   const int tid = threadIdx.x;
@@ -71,6 +87,14 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
   const int wm0 = (warp / Cfg::WARPS_N) * WM;
   const int wn0 = (warp % Cfg::WARPS_N) * WN;
   const int G = gridDim.x;
+
+  // per-thread loader geometry (first chunk; the others are +ROW_STEP rows)
+  const int a_row = tid / Cfg::A_ROWW, a_col = (tid % Cfg::A_ROWW) * 2;
+  const int b_row = tid / Cfg::B_ROWW, b_col = (tid % Cfg::B_ROWW) * 2;
+  const long a_kstep = TRANS_A ? long(BK) * p.lda : long(BK);  // pointer advance per k-block
+  const long b_kstep = long(BK) * p.ldb;
+  const long a_rstep = long(Cfg::A_ROW_STEP) * p.lda;
+  const long b_rstep = long(Cfg::B_ROW_STEP) * p.ldb;
 
   long it = long(blockIdx.x) * p.total_iters / G;
   const long it_end = long(blockIdx.x + 1) * p.total_iters / G;
@@ -82,7 +106,23 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
     const int ke = int(lmin(p.k_iters, kb + (it_end - it)));
     const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
     const long m0 = long(tm) * BM, n0 = long(tn) * BN;
-    const bool check = (p.nonfinite != nullptr) && (tn == 0);
+    const bool check = CHECK && (tn == 0);
+
+    // loader state for this tile: one source pointer per operand, byte
+    // counts for the M/N edge (K edge checked only on the last k-block)
+    const double* a_src;
+    int a_bytes;
+    if (TRANS_A) {
+      const long gm = m0 + a_col;
+      a_bytes = gm < p.M ? int(lmin(2, p.M - gm)) * 8 : 0;
+      a_src = p.A + (long(kb) * BK + a_row) * p.lda + (a_bytes ? gm : 0);
+    } else {
+      a_bytes = 16;
+      a_src = p.A + (m0 + a_row) * p.lda + long(kb) * BK + a_col;
+    }
+    const long gn = n0 + b_col;
+    const int b_bytes = gn < p.N ? int(lmin(2, p.N - gn)) * 8 : 0;
+    const double* b_src = p.B + (long(kb) * BK + b_row) * p.ldb + (b_bytes ? gn : 0);
 
     double acc[MT][NT][2];
 #pragma unroll
@@ -90,66 +130,53 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    // ---- stage loader --------------------------------------------------
     auto load_stage = [&](int stage, int kblk) {
       double* sA = smem + stage * Cfg::STAGE_ELEMS;
       double* sB = sA + Cfg::SA_ELEMS;
       const long k0 = long(kblk) * BK;
-      if (TRANS_A) {
-        // sA[kk][m]: BK rows of A (global row k0+kk), columns m0..m0+BM
-        constexpr int CH = BK * (BM / 2);
-        for (int c = tid; c < CH; c += THREADS) {
-          const int kk = c / (BM / 2), mc = (c % (BM / 2)) * 2;
-          const long gk = k0 + kk, gm = m0 + mc;
-          int bytes = 0;
-          const double* src = p.A;
-          if (gk < p.K && gm < p.M) {
-            bytes = int(lmin(2, p.M - gm)) * 8;
-            src = p.A + gk * p.lda + gm;
-          }
-          cp_async16(sA + kk * Cfg::SA_LD + mc, src, bytes);
+      const bool kfull = k0 + BK <= p.K;
+#pragma unroll
+      for (int i = 0; i < Cfg::A_PER_THREAD; ++i) {
+        const int r = a_row + i * Cfg::A_ROW_STEP;  // staged row
+        int bytes;
+        if (TRANS_A) {
+          bytes = (kfull || k0 + r < p.K) ? a_bytes : 0;
+        } else {
+          const long gk = k0 + a_col;
+          bytes = (m0 + r < p.M) ? (kfull ? 16 : (gk < p.K ? int(lmin(2, p.K - gk)) * 8 : 0)) : 0;
         }
-      } else {
-        // sA[m][kk]: BM rows of A (global row m0+i), columns k0..k0+BK
-        constexpr int CH = BM * (BK / 2);
-        for (int c = tid; c < CH; c += THREADS) {
-          const int i = c / (BK / 2), kc = (c % (BK / 2)) * 2;
-          const long gm = m0 + i, gk = k0 + kc;
-          int bytes = 0;
-          const double* src = p.A;
-          if (gm < p.M && gk < p.K) {
-            bytes = int(lmin(2, p.K - gk)) * 8;
-            src = p.A + gm * p.lda + gk;
-          }
-          cp_async16(sA + i * Cfg::SA_LD + kc, src, bytes);
-        }
+        cp_async16(sA + r * Cfg::SA_LD + a_col, bytes ? a_src + i * a_rstep : p.A, bytes);
       }
-      {
-        constexpr int CH = BK * (BN / 2);
-        for (int c = tid; c < CH; c += THREADS) {
-          const int kk = c / (BN / 2), nc = (c % (BN / 2)) * 2;
-          const long gk = k0 + kk, gn = n0 + nc;
-          int bytes = 0;
-          const double* src = p.B;
-          if (gk < p.K && gn < p.N) {
-            bytes = int(lmin(2, p.N - gn)) * 8;
-            src = p.B + gk * p.ldb + gn;
-          }
-          cp_async16(sB + kk * Cfg::SB_LD + nc, src, bytes);
-        }
+#pragma unroll
+      for (int i = 0; i < Cfg::B_PER_THREAD; ++i) {
+        const int r = b_row + i * Cfg::B_ROW_STEP;
+        const int bytes = (kfull || k0 + r < p.K) ? b_bytes : 0;
+        cp_async16(sB + r * Cfg::SB_LD + b_col, bytes ? b_src + i * b_rstep : p.B, bytes);
       }
+      a_src += a_kstep;
+      b_src += b_kstep;
     };
     // Non-finite scan of the A chunks this thread staged (own cp.async data is
     // visible to the issuing thread after wait_group).
     auto scan_stage = [&](int stage) {
       const double* sA = smem + stage * Cfg::STAGE_ELEMS;
-      constexpr int CH = TRANS_A ? BK * (BM / 2) : BM * (BK / 2);
-      constexpr int ROWW = TRANS_A ? BM / 2 : BK / 2;
-      for (int c = tid; c < CH; c += THREADS) {
-        const int r = c / ROWW, cc = (c % ROWW) * 2;
-        const double2 v = *reinterpret_cast<const double2*>(sA + r * Cfg::SA_LD + cc);
+#pragma unroll
+      for (int i = 0; i < Cfg::A_PER_THREAD; ++i) {
+        const int r = a_row + i * Cfg::A_ROW_STEP;
+        const double2 v = *reinterpret_cast<const double2*>(sA + r * Cfg::SA_LD + a_col);
         saw_nonfinite |= nonfinite_bits(v.x) | nonfinite_bits(v.y);
       }
+    };
+    auto load_frags = [&](const double* sA, const double* sB, int kk, double (&a)[MT], double (&b)[NT]) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        if (TRANS_A)
+          a[mt] = sA[(kk * 4 + t) * Cfg::SA_LD + wm0 + mt * 8 + g];
+        else
+          a[mt] = sA[(wm0 + mt * 8 + g) * Cfg::SA_LD + kk * 4 + t];
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) b[nt] = sB[(kk * 4 + t) * Cfg::SB_LD + wn0 + nt * 8 + g];
     };
 
     // ---- prologue ------------------------------------------------------
@@ -165,7 +192,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
       cp_async_wait<STAGES - 2>();
       __syncthreads();
       const int stage = i % STAGES;
-      if (check) scan_stage(stage);
+      if (CHECK && check) scan_stage(stage);
       {
         const int nxt = i + STAGES - 1;
         if (nxt < nk) load_stage(nxt % STAGES, kb + nxt);
@@ -173,22 +200,16 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
       }
       const double* sA = smem + stage * Cfg::STAGE_ELEMS;
       const double* sB = sA + Cfg::SA_ELEMS;
+      double fa[2][MT], fb[2][NT];
+      load_frags(sA, sB, 0, fa[0], fb[0]);
 #pragma unroll
-      for (int kk = 0; kk < BK / 4; ++kk) {
-        double a[MT], b[NT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          if (TRANS_A)
-            a[mt] = sA[(kk * 4 + t) * Cfg::SA_LD + wm0 + mt * 8 + g];
-          else
-            a[mt] = sA[(wm0 + mt * 8 + g) * Cfg::SA_LD + kk * 4 + t];
-        }
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) b[nt] = sB[(kk * 4 + t) * Cfg::SB_LD + wn0 + nt * 8 + g];
+      for (int kk = 0; kk < KSTEPS; ++kk) {
+        const int cur = kk & 1;
+        if (kk + 1 < KSTEPS) load_frags(sA, sB, kk + 1, fa[cur ^ 1], fb[cur ^ 1]);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], fa[cur][mt], fb[cur][nt]);
       }
     }
     cp_async_wait<0>();
@@ -256,7 +277,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
     }
     it += nk;
   }
-  if (saw_nonfinite) atomicOr(p.nonfinite, 1);
+  if (CHECK && saw_nonfinite) atomicOr(p.nonfinite, 1);
 }
 
 }  // namespace pbq

@@ -75,12 +75,15 @@ struct Carve {
 
 // ---------------------------------------------------------------- GEMM ----
 // Two tile shapes: d ≤ 64 uses 128×64 (warp 32×32), larger d 128×128 (warp 64×32).
-constexpr int G_BM = 128, G_BK = 16, G_STAGES = 4;
+constexpr int G_BM = 128, G_BK = 32, G_STAGES = 3;
 
 template <bool T, int BN, int WM, int WN>
 struct GemmKernel {
   using Cfg = GemmCfg<T, G_BM, BN, G_BK, WM, WN, G_STAGES>;
-  static void* fn() { return reinterpret_cast<void*>(&gemm_f64_streamk<T, G_BM, BN, G_BK, WM, WN, G_STAGES>); }
+  static void* fn(bool check) {
+    return check ? reinterpret_cast<void*>(&gemm_f64_streamk<T, G_BM, BN, G_BK, WM, WN, G_STAGES, true>)
+                 : reinterpret_cast<void*>(&gemm_f64_streamk<T, G_BM, BN, G_BK, WM, WN, G_STAGES, false>);
+  }
 };
 
 struct GemmPlan {
@@ -130,10 +133,10 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   int threads;
   if (pl.bn == 64) {
     using K_ = GemmKernel<TRANS, 64, 32, 32>;
-    fn = K_::fn(); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
+    fn = K_::fn(nonfinite != nullptr); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
   } else {
     using K_ = GemmKernel<TRANS, 128, 64, 32>;
-    fn = K_::fn(); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
+    fn = K_::fn(nonfinite != nullptr); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
   }
   PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   void* args[] = {&a};
@@ -267,11 +270,12 @@ int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t 
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gaussian: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   a.error = error_flag ? error_flag : own_err;
   if (!error_flag) PBQ_CUDA(ctx, cudaMemsetAsync(own_err, 0, sizeof(int), st));
-  sketch_k1<<<dim3(unsigned(pl.n_chunks)), PBQ_SK_THREADS, 0, st>>>(a);
+  const unsigned sk_grid = unsigned(ceil_div(pl.n_chunks, PBQ_SK_WARPS));
+  sketch_k1<<<dim3(sk_grid), PBQ_SK_THREADS, 0, st>>>(a);
   PBQ_CUDA(ctx, cudaGetLastError());
   sketch_k2<<<1, 1024, 0, st>>>(a);
   PBQ_CUDA(ctx, cudaGetLastError());
-  sketch_k3<<<dim3(unsigned(pl.n_chunks)), PBQ_SK_THREADS, 0, st>>>(a);
+  sketch_k3<<<dim3(sk_grid), PBQ_SK_THREADS, 0, st>>>(a);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 3;
   return PBQ_OK;

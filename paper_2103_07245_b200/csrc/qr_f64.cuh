@@ -34,7 +34,11 @@
 
 namespace pbq {
 
-constexpr int QR_THREADS = 256;
+constexpr int QR_THREADS = 512;
+constexpr int QR_TPR = QR_THREADS / 32;  // threads per row of a 32×32 tile
+constexpr int QR_EPT = 32 / QR_TPR;      // entries per thread of a 32×32 tile
+constexpr int QR_RG = QR_THREADS / 64;   // row groups of the Gram accumulation
+constexpr int QR_IPT = 32 / (QR_THREADS / 32);  // W-partial i-rows per thread (32 columns per warp)
 constexpr int QR_NB = 32;                 // panel width
 constexpr int QR_SLD = QR_NB + 1;         // leading dimension of 32×32 smem matrices
 constexpr int QR_PLD = QR_NB + 1;         // leading dimension of the panel rows
@@ -93,14 +97,14 @@ struct QrSmem {
   double* Ps;     // rch × 33: the CTA's rows of the panel (one chunk)
   double* mat;    // QR_NSMALL × 32 × 33 scratch matrices
   double* beta;   // n   (signed diag of R)
-  double* small;  // 256 reduction + 8 × 32 vectors
+  double* small;  // QR_THREADS reduction + 8 × 32 vectors
   double* stage;  // 2 × 4096 (double-buffered tiles)
   double* wsl;    // 32 × ⌈n/G⌉
   __device__ double* M(int k) const { return mat + k * qr_pad4(QR_NB * QR_SLD); }
 };
 
 __host__ __device__ inline size_t qr_smem_doubles(long rch, long n, int grid) {
-  return qr_pad4(size_t(rch) * QR_PLD) + QR_NSMALL * qr_pad4(size_t(QR_NB) * QR_SLD) + qr_pad4(n) + 256 +
+  return qr_pad4(size_t(rch) * QR_PLD) + QR_NSMALL * qr_pad4(size_t(QR_NB) * QR_SLD) + qr_pad4(n) + QR_THREADS +
          8 * 32 + 2 * QR_TILE_DOUBLES + qr_pad4(size_t(QR_NB) * ceil_div(n, grid)) + 8;
 }
 
@@ -149,16 +153,18 @@ __device__ __forceinline__ void qr_reduce_entries(int E, int G, size_t stride, A
 // C = op(A)·op(B) (opX = transpose when TX); C must not alias A or B.
 template <bool TA, bool TB>
 __device__ __forceinline__ void sm_mm(double* C, const double* A, const double* B) {
-  const int i = threadIdx.x >> 3, c0 = (threadIdx.x & 7) << 2;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int i = threadIdx.x / QR_TPR, c0 = (threadIdx.x % QR_TPR) * QR_EPT;
+  double acc[QR_EPT];
+#pragma unroll
+  for (int u = 0; u < QR_EPT; ++u) acc[u] = 0.0;
 #pragma unroll
   for (int q = 0; q < QR_NB; ++q) {
     const double a = TA ? A[q * QR_SLD + i] : A[i * QR_SLD + q];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc[u] = fma(a, TB ? B[(c0 + u) * QR_SLD + q] : B[q * QR_SLD + c0 + u], acc[u]);
+    for (int u = 0; u < QR_EPT; ++u) acc[u] = fma(a, TB ? B[(c0 + u) * QR_SLD + q] : B[q * QR_SLD + c0 + u], acc[u]);
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) C[i * QR_SLD + c0 + u] = acc[u];
+  for (int u = 0; u < QR_EPT; ++u) C[i * QR_SLD + c0 + u] = acc[u];
   __syncthreads();
 }
 
@@ -169,12 +175,12 @@ __device__ __forceinline__ void sm_mm(double* C, const double* A, const double* 
 template <bool TRANS, bool UNIT>
 __device__ __forceinline__ void sm_tri_inv_upper(double* X, const double* U, double* Z) {
   const int tid = threadIdx.x;
-  const int i = tid >> 3, c0 = (tid & 7) << 2;
+  const int i = tid / QR_TPR, c0 = (tid % QR_TPR) * QR_EPT;
   auto u_at = [&](int r, int c) { return TRANS ? U[c * QR_SLD + r] : U[r * QR_SLD + c]; };
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
+  for (int v = 0; v < QR_EPT; ++v) {
     const int c = c0 + v;
-    X[i * QR_SLD + c] = (i == c) ? (UNIT ? 1.0 : 1.0 / u_at(i, i)) : 0.0;
+    X[i * QR_SLD + c] = (i == c) ? (UNIT ? 1.0 : fast_rcp(u_at(i, i))) : 0.0;
   }
   __syncthreads();
 #pragma unroll
@@ -208,37 +214,37 @@ __device__ __forceinline__ void sm_tri_inv_upper(double* X, const double* U, dou
 // multipliers from the pivot row), else LU (multipliers from the own row,
 // stored in place of the eliminated entry).
 template <bool SYM>
-__device__ __forceinline__ void sm_eliminate(double (&v)[4], double* row_sm /*64*/, double* inv_sm /*2*/) {
+__device__ __forceinline__ void sm_eliminate(double (&v)[QR_EPT], double* row_sm /*64*/, double* inv_sm /*2*/) {
   const int tid = threadIdx.x;
-  const int i = tid >> 3, c0 = (tid & 7) << 2;
+  const int i = tid / QR_TPR, c0 = (tid % QR_TPR) * QR_EPT;
 #pragma unroll 1
   for (int j = 0; j < QR_NB; ++j) {
     const int b = j & 1;
     if (i == j) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) row_sm[b * 32 + c0 + u] = v[u];
+      for (int u = 0; u < QR_EPT; ++u) row_sm[b * 32 + c0 + u] = v[u];
       const int jj = j - c0;
-      if (jj >= 0 && jj < 4) {
+      if (jj >= 0 && jj < QR_EPT) {
         double pv = v[0];
-        if (jj == 1) pv = v[1];
-        if (jj == 2) pv = v[2];
-        if (jj == 3) pv = v[3];
-        inv_sm[b] = 1.0 / pv;
+#pragma unroll
+        for (int u = 1; u < QR_EPT; ++u)
+          if (jj == u) pv = v[u];
+        inv_sm[b] = fast_rcp(pv);
       }
     }
     double own = 0.0;
-    if (!SYM) {  // entry (i, j), held by lane (row base + j/4) of this warp
+    if (!SYM) {  // entry (i, j), held by lane (row base + j/EPT) of this warp
       double cand = v[0];
-      if ((j & 3) == 1) cand = v[1];
-      if ((j & 3) == 2) cand = v[2];
-      if ((j & 3) == 3) cand = v[3];
-      own = __shfl_sync(0xffffffffu, cand, ((tid & ~7) | (j >> 2)) & 31);
+#pragma unroll
+      for (int u = 1; u < QR_EPT; ++u)
+        if ((j % QR_EPT) == u) cand = v[u];
+      own = __shfl_sync(0xffffffffu, cand, ((tid & ~(QR_TPR - 1)) | (j / QR_EPT)) & 31);
     }
     __syncthreads();
     if (i > j) {
       const double f = (SYM ? row_sm[b * 32 + i] : own) * inv_sm[b];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < QR_EPT; ++u) {
         const int l = c0 + u;
         if (l > j) v[u] = fma(-f, row_sm[b * 32 + l], v[u]);
         if (!SYM && l == j) v[u] = f;
@@ -253,16 +259,16 @@ __device__ __forceinline__ void sm_eliminate(double (&v)[4], double* row_sm /*64
 __device__ double sm_chol(double* G, double* vec /*≥ 96*/) {
   __shared__ double s_ratio;
   const int tid = threadIdx.x;
-  const int i = tid >> 3, c0 = (tid & 7) << 2;
-  double v[4];
+  const int i = tid / QR_TPR, c0 = (tid % QR_TPR) * QR_EPT;
+  double v[QR_EPT];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) v[u] = G[i * QR_SLD + c0 + u];
+  for (int u = 0; u < QR_EPT; ++u) v[u] = G[i * QR_SLD + c0 + u];
   __syncthreads();
   sm_eliminate<true>(v, vec, vec + 64);
   __syncthreads();
   // pivots → diag(R); row i of R = (row i of the Schur complement)/R_ii
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < QR_EPT; ++u)
     if (c0 + u == i) vec[i] = v[u];
   __syncthreads();
   if (tid < 32) {
@@ -277,9 +283,9 @@ __device__ double sm_chol(double* G, double* vec /*≥ 96*/) {
     }
     if (tid == 0) s_ratio = ok ? mn / mx : -1.0;
   }
-  const double rd = sqrt(vec[i]), inv = 1.0 / rd;
+  const double rd = sqrt(vec[i]), inv = fast_rcp(rd);
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < QR_EPT; ++u) {
     const int l = c0 + u;
     G[i * QR_SLD + l] = (l > i) ? v[u] * inv : ((l == i) ? rd : 0.0);
   }
@@ -290,14 +296,14 @@ __device__ double sm_chol(double* G, double* vec /*≥ 96*/) {
 // Unpivoted LU of the 32×32 matrix M in place: strict lower = unit-lower
 // factor, upper = U.
 __device__ void sm_lu(double* M, double* vec) {
-  const int i = threadIdx.x >> 3, c0 = (threadIdx.x & 7) << 2;
-  double v[4];
+  const int i = threadIdx.x / QR_TPR, c0 = (threadIdx.x % QR_TPR) * QR_EPT;
+  double v[QR_EPT];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) v[u] = M[i * QR_SLD + c0 + u];
+  for (int u = 0; u < QR_EPT; ++u) v[u] = M[i * QR_SLD + c0 + u];
   __syncthreads();
   sm_eliminate<false>(v, vec, vec + 64);
 #pragma unroll
-  for (int u = 0; u < 4; ++u) M[i * QR_SLD + c0 + u] = v[u];
+  for (int u = 0; u < QR_EPT; ++u) M[i * QR_SLD + c0 + u] = v[u];
   __syncthreads();
 }
 
@@ -309,11 +315,11 @@ __device__ void sm_lu(double* M, double* vec) {
 __device__ double sm_chol_near_identity(double* Rout, const double* G, double* X) {
   __shared__ unsigned long long s_emax;
   const int tid = threadIdx.x;
-  const int i = tid >> 3, c0 = (tid & 7) << 2;
-  double e[4];
+  const int i = tid / QR_TPR, c0 = (tid % QR_TPR) * QR_EPT;
+  double e[QR_EPT];
   double emax = 0.0;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < QR_EPT; ++u) {
     e[u] = G[i * QR_SLD + c0 + u] - ((i == c0 + u) ? 1.0 : 0.0);
     emax = fmax(emax, fabs(e[u]));
   }
@@ -324,24 +330,26 @@ __device__ double sm_chol_near_identity(double* Rout, const double* G, double* X
   if ((tid & 31) == 0) atomicMax(&s_emax, (unsigned long long)__double_as_longlong(emax));
   auto split = [&](int l, double x) { return (l > i) ? x : ((l == i) ? 0.5 * x : 0.0); };
 #pragma unroll
-  for (int u = 0; u < 4; ++u) X[i * QR_SLD + c0 + u] = split(c0 + u, e[u]);
+  for (int u = 0; u < QR_EPT; ++u) X[i * QR_SLD + c0 + u] = split(c0 + u, e[u]);
   __syncthreads();
 #pragma unroll 1
   for (int it = 0; it < 3; ++it) {
-    double nx[4] = {e[0], e[1], e[2], e[3]};
+    double nx[QR_EPT];
+#pragma unroll
+    for (int u = 0; u < QR_EPT; ++u) nx[u] = e[u];
 #pragma unroll
     for (int q = 0; q < QR_NB; ++q) {
       const double xqi = (q <= i) ? X[q * QR_SLD + i] : 0.0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) nx[u] = fma(-xqi, X[q * QR_SLD + c0 + u], nx[u]);
+      for (int u = 0; u < QR_EPT; ++u) nx[u] = fma(-xqi, X[q * QR_SLD + c0 + u], nx[u]);
     }
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) X[i * QR_SLD + c0 + u] = split(c0 + u, nx[u]);
+    for (int u = 0; u < QR_EPT; ++u) X[i * QR_SLD + c0 + u] = split(c0 + u, nx[u]);
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < QR_EPT; ++u) {
     const int l = c0 + u;
     Rout[i * QR_SLD + l] = (l >= i) ? X[i * QR_SLD + l] + ((l == i) ? 1.0 : 0.0) : 0.0;
   }
@@ -393,7 +401,7 @@ __device__ __forceinline__ void qr_gram_accum(const QrSmem& s, int rows, double 
   const int tid = threadIdx.x;
   const int rg = tid >> 6, blk = tid & 63;
   const int ab = (blk >> 3) << 2, bb = (blk & 7) << 2;
-  for (int rr = rg; rr < rows; rr += 4) {
+  for (int rr = rg; rr < rows; rr += QR_RG) {
     const double* row = s.Ps + rr * QR_PLD;
     double pa[4], pb[4];
 #pragma unroll
@@ -418,8 +426,12 @@ __device__ __forceinline__ void qr_gram_publish(const QrSmem& s, double (&acc)[4
 #pragma unroll
     for (int b = 0; b < 4; ++b) s.stage[rg * 1024 + (ab + a) * 32 + bb + b] = acc[a][b];
   __syncthreads();
-  for (int e = tid; e < 1024; e += QR_THREADS)
-    __stcg(dst + e, ((s.stage[e] + s.stage[1024 + e]) + s.stage[2048 + e]) + s.stage[3072 + e]);
+  for (int e = tid; e < 1024; e += QR_THREADS) {
+    double v = s.stage[e];
+#pragma unroll
+    for (int g = 1; g < QR_RG; ++g) v += s.stage[g * 1024 + e];
+    __stcg(dst + e, v);
+  }
 }
 
 // Slice reduction of the Gram partials (1024 entries) into p.gfin.
@@ -438,7 +450,7 @@ __device__ void qr_gram_reduce(const QrArgs& p, double* red) {
 __device__ __forceinline__ void qr_rows_times(const QrSmem& s, int rows, const double* W) {
   const int tid = threadIdx.x;
   const int rb = (tid >> 3) << 2, cb = (tid & 7) << 2;
-  for (int b0 = 0; b0 < rows; b0 += 128) {
+  for (int b0 = 0; b0 < rows; b0 += QR_THREADS / 2) {
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -481,7 +493,7 @@ __device__ void qr_wpartial_chunk(const QrArgs& p, const QrSmem& s, long cs, lon
                                   bool first) {
   const int tid = threadIdx.x;
   constexpr int CB = QR_CW / 4;  // 32
-  const int ib = tid / CB, cb = tid % CB;
+  const int ib = tid / CB, cb = tid % CB;  // i rows ib·IPT .. +IPT
   const long ldw = qr_ldw(p.n);
   double* wdst = p.wpart + size_t(blockIdx.x) * QR_NB * ldw;
   const int nrows = int(ce - cs);
@@ -503,9 +515,9 @@ __device__ void qr_wpartial_chunk(const QrArgs& p, const QrSmem& s, long cs, lon
       }
       cp_async_commit();
     };
-    double acc[4][4];
+    double acc[QR_IPT][4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < QR_IPT; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
     if (nrc > 0) load(0, 0);
@@ -520,27 +532,27 @@ __device__ void qr_wpartial_chunk(const QrArgs& p, const QrSmem& s, long cs, lon
       const double* tile = s.stage + (t & 1) * QR_TILE_DOUBLES;
       const int rows = min(QR_NB, nrows - t * QR_NB);
       for (int rr = 0; rr < rows; ++rr) {
-        const double* vrow = s.Ps + (t * QR_NB + rr) * QR_PLD + ib * 4;
+        const double* vrow = s.Ps + (t * QR_NB + rr) * QR_PLD + ib * QR_IPT;
         const double* xrow = tile + rr * QR_CW + cb;
-        double v[4], x[4];
+        double v[QR_IPT], x[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) v[a] = vrow[a];
+        for (int a = 0; a < QR_IPT; ++a) v[a] = vrow[a];
 #pragma unroll
         for (int b = 0; b < 4; ++b) x[b] = xrow[b * CB];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < QR_IPT; ++a)
 #pragma unroll
           for (int b = 0; b < 4; ++b) acc[a][b] = fma(v[a], x[b], acc[a][b]);
       }
       __syncthreads();
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < QR_IPT; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const long c = c0 + cb + b * CB;
         if (c < ntr) {
-          double* w = wdst + size_t(ib * 4 + a) * ldw + c;
+          double* w = wdst + size_t(ib * QR_IPT + a) * ldw + c;
           __stcg(w, first ? acc[a][b] : acc[a][b] + __ldcg(w));
         }
       }
@@ -592,11 +604,11 @@ __device__ void qr_update_chunk(const QrArgs& p, const QrSmem& s, long cs, long 
     cp_async_wait<0>();
     __syncthreads();
     for (int rc = 0; rc < nrows; rc += QR_NB) {
-      double acc[4][4];
-      bool ok[4];
+      double acc[QR_IPT][4];
+      bool ok[QR_IPT];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int rr = rc + rb * 4 + a;
+      for (int a = 0; a < QR_IPT; ++a) {
+        const int rr = rc + rb * QR_IPT + a;
         ok[a] = rr < nrows;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -606,20 +618,20 @@ __device__ void qr_update_chunk(const QrArgs& p, const QrSmem& s, long cs, long 
       }
 #pragma unroll 4
       for (int i = 0; i < QR_NB; ++i) {
-        double y[4], v[4];
+        double y[4], v[QR_IPT];
 #pragma unroll
         for (int b = 0; b < 4; ++b) y[b] = s.stage[i * QR_CW + cb + b * CB];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) v[a] = ok[a] ? s.Ps[(rc + rb * 4 + a) * QR_PLD + i] : 0.0;
+        for (int a = 0; a < QR_IPT; ++a) v[a] = ok[a] ? s.Ps[(rc + rb * QR_IPT + a) * QR_PLD + i] : 0.0;
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < QR_IPT; ++a)
 #pragma unroll
           for (int b = 0; b < 4; ++b) acc[a][b] = fma(-v[a], y[b], acc[a][b]);
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
+      for (int a = 0; a < QR_IPT; ++a) {
         if (!ok[a]) continue;
-        const long r = cs + rc + rb * 4 + a;
+        const long r = cs + rc + rb * QR_IPT + a;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const long c = c0 + cb + b * CB;
@@ -639,8 +651,8 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
                                      long r1, unsigned int& gen) {
   const int tid = threadIdx.x;
   const int G = gridDim.x;
-  double* red = s.small;          // 256
-  double* svec = s.small + 256;   // 32
+  double* red = s.small;                 // QR_THREADS
+  double* svec = s.small + QR_THREADS;   // 32
   double* prow = svec + 32;       // 32
   double* wt = prow + 32;         // 32
   for (int e = tid; e < QR_NB * QR_SLD; e += QR_THREADS) Ts[e] = 0.0;
@@ -652,11 +664,12 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
     {
       const int c = tid & 31, grp = tid >> 5;
       double a0 = 0.0, a1 = 0.0;
+      constexpr int NG = QR_THREADS / 32;
       if (c < jb) {
         int rr = int(lmax(0L, piv + 1 - ra)) + grp;
-        for (; rr + 8 < nrows; rr += 16) {
+        for (; rr + NG < nrows; rr += 2 * NG) {
           const double* row0 = s.Ps + rr * QR_PLD;
-          const double* row1 = row0 + 8 * QR_PLD;
+          const double* row1 = row0 + NG * QR_PLD;
           a0 = fma(row0[jj], row0[c], a0);
           a1 = fma(row1[jj], row1[c], a1);
         }
@@ -671,7 +684,7 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
     if (tid < jb) {
       double acc = 0.0;
 #pragma unroll
-      for (int g2 = 0; g2 < 8; ++g2) acc += red[g2 * 32 + tid];
+      for (int g2 = 0; g2 < QR_THREADS / 32; ++g2) acc += red[g2 * 32 + tid];
       __stcg(p.part + (size_t(buf) * G + blockIdx.x) * 32 + tid, acc);
       if (piv >= ra && piv < r1) __stcg(p.pivrow + buf * 32 + tid, s.Ps[(piv - ra) * QR_PLD + tid]);
     }
@@ -692,8 +705,8 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
     } else {
       const double nrm = sqrt(fma(alpha, alpha, sigma));
       beta = signbit(alpha) ? nrm : -nrm;
-      tau = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
+      tau = (beta - alpha) * fast_rcp(beta);
+      scale = fast_rcp(alpha - beta);
     }
     if (tid < jb) wt[tid] = (tid > jj) ? tau * fma(scale, svec[tid], prow[tid]) : 0.0;
     if (tid < jj) {
@@ -739,7 +752,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
     s.Ps = q; q += qr_pad4(size_t(rch) * QR_PLD);
     s.mat = q; q += QR_NSMALL * qr_pad4(size_t(QR_NB) * QR_SLD);
     s.beta = q; q += qr_pad4(n);
-    s.small = q; q += 256 + 8 * 32;
+    s.small = q; q += QR_THREADS + 8 * 32;
     s.stage = q; q += 2 * QR_TILE_DOUBLES;
     s.wsl = q;
   }
@@ -756,8 +769,8 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
   double* Ui = s.M(9);    // U⁻¹
   double* Lt = s.M(10);   // V₁⁻ᵀ, later M1 = T·V₁ᵀ
   double* SR = s.M(11);   // S·R_p
-  double* vec = s.small + 256;         // 96: elimination rows (0..63) and pivots (64..65)
-  double* svec = s.small + 256 + 128;  // 32: S signs
+  double* vec = s.small + QR_THREADS;         // 96: elimination rows (0..63) and pivots (64..65)
+  double* svec = s.small + QR_THREADS + 128;  // 32: S signs
   unsigned int gen = 0;
   int nfallback = 0;
   unsigned long long t_phase = (p.phase_ns && blockIdx.x == 0 && tid == 0) ? qr_now() : 0;
@@ -858,11 +871,11 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
       sm_mm<false, false>(Wm, R1i, R2i);   // R_p⁻¹ = R₁⁻¹R₂⁻¹
       sm_mm<false, false>(Z, Pp, Wm);      // Q₁ = P_piv·R_p⁻¹
       {
-        const int i = tid >> 3, c0 = (tid & 7) << 2;
+        const int i = tid / QR_TPR, c0 = (tid % QR_TPR) * QR_EPT;
         if (tid < 32) svec[tid] = (Z[tid * QR_SLD + tid] >= 0.0) ? -1.0 : 1.0;  // S = −sign(diag Q₁)
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < QR_EPT; ++u) {
           const int l = c0 + u;
           LU[i * QR_SLD + l] = ((i == l) ? 1.0 : 0.0) - Z[i * QR_SLD + l] * svec[l];
         }
@@ -873,9 +886,9 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
       sm_lu(LU, vec);
       QR_PHASE(14);
       {
-        const int i = tid >> 3, c0 = (tid & 7) << 2;
+        const int i = tid / QR_TPR, c0 = (tid % QR_TPR) * QR_EPT;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < QR_EPT; ++u) {
           const int l = c0 + u;
           Z[i * QR_SLD + l] = (l >= i) ? LU[i * QR_SLD + l] : 0.0;            // U
           SR[i * QR_SLD + l] = (l >= i) ? svec[i] * Pp[i * QR_SLD + l] : 0.0;  // S·R_p
@@ -886,9 +899,9 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
       sm_tri_inv_upper<true, true>(Lt, LU, Wm);   // (V₁ᵀ)⁻¹ = V₁⁻ᵀ
       sm_mm<false, false>(Ts, Z, Lt);             // T = U·V₁⁻ᵀ
       {
-        const int i = tid >> 3, c0 = (tid & 7) << 2;
+        const int i = tid / QR_TPR, c0 = (tid % QR_TPR) * QR_EPT;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) Z[i * QR_SLD + c0 + u] = -R2i[i * QR_SLD + c0 + u] * svec[c0 + u];
+        for (int u = 0; u < QR_EPT; ++u) Z[i * QR_SLD + c0 + u] = -R2i[i * QR_SLD + c0 + u] * svec[c0 + u];
         __syncthreads();
       }
       sm_mm<false, false>(Wm, Z, Ui);             // W₃ = R₂⁻¹·(−S)·U⁻¹

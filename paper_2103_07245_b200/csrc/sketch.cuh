@@ -5,19 +5,20 @@
 // Stream: Philox4x64-10 (Salmon et al., SC'11) keyed by the 128-bit seed, counter
 // (c+1, 0, 0, 0) for block c, four u64 words per block in order — stream
 // position p is word p%4 of block p/4.  Each normal consumes ≥ 1 word (numpy's
-// ziggurat: ~1.023 words/normal on average), so the position at which normal i
+// ziggurat: ~1.022 words/normal on average), so the position at which normal i
 // starts depends on every earlier draw.  The GPU resolves that dependency in
-// three passes over fixed-size chunks of the stream:
-//   K1 (one CTA per chunk) finds the rare "special" positions (draws that are
-//      not accepted by the rectangle test), resolves where each special draw's
-//      normal ends, and walks the start chain for every possible entry offset
-//      e ∈ [0, PBQ_SK_E).  Chains from different entries merge within a few
-//      positions, so every chunk's exit position is entry-independent (checked;
-//      a violation sets the error flag).
+// three passes over fixed 1024-position chunks of the stream, one chunk per
+// warp (lane ℓ owns positions 32ℓ..32ℓ+31 as a 32-bit mask; no CTA barriers):
+//   K1 finds the rare "special" positions (draws the rectangle test rejects),
+//      resolves where each special draw's normal ends, and walks the start
+//      chain for every possible entry offset e ∈ [0, 32).  Chains from
+//      different entries merge within a few positions, so a chunk's exit
+//      position does not depend on its entry (checked; a violation sets the
+//      error flag).
 //   K2 (one CTA) turns exits into per-chunk entry offsets and exclusive-scans
 //      the per-chunk normal counts.
-//   K3 (one CTA per chunk) marks the chain's start positions, ranks them with a
-//      block scan and writes each normal to Φ[(i - first)/cols][(i - first)%cols].
+//   K3 marks the chain's start positions, ranks them with a warp scan, stages
+//      the values in shared memory and writes them coalesced to Φ.
 // Values equal numpy's bit for bit, except that the exponential-tail branch
 // (idx 0, ~2.6e-4 of draws) uses CUDA's log1p, which can differ from glibc's by
 // 1 ulp; see DESIGN.md §5.
@@ -27,10 +28,11 @@
 
 namespace pbq {
 
-constexpr int PBQ_SK_CHUNK = 2048;     // stream positions per chunk
-constexpr int PBQ_SK_THREADS = 256;
-constexpr int PBQ_SK_E = 32;           // entry offsets tracked per chunk
-constexpr int PBQ_SK_MAXSPECIAL = 256; // special draws per chunk (mean ≈ 15)
+constexpr int PBQ_SK_CHUNK = 1024;      // stream positions per chunk (one warp)
+constexpr int PBQ_SK_WARPS = 4;         // chunks per CTA (static smem ≤ 48 KB)
+constexpr int PBQ_SK_THREADS = 32 * PBQ_SK_WARPS;
+constexpr int PBQ_SK_E = 32;            // entry offsets tracked per chunk
+constexpr int PBQ_SK_MAXSPECIAL = 96;   // special draws per chunk (mean ≈ 7.5)
 
 __constant__ uint64_t c_zig_ki[256];
 __constant__ double c_zig_wi[256];
@@ -40,18 +42,12 @@ struct Philox4x64 {
   uint64_t x[4];
 };
 
-__device__ __forceinline__ void mulhilo64(uint64_t a, uint64_t b, uint64_t& hi, uint64_t& lo) {
-  lo = a * b;
-  hi = __umul64hi(a, b);
-}
-
 __device__ __forceinline__ Philox4x64 philox4x64_10(uint64_t ctr0, uint64_t k0, uint64_t k1) {
   uint64_t x0 = ctr0, x1 = 0, x2 = 0, x3 = 0;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    uint64_t hi0, lo0, hi1, lo1;
-    mulhilo64(0xD2E7470EE14C6C93ULL, x0, hi0, lo0);
-    mulhilo64(0xCA5A826395121157ULL, x2, hi1, lo1);
+    const uint64_t lo0 = 0xD2E7470EE14C6C93ULL * x0, hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, x0);
+    const uint64_t lo1 = 0xCA5A826395121157ULL * x2, hi1 = __umul64hi(0xCA5A826395121157ULL, x2);
     const uint64_t n0 = hi1 ^ x1 ^ k0, n2 = hi0 ^ x3 ^ k1;
     x0 = n0; x1 = lo1; x2 = n2; x3 = lo0;
     k0 += 0x9E3779B97F4A7C15ULL;
@@ -73,31 +69,47 @@ __device__ __forceinline__ double u64_to_unit(uint64_t v) {
   return double(v >> 11) * (1.0 / 9007199254740992.0);
 }
 
-// A draw at position p is "fast" when the rectangle test accepts it.
-__device__ __forceinline__ bool zig_fast(uint64_t r) {
-  const int idx = int(r & 0xff);
-  const uint64_t rabs = (r >> 9) & 0x000fffffffffffffULL;
-  return rabs < c_zig_ki[idx];
+// Layer tables staged in shared memory: lanes index different layers, which
+// would serialise 32-way through the constant cache.
+struct ZigTables {
+  uint64_t ki[256];
+  double wi[256];
+  double fi[256];
+};
+__device__ __forceinline__ void zig_stage(ZigTables& t) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    t.ki[i] = c_zig_ki[i];
+    t.wi[i] = c_zig_wi[i];
+    t.fi[i] = c_zig_fi[i];
+  }
+  __syncthreads();
 }
-__device__ __forceinline__ double zig_fast_value(uint64_t r) {
+
+// A draw is "fast" when the rectangle test accepts it.
+__device__ __forceinline__ bool zig_fast(const ZigTables& t, uint64_t r) {
   const int idx = int(r & 0xff);
   const uint64_t rabs = (r >> 9) & 0x000fffffffffffffULL;
-  double x = double(rabs) * c_zig_wi[idx];
+  return rabs < t.ki[idx];
+}
+__device__ __forceinline__ double zig_fast_value(const ZigTables& t, uint64_t r) {
+  const int idx = int(r & 0xff);
+  const uint64_t rabs = (r >> 9) & 0x000fffffffffffffULL;
+  double x = double(rabs) * t.wi[idx];
   return ((r >> 8) & 1) ? -x : x;
 }
 
 // Full sampler for a normal whose first attempt starts at stream position p.
 // Returns the position after the normal and (optionally) its value.
-__device__ uint64_t zig_resolve(uint64_t p, uint64_t k0, uint64_t k1, double* value) {
+__device__ uint64_t zig_resolve(const ZigTables& t, uint64_t p, uint64_t k0, uint64_t k1, double* value) {
   for (;;) {
     const uint64_t r = philox_word(p, k0, k1);
     p += 1;
     const int idx = int(r & 0xff);
     const uint64_t rr = r >> 8;
     const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
-    double x = double(rabs) * c_zig_wi[idx];
+    double x = double(rabs) * t.wi[idx];
     if (rr & 1) x = -x;
-    if (rabs < c_zig_ki[idx]) {
+    if (rabs < t.ki[idx]) {
       if (value) *value = x;
       return p;
     }
@@ -114,7 +126,7 @@ __device__ uint64_t zig_resolve(uint64_t p, uint64_t k0, uint64_t k1, double* va
     }
     const double u = u64_to_unit(philox_word(p, k0, k1));
     p += 1;
-    if ((c_zig_fi[idx - 1] - c_zig_fi[idx]) * u + c_zig_fi[idx] < exp(-0.5 * x * x)) {
+    if ((t.fi[idx - 1] - t.fi[idx]) * u + t.fi[idx] < exp(-0.5 * x * x)) {
       if (value) *value = x;
       return p;
     }
@@ -129,69 +141,65 @@ struct SketchArgs {
   long cols;
   double* out;
   long ldo;
-  int* exits;      // n_chunks: exit offset past chunk end (chunk-relative entry of the next)
-  int* counts;     // n_chunks × E
-  long* base;      // n_chunks: global normal index of the chunk's first start
-  int* entry;      // n_chunks: entry offset of the chunk
-  int* error;      // set on internal overflow
+  int* exits;   // n_chunks: exit offset past chunk end (= entry of the next)
+  int* counts;  // n_chunks × E
+  long* base;   // n_chunks: global normal index of the chunk's first start
+  int* entry;   // n_chunks: entry offset of the chunk
+  int* error;   // set on internal overflow
 };
 
-// Block-level discovery of the sorted special positions of one chunk.
-// Returns the number of specials (≤ PBQ_SK_MAXSPECIAL, else sets error).
-__device__ int sk_find_specials(const SketchArgs& a, long chunk, uint64_t* sp_pos, uint64_t* sp_next,
-                                int* warp_cnt) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int PER = PBQ_SK_CHUNK / PBQ_SK_THREADS;  // 8 consecutive positions per thread
-  const uint64_t p0 = uint64_t(chunk) * PBQ_SK_CHUNK + uint64_t(tid) * PER;
-  unsigned mask = 0;
+struct SkWarpSmem {
+  uint64_t sp_pos[PBQ_SK_MAXSPECIAL];
+  uint64_t sp_next[PBQ_SK_MAXSPECIAL];
+  unsigned keep[32];  // K3: per-lane start masks
+};
+
+// Warp-level discovery of the sorted special positions of one chunk; lane ℓ's
+// 32 positions → `mask` bit j (special draw at chunk position 32ℓ + j).
+__device__ __forceinline__ int sk_find_specials(const ZigTables& t, const SketchArgs& a, long chunk, SkWarpSmem& w,
+                                                unsigned& mask) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t p0 = uint64_t(chunk) * PBQ_SK_CHUNK + uint64_t(lane) * 32;
+  mask = 0;
 #pragma unroll
-  for (int b = 0; b < PER / 4; ++b) {
+  for (int b = 0; b < 8; ++b) {
     const Philox4x64 blk = philox4x64_10((p0 >> 2) + b + 1, a.k0, a.k1);
 #pragma unroll
-    for (int w = 0; w < 4; ++w)
-      if (!zig_fast(blk.x[w])) mask |= 1u << (b * 4 + w);
+    for (int q = 0; q < 4; ++q)
+      if (!zig_fast(t, blk.x[q])) mask |= 1u << (b * 4 + q);
   }
   const int mine = __popc(mask);
-  // block exclusive scan of counts (thread order == position order)
   int incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  if (lane == 31) warp_cnt[warp] = incl;
-  __syncthreads();
-  int wbase = 0, total = 0;
-  for (int w = 0; w < PBQ_SK_THREADS / 32; ++w) {
-    if (w < warp) wbase += warp_cnt[w];
-    total += warp_cnt[w];
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int off = incl - mine;
+  for (unsigned m = mask; m; m &= m - 1) {
+    const int j = __ffs(m) - 1;
+    if (off < PBQ_SK_MAXSPECIAL) w.sp_pos[off] = p0 + j;
+    ++off;
   }
-  int off = wbase + incl - mine;
-  for (int j = 0; j < PER; ++j)
-    if (mask & (1u << j)) {
-      if (off < PBQ_SK_MAXSPECIAL) sp_pos[off] = p0 + j;
-      ++off;
-    }
-  __syncthreads();
-  if (total > PBQ_SK_MAXSPECIAL) {
-    if (tid == 0) atomicExch(a.error, 1);
-    total = PBQ_SK_MAXSPECIAL;
-  }
-  for (int i = tid; i < total; i += PBQ_SK_THREADS) sp_next[i] = zig_resolve(sp_pos[i], a.k0, a.k1, nullptr);
-  __syncthreads();
-  return total;
+  const int nsp = min(total, PBQ_SK_MAXSPECIAL);
+  if (total > PBQ_SK_MAXSPECIAL && lane == 0) atomicExch(a.error, 1);
+  __syncwarp();
+  for (int i = lane; i < nsp; i += 32) w.sp_next[i] = zig_resolve(t, w.sp_pos[i], a.k0, a.k1, nullptr);
+  __syncwarp();
+  return nsp;
 }
 
 // Walk the start chain of one chunk from entry position s.
-__device__ __forceinline__ void sk_walk(uint64_t s, uint64_t cend, const uint64_t* sp_pos, const uint64_t* sp_next,
-                                        int nsp, int& count, uint64_t& exit_pos) {
+__device__ __forceinline__ void sk_walk(uint64_t s, uint64_t cend, const SkWarpSmem& w, int nsp, int& count,
+                                        uint64_t& exit_pos) {
   int c = 0;
   for (int i = 0; i < nsp; ++i) {
-    const uint64_t sp = sp_pos[i];
+    const uint64_t sp = w.sp_pos[i];
     if (sp < s) continue;
     if (sp >= cend) break;
     c += int(sp - s) + 1;
-    s = sp_next[i];
+    s = w.sp_next[i];
     if (s >= cend) break;
   }
   if (s < cend) {
@@ -203,25 +211,24 @@ __device__ __forceinline__ void sk_walk(uint64_t s, uint64_t cend, const uint64_
 }
 
 __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k1(SketchArgs a) {
-  __shared__ uint64_t sp_pos[PBQ_SK_MAXSPECIAL], sp_next[PBQ_SK_MAXSPECIAL];
-  __shared__ int warp_cnt[PBQ_SK_THREADS / 32];
-  __shared__ uint64_t exits_s[PBQ_SK_E];
-  const long chunk = blockIdx.x;
-  const int nsp = sk_find_specials(a, chunk, sp_pos, sp_next, warp_cnt);
+  __shared__ SkWarpSmem sw[PBQ_SK_WARPS];
+  __shared__ ZigTables zt;
+  zig_stage(zt);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long chunk = long(blockIdx.x) * PBQ_SK_WARPS + warp;
+  if (chunk >= a.n_chunks) return;
+  SkWarpSmem& w = sw[warp];
+  unsigned mask;
+  const int nsp = sk_find_specials(zt, a, chunk, w, mask);
   const uint64_t cstart = uint64_t(chunk) * PBQ_SK_CHUNK, cend = cstart + PBQ_SK_CHUNK;
-  const int tid = threadIdx.x;
-  if (tid < PBQ_SK_E) {
-    int cnt;
-    uint64_t ex;
-    sk_walk(cstart + tid, cend, sp_pos, sp_next, nsp, cnt, ex);
-    a.counts[chunk * PBQ_SK_E + tid] = cnt;
-    exits_s[tid] = ex;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    bool merged = true;
-    for (int e = 1; e < PBQ_SK_E; ++e) merged &= (exits_s[e] == exits_s[0]);
-    const uint64_t off = exits_s[0] - cend;
+  int cnt;
+  uint64_t ex;
+  sk_walk(cstart + lane, cend, w, nsp, cnt, ex);  // entry offset = lane
+  a.counts[chunk * PBQ_SK_E + lane] = cnt;
+  const uint64_t ex0 = __shfl_sync(0xffffffffu, ex, 0);
+  const bool merged = __all_sync(0xffffffffu, ex == ex0);
+  if (lane == 0) {
+    const uint64_t off = ex0 - cend;
     if (!merged || off >= uint64_t(PBQ_SK_E)) atomicExch(a.error, 2);
     a.exits[chunk] = int(off < uint64_t(PBQ_SK_E) ? off : 0);
   }
@@ -233,7 +240,7 @@ __global__ void __launch_bounds__(1024) sketch_k2(SketchArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long n = a.n_chunks;
   const long per = (n + 1023) / 1024;
-  const long c0 = tid * per, c1 = min(n, c0 + per);
+  const long c0 = tid * per, c1 = lmin(n, c0 + per);
   long local = 0;
   for (long c = c0; c < c1; ++c) {
     const int e = (c == 0) ? 0 : a.exits[c - 1];
@@ -264,67 +271,82 @@ __global__ void __launch_bounds__(1024) sketch_k2(SketchArgs a) {
 }
 
 __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k3(SketchArgs a) {
-  __shared__ uint64_t sp_pos[PBQ_SK_MAXSPECIAL], sp_next[PBQ_SK_MAXSPECIAL];
-  __shared__ int warp_cnt[PBQ_SK_THREADS / 32];
-  __shared__ unsigned char is_start[PBQ_SK_CHUNK];
-  const long chunk = blockIdx.x;
+  __shared__ SkWarpSmem sw[PBQ_SK_WARPS];
+  __shared__ double vals[PBQ_SK_WARPS][PBQ_SK_CHUNK];
+  __shared__ ZigTables zt;
+  zig_stage(zt);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long chunk = long(blockIdx.x) * PBQ_SK_WARPS + warp;
+  if (chunk >= a.n_chunks) return;
   const long base = a.base[chunk];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // chunk entirely outside the requested normal range: nothing to emit
-  const int cnt_here = a.counts[chunk * PBQ_SK_E + a.entry[chunk]];
-  if (base >= a.first + a.count || base + cnt_here <= a.first) return;
-  const int nsp = sk_find_specials(a, chunk, sp_pos, sp_next, warp_cnt);
+  const int entry = a.entry[chunk];
+  const int cnt_here = a.counts[chunk * PBQ_SK_E + entry];
+  if (base >= a.first + a.count || base + cnt_here <= a.first) return;  // nothing requested here
+  SkWarpSmem& w = sw[warp];
+  unsigned special;
+  const int nsp = sk_find_specials(zt, a, chunk, w, special);
   const uint64_t cstart = uint64_t(chunk) * PBQ_SK_CHUNK, cend = cstart + PBQ_SK_CHUNK;
-  for (int i = tid; i < PBQ_SK_CHUNK; i += PBQ_SK_THREADS) is_start[i] = (i >= a.entry[chunk]) ? 1 : 0;
-  __syncthreads();
-  if (tid == 0) {
-    // clear the positions a special draw consumes beyond its own
-    uint64_t s = cstart + a.entry[chunk];
+  // start mask: every position from the entry on, minus the words consumed by
+  // special normals beyond their first word (walked by lane 0, set in smem)
+  unsigned start = (lane * 32 >= entry) ? 0xffffffffu : ((entry - lane * 32 >= 32) ? 0u : (0xffffffffu << (entry - lane * 32)));
+  w.keep[lane] = start;
+  __syncwarp();
+  if (lane == 0) {
+    uint64_t s = cstart + entry;
     for (int i = 0; i < nsp; ++i) {
-      const uint64_t sp = sp_pos[i];
-      if (sp < s) {
-        continue;  // consumed by an earlier normal (already cleared)
+      const uint64_t sp = w.sp_pos[i];
+      if (sp < s) continue;
+      const uint64_t nx = w.sp_next[i];
+      for (uint64_t q = sp + 1; q < nx && q < cend; ++q) {
+        const int rel = int(q - cstart);
+        w.keep[rel >> 5] &= ~(1u << (rel & 31));
       }
-      const uint64_t nx = sp_next[i];
-      for (uint64_t q = sp + 1; q < nx && q < cend; ++q) is_start[q - cstart] = 0;
       s = nx;
       if (s >= cend) break;
     }
   }
-  __syncthreads();
-  constexpr int PER = PBQ_SK_CHUNK / PBQ_SK_THREADS;
-  int mine = 0;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) mine += is_start[tid * PER + j];
+  __syncwarp();
+  start = w.keep[lane];
+  const int mine = __popc(start);
   int incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  __syncthreads();
-  if (lane == 31) warp_cnt[warp] = incl;
-  __syncthreads();
-  int wbase = 0;
-  for (int w = 0; w < warp; ++w) wbase += warp_cnt[w];
-  long idx = base + wbase + incl - mine;
-  const uint64_t p0 = cstart + uint64_t(tid) * PER;
+  int rank = incl - mine;  // chunk-local index of this lane's first normal
+  const uint64_t p0 = cstart + uint64_t(lane) * 32;
 #pragma unroll
-  for (int b = 0; b < PER / 4; ++b) {
+  for (int b = 0; b < 8; ++b) {
     const Philox4x64 blk = philox4x64_10((p0 >> 2) + b + 1, a.k0, a.k1);
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const int j = b * 4 + w;
-      if (!is_start[tid * PER + j]) continue;
-      if (idx >= a.first && idx < a.first + a.count) {
-        const uint64_t r = blk.x[w];
-        double v;
-        if (zig_fast(r)) v = zig_fast_value(r);
-        else zig_resolve(p0 + j, a.k0, a.k1, &v);
-        const long rel = idx - a.first;
-        a.out[(rel / a.cols) * a.ldo + rel % a.cols] = v;
-      }
-      ++idx;
+    for (int q = 0; q < 4; ++q) {
+      const int j = b * 4 + q;
+      if (!((start >> j) & 1u)) continue;
+      const uint64_t r = blk.x[q];
+      double v;
+      if (zig_fast(zt, r)) v = zig_fast_value(zt, r);
+      else zig_resolve(zt, p0 + j, a.k0, a.k1, &v);
+      vals[warp][rank++] = v;
+    }
+  }
+  __syncwarp();
+  // coalesced write-out of this chunk's normals [base, base + cnt_here)
+  const long lo = lmax(base, a.first), hi = lmin(base + cnt_here, a.first + a.count);
+  const long rel0 = lo - a.first;
+  long row = rel0 / a.cols;
+  long col = rel0 - row * a.cols;
+  // lane-strided: element e ↔ lo + e
+  long step_row = 32 / a.cols, step_col = 32 % a.cols;
+  long r_l = row + (col + lane) / a.cols;
+  long c_l = (col + lane) % a.cols;
+  for (long e = lane; e < hi - lo; e += 32) {
+    a.out[r_l * a.ldo + c_l] = vals[warp][lo - base + e];
+    r_l += step_row;
+    c_l += step_col;
+    if (c_l >= a.cols) {
+      c_l -= a.cols;
+      r_l += 1;
     }
   }
 }

@@ -41,10 +41,10 @@ __global__ void bench(double* out, long long* cyc) {
 int main() {
   double* out;
   long long* cyc;
-  cudaMalloc(&out, 256 * 8);
+  cudaMalloc(&out, 1024 * 8);
   cudaMallocManaged(&cyc, 64);
   for (int it = 0; it < 2; ++it) {
-    bench<<<1, 256>>>(out, cyc);
+    bench<<<1, QR_THREADS>>>(out, cyc);
     cudaDeviceSynchronize();
   }
   printf("{\"chol32\": %lld, \"lu32\": %lld, \"tri_inv32\": %lld, \"mm32\": %lld, \"err\": \"%s\"}\n", cyc[0], cyc[1],

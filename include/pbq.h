@@ -133,6 +133,15 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* prob, const pbq_outputs* out, v
 int pbq_transpose(pbq_ctx* ctx, int64_t n, const double* src, int64_t lds, double* dst,
                   int64_t ldd, int32_t lower, void* stream);
 
+/* Per-kernel-class timing of everything this context enqueues between
+ * begin and end: CUDA events recorded on the launch stream around each kernel.
+ * end() synchronises on the recorded events and returns the summed
+ * milliseconds and launch counts for 4 classes: 0 GEMM, 1 QR, 2 sketch,
+ * 3 other (transposes, flag merges).  Used by bench.py for the roofline of
+ * the dominant kernel, measured inside the timed region. */
+int pbq_profile_begin(pbq_ctx* ctx, int32_t capacity);
+int pbq_profile_end(pbq_ctx* ctx, double* ms_by_class, int32_t* launches_by_class);
+
 /* Profiling hooks (device pointers, NULL to disable): number of QR panels
  * that took the column-by-column fallback, and CTA-0 nanoseconds per QR
  * phase (12 slots, see qr_f64.cuh). */

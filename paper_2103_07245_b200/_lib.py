@@ -40,6 +40,8 @@ EXPORTED = (
     "pbq_pbp_qlp",
     "pbq_transpose",
     "pbq_debug_qr_hooks",
+    "pbq_profile_begin",
+    "pbq_profile_end",
 )
 
 c_i64 = ctypes.c_int64
@@ -91,6 +93,8 @@ _SIGS = {
     "pbq_pbp_qlp": ([c_p, ctypes.POINTER(PbqProblem), ctypes.POINTER(PbqOutputs), c_p, c_sz, c_p], ctypes.c_int),
     "pbq_transpose": ([c_p, c_i64, c_p, c_i64, c_p, c_i64, c_i32, c_p], ctypes.c_int),
     "pbq_debug_qr_hooks": ([c_p, c_p, c_p], ctypes.c_int),
+    "pbq_profile_begin": ([c_p, c_i32], ctypes.c_int),
+    "pbq_profile_end": ([c_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)], ctypes.c_int),
 }
 
 _lib = None

@@ -14,7 +14,17 @@
 #include "qr_f64.cuh"
 #include "sketch.cuh"
 
+// Optional per-kernel-class timing (pbq_profile_*): event pairs recorded on
+// the launch stream around every kernel of the pipeline.
+struct PbqProfile {
+  bool on = false;
+  int cap = 0, used = 0;
+  cudaEvent_t* ev = nullptr;  // 2·cap events
+  int* cls = nullptr;         // class per pair: 0 GEMM, 1 QR, 2 sketch, 3 other
+};
+
 struct pbq_ctx {
+  PbqProfile prof;
   int device = 0;
   int sms = 0;
   size_t smem_optin = 0;
@@ -55,6 +65,24 @@ int fail(pbq_ctx* ctx, int code, const char* fmt, ...) {
   } while (0)
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// RAII bracket: records a start/stop event pair around one kernel class when
+// profiling is on (no-op otherwise).
+struct ProfScope {
+  PbqProfile& pr;
+  cudaStream_t st;
+  int slot = -1;
+  ProfScope(PbqProfile& p, cudaStream_t s, int cls) : pr(p), st(s) {
+    if (pr.on && pr.used < pr.cap) {
+      slot = pr.used++;
+      pr.cls[slot] = cls;
+      cudaEventRecord(pr.ev[2 * slot], st);
+    }
+  }
+  ~ProfScope() {
+    if (slot >= 0) cudaEventRecord(pr.ev[2 * slot + 1], st);
+  }
+};
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -140,6 +168,7 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   }
   PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   void* args[] = {&a};
+  ProfScope ps(ctx->prof, st, 0);
   PBQ_CUDA(ctx, cudaLaunchKernel(fn, dim3(pl.grid), dim3(threads), args, smem, st));
   ctx->launches += 1;
   return PBQ_OK;
@@ -214,6 +243,7 @@ int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&qr_tall_kernel),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
   void* args[] = {&a};
+  ProfScope ps(ctx->prof, st, 1);
   PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&qr_tall_kernel), dim3(pl.grid),
                                             dim3(QR_THREADS), args, pl.smem, st));
   ctx->launches += 1;
@@ -271,6 +301,7 @@ int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t 
   a.error = error_flag ? error_flag : own_err;
   if (!error_flag) PBQ_CUDA(ctx, cudaMemsetAsync(own_err, 0, sizeof(int), st));
   const unsigned sk_grid = unsigned(ceil_div(pl.n_chunks, PBQ_SK_WARPS));
+  ProfScope ps(ctx->prof, st, 2);
   sketch_k1<<<dim3(sk_grid), PBQ_SK_THREADS, 0, st>>>(a);
   PBQ_CUDA(ctx, cudaGetLastError());
   sketch_k2<<<1, 1024, 0, st>>>(a);
@@ -300,6 +331,7 @@ __global__ void transpose_kernel(long n, const double* __restrict__ src, long ld
 int transpose_launch(pbq_ctx* ctx, long n, const double* src, long lds, double* dst, long ldd, int lower,
                      cudaStream_t st) {
   dim3 grid(unsigned(ceil_div(n, 32)), unsigned(ceil_div(n, 32)));
+  ProfScope ps(ctx->prof, st, 3);
   transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(n, src, lds, dst, ldd, lower);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 1;
@@ -336,7 +368,50 @@ int pbq_ctx_create(int device, pbq_ctx** out) {
 }
 
 int pbq_ctx_destroy(pbq_ctx* ctx) {
+  if (ctx && ctx->prof.ev) {
+    for (int i = 0; i < 2 * ctx->prof.cap; ++i) cudaEventDestroy(ctx->prof.ev[i]);
+    delete[] ctx->prof.ev;
+    delete[] ctx->prof.cls;
+  }
   delete ctx;
+  return PBQ_OK;
+}
+
+int pbq_profile_begin(pbq_ctx* ctx, int32_t capacity) {
+  if (!ctx || capacity < 1) return PBQ_ERR_PARAM;
+  PbqProfile& pr = ctx->prof;
+  if (pr.cap < capacity) {
+    if (pr.ev) {
+      for (int i = 0; i < 2 * pr.cap; ++i) cudaEventDestroy(pr.ev[i]);
+      delete[] pr.ev;
+      delete[] pr.cls;
+    }
+    pr.ev = new cudaEvent_t[2 * capacity];
+    pr.cls = new int[capacity];
+    for (int i = 0; i < 2 * capacity; ++i) PBQ_CUDA(ctx, cudaEventCreate(&pr.ev[i]));
+    pr.cap = capacity;
+  }
+  pr.used = 0;
+  pr.on = true;
+  return PBQ_OK;
+}
+
+int pbq_profile_end(pbq_ctx* ctx, double* ms_by_class, int32_t* launches_by_class) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  PbqProfile& pr = ctx->prof;
+  pr.on = false;
+  for (int c = 0; c < 4; ++c) {
+    ms_by_class[c] = 0.0;
+    launches_by_class[c] = 0;
+  }
+  for (int i = 0; i < pr.used; ++i) {
+    PBQ_CUDA(ctx, cudaEventSynchronize(pr.ev[2 * i + 1]));
+    float ms = 0.f;
+    PBQ_CUDA(ctx, cudaEventElapsedTime(&ms, pr.ev[2 * i], pr.ev[2 * i + 1]));
+    ms_by_class[pr.cls[i]] += ms;
+    launches_by_class[pr.cls[i]] += 1;
+  }
+  pr.used = 0;
   return PBQ_OK;
 }
 

@@ -41,6 +41,18 @@ class Context:
     def check(self, status, what):
         _lib.raise_status(status, self.handle, what)
 
+    def profile_begin(self, capacity=4096):
+        """Start bracketing every kernel this context enqueues with CUDA events."""
+        self.check(self.lib.pbq_profile_begin(self.handle, int(capacity)), "profile_begin")
+
+    def profile_end(self):
+        """(ms, launches) per kernel class {gemm, qr, sketch, other} since begin."""
+        ms = (ctypes.c_double * 4)()
+        n = (ctypes.c_int32 * 4)()
+        self.check(self.lib.pbq_profile_end(self.handle, ms, n), "profile_end")
+        names = ("gemm", "qr", "sketch", "other")
+        return {k: (ms[i], n[i]) for i, k in enumerate(names)}
+
 
 def require_cuda(device=None):
     if not torch.cuda.is_available():

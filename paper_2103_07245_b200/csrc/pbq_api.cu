@@ -103,19 +103,22 @@ struct Carve {
 
 // ---------------------------------------------------------------- GEMM ----
 // Two tile shapes: d ≤ 64 uses 128×64 (warp 32×32), larger d 128×128 (warp 64×32).
-constexpr int G_BM = 128, G_BK = 32, G_STAGES = 3;
-
-template <bool T, int BN, int WM, int WN>
+// Tile configurations (BM×BN, BK, warp tile, stages), all 8 warps:
+//   N ≤ 64 : 128×64,  BK 32, warp 32×32, 3 stages
+//   N > 64 : 128×128, BK 32, warp 64×32, 3 stages (A streamed ⌈N/128⌉ times;
+//            a 64×256 tile that reads A once measured 6% slower at d = 256:
+//            BK 16 doubles the barriers and DRAM is at 14% of bandwidth)
+template <bool T, int BM, int BN, int BK, int WM, int WN, int ST>
 struct GemmKernel {
-  using Cfg = GemmCfg<T, G_BM, BN, G_BK, WM, WN, G_STAGES>;
+  using Cfg = GemmCfg<T, BM, BN, BK, WM, WN, ST>;
   static void* fn(bool check) {
-    return check ? reinterpret_cast<void*>(&gemm_f64_streamk<T, G_BM, BN, G_BK, WM, WN, G_STAGES, true>)
-                 : reinterpret_cast<void*>(&gemm_f64_streamk<T, G_BM, BN, G_BK, WM, WN, G_STAGES, false>);
+    return check ? reinterpret_cast<void*>(&gemm_f64_streamk<T, BM, BN, BK, WM, WN, ST, true>)
+                 : reinterpret_cast<void*>(&gemm_f64_streamk<T, BM, BN, BK, WM, WN, ST, false>);
   }
 };
 
 struct GemmPlan {
-  int bn;
+  int bm, bn;
   int tiles_m, tiles_n, k_iters;
   long total;
   int grid;
@@ -123,17 +126,22 @@ struct GemmPlan {
 
 GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K) {
   GemmPlan p;
-  p.bn = (N <= 64) ? 64 : 128;
-  p.tiles_m = int(ceil_div(M, G_BM));
+  const int bk = 32;
+  if (N <= 64) {
+    p.bm = 128; p.bn = 64;
+  } else {
+    p.bm = 128; p.bn = 128;
+  }
+  p.tiles_m = int(ceil_div(M, p.bm));
   p.tiles_n = int(ceil_div(N, p.bn));
-  p.k_iters = int(ceil_div(K, G_BK));
+  p.k_iters = int(ceil_div(K, bk));
   p.total = long(p.tiles_m) * p.tiles_n * p.k_iters;
   p.grid = int(std::min<long>(ctx->sms, p.total));
   return p;
 }
 
 size_t gemm_ws_bytes(const GemmPlan& p) {
-  return align_up(size_t(p.grid) * G_BM * p.bn * sizeof(double), 256) + align_up(size_t(p.grid) * sizeof(int), 256) + 512;
+  return align_up(size_t(p.grid) * p.bm * p.bn * sizeof(double), 256) + align_up(size_t(p.grid) * sizeof(int), 256) + 512;
 }
 
 template <bool TRANS>
@@ -151,7 +159,7 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.C = C; a.ldc = ldc;
   a.alpha = alpha; a.beta = beta;
   a.tiles_m = pl.tiles_m; a.tiles_n = pl.tiles_n; a.k_iters = pl.k_iters; a.total_iters = pl.total;
-  a.partials = cv.take<double>(size_t(pl.grid) * G_BM * pl.bn);
+  a.partials = cv.take<double>(size_t(pl.grid) * pl.bm * pl.bn);
   a.flags = cv.take<int>(pl.grid);
   a.nonfinite = nonfinite;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gemm: workspace too small (%zu < %zu)", ws_bytes, cv.off);
@@ -160,10 +168,10 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   size_t smem;
   int threads;
   if (pl.bn == 64) {
-    using K_ = GemmKernel<TRANS, 64, 32, 32>;
+    using K_ = GemmKernel<TRANS, 128, 64, 32, 32, 32, 3>;
     fn = K_::fn(nonfinite != nullptr); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
   } else {
-    using K_ = GemmKernel<TRANS, 128, 64, 32>;
+    using K_ = GemmKernel<TRANS, 128, 128, 32, 64, 32, 3>;
     fn = K_::fn(nonfinite != nullptr); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
   }
   PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

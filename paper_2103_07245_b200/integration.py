@@ -1,0 +1,75 @@
+"""Drop-in wiring for the reference package.
+
+``install(pbpqlp)`` rebinds the reference's PbP-QLP entry point — in every
+module that imported it by name (algorithms.py:209, __init__.py:18,
+analysis.py:16-25 → factorize :153-154, estimators.py:17 → PbpQlp
+:98-105, bounds.py:42 → eval_highprob_bounds :589, cli.py:43 → :448, :733)
+— to a wrapper around :func:`paper_2103_07245_b200.pbp_qlp` that
+
+* returns the reference's own ``QlpFactors`` / ``SketchRecord`` dataclasses
+  holding numpy arrays (so every downstream consumer keeps working),
+* raises the reference's exception classes (ParameterError, DimensionError,
+  MatrixInputError), and
+* re-emits rank-deficiency warnings as the reference's RankDeficiencyWarning.
+
+The GPU does every FLOP; this module only adapts types.
+"""
+import warnings
+
+from . import algorithms as _alg
+from . import exceptions as _exc
+
+# modules of the reference that bind the name `pbp_qlp` at import time
+_BINDERS = ("", ".algorithms", ".analysis", ".estimators", ".bounds", ".cli")
+
+
+def make_dropin(pbpqlp):
+    """Return a reference-typed ``pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True)``."""
+    ref_alg = pbpqlp.algorithms
+    ref_exc = pbpqlp.exceptions
+
+    def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True):
+        with warnings.catch_warnings(record=True) as rec:
+            warnings.simplefilter("always", _exc.RankDeficiencyWarning)
+            try:
+                f = _alg.pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
+            except _exc.DimensionError as e:
+                raise ref_exc.DimensionError(str(e)) from None
+            except _exc.ParameterError as e:
+                raise ref_exc.ParameterError(str(e)) from None
+            except _exc.MatrixInputError as e:
+                raise ref_exc.MatrixInputError(str(e)) from None
+        for w in rec:
+            if issubclass(w.category, _exc.RankDeficiencyWarning):
+                warnings.warn(str(w.message), ref_exc.RankDeficiencyWarning, stacklevel=2)
+            else:
+                warnings.warn_explicit(w.message, w.category, w.filename, w.lineno)
+        sk = f.sketch
+        sketch = ref_alg.SketchRecord(sk.test_matrix, int(seed), sk.d, sk.q, sk.passes_over_a)
+        return ref_alg.QlpFactors(f.q_basis, f.l, f.p_basis, f.first_stage_r, sketch)
+
+    pbp_qlp.__doc__ = ref_alg.pbp_qlp.__doc__
+    pbp_qlp.__wrapped_gpu__ = True
+    return pbp_qlp
+
+
+def install(pbpqlp):
+    """Patch every module of the imported reference package ``pbpqlp`` that
+    bound ``pbp_qlp``; returns the previous bindings (for ``uninstall``)."""
+    import importlib
+
+    dropin = make_dropin(pbpqlp)
+    saved = {}
+    for suffix in _BINDERS:
+        mod = importlib.import_module(pbpqlp.__name__ + suffix) if suffix else pbpqlp
+        if hasattr(mod, "pbp_qlp"):
+            saved[mod.__name__] = mod.pbp_qlp
+            mod.pbp_qlp = dropin
+    return saved
+
+
+def uninstall(saved):
+    import sys
+
+    for name, fn in saved.items():
+        setattr(sys.modules[name], "pbp_qlp", fn)

@@ -106,3 +106,25 @@ def test_flop_model_matches_baseline():
              (200000, 8192, 512, 1): 7.151e12, (65536, 16384, 64, 0): 2.764e11, (65536, 16384, 1024, 2): 1.425e13}
     for key, f in table.items():
         assert abs(pbp_qlp_flops(*key) / f - 1) < 2e-3, key
+
+
+def test_integration_shim_maps_errors_to_reference_classes(reference_pkg):
+    """integration.install rebinds every reference module that imported
+    pbp_qlp; invalid arguments then raise the reference's own classes."""
+    import sys
+
+    from paper_2103_07245_b200 import integration
+
+    saved = integration.install(reference_pkg)
+    try:
+        for name in saved:
+            assert getattr(sys.modules[name], "pbp_qlp").__wrapped_gpu__
+        with pytest.raises(reference_pkg.ParameterError):
+            reference_pkg.pbp_qlp(np.eye(4), 9)
+        with pytest.raises(reference_pkg.DimensionError):
+            reference_pkg.pbp_qlp(np.eye(4), 2, q=-1)
+        with pytest.raises(reference_pkg.MatrixInputError):
+            reference_pkg.pbp_qlp(np.ones(3), 1)
+    finally:
+        integration.uninstall(saved)
+    assert not getattr(reference_pkg.pbp_qlp, "__wrapped_gpu__", False)

@@ -110,3 +110,59 @@ def test_torch_input_stays_on_device(cuda):
     assert isinstance(f.q_basis, torch.Tensor) and f.q_basis.is_cuda
     ref = pbp_qlp(a.cpu().numpy(), 32, q=1)
     assert np.array_equal(f.l.cpu().numpy(), ref.l)
+
+
+def test_integration_shim_returns_reference_types(cuda):
+    """The drop-in wrapper hands back the reference's dataclasses; a stand-in
+    module with the reference's attribute layout replaces the reference here
+    (it is not present on the GPU box)."""
+    import types
+    from dataclasses import dataclass
+    from typing import Any
+
+    from paper_2103_07245_b200 import integration
+
+    @dataclass(frozen=True)
+    class SketchRecord:
+        test_matrix: Any
+        seed: int
+        d: int
+        q: int
+        passes_over_a: int
+
+    @dataclass(frozen=True)
+    class QlpFactors:
+        q_basis: Any
+        l: Any
+        p_basis: Any
+        first_stage_r: Any
+        sketch: Any = None
+
+    class ParameterError(ValueError):
+        pass
+
+    class DimensionError(ParameterError):
+        pass
+
+    class MatrixInputError(ValueError):
+        pass
+
+    class RankDeficiencyWarning(UserWarning):
+        pass
+
+    fake = types.SimpleNamespace(
+        algorithms=types.SimpleNamespace(SketchRecord=SketchRecord, QlpFactors=QlpFactors, pbp_qlp=lambda *a, **k: None),
+        exceptions=types.SimpleNamespace(ParameterError=ParameterError, DimensionError=DimensionError,
+                                         MatrixInputError=MatrixInputError, RankDeficiencyWarning=RankDeficiencyWarning),
+    )
+    fn = integration.make_dropin(fake)
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((200, 120))
+    f = fn(a, 16, q=1, seed=3)
+    assert isinstance(f, QlpFactors) and isinstance(f.sketch, SketchRecord)
+    assert f.sketch.passes_over_a == 4 and f.sketch.test_matrix.shape == (200, 16)
+    with pytest.raises(ParameterError):
+        fn(a, 500)
+    low = rng.standard_normal((200, 3)) @ rng.standard_normal((3, 120))
+    with pytest.warns(RankDeficiencyWarning):
+        fn(low, 10)

@@ -1,0 +1,182 @@
+"""Row-sharded multi-GPU PbP-QLP.
+
+Rank g of G owns the contiguous row block A_g = A[r_g : r_{g+1}] and the
+matching rows Φ_g of the sketch (the device generator produces any row range
+of the global stream, so Φ does not depend on G).  Exchanges:
+
+* AᵀX = Σ_g A_gᵀ X_g — a local GEMM, then one NCCL allreduce(sum) of the
+  n2×d partial; the result is identical on all ranks, so ``orth`` of it is
+  computed replicated (same input → same bits).
+* qr(A·P̄) — A_g·P̄ is local; its QR is a distributed TSQR: local Householder
+  QR (Q_g, R_g), all-gather of the d×d R factors, a replicated QR of the
+  stacked (G·d)×d matrix → (Q̂, R), then Q_g ← Q_g·Q̂_g (local GEMM).  R and
+  the `orth` rank test come from the replicated QR.
+* qr(Rᵀ), L = tril(R̃ᵀ) and P = P̄·W are replicated.
+
+Q stays row-sharded (rank g holds Q[r_g : r_{g+1}]); L, P, R are replicated.
+The local arithmetic goes through a backend: :class:`CudaBackend` (libpbq's
+sm_100a kernels through the C ABI) in the product.  The CPU ``gloo`` tests
+substitute a numpy backend defined in tests/ to exercise exactly this
+orchestration without a GPU.
+"""
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from . import device as _dev
+from . import exceptions as _exc
+from .linalg import warn_rank
+
+__all__ = ["shard_rows", "DistributedPbpQlp", "CudaBackend"]
+
+
+def shard_rows(n1, world):
+    """Contiguous, balanced row offsets [r_0 = 0, …, r_G = n1]."""
+    return [(n1 * g) // world for g in range(world + 1)]
+
+
+class CudaBackend:
+    """Local kernels of one rank: libpbq through the C ABI (no CPU path)."""
+
+    def __init__(self, device):
+        self.device = _dev.require_cuda(device)
+        self.ctx = _dev.context(self.device)
+
+    def empty(self, rows, cols):
+        return _dev.empty_matrix(rows, cols, self.device)
+
+    def zeros_i32(self, n):
+        return torch.zeros(n, dtype=torch.int32, device=self.device)
+
+    def gaussian(self, rows, cols, seed, row_offset):
+        return _dev.gaussian(self.ctx, rows, cols, seed, self.device, row_offset=row_offset)
+
+    def gemm_tn(self, a, x, out, nonfinite=None):
+        return _dev.gemm(self.ctx, a, x, trans_a=True, out=out, nonfinite=nonfinite)
+
+    def gemm_nn(self, a, x, out):
+        return _dev.gemm(self.ctx, a, x, trans_a=False, out=out)
+
+    def qr_(self, m, r, flag=None):
+        """In-place thin QR of m (m ≥ n); R into r; rank test into flag[0]."""
+        _dev.householder_qr_(self.ctx, m, r, want_q=True, rank_flag=flag)
+
+    def transpose(self, src, dst, lower=False):
+        return _dev.transpose(self.ctx, src, dst, lower=lower)
+
+    def contiguous(self, t):
+        return _dev.as_kernel_operand(t)
+
+
+class DistributedPbpQlp:
+    """One rank's part of a row-sharded PbP-QLP; all ranks call ``run``."""
+
+    def __init__(self, n1, n2, d, q, rows, device=None, reorthonormalize=True, group=None, backend=None):
+        self.n1, self.n2, self.d, self.q = int(n1), int(n2), int(d), int(q)
+        self.rows = list(rows)
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if len(self.rows) != self.world + 1 or self.rows[0] != 0 or self.rows[-1] != n1:
+            raise _exc.ParameterError("rows must be the G+1 shard offsets of [0, n1]")
+        self.m = self.rows[self.rank + 1] - self.rows[self.rank]
+        if self.m < self.d:
+            raise _exc.ParameterError(f"each shard needs ≥ d={d} rows for the local TSQR leaf (rank {self.rank} has {self.m})")
+        if not 1 <= self.d <= min(n1, n2):
+            raise _exc.ParameterError(f"d must be in [1, {min(n1, n2)}], got {d}")
+        self.reorthonormalize = bool(reorthonormalize)
+        self.be = backend if backend is not None else CudaBackend(device)
+        be = self.be
+        self.C = be.empty(self.n2, self.d)         # AᵀX partial → allreduced → P̄ (in place)
+        self.Q = be.empty(self.m, self.d)          # A_g·P̄ → local Q_g → Q rows of this rank
+        self.R = be.empty(self.d, self.d)
+        self.Rloc = be.empty(self.d, self.d)
+        self.stack = be.empty(self.world * self.d, self.d)
+        self.Rs = be.empty(self.d, self.d)
+        self.W = be.empty(self.d, self.d)
+        self.Rt = be.empty(self.d, self.d)
+        self.L = be.empty(self.d, self.d)
+        self.P = be.empty(self.n2, self.d)
+        self.Qtmp = be.empty(self.m, self.d)
+        self.flags = be.zeros_i32(2 * self.q + 2)  # [non-finite, rank flags …]
+        self.PHI = None
+
+    # -- collectives ---------------------------------------------------------
+    def _allreduce(self, t):
+        dense = t if t.is_contiguous() else t.contiguous()
+        dist.all_reduce(dense, op=dist.ReduceOp.SUM, group=self.group)
+        if dense is not t:
+            t.copy_(dense)
+        return t
+
+    def _tsqr_(self, flag=None):
+        """Distributed QR of the row-sharded self.Q (m_g × d) in place; R → self.R."""
+        be = self.be
+        be.qr_(self.Q, self.Rloc)
+        rl = self.Rloc.contiguous()
+        if dist.get_backend(self.group) == "nccl":
+            gathered = torch.empty((self.world * self.d, self.d), dtype=rl.dtype, device=rl.device)
+            dist.all_gather_into_tensor(gathered, rl, group=self.group)
+        else:
+            parts = [torch.empty_like(rl) for _ in range(self.world)]
+            dist.all_gather(parts, rl, group=self.group)
+            gathered = torch.cat(parts, 0)
+        self.stack.copy_(gathered)
+        be.qr_(self.stack, self.R, flag)  # replicated: same input on every rank
+        qhat = self.stack[self.rank * self.d:(self.rank + 1) * self.d]
+        be.gemm_nn(self.Q, be.contiguous(qhat), self.Qtmp)
+        self.Q.copy_(self.Qtmp)
+
+    # -- the algorithm ------------------------------------------------------
+    def run(self, A_local, seed=0, phi_local=None):
+        """Enqueue one factorization of this rank's rows (kernel-ready operand)."""
+        be = self.be
+        d, q = self.d, self.q
+        self.flags.zero_()
+        flags = self.flags
+        if phi_local is None:
+            self.PHI = be.gaussian(self.m, d, seed, self.rows[self.rank])
+        else:
+            self.PHI = be.contiguous(phi_local)
+        site = 1
+        be.gemm_tn(A_local, self.PHI, self.C, nonfinite=flags[0:1])
+        self._allreduce(self.C)
+        if self.reorthonormalize:
+            be.qr_(self.C, self.Rs, flags[site:site + 1])
+            site += 1
+            for _ in range(q):
+                be.gemm_nn(A_local, self.C, self.Q)
+                self._tsqr_(flags[site:site + 1])
+                site += 1
+                be.gemm_tn(A_local, self.Q, self.C)
+                self._allreduce(self.C)
+                be.qr_(self.C, self.Rs, flags[site:site + 1])
+                site += 1
+        else:
+            for _ in range(q):
+                be.gemm_nn(A_local, self.C, self.Q)
+                be.gemm_tn(A_local, self.Q, self.C)
+                self._allreduce(self.C)
+            be.qr_(self.C, self.Rs, flags[site:site + 1])
+        be.gemm_nn(A_local, self.C, self.Q)
+        self._tsqr_()
+        be.transpose(self.R, self.W)
+        be.qr_(self.W, self.Rt)
+        be.transpose(self.Rt, self.L, lower=True)
+        be.gemm_nn(self.C, self.W, self.P)
+
+    def finish(self, stacklevel=3):
+        """Synchronise, raise / warn like the reference (every rank)."""
+        # a non-finite entry in any shard fails every rank
+        dist.all_reduce(self.flags[0:1], op=dist.ReduceOp.MAX, group=self.group)
+        fl = self.flags.cpu().tolist()
+        if fl[0]:
+            raise _exc.MatrixInputError("a contains non-finite entries")
+        for f in fl[1:]:
+            warn_rank(f, stacklevel=stacklevel + 1)
+        return fl
+
+    def factors(self):
+        """(Q rows of this rank, L, P, R)."""
+        return self.Q, self.L, self.P, self.R

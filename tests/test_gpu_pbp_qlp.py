@@ -166,3 +166,37 @@ def test_integration_shim_returns_reference_types(cuda):
     low = rng.standard_normal((200, 3)) @ rng.standard_normal((3, 120))
     with pytest.warns(RankDeficiencyWarning):
         fn(low, 10)
+
+
+def test_distributed_driver_on_one_gpu(cuda):
+    """The row-sharded driver with NCCL and the CUDA backend (world size 1 on
+    the single-GPU box): TSQR + allreduce path against the fused pipeline."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2103_07245_b200 import pbp_qlp
+    from paper_2103_07245_b200.distributed import DistributedPbpQlp, shard_rows
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=cuda)
+    try:
+        rng = np.random.default_rng(9)
+        a = rng.standard_normal((900, 60)) @ rng.standard_normal((60, 500)) / 8 + 1e-3 * rng.standard_normal((900, 500))
+        at = torch.from_numpy(a).to(cuda)
+        run = DistributedPbpQlp(900, 500, 48, 1, shard_rows(900, 1), device=cuda)
+        run.run(at, seed=7)
+        run.finish()
+        qg, l, p, r = (t.cpu().numpy() for t in run.factors())
+        ref = pbp_qlp(a, 48, q=1, seed=7)
+        tol = conditioning_tolerance(ref.l, strict=1e-10)
+        assert np.all(column_relative_error(qg, ref.q_basis) <= tol)
+        assert np.all(column_relative_error(p, ref.p_basis) <= tol)
+        assert np.allclose(np.diag(l), np.diag(ref.l), rtol=1e-10, atol=0)
+    finally:
+        dist.destroy_process_group()

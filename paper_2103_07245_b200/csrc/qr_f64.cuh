@@ -40,10 +40,14 @@ constexpr int QR_EPT = 32 / QR_TPR;      // entries per thread of a 32×32 tile
 constexpr int QR_RG = QR_THREADS / 64;   // row groups of the Gram accumulation
 constexpr int QR_IPT = 32 / (QR_THREADS / 32);  // W-partial i-rows per thread (32 columns per warp)
 constexpr int QR_NB = 32;                 // panel width
-constexpr int QR_SLD = QR_NB + 1;         // leading dimension of 32×32 smem matrices
-constexpr int QR_PLD = QR_NB + 1;         // leading dimension of the panel rows
-constexpr int QR_TILE_DOUBLES = 4096;     // one 32 KB staging tile (32 rows × 128 columns)
-constexpr int QR_CW = QR_TILE_DOUBLES / QR_NB;  // 128 columns per tile
+// Row strides ≡ 4 (mod 16) doubles: DMMA fragment loads of either
+// orientation (rows g / columns t of an 8×4 fragment) hit 16 distinct bank
+// pairs per half-warp.
+constexpr int QR_SLD = QR_NB + 4;         // leading dimension of 32×32 smem matrices
+constexpr int QR_PLD = QR_NB + 4;         // leading dimension of the panel rows
+constexpr int QR_CW = 128;                // trailing columns per staged tile
+constexpr int QR_XLD = QR_CW + 4;         // leading dimension of staged tiles
+constexpr int QR_TILE_DOUBLES = QR_NB * QR_XLD;  // one staged tile (32 rows × 128 columns)
 constexpr double QR_RANK_RTOL = 1e-14;    // RANK_DEFICIENCY_RTOL, linalg.py:48
 constexpr double QR_FAST_DIAG_RATIO = 1e-4;  // min/max diag(R₁) accepted by the fast path
 constexpr int QR_NSMALL = 12;             // 32×32 scratch matrices in shared memory
@@ -395,43 +399,25 @@ __device__ __forceinline__ void qr_load_chunk_vform(const QrArgs& p, const QrSme
   }
 }
 
-// Gram partial accumulation over chunk rows: thread (rg = t/64, blk = t%64)
-// owns a 4×4 block of the 32×32 Gram for rows ≡ rg (mod 4).
-__device__ __forceinline__ void qr_gram_accum(const QrSmem& s, int rows, double (&acc)[4][4]) {
-  const int tid = threadIdx.x;
-  const int rg = tid >> 6, blk = tid & 63;
-  const int ab = (blk >> 3) << 2, bb = (blk & 7) << 2;
-  for (int rr = rg; rr < rows; rr += QR_RG) {
-    const double* row = s.Ps + rr * QR_PLD;
-    double pa[4], pb[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      pa[u] = row[ab + u];
-      pb[u] = row[bb + u];
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fma(pa[a], pb[b], acc[a][b]);
+// Gram partial PᵀP (32×32) over chunk rows on the FP64 tensor pipe: warp w
+// owns the 8×8 tile (w/4, w%4) and accumulates it over all rows (k = rows).
+__device__ __forceinline__ void qr_gram_mma(const QrSmem& s, int rows, double (&acc)[2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mi = (warp >> 2) * 8, ni = (warp & 3) * 8;
+  for (int k0 = 0; k0 < rows; k0 += 4) {
+    const int r = k0 + t;
+    const double a = (r < rows) ? s.Ps[r * QR_PLD + mi + g] : 0.0;
+    const double b = (r < rows) ? s.Ps[r * QR_PLD + ni + g] : 0.0;
+    dmma884(acc[0], acc[1], a, b);
   }
 }
-// Combine the 4 row-group partials (fixed order) and publish to dst (global).
-__device__ __forceinline__ void qr_gram_publish(const QrSmem& s, double (&acc)[4][4], double* dst) {
-  const int tid = threadIdx.x;
-  const int rg = tid >> 6, blk = tid & 63;
-  const int ab = (blk >> 3) << 2, bb = (blk & 7) << 2;
-  __syncthreads();
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) s.stage[rg * 1024 + (ab + a) * 32 + bb + b] = acc[a][b];
-  __syncthreads();
-  for (int e = tid; e < 1024; e += QR_THREADS) {
-    double v = s.stage[e];
-#pragma unroll
-    for (int g = 1; g < QR_RG; ++g) v += s.stage[g * 1024 + e];
-    __stcg(dst + e, v);
-  }
+__device__ __forceinline__ void qr_gram_store(const double (&acc)[2], double* dst) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mi = (warp >> 2) * 8, ni = (warp & 3) * 8;
+  __stcg(dst + (mi + g) * 32 + ni + 2 * t, acc[0]);
+  __stcg(dst + (mi + g) * 32 + ni + 2 * t + 1, acc[1]);
 }
 
 // Slice reduction of the Gram partials (1024 entries) into p.gfin.
@@ -445,63 +431,72 @@ __device__ void qr_gram_reduce(const QrArgs& p, double* red) {
       [=](int e, double v) { __stcg(out + e0 + e, v); }, red);
 }
 
-// Chunk rows × W (32×32, smem) in place: Ps[rr][:] ← Ps[rr][:]·W.  Thread
-// (rb = t/8, cb = t%8) computes 4 rows × 4 columns per 128-row block.
-__device__ __forceinline__ void qr_rows_times(const QrSmem& s, int rows, const double* W) {
-  const int tid = threadIdx.x;
-  const int rb = (tid >> 3) << 2, cb = (tid & 7) << 2;
-  for (int b0 = 0; b0 < rows; b0 += QR_THREADS / 2) {
-    double acc[4][4];
+// out[r][c] = init(r, c) + sign·Σ_k Ps[r][k]·W[k][c] for the chunk rows
+// r < rows and c < 32, on the FP64 tensor pipe.  Warp w owns rows
+// b0 + 8w .. +8 of each 128-row block and all 32 columns (4 DMMA tiles); it
+// reads only its own Ps rows, so writing back in place needs just a warp
+// barrier.  Sink(rr, c, v0, v1) receives columns c, c+1 of row rr.
+template <class Init, class Sink>
+__device__ __forceinline__ void qr_rows_mma(const QrSmem& s, int rows, const double* W, double sign, Init init,
+                                            Sink sink) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  for (int b0 = 0; b0 < rows; b0 += 8 * (QR_THREADS / 32)) {
+    const int r = b0 + warp * 8 + g;  // this lane's output row
+    if (b0 + warp * 8 >= rows) continue;
+    double acc[4][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    const bool any = b0 + rb < rows;
-    if (any) {
-#pragma unroll 8
-      for (int q = 0; q < QR_NB; ++q) {
-        double x[4], w[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) x[a] = (b0 + rb + a < rows) ? s.Ps[(b0 + rb + a) * QR_PLD + q] : 0.0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) w[b] = W[q * QR_SLD + cb + b];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], w[b], acc[a][b]);
-      }
+    for (int nt = 0; nt < 4; ++nt) {
+      acc[nt][0] = init(r, nt * 8 + 2 * t);
+      acc[nt][1] = init(r, nt * 8 + 2 * t + 1);
     }
-    __syncthreads();
-    if (any) {
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-        if (b0 + rb + a < rows)
+    for (int k0 = 0; k0 < QR_NB; k0 += 4) {
+      const double a = (r < rows) ? sign * s.Ps[r * QR_PLD + k0 + t] : 0.0;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) s.Ps[(b0 + rb + a) * QR_PLD + cb + b] = acc[a][b];
+      for (int nt = 0; nt < 4; ++nt) dmma884(acc[nt][0], acc[nt][1], a, W[(k0 + t) * QR_SLD + nt * 8 + g]);
     }
-    __syncthreads();
+    __syncwarp();
+    if (r < rows) {
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) sink(r, nt * 8 + 2 * t, acc[nt][0], acc[nt][1]);
+    }
   }
+  __syncthreads();
+}
+
+// Chunk rows × W (32×32, smem) in place: Ps[rr][:] ← Ps[rr][:]·W.
+__device__ __forceinline__ void qr_rows_times(const QrSmem& s, int rows, const double* W) {
+  double* Ps = s.Ps;
+  qr_rows_mma(
+      s, rows, W, 1.0, [](int, int) { return 0.0; },
+      [=](int r, int c, double v0, double v1) {
+        Ps[r * QR_PLD + c] = v0;
+        Ps[r * QR_PLD + c + 1] = v1;
+      });
 }
 
 // ====================== trailing update (GEMM-shaped) =======================
 // Accumulate this chunk's contribution to the W partial of columns
-// [col0, col0+ntr):  W[i][c] += Σ_rr V[rr][i]·X[row][c].  The W partial lives
-// in the CTA's wpart slot (first chunk writes, later chunks accumulate).
-// X tiles (32 rows × 128 columns) stream through a double-buffered cp.async
-// ring; thread (ib, cb) owns 4 i × 4 strided columns.
+// [col0, col0+ntr):  W[i][c] += Σ_rr V[rr][i]·X[row][c] on the FP64 tensor
+// pipe.  X tiles (32 rows × 128 columns) stream through a double-buffered
+// cp.async ring; warp w owns i-tile w%4 and column tiles 4·(w/4)..+4 of each
+// 128-column chunk.  The W partial lives in the CTA's wpart slot (first chunk
+// writes, later chunks accumulate).
 __device__ void qr_wpartial_chunk(const QrArgs& p, const QrSmem& s, long cs, long ce, long col0, long ntr,
                                   bool first) {
   const int tid = threadIdx.x;
-  constexpr int CB = QR_CW / 4;  // 32
-  const int ib = tid / CB, cb = tid % CB;  // i rows ib·IPT .. +IPT
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mi = (warp & 3) * 8, nt0 = (warp >> 2) * 4;
   const long ldw = qr_ldw(p.n);
   double* wdst = p.wpart + size_t(blockIdx.x) * QR_NB * ldw;
   const int nrows = int(ce - cs);
   const int nrc = (nrows + QR_NB - 1) / QR_NB;
   for (long c0 = 0; c0 < ntr; c0 += QR_CW) {
-    auto load = [&](int t, int buf) {
+    auto load = [&](int tt, int buf) {
       double* dst = s.stage + buf * QR_TILE_DOUBLES;
-      const long rc = cs + long(t) * QR_NB;
+      const long rc = cs + long(tt) * QR_NB;
       for (int e = tid; e < QR_NB * QR_CW / 2; e += QR_THREADS) {
         const int rr = e / (QR_CW / 2), cc = (e % (QR_CW / 2)) * 2;
         const long c = c0 + cc;
@@ -511,49 +506,42 @@ __device__ void qr_wpartial_chunk(const QrArgs& p, const QrSmem& s, long cs, lon
           bytes = int(lmin(2, ntr - c)) * 8;
           src = p.A + (rc + rr) * p.lda + col0 + c;
         }
-        cp_async16(dst + rr * QR_CW + cc, src, bytes);
+        cp_async16(dst + rr * QR_XLD + cc, src, bytes);
       }
       cp_async_commit();
     };
-    double acc[QR_IPT][4];
+    double acc[4][2];
 #pragma unroll
-    for (int a = 0; a < QR_IPT; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
     if (nrc > 0) load(0, 0);
-    for (int t = 0; t < nrc; ++t) {
-      if (t + 1 < nrc) {
-        load(t + 1, (t + 1) & 1);
+    for (int tt = 0; tt < nrc; ++tt) {
+      if (tt + 1 < nrc) {
+        load(tt + 1, (tt + 1) & 1);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncthreads();
-      const double* tile = s.stage + (t & 1) * QR_TILE_DOUBLES;
-      const int rows = min(QR_NB, nrows - t * QR_NB);
-      for (int rr = 0; rr < rows; ++rr) {
-        const double* vrow = s.Ps + (t * QR_NB + rr) * QR_PLD + ib * QR_IPT;
-        const double* xrow = tile + rr * QR_CW + cb;
-        double v[QR_IPT], x[4];
+      const double* tile = s.stage + (tt & 1) * QR_TILE_DOUBLES;
+      const int rbase = tt * QR_NB;
 #pragma unroll
-        for (int a = 0; a < QR_IPT; ++a) v[a] = vrow[a];
+      for (int k0 = 0; k0 < QR_NB; k0 += 4) {
+        const int rr = rbase + k0 + t;
+        const double a = (rr < nrows) ? s.Ps[rr * QR_PLD + mi + g] : 0.0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) x[b] = xrow[b * CB];
-#pragma unroll
-        for (int a = 0; a < QR_IPT; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(v[a], x[b], acc[a][b]);
+        for (int nt = 0; nt < 4; ++nt)
+          dmma884(acc[nt][0], acc[nt][1], a, tile[(k0 + t) * QR_XLD + (nt0 + nt) * 8 + g]);
       }
       __syncthreads();
     }
 #pragma unroll
-    for (int a = 0; a < QR_IPT; ++a)
+    for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const long c = c0 + cb + b * CB;
+      for (int e = 0; e < 2; ++e) {
+        const long c = c0 + (nt0 + nt) * 8 + 2 * t + e;
         if (c < ntr) {
-          double* w = wdst + size_t(ib * QR_IPT + a) * ldw + c;
-          __stcg(w, first ? acc[a][b] : acc[a][b] + __ldcg(w));
+          double* w = wdst + size_t(mi + g) * ldw + c;
+          __stcg(w, first ? acc[nt][e] : acc[nt][e] + __ldcg(w));
         }
       }
   }
@@ -586,11 +574,16 @@ __device__ void qr_reduce_slice(const QrArgs& p, const QrSmem& s, const double* 
   }
 }
 
-// Row-local update of this chunk: X[row][c] -= Σ_i V[rr][i]·Y[i][c].
+// Row-local update of this chunk: X[row][c] -= Σ_i V[rr][i]·Y[i][c], on the
+// FP64 tensor pipe.  Y (32 × 128 chunk) is staged in shared memory; warp w
+// owns row tile w%4 and column tiles 4·(w/4)..+4 of each 32-row block; the
+// accumulators start from X (read straight into fragment layout) and the A
+// fragments carry −V.
 __device__ void qr_update_chunk(const QrArgs& p, const QrSmem& s, long cs, long ce, long col0, long ntr) {
   const int tid = threadIdx.x;
-  constexpr int CB = QR_CW / 4;
-  const int rb = tid / CB, cb = tid % CB;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mi = (warp & 3) * 8, nt0 = (warp >> 2) * 4;
   const int nrows = int(ce - cs);
   for (long c0 = 0; c0 < ntr; c0 += QR_CW) {
     __syncthreads();
@@ -598,44 +591,41 @@ __device__ void qr_update_chunk(const QrArgs& p, const QrSmem& s, long cs, long 
       const int i = e / (QR_CW / 2), cc = (e % (QR_CW / 2)) * 2;
       const long c = c0 + cc;
       const int bytes = (c < ntr) ? int(lmin(2, ntr - c)) * 8 : 0;
-      cp_async16(s.stage + i * QR_CW + cc, bytes ? p.ybuf + size_t(i) * qr_ldy(p.n) + c : p.ybuf, bytes);
+      cp_async16(s.stage + i * QR_XLD + cc, bytes ? p.ybuf + size_t(i) * qr_ldy(p.n) + c : p.ybuf, bytes);
     }
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     for (int rc = 0; rc < nrows; rc += QR_NB) {
-      double acc[QR_IPT][4];
-      bool ok[QR_IPT];
+      const int rr = rc + mi + g;  // this lane's row (chunk-relative)
+      const bool rok = rr < nrows;
+      double* xrow = p.A + (cs + rr) * p.lda + col0;
+      double acc[4][2];
 #pragma unroll
-      for (int a = 0; a < QR_IPT; ++a) {
-        const int rr = rc + rb * QR_IPT + a;
-        ok[a] = rr < nrows;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const long c = c0 + cb + b * CB;
-          acc[a][b] = (ok[a] && c < ntr) ? p.A[(cs + rr) * p.lda + col0 + c] : 0.0;
+      for (int nt = 0; nt < 4; ++nt) {
+        const long c = c0 + (nt0 + nt) * 8 + 2 * t;
+        if (rok && c + 1 < ntr) {
+          const double2 v = *reinterpret_cast<const double2*>(xrow + c);
+          acc[nt][0] = v.x;
+          acc[nt][1] = v.y;
+        } else {
+          acc[nt][0] = (rok && c < ntr) ? xrow[c] : 0.0;
+          acc[nt][1] = 0.0;
         }
       }
-#pragma unroll 4
-      for (int i = 0; i < QR_NB; ++i) {
-        double y[4], v[QR_IPT];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) y[b] = s.stage[i * QR_CW + cb + b * CB];
+      for (int k0 = 0; k0 < QR_NB; k0 += 4) {
+        const double a = rok ? -s.Ps[rr * QR_PLD + k0 + t] : 0.0;
 #pragma unroll
-        for (int a = 0; a < QR_IPT; ++a) v[a] = ok[a] ? s.Ps[(rc + rb * QR_IPT + a) * QR_PLD + i] : 0.0;
-#pragma unroll
-        for (int a = 0; a < QR_IPT; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(-v[a], y[b], acc[a][b]);
+        for (int nt = 0; nt < 4; ++nt)
+          dmma884(acc[nt][0], acc[nt][1], a, s.stage[(k0 + t) * QR_XLD + (nt0 + nt) * 8 + g]);
       }
+      if (rok) {
 #pragma unroll
-      for (int a = 0; a < QR_IPT; ++a) {
-        if (!ok[a]) continue;
-        const long r = cs + rc + rb * QR_IPT + a;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const long c = c0 + cb + b * CB;
-          if (c < ntr) p.A[r * p.lda + col0 + c] = acc[a][b];
+        for (int nt = 0; nt < 4; ++nt) {
+          const long c = c0 + (nt0 + nt) * 8 + 2 * t;
+          if (c + 1 < ntr) *reinterpret_cast<double2*>(xrow + c) = make_double2(acc[nt][0], acc[nt][1]);
+          else if (c < ntr) xrow[c] = acc[nt][0];
         }
       }
     }
@@ -784,23 +774,19 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
     bool fast = false;
     if (jb == QR_NB) {
       // ---- pass 1: Gram partial (+ publish the pivot rows)
-      double acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      double acc[2] = {0.0, 0.0};
       for (long cs = ra; cs < r1; cs += rch) {
         const long ce = lmin(r1, cs + rch);
         qr_load_chunk(p, s, cs, ce, k);
         __syncthreads();
-        qr_gram_accum(s, int(ce - cs), acc);
+        qr_gram_mma(s, int(ce - cs), acc);
         for (int e = tid; e < int(lmin(ce, k + QR_NB) - cs) * QR_NB; e += QR_THREADS) {
           const int rr = e >> 5, c = e & 31;
           __stcg(p.pivbuf + (cs + rr - k) * 32 + c, s.Ps[rr * QR_PLD + c]);
         }
         if (!resident) __syncthreads();
       }
-      qr_gram_publish(s, acc, gdst);
+      qr_gram_store(acc, gdst);
       grid_barrier(p.counter, gen);
       QR_PHASE(0);
       qr_gram_reduce(p, s.small);
@@ -816,10 +802,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
       if (fast) {
         sm_tri_inv_upper<false, false>(R1i, R1, Z);
         // ---- pass 2: Q₁ = P·R₁⁻¹ (rows in place) + Gram of Q₁
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        acc[0] = acc[1] = 0.0;
         for (long cs = ra; cs < r1; cs += rch) {
           const long ce = lmin(r1, cs + rch);
           if (!resident) {
@@ -827,14 +810,14 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
             __syncthreads();
           }
           qr_rows_times(s, int(ce - cs), R1i);
-          qr_gram_accum(s, int(ce - cs), acc);
+          qr_gram_mma(s, int(ce - cs), acc);
           if (!resident) {
             __syncthreads();
             qr_store_chunk(p, s, cs, ce, k);
             __syncthreads();
           }
         }
-        qr_gram_publish(s, acc, gdst);
+        qr_gram_store(acc, gdst);
         grid_barrier(p.counter, gen);
         qr_gram_reduce(p, s.small);
         grid_barrier(p.counter, gen);
@@ -1080,17 +1063,15 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
         qr_load_chunk_vform(p, s, cs, ce, k, jb);
         __syncthreads();
       }
-      for (int e = tid; e < int(ce - cs) * QR_NB; e += QR_THREADS) {
-        const int rr = e >> 5, c = e & 31;
-        if (c >= jb) continue;
-        const long r = cs + rr;
-        const double* vrow = s.Ps + rr * QR_PLD;
-        double acc = (r == k + c) ? 1.0 : 0.0;
-#pragma unroll 8
-        for (int i = 0; i < QR_NB; ++i) acc = fma(-vrow[i], Lt[i * QR_SLD + c], acc);
-        p.A[r * p.lda + k + c] = acc;
-      }
-      __syncthreads();
+      double* Acol = p.A + k;
+      const long lda = p.lda;
+      qr_rows_mma(
+          s, int(ce - cs), Lt, -1.0, [=](int rr, int c) { return (cs + rr == k + c) ? 1.0 : 0.0; },
+          [=](int rr, int c, double v0, double v1) {
+            double* dst = Acol + (cs + rr) * lda + c;
+            if (c < jb) dst[0] = v0;
+            if (c + 1 < jb) dst[1] = v1;
+          });
     }
     QR_PHASE(11);
   }

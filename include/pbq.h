@@ -91,8 +91,10 @@ int pbq_qr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes);
  * [row_offset, row_offset+rows) of the same global rows×... matrix whose
  * column count is `cols` (row-sharded multi-GPU generation). */
 int pbq_gaussian(pbq_ctx* ctx, int64_t rows, int64_t cols, int64_t row_offset, uint64_t seed_lo,
-                 uint64_t seed_hi, double* out, int64_t ldo, void* workspace,
+                 uint64_t seed_hi, double* out, int64_t ldo, int32_t* status, void* workspace,
                  size_t workspace_bytes, void* stream);
+/* `status` (device int, may be NULL) is OR-ed with a nonzero code if the
+ * generator's internal bounds were exceeded (never observed; checked). */
 int pbq_gaussian_workspace_bytes(pbq_ctx* ctx, int64_t rows, int64_t cols, int64_t row_offset,
                                  size_t* bytes);
 
@@ -106,6 +108,12 @@ typedef struct {
   uint64_t seed_lo, seed_hi;
   int32_t reorthonormalize;
   int32_t check_finite;
+  /* Optional n2×d AᵀΦ computed by the caller (row stride ldc_init), e.g.
+   * accumulated chunk by chunk while A streams in from the host.  When set,
+   * the pipeline skips the sketch and the first pass; `phi` must then hold
+   * the sketch used (it is not regenerated). */
+  const double* c_init;
+  int64_t ldc_init;
 } pbq_problem;
 
 typedef struct {
@@ -143,9 +151,10 @@ int pbq_profile_begin(pbq_ctx* ctx, int32_t capacity);
 int pbq_profile_end(pbq_ctx* ctx, double* ms_by_class, int32_t* launches_by_class);
 
 /* Profiling hooks (device pointers, NULL to disable): number of QR panels
- * that took the column-by-column fallback, and CTA-0 nanoseconds per QR
- * phase (12 slots, see qr_f64.cuh). */
-int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns);
+ * that took the column-by-column fallback, CTA-0 nanoseconds per QR phase
+ * (16 slots, see qr_f64.cuh), and per-CTA nanoseconds spent spinning in the
+ * QR kernel's grid barriers (one slot per CTA, ≥ SM count). */
+int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns, uint64_t* bar_wait_ns);
 
 #ifdef __cplusplus
 }

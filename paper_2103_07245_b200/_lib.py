@@ -59,6 +59,7 @@ class PbqProblem(ctypes.Structure):
         ("phi", c_p), ("ldphi", c_i64),
         ("seed_lo", c_u64), ("seed_hi", c_u64),
         ("reorthonormalize", c_i32), ("check_finite", c_i32),
+        ("c_init", c_p), ("ldc_init", c_i64),
     ]
 
 
@@ -87,12 +88,12 @@ _SIGS = {
     "pbq_gemm_workspace_bytes": ([c_p, c_i64, c_i64, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_householder_qr": ([c_p, c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_i32, c_p, c_p, c_sz, c_p], ctypes.c_int),
     "pbq_qr_workspace_bytes": ([c_p, c_i64, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),
-    "pbq_gaussian": ([c_p, c_i64, c_i64, c_i64, c_u64, c_u64, c_p, c_i64, c_p, c_sz, c_p], ctypes.c_int),
+    "pbq_gaussian": ([c_p, c_i64, c_i64, c_i64, c_u64, c_u64, c_p, c_i64, c_p, c_p, c_sz, c_p], ctypes.c_int),
     "pbq_gaussian_workspace_bytes": ([c_p, c_i64, c_i64, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_pbp_qlp_workspace_bytes": ([c_p, ctypes.POINTER(PbqProblem), ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_pbp_qlp": ([c_p, ctypes.POINTER(PbqProblem), ctypes.POINTER(PbqOutputs), c_p, c_sz, c_p], ctypes.c_int),
     "pbq_transpose": ([c_p, c_i64, c_p, c_i64, c_p, c_i64, c_i32, c_p], ctypes.c_int),
-    "pbq_debug_qr_hooks": ([c_p, c_p, c_p], ctypes.c_int),
+    "pbq_debug_qr_hooks": ([c_p, c_p, c_p, c_p], ctypes.c_int),
     "pbq_profile_begin": ([c_p, c_i32], ctypes.c_int),
     "pbq_profile_end": ([c_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)], ctypes.c_int),
 }

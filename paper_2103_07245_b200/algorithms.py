@@ -148,7 +148,7 @@ class PbpQlpPlan:
         self.L = _dev.empty_matrix(d, d, dev)
         self.R = _dev.empty_matrix(d, d, dev)
         self.PHI = None if explicit_phi else _dev.empty_matrix(n1, d, dev)
-        self.flags = torch.zeros(2 * q + 2, dtype=torch.int32, device=dev)  # [status, rank flags...]
+        self.flags = torch.zeros(2 * q + 2, dtype=torch.int32, device=dev)  # [status bits, rank flags...]
         self.prob = _lib.PbqProblem()
         self.prob.n1, self.prob.n2, self.prob.d, self.prob.q = n1, n2, d, q
         self.prob.reorthonormalize = 1 if reorthonormalize else 0
@@ -173,6 +173,55 @@ class PbpQlpPlan:
         self.seed = 0
         self.phi_in = None
 
+    def run_streamed(self, host, seed=0, chunks=16):
+        """Factor a host (CPU) float64 tensor, streaming it to the device in
+        row chunks on a copy stream while the first pass C = AᵀΦ accumulates
+        chunk by chunk on the compute stream (β = 1 GEMM updates); the rest of
+        the pipeline starts from that C.  Returns the device copy of A."""
+        dev = self.device
+        if tuple(host.shape) != (self.n1, self.n2):
+            raise _exc.DimensionError(f"plan is for {(self.n1, self.n2)}, got {tuple(host.shape)}")
+        seed = check_seed(seed)
+        self.seed = seed
+        if self.PHI is None:
+            raise _exc.ParameterError("plan was built for an explicit sketch")
+        if getattr(self, "A_dev", None) is None:
+            self.A_dev = _dev.empty_matrix(self.n1, self.n2, dev)
+            self.C0 = _dev.empty_matrix(self.n2, self.d, dev)
+            self.copy_stream = torch.cuda.Stream(dev)
+        A, C0 = self.A_dev, self.C0
+        compute = torch.cuda.current_stream(dev)
+        self.copy_stream.wait_stream(compute)  # A may still be read by a previous call
+        self.flags.zero_()
+        self.sk_status = getattr(self, "sk_status", None)
+        if self.sk_status is None:
+            self.sk_status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.sk_status.zero_()
+        _dev.gaussian(self.ctx, self.n1, self.d, seed, dev, out=self.PHI, status=self.sk_status)
+        nchunks = max(1, min(int(chunks), self.n1 // max(self.d, 1)))
+        bounds = [(self.n1 * i) // nchunks for i in range(nchunks + 1)]
+        for i in range(nchunks):
+            r0, r1 = bounds[i], bounds[i + 1]
+            with torch.cuda.stream(self.copy_stream):
+                A[r0:r1].copy_(host[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.copy_stream)
+            compute.wait_event(ev)
+            _dev.gemm(self.ctx, A[r0:r1], self.PHI[r0:r1], trans_a=True, out=C0, beta=0.0 if i == 0 else 1.0,
+                      nonfinite=self.flags[0:1])
+        self.prob.c_init, self.prob.ldc_init = C0.data_ptr(), C0.stride(0)
+        self.prob.phi, self.prob.ldphi = self.PHI.data_ptr(), self.PHI.stride(0)
+        self.prob.a, self.prob.lda = A.data_ptr(), A.stride(0)
+        self.prob.seed_lo, self.prob.seed_hi = seed & ((1 << 64) - 1), seed >> 64
+        self.phi_in = None
+        with self.ctx.lock:
+            st = self.ctx.lib.pbq_pbp_qlp(self.ctx.handle, ctypes.byref(self.prob), ctypes.byref(self.out),
+                                          _dev.ptr(self.ws), self.ws_bytes, _dev.stream_ptr(dev))
+            self.ctx.check(st, "pbp_qlp")
+        self.prob.c_init, self.prob.ldc_init = None, 0
+        self._streamed = True
+        return A
+
     def run(self, A, seed=0, phi=None):
         """Enqueue one factorization of the kernel-ready device matrix ``A``."""
         if tuple(A.shape) != (self.n1, self.n2):
@@ -190,6 +239,7 @@ class PbpQlpPlan:
                 raise _exc.ParameterError("plan was built for an explicit sketch; pass phi")
             self.prob.phi, self.prob.ldphi = None, 0
         self.phi_in = phi
+        self._streamed = False
         with self.ctx.lock:
             st = self.ctx.lib.pbq_pbp_qlp(self.ctx.handle, ctypes.byref(self.prob), ctypes.byref(self.out),
                                           _dev.ptr(self.ws), self.ws_bytes, _dev.stream_ptr(self.device))
@@ -197,6 +247,8 @@ class PbpQlpPlan:
 
     def finish(self, stacklevel=3):
         fl = self.flags.cpu().tolist()  # the one device→host synchronisation
+        if getattr(self, "_streamed", False) and int(self.sk_status.item()):
+            fl[0] |= 2
         if fl[0] & 1:
             raise _exc.MatrixInputError("a contains non-finite entries")
         if fl[0] & 2:
@@ -204,6 +256,20 @@ class PbpQlpPlan:
         for flag in fl[1:]:
             warn_rank(flag, stacklevel=stacklevel + 1)
         return fl
+
+
+#: host inputs at least this large stream to the GPU in row chunks overlapped
+#: with the first pass (PbpQlpPlan.run_streamed)
+STREAM_MIN_BYTES = 64 << 20
+
+
+def _to_host(t, kind, home):
+    """Device result → caller type, through a pinned buffer for host callers."""
+    if kind == "torch" and home is not None and torch.device(home).type == "cuda":
+        return from_device(t, kind, home)
+    buf = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    buf.copy_(t, non_blocking=True)
+    return buf
 
 
 def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, *, phi=None, device=None):
@@ -214,6 +280,8 @@ def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, *, phi=None, device=None):
     ``phi`` supplies the sketch explicitly (oracle mode, n1×d); ``device``
     picks the GPU for array-like inputs.  numpy/array-like input returns numpy
     factors; a torch tensor returns torch tensors on the tensor's home device.
+    Large host inputs are streamed to the GPU in row chunks while the first
+    pass over A runs (PbpQlpPlan.run_streamed).
     """
     ha = HostMatrix(a, "a")
     n1, n2 = ha.shape
@@ -226,22 +294,31 @@ def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, *, phi=None, device=None):
         raise
     seed = check_seed(seed)
     kind, home = ha.kind, ha.home
-    A = ha.to_device(device)
-    dev = A.device
-    PHI = None
-    if phi is not None:
-        _, PHI, _, _ = to_device_matrix(phi, "phi", dev)
-    plan = PbpQlpPlan(n1, n2, d, q, reorthonormalize, dev, explicit_phi=phi is not None)
-    plan.run(A, seed, PHI)
-    plan.finish(stacklevel=3)
+    host = ha.host_tensor()
+    streamed = host is not None and phi is None and n1 * n2 * 8 >= STREAM_MIN_BYTES and n1 >= 2 * d
+    if streamed:
+        dev = _dev.require_cuda(device)
+        plan = PbpQlpPlan(n1, n2, d, q, reorthonormalize, dev)
+        plan.run_streamed(host, seed)
+        PHI = None
+    else:
+        A = ha.to_device(device)
+        dev = A.device
+        PHI = None
+        if phi is not None:
+            _, PHI, _, _ = to_device_matrix(phi, "phi", dev)
+        plan = PbpQlpPlan(n1, n2, d, q, reorthonormalize, dev, explicit_phi=phi is not None)
+        plan.run(A, seed, PHI)
+    host_side = not (kind == "torch" and home is not None and torch.device(home).type == "cuda")
+    if host_side:
+        outs = [_to_host(t, kind, home) for t in (plan.Q, plan.L, plan.P, plan.R)]
+    plan.finish(stacklevel=3)  # synchronises the stream (also completes the copies above)
+    if host_side:
+        outs = [o.numpy() if kind == "numpy" else o for o in outs]
+    else:
+        outs = [from_device(t, kind, home) for t in (plan.Q, plan.L, plan.P, plan.R)]
     passes = 2 * q + 2
     sketch = SketchRecord(PHI if PHI is not None else plan.PHI, kind, seed, d, q, passes, home)
     if phi is not None and kind == "numpy":
         sketch._host = np.asarray(phi, dtype=np.float64)
-    return QlpFactors(
-        from_device(plan.Q, kind, home),
-        from_device(plan.L, kind, home),
-        from_device(plan.P, kind, home),
-        from_device(plan.R, kind, home),
-        sketch,
-    )
+    return QlpFactors(outs[0], outs[1], outs[2], outs[3], sketch)

@@ -102,14 +102,22 @@ __device__ __forceinline__ bool nonfinite_bits(double x) {
 // `counter` must be zeroed before the launch; `*generation` counts barriers
 // already passed by this CTA.  All writes made before the barrier by any CTA
 // are visible after it to loads that bypass L1 (ld.global.cg / acquire).
-__device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int& generation) {
+__device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int& generation,
+                                             unsigned long long* wait_ns = nullptr) {
   __threadfence();
   __syncthreads();
   generation += 1;
   if (threadIdx.x == 0) {
+    unsigned long long t0 = 0;
+    if (wait_ns) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
     atom_add_release(counter, 1u);
     const unsigned int target = generation * gridDim.x;
     while (ld_acquire_u32(counter) < target) {
+    }
+    if (wait_ns) {
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+      wait_ns[blockIdx.x] += t1 - t0;  // per-CTA spin time (profiling only)
     }
   }
   __syncthreads();

@@ -33,6 +33,7 @@ struct pbq_ctx {
   int* qr_fallbacks = nullptr;                // profiling hooks (device pointers), off by default
   int* qr_error = nullptr;                    // when set: QR kernels report unsupported panels here
   unsigned long long* qr_phase_ns = nullptr;
+  unsigned long long* qr_bar_wait_ns = nullptr;
   char err[512] = {0};
 };
 
@@ -246,6 +247,7 @@ int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   a.rank_flag = rank_flag;
   a.fallbacks = ctx->qr_fallbacks;
   a.phase_ns = ctx->qr_phase_ns;
+  a.bar_wait_ns = ctx->qr_bar_wait_ns;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
   PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&qr_tall_kernel),
@@ -472,16 +474,17 @@ int pbq_gaussian_workspace_bytes(pbq_ctx* ctx, int64_t rows, int64_t cols, int64
 }
 
 int pbq_gaussian(pbq_ctx* ctx, int64_t rows, int64_t cols, int64_t row_offset, uint64_t seed_lo, uint64_t seed_hi,
-                 double* out, int64_t ldo, void* ws, size_t ws_bytes, void* stream) {
+                 double* out, int64_t ldo, int32_t* status, void* ws, size_t ws_bytes, void* stream) {
   if (!ctx) return PBQ_ERR_PARAM;
-  return sketch_launch(ctx, rows, cols, row_offset, seed_lo, seed_hi, out, ldo, nullptr, ws, ws_bytes,
+  return sketch_launch(ctx, rows, cols, row_offset, seed_lo, seed_hi, out, ldo, status, ws, ws_bytes,
                        static_cast<cudaStream_t>(stream));
 }
 
-int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns) {
+int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns, uint64_t* bar_wait_ns) {
   if (!ctx) return PBQ_ERR_PARAM;
   ctx->qr_fallbacks = fallbacks;
   ctx->qr_phase_ns = reinterpret_cast<unsigned long long*>(phase_ns);
+  ctx->qr_bar_wait_ns = reinterpret_cast<unsigned long long*>(bar_wait_ns);
   return PBQ_OK;
 }
 
@@ -501,7 +504,7 @@ static int pipeline_sizes(pbq_ctx* ctx, const pbq_problem* pr, size_t* total, si
   PBQ_TRY(pbq_qr_workspace_bytes(ctx, n2, d, &q1));
   PBQ_TRY(pbq_qr_workspace_bytes(ctx, n1, d, &q2));
   PBQ_TRY(pbq_qr_workspace_bytes(ctx, d, d, &q3));
-  if (!pr->phi) PBQ_TRY(pbq_gaussian_workspace_bytes(ctx, n1, d, 0, &s1));
+  if (!pr->phi && !pr->c_init) PBQ_TRY(pbq_gaussian_workspace_bytes(ctx, n1, d, 0, &s1));
   const size_t sc = std::max({g1, g2, g3, q1, q2, q3, s1});
   const long ld = thin_ld(d);
   *scratch = sc;
@@ -525,7 +528,8 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   if (q < 0) return fail(ctx, PBQ_ERR_DIM, "q must be >= 0, got %ld", q);
   if (!pr->a || !o->q || !o->l || !o->p || !o->r || !o->rank_flags || !o->nonfinite)
     return fail(ctx, PBQ_ERR_PARAM, "null pointer argument");
-  if (!pr->phi && !o->phi) return fail(ctx, PBQ_ERR_PARAM, "seeded mode needs an output buffer for the sketch");
+  if (!pr->phi && !o->phi && !pr->c_init)
+    return fail(ctx, PBQ_ERR_PARAM, "seeded mode needs an output buffer for the sketch");
   size_t total, scratch;
   PBQ_TRY(pipeline_sizes(ctx, pr, &total, &scratch));
   if (ws_bytes < total) return fail(ctx, PBQ_ERR_PARAM, "pbp_qlp: workspace too small (%zu < %zu)", ws_bytes, total);
@@ -538,19 +542,25 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   void* sc = cv.take<char>(scratch);
   const int32_t check = pr->check_finite ? 1 : 0;
 
-  PBQ_CUDA(ctx, cudaMemsetAsync(o->nonfinite, 0, sizeof(int32_t), st));
+  if (!pr->c_init) PBQ_CUDA(ctx, cudaMemsetAsync(o->nonfinite, 0, sizeof(int32_t), st));
   PBQ_CUDA(ctx, cudaMemsetAsync(o->rank_flags, 0, sizeof(int32_t) * (2 * q + 1), st));
   const double* phi = pr->phi;
   long ldphi = pr->ldphi;
-  if (!phi) {
-    PBQ_CUDA(ctx, cudaMemsetAsync(sk_err, 0, sizeof(int32_t), st));
-    PBQ_TRY(sketch_launch(ctx, n1, d, 0, pr->seed_lo, pr->seed_hi, o->phi, o->ldphi, sk_err, sc, scratch, st));
-    phi = o->phi;
-    ldphi = o->ldphi;
+  if (pr->c_init) {
+    // pass 1 done by the caller (streamed from the host): C = c_init
+    PBQ_CUDA(ctx, cudaMemcpy2DAsync(cbuf, ld * sizeof(double), pr->c_init, pr->ldc_init * sizeof(double),
+                                    d * sizeof(double), n2, cudaMemcpyDeviceToDevice, st));
+  } else {
+    if (!phi) {
+      PBQ_CUDA(ctx, cudaMemsetAsync(sk_err, 0, sizeof(int32_t), st));
+      PBQ_TRY(sketch_launch(ctx, n1, d, 0, pr->seed_lo, pr->seed_hi, o->phi, o->ldphi, sk_err, sc, scratch, st));
+      phi = o->phi;
+      ldphi = o->ldphi;
+    }
+    // pass 1: C = Aᵀ Φ  (+ fused isfinite scan of A)
+    PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, phi, ldphi, 0.0, cbuf, ld,
+                              check ? o->nonfinite : nullptr, sc, scratch, st));
   }
-  // pass 1: C = Aᵀ Φ  (+ fused isfinite scan of A)
-  PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, phi, ldphi, 0.0, cbuf, ld,
-                            check ? o->nonfinite : nullptr, sc, scratch, st));
   int site = 0;
   double* dbuf = o->q;  // n1×d scratch for A·P̄, finally D itself
   const long ldq = o->ldq;
@@ -577,7 +587,7 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   PBQ_TRY(qr_launch(ctx, d, d, wbuf, ld, rt, ld, 1, nullptr, sc, scratch, st));
   PBQ_TRY(transpose_launch(ctx, d, rt, ld, o->l, o->ldl, 1, st));
   PBQ_TRY(gemm_launch<false>(ctx, n2, d, d, 1.0, cbuf, ld, wbuf, ld, 0.0, o->p, o->ldp, nullptr, sc, scratch, st));
-  if (!pr->phi) {
+  if (!pr->phi && !pr->c_init) {
     // fold a sketch-generator overflow into bit 1 of the status word so the
     // host reads one int
     merge_flag_kernel<<<1, 1, 0, st>>>(o->nonfinite, sk_err);

@@ -73,6 +73,7 @@ struct QrArgs {
   int* fallbacks;  // may be null: number of panels that took the fallback
   int* error;      // may be null: set to 1 if a fallback panel met non-resident rows
   unsigned long long* phase_ns;  // may be null: CTA-0 time per phase (profiling)
+  unsigned long long* bar_wait_ns;  // may be null: per-CTA grid-barrier spin time (profiling)
 };
 
 __device__ __forceinline__ unsigned long long qr_now() {
@@ -678,7 +679,7 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
       __stcg(p.part + (size_t(buf) * G + blockIdx.x) * 32 + tid, acc);
       if (piv >= ra && piv < r1) __stcg(p.pivrow + buf * 32 + tid, s.Ps[(piv - ra) * QR_PLD + tid]);
     }
-    grid_barrier(p.counter, gen);
+    grid_barrier(p.counter, gen, p.bar_wait_ns);
     {
       const double* base = p.part + size_t(buf) * G * 32;
       qr_reduce_entries(
@@ -787,10 +788,10 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
         if (!resident) __syncthreads();
       }
       qr_gram_store(acc, gdst);
-      grid_barrier(p.counter, gen);
+      grid_barrier(p.counter, gen, p.bar_wait_ns);
       QR_PHASE(0);
       qr_gram_reduce(p, s.small);
-      grid_barrier(p.counter, gen);
+      grid_barrier(p.counter, gen, p.bar_wait_ns);
       for (int e = tid; e < 1024; e += QR_THREADS) {
         R1[(e >> 5) * QR_SLD + (e & 31)] = __ldcg(p.gfin + e);
         Pp[(e >> 5) * QR_SLD + (e & 31)] = __ldcg(p.pivbuf + e);
@@ -818,9 +819,9 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
           }
         }
         qr_gram_store(acc, gdst);
-        grid_barrier(p.counter, gen);
+        grid_barrier(p.counter, gen, p.bar_wait_ns);
         qr_gram_reduce(p, s.small);
-        grid_barrier(p.counter, gen);
+        grid_barrier(p.counter, gen, p.bar_wait_ns);
         for (int e = tid; e < 1024; e += QR_THREADS) Z[(e >> 5) * QR_SLD + (e & 31)] = __ldcg(p.gfin + e);
         __syncthreads();
         QR_PHASE(2);
@@ -958,10 +959,10 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
         double* wdst = p.wpart + size_t(blockIdx.x) * QR_NB * qr_ldw(n);
         for (long e = tid; e < QR_NB * ntr; e += QR_THREADS) __stcg(wdst + (e / ntr) * qr_ldw(n) + e % ntr, 0.0);
       }
-      grid_barrier(p.counter, gen);
+      grid_barrier(p.counter, gen, p.bar_wait_ns);
       QR_PHASE(6);
       qr_reduce_slice(p, s, Ts, ntr, /*trans_t=*/true);
-      grid_barrier(p.counter, gen);
+      grid_barrier(p.counter, gen, p.bar_wait_ns);
       QR_PHASE(7);
       for (long cs = ra; cs < r1; cs += rch) {
         const long ce = lmin(r1, cs + rch);
@@ -1005,7 +1006,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
   }
   // every CTA's factored panels (V₁ blocks, T factors) are published before
   // any CTA starts reading them
-  grid_barrier(p.counter, gen);
+  grid_barrier(p.counter, gen, p.bar_wait_ns);
   QR_PHASE(9);
 
   // ===================== Q formation (dorgqr, backward) =====================
@@ -1038,9 +1039,9 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
         double* wdst = p.wpart + size_t(blockIdx.x) * QR_NB * qr_ldw(n);
         for (long e = tid; e < QR_NB * ntr; e += QR_THREADS) __stcg(wdst + (e / ntr) * qr_ldw(n) + e % ntr, 0.0);
       }
-      grid_barrier(p.counter, gen);
+      grid_barrier(p.counter, gen, p.bar_wait_ns);
       qr_reduce_slice(p, s, Ts, ntr, /*trans_t=*/false);
-      grid_barrier(p.counter, gen);
+      grid_barrier(p.counter, gen, p.bar_wait_ns);
       QR_PHASE(10);
       for (long cs = ra; cs < r1; cs += rch) {
         const long ce = lmin(r1, cs + rch);
@@ -1052,7 +1053,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
         qr_update_chunk(p, s, cs, ce, k + jb, ntr);
       }
     } else {
-      grid_barrier(p.counter, gen);  // every CTA has read V₁ before it is overwritten
+      grid_barrier(p.counter, gen, p.bar_wait_ns);  // every CTA has read V₁ before it is overwritten
     }
     // M1 = T·V₁ᵀ; panel columns Q[r][k+c] = δ(r, k+c) − Σ_i V[r][i]·M1[i][c]
     sm_mm<false, true>(Lt, Ts, LU);

@@ -161,7 +161,9 @@ def householder_qr_(ctx, a, r=None, want_q=True, rank_flag=None):
     return a, r
 
 
-def gaussian(ctx, rows, cols, seed, device, row_offset=0, out=None):
+def gaussian(ctx, rows, cols, seed, device, row_offset=0, out=None, status=None):
+    """Enqueue the sketch; ``status`` (int32 device tensor) receives the
+    generator's overflow flag (callers check it when they synchronise)."""
     if out is None:
         out = empty_matrix(rows, cols, device)
     nbytes = ctypes.c_size_t()
@@ -170,7 +172,7 @@ def gaussian(ctx, rows, cols, seed, device, row_offset=0, out=None):
                   "gaussian workspace")
         ws = workspace(nbytes.value, device)
         st = ctx.lib.pbq_gaussian(ctx.handle, rows, cols, row_offset, seed & ((1 << 64) - 1), seed >> 64, ptr(out),
-                                  ld_of(out), ptr(ws), nbytes.value, stream_ptr(device))
+                                  ld_of(out), ptr(status), ptr(ws), nbytes.value, stream_ptr(device))
         ctx.check(st, "gaussian")
     return out
 

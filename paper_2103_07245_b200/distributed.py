@@ -49,8 +49,8 @@ class CudaBackend:
     def zeros_i32(self, n):
         return torch.zeros(n, dtype=torch.int32, device=self.device)
 
-    def gaussian(self, rows, cols, seed, row_offset):
-        return _dev.gaussian(self.ctx, rows, cols, seed, self.device, row_offset=row_offset)
+    def gaussian(self, rows, cols, seed, row_offset, status=None):
+        return _dev.gaussian(self.ctx, rows, cols, seed, self.device, row_offset=row_offset, status=status)
 
     def gemm_tn(self, a, x, out, nonfinite=None):
         return _dev.gemm(self.ctx, a, x, trans_a=True, out=out, nonfinite=nonfinite)
@@ -99,7 +99,7 @@ class DistributedPbpQlp:
         self.L = be.empty(self.d, self.d)
         self.P = be.empty(self.n2, self.d)
         self.Qtmp = be.empty(self.m, self.d)
-        self.flags = be.zeros_i32(2 * self.q + 2)  # [non-finite, rank flags …]
+        self.flags = be.zeros_i32(2 * self.q + 3)  # [non-finite, sketch status, rank flags …]
         self.PHI = None
 
     # -- collectives ---------------------------------------------------------
@@ -136,10 +136,10 @@ class DistributedPbpQlp:
         self.flags.zero_()
         flags = self.flags
         if phi_local is None:
-            self.PHI = be.gaussian(self.m, d, seed, self.rows[self.rank])
+            self.PHI = be.gaussian(self.m, d, seed, self.rows[self.rank], status=flags[1:2])
         else:
             self.PHI = be.contiguous(phi_local)
-        site = 1
+        site = 2
         be.gemm_tn(A_local, self.PHI, self.C, nonfinite=flags[0:1])
         self._allreduce(self.C)
         if self.reorthonormalize:
@@ -169,11 +169,13 @@ class DistributedPbpQlp:
     def finish(self, stacklevel=3):
         """Synchronise, raise / warn like the reference (every rank)."""
         # a non-finite entry in any shard fails every rank
-        dist.all_reduce(self.flags[0:1], op=dist.ReduceOp.MAX, group=self.group)
+        dist.all_reduce(self.flags[0:2], op=dist.ReduceOp.MAX, group=self.group)
         fl = self.flags.cpu().tolist()
         if fl[0]:
             raise _exc.MatrixInputError("a contains non-finite entries")
-        for f in fl[1:]:
+        if fl[1]:
+            raise _exc.DeviceError("sketch generator overflow (internal error)")
+        for f in fl[2:]:
             warn_rank(f, stacklevel=stacklevel + 1)
         return fl
 

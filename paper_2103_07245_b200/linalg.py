@@ -61,6 +61,17 @@ class HostMatrix:
             self.kind, self.tensor, self.array, self.home = "numpy", None, coerce_host_matrix(m, name), None
         self.shape = tuple(self.tensor.shape if self.tensor is not None else self.array.shape)
 
+    def host_tensor(self):
+        """CPU float64 contiguous torch view/copy of a host input, else None."""
+        if self.array is not None:
+            return torch.from_numpy(np.ascontiguousarray(self.array))
+        t = self.tensor
+        if t.is_cuda:
+            return None
+        if t.dtype != torch.float64:
+            t = t.to(torch.float64)
+        return t.contiguous()
+
     def all_finite(self):
         if self.array is not None:
             return bool(np.isfinite(self.array).all())
@@ -112,7 +123,10 @@ def gaussian_matrix(rows, cols, seed=0, *, device=None, as_tensor=False, row_off
     seed = check_seed(seed)
     dev = _dev.require_cuda(device)
     ctx = _dev.context(dev)
-    out = _dev.gaussian(ctx, rows, cols, seed, dev, row_offset=int(row_offset))
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = _dev.gaussian(ctx, rows, cols, seed, dev, row_offset=int(row_offset), status=status)
+    if int(status.item()):
+        raise _exc.DeviceError("sketch generator overflow (internal error)")
     return out if as_tensor else from_device(out, "numpy")
 
 

@@ -16,7 +16,7 @@ class NumpyBackend:
     def zeros_i32(self, n):
         return torch.zeros(n, dtype=torch.int32)
 
-    def gaussian(self, rows, cols, seed, row_offset):
+    def gaussian(self, rows, cols, seed, row_offset, status=None):
         return torch.from_numpy(c_gaussian(rows, cols, seed, row_offset=row_offset))
 
     def gemm_tn(self, a, x, out, nonfinite=None):

@@ -200,3 +200,26 @@ def test_distributed_driver_on_one_gpu(cuda):
         assert np.allclose(np.diag(l), np.diag(ref.l), rtol=1e-10, atol=0)
     finally:
         dist.destroy_process_group()
+
+
+def test_streamed_host_path_matches_oracle(cuda, monkeypatch):
+    """Host inputs above STREAM_MIN_BYTES stream to the device in row chunks
+    overlapped with the first pass; force it on a small case (pinned torch
+    and numpy inputs) and check parity with the oracle."""
+    from paper_2103_07245_b200 import algorithms
+
+    monkeypatch.setattr(algorithms, "STREAM_MIN_BYTES", 0)
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((1500, 50)) @ rng.standard_normal((50, 700)) / 7 + 1e-3 * rng.standard_normal((1500, 700))
+    got_np, ref = _check_against_oracle(a, 40, 1, 21)
+    assert isinstance(got_np.q_basis, np.ndarray)
+    ta = torch.from_numpy(a).pin_memory()
+    got_t = algorithms.pbp_qlp(ta, 40, q=1, seed=21)
+    assert isinstance(got_t.q_basis, torch.Tensor) and not got_t.q_basis.is_cuda
+    assert np.array_equal(got_t.l.numpy(), got_np.l)
+    bad = a.copy()
+    bad[1499, 3] = np.inf
+    from paper_2103_07245_b200 import MatrixInputError
+
+    with pytest.raises(MatrixInputError):
+        algorithms.pbp_qlp(bad, 40, q=1)

@@ -38,14 +38,21 @@ if os.environ.get("QR_PHASES"):
              "reduce+bar", "update", "R/zero+bar", "orgqr W+bars", "orgqr update+gen", "chol2", "Qp", "LU", "T+M1"]
     fb = torch.zeros(1, dtype=torch.int32, device=dev)
     ph = torch.zeros(16, dtype=torch.int64, device=dev)
-    ctx.lib.pbq_debug_qr_hooks(ctx.handle, ctypes.c_void_p(fb.data_ptr()), ctypes.c_void_p(ph.data_ptr()))
+    bw = torch.zeros(1024, dtype=torch.int64, device=dev)
+    ctx.lib.pbq_debug_qr_hooks(ctx.handle, ctypes.c_void_p(fb.data_ptr()), ctypes.c_void_p(ph.data_ptr()),
+                               ctypes.c_void_p(bw.data_ptr()))
     for m, n in shapes:
         x = D.empty_matrix(m, n, dev)
         x.normal_()
         ph.zero_()
+        bw.zero_()
         D.householder_qr_(ctx, x, D.empty_matrix(n, n, dev))
         torch.cuda.synchronize()
+        w = bw[:148].double() / 1e3
+        nz = w[w > 0]
+        print(f"  barrier spin per CTA (us): min {nz.min():.1f} median {nz.median():.1f} max {nz.max():.1f} "
+              f"argmin {int(torch.argmin(torch.where(w > 0, w, torch.full_like(w, 1e18))))}")
         tot = ph.sum().item()
         print(f"{m}x{n}: fallbacks={fb.item()} total {tot/1e3:.1f} us: " +
               ", ".join(f"{nm}={v/1e3:.1f}" for nm, v in zip(names, ph.tolist()) if v))
-    ctx.lib.pbq_debug_qr_hooks(ctx.handle, None, None)
+    ctx.lib.pbq_debug_qr_hooks(ctx.handle, None, None, None)

@@ -84,7 +84,7 @@ __device__ __forceinline__ unsigned long long qr_now() {
 // accumulate elapsed time since the previous mark into slot `ph` (CTA 0, thread 0)
 #define QR_PHASE(ph)                                          \
   do {                                                       \
-    if (p.phase_ns && blockIdx.x == 0 && threadIdx.x == 0) { \
+    if (p.phase_ns && blockIdx.x == gridDim.x / 2 && threadIdx.x == 0) { \
       const unsigned long long now_ = qr_now();              \
       p.phase_ns[ph] += now_ - t_phase;                      \
       t_phase = now_;                                        \
@@ -155,21 +155,24 @@ __device__ __forceinline__ void qr_reduce_entries(int E, int G, size_t stride, A
 // All routines run on the whole CTA; thread t owns row t/8, columns
 // 4·(t%8)..+3 of the 32×32 result.  Matrices live in shared memory, ld 33.
 
-// C = op(A)·op(B) (opX = transpose when TX); C must not alias A or B.
+// C = op(A)·op(B) (opX = transpose when TX); C must not alias A or B.  One
+// 8×8 DMMA tile per warp (16 warps = 4×4 tiles), 8 k-steps; the ld-36 layout
+// keeps both fragment orientations conflict-free.
 template <bool TA, bool TB>
 __device__ __forceinline__ void sm_mm(double* C, const double* A, const double* B) {
-  const int i = threadIdx.x / QR_TPR, c0 = (threadIdx.x % QR_TPR) * QR_EPT;
-  double acc[QR_EPT];
+  static_assert(QR_THREADS == 512, "one 8x8 tile per warp");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mi = (warp >> 2) * 8, ni = (warp & 3) * 8;
+  double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-  for (int u = 0; u < QR_EPT; ++u) acc[u] = 0.0;
-#pragma unroll
-  for (int q = 0; q < QR_NB; ++q) {
-    const double a = TA ? A[q * QR_SLD + i] : A[i * QR_SLD + q];
-#pragma unroll
-    for (int u = 0; u < QR_EPT; ++u) acc[u] = fma(a, TB ? B[(c0 + u) * QR_SLD + q] : B[q * QR_SLD + c0 + u], acc[u]);
+  for (int k0 = 0; k0 < QR_NB; k0 += 4) {
+    const double a = TA ? A[(k0 + t) * QR_SLD + mi + g] : A[(mi + g) * QR_SLD + k0 + t];
+    const double b = TB ? B[(ni + g) * QR_SLD + k0 + t] : B[(k0 + t) * QR_SLD + ni + g];
+    dmma884(c0, c1, a, b);
   }
-#pragma unroll
-  for (int u = 0; u < QR_EPT; ++u) C[i * QR_SLD + c0 + u] = acc[u];
+  C[(mi + g) * QR_SLD + ni + 2 * t] = c0;
+  C[(mi + g) * QR_SLD + ni + 2 * t + 1] = c1;
   __syncthreads();
 }
 
@@ -486,6 +489,9 @@ __device__ __forceinline__ void qr_rows_times(const QrSmem& s, int rows, const d
 // writes, later chunks accumulate).
 __device__ void qr_wpartial_chunk(const QrArgs& p, const QrSmem& s, long cs, long ce, long col0, long ntr,
                                   bool first) {
+  constexpr int TR = QR_NB / 2;     // rows per staged tile
+  constexpr int NST = 4;            // ring depth (same shared memory as 2 × 32 rows)
+  constexpr int TD = TR * QR_XLD;   // doubles per tile
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -493,12 +499,12 @@ __device__ void qr_wpartial_chunk(const QrArgs& p, const QrSmem& s, long cs, lon
   const long ldw = qr_ldw(p.n);
   double* wdst = p.wpart + size_t(blockIdx.x) * QR_NB * ldw;
   const int nrows = int(ce - cs);
-  const int nrc = (nrows + QR_NB - 1) / QR_NB;
+  const int nrc = (nrows + TR - 1) / TR;
   for (long c0 = 0; c0 < ntr; c0 += QR_CW) {
-    auto load = [&](int tt, int buf) {
-      double* dst = s.stage + buf * QR_TILE_DOUBLES;
-      const long rc = cs + long(tt) * QR_NB;
-      for (int e = tid; e < QR_NB * QR_CW / 2; e += QR_THREADS) {
+    auto load = [&](int tt) {
+      double* dst = s.stage + (tt % NST) * TD;
+      const long rc = cs + long(tt) * TR;
+      for (int e = tid; e < TR * QR_CW / 2; e += QR_THREADS) {
         const int rr = e / (QR_CW / 2), cc = (e % (QR_CW / 2)) * 2;
         const long c = c0 + cc;
         int bytes = 0;
@@ -509,32 +515,33 @@ __device__ void qr_wpartial_chunk(const QrArgs& p, const QrSmem& s, long cs, lon
         }
         cp_async16(dst + rr * QR_XLD + cc, src, bytes);
       }
-      cp_async_commit();
     };
     double acc[4][2];
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-    if (nrc > 0) load(0, 0);
-    for (int tt = 0; tt < nrc; ++tt) {
-      if (tt + 1 < nrc) {
-        load(tt + 1, (tt + 1) & 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncthreads();
-      const double* tile = s.stage + (tt & 1) * QR_TILE_DOUBLES;
-      const int rbase = tt * QR_NB;
 #pragma unroll
-      for (int k0 = 0; k0 < QR_NB; k0 += 4) {
+    for (int tt = 0; tt < NST - 1; ++tt) {
+      if (tt < nrc) load(tt);
+      cp_async_commit();
+    }
+    for (int tt = 0; tt < nrc; ++tt) {
+      cp_async_wait<NST - 2>();
+      __syncthreads();
+      if (tt + NST - 1 < nrc) load(tt + NST - 1);
+      cp_async_commit();
+      const double* tile = s.stage + (tt % NST) * TD;
+      const int rbase = tt * TR;
+#pragma unroll
+      for (int k0 = 0; k0 < TR; k0 += 4) {
         const int rr = rbase + k0 + t;
         const double a = (rr < nrows) ? s.Ps[rr * QR_PLD + mi + g] : 0.0;
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
           dmma884(acc[nt][0], acc[nt][1], a, tile[(k0 + t) * QR_XLD + (nt0 + nt) * 8 + g]);
       }
-      __syncthreads();
     }
+    cp_async_wait<0>();
+    __syncthreads();
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -597,6 +604,25 @@ __device__ void qr_update_chunk(const QrArgs& p, const QrSmem& s, long cs, long 
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
+    auto load_x = [&](int rc, double (&x)[4][2]) {
+      const int rr = rc + mi + g;
+      const bool rok = rr < nrows;
+      const double* xrow = p.A + (cs + rr) * p.lda + col0;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const long c = c0 + (nt0 + nt) * 8 + 2 * t;
+        if (rok && c + 1 < ntr) {
+          const double2 v = *reinterpret_cast<const double2*>(xrow + c);
+          x[nt][0] = v.x;
+          x[nt][1] = v.y;
+        } else {
+          x[nt][0] = (rok && c < ntr) ? xrow[c] : 0.0;
+          x[nt][1] = 0.0;
+        }
+      }
+    };
+    double nxt[4][2];
+    if (nrows > 0) load_x(0, nxt);
     for (int rc = 0; rc < nrows; rc += QR_NB) {
       const int rr = rc + mi + g;  // this lane's row (chunk-relative)
       const bool rok = rr < nrows;
@@ -604,16 +630,10 @@ __device__ void qr_update_chunk(const QrArgs& p, const QrSmem& s, long cs, long 
       double acc[4][2];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
-        const long c = c0 + (nt0 + nt) * 8 + 2 * t;
-        if (rok && c + 1 < ntr) {
-          const double2 v = *reinterpret_cast<const double2*>(xrow + c);
-          acc[nt][0] = v.x;
-          acc[nt][1] = v.y;
-        } else {
-          acc[nt][0] = (rok && c < ntr) ? xrow[c] : 0.0;
-          acc[nt][1] = 0.0;
-        }
+        acc[nt][0] = nxt[nt][0];
+        acc[nt][1] = nxt[nt][1];
       }
+      if (rc + QR_NB < nrows) load_x(rc + QR_NB, nxt);  // prefetch the next row block
 #pragma unroll
       for (int k0 = 0; k0 < QR_NB; k0 += 4) {
         const double a = rok ? -s.Ps[rr * QR_PLD + k0 + t] : 0.0;
@@ -764,7 +784,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
   double* svec = s.small + QR_THREADS + 128;  // 32: S signs
   unsigned int gen = 0;
   int nfallback = 0;
-  unsigned long long t_phase = (p.phase_ns && blockIdx.x == 0 && tid == 0) ? qr_now() : 0;
+  unsigned long long t_phase = (p.phase_ns && blockIdx.x == gridDim.x / 2 && tid == 0) ? qr_now() : 0;
   const bool resident = p.rows_per_cta <= rch;  // same for every CTA (barrier counts must agree)
 
   // ===================== factorization (dgeqrf) =====================
@@ -1024,6 +1044,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
       Ts[a * QR_SLD + c] = __ldcg(p.tall + pidx * 1024 + e);
     }
     __syncthreads();
+    QR_PHASE(16);
     const long ntr = n - k - jb;
     if (ntr > 0) {
       bool first = true;
@@ -1032,6 +1053,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
         __syncthreads();
         qr_load_chunk_vform(p, s, cs, ce, k, jb);
         __syncthreads();
+        QR_PHASE(17);
         qr_wpartial_chunk(p, s, cs, ce, k + jb, ntr, first);
         first = false;
       }
@@ -1039,8 +1061,11 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
         double* wdst = p.wpart + size_t(blockIdx.x) * QR_NB * qr_ldw(n);
         for (long e = tid; e < QR_NB * ntr; e += QR_THREADS) __stcg(wdst + (e / ntr) * qr_ldw(n) + e % ntr, 0.0);
       }
+      QR_PHASE(18);
       grid_barrier(p.counter, gen, p.bar_wait_ns);
+      QR_PHASE(19);
       qr_reduce_slice(p, s, Ts, ntr, /*trans_t=*/false);
+      QR_PHASE(20);
       grid_barrier(p.counter, gen, p.bar_wait_ns);
       QR_PHASE(10);
       for (long cs = ra; cs < r1; cs += rch) {

@@ -35,9 +35,9 @@ for m, n in shapes:
 if os.environ.get("QR_PHASES"):
     import ctypes
     names = ["gram1+bar", "reduce1+chol1", "pass2+gram2+bars", "chol2+small", "pass3", "fallback", "wpartial+bar",
-             "reduce+bar", "update", "R/zero+bar", "orgqr W+bars", "orgqr update+gen", "chol2", "Qp", "LU", "T+M1"]
+             "reduce+bar", "update", "R/zero+bar", "orgqr W+bars", "orgqr update+gen", "chol2", "Qp", "LU", "T+M1", "oq:V1T", "oq:vform", "oq:wpart", "oq:bar1", "oq:reduce"]
     fb = torch.zeros(1, dtype=torch.int32, device=dev)
-    ph = torch.zeros(16, dtype=torch.int64, device=dev)
+    ph = torch.zeros(24, dtype=torch.int64, device=dev)
     bw = torch.zeros(1024, dtype=torch.int64, device=dev)
     ctx.lib.pbq_debug_qr_hooks(ctx.handle, ctypes.c_void_p(fb.data_ptr()), ctypes.c_void_p(ph.data_ptr()),
                                ctypes.c_void_p(bw.data_ptr()))

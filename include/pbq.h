@@ -77,7 +77,11 @@ int pbq_gemm_workspace_bytes(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, size
  * On return A (if want_q) holds the thin Q, R (if non-null) the n×n upper
  * triangular factor with diag(R) ≥ 0 and exact zeros below the diagonal.
  * If rank_flag is non-null it receives the `orth` rank test
- * (linalg.py:142-165): 0 full rank, 1 some |R_ii| < 1e-14·|R_00|, 2 R_00 == 0. */
+ * (linalg.py:142-165): 0 full rank, 1 some |R_ii| < 1e-14·|R_00|, 2 R_00 == 0.
+ * Method (pbq_set_qr_method): by default a guarded whole-matrix Cholesky-QR2
+ * (same unique factors for full-rank A, to rounding) that hands the call to
+ * the blocked Householder kernel on the device whenever κ₁(R₁) > 1e6 or a
+ * pivot fails; method 1 forces the Householder kernel. */
 int pbq_householder_qr(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, double* R,
                        int64_t ldr, int32_t want_q, int32_t* rank_flag, void* workspace,
                        size_t workspace_bytes, void* stream);
@@ -155,6 +159,20 @@ int pbq_profile_end(pbq_ctx* ctx, double* ms_by_class, int32_t* launches_by_clas
  * (16 slots, see qr_f64.cuh), and per-CTA nanoseconds spent spinning in the
  * QR kernel's grid barriers (one slot per CTA, ≥ SM count). */
 int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns, uint64_t* bar_wait_ns);
+
+/* QR method for every later call on this context: 0 auto (Cholesky-QR2 with
+ * on-device Householder fallback, the default), 1 Householder only, 2 auto
+ * but with the blocked Cholesky (not the near-identity series) in the second
+ * pass (a test hook for that safety path). */
+#define PBQ_QR_AUTO 0
+#define PBQ_QR_HOUSEHOLDER 1
+#define PBQ_QR_CHOLQR_NOSERIES 2
+int pbq_set_qr_method(pbq_ctx* ctx, int32_t method);
+
+/* Debug counters (device int[3], NULL to disable): QR calls completed by
+ * Cholesky-QR2, calls handed to the Householder fallback, and completed
+ * calls whose second pass used the near-identity series. */
+int pbq_debug_cholqr_stats(pbq_ctx* ctx, int32_t* stats);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,8 @@ EXPORTED = (
     "pbq_debug_qr_hooks",
     "pbq_profile_begin",
     "pbq_profile_end",
+    "pbq_set_qr_method",
+    "pbq_debug_cholqr_stats",
 )
 
 c_i64 = ctypes.c_int64
@@ -96,6 +98,8 @@ _SIGS = {
     "pbq_debug_qr_hooks": ([c_p, c_p, c_p, c_p], ctypes.c_int),
     "pbq_profile_begin": ([c_p, c_i32], ctypes.c_int),
     "pbq_profile_end": ([c_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)], ctypes.c_int),
+    "pbq_set_qr_method": ([c_p, c_i32], ctypes.c_int),
+    "pbq_debug_cholqr_stats": ([c_p, c_p], ctypes.c_int),
 }
 
 _lib = None

@@ -8,7 +8,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpbq.so")
 SOURCES = ["pbq_api.cu"]
-HEADERS = ["common.cuh", "gemm_f64.cuh", "qr_f64.cuh", "sketch.cuh", "ziggurat_tables.h"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -93,6 +93,17 @@ __device__ __forceinline__ double fast_rcp(double d) {
   return fma(r, e, r);
 }
 
+// 1/sqrt(d) for finite d > 0: rsqrt.approx (MUFU) + two Newton steps.
+__device__ __forceinline__ double fast_rsqrt(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double h = 0.5 * d;
+  double e = fma(-h * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+
 // True when the IEEE-754 binary64 exponent field is all ones (Inf or NaN).
 __device__ __forceinline__ bool nonfinite_bits(double x) {
   return ((__double_as_longlong(x) >> 52) & 0x7ff) == 0x7ff;
@@ -121,6 +132,16 @@ __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int
     }
   }
   __syncthreads();
+}
+
+// (tm, tn) of the t-th tile with tm <= tn in row-major order
+__device__ __forceinline__ void upper_tile(int t, int tiles, int& tm, int& tn) {
+  tm = 0;
+  while (t >= tiles - tm) {
+    t -= tiles - tm;
+    ++tm;
+  }
+  tn = tm + t;
 }
 
 __host__ __device__ constexpr long ceil_div(long a, long b) { return (a + b - 1) / b; }

@@ -39,7 +39,18 @@ struct GemmArgs {
   double* partials;  // grid × (BM·BN) doubles
   int* flags;        // grid ints, zeroed before the launch
   int* nonfinite;    // CHECK only: OR-flag set if any element of A is Inf/NaN
+  // SPLIT mode (Gram matrices of the Cholesky-QR path): unit u = (tile u/split,
+  // k-slice u%split) writes its partial tile to partials[u] (plain row-major
+  // BM×BN); `sym` enumerates only tiles with tm <= tn (requires BM == BN or a
+  // single tile).  A separate kernel sums the slices in fixed order.
+  int split, sym, units;
+  const int* skip;   // when non-null and *skip != 0 the launch is a no-op
+  // tri_b: B is upper triangular (K == N), so output column tile tn only
+  // needs k < (tn+1)·BN — the stream-K space then has row_iters =
+  // Σ_tn k-blocks(tn) iterations per row of tiles (total_iters = tiles_m·row_iters)
+  int tri_b, row_iters;
 };
+
 
 template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES>
 struct GemmCfg {
@@ -72,9 +83,10 @@ struct GemmCfg {
   static_assert((BK * B_ROWW) % THREADS == 0 && THREADS % B_ROWW == 0, "B loader geometry");
 };
 
-template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES, bool CHECK>
+template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES, bool CHECK, bool SPLIT = false>
 __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::THREADS, 1)
     gemm_f64_streamk(GemmArgs p) {
+  if (p.skip && __ldcg(p.skip) != 0) return;
   using Cfg = GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>;
   constexpr int THREADS = Cfg::THREADS;
   constexpr int MT = Cfg::MT, NT = Cfg::NT;
@@ -98,13 +110,52 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
 
   long it = long(blockIdx.x) * p.total_iters / G;
   const long it_end = long(blockIdx.x + 1) * p.total_iters / G;
+  int unit = blockIdx.x;
   bool saw_nonfinite = false;
 
-  while (it < it_end) {
-    const int tile = int(it / p.k_iters);
-    const int kb = int(it % p.k_iters);
-    const int ke = int(lmin(p.k_iters, kb + (it_end - it)));
-    const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
+  for (;;) {
+    int tile, kb, ke, tm, tn;
+    int tile_k = p.k_iters;  // k-blocks of this tile
+    long tile_it0 = 0;       // stream-K index of this tile's k=0 block
+    if (SPLIT) {
+      if (unit >= p.units) break;
+      const int tsel = unit / p.split, s = unit % p.split;
+      if (p.sym) {
+        upper_tile(tsel, p.tiles_n, tm, tn);
+      } else {
+        tm = tsel / p.tiles_n;
+        tn = tsel % p.tiles_n;
+      }
+      tile = tsel;
+      kb = int(long(s) * p.k_iters / p.split);
+      ke = int(long(s + 1) * p.k_iters / p.split);
+    } else {
+      if (it >= it_end) break;
+      if (p.tri_b) {
+        tm = int(it / p.row_iters);
+        int rem = int(it % p.row_iters);
+        tn = 0;
+        for (;;) {
+          const int kt = int(lmin(p.k_iters, long(tn + 1) * BN / BK));
+          if (rem < kt) {
+            tile_k = kt;
+            break;
+          }
+          rem -= kt;
+          ++tn;
+        }
+        kb = rem;
+        tile = tm * p.tiles_n + tn;
+      } else {
+        tile = int(it / p.k_iters);
+        kb = int(it % p.k_iters);
+        tm = tile / p.tiles_n;
+        tn = tile % p.tiles_n;
+        tile_k = p.k_iters;
+      }
+      tile_it0 = it - kb;
+      ke = int(lmin(tile_k, kb + (it_end - it)));
+    }
     const long m0 = long(tm) * BM, n0 = long(tn) * BN;
     const bool check = CHECK && (tn == 0);
 
@@ -215,8 +266,20 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
     cp_async_wait<0>();
     __syncthreads();  // ring buffer is reused by the next tile
 
+    if (SPLIT) {
+      // partial tile of this (tile, k-slice) unit, plain row-major layout
+      double* slot = p.partials + size_t(unit) * (BM * BN);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          __stcg(reinterpret_cast<double2*>(slot + (wm0 + mt * 8 + g) * BN + wn0 + nt * 8 + 2 * t),
+                 make_double2(acc[mt][nt][0], acc[mt][nt][1]));
+      unit += G;
+      continue;
+    }
     // ---- stream-K fix-up + epilogue ------------------------------------
-    const bool full = (kb == 0 && ke == p.k_iters);
+    const bool full = (kb == 0 && ke == tile_k);
     if (!full && kb != 0) {
       // contributor: publish the partial tile in fragment-native layout
       double* slot = p.partials + size_t(blockIdx.x) * (BM * BN);
@@ -233,7 +296,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
     } else {
       if (!full) {
         // owner of the k=0 block: add later CTAs' partials in k order
-        const long tile_end = long(tile + 1) * p.k_iters;
+        const long tile_end = tile_it0 + tile_k;
         for (int c = blockIdx.x + 1; c < G; ++c) {
           if (tid == 0) {
             while (ld_acquire(p.flags + c) == 0) {

@@ -11,6 +11,7 @@
 #include "../../include/pbq.h"
 #include "common.cuh"
 #include "gemm_f64.cuh"
+#include "cholqr_f64.cuh"
 #include "qr_f64.cuh"
 #include "sketch.cuh"
 
@@ -21,6 +22,7 @@ struct PbqProfile {
   int cap = 0, used = 0;
   cudaEvent_t* ev = nullptr;  // 2·cap events
   int* cls = nullptr;         // class per pair: 0 GEMM, 1 QR, 2 sketch, 3 other
+  int suppress = 0;           // >0 inside a composite launch timed as one unit
 };
 
 struct pbq_ctx {
@@ -34,6 +36,8 @@ struct pbq_ctx {
   int* qr_error = nullptr;                    // when set: QR kernels report unsupported panels here
   unsigned long long* qr_phase_ns = nullptr;
   unsigned long long* qr_bar_wait_ns = nullptr;
+  int qr_method = PBQ_QR_AUTO;
+  int* cq_stats = nullptr;                    // debug: [Cholesky-QR2 done, fallbacks]
   char err[512] = {0};
 };
 
@@ -74,7 +78,7 @@ struct ProfScope {
   cudaStream_t st;
   int slot = -1;
   ProfScope(PbqProfile& p, cudaStream_t s, int cls) : pr(p), st(s) {
-    if (pr.on && pr.used < pr.cap) {
+    if (pr.on && pr.suppress == 0 && pr.used < pr.cap) {
       slot = pr.used++;
       pr.cls[slot] = cls;
       cudaEventRecord(pr.ev[2 * slot], st);
@@ -83,6 +87,13 @@ struct ProfScope {
   ~ProfScope() {
     if (slot >= 0) cudaEventRecord(pr.ev[2 * slot + 1], st);
   }
+};
+
+// Inner launches of a composite operation are not timed separately.
+struct ProfSuppress {
+  PbqProfile& pr;
+  explicit ProfSuppress(PbqProfile& p) : pr(p) { ++pr.suppress; }
+  ~ProfSuppress() { --pr.suppress; }
 };
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -119,13 +130,14 @@ struct GemmKernel {
 };
 
 struct GemmPlan {
+  int row_iters;
   int bm, bn;
   int tiles_m, tiles_n, k_iters;
   long total;
   int grid;
 };
 
-GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K) {
+GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K, bool tri_b = false) {
   GemmPlan p;
   const int bk = 32;
   if (N <= 64) {
@@ -137,6 +149,11 @@ GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K) {
   p.tiles_n = int(ceil_div(N, p.bn));
   p.k_iters = int(ceil_div(K, bk));
   p.total = long(p.tiles_m) * p.tiles_n * p.k_iters;
+  p.row_iters = 0;
+  if (tri_b) {
+    for (int tn = 0; tn < p.tiles_n; ++tn) p.row_iters += int(std::min<long>(p.k_iters, long(tn + 1) * p.bn / bk));
+    p.total = long(p.tiles_m) * p.row_iters;
+  }
   p.grid = int(std::min<long>(ctx->sms, p.total));
   return p;
 }
@@ -148,14 +165,16 @@ size_t gemm_ws_bytes(const GemmPlan& p) {
 template <bool TRANS>
 int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double* A, long lda, const double* B,
                 long ldb, double beta, double* C, long ldc, int32_t* nonfinite, void* ws, size_t ws_bytes,
-                cudaStream_t st) {
+                cudaStream_t st, const int* skip = nullptr, bool tri_b = false) {
   if (M <= 0 || N <= 0 || K < 0) return fail(ctx, PBQ_ERR_DIM, "gemm: bad shape M=%ld N=%ld K=%ld", M, N, K);
   if ((lda & 1) || (ldb & 1) || (ldc & 1) || !aligned16(A) || !aligned16(B) || !aligned16(C))
     return fail(ctx, PBQ_ERR_PARAM, "gemm: leading dimensions must be even and pointers 16-byte aligned");
   if (K == 0) return fail(ctx, PBQ_ERR_DIM, "gemm: K == 0");
-  const GemmPlan pl = gemm_plan(ctx, M, N, K);
+  if (tri_b && K != N) return fail(ctx, PBQ_ERR_DIM, "gemm: triangular B must be square");
+  const GemmPlan pl = gemm_plan(ctx, M, N, K, tri_b);
   Carve cv(ws, ws_bytes);
   GemmArgs a;
+  memset(&a, 0, sizeof(a));
   a.M = M; a.N = N; a.K = K;
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.C = C; a.ldc = ldc;
   a.alpha = alpha; a.beta = beta;
@@ -163,6 +182,9 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   a.partials = cv.take<double>(size_t(pl.grid) * pl.bm * pl.bn);
   a.flags = cv.take<int>(pl.grid);
   a.nonfinite = nonfinite;
+  a.split = 0; a.sym = 0; a.units = 0;
+  a.skip = skip;
+  a.tri_b = tri_b; a.row_iters = pl.row_iters;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gemm: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
   void* fn;
@@ -225,8 +247,8 @@ size_t qr_ws_bytes(const QrPlan& pl, long n) {
   return b;
 }
 
-int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int want_q, int32_t* rank_flag,
-              void* ws, size_t ws_bytes, cudaStream_t st) {
+int hh_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int want_q, int32_t* rank_flag,
+              void* ws, size_t ws_bytes, cudaStream_t st, const int* run_if) {
   QrPlan pl;
   PBQ_TRY(qr_plan(ctx, m, n, pl));
   if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "qr: leading dimension too small");
@@ -248,6 +270,7 @@ int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   a.fallbacks = ctx->qr_fallbacks;
   a.phase_ns = ctx->qr_phase_ns;
   a.bar_wait_ns = ctx->qr_bar_wait_ns;
+  a.run_if = run_if;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
   PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&qr_tall_kernel),
@@ -258,6 +281,168 @@ int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
                                             dim3(QR_THREADS), args, pl.smem, st));
   ctx->launches += 1;
   return PBQ_OK;
+}
+
+// ------------------------------------------------------- Cholesky-QR2 ----
+// Guarded whole-matrix CholQR2 (cholqr_f64.cuh) + on-device Householder
+// fallback.  Launch sequence on one stream, no host synchronisation:
+//   Gram(A) → reduce → factor pass 1 (R₁, R₁⁻¹, κ guard) → Q₁ = A·R₁⁻¹
+//   → Gram(Q₁) → reduce → factor pass 2 (R₂, R₂⁻¹, R = R₂R₁, rank test)
+//   → A ← Q₁·R₂⁻¹ → Householder kernel (runs only if the guard fired).
+struct CqPlan {
+  int nb;
+  long np;
+  int bm, bn, tiles_m, tiles_n, ntiles, k_iters, S, units;  // Gram GEMM (split-K partials)
+  int grid;                                                // factor kernel CTAs
+  long ldq1;
+  size_t gemm_ws;
+};
+
+constexpr double CQ_KAPPA_MAX = 1e6;
+
+CqPlan cq_plan(const pbq_ctx* ctx, long m, long n) {
+  CqPlan p;
+  p.nb = int(ceil_div(n, 32));
+  p.np = 32L * p.nb;
+  p.bm = 128;
+  p.bn = n <= 64 ? 64 : 128;
+  p.tiles_m = int(ceil_div(n, p.bm));
+  p.tiles_n = int(ceil_div(n, p.bn));
+  p.ntiles = (p.tiles_m == 1 && p.tiles_n == 1) ? 1 : p.tiles_n * (p.tiles_n + 1) / 2;
+  p.k_iters = int(ceil_div(m, 32));
+  p.S = int(std::max<long>(1, std::min<long>(p.k_iters, ctx->sms / p.ntiles)));
+  p.units = p.ntiles * p.S;
+  p.grid = int(std::max<long>(1, std::min<long>(ctx->sms, std::max<long>(long(p.nb) * (p.nb - 1) / 2, p.nb - 1))));
+  p.ldq1 = (n + 1) & ~1L;
+  const size_t gram = align_up(size_t(p.units) * p.bm * p.bn * sizeof(double), 256);
+  p.gemm_ws = std::max(gram, gemm_ws_bytes(gemm_plan(ctx, m, n, n, true)));
+  return p;
+}
+
+size_t cq_ws_bytes(const CqPlan& p, const QrPlan& hp, long m, long n) {
+  const size_t sq = align_up(size_t(p.np) * p.np * sizeof(double), 256);
+  return 256 + 6 * sq + align_up(2 * size_t(p.nb) * p.np * sizeof(double), 256) + align_up(p.gemm_ws, 256) +
+         align_up(size_t(m) * p.ldq1 * sizeof(double), 256) + qr_ws_bytes(hp, n) + 1024;
+}
+
+int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X, long ldx, double* part,
+                const int* skip, cudaStream_t st) {
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = n; a.N = n; a.K = m;
+  a.A = X; a.lda = ldx; a.B = X; a.ldb = ldx;
+  a.alpha = 1.0;
+  a.tiles_m = pl.tiles_m; a.tiles_n = pl.tiles_n; a.k_iters = pl.k_iters;
+  a.partials = part;
+  a.split = pl.S; a.sym = pl.ntiles > 1; a.units = pl.units;
+  a.skip = skip;
+  void* fn;
+  size_t smem;
+  int threads;
+  if (pl.bn == 64) {
+    using C_ = GemmCfg<true, 128, 64, 32, 32, 32, 3>;
+    fn = reinterpret_cast<void*>(&gemm_f64_streamk<true, 128, 64, 32, 32, 32, 3, false, true>);
+    smem = C_::SMEM_BYTES; threads = C_::THREADS;
+  } else {
+    using C_ = GemmCfg<true, 128, 128, 32, 64, 32, 3>;
+    fn = reinterpret_cast<void*>(&gemm_f64_streamk<true, 128, 128, 32, 64, 32, 3, false, true>);
+    smem = C_::SMEM_BYTES; threads = C_::THREADS;
+  }
+  PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  void* args[] = {&a};
+  PBQ_CUDA(ctx, cudaLaunchKernel(fn, dim3(std::min(pl.units, ctx->sms)), dim3(threads), args, smem, st));
+  ctx->launches += 1;
+  const long total = long(pl.ntiles) * pl.bm * pl.bn;
+  (void)total;
+  return PBQ_OK;
+}
+
+int gram_reduce_launch(pbq_ctx* ctx, const CqPlan& pl, long n, const double* part, double* G, const int* skip,
+                       unsigned long long* emax, cudaStream_t st) {
+  const long total = long(pl.ntiles) * pl.bm * pl.bn;
+  const int grid = int(std::min<long>(ceil_div(total, 32), 8L * ctx->sms));
+  cholqr_gram_reduce<<<grid, 256, 0, st>>>(part, pl.S, pl.ntiles, pl.tiles_n, pl.ntiles > 1, pl.bm, pl.bn, n, pl.np,
+                                            G, skip, emax);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
+int factor_launch(pbq_ctx* ctx, const CqPlan& pl, CqArgs& a, cudaStream_t st) {
+  PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&cholqr_factor_kernel),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(CQ_SMEM_BYTES)));
+  void* args[] = {&a};
+  PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&cholqr_factor_kernel), dim3(pl.grid),
+                                            dim3(CQ_THREADS), args, CQ_SMEM_BYTES, st));
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
+int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int32_t* rank_flag, void* ws,
+              size_t ws_bytes, cudaStream_t st) {
+  QrPlan hp;
+  PBQ_TRY(qr_plan(ctx, m, n, hp));
+  if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "qr: leading dimension too small");
+  if ((lda & 1) || !aligned16(A)) return fail(ctx, PBQ_ERR_PARAM, "qr: lda must be even and A 16-byte aligned");
+  const CqPlan pl = cq_plan(ctx, m, n);
+  const size_t sq = size_t(pl.np) * pl.np;
+  Carve cv(ws, ws_bytes);
+  int* ctl = cv.take<int>(64);  // [0] fallback flag, [1] [2] grid-barrier counters, [4:6] max|G₂ − I|
+  double* X1 = cv.take<double>(sq);
+  double* X2 = cv.take<double>(sq);
+  const size_t zero_bytes = size_t(reinterpret_cast<char*>(X2 + sq) - reinterpret_cast<char*>(ctl));
+  double* G = cv.take<double>(sq);
+  double* R1 = cv.take<double>(sq);
+  double* R2 = cv.take<double>(sq);
+  double* T = cv.take<double>(sq);
+  double* colsum = cv.take<double>(2 * size_t(pl.nb) * pl.np);
+  char* gws = cv.take<char>(pl.gemm_ws);
+  double* Q1 = cv.take<double>(size_t(m) * pl.ldq1);
+  const size_t hws_bytes = qr_ws_bytes(hp, n);
+  char* hws = cv.take<char>(hws_bytes);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  int* fallback = ctl;
+  PBQ_CUDA(ctx, cudaMemsetAsync(ctl, 0, zero_bytes, st));
+
+  ProfScope ps(ctx->prof, st, 1);
+  ProfSuppress quiet(ctx->prof);
+  double* part = reinterpret_cast<double*>(gws);
+  CqArgs f;
+  memset(&f, 0, sizeof(f));
+  f.nb = pl.nb; f.n = n; f.np = pl.np;
+  f.G = G; f.T = T; f.fallback = fallback;
+  unsigned long long* emax = reinterpret_cast<unsigned long long*>(ctl + 4);
+  f.emax = emax; f.colsum = colsum; f.stats = ctx->cq_stats; f.kappa_max = CQ_KAPPA_MAX;
+  f.phase_ns = ctx->qr_phase_ns;
+  f.allow_series = ctx->qr_method != PBQ_QR_CHOLQR_NOSERIES;
+  // pass 1
+  PBQ_TRY(gram_launch(ctx, pl, m, n, A, lda, part, fallback, st));
+  PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, nullptr, st));
+  f.pass = 1; f.R = R1; f.X = X1; f.counter = reinterpret_cast<unsigned int*>(ctl + 1);
+  PBQ_TRY(factor_launch(ctx, pl, f, st));
+  PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
+                             fallback, true));
+  // pass 2
+  PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st));
+  PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, emax, st));
+  f.pass = 2; f.R = R2; f.X = X2; f.R1 = R1; f.Rout = R; f.ldr = ldr; f.rank_flag = rank_flag;
+  f.counter = reinterpret_cast<unsigned int*>(ctl + 2);
+  PBQ_TRY(factor_launch(ctx, pl, f, st));
+  PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q1, pl.ldq1, X2, pl.np, 0.0, A, lda, nullptr, gws, pl.gemm_ws, st,
+                             fallback, true));
+  // Householder fallback (returns immediately unless the guard fired)
+  return hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, fallback);
+}
+
+size_t qr_any_ws_bytes(const pbq_ctx* ctx, const QrPlan& hp, long m, long n) {
+  if (ctx->qr_method != PBQ_QR_HOUSEHOLDER) return cq_ws_bytes(cq_plan(ctx, m, n), hp, m, n);
+  return qr_ws_bytes(hp, n);
+}
+
+int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int want_q, int32_t* rank_flag,
+              void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (ctx->qr_method != PBQ_QR_HOUSEHOLDER && want_q) return cq_launch(ctx, m, n, A, lda, R, ldr, rank_flag, ws, ws_bytes, st);
+  return hh_launch(ctx, m, n, A, lda, R, ldr, want_q, rank_flag, ws, ws_bytes, st, nullptr);
 }
 
 // -------------------------------------------------------------- sketch ----
@@ -457,7 +642,7 @@ int pbq_qr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes) {
   if (!ctx || !bytes) return PBQ_ERR_PARAM;
   QrPlan pl;
   PBQ_TRY(qr_plan(ctx, m, n, pl));
-  *bytes = qr_ws_bytes(pl, n);
+  *bytes = qr_any_ws_bytes(ctx, pl, m, n);
   return PBQ_OK;
 }
 
@@ -485,6 +670,20 @@ int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns, uin
   ctx->qr_fallbacks = fallbacks;
   ctx->qr_phase_ns = reinterpret_cast<unsigned long long*>(phase_ns);
   ctx->qr_bar_wait_ns = reinterpret_cast<unsigned long long*>(bar_wait_ns);
+  return PBQ_OK;
+}
+
+int pbq_set_qr_method(pbq_ctx* ctx, int32_t method) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  if (method != PBQ_QR_AUTO && method != PBQ_QR_HOUSEHOLDER && method != PBQ_QR_CHOLQR_NOSERIES)
+    return fail(ctx, PBQ_ERR_PARAM, "unknown QR method %d", method);
+  ctx->qr_method = method;
+  return PBQ_OK;
+}
+
+int pbq_debug_cholqr_stats(pbq_ctx* ctx, int32_t* stats) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  ctx->cq_stats = stats;
   return PBQ_OK;
 }
 

@@ -74,6 +74,7 @@ struct QrArgs {
   int* error;      // may be null: set to 1 if a fallback panel met non-resident rows
   unsigned long long* phase_ns;  // may be null: CTA-0 time per phase (profiling)
   unsigned long long* bar_wait_ns;  // may be null: per-CTA grid-barrier spin time (profiling)
+  const int* run_if;  // may be null; else the kernel runs only when *run_if != 0 (Cholesky-QR fallback)
 };
 
 __device__ __forceinline__ unsigned long long qr_now() {
@@ -751,6 +752,7 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
 // ================================ the kernel ================================
 __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
   extern __shared__ __align__(16) double qsm[];
+  if (p.run_if && __ldcg(p.run_if) == 0) return;  // uniform across the grid
   const long m = p.m, n = p.n;
   const int tid = threadIdx.x;
   const long r0 = long(blockIdx.x) * p.rows_per_cta;

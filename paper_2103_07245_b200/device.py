@@ -41,6 +41,21 @@ class Context:
     def check(self, status, what):
         _lib.raise_status(status, self.handle, what)
 
+    QR_AUTO, QR_HOUSEHOLDER, QR_CHOLQR_NOSERIES = 0, 1, 2
+
+    def set_qr_method(self, method):
+        """0: Cholesky-QR2 with on-device Householder fallback (default);
+        1: Householder kernel only; 2: as 0 with the blocked Cholesky in the
+        second pass (test hook)."""
+        with self.lock:
+            self.check(self.lib.pbq_set_qr_method(self.handle, int(method)), "set_qr_method")
+
+    def cholqr_stats(self, stats):
+        """Count [Cholesky-QR2 completions, Householder fallbacks, series pass 2] into the
+        int32 device tensor ``stats`` (None to stop)."""
+        with self.lock:
+            self.check(self.lib.pbq_debug_cholqr_stats(self.handle, ptr(stats)), "cholqr_stats")
+
     def profile_begin(self, capacity=4096):
         """Start bracketing every kernel this context enqueues with CUDA events."""
         self.check(self.lib.pbq_profile_begin(self.handle, int(capacity)), "profile_begin")

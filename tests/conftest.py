@@ -37,3 +37,15 @@ def reference_pkg():
     import pbpqlp
 
     return pbpqlp
+
+
+@pytest.fixture(params=["auto", "householder"])
+def qr_method(request, cuda):
+    """Run a test under both QR methods: the default guarded Cholesky-QR2
+    (cholqr_f64.cuh) and the blocked Householder kernel (qr_f64.cuh)."""
+    from paper_2103_07245_b200 import device as D
+
+    ctx = D.context(cuda)
+    ctx.set_qr_method(ctx.QR_AUTO if request.param == "auto" else ctx.QR_HOUSEHOLDER)
+    yield request.param
+    ctx.set_qr_method(ctx.QR_AUTO)

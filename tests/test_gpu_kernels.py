@@ -72,8 +72,8 @@ def test_gemm_nonfinite_flag(cuda):
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 5), (40, 40), (64, 33), (1000, 40), (4000, 100), (10000, 256),
-                                 (256, 256), (2500, 301), (700, 1)])
-def test_qr_matches_lapack(cuda, m, n):
+                                 (256, 256), (2500, 301), (700, 1), (3000, 544)])
+def test_qr_matches_lapack(cuda, qr_method, m, n):
     from paper_2103_07245_b200 import device as D
 
     rng = np.random.default_rng(m + 31 * n)
@@ -94,7 +94,7 @@ def test_qr_matches_lapack(cuda, m, n):
     assert np.abs(q.T @ q - np.eye(n)).max() < 1e-13
 
 
-def test_qr_rank_flags(cuda):
+def test_qr_rank_flags(cuda, qr_method):
     from paper_2103_07245_b200 import device as D
 
     ctx = D.context(cuda)
@@ -105,6 +105,64 @@ def test_qr_rank_flags(cuda):
         flag = torch.full((1,), -1, dtype=torch.int32, device=cuda)
         D.householder_qr_(ctx, t, D.empty_matrix(x.shape[1], x.shape[1], cuda), rank_flag=flag)
         assert int(flag.item()) == expect
+
+
+def _cholqr_counts(ctx, cuda, x):
+    from paper_2103_07245_b200 import device as D
+
+    stats = torch.zeros(3, dtype=torch.int32, device=cuda)
+    ctx.cholqr_stats(stats)
+    try:
+        t = _dev_matrix(x, cuda)
+        r = D.empty_matrix(x.shape[1], x.shape[1], cuda)
+        flag = torch.full((1,), -1, dtype=torch.int32, device=cuda)
+        D.householder_qr_(ctx, t, r, rank_flag=flag)
+        return stats.tolist(), t.cpu().numpy(), r.cpu().numpy(), int(flag.item())
+    finally:
+        ctx.cholqr_stats(None)
+
+
+def test_cholqr_path_and_guard(cuda):
+    """The default method completes well-conditioned inputs (κ₁ ≤ 1e6, both
+    the series and the Cholesky variant of pass 2) by Cholesky-QR2 and hands
+    ill-conditioned, rank-deficient and zero inputs to the Householder kernel
+    on the device; either way the factors match LAPACK (linalg.py:106-115)."""
+    from paper_2103_07245_b200 import device as D
+
+    ctx = D.context(cuda)
+    ctx.set_qr_method(ctx.QR_AUTO)
+    rng = np.random.default_rng(5)
+    u, _ = np.linalg.qr(rng.standard_normal((3000, 96)))
+    v, _ = np.linalg.qr(rng.standard_normal((96, 96)))
+    # expected [CholQR2 done, fallbacks, pass 2 by the near-identity series];
+    # method 2 forces the blocked Cholesky in pass 2 (its safety path: the κ₁
+    # guard fires long before G₂ stops being near the identity)
+    cases = [
+        ("gaussian", rng.standard_normal((3000, 96)), [1, 0, 1], 0),
+        ("graded 1e-4", rng.standard_normal((3000, 96)) * np.logspace(0, -4, 96), [1, 0, 1], 0),
+        ("kappa 1e5", (u * np.logspace(0, -5, 96)) @ v.T, [1, 0, 1], 0),
+        ("kappa 1e12", (u * np.logspace(0, -12, 96)) @ v.T, [0, 1, 0], 0),
+        ("rank deficient", np.hstack([u[:, :40], u[:, :40] @ rng.standard_normal((40, 56))]), [0, 1, 0], 0),
+        ("zero", np.zeros((300, 40)), [0, 1, 0], 0),
+        ("gaussian, no series", rng.standard_normal((3000, 96)), [1, 0, 0], 2),
+        ("kappa 1e5, no series", (u * np.logspace(0, -5, 96)) @ v.T, [1, 0, 0], 2),
+        ("300x257, no series", rng.standard_normal((300, 257)), [1, 0, 0], 2),
+    ]
+    for name, x, expect, method in cases:
+        ctx.set_qr_method(method)
+        try:
+            counts, q, r, flag = _cholqr_counts(ctx, cuda, x)
+        finally:
+            ctx.set_qr_method(ctx.QR_AUTO)
+        assert counts == expect, (name, counts)
+        qr_, rr = oracle_qr(x)
+        assert flag == rank_flag(rr), name
+        if rank_flag(rr) == 0:
+            kappa = np.linalg.cond(x)
+            tol = max(1e-11, 64 * 2.0**-53 * kappa)
+            assert column_relative_error(q, qr_).max() < tol, name
+            assert np.abs(q.T @ q - np.eye(x.shape[1])).max() < 1e-13, name
+        assert np.abs(r - rr).max() <= 1e-11 * max(np.abs(rr).max(), 1e-300), name
 
 
 @pytest.mark.parametrize("rows,cols,seed", [(1, 1, 0), (7, 13, 2**100 + 7), (1000, 40, 0), (4000, 100, 1),

@@ -46,7 +46,7 @@ def test_small_seeded(cuda):
 
 
 @pytest.mark.parametrize("q,reorth", [(0, True), (2, True), (0, False), (2, False)])
-def test_low_rank_plus_noise(cuda, q, reorth):
+def test_low_rank_plus_noise(cuda, qr_method, q, reorth):
     rng = np.random.default_rng(7)
     a = rng.standard_normal((800, 30)) @ rng.standard_normal((30, 500)) / 30 + 1e-4 * rng.standard_normal((800, 500))
     # without re-orthonormalization the q=2 sketch squares the spectrum twice:

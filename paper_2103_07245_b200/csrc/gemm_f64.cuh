@@ -343,4 +343,305 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
   if (CHECK && saw_nonfinite) atomicOr(p.nonfinite, 1);
 }
 
+// ---------------------------------------------------------------------------
+// Same contract and schedule as gemm_f64_streamk, with the k-block ring
+// synchronised by mbarriers instead of a CTA barrier per k-block:
+//   full[s]  — expected THREADS arrivals; each thread arrives through
+//              cp.async.mbarrier.arrive.noinc once its copies for the stage
+//              have landed;
+//   empty[s] — expected THREADS arrivals; each thread arrives after its warp
+//              has read the stage.
+// A thread refills stage s (for k-block f + STAGES − 1) only after all warps
+// released it (k-block f − 1), so warps drift up to one stage apart instead of
+// re-aligning at every k-block, and the ring runs on across the CTA's tiles
+// (the next tile's first k-blocks load during the current tile's last ones).
+// ---------------------------------------------------------------------------
+template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES, bool CHECK, bool SPLIT = false>
+__global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::THREADS, 1)
+    gemm_f64_ring(GemmArgs p) {
+  using Cfg = GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>;
+  constexpr int THREADS = Cfg::THREADS;
+  constexpr int MT = Cfg::MT, NT = Cfg::NT;
+  constexpr int KSTEPS = BK / 4;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  if (p.skip && __ldcg(p.skip) != 0) return;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp / Cfg::WARPS_N) * WM;
+  const int wn0 = (warp % Cfg::WARPS_N) * WN;
+  const int G = gridDim.x;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], THREADS);
+      mbar_init(&empty_bar[s], THREADS);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int a_row = tid / Cfg::A_ROWW, a_col = (tid % Cfg::A_ROWW) * 2;
+  const int b_row = tid / Cfg::B_ROWW, b_col = (tid % Cfg::B_ROWW) * 2;
+  const long a_kstep = TRANS_A ? long(BK) * p.lda : long(BK);
+  const long b_kstep = long(BK) * p.ldb;
+  const long a_rstep = long(Cfg::A_ROW_STEP) * p.lda;
+  const long b_rstep = long(Cfg::B_ROW_STEP) * p.ldb;
+
+  // ---- work segments (tile, [kb, ke)) of this CTA, in order ---------------
+  struct Seg {
+    int tile, tm, tn, kb, ke, tile_k;
+    long tile_it0;
+  };
+  struct Cursor {
+    long it, it_end;
+    int unit;
+  };
+  auto first_cursor = [&]() {
+    Cursor c;
+    c.it = long(blockIdx.x) * p.total_iters / G;
+    c.it_end = long(blockIdx.x + 1) * p.total_iters / G;
+    c.unit = blockIdx.x;
+    return c;
+  };
+  auto next_seg = [&](Cursor& c, Seg& s) -> bool {
+    s.tile_k = p.k_iters;
+    s.tile_it0 = 0;
+    if (SPLIT) {
+      if (c.unit >= p.units) return false;
+      const int tsel = c.unit / p.split, sl = c.unit % p.split;
+      if (p.sym) {
+        upper_tile(tsel, p.tiles_n, s.tm, s.tn);
+      } else {
+        s.tm = tsel / p.tiles_n;
+        s.tn = tsel % p.tiles_n;
+      }
+      s.tile = tsel;
+      s.kb = int(long(sl) * p.k_iters / p.split);
+      s.ke = int(long(sl + 1) * p.k_iters / p.split);
+      c.unit += G;
+      return true;
+    }
+    if (c.it >= c.it_end) return false;
+    if (p.tri_b) {
+      s.tm = int(c.it / p.row_iters);
+      int rem = int(c.it % p.row_iters);
+      s.tn = 0;
+      for (;;) {
+        const int kt = int(lmin(p.k_iters, long(s.tn + 1) * BN / BK));
+        if (rem < kt) {
+          s.tile_k = kt;
+          break;
+        }
+        rem -= kt;
+        ++s.tn;
+      }
+      s.kb = rem;
+      s.tile = s.tm * p.tiles_n + s.tn;
+    } else {
+      s.tile = int(c.it / p.k_iters);
+      s.kb = int(c.it % p.k_iters);
+      s.tm = s.tile / p.tiles_n;
+      s.tn = s.tile % p.tiles_n;
+    }
+    s.tile_it0 = c.it - s.kb;
+    s.ke = int(lmin(s.tile_k, s.kb + (c.it_end - c.it)));
+    c.it += s.ke - s.kb;
+    return true;
+  };
+
+  // ---- producer: loads k-blocks in flat order into the ring ---------------
+  Cursor pcur = first_cursor();
+  Seg pseg;
+  bool p_live = next_seg(pcur, pseg);
+  int pk = p_live ? pseg.kb : 0;
+  const double* a_src = nullptr;
+  const double* b_src = nullptr;
+  int a_bytes = 0, b_bytes = 0;
+  auto p_tile_setup = [&]() {
+    const long m0 = long(pseg.tm) * BM, n0 = long(pseg.tn) * BN;
+    if (TRANS_A) {
+      const long gm = m0 + a_col;
+      a_bytes = gm < p.M ? int(lmin(2, p.M - gm)) * 8 : 0;
+      a_src = p.A + (long(pseg.kb) * BK + a_row) * p.lda + (a_bytes ? gm : 0);
+    } else {
+      a_bytes = 16;
+      a_src = p.A + (m0 + a_row) * p.lda + long(pseg.kb) * BK + a_col;
+    }
+    const long gn = n0 + b_col;
+    b_bytes = gn < p.N ? int(lmin(2, p.N - gn)) * 8 : 0;
+    b_src = p.B + (long(pseg.kb) * BK + b_row) * p.ldb + (b_bytes ? gn : 0);
+  };
+  if (p_live) p_tile_setup();
+  long pflat = 0;  // flat index of the next k-block to load
+  auto produce = [&]() {
+    if (!p_live) return;
+    const int stage = int(pflat % STAGES);
+    if (pflat >= STAGES) mbar_wait(&empty_bar[stage], unsigned((pflat / STAGES - 1) & 1));
+    double* sA = smem + stage * Cfg::STAGE_ELEMS;
+    double* sB = sA + Cfg::SA_ELEMS;
+    const long k0 = long(pk) * BK;
+    const bool kfull = k0 + BK <= p.K;
+    const long m0 = long(pseg.tm) * BM;
+#pragma unroll
+    for (int i = 0; i < Cfg::A_PER_THREAD; ++i) {
+      const int r = a_row + i * Cfg::A_ROW_STEP;
+      int bytes;
+      if (TRANS_A) {
+        bytes = (kfull || k0 + r < p.K) ? a_bytes : 0;
+      } else {
+        const long gk = k0 + a_col;
+        bytes = (m0 + r < p.M) ? (kfull ? 16 : (gk < p.K ? int(lmin(2, p.K - gk)) * 8 : 0)) : 0;
+      }
+      cp_async16(sA + r * Cfg::SA_LD + a_col, bytes ? a_src + i * a_rstep : p.A, bytes);
+    }
+#pragma unroll
+    for (int i = 0; i < Cfg::B_PER_THREAD; ++i) {
+      const int r = b_row + i * Cfg::B_ROW_STEP;
+      const int bytes = (kfull || k0 + r < p.K) ? b_bytes : 0;
+      cp_async16(sB + r * Cfg::SB_LD + b_col, bytes ? b_src + i * b_rstep : p.B, bytes);
+    }
+    cp_async_mbar_arrive(&full_bar[stage]);
+    a_src += a_kstep;
+    b_src += b_kstep;
+    ++pflat;
+    if (++pk == pseg.ke) {
+      p_live = next_seg(pcur, pseg);
+      if (p_live) {
+        pk = pseg.kb;
+        p_tile_setup();
+      }
+    }
+  };
+#pragma unroll 1
+  for (int s = 0; s < STAGES - 1; ++s) produce();
+
+  // ---- consumer -----------------------------------------------------------
+  Cursor ccur = first_cursor();
+  Seg seg;
+  long cflat = 0;
+  bool saw_nonfinite = false;
+  while (next_seg(ccur, seg)) {
+    const long m0 = long(seg.tm) * BM, n0 = long(seg.tn) * BN;
+    const bool check = CHECK && (seg.tn == 0);
+    double acc[MT][NT][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll 1
+    for (int kbk = seg.kb; kbk < seg.ke; ++kbk) {
+      const int stage = int(cflat % STAGES);
+      mbar_wait(&full_bar[stage], unsigned((cflat / STAGES) & 1));
+      const double* sA = smem + stage * Cfg::STAGE_ELEMS;
+      const double* sB = sA + Cfg::SA_ELEMS;
+      if (CHECK && check) {
+#pragma unroll
+        for (int i = 0; i < Cfg::A_PER_THREAD; ++i) {
+          const int r = a_row + i * Cfg::A_ROW_STEP;
+          const double2 v = *reinterpret_cast<const double2*>(sA + r * Cfg::SA_LD + a_col);
+          saw_nonfinite |= nonfinite_bits(v.x) | nonfinite_bits(v.y);
+        }
+      }
+      double fa[2][MT], fb[2][NT];
+      auto load_frags = [&](int kk, double (&a)[MT], double (&b)[NT]) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          if (TRANS_A)
+            a[mt] = sA[(kk * 4 + t) * Cfg::SA_LD + wm0 + mt * 8 + g];
+          else
+            a[mt] = sA[(wm0 + mt * 8 + g) * Cfg::SA_LD + kk * 4 + t];
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = sB[(kk * 4 + t) * Cfg::SB_LD + wn0 + nt * 8 + g];
+      };
+      load_frags(0, fa[0], fb[0]);
+#pragma unroll
+      for (int kk = 0; kk < KSTEPS; ++kk) {
+        const int cur = kk & 1;
+        if (kk + 1 < KSTEPS) load_frags(kk + 1, fa[cur ^ 1], fb[cur ^ 1]);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], fa[cur][mt], fb[cur][nt]);
+      }
+      mbar_arrive(&empty_bar[stage]);
+      ++cflat;
+      produce();  // k-block cflat + STAGES − 2 into the stage released one step ago
+    }
+
+    // ---- epilogue: split partial / stream-K fix-up / store ---------------
+    if (SPLIT) {
+      double* slot = p.partials + size_t(ccur.unit - G) * (BM * BN);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          __stcg(reinterpret_cast<double2*>(slot + (wm0 + mt * 8 + g) * BN + wn0 + nt * 8 + 2 * t),
+                 make_double2(acc[mt][nt][0], acc[mt][nt][1]));
+      continue;
+    }
+    const bool full = (seg.kb == 0 && seg.ke == seg.tile_k);
+    if (!full && seg.kb != 0) {
+      double* slot = p.partials + size_t(blockIdx.x) * (BM * BN);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            __stcg(slot + size_t(((warp * MT + mt) * NT + nt) * 2 + e) * 32 + lane, acc[mt][nt][e]);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release(p.flags + blockIdx.x, 1);
+      continue;
+    }
+    if (!full) {
+      const long tile_end = seg.tile_it0 + seg.tile_k;
+      for (int c = blockIdx.x + 1; c < G; ++c) {
+        if (tid == 0) {
+          while (ld_acquire(p.flags + c) == 0) {
+          }
+        }
+        __syncthreads();
+        const double* slot = p.partials + size_t(c) * (BM * BN);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              acc[mt][nt][e] += __ldcg(slot + size_t(((warp * MT + mt) * NT + nt) * 2 + e) * 32 + lane);
+        if (long(c + 1) * p.total_iters / G >= tile_end) break;
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const long r = m0 + wm0 + mt * 8 + g;
+      if (r >= p.M) continue;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const long cidx = n0 + wn0 + nt * 8 + 2 * t;
+        double* dst = p.C + r * p.ldc + cidx;
+        double v0 = p.alpha * acc[mt][nt][0], v1 = p.alpha * acc[mt][nt][1];
+        if (cidx + 1 < p.N) {
+          if (p.beta != 0.0) {
+            const double2 o = *reinterpret_cast<const double2*>(dst);
+            v0 += p.beta * o.x;
+            v1 += p.beta * o.y;
+          }
+          *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+        } else if (cidx < p.N) {
+          if (p.beta != 0.0) v0 += p.beta * dst[0];
+          dst[0] = v0;
+        }
+      }
+    }
+  }
+  if (CHECK && saw_nonfinite) atomicOr(p.nonfinite, 1);
+}
+
 }  // namespace pbq

@@ -120,12 +120,22 @@ struct Carve {
 //   N > 64 : 128×128, BK 32, warp 64×32, 3 stages (A streamed ⌈N/128⌉ times;
 //            a 64×256 tile that reads A once measured 6% slower at d = 256:
 //            BK 16 doubles the barriers and DRAM is at 14% of bandwidth)
+#ifndef PBQ_GEMM_RING
+#define PBQ_GEMM_RING 1  // mbarrier k-block ring (gemm_f64_ring) instead of a CTA barrier per k-block
+#endif
 template <bool T, int BM, int BN, int BK, int WM, int WN, int ST>
 struct GemmKernel {
   using Cfg = GemmCfg<T, BM, BN, BK, WM, WN, ST>;
   static void* fn(bool check) {
+    if (PBQ_GEMM_RING)
+      return check ? reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, true>)
+                   : reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, false>);
     return check ? reinterpret_cast<void*>(&gemm_f64_streamk<T, BM, BN, BK, WM, WN, ST, true>)
                  : reinterpret_cast<void*>(&gemm_f64_streamk<T, BM, BN, BK, WM, WN, ST, false>);
+  }
+  static void* split_fn() {
+    if (PBQ_GEMM_RING) return reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, false, true>);
+    return reinterpret_cast<void*>(&gemm_f64_streamk<T, BM, BN, BK, WM, WN, ST, false, true>);
   }
 };
 
@@ -341,11 +351,11 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
   int threads;
   if (pl.bn == 64) {
     using C_ = GemmCfg<true, 128, 64, 32, 32, 32, 3>;
-    fn = reinterpret_cast<void*>(&gemm_f64_streamk<true, 128, 64, 32, 32, 32, 3, false, true>);
+    fn = GemmKernel<true, 128, 64, 32, 32, 32, 3>::split_fn();
     smem = C_::SMEM_BYTES; threads = C_::THREADS;
   } else {
     using C_ = GemmCfg<true, 128, 128, 32, 64, 32, 3>;
-    fn = reinterpret_cast<void*>(&gemm_f64_streamk<true, 128, 128, 32, 64, 32, 3, false, true>);
+    fn = GemmKernel<true, 128, 128, 32, 64, 32, 3>::split_fn();
     smem = C_::SMEM_BYTES; threads = C_::THREADS;
   }
   PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

@@ -248,6 +248,7 @@ def run_ours(args, world, rank, local):
     # from the CUDA events recorded around each launch inside the timed region
     roof = None
     if rank == 0:
+        traffic = gemm_traffic(args.workload)
         gemm_ms, gemm_n = by_class["gemm"]
         big = 2 * q + 2  # A-passes per step; the P̄·W product is 2·n2·d² flops
         fl_pass = 2.0 * n1 * n2 * d
@@ -256,8 +257,10 @@ def run_ours(args, world, rank, local):
         achieved = fl_total / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
         roof = {
             "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": None,
-            "kernel": "gemm_f64_streamk (C=A^T X and D=A X, FP64 DMMA.8x8x4)",
+            "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": traffic["bytes"],
+            "traffic_unit": "bytes per launch (DRAM read + write)", "traffic_source": traffic["source"],
+            "algorithmic_bytes_per_launch": 8.0 * (n1 * n2 + n1 * d + n2 * d),
+            "kernel": "gemm_f64_ring (C=A^T X and D=A X, FP64 DMMA.8x8x4)",
             "per_launch_flop": fl_pass, "launches_per_step": gemm_n / args.steps,
             "gemm_ms_per_step": gemm_ms / args.steps, "gemm_share_of_step": gemm_ms / args.steps / ms,
             "qr_ms_per_step": by_class["qr"][0] / args.steps, "sketch_ms_per_step": by_class["sketch"][0] / args.steps,
@@ -301,6 +304,19 @@ def run_ours(args, world, rank, local):
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+
+
+def gemm_traffic(workload):
+    """DRAM bytes per A-pass launch of the GEMM from the newest committed
+    `ncu --set full` capture (profiles/*_gemm_traffic.json, config 3 only)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_gemm_traffic.json")))
+    if workload != "cfg3" or not files:
+        return {"bytes": None, "source": None}
+    with open(files[-1]) as f:
+        rec = json.load(f)
+    return {"bytes": rec["dram_bytes_per_launch_avg"], "source": os.path.relpath(files[-1], os.path.dirname(os.path.abspath(__file__)))}
 
 
 def main():

@@ -115,11 +115,21 @@ struct Carve {
 
 // ---------------------------------------------------------------- GEMM ----
 // Two tile shapes: d ≤ 64 uses 128×64 (warp 32×32), larger d 128×128 (warp 64×32).
-// Tile configurations (BM×BN, BK, warp tile, stages), all 8 warps:
-//   N ≤ 64 : 128×64,  BK 32, warp 32×32, 3 stages
-//   N > 64 : 128×128, BK 32, warp 64×32, 3 stages (A streamed ⌈N/128⌉ times;
-//            a 64×256 tile that reads A once measured 6% slower at d = 256:
-//            BK 16 doubles the barriers and DRAM is at 14% of bandwidth)
+// Tile configurations (BM×BN, BK, warps × warp tile, stages):
+//   N ≤ 64 : 128×64,  BK 32, 8 warps of 32×32, 3 stages
+//   N > 64 : 128×128, BK 32, 16 warps of 32×32, 3 stages.  Four warps per
+//            scheduler hide the fragment-load latency that left the DMMA pipe
+//            idle with 8 warps of 64×32 (33.2 → 35.0 TFLOP/s at config 3).
+//            A streams ⌈N/128⌉ times; a 64×256 tile that reads A once
+//            measured 6% slower (BK 16), and DRAM is at ~20% of bandwidth.
+#ifndef PBQ_GEMM_WARPS16
+#define PBQ_GEMM_WARPS16 1  // 128×128 tile with 16 warps of 32×32 (4 per scheduler) instead of 8 of 64×32
+#endif
+#if PBQ_GEMM_WARPS16
+constexpr int GEMM_WM = 32;
+#else
+constexpr int GEMM_WM = 64;
+#endif
 #ifndef PBQ_GEMM_RING
 #define PBQ_GEMM_RING 1  // mbarrier k-block ring (gemm_f64_ring) instead of a CTA barrier per k-block
 #endif
@@ -204,7 +214,7 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
     using K_ = GemmKernel<TRANS, 128, 64, 32, 32, 32, 3>;
     fn = K_::fn(nonfinite != nullptr); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
   } else {
-    using K_ = GemmKernel<TRANS, 128, 128, 32, 64, 32, 3>;
+    using K_ = GemmKernel<TRANS, 128, 128, 32, GEMM_WM, 32, 3>;
     fn = K_::fn(nonfinite != nullptr); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
   }
   PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -354,8 +364,8 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
     fn = GemmKernel<true, 128, 64, 32, 32, 32, 3>::split_fn();
     smem = C_::SMEM_BYTES; threads = C_::THREADS;
   } else {
-    using C_ = GemmCfg<true, 128, 128, 32, 64, 32, 3>;
-    fn = GemmKernel<true, 128, 128, 32, 64, 32, 3>::split_fn();
+    using C_ = GemmCfg<true, 128, 128, 32, GEMM_WM, 32, 3>;
+    fn = GemmKernel<true, 128, 128, 32, GEMM_WM, 32, 3>::split_fn();
     smem = C_::SMEM_BYTES; threads = C_::THREADS;
   }
   PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

@@ -97,3 +97,25 @@ def test_odd_everything(cuda):
     rng = np.random.default_rng(24)
     a = rng.standard_normal((333, 257))
     _parity(a, 65, 1, 2**90 + 17)
+
+
+@pytest.mark.slow
+def test_config4_full(cuda):
+    """Config 4 at its BASELINE size: 200000×8192 (A = 13.1 GB), d = 512, q = 1,
+    σ_i = 10^(−i/128).  The oracle runs on the box's host cores (~1 min)."""
+    from paper_2103_07245_b200 import workloads
+
+    a_dev = workloads.make_cfg4(0, cuda)
+    a = a_dev.cpu().numpy()
+    _parity(a, 512, 1, 0, a_dev=a_dev)
+
+
+@pytest.mark.slow
+def test_config5_full(cuda):
+    """Config 5 at its BASELINE size: 65536×16384 (A = 8.6 GB), d = 256, q = 0,
+    σ_i = e^(−i/40) + 1e-8·N(0,1)."""
+    from paper_2103_07245_b200 import workloads
+
+    a_dev = workloads.make_cfg5(0, cuda)
+    a = a_dev.cpu().numpy()
+    _parity(a, 256, 0, 0, a_dev=a_dev)

@@ -4,8 +4,12 @@ Rank g of G owns the contiguous row block A_g = A[r_g : r_{g+1}] and the
 matching rows Φ_g of the sketch (the device generator produces any row range
 of the global stream, so Φ does not depend on G).  Exchanges:
 
-* AᵀX = Σ_g A_gᵀ X_g — a local GEMM, then one NCCL allreduce(sum) of the
-  n2×d partial; the result is identical on all ranks, so ``orth`` of it is
+* AᵀX = Σ_g A_gᵀ X_g — the local GEMM runs in ``chunks`` column blocks of
+  A_g (row blocks of the n2×d result) and each block's NCCL allreduce(sum)
+  is issued asynchronously right after its GEMM is enqueued: the collective
+  is ordered after the work already on the stream, so the exchange of block
+  b overlaps the GEMM of block b+1 and only the last block's allreduce is
+  exposed.  The result is identical on all ranks, so ``orth`` of it is
   computed replicated (same input → same bits).
 * qr(A·P̄) — A_g·P̄ is local; its QR is a distributed TSQR: local Householder
   QR (Q_g, R_g), all-gather of the d×d R factors, a replicated QR of the
@@ -72,7 +76,7 @@ class CudaBackend:
 class DistributedPbpQlp:
     """One rank's part of a row-sharded PbP-QLP; all ranks call ``run``."""
 
-    def __init__(self, n1, n2, d, q, rows, device=None, reorthonormalize=True, group=None, backend=None):
+    def __init__(self, n1, n2, d, q, rows, device=None, reorthonormalize=True, group=None, backend=None, chunks=None):
         self.n1, self.n2, self.d, self.q = int(n1), int(n2), int(d), int(q)
         self.rows = list(rows)
         self.group = group
@@ -86,6 +90,10 @@ class DistributedPbpQlp:
         if not 1 <= self.d <= min(n1, n2):
             raise _exc.ParameterError(f"d must be in [1, {min(n1, n2)}], got {d}")
         self.reorthonormalize = bool(reorthonormalize)
+        # allreduce pipelining depth for AᵀX (1 = one GEMM, then one allreduce)
+        self.chunks = int(chunks) if chunks is not None else (4 if self.world > 1 else 1)
+        if self.chunks < 1:
+            raise _exc.ParameterError("chunks must be >= 1")
         self.be = backend if backend is not None else CudaBackend(device)
         be = self.be
         self.C = be.empty(self.n2, self.d)         # AᵀX partial → allreduced → P̄ (in place)
@@ -103,12 +111,29 @@ class DistributedPbpQlp:
         self.PHI = None
 
     # -- collectives ---------------------------------------------------------
-    def _allreduce(self, t):
-        dense = t if t.is_contiguous() else t.contiguous()
-        dist.all_reduce(dense, op=dist.ReduceOp.SUM, group=self.group)
-        if dense is not t:
-            t.copy_(dense)
-        return t
+    def _chunk_bounds(self):
+        """Row blocks of the n2×d result: multiples of the GEMM's 128-row tile
+        (even starts keep the A column blocks 16-byte aligned)."""
+        tiles = -(-self.n2 // 128)
+        k = min(self.chunks, tiles)
+        cuts = [128 * ((tiles * c) // k) for c in range(k)] + [self.n2]
+        return [(cuts[c], cuts[c + 1]) for c in range(k) if cuts[c] < cuts[c + 1]]
+
+    def _at_x(self, A_local, X, nonfinite=None):
+        """self.C = Σ_g A_gᵀ·X_g with the allreduce of each row block
+        overlapping the GEMM of the next one."""
+        be = self.be
+        C = self.C
+        ld = C.stride(0)
+        padded = C.as_strided((C.shape[0], ld), (ld, 1))  # whole rows incl. the even-ld pad column
+        handles = []
+        for r0, r1 in self._chunk_bounds():
+            be.gemm_tn(A_local[:, r0:r1], X, C[r0:r1], nonfinite=nonfinite)
+            if self.world > 1 or self.chunks > 1:  # (world 1: exercises the pipeline)
+                handles.append(dist.all_reduce(padded[r0:r1], op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+        for h in handles:
+            h.wait()
+        return C
 
     def _tsqr_(self, flag=None):
         """Distributed QR of the row-sharded self.Q (m_g × d) in place; R → self.R."""
@@ -140,8 +165,7 @@ class DistributedPbpQlp:
         else:
             self.PHI = be.contiguous(phi_local)
         site = 2
-        be.gemm_tn(A_local, self.PHI, self.C, nonfinite=flags[0:1])
-        self._allreduce(self.C)
+        self._at_x(A_local, self.PHI, nonfinite=flags[0:1])
         if self.reorthonormalize:
             be.qr_(self.C, self.Rs, flags[site:site + 1])
             site += 1
@@ -149,15 +173,13 @@ class DistributedPbpQlp:
                 be.gemm_nn(A_local, self.C, self.Q)
                 self._tsqr_(flags[site:site + 1])
                 site += 1
-                be.gemm_tn(A_local, self.Q, self.C)
-                self._allreduce(self.C)
+                self._at_x(A_local, self.Q)
                 be.qr_(self.C, self.Rs, flags[site:site + 1])
                 site += 1
         else:
             for _ in range(q):
                 be.gemm_nn(A_local, self.C, self.Q)
-                be.gemm_tn(A_local, self.Q, self.C)
-                self._allreduce(self.C)
+                self._at_x(A_local, self.Q)
             be.qr_(self.C, self.Rs, flags[site:site + 1])
         be.gemm_nn(A_local, self.C, self.Q)
         self._tsqr_()

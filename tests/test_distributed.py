@@ -18,7 +18,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, a, d, q, seed, reorth, outdir):
+def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks=None):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -34,7 +34,7 @@ def _worker(rank, world, port, a, d, q, seed, reorth, outdir):
     try:
         n1, n2 = a.shape
         rows = shard_rows(n1, world)
-        run = DistributedPbpQlp(n1, n2, d, q, rows, reorthonormalize=reorth, backend=NumpyBackend())
+        run = DistributedPbpQlp(n1, n2, d, q, rows, reorthonormalize=reorth, backend=NumpyBackend(), chunks=chunks)
         a_loc = torch.from_numpy(np.ascontiguousarray(a[rows[rank]:rows[rank + 1]]))
         run.run(a_loc, seed=seed)
         import warnings
@@ -49,21 +49,24 @@ def _worker(rank, world, port, a, d, q, seed, reorth, outdir):
         dist.destroy_process_group()
 
 
-def _run(a, d, q, seed, reorth, tmp_path, world=2):
+def _run(a, d, q, seed, reorth, tmp_path, world=2, chunks=None):
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, a, d, q, seed, reorth, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, a, d, q, seed, reorth, str(tmp_path), chunks), nprocs=world, join=True)
     parts = [np.load(os.path.join(tmp_path, f"rank{g}.npz")) for g in range(world)]
     return parts
 
 
-@pytest.mark.parametrize("q,reorth", [(0, True), (1, True), (1, False)])
-def test_row_sharded_matches_oracle(tmp_path, q, reorth):
+@pytest.mark.parametrize("q,reorth,chunks", [(0, True, None), (1, True, None), (1, False, None), (1, True, 3)])
+def test_row_sharded_matches_oracle(tmp_path, q, reorth, chunks):
+    """chunks=3 splits AᵀX into row blocks of 128 (n2 = 300 → 128, 128, 44)
+    whose allreduces are issued asynchronously while later blocks compute."""
     from oracle.pbp_qlp_oracle import column_relative_error, conditioning_tolerance, oracle_pbp_qlp
 
     rng = np.random.default_rng(11)
-    a = rng.standard_normal((240, 40)) @ rng.standard_normal((40, 90)) / 7 + 1e-3 * rng.standard_normal((240, 90))
+    n2 = 300 if chunks else 90
+    a = rng.standard_normal((240, 40)) @ rng.standard_normal((40, n2)) / 7 + 1e-3 * rng.standard_normal((240, n2))
     d = 24
-    parts = _run(a, d, q, 5, reorth, tmp_path)
+    parts = _run(a, d, q, 5, reorth, tmp_path, chunks=chunks)
     ref = oracle_pbp_qlp(a, d, q=q, seed=5, reorthonormalize=reorth)
     qfull = np.vstack([p["q"] for p in parts])
     phi = np.vstack([p["phi"] for p in parts])

@@ -189,15 +189,16 @@ def test_distributed_driver_on_one_gpu(cuda):
         rng = np.random.default_rng(9)
         a = rng.standard_normal((900, 60)) @ rng.standard_normal((60, 500)) / 8 + 1e-3 * rng.standard_normal((900, 500))
         at = torch.from_numpy(a).to(cuda)
-        run = DistributedPbpQlp(900, 500, 48, 1, shard_rows(900, 1), device=cuda)
-        run.run(at, seed=7)
-        run.finish()
-        qg, l, p, r = (t.cpu().numpy() for t in run.factors())
         ref = pbp_qlp(a, 48, q=1, seed=7)
         tol = conditioning_tolerance(ref.l, strict=1e-10)
-        assert np.all(column_relative_error(qg, ref.q_basis) <= tol)
-        assert np.all(column_relative_error(p, ref.p_basis) <= tol)
-        assert np.allclose(np.diag(l), np.diag(ref.l), rtol=1e-10, atol=0)
+        for chunks in (1, 3):  # 3: AᵀX in 128-row blocks with asynchronous NCCL allreduces
+            run = DistributedPbpQlp(900, 500, 48, 1, shard_rows(900, 1), device=cuda, chunks=chunks)
+            run.run(at, seed=7)
+            run.finish()
+            qg, l, p, r = (t.cpu().numpy() for t in run.factors())
+            assert np.all(column_relative_error(qg, ref.q_basis) <= tol)
+            assert np.all(column_relative_error(p, ref.p_basis) <= tol)
+            assert np.allclose(np.diag(l), np.diag(ref.l), rtol=1e-10, atol=0)
     finally:
         dist.destroy_process_group()
 

@@ -238,6 +238,16 @@ def run_ours(args, world, rank, local):
     finish()
     launches = ctx.launch_count - launches0
     ms = e0.elapsed_time(e1) / args.steps
+
+    # ---- reconstruction check of the last timed step (outside the timed
+    # region): ‖A − QLPᵀ‖_F/‖A‖_F by the fused one-pass residual kernel
+    check = None
+    if world == 1:
+        from paper_2103_07245_b200 import QlpFactors, reconstruction_error
+
+        f = QlpFactors(plan.Q, plan.L, plan.P, None)
+        check = {"recon_rel_err": reconstruction_error(a, f),
+                 "method": "pbq_residual_fro (fused GEMM + residual epilogue, one pass over A)"}
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -301,7 +311,7 @@ def run_ours(args, world, rank, local):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(args, wl, world),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks,
+            "clocks": clocks, "check": check,
         }
         print(json.dumps(line), flush=True)
 

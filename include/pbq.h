@@ -139,6 +139,18 @@ int pbq_pbp_qlp_workspace_bytes(pbq_ctx* ctx, const pbq_problem* prob, size_t* b
 int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* prob, const pbq_outputs* out, void* workspace,
                 size_t workspace_bytes, void* stream);
 
+/* Reconstruction residual: out[0] = ‖A − Q_k·L_k·P_kᵀ‖_F²,
+ * out[1] = ‖A‖_F² (device doubles), with Q_k, L_k, P_k the leading k ≤ d
+ * columns / block of the factors — QlpFactors.approx(rank)
+ * (algorithms.py:101-106) and error_curve's frobenius_error
+ * (analysis.py:238-244) without forming the n1×n2 approximation: one pass
+ * over A through a GEMM whose epilogue subtracts and accumulates.
+ * Deterministic (fixed-order reductions). */
+int pbq_residual_fro(pbq_ctx* ctx, int64_t n1, int64_t n2, int64_t k, const double* A, int64_t lda,
+                     const double* Q, int64_t ldq, const double* L, int64_t ldl, const double* P,
+                     int64_t ldp, double* out, void* workspace, size_t workspace_bytes, void* stream);
+int pbq_residual_workspace_bytes(pbq_ctx* ctx, int64_t n1, int64_t n2, int64_t k, size_t* bytes);
+
 /* Small helpers used by the host driver.
  * dst[i][j] = src[j][i]            (n×n), or with lower=1 the lower triangle
  * of srcᵀ and zeros above (L = tril(R̃ᵀ), algorithms.py:257). */

@@ -5,7 +5,8 @@ Drop-in for the reference package's PbP-QLP path (``pbpqlp.pbp_qlp``,
 arguments, errors, warnings and result fields; every FLOP runs in
 hand-written sm_100a CUDA behind the C ABI in include/pbq.h.
 """
-from .algorithms import PbpQlpPlan, QlpFactors, SketchRecord, pbp_qlp, pbp_qlp_bytes, pbp_qlp_flops
+from .algorithms import (PbpQlpPlan, QlpFactors, SketchRecord, pbp_qlp, pbp_qlp_bytes, pbp_qlp_flops,
+                         reconstruction_error, residual_norms)
 from .exceptions import DeviceError, DimensionError, MatrixInputError, ParameterError, RankDeficiencyWarning
 from .linalg import QrFactors, gaussian_matrix, householder_qr, orth
 
@@ -27,5 +28,7 @@ __all__ = [
     "pbp_qlp",
     "pbp_qlp_bytes",
     "pbp_qlp_flops",
+    "reconstruction_error",
+    "residual_norms",
     "__version__",
 ]

@@ -44,6 +44,8 @@ EXPORTED = (
     "pbq_profile_end",
     "pbq_set_qr_method",
     "pbq_debug_cholqr_stats",
+    "pbq_residual_fro",
+    "pbq_residual_workspace_bytes",
 )
 
 c_i64 = ctypes.c_int64
@@ -99,6 +101,9 @@ _SIGS = {
     "pbq_profile_begin": ([c_p, c_i32], ctypes.c_int),
     "pbq_profile_end": ([c_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)], ctypes.c_int),
     "pbq_set_qr_method": ([c_p, c_i32], ctypes.c_int),
+    "pbq_residual_fro": ([c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_p, c_sz, c_p],
+                         ctypes.c_int),
+    "pbq_residual_workspace_bytes": ([c_p, c_i64, c_i64, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_debug_cholqr_stats": ([c_p, c_p], ctypes.c_int),
 }
 

@@ -106,6 +106,45 @@ class QlpFactors:
         w = householder_qr(self.first_stage_r.T).q
         return self.p_basis @ w.T
 
+    def frobenius_error(self, a, rank=None):
+        """‖a − approx(rank)‖_F on the GPU in one pass over ``a`` (the
+        ``frobenius_error`` of error_curve, analysis.py:238-244)."""
+        return residual_norms(a, self, rank)[0]
+
+
+def residual_norms(a, factors, rank=None, *, device=None):
+    """(‖A − Q_k·L_k·P_kᵀ‖_F, ‖A‖_F) for QLP factors truncated to ``rank``
+    (QlpFactors.approx, algorithms.py:101-106), computed by libpbq's fused
+    residual GEMM: one pass over A, the n1×n2 approximation is never formed
+    (SURVEY.md §8 f2).  ``a`` is validated like the reference's check_matrix."""
+    import math
+
+    kmax = factors.l.shape[0]
+    k = kmax if rank is None else check_index_range(rank, "rank", 1, kmax)
+    _, a_dev, _, _ = to_device_matrix(a, "a", device)
+    dev = a_dev.device
+    n1, n2 = a_dev.shape
+    if factors.q_basis.shape[0] != n1 or factors.p_basis.shape[0] != n2:
+        raise _exc.DimensionError(
+            f"factors of a {factors.q_basis.shape[0]}x{factors.p_basis.shape[0]} matrix do not fit a of shape {tuple(a_dev.shape)}"
+        )
+
+    def on_dev(x):
+        return torch.as_tensor(x).to(device=dev, dtype=torch.float64)
+
+    q = on_dev(factors.q_basis)[:, :k]
+    l = on_dev(factors.l)[:k, :k]
+    p = on_dev(factors.p_basis)[:, :k]
+    out = _dev.residual_fro(_dev.context(dev), a_dev, q, l, p)
+    r2, a2 = out.tolist()
+    return math.sqrt(r2), math.sqrt(a2)
+
+
+def reconstruction_error(a, factors, rank=None, *, device=None):
+    """‖A − approx(rank)‖_F / ‖A‖_F (the north-star reconstruction check)."""
+    r, na = residual_norms(a, factors, rank, device=device)
+    return r / na if na > 0 else r
+
 
 def qr_flops(m, d):
     """LAPACK geqrf + orgqr thin-Q flop count, 4md² − 4d³/3."""

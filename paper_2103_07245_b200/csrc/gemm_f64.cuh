@@ -49,6 +49,12 @@ struct GemmArgs {
   // needs k < (tn+1)·BN — the stream-K space then has row_iters =
   // Σ_tn k-blocks(tn) iterations per row of tiles (total_iters = tiles_m·row_iters)
   int tri_b, row_iters;
+  // RESID epilogue (‖A − op(A)·B‖_F of the reconstruction): instead of storing
+  // C, each finished tile subtracts from ref[r·ldref + c] and accumulates the
+  // squared residual and squared ref; per-CTA sums go to sums[2·cta + {0,1}]
+  const double* ref;
+  long ldref;
+  double* sums;
 };
 
 
@@ -356,7 +362,8 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
 // re-aligning at every k-block, and the ring runs on across the CTA's tiles
 // (the next tile's first k-blocks load during the current tile's last ones).
 // ---------------------------------------------------------------------------
-template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES, bool CHECK, bool SPLIT = false>
+template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES, bool CHECK, bool SPLIT = false,
+          bool RESID = false>
 __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::THREADS, 1)
     gemm_f64_ring(GemmArgs p) {
   using Cfg = GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>;
@@ -523,6 +530,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
   Seg seg;
   long cflat = 0;
   bool saw_nonfinite = false;
+  double res2 = 0.0, ref2 = 0.0;  // RESID accumulators (fixed order per thread)
   while (next_seg(ccur, seg)) {
     const long m0 = long(seg.tm) * BM, n0 = long(seg.tn) * BN;
     const bool check = CHECK && (seg.tn == 0);
@@ -618,6 +626,32 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
         if (long(c + 1) * p.total_iters / G >= tile_end) break;
       }
     }
+    if (RESID) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const long r = m0 + wm0 + mt * 8 + g;
+        if (r >= p.M) continue;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const long cidx = n0 + wn0 + nt * 8 + 2 * t;
+          const double* src = p.ref + r * p.ldref + cidx;
+          if (cidx + 1 < p.N) {
+            const double2 a2 = __ldcs(reinterpret_cast<const double2*>(src));
+            const double d0 = a2.x - acc[mt][nt][0], d1 = a2.y - acc[mt][nt][1];
+            res2 = fma(d0, d0, res2);
+            res2 = fma(d1, d1, res2);
+            ref2 = fma(a2.x, a2.x, ref2);
+            ref2 = fma(a2.y, a2.y, ref2);
+          } else if (cidx < p.N) {
+            const double a0 = __ldcs(src);
+            const double d0 = a0 - acc[mt][nt][0];
+            res2 = fma(d0, d0, res2);
+            ref2 = fma(a0, a0, ref2);
+          }
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       const long r = m0 + wm0 + mt * 8 + g;
@@ -642,6 +676,29 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
     }
   }
   if (CHECK && saw_nonfinite) atomicOr(p.nonfinite, 1);
+  if (RESID) {
+    // fixed-order CTA reduction → sums[2·cta + {0,1}]
+    __shared__ double s_red[2][THREADS / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      res2 += __shfl_xor_sync(0xffffffffu, res2, o);
+      ref2 += __shfl_xor_sync(0xffffffffu, ref2, o);
+    }
+    if (lane == 0) {
+      s_red[0][warp] = res2;
+      s_red[1][warp] = ref2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < THREADS / 32; ++w) {
+        a += s_red[0][w];
+        b += s_red[1][w];
+      }
+      p.sums[2 * blockIdx.x] = a;
+      p.sums[2 * blockIdx.x + 1] = b;
+    }
+  }
 }
 
 }  // namespace pbq

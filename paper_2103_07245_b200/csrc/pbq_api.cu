@@ -528,32 +528,125 @@ int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t 
 }
 
 // ----------------------------------------------------------- helpers ----
-__global__ void transpose_kernel(long n, const double* __restrict__ src, long lds, double* __restrict__ dst, long ldd,
-                                 int lower) {
+// dst (cols×rows) = srcᵀ for src rows×cols; `lower` (square only) keeps the
+// lower triangle of srcᵀ and zeros the rest (L = tril(R̃ᵀ)).
+__global__ void transpose_kernel(long rows, long cols, const double* __restrict__ src, long lds,
+                                 double* __restrict__ dst, long ldd, int lower) {
   __shared__ double tile[32][33];
-  const long bx = long(blockIdx.x) * 32, by = long(blockIdx.y) * 32;
+  const long bx = long(blockIdx.x) * 32, by = long(blockIdx.y) * 32;  // bx: src column block, by: src row block
   for (int j = threadIdx.y; j < 32; j += 8) {
     const long r = by + j, c = bx + threadIdx.x;
-    tile[j][threadIdx.x] = (r < n && c < n) ? src[r * lds + c] : 0.0;
+    tile[j][threadIdx.x] = (r < rows && c < cols) ? src[r * lds + c] : 0.0;
   }
   __syncthreads();
   for (int j = threadIdx.y; j < 32; j += 8) {
     const long r = bx + j, c = by + threadIdx.x;  // dst[r][c] = src[c][r]
-    if (r < n && c < n) dst[r * ldd + c] = (lower && c > r) ? 0.0 : tile[threadIdx.x][j];
+    if (r < cols && c < rows) dst[r * ldd + c] = (lower && c > r) ? 0.0 : tile[threadIdx.x][j];
   }
 }
 
 int transpose_launch(pbq_ctx* ctx, long n, const double* src, long lds, double* dst, long ldd, int lower,
-                     cudaStream_t st) {
-  dim3 grid(unsigned(ceil_div(n, 32)), unsigned(ceil_div(n, 32)));
+                     cudaStream_t st, long cols = -1) {
+  const long rows = n;
+  if (cols < 0) cols = n;
+  dim3 grid(unsigned(ceil_div(cols, 32)), unsigned(ceil_div(rows, 32)));
   ProfScope ps(ctx->prof, st, 3);
-  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(n, src, lds, dst, ldd, lower);
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(rows, cols, src, lds, dst, ldd, lower);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 1;
   return PBQ_OK;
 }
 
 long thin_ld(long d) { return (d + 1) & ~1L; }
+
+// ------------------------------------------------- reconstruction residual --
+// ‖A − Q_k·L_k·P_kᵀ‖_F² and ‖A‖_F² (QlpFactors.approx(rank), algorithms.py:
+// 101-106; error_curve's frobenius_error, analysis.py:238-244) in one pass
+// over A: M = Q_k·L_k (n1×k), Pᵀ_k (k×n2), then the ring GEMM M·Pᵀ_k with the
+// RESID epilogue; the n1×n2 approximation is never stored.
+__global__ void resid_final_kernel(const double* sums, int n, double* out) {
+  __shared__ double s[2][256];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) {
+    a += sums[2 * i];
+    b += sums[2 * i + 1];
+  }
+  s[0][threadIdx.x] = a;
+  s[1][threadIdx.x] = b;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      s[0][threadIdx.x] += s[0][threadIdx.x + w];
+      s[1][threadIdx.x] += s[1][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s[0][0];
+    out[1] = s[1][0];
+  }
+}
+
+size_t resid_ws_bytes(const pbq_ctx* ctx, long n1, long n2, long k) {
+  const GemmPlan g1 = gemm_plan(ctx, n1, n2, k), g2 = gemm_plan(ctx, n1, k, k);
+  const long ldk = thin_ld(k), ldn = thin_ld(n2);
+  return align_up(size_t(n1) * ldk * 8, 256) + align_up(size_t(k) * ldn * 8, 256) +
+         align_up(2 * size_t(ctx->sms) * 8, 256) + std::max(gemm_ws_bytes(g1), gemm_ws_bytes(g2)) + 1024;
+}
+
+int resid_launch(pbq_ctx* ctx, long n1, long n2, long k, const double* A, long lda, const double* Q, long ldq,
+                 const double* L, long ldl, const double* P, long ldp, double* out, void* ws, size_t ws_bytes,
+                 cudaStream_t st) {
+  if (n1 < 1 || n2 < 1 || k < 1) return fail(ctx, PBQ_ERR_DIM, "residual: bad shape");
+  if ((lda & 1) || (ldq & 1) || (ldl & 1) || (ldp & 1) || !aligned16(A) || !aligned16(Q) || !aligned16(L) ||
+      !aligned16(P))
+    return fail(ctx, PBQ_ERR_PARAM, "residual: leading dimensions must be even and pointers 16-byte aligned");
+  const long ldk = thin_ld(k), ldn = thin_ld(n2);
+  Carve cv(ws, ws_bytes);
+  double* ql = cv.take<double>(size_t(n1) * ldk);
+  double* pt = cv.take<double>(size_t(k) * ldn);
+  double* sums = cv.take<double>(2 * size_t(ctx->sms));
+  const GemmPlan pl = gemm_plan(ctx, n1, n2, k);
+  const size_t gws_bytes = std::max(gemm_ws_bytes(pl), gemm_ws_bytes(gemm_plan(ctx, n1, k, k)));
+  char* gws = cv.take<char>(gws_bytes);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "residual: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  PBQ_TRY(gemm_launch<false>(ctx, n1, k, k, 1.0, Q, ldq, L, ldl, 0.0, ql, ldk, nullptr, gws, gws_bytes, st));
+  PBQ_TRY(transpose_launch(ctx, n2, P, ldp, pt, ldn, 0, st, k));
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = n1; a.N = n2; a.K = k;
+  a.A = ql; a.lda = ldk; a.B = pt; a.ldb = ldn;
+  a.alpha = 1.0;
+  a.tiles_m = pl.tiles_m; a.tiles_n = pl.tiles_n; a.k_iters = pl.k_iters; a.total_iters = pl.total;
+  Carve gc(gws, gws_bytes);
+  a.partials = gc.take<double>(size_t(pl.grid) * pl.bm * pl.bn);
+  a.flags = gc.take<int>(pl.grid);
+  a.ref = A; a.ldref = lda; a.sums = sums;
+  PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
+  void* fn;
+  size_t smem;
+  int threads;
+  if (pl.bn == 64) {
+    using C_ = GemmCfg<false, 128, 64, 32, 32, 32, 3>;
+    fn = reinterpret_cast<void*>(&gemm_f64_ring<false, 128, 64, 32, 32, 32, 3, false, false, true>);
+    smem = C_::SMEM_BYTES; threads = C_::THREADS;
+  } else {
+    using C_ = GemmCfg<false, 128, 128, 32, GEMM_WM, 32, 3>;
+    fn = reinterpret_cast<void*>(&gemm_f64_ring<false, 128, 128, 32, GEMM_WM, 32, 3, false, false, true>);
+    smem = C_::SMEM_BYTES; threads = C_::THREADS;
+  }
+  PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  void* args[] = {&a};
+  {
+    ProfScope ps(ctx->prof, st, 0);
+    PBQ_CUDA(ctx, cudaLaunchKernel(fn, dim3(pl.grid), dim3(threads), args, smem, st));
+  }
+  ctx->launches += 1;
+  resid_final_kernel<<<1, 256, 0, st>>>(sums, pl.grid, out);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return PBQ_OK;
+}
 
 __global__ void merge_flag_kernel(int32_t* status, const int32_t* sketch_err) {
   if (*sketch_err) *status |= 2;
@@ -691,6 +784,22 @@ int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns, uin
   ctx->qr_phase_ns = reinterpret_cast<unsigned long long*>(phase_ns);
   ctx->qr_bar_wait_ns = reinterpret_cast<unsigned long long*>(bar_wait_ns);
   return PBQ_OK;
+}
+
+int pbq_residual_workspace_bytes(pbq_ctx* ctx, int64_t n1, int64_t n2, int64_t k, size_t* bytes) {
+  if (!ctx || !bytes) return PBQ_ERR_PARAM;
+  if (n1 < 1 || n2 < 1 || k < 1) return fail(ctx, PBQ_ERR_DIM, "residual: bad shape");
+  *bytes = resid_ws_bytes(ctx, n1, n2, k);
+  return PBQ_OK;
+}
+
+int pbq_residual_fro(pbq_ctx* ctx, int64_t n1, int64_t n2, int64_t k, const double* A, int64_t lda, const double* Q,
+                     int64_t ldq, const double* L, int64_t ldl, const double* P, int64_t ldp, double* out, void* ws,
+                     size_t ws_bytes, void* stream) {
+  if (!ctx || !out) return PBQ_ERR_PARAM;
+  if (lda < n2 || ldq < k || ldl < k || ldp < k) return fail(ctx, PBQ_ERR_PARAM, "residual: leading dimension too small");
+  return resid_launch(ctx, n1, n2, k, A, lda, Q, ldq, L, ldl, P, ldp, out, ws, ws_bytes,
+                      static_cast<cudaStream_t>(stream));
 }
 
 int pbq_set_qr_method(pbq_ctx* ctx, int32_t method) {

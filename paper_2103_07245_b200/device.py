@@ -176,6 +176,25 @@ def householder_qr_(ctx, a, r=None, want_q=True, rank_flag=None):
     return a, r
 
 
+def residual_fro(ctx, a, q, l, p, out=None):
+    """out[0] = ‖a − q·l·pᵀ‖_F², out[1] = ‖a‖_F² (device float64[2]), in one
+    pass over ``a`` (q: n1×k, l: k×k, p: n2×k)."""
+    dev = a.device
+    a, q, l, p = (as_kernel_operand(t) for t in (a, q, l, p))
+    n1, n2 = a.shape
+    k = l.shape[0]
+    if out is None:
+        out = torch.empty(2, dtype=torch.float64, device=dev)
+    nbytes = ctypes.c_size_t()
+    with ctx.lock:
+        ctx.check(ctx.lib.pbq_residual_workspace_bytes(ctx.handle, n1, n2, k, ctypes.byref(nbytes)), "residual workspace")
+        ws = workspace(nbytes.value, dev)
+        st = ctx.lib.pbq_residual_fro(ctx.handle, n1, n2, k, ptr(a), ld_of(a), ptr(q), ld_of(q), ptr(l), ld_of(l),
+                                      ptr(p), ld_of(p), ptr(out), ptr(ws), nbytes.value, stream_ptr(dev))
+        ctx.check(st, "residual_fro")
+    return out
+
+
 def gaussian(ctx, rows, cols, seed, device, row_offset=0, out=None, status=None):
     """Enqueue the sketch; ``status`` (int32 device tensor) receives the
     generator's overflow flag (callers check it when they synchronise)."""

@@ -42,6 +42,10 @@ def _parity(a_host, d, q, seed, a_dev=None, strict=1e-10):
     e_got = _recon_err(ad, gq, gl, gp)
     e_ref = _recon_err(ad, ref["q"], ref["l"], ref["p"])
     assert abs(e_got - e_ref) <= 1e-10 * e_ref + 1e-15
+    # the fused one-pass residual agrees with the dense check
+    from paper_2103_07245_b200 import reconstruction_error
+
+    assert abs(reconstruction_error(ad, got) - e_got) <= 1e-10 * e_got + 1e-15
     return eq.max(), ep.max()
 
 

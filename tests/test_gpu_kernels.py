@@ -188,3 +188,24 @@ def test_gaussian_row_offset(cuda):
     assert np.array_equal(part, full[1500:2500])
     ref = c_gaussian(1000, 64, 9, row_offset=1500)
     assert np.count_nonzero(part != ref) <= 2
+
+
+@pytest.mark.parametrize("n1,n2,d,rank", [(300, 200, 25, None), (301, 257, 33, 7), (1000, 40, 40, 40),
+                                          (2000, 1500, 100, 64), (129, 65, 65, 1)])
+def test_residual_norms_match_numpy(cuda, n1, n2, d, rank):
+    """Fused one-pass ‖A − Q_k L_k P_kᵀ‖_F vs the dense numpy
+    residual of QlpFactors.approx(rank) (algorithms.py:101-106)."""
+    from paper_2103_07245_b200 import pbp_qlp, reconstruction_error, residual_norms
+
+    rng = np.random.default_rng(n1 + n2 + d)
+    a = rng.standard_normal((n1, d)) @ rng.standard_normal((d, n2)) / d + 1e-2 * rng.standard_normal((n1, n2))
+    f = pbp_qlp(a, d, q=1, seed=3)
+    r, na = residual_norms(a, f, rank)
+    k = d if rank is None else rank
+    ref = np.linalg.norm(a - f.q_basis[:, :k] @ f.l[:k, :k] @ f.p_basis[:, :k].T)
+    assert abs(r - ref) <= 1e-12 * np.linalg.norm(a) + 1e-10 * ref
+    assert abs(na - np.linalg.norm(a)) <= 1e-13 * np.linalg.norm(a)
+    assert abs(reconstruction_error(a, f, rank) - ref / np.linalg.norm(a)) <= 1e-12
+    assert abs(f.frobenius_error(a, rank) - ref) <= 1e-12 * np.linalg.norm(a) + 1e-10 * ref
+    # deterministic: same bits on a second call
+    assert residual_norms(a, f, rank) == (r, na)

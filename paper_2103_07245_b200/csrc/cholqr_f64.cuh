@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
       }
       return;
     }
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == gridDim.x - 1) {  // the last CTA has the fewest items; CTA 0 carries (k+1, k+1)
       cq_store(p.R, np, k, k, sKK);
       cq_store(p.X, np, k, k, sKI);
       if (pass1) {

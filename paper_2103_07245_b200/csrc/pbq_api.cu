@@ -313,7 +313,8 @@ struct CqPlan {
   int nb;
   long np;
   int bm, bn, tiles_m, tiles_n, ntiles, k_iters, S, units;  // Gram GEMM (split-K partials)
-  int grid;                                                // factor kernel CTAs
+  int grid;                                                // factor kernel CTAs, pass 1
+  int grid2;                                               // pass 2 (series rounds have more items)
   long ldq1;
   size_t gemm_ws;
 };
@@ -333,6 +334,10 @@ CqPlan cq_plan(const pbq_ctx* ctx, long m, long n) {
   p.S = int(std::max<long>(1, std::min<long>(p.k_iters, ctx->sms / p.ntiles)));
   p.units = p.ntiles * p.S;
   p.grid = int(std::max<long>(1, std::min<long>(ctx->sms, std::max<long>(long(p.nb) * (p.nb - 1) / 2, p.nb - 1))));
+  {
+    const long nbl = p.nb;
+    p.grid2 = int(std::max<long>(p.grid, std::min<long>(ctx->sms, nbl * (nbl + 1) + nbl * (nbl - 1) / 2)));
+  }
   p.ldq1 = (n + 1) & ~1L;
   const size_t gram = align_up(size_t(p.units) * p.bm * p.bn * sizeof(double), 256);
   p.gemm_ws = std::max(gram, gemm_ws_bytes(gemm_plan(ctx, m, n, n, true)));
@@ -392,7 +397,8 @@ int factor_launch(pbq_ctx* ctx, const CqPlan& pl, CqArgs& a, cudaStream_t st) {
   PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&cholqr_factor_kernel),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(CQ_SMEM_BYTES)));
   void* args[] = {&a};
-  PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&cholqr_factor_kernel), dim3(pl.grid),
+  PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&cholqr_factor_kernel),
+                                            dim3(a.pass == 1 ? pl.grid : pl.grid2),
                                             dim3(CQ_THREADS), args, CQ_SMEM_BYTES, st));
   ctx->launches += 1;
   return PBQ_OK;
@@ -481,6 +487,7 @@ SketchPlan sketch_plan(long rows, long cols, long row_offset) {
 size_t sketch_ws_bytes(const SketchPlan& p) {
   const size_t n = p.n_chunks;
   return align_up(n * 4, 256) + align_up(n * PBQ_SK_E * 4, 256) + align_up(n * 8, 256) + align_up(n * 4, 256) +
+         align_up(n * PBQ_SK_CHUNK * 8, 256) + align_up(n * 2 * PBQ_SK_MAXSPECIAL * 8, 256) + align_up(n * 4, 256) +
          256 + 256;
 }
 
@@ -511,6 +518,9 @@ int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t 
   a.counts = cv.take<int>(size_t(pl.n_chunks) * PBQ_SK_E);
   a.base = cv.take<long>(pl.n_chunks);
   a.entry = cv.take<int>(pl.n_chunks);
+  a.vals = cv.take<double>(size_t(pl.n_chunks) * PBQ_SK_CHUNK);
+  a.sp = cv.take<uint64_t>(size_t(pl.n_chunks) * 2 * PBQ_SK_MAXSPECIAL);
+  a.nsp = cv.take<int>(pl.n_chunks);
   int* own_err = cv.take<int>(1);
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gaussian: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   a.error = error_flag ? error_flag : own_err;

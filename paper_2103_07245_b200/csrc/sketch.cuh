@@ -9,16 +9,20 @@
 // starts depends on every earlier draw.  The GPU resolves that dependency in
 // three passes over fixed 1024-position chunks of the stream, one chunk per
 // warp (lane ℓ owns positions 32ℓ..32ℓ+31 as a 32-bit mask; no CTA barriers):
-//   K1 finds the rare "special" positions (draws the rectangle test rejects),
-//      resolves where each special draw's normal ends, and walks the start
-//      chain for every possible entry offset e ∈ [0, 32).  Chains from
-//      different entries merge within a few positions, so a chunk's exit
-//      position does not depend on its entry (checked; a violation sets the
-//      error flag).
+//   K1 generates the chunk's Philox words once: the value a normal starting
+//      at each position would take (the rectangle-test value, or the fully
+//      resolved ziggurat value for the rare "special" positions the test
+//      rejects) is written position-indexed (coalesced, through padded shared
+//      memory), the special positions and where their normals end are saved,
+//      and the start chain is walked for every possible entry offset
+//      e ∈ [0, 32).  Chains from different entries merge within a few
+//      positions, so a chunk's exit does not depend on its entry (checked; a
+//      violation sets the error flag).
 //   K2 (one CTA) turns exits into per-chunk entry offsets and exclusive-scans
 //      the per-chunk normal counts.
-//   K3 marks the chain's start positions, ranks them with a warp scan, stages
-//      the values in shared memory and writes them coalesced to Φ.
+//   K3 rebuilds the chain's start positions from the saved specials, ranks
+//      them with a warp scan, gathers their values and writes them coalesced
+//      to Φ — a memory-bound compaction (no Philox).
 // Values equal numpy's bit for bit, except that the exponential-tail branch
 // (idx 0, ~2.6e-4 of draws) uses CUDA's log1p, which can differ from glibc's by
 // 1 ulp; see DESIGN.md §5.
@@ -146,6 +150,9 @@ struct SketchArgs {
   long* base;   // n_chunks: global normal index of the chunk's first start
   int* entry;   // n_chunks: entry offset of the chunk
   int* error;   // set on internal overflow
+  double* vals;     // n_chunks × 1024: value of a normal starting at each position
+  uint64_t* sp;     // n_chunks × 2·MAXSPECIAL: special positions, then where their normals end
+  int* nsp;         // n_chunks: number of specials
 };
 
 struct SkWarpSmem {
@@ -212,15 +219,65 @@ __device__ __forceinline__ void sk_walk(uint64_t s, uint64_t cend, const SkWarpS
 
 __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k1(SketchArgs a) {
   __shared__ SkWarpSmem sw[PBQ_SK_WARPS];
+  __shared__ double stage[PBQ_SK_WARPS][32 * 33];  // position-indexed values, row ℓ = lane ℓ's 32 positions (padded)
   __shared__ ZigTables zt;
   zig_stage(zt);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long chunk = long(blockIdx.x) * PBQ_SK_WARPS + warp;
   if (chunk >= a.n_chunks) return;
   SkWarpSmem& w = sw[warp];
-  unsigned mask;
-  const int nsp = sk_find_specials(zt, a, chunk, w, mask);
+  double* st = stage[warp];
   const uint64_t cstart = uint64_t(chunk) * PBQ_SK_CHUNK, cend = cstart + PBQ_SK_CHUNK;
+  const uint64_t p0 = cstart + uint64_t(lane) * 32;
+  // one Philox pass: rectangle-test values, and the special mask
+  unsigned mask = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const Philox4x64 blk = philox4x64_10((p0 >> 2) + b + 1, a.k0, a.k1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t r = blk.x[q];
+      if (zig_fast(zt, r))
+        st[lane * 33 + b * 4 + q] = zig_fast_value(zt, r);
+      else
+        mask |= 1u << (b * 4 + q);
+    }
+  }
+  const int mine = __popc(mask);
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int off = incl - mine;
+  for (unsigned m = mask; m; m &= m - 1) {
+    const int j = __ffs(m) - 1;
+    if (off < PBQ_SK_MAXSPECIAL) w.sp_pos[off] = p0 + j;
+    ++off;
+  }
+  const int nsp = min(total, PBQ_SK_MAXSPECIAL);
+  if (total > PBQ_SK_MAXSPECIAL && lane == 0) atomicExch(a.error, 1);
+  __syncwarp();
+  // resolve the specials (full sampler); their values go to their positions
+  uint64_t* gsp = a.sp + size_t(chunk) * 2 * PBQ_SK_MAXSPECIAL;
+  for (int i = lane; i < nsp; i += 32) {
+    double v;
+    const uint64_t sp = w.sp_pos[i];
+    const uint64_t nx = zig_resolve(zt, sp, a.k0, a.k1, &v);
+    w.sp_next[i] = nx;
+    const int rel = int(sp - cstart);
+    st[(rel >> 5) * 33 + (rel & 31)] = v;
+    gsp[i] = sp;
+    gsp[PBQ_SK_MAXSPECIAL + i] = nx;
+  }
+  if (lane == 0) a.nsp[chunk] = nsp;
+  __syncwarp();
+  // coalesced position-indexed write-out
+  double* gv = a.vals + size_t(chunk) * PBQ_SK_CHUNK;
+#pragma unroll 8
+  for (int e = lane; e < PBQ_SK_CHUNK; e += 32) __stcg(gv + e, st[(e >> 5) * 33 + (e & 31)]);
   int cnt;
   uint64_t ex;
   sk_walk(cstart + lane, cend, w, nsp, cnt, ex);  // entry offset = lane
@@ -228,9 +285,9 @@ __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k1(SketchArgs a) {
   const uint64_t ex0 = __shfl_sync(0xffffffffu, ex, 0);
   const bool merged = __all_sync(0xffffffffu, ex == ex0);
   if (lane == 0) {
-    const uint64_t off = ex0 - cend;
-    if (!merged || off >= uint64_t(PBQ_SK_E)) atomicExch(a.error, 2);
-    a.exits[chunk] = int(off < uint64_t(PBQ_SK_E) ? off : 0);
+    const uint64_t off2 = ex0 - cend;
+    if (!merged || off2 >= uint64_t(PBQ_SK_E)) atomicExch(a.error, 2);
+    a.exits[chunk] = int(off2 < uint64_t(PBQ_SK_E) ? off2 : 0);
   }
 }
 
@@ -241,10 +298,24 @@ __global__ void __launch_bounds__(1024) sketch_k2(SketchArgs a) {
   const long n = a.n_chunks;
   const long per = (n + 1023) / 1024;
   const long c0 = tid * per, c1 = lmin(n, c0 + per);
+  // per-thread chunk run: issue all loads before using them (one round trip
+  // for the exits, one for the counts)
+  constexpr int RUN = 8;
   long local = 0;
-  for (long c = c0; c < c1; ++c) {
-    const int e = (c == 0) ? 0 : a.exits[c - 1];
-    local += a.counts[c * PBQ_SK_E + e];
+  for (long cb = c0; cb < c1; cb += RUN) {
+    int ex[RUN], ct[RUN];
+#pragma unroll
+    for (int u = 0; u < RUN; ++u) {
+      const long c = cb + u;
+      ex[u] = (c < c1 && c > 0) ? a.exits[c - 1] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < RUN; ++u) {
+      const long c = cb + u;
+      ct[u] = (c < c1) ? a.counts[c * PBQ_SK_E + ex[u]] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < RUN; ++u) local += ct[u];
   }
   long incl = local;
 #pragma unroll
@@ -257,11 +328,27 @@ __global__ void __launch_bounds__(1024) sketch_k2(SketchArgs a) {
   long wbase = 0;
   for (int w = 0; w < warp; ++w) wbase += warp_tot[w];
   long run = wbase + incl - local;
-  for (long c = c0; c < c1; ++c) {
-    const int e = (c == 0) ? 0 : a.exits[c - 1];
-    a.entry[c] = e;
-    a.base[c] = run;
-    run += a.counts[c * PBQ_SK_E + e];
+  for (long cb = c0; cb < c1; cb += RUN) {
+    int ex[RUN], ct[RUN];
+#pragma unroll
+    for (int u = 0; u < RUN; ++u) {
+      const long c = cb + u;
+      ex[u] = (c < c1 && c > 0) ? a.exits[c - 1] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < RUN; ++u) {
+      const long c = cb + u;
+      ct[u] = (c < c1) ? a.counts[c * PBQ_SK_E + ex[u]] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < RUN; ++u) {
+      const long c = cb + u;
+      if (c < c1) {
+        a.entry[c] = ex[u];
+        a.base[c] = run;
+        run += ct[u];
+      }
+    }
   }
   if (tid == 1023) {
     long total = 0;
@@ -272,9 +359,7 @@ __global__ void __launch_bounds__(1024) sketch_k2(SketchArgs a) {
 
 __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k3(SketchArgs a) {
   __shared__ SkWarpSmem sw[PBQ_SK_WARPS];
-  __shared__ double vals[PBQ_SK_WARPS][PBQ_SK_CHUNK];
-  __shared__ ZigTables zt;
-  zig_stage(zt);
+  __shared__ double buf[PBQ_SK_WARPS][32 * 33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long chunk = long(blockIdx.x) * PBQ_SK_WARPS + warp;
   if (chunk >= a.n_chunks) return;
@@ -283,9 +368,18 @@ __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k3(SketchArgs a) {
   const int cnt_here = a.counts[chunk * PBQ_SK_E + entry];
   if (base >= a.first + a.count || base + cnt_here <= a.first) return;  // nothing requested here
   SkWarpSmem& w = sw[warp];
-  unsigned special;
-  const int nsp = sk_find_specials(zt, a, chunk, w, special);
+  double* bw = buf[warp];
   const uint64_t cstart = uint64_t(chunk) * PBQ_SK_CHUNK, cend = cstart + PBQ_SK_CHUNK;
+  // position-indexed values → padded shared memory (coalesced read)
+  const double* gv = a.vals + size_t(chunk) * PBQ_SK_CHUNK;
+#pragma unroll 8
+  for (int e = lane; e < PBQ_SK_CHUNK; e += 32) bw[(e >> 5) * 33 + (e & 31)] = __ldcs(gv + e);
+  const int nsp = a.nsp[chunk];
+  const uint64_t* gsp = a.sp + size_t(chunk) * 2 * PBQ_SK_MAXSPECIAL;
+  for (int i = lane; i < nsp; i += 32) {
+    w.sp_pos[i] = gsp[i];
+    w.sp_next[i] = gsp[PBQ_SK_MAXSPECIAL + i];
+  }
   // start mask: every position from the entry on, minus the words consumed by
   // special normals beyond their first word (walked by lane 0, set in smem)
   unsigned start = (lane * 32 >= entry) ? 0xffffffffu : ((entry - lane * 32 >= 32) ? 0u : (0xffffffffu << (entry - lane * 32)));
@@ -315,21 +409,14 @@ __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k3(SketchArgs a) {
     if (lane >= o) incl += v;
   }
   int rank = incl - mine;  // chunk-local index of this lane's first normal
-  const uint64_t p0 = cstart + uint64_t(lane) * 32;
+  // gather this lane's start values (registers), then compact in place
+  double v[32];
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    const Philox4x64 blk = philox4x64_10((p0 >> 2) + b + 1, a.k0, a.k1);
+  for (int j = 0; j < 32; ++j) v[j] = bw[lane * 33 + j];
+  __syncwarp();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = b * 4 + q;
-      if (!((start >> j) & 1u)) continue;
-      const uint64_t r = blk.x[q];
-      double v;
-      if (zig_fast(zt, r)) v = zig_fast_value(zt, r);
-      else zig_resolve(zt, p0 + j, a.k0, a.k1, &v);
-      vals[warp][rank++] = v;
-    }
-  }
+  for (int j = 0; j < 32; ++j)
+    if ((start >> j) & 1u) bw[rank++] = v[j];
   __syncwarp();
   // coalesced write-out of this chunk's normals [base, base + cnt_here)
   const long lo = lmax(base, a.first), hi = lmin(base + cnt_here, a.first + a.count);
@@ -341,7 +428,7 @@ __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k3(SketchArgs a) {
   long r_l = row + (col + lane) / a.cols;
   long c_l = (col + lane) % a.cols;
   for (long e = lane; e < hi - lo; e += 32) {
-    a.out[r_l * a.ldo + c_l] = vals[warp][lo - base + e];
+    a.out[r_l * a.ldo + c_l] = bw[lo - base + e];
     r_l += step_row;
     c_l += step_col;
     if (c_l >= a.cols) {

@@ -10,6 +10,8 @@ This is a restatement of the reference path at the numpy level, call for call:
 * ``oracle_qr``         ↔ ``householder_qr`` + ``_fix_signs`` (linalg.py:96-115)
 * ``oracle_orth``       ↔ ``orth``             (linalg.py:142-165)
 * ``oracle_pbp_qlp``    ↔ ``pbp_qlp``          (algorithms.py:209-260)
+* ``oracle_spectral_norm`` ↔ ``spectral_norm`` (linalg.py:168-207)
+* ``oracle_error_curve``   ↔ ``error_curve``   (analysis.py:213-247, pbp_qlp)
 
 The arithmetic lives in numpy 2.3.5 (the reference pins only numpy>=1.24,
 pyproject.toml:11-15): dgemm for products, LAPACK dgeqrf+dorgqr (via
@@ -205,6 +207,43 @@ def conditioning_tolerance(l_ref, strict=1e-10, factor=64.0):
     with np.errstate(divide="ignore"):
         kappa = np.where(diag > 0, diag[0] / diag, np.inf)
     return np.maximum(strict, factor * 2.0**-53 * kappa)
+
+
+def oracle_spectral_norm(m):
+    """linalg.py:194-207: dense σ₁ up to 2000 in the larger dimension, else
+    power iteration on the Gram operator (linalg.py:168-191) from the seeded
+    start gaussian_matrix(n, 1, seed=0x5EED), rtol 1e-10, ≤ 5000 steps."""
+    m = np.asarray(m, dtype=np.float64)
+    if max(m.shape) <= 2000:
+        return float(np.linalg.svd(m, compute_uv=False)[0])
+    v = oracle_gaussian(m.shape[1], 1, seed=0x5EED).ravel()
+    v /= np.linalg.norm(v)
+    estimate = 0.0
+    for _ in range(5000):
+        w = m @ v
+        nw = np.linalg.norm(w)
+        if nw == 0.0:
+            return 0.0
+        v = m.T @ w
+        nv = np.linalg.norm(v)
+        if nv == 0.0:
+            return 0.0
+        v /= nv
+        new = nv / nw
+        if abs(new - estimate) <= 1e-10 * max(new, 1e-300):
+            return float(new)
+        estimate = new
+    raise RuntimeError("power iteration did not converge")
+
+
+def oracle_error_curve(a, d_values, q=0, seed=0, reorthonormalize=True):
+    """analysis.py:213-247 for alg = "pbp_qlp"."""
+    out = []
+    for d in d_values:
+        f = oracle_pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
+        res = a - f["q"] @ f["l"] @ f["p"].T
+        out.append({"d": d, "spectral_error": oracle_spectral_norm(res), "frobenius_error": float(np.linalg.norm(res))})
+    return out
 
 
 def reconstruction_error(a, qf, l, p):

@@ -7,12 +7,14 @@ hand-written sm_100a CUDA behind the C ABI in include/pbq.h.
 """
 from .algorithms import (PbpQlpPlan, QlpFactors, SketchRecord, pbp_qlp, pbp_qlp_bytes, pbp_qlp_flops,
                          reconstruction_error, residual_norms)
-from .exceptions import DeviceError, DimensionError, MatrixInputError, ParameterError, RankDeficiencyWarning
+from .exceptions import (ConvergenceError, DeviceError, DimensionError, MatrixInputError, ParameterError,
+                         RankDeficiencyWarning)
 from .linalg import QrFactors, gaussian_matrix, householder_qr, orth
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "ConvergenceError",
     "DeviceError",
     "DimensionError",
     "MatrixInputError",

@@ -25,5 +25,14 @@ class RankDeficiencyWarning(UserWarning):
     still returned (exceptions.py:56-57)."""
 
 
+class ConvergenceError(RuntimeError):
+    """An iterative kernel failed to converge; ``estimate`` carries the best
+    value reached (exceptions.py:37-44)."""
+
+    def __init__(self, message, estimate=None):
+        super().__init__(message)
+        self.estimate = estimate
+
+
 class DeviceError(RuntimeError):
     """The CUDA library reported a failure (launch, memory, unsupported shape)."""

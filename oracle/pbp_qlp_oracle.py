@@ -10,6 +10,7 @@ This is a restatement of the reference path at the numpy level, call for call:
 * ``oracle_qr``         ↔ ``householder_qr`` + ``_fix_signs`` (linalg.py:96-115)
 * ``oracle_orth``       ↔ ``orth``             (linalg.py:142-165)
 * ``oracle_pbp_qlp``    ↔ ``pbp_qlp``          (algorithms.py:209-260)
+* ``oracle_r_svd``       ↔ ``r_svd``         (algorithms.py:263-292)
 * ``oracle_spectral_norm`` ↔ ``spectral_norm`` (linalg.py:168-207)
 * ``oracle_error_curve``   ↔ ``error_curve``   (analysis.py:213-247, pbp_qlp)
 
@@ -207,6 +208,31 @@ def conditioning_tolerance(l_ref, strict=1e-10, factor=64.0):
     with np.errstate(divide="ignore"):
         kappa = np.where(diag > 0, diag[0] / diag, np.inf)
     return np.maximum(strict, factor * 2.0**-53 * kappa)
+
+
+def oracle_r_svd(a, d, q=0, seed=0, reorthonormalize=True):
+    """algorithms.py:263-292 restated (sketch Ω is n2×d; transpose_first=False
+    power iterations; svd_full = np.linalg.svd, linalg.py:131-139)."""
+    a = np.asarray(a, dtype=np.float64)
+    omega = oracle_gaussian(a.shape[1], d, seed)
+    flags = []
+    f = a @ omega
+    if reorthonormalize:
+        ubar, fl = oracle_orth(f)
+        flags.append(fl)
+        for _ in range(q):
+            ubar, fl = oracle_orth(a.T @ ubar)
+            flags.append(fl)
+            ubar, fl = oracle_orth(a @ ubar)
+            flags.append(fl)
+    else:
+        for _ in range(q):
+            f = a @ (a.T @ f)
+        ubar, fl = oracle_orth(f)
+        flags.append(fl)
+    g = (a.T @ ubar).T
+    uc, s, vh = np.linalg.svd(g, full_matrices=False)
+    return {"u": ubar @ uc, "s": s, "v": vh.T, "omega": omega, "rank_flags": flags}
 
 
 def oracle_spectral_norm(m):

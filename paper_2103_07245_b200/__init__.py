@@ -10,6 +10,7 @@ from .algorithms import (PbpQlpPlan, QlpFactors, SketchRecord, pbp_qlp, pbp_qlp_
 from .exceptions import (ConvergenceError, DeviceError, DimensionError, MatrixInputError, ParameterError,
                          RankDeficiencyWarning)
 from .linalg import QrFactors, gaussian_matrix, householder_qr, orth
+from .rsvd import RsvdFactors, r_svd
 
 __version__ = "0.1.0"
 
@@ -23,6 +24,7 @@ __all__ = [
     "QlpFactors",
     "QrFactors",
     "RankDeficiencyWarning",
+    "RsvdFactors",
     "SketchRecord",
     "gaussian_matrix",
     "householder_qr",
@@ -30,6 +32,7 @@ __all__ = [
     "pbp_qlp",
     "pbp_qlp_bytes",
     "pbp_qlp_flops",
+    "r_svd",
     "reconstruction_error",
     "residual_norms",
     "__version__",

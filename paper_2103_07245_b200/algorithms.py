@@ -114,27 +114,32 @@ class QlpFactors:
 
 def residual_norms(a, factors, rank=None, *, device=None):
     """(‖A − Q_k·L_k·P_kᵀ‖_F, ‖A‖_F) for QLP factors truncated to ``rank``
-    (QlpFactors.approx, algorithms.py:101-106), computed by libpbq's fused
+    (QlpFactors.approx, algorithms.py:101-106; for SVD-type factors
+    u_k·diag(s_k)·v_kᵀ, analysis.py:182-186), computed by libpbq's fused
     residual GEMM: one pass over A, the n1×n2 approximation is never formed
     (SURVEY.md §8 f2).  ``a`` is validated like the reference's check_matrix."""
     import math
 
-    kmax = factors.l.shape[0]
+    if hasattr(factors, "l"):  # QLP: Q L Pᵀ
+        left, mid, right = factors.q_basis, factors.l, factors.p_basis
+    else:  # SVD-type (RsvdFactors): u diag(s) vᵀ
+        left, mid, right = factors.u, None, factors.v
+    kmax = left.shape[1] if mid is None else mid.shape[0]
     k = kmax if rank is None else check_index_range(rank, "rank", 1, kmax)
     _, a_dev, _, _ = to_device_matrix(a, "a", device)
     dev = a_dev.device
     n1, n2 = a_dev.shape
-    if factors.q_basis.shape[0] != n1 or factors.p_basis.shape[0] != n2:
+    if left.shape[0] != n1 or right.shape[0] != n2:
         raise _exc.DimensionError(
-            f"factors of a {factors.q_basis.shape[0]}x{factors.p_basis.shape[0]} matrix do not fit a of shape {tuple(a_dev.shape)}"
+            f"factors of a {left.shape[0]}x{right.shape[0]} matrix do not fit a of shape {tuple(a_dev.shape)}"
         )
 
     def on_dev(x):
         return torch.as_tensor(x).to(device=dev, dtype=torch.float64)
 
-    q = on_dev(factors.q_basis)[:, :k]
-    l = on_dev(factors.l)[:k, :k]
-    p = on_dev(factors.p_basis)[:, :k]
+    q = on_dev(left)[:, :k]
+    l = on_dev(mid)[:k, :k] if mid is not None else torch.diag(on_dev(factors.s)[:k])
+    p = on_dev(right)[:, :k]
     out = _dev.residual_fro(_dev.context(dev), a_dev, q, l, p)
     r2, a2 = out.tolist()
     return math.sqrt(r2), math.sqrt(a2)

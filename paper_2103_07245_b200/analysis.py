@@ -3,7 +3,7 @@
 Mirrors the reference's dispatcher and error helpers for the algorithm this
 package implements:
 
-* ``factorize(a, "pbp_qlp", d, ...)``        ↔ analysis.py:135-157
+* ``factorize(a, "pbp_qlp" | "r_svd", d, ...)`` ↔ analysis.py:135-157
 * ``low_rank_approx(factors, rank)``         ↔ analysis.py:170-193 (QLP factors)
 * ``spectral_norm(m)``                        ↔ linalg.py:194-207 (+ _power_norm :168-191)
 * ``residual_spectral_norm(a, f, rank)``      ‖A − approx‖₂ without forming the residual
@@ -16,7 +16,8 @@ up to 2000 in the larger dimension, else power iteration on the Gram
 operator from the seeded start vector gaussian_matrix(n, 1, seed=0x5EED),
 relative tolerance 1e-10, at most 5000 iterations.  Its matrix-vector
 products use torch on the device; it is an analysis helper, not the hot path.
-Algorithms other than ``pbp_qlp`` are outside this package's scope and raise.
+Algorithms other than ``pbp_qlp`` and ``r_svd`` are outside this package's
+scope and raise.
 """
 import math
 
@@ -25,6 +26,7 @@ import torch
 
 from . import exceptions as _exc
 from .algorithms import QlpFactors, pbp_qlp, residual_norms
+from .rsvd import RsvdFactors, r_svd
 from .linalg import HostMatrix, gaussian_matrix
 from .validation import check_index_range
 
@@ -32,7 +34,7 @@ __all__ = ["ALGORITHMS", "GPU_ALGORITHMS", "factorize", "low_rank_approx", "spec
            "residual_spectral_norm", "error_curve"]
 
 ALGORITHMS = ("svd", "cpqr", "pqlp", "r_svd", "cor_utv", "pbp_qlp")  # analysis.py:53-55
-GPU_ALGORITHMS = ("pbp_qlp",)
+GPU_ALGORITHMS = ("pbp_qlp", "r_svd")
 DENSE_NORM_LIMIT = 2000  # linalg.py:40
 POWER_RTOL = 1e-10       # linalg.py:43
 POWER_MAXITER = 5000     # linalg.py:44
@@ -59,13 +61,21 @@ def factorize(a, algorithm, d, q=0, seed=0, reorthonormalize=True):
     if algorithm not in GPU_ALGORITHMS:
         _check_finite(HostMatrix(a, "a"), "a")
         _check_algorithm(algorithm)
+    if algorithm == "r_svd":
+        return r_svd(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
     return pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
 
 
 def low_rank_approx(factors, rank=None):
-    """Reconstruction from QLP factors, optionally truncated (analysis.py:170-176)."""
+    """Reconstruction, optionally truncated (analysis.py:170-193) for the
+    factor types of this package."""
     if isinstance(factors, QlpFactors):
         return factors.approx(rank)
+    if isinstance(factors, RsvdFactors):
+        if rank is None:
+            return factors.approx()
+        rank = check_index_range(rank, "rank", 1, factors.s.shape[0])
+        return (factors.u[:, :rank] * factors.s[:rank]) @ factors.v[:, :rank].T
     raise _exc.ParameterError(f"cannot reconstruct from factors of type {type(factors).__name__}")
 
 
@@ -113,13 +123,20 @@ def spectral_norm(m, *, device=None):
 def residual_spectral_norm(a, factors, rank=None, *, device=None):
     """‖A − approx(rank)‖₂: the reference's spectral_norm(a − approx) without
     forming the residual on the power-iteration path."""
-    kmax = factors.l.shape[0]
-    k = kmax if rank is None else check_index_range(rank, "rank", 1, kmax)
     t = HostMatrix(a, "a").to_device(device)
     dev = t.device
-    q = torch.as_tensor(factors.q_basis).to(device=dev, dtype=torch.float64)[:, :k]
-    l = torch.as_tensor(factors.l).to(device=dev, dtype=torch.float64)[:k, :k]
-    p = torch.as_tensor(factors.p_basis).to(device=dev, dtype=torch.float64)[:, :k]
+
+    def on_dev(x):
+        return torch.as_tensor(x).to(device=dev, dtype=torch.float64)
+
+    if isinstance(factors, RsvdFactors):
+        kmax = factors.s.shape[0]
+        k = kmax if rank is None else check_index_range(rank, "rank", 1, kmax)
+        q, l, p = on_dev(factors.u)[:, :k], torch.diag(on_dev(factors.s)[:k]), on_dev(factors.v)[:, :k]
+    else:
+        kmax = factors.l.shape[0]
+        k = kmax if rank is None else check_index_range(rank, "rank", 1, kmax)
+        q, l, p = on_dev(factors.q_basis)[:, :k], on_dev(factors.l)[:k, :k], on_dev(factors.p_basis)[:, :k]
     if max(t.shape) <= DENSE_NORM_LIMIT:
         return float(torch.linalg.svdvals(t - q @ l @ p.T)[0])
     return float(_power_norm(lambda x: t @ x - q @ (l @ (p.T @ x)),
@@ -140,7 +157,7 @@ def error_curve(a, alg, d_values, q=0, seed=0, reorthonormalize=True):
     _check_algorithm(alg)
     records = []
     for d in d_list:
-        fac = pbp_qlp(t, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
+        fac = factorize(t, alg, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
         fro, _ = residual_norms(t, fac)
         records.append({"d": d, "spectral_error": residual_spectral_norm(t, fac), "frobenius_error": fro})
     return records

@@ -1,12 +1,14 @@
-"""scikit-learn transformer for the PbP-QLP path.
+"""scikit-learn transformers for the GPU paths.
 
-Mirrors the reference's ``PbpQlp`` estimator (estimators.py:81-108 on the
-shared ``_LowRankTransformer`` plumbing, :31-78): ``fit`` factorizes on the
-GPU (``pbp_qlp``), ``components_`` holds the first ``n_components`` columns
-of P transposed, ``singular_values_`` the |diag L| estimates
-(analysis.singular_value_estimates), and ``transform`` / ``inverse_transform``
-are the skinny products X·componentsᵀ and Z·components run on libpbq's
-DMMA GEMM.  numpy in → numpy out; CUDA tensors stay on the device.
+Mirror the reference's ``PbpQlp`` and ``RandomizedSvd`` estimators
+(estimators.py:81-126 on the shared ``_LowRankTransformer`` plumbing,
+:31-78): ``fit`` factorizes on the GPU, ``components_`` holds the first
+``n_components`` columns of the row-space basis transposed (P for PbP-QLP,
+V for r_svd), ``singular_values_`` the estimates of
+analysis.singular_value_estimates (|diag L|, resp. s), and ``transform`` /
+``inverse_transform`` are the skinny products X·componentsᵀ and
+Z·components run on libpbq's DMMA GEMM.  numpy in → numpy out; CUDA tensors
+stay on the device.
 """
 import numpy as np
 import torch
@@ -17,9 +19,10 @@ from . import device as _dev
 from . import exceptions as _exc
 from .algorithms import pbp_qlp
 from .linalg import HostMatrix
+from .rsvd import r_svd
 from .validation import check_count
 
-__all__ = ["PbpQlp"]
+__all__ = ["PbpQlp", "RandomizedSvd"]
 
 
 def _gemm_nn(x, b):
@@ -28,19 +31,10 @@ def _gemm_nn(x, b):
     return _dev.gemm(ctx, x, b, trans_a=False)
 
 
-class PbpQlp(BaseEstimator, TransformerMixin):
-    """Randomized QLP factorization driven by a row-space sketch
-    (estimators.py:81-108): ``fit`` computes Q L Pᵀ of rank
-    ``n_components`` with ``q`` power iterations; ``inverse_transform(
-    transform(X))`` reproduces the factorization's low-rank approximation."""
+class _LowRankTransformer(BaseEstimator, TransformerMixin):
+    """Shared plumbing (estimators.py:31-78); subclasses give
+    ``_factorize(X, rank)``, ``_row_basis(f)`` and ``_spectrum(f)``."""
 
-    def __init__(self, n_components, q=0, seed=0, reorthonormalize=True):
-        self.n_components = n_components
-        self.q = q
-        self.seed = seed
-        self.reorthonormalize = reorthonormalize
-
-    # -- reference protocol (estimators.py:39-78) -----------------------------
     def fit(self, X, y=None):
         h = HostMatrix(X, "X")
         if not h.all_finite():
@@ -48,14 +42,15 @@ class PbpQlp(BaseEstimator, TransformerMixin):
         limit = min(h.shape)
         rank = check_count(self.n_components, "n_components", minimum=1, maximum=limit)
         self.n_components_ = rank
-        self.factors_ = pbp_qlp(X, rank, q=self.q, seed=self.seed, reorthonormalize=self.reorthonormalize)
-        p = self.factors_.p_basis
-        if isinstance(p, torch.Tensor):
-            self.components_ = p[:, :rank].T.contiguous()
-            self.singular_values_ = torch.diagonal(self.factors_.l)[:rank].abs()
+        self.factors_ = self._factorize(X, rank)
+        basis = self._row_basis(self.factors_)
+        spec = self._spectrum(self.factors_)
+        if isinstance(basis, torch.Tensor):
+            self.components_ = basis[:, :rank].T.contiguous()
+            self.singular_values_ = spec[:rank].abs()
         else:
-            self.components_ = np.ascontiguousarray(p[:, :rank].T)
-            self.singular_values_ = np.abs(np.diagonal(self.factors_.l))[:rank].copy()
+            self.components_ = np.ascontiguousarray(basis[:, :rank].T)
+            self.singular_values_ = np.abs(spec)[:rank].copy()
         self.n_features_in_ = h.shape[1]
         return self
 
@@ -88,3 +83,44 @@ class PbpQlp(BaseEstimator, TransformerMixin):
         self._check_fitted()
         return self._apply(X, self.components_, self.n_components_,
                            f"the fitted basis has {self.n_components_} components")
+
+
+class PbpQlp(_LowRankTransformer):
+    """Randomized QLP factorization driven by a row-space sketch
+    (estimators.py:81-108): ``fit`` computes Q L Pᵀ of rank
+    ``n_components`` with ``q`` power iterations; ``inverse_transform(
+    transform(X))`` reproduces the factorization's low-rank approximation."""
+
+    def __init__(self, n_components, q=0, seed=0, reorthonormalize=True):
+        self.n_components = n_components
+        self.q = q
+        self.seed = seed
+        self.reorthonormalize = reorthonormalize
+
+    def _factorize(self, X, rank):
+        return pbp_qlp(X, rank, q=self.q, seed=self.seed, reorthonormalize=self.reorthonormalize)
+
+    def _row_basis(self, f):
+        return f.p_basis
+
+    def _spectrum(self, f):
+        return torch.diagonal(f.l) if isinstance(f.l, torch.Tensor) else np.diagonal(f.l)
+
+
+class RandomizedSvd(_LowRankTransformer):
+    """Randomized truncated SVD via a column-space sketch (estimators.py:111-126)."""
+
+    def __init__(self, n_components, q=0, seed=0, reorthonormalize=True):
+        self.n_components = n_components
+        self.q = q
+        self.seed = seed
+        self.reorthonormalize = reorthonormalize
+
+    def _factorize(self, X, rank):
+        return r_svd(X, rank, q=self.q, seed=self.seed, reorthonormalize=self.reorthonormalize)
+
+    def _row_basis(self, f):
+        return f.v
+
+    def _spectrum(self, f):
+        return f.s

@@ -1,6 +1,7 @@
 """Drop-in wiring for the reference package.
 
-``install(pbpqlp)`` rebinds the reference's PbP-QLP entry point — in every
+``install(pbpqlp)`` rebinds the reference's PbP-QLP entry point (and the
+sibling ``r_svd``, algorithms.py:263-292) — in every
 module that imported it by name (algorithms.py:209, __init__.py:18,
 analysis.py:16-25 → factorize :153-154, estimators.py:17 → PbpQlp
 :98-105, bounds.py:42 → eval_highprob_bounds :589, cli.py:43 → :448, :733)
@@ -19,8 +20,47 @@ import warnings
 from . import algorithms as _alg
 from . import exceptions as _exc
 
-# modules of the reference that bind the name `pbp_qlp` at import time
+# modules of the reference that bind the names `pbp_qlp` / `r_svd` at import time
 _BINDERS = ("", ".algorithms", ".analysis", ".estimators", ".bounds", ".cli")
+
+
+def _translated(pbpqlp, fn):
+    """Run ``fn`` mapping this package's exceptions / warnings to the reference's."""
+    ref_exc = pbpqlp.exceptions
+    with warnings.catch_warnings(record=True) as rec:
+        warnings.simplefilter("always", _exc.RankDeficiencyWarning)
+        try:
+            out = fn()
+        except _exc.DimensionError as e:
+            raise ref_exc.DimensionError(str(e)) from None
+        except _exc.ParameterError as e:
+            raise ref_exc.ParameterError(str(e)) from None
+        except _exc.MatrixInputError as e:
+            raise ref_exc.MatrixInputError(str(e)) from None
+    for w in rec:
+        if issubclass(w.category, _exc.RankDeficiencyWarning):
+            warnings.warn(str(w.message), ref_exc.RankDeficiencyWarning, stacklevel=3)
+        else:
+            warnings.warn_explicit(w.message, w.category, w.filename, w.lineno)
+    return out
+
+
+def make_rsvd_dropin(pbpqlp):
+    """Reference-typed ``r_svd(a, d, q=0, seed=0, reorthonormalize=True)``
+    (algorithms.py:263-292) running on the GPU path."""
+    from . import rsvd as _rsvd
+
+    ref_alg = pbpqlp.algorithms
+
+    def r_svd(a, d, q=0, seed=0, reorthonormalize=True):
+        f = _translated(pbpqlp, lambda: _rsvd.r_svd(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize))
+        sk = f.sketch
+        sketch = ref_alg.SketchRecord(sk.test_matrix, int(seed), sk.d, sk.q, sk.passes_over_a)
+        return ref_alg.RsvdFactors(f.u, f.s, f.v, sketch)
+
+    r_svd.__doc__ = ref_alg.r_svd.__doc__
+    r_svd.__wrapped_gpu__ = True
+    return r_svd
 
 
 def make_dropin(pbpqlp):
@@ -58,18 +98,19 @@ def install(pbpqlp):
     bound ``pbp_qlp``; returns the previous bindings (for ``uninstall``)."""
     import importlib
 
-    dropin = make_dropin(pbpqlp)
+    dropins = {"pbp_qlp": make_dropin(pbpqlp), "r_svd": make_rsvd_dropin(pbpqlp)}
     saved = {}
     for suffix in _BINDERS:
         mod = importlib.import_module(pbpqlp.__name__ + suffix) if suffix else pbpqlp
-        if hasattr(mod, "pbp_qlp"):
-            saved[mod.__name__] = mod.pbp_qlp
-            mod.pbp_qlp = dropin
+        for name, fn in dropins.items():
+            if hasattr(mod, name):
+                saved[(mod.__name__, name)] = getattr(mod, name)
+                setattr(mod, name, fn)
     return saved
 
 
 def uninstall(saved):
     import sys
 
-    for name, fn in saved.items():
-        setattr(sys.modules[name], "pbp_qlp", fn)
+    for (modname, name), fn in saved.items():
+        setattr(sys.modules[modname], name, fn)

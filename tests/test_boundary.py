@@ -117,10 +117,13 @@ def test_integration_shim_maps_errors_to_reference_classes(reference_pkg):
 
     saved = integration.install(reference_pkg)
     try:
-        for name in saved:
-            assert getattr(sys.modules[name], "pbp_qlp").__wrapped_gpu__
+        assert {name for _, name in saved} == {"pbp_qlp", "r_svd"}
+        for modname, name in saved:
+            assert getattr(sys.modules[modname], name).__wrapped_gpu__
         with pytest.raises(reference_pkg.ParameterError):
             reference_pkg.pbp_qlp(np.eye(4), 9)
+        with pytest.raises(reference_pkg.ParameterError):
+            reference_pkg.r_svd(np.eye(4), 9)
         with pytest.raises(reference_pkg.DimensionError):
             reference_pkg.pbp_qlp(np.eye(4), 2, q=-1)
         with pytest.raises(reference_pkg.MatrixInputError):
@@ -128,3 +131,4 @@ def test_integration_shim_maps_errors_to_reference_classes(reference_pkg):
     finally:
         integration.uninstall(saved)
     assert not getattr(reference_pkg.pbp_qlp, "__wrapped_gpu__", False)
+    assert not getattr(reference_pkg.r_svd, "__wrapped_gpu__", False)

@@ -40,7 +40,7 @@ def test_factorize_rejects_other_algorithms_after_validating_a():
     with pytest.raises(ParameterError, match="unknown algorithm"):
         factorize(a, "nope", 2)
     with pytest.raises(ParameterError, match="outside the B200 path"):
-        factorize(a, "r_svd", 2)
+        factorize(a, "cor_utv", 2)
     bad = a.copy()
     bad[0, 0] = np.nan
     with pytest.raises(MatrixInputError):  # analysis.py:140: check_matrix runs before the dispatch
@@ -62,6 +62,7 @@ class TestPbpQlpEstimator:
         from paper_2103_07245_b200.estimators import PbpQlp
 
         return PbpQlp(n_components=8, q=1, seed=0)
+
 
     def test_fit_transform_shapes(self, cuda):
         x = exact_rank_matrix(40, 30, 8, seed=0)
@@ -151,3 +152,36 @@ def test_error_curve_matches_oracle(cuda, shape, d_values, q):
         assert g["d"] == r["d"]
         assert abs(g["frobenius_error"] - r["frobenius_error"]) <= 1e-10 * r["frobenius_error"]
         assert abs(g["spectral_error"] - r["spectral_error"]) <= 1e-8 * r["spectral_error"]
+
+
+@pytest.mark.gpu
+def test_error_curve_r_svd(cuda):
+    """error_curve(a, "r_svd", …): frobenius / spectral error of u·diag(s)·vᵀ."""
+    from oracle.pbp_qlp_oracle import oracle_r_svd, oracle_spectral_norm
+    from paper_2103_07245_b200.analysis import error_curve
+
+    rng = np.random.default_rng(9)
+    a = (rng.standard_normal((400, 25)) * np.geomspace(1, 1e-3, 25)) @ rng.standard_normal((25, 250)) \
+        + 1e-5 * rng.standard_normal((400, 250))
+    for rec in error_curve(a, "r_svd", [8, 20], q=1, seed=3):
+        f = oracle_r_svd(a, rec["d"], q=1, seed=3)
+        res = a - (f["u"] * f["s"]) @ f["v"].T
+        assert abs(rec["frobenius_error"] - np.linalg.norm(res)) <= 1e-9 * np.linalg.norm(res)
+        assert abs(rec["spectral_error"] - oracle_spectral_norm(res)) <= 1e-8 * oracle_spectral_norm(res)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_randomized_svd_estimator_protocol(cuda, seed):
+    """test_estimators.py:36-95 for RandomizedSvd (GPU r_svd): shapes, exact
+    round trip, orthonormal components, spectrum = the oracle's s."""
+    from oracle.pbp_qlp_oracle import oracle_r_svd
+    from paper_2103_07245_b200.estimators import RandomizedSvd
+
+    x = exact_rank_matrix(40, 30, 8, seed=seed)
+    est = RandomizedSvd(n_components=8, q=1, seed=0)
+    coords = est.fit_transform(x)
+    assert coords.shape == (40, 8) and est.components_.shape == (8, 30)
+    assert np.linalg.norm(x - est.inverse_transform(coords), 2) <= 1e-9 * np.linalg.norm(x, 2)
+    np.testing.assert_allclose(est.components_ @ est.components_.T, np.eye(8), atol=1e-10)
+    np.testing.assert_allclose(est.singular_values_, oracle_r_svd(x, 8, q=1, seed=0)["s"], rtol=1e-10)

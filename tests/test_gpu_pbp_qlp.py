@@ -138,6 +138,13 @@ def test_integration_shim_returns_reference_types(cuda):
         first_stage_r: Any
         sketch: Any = None
 
+    @dataclass(frozen=True)
+    class RsvdFactors:
+        u: Any
+        s: Any
+        v: Any
+        sketch: Any
+
     class ParameterError(ValueError):
         pass
 
@@ -151,7 +158,8 @@ def test_integration_shim_returns_reference_types(cuda):
         pass
 
     fake = types.SimpleNamespace(
-        algorithms=types.SimpleNamespace(SketchRecord=SketchRecord, QlpFactors=QlpFactors, pbp_qlp=lambda *a, **k: None),
+        algorithms=types.SimpleNamespace(SketchRecord=SketchRecord, QlpFactors=QlpFactors, RsvdFactors=RsvdFactors,
+                                         pbp_qlp=lambda *a, **k: None, r_svd=lambda *a, **k: None),
         exceptions=types.SimpleNamespace(ParameterError=ParameterError, DimensionError=DimensionError,
                                          MatrixInputError=MatrixInputError, RankDeficiencyWarning=RankDeficiencyWarning),
     )
@@ -163,6 +171,12 @@ def test_integration_shim_returns_reference_types(cuda):
     assert f.sketch.passes_over_a == 4 and f.sketch.test_matrix.shape == (200, 16)
     with pytest.raises(ParameterError):
         fn(a, 500)
+    rs = integration.make_rsvd_dropin(fake)
+    g = rs(a, 16, q=1, seed=3)
+    assert isinstance(g, RsvdFactors) and isinstance(g.sketch, SketchRecord)
+    assert g.sketch.passes_over_a == 4 and g.sketch.test_matrix.shape == (120, 16) and g.u.shape == (200, 16)
+    with pytest.raises(ParameterError):
+        rs(a, 500)
     low = rng.standard_normal((200, 3)) @ rng.standard_normal((3, 120))
     with pytest.warns(RankDeficiencyWarning):
         fn(low, 10)

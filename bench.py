@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--d", type=int, default=None, help="override the workload's d (config-5 d-sweep)")
+    ap.add_argument("--q", type=int, default=None, help="override the workload's q")
     ap.add_argument("--path", default="pbp_qlp", choices=["pbp_qlp", "r_svd"],
                     help="r_svd: the sibling randomized SVD (SURVEY §8 f3), single GPU")
     return ap.parse_args()
@@ -157,7 +159,7 @@ def run_reference(args, world, rank):
 
     from paper_2103_07245_b200 import workloads
 
-    wl = workloads.CONFIGS[args.workload]
+    wl = workload(args)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     a = workloads.make(args.workload, args.seed, dev).cpu().numpy()
     res = time_cpu_oracle(a, wl, args.seed, args.steps, budget_s=180.0)
@@ -171,6 +173,18 @@ def run_reference(args, world, rank):
         "e2e": {"value": res["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def workload(args):
+    """BASELINE config, with optional --d / --q overrides (the config-5 sweep)."""
+    from paper_2103_07245_b200 import workloads
+
+    wl = dict(workloads.CONFIGS[args.workload])
+    if args.d is not None:
+        wl["d"] = args.d
+    if args.q is not None:
+        wl["q"] = args.q
+    return wl
 
 
 def config_dict(args, wl, world):
@@ -192,7 +206,7 @@ def run_ours(args, world, rank, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    wl = workloads.CONFIGS[args.workload]
+    wl = workload(args)
     n1, n2, d, q = wl["n1"], wl["n2"], wl["d"], wl["q"]
     flops = pbp_qlp_flops(n1, n2, d, q)
 
@@ -331,7 +345,7 @@ def run_rsvd(args):
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    wl = workloads.CONFIGS[args.workload]
+    wl = workload(args)
     n1, n2, d, q = wl["n1"], wl["n2"], wl["d"], wl["q"]
     flops = r_svd_flops(n1, n2, d, q)
     a = workloads.make(args.workload, args.seed, dev)

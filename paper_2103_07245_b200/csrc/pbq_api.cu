@@ -116,7 +116,7 @@ struct Carve {
 // ---------------------------------------------------------------- GEMM ----
 // Two tile shapes: d ≤ 64 uses 128×64 (warp 32×32), larger d 128×128 (warp 64×32).
 // Tile configurations (BM×BN, BK, warps × warp tile, stages):
-//   N ≤ 64 : 128×64,  BK 32, 8 warps of 32×32, 3 stages
+//   N ≤ 64 : 128×64,  BK 32, 16 warps of 32×16, 3 stages
 //   N > 64 : 128×128, BK 32, 16 warps of 32×32, 3 stages.  Four warps per
 //            scheduler hide the fragment-load latency that left the DMMA pipe
 //            idle with 8 warps of 64×32 (33.2 → 35.0 TFLOP/s at config 3).
@@ -127,8 +127,10 @@ struct Carve {
 #endif
 #if PBQ_GEMM_WARPS16
 constexpr int GEMM_WM = 32;
+constexpr int GEMM_WN64 = 16;  // 128×64 tile: 16 warps of 32×16 (31.7 → 33.2 TFLOP/s at d = 64)
 #else
 constexpr int GEMM_WM = 64;
+constexpr int GEMM_WN64 = 32;
 #endif
 #ifndef PBQ_GEMM_RING
 #define PBQ_GEMM_RING 1  // mbarrier k-block ring (gemm_f64_ring) instead of a CTA barrier per k-block
@@ -211,7 +213,7 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   size_t smem;
   int threads;
   if (pl.bn == 64) {
-    using K_ = GemmKernel<TRANS, 128, 64, 32, 32, 32, 3>;
+    using K_ = GemmKernel<TRANS, 128, 64, 32, 32, GEMM_WN64, 3>;
     fn = K_::fn(nonfinite != nullptr); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
   } else {
     using K_ = GemmKernel<TRANS, 128, 128, 32, GEMM_WM, 32, 3>;
@@ -365,8 +367,8 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
   size_t smem;
   int threads;
   if (pl.bn == 64) {
-    using C_ = GemmCfg<true, 128, 64, 32, 32, 32, 3>;
-    fn = GemmKernel<true, 128, 64, 32, 32, 32, 3>::split_fn();
+    using C_ = GemmCfg<true, 128, 64, 32, 32, GEMM_WN64, 3>;
+    fn = GemmKernel<true, 128, 64, 32, 32, GEMM_WN64, 3>::split_fn();
     smem = C_::SMEM_BYTES; threads = C_::THREADS;
   } else {
     using C_ = GemmCfg<true, 128, 128, 32, GEMM_WM, 32, 3>;
@@ -637,8 +639,8 @@ int resid_launch(pbq_ctx* ctx, long n1, long n2, long k, const double* A, long l
   size_t smem;
   int threads;
   if (pl.bn == 64) {
-    using C_ = GemmCfg<false, 128, 64, 32, 32, 32, 3>;
-    fn = reinterpret_cast<void*>(&gemm_f64_ring<false, 128, 64, 32, 32, 32, 3, false, false, true>);
+    using C_ = GemmCfg<false, 128, 64, 32, 32, GEMM_WN64, 3>;
+    fn = reinterpret_cast<void*>(&gemm_f64_ring<false, 128, 64, 32, 32, GEMM_WN64, 3, false, false, true>);
     smem = C_::SMEM_BYTES; threads = C_::THREADS;
   } else {
     using C_ = GemmCfg<false, 128, 128, 32, GEMM_WM, 32, 3>;

@@ -79,9 +79,11 @@ int pbq_gemm_workspace_bytes(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, size
  * If rank_flag is non-null it receives the `orth` rank test
  * (linalg.py:142-165): 0 full rank, 1 some |R_ii| < 1e-14·|R_00|, 2 R_00 == 0.
  * Method (pbq_set_qr_method): by default a guarded whole-matrix Cholesky-QR2
- * (same unique factors for full-rank A, to rounding) that hands the call to
- * the blocked Householder kernel on the device whenever κ₁(R₁) > 1e6 or a
- * pivot fails; method 1 forces the Householder kernel. */
+ * (same unique factors for full-rank A, to rounding).  When κ₁(R₁) > 1e6 or
+ * a pivot fails it continues, for n ≥ 384, with shifted Cholesky-QR3, and
+ * otherwise (or if that fails too) hands the call to the blocked
+ * Householder kernel, all decided on the device; method 1 forces the
+ * Householder kernel. */
 int pbq_householder_qr(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, double* R,
                        int64_t ldr, int32_t want_q, int32_t* rank_flag, void* workspace,
                        size_t workspace_bytes, void* stream);
@@ -181,9 +183,10 @@ int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns, uin
 #define PBQ_QR_CHOLQR_NOSERIES 2
 int pbq_set_qr_method(pbq_ctx* ctx, int32_t method);
 
-/* Debug counters (device int[3], NULL to disable): QR calls completed by
- * Cholesky-QR2, calls handed to the Householder fallback, and completed
- * calls whose second pass used the near-identity series. */
+/* Debug counters (device int[4], NULL to disable): QR calls completed by
+ * Cholesky-QR, calls handed to the Householder fallback, completed calls
+ * whose last pass used the near-identity series, and calls completed by the
+ * shifted Cholesky-QR3 route (n ≥ 384 after a failed first pass). */
 int pbq_debug_cholqr_stats(pbq_ctx* ctx, int32_t* stats);
 
 #ifdef __cplusplus

@@ -47,8 +47,10 @@ constexpr double CQ_SERIES_EMAX = 1e-5;
 __global__ void __launch_bounds__(256) cholqr_gram_reduce(const double* __restrict__ part, int S, int ntiles,
                                                           int tiles_n, int sym, int bm, int bn, long n, long np,
                                                           double* __restrict__ G, const int* skip,
-                                                          unsigned long long* emax) {
-  if (__ldcg(skip) != 0) return;
+                                                          unsigned long long* emax, const int* run_if,
+                                                          double* __restrict__ Gcopy) {
+  if (skip && __ldcg(skip) != 0) return;
+  if (run_if && __ldcg(run_if) == 0) return;
   __shared__ double s_part[8][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long tile_elems = long(bm) * bn;
@@ -86,6 +88,7 @@ __global__ void __launch_bounds__(256) cholqr_gram_reduce(const double* __restri
       if (r < np && c < np) {
         if (r >= n || c >= n) g = (r == c) ? 1.0 : 0.0;
         G[r * np + c] = g;
+        if (Gcopy) Gcopy[r * np + c] = g;
         const double d = fabs(g - (r == c ? 1.0 : 0.0));
         dev = (d <= dev) ? dev : d;  // NaN sticks
       }
@@ -121,10 +124,19 @@ struct CqArgs {
   double* colsum;     // pass 1: [2][nb][np] per-block column |·| sums of R and X
   const unsigned long long* emax;  // pass 2: max|G − I| (bits), from the reduce
   unsigned int* counter;
-  int* stats;         // optional [CholQR2 done, fallbacks, pass 2 by the series]
+  int* stats;         // optional [done, Householder fallbacks, pass 2 by the series, done by the shifted route]
   double kappa_max;
   unsigned long long* phase_ns;  // optional profiling: [pass-1 slots 0..3, pass-2 slots 4..7]
   int allow_series;              // 0: always the blocked Cholesky (test hook)
+  // shifted Cholesky-QR3 route (n ≥ CQ_EXT_MIN_N; null/0 otherwise):
+  int* shift_req;   // pass 1: a failed guard or pivot requests the route (instead of Householder)
+  int* route;       // route kernels run while *route != 0; a failure clears it
+  int* hh_req;      // set → the Householder kernel runs
+  int shift_mode;   // 1: G += s·I, s = 11(mn + n(n+1))·u·trace(G); no κ guard
+  long m;           // rows of the factored matrix (for the shift)
+  int rout_full;    // 1: write Rout over the padded np×np (an intermediate product)
+  int route_final;  // 1: last factorization of the shifted route (stats[3] counts it)
+  int* fail_stats;  // optional: stats[1] counts hand-overs to Householder (also from intermediate passes)
 };
 
 #define CQ_MARK(slot)                                                                  \
@@ -392,7 +404,20 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
   double* sT = pairs + 3 * CQ_BLK;
   __shared__ int s_ok;
   __shared__ __align__(16) double s_rowbuf[64];
-  if (__ldcg(p.fallback) != 0) return;  // uniform: written by an earlier launch
+  if (p.fallback && __ldcg(p.fallback) != 0) return;  // uniform: written by an earlier launch
+  if (p.route && __ldcg(p.route) == 0) return;
+  // a failed factorization: pass 1 of the extended chain asks for the shifted
+  // route, anything else hands the call to the Householder kernel
+  auto fail_all = [&]() {
+    if (p.pass == 1 && !p.shift_mode && p.shift_req) {
+      *p.shift_req = 1;
+    } else {
+      if (p.hh_req) *p.hh_req = 1;
+      if (p.fail_stats) atomicAdd(p.fail_stats + 1, 1);
+    }
+    if (p.fallback) *p.fallback = 1;
+    if (p.route) *p.route = 0;
+  };
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nb = p.nb;
   const long np = p.np;
@@ -401,6 +426,19 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
   unsigned long long t_mark = 0;
   if (p.phase_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_mark));
 
+  double shift = 0.0;
+  if (pass1 && p.shift_mode) {  // s = 11(mn + n(n+1))·u·‖A‖_F², ‖A‖_F² = trace(G) (fixed order in every CTA)
+    __shared__ double s_tr[CQ_THREADS / 32];
+    double tr = 0.0;
+    for (long i = tid; i < p.n; i += CQ_THREADS) tr += __ldcg(p.G + i * np + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    if ((tid & 31) == 0) s_tr[warp] = tr;
+    __syncthreads();
+    tr = 0.0;
+    for (int w = 0; w < CQ_THREADS / 32; ++w) tr += s_tr[w];
+    shift = 11.0 * (double(p.m) * double(p.n) + double(p.n) * double(p.n + 1)) * 1.1102230246251565e-16 * tr;
+  }
   bool series = false;
   if (!pass1 && p.allow_series) {
     const double em = __longlong_as_double(static_cast<long long>(__ldcg(p.emax)));
@@ -456,13 +494,14 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
         upper_tile(w - n_up, nb, i, j);
         cq_block_sum<false>(c, Xs, p.R1, np, i, j, i, j, pairs);
         const long r = long(i) * 32 + cq_row();
-        if (r < p.n) {
+        const long lim = p.rout_full ? np : p.n;
+        if (r < lim) {
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const long col = long(j) * 32 + cq_col(h) + e;
-              if (col < p.n)
+              if (col < lim)
                 p.Rout[r * p.ldr + col] = (col >= r) ? __ldcg(p.R1 + r * np + col) + c[h][e] : 0.0;
             }
         }
@@ -470,9 +509,10 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
         int i, j;  // strictly lower block (i > j): zeros
         upper_tile(w - 2 * n_up, nb - 1, j, i);
         i += 1;
+        const long lim = p.rout_full ? np : p.n;
         for (int e = tid; e < 1024; e += CQ_THREADS) {
           const long r = long(i) * 32 + e / 32, col = long(j) * 32 + e % 32;
-          if (r < p.n && col < p.n) p.Rout[r * p.ldr + col] = 0.0;
+          if (r < lim && col < lim) p.Rout[r * p.ldr + col] = 0.0;
         }
       }
     }
@@ -493,6 +533,7 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
         if (p.stats) {
           atomicAdd(p.stats, 1);
           atomicAdd(p.stats + 2, 1);
+          if (p.route_final) atomicAdd(p.stats + 3, 1);
         }
       }
     }
@@ -518,16 +559,18 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
+    if (shift != 0.0) {  // G_kk + s·I (the Schur updates commute with the shift); after the barrier:
+      // a thread's cp.async wait covers only its own copies
+      if (tid < 32 && k * 32 + tid < p.n) sKK[tid * CQ_LD + tid] += shift;
+      __syncthreads();
+    }
     if (warp == 0) {
       const bool ok = cq_chol_inv32_warp(sKK, sKI, s_rowbuf);
       if (tid == 0) s_ok = ok;
     }
     __syncthreads();
     if (!s_ok) {  // identical in every CTA (same data, same code): all leave together
-      if (blockIdx.x == 0 && tid == 0) {
-        *p.fallback = 1;
-        if (p.stats) atomicAdd(p.stats + 1, 1);
-      }
+      if (blockIdx.x == 0 && tid == 0) fail_all();
       return;
     }
     if (blockIdx.x == gridDim.x - 1) {  // the last CTA has the fewest items; CTA 0 carries (k+1, k+1)
@@ -585,10 +628,7 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
           mx = fmax(mx, s_max[1][w]);
         }
         const double kappa = mr * mx;
-        if (!(kappa <= p.kappa_max)) {
-          *p.fallback = 1;
-          if (p.stats) atomicAdd(p.stats + 1, 1);
-        }
+        if (!p.shift_mode && !(kappa <= p.kappa_max)) fail_all();
       }
     }
     return;
@@ -603,13 +643,14 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
       cq_zero(c);
       if (i <= j) cq_block_sum<false>(c, p.R, p.R1, np, i, j, i, j, pairs);
       const long r = long(i) * 32 + cq_row();
-      if (r < p.n) {
+      const long lim = p.rout_full ? np : p.n;
+      if (r < lim) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const long col = long(j) * 32 + cq_col(h) + e;
-            if (col < p.n) p.Rout[r * p.ldr + col] = (col >= r) ? c[h][e] : 0.0;
+            if (col < lim) p.Rout[r * p.ldr + col] = (col >= r) ? c[h][e] : 0.0;
           }
       }
     }
@@ -627,7 +668,10 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
     __syncthreads();
     if (tid == 0) {
       if (p.rank_flag) *p.rank_flag = (d0 == 0.0) ? 2 : s_def;
-      if (p.stats) atomicAdd(p.stats, 1);
+      if (p.stats) {
+        atomicAdd(p.stats, 1);
+        if (p.route_final) atomicAdd(p.stats + 3, 1);
+      }
     }
   }
 }

@@ -45,6 +45,7 @@ struct GemmArgs {
   // single tile).  A separate kernel sums the slices in fixed order.
   int split, sym, units;
   const int* skip;   // when non-null and *skip != 0 the launch is a no-op
+  const int* run_if; // when non-null and *run_if == 0 the launch is a no-op
   // tri_b: B is upper triangular (K == N), so output column tile tn only
   // needs k < (tn+1)·BN — the stream-K space then has row_iters =
   // Σ_tn k-blocks(tn) iterations per row of tiles (total_iters = tiles_m·row_iters)
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   if (p.skip && __ldcg(p.skip) != 0) return;
+  if (p.run_if && __ldcg(p.run_if) == 0) return;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;

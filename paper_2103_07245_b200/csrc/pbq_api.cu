@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/pbq.h"
@@ -187,7 +188,7 @@ size_t gemm_ws_bytes(const GemmPlan& p) {
 template <bool TRANS>
 int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double* A, long lda, const double* B,
                 long ldb, double beta, double* C, long ldc, int32_t* nonfinite, void* ws, size_t ws_bytes,
-                cudaStream_t st, const int* skip = nullptr, bool tri_b = false) {
+                cudaStream_t st, const int* skip = nullptr, bool tri_b = false, const int* run_if = nullptr) {
   if (M <= 0 || N <= 0 || K < 0) return fail(ctx, PBQ_ERR_DIM, "gemm: bad shape M=%ld N=%ld K=%ld", M, N, K);
   if ((lda & 1) || (ldb & 1) || (ldc & 1) || !aligned16(A) || !aligned16(B) || !aligned16(C))
     return fail(ctx, PBQ_ERR_PARAM, "gemm: leading dimensions must be even and pointers 16-byte aligned");
@@ -207,6 +208,7 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   a.split = 0; a.sym = 0; a.units = 0;
   a.skip = skip;
   a.tri_b = tri_b; a.row_iters = pl.row_iters;
+  a.run_if = run_if;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gemm: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
   void* fn;
@@ -346,14 +348,22 @@ CqPlan cq_plan(const pbq_ctx* ctx, long m, long n) {
   return p;
 }
 
+// n ≥ this: the chain also carries the shifted Cholesky-QR3 route, so an
+// ill-conditioned input stays on GEMM-shaped passes instead of falling back
+// to the Householder kernel (whose column-by-column panel fallback needs its
+// rows resident in shared memory, which large n does not allow)
+constexpr long CQ_EXT_MIN_N = 384;
+
 size_t cq_ws_bytes(const CqPlan& p, const QrPlan& hp, long m, long n) {
   const size_t sq = align_up(size_t(p.np) * p.np * sizeof(double), 256);
-  return 256 + 6 * sq + align_up(2 * size_t(p.nb) * p.np * sizeof(double), 256) + align_up(p.gemm_ws, 256) +
-         align_up(size_t(m) * p.ldq1 * sizeof(double), 256) + qr_ws_bytes(hp, n) + 1024;
+  const size_t thin = align_up(size_t(m) * p.ldq1 * sizeof(double), 256);
+  const bool ext = n >= CQ_EXT_MIN_N;
+  return 256 + 6 * sq + align_up(2 * size_t(p.nb) * p.np * sizeof(double), 256) + align_up(p.gemm_ws, 256) + thin +
+         (ext ? 2 * sq + thin : 0) + qr_ws_bytes(hp, n) + 1024;
 }
 
 int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X, long ldx, double* part,
-                const int* skip, cudaStream_t st) {
+                const int* skip, cudaStream_t st, const int* run_if = nullptr) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.M = n; a.N = n; a.K = m;
@@ -363,6 +373,7 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
   a.partials = part;
   a.split = pl.S; a.sym = pl.ntiles > 1; a.units = pl.units;
   a.skip = skip;
+  a.run_if = run_if;
   void* fn;
   size_t smem;
   int threads;
@@ -385,11 +396,12 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
 }
 
 int gram_reduce_launch(pbq_ctx* ctx, const CqPlan& pl, long n, const double* part, double* G, const int* skip,
-                       unsigned long long* emax, cudaStream_t st) {
+                       unsigned long long* emax, cudaStream_t st, const int* run_if = nullptr,
+                       double* gcopy = nullptr) {
   const long total = long(pl.ntiles) * pl.bm * pl.bn;
   const int grid = int(std::min<long>(ceil_div(total, 32), 8L * ctx->sms));
   cholqr_gram_reduce<<<grid, 256, 0, st>>>(part, pl.S, pl.ntiles, pl.tiles_n, pl.ntiles > 1, pl.bm, pl.bn, n, pl.np,
-                                            G, skip, emax);
+                                            G, skip, emax, run_if, gcopy);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 1;
   return PBQ_OK;
@@ -406,6 +418,18 @@ int factor_launch(pbq_ctx* ctx, const CqPlan& pl, CqArgs& a, cudaStream_t st) {
   return PBQ_OK;
 }
 
+// PBQ_DEBUG_SYNC=1: synchronise and report after each launch of the chain (debugging only)
+#define CQ_DEBUG_SYNC(what)                                                                      \
+  do {                                                                                           \
+    static const bool on_ = getenv("PBQ_DEBUG_SYNC") != nullptr;                                 \
+    if (on_) {                                                                                   \
+      cudaError_t e_ = cudaStreamSynchronize(st);                                                \
+      int h_[16];                                                                                \
+      cudaMemcpy(h_, ctl + 8, sizeof(h_), cudaMemcpyDeviceToHost);                               \
+      fprintf(stderr, "cq %s: %s fallback=%d route=%d hh=%d\n", what, cudaGetErrorString(e_), 0, h_[2], h_[4]); \
+    }                                                                                            \
+  } while (0)
+
 int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int32_t* rank_flag, void* ws,
               size_t ws_bytes, cudaStream_t st) {
   QrPlan hp;
@@ -413,9 +437,13 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "qr: leading dimension too small");
   if ((lda & 1) || !aligned16(A)) return fail(ctx, PBQ_ERR_PARAM, "qr: lda must be even and A 16-byte aligned");
   const CqPlan pl = cq_plan(ctx, m, n);
+  const bool ext = n >= CQ_EXT_MIN_N;
   const size_t sq = size_t(pl.np) * pl.np;
   Carve cv(ws, ws_bytes);
-  int* ctl = cv.take<int>(64);  // [0] fallback flag, [1] [2] grid-barrier counters, [4:6] max|G₂ − I|
+  // ctl: [0] fallback (stops the CholQR2 path), [1] [2] [16] [17] [18] grid-barrier
+  // counters, [4:6] [20:22] [22:24] max|G − I| slots, [10] shifted route running,
+  // [12] Householder requested (extended chain)
+  int* ctl = cv.take<int>(64);
   double* X1 = cv.take<double>(sq);
   double* X2 = cv.take<double>(sq);
   const size_t zero_bytes = size_t(reinterpret_cast<char*>(X2 + sq) - reinterpret_cast<char*>(ctl));
@@ -426,40 +454,91 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   double* colsum = cv.take<double>(2 * size_t(pl.nb) * pl.np);
   char* gws = cv.take<char>(pl.gemm_ws);
   double* Q1 = cv.take<double>(size_t(m) * pl.ldq1);
+  double* Gc = ext ? cv.take<double>(sq) : nullptr;     // copy of G₁ for the shifted factorization
+  double* Racc = ext ? cv.take<double>(sq) : nullptr;   // R₂·R₁ of the route
+  double* Q2 = ext ? cv.take<double>(size_t(m) * pl.ldq1) : nullptr;
   const size_t hws_bytes = qr_ws_bytes(hp, n);
   char* hws = cv.take<char>(hws_bytes);
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   int* fallback = ctl;
+  int* route = ctl + 10;
+  int* hh_req = ctl + 12;
   PBQ_CUDA(ctx, cudaMemsetAsync(ctl, 0, zero_bytes, st));
 
   ProfScope ps(ctx->prof, st, 1);
   ProfSuppress quiet(ctx->prof);
   double* part = reinterpret_cast<double*>(gws);
+  auto counter = [&](int i) { return reinterpret_cast<unsigned int*>(ctl + i); };
+  auto emax_slot = [&](int i) { return reinterpret_cast<unsigned long long*>(ctl + i); };
   CqArgs f;
   memset(&f, 0, sizeof(f));
-  f.nb = pl.nb; f.n = n; f.np = pl.np;
+  f.nb = pl.nb; f.n = n; f.np = pl.np; f.m = m;
   f.G = G; f.T = T; f.fallback = fallback;
-  unsigned long long* emax = reinterpret_cast<unsigned long long*>(ctl + 4);
-  f.emax = emax; f.colsum = colsum; f.stats = ctx->cq_stats; f.kappa_max = CQ_KAPPA_MAX;
+  f.emax = emax_slot(4); f.colsum = colsum; f.stats = ctx->cq_stats; f.fail_stats = ctx->cq_stats;
+  f.kappa_max = CQ_KAPPA_MAX;
   f.phase_ns = ctx->qr_phase_ns;
   f.allow_series = ctx->qr_method != PBQ_QR_CHOLQR_NOSERIES;
-  // pass 1
+  if (ext) {
+    f.shift_req = route;  // pass 1 failing → the shifted route
+    f.hh_req = hh_req;
+  }
+  // ---- Cholesky-QR2
   PBQ_TRY(gram_launch(ctx, pl, m, n, A, lda, part, fallback, st));
-  PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, nullptr, st));
-  f.pass = 1; f.R = R1; f.X = X1; f.counter = reinterpret_cast<unsigned int*>(ctl + 1);
+  PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, nullptr, st, nullptr, Gc));
+  f.pass = 1; f.R = R1; f.X = X1; f.counter = counter(1);
   PBQ_TRY(factor_launch(ctx, pl, f, st));
   PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
                              fallback, true));
-  // pass 2
   PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st));
-  PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, emax, st));
+  PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, emax_slot(4), st));
   f.pass = 2; f.R = R2; f.X = X2; f.R1 = R1; f.Rout = R; f.ldr = ldr; f.rank_flag = rank_flag;
-  f.counter = reinterpret_cast<unsigned int*>(ctl + 2);
+  f.counter = counter(2);
+  f.shift_req = nullptr;
   PBQ_TRY(factor_launch(ctx, pl, f, st));
   PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q1, pl.ldq1, X2, pl.np, 0.0, A, lda, nullptr, gws, pl.gemm_ws, st,
                              fallback, true));
-  // Householder fallback (returns immediately unless the guard fired)
-  return hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, fallback);
+  CQ_DEBUG_SYNC("cholqr2 done");
+  if (ext) {
+    // ---- shifted Cholesky-QR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto,
+    // Yanagisawa 2020), only when pass 1 failed: R₁ = chol(G₁ + s·I),
+    // Q₁ = A·R₁⁻¹, then two Cholesky-QR passes Q₁ → Q₂ → Q.  Every launch
+    // returns at once unless *route; a failure clears it and asks for the
+    // Householder kernel.  A is only written by the last product.
+    CqArgs g = f;
+    g.fallback = nullptr; g.route = route; g.hh_req = hh_req; g.shift_req = nullptr;
+    g.pass = 1; g.shift_mode = 1; g.G = Gc; g.R = R1; g.X = X1; g.counter = counter(16);
+    g.Rout = nullptr; g.rank_flag = nullptr; g.R1 = nullptr;
+    PBQ_TRY(factor_launch(ctx, pl, g, st));
+    CQ_DEBUG_SYNC("route 1");
+    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
+                               nullptr, true, route));
+    CQ_DEBUG_SYNC("route 2");
+    PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, nullptr, st, route));
+    CQ_DEBUG_SYNC("route 3");
+    PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, nullptr, emax_slot(20), st, route));
+    CQ_DEBUG_SYNC("route 4");
+    g.pass = 2; g.shift_mode = 0; g.G = G; g.R = R2; g.X = X2; g.R1 = R1; g.emax = emax_slot(20);
+    g.Rout = Racc; g.ldr = pl.np; g.rout_full = 1; g.rank_flag = nullptr; g.stats = nullptr; g.counter = counter(17);
+    PBQ_TRY(factor_launch(ctx, pl, g, st));
+    CQ_DEBUG_SYNC("route 5");
+    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q1, pl.ldq1, X2, pl.np, 0.0, Q2, pl.ldq1, nullptr, gws, pl.gemm_ws,
+                               st, nullptr, true, route));
+    CQ_DEBUG_SYNC("route 6");
+    PBQ_TRY(gram_launch(ctx, pl, m, n, Q2, pl.ldq1, part, nullptr, st, route));
+    CQ_DEBUG_SYNC("route 7");
+    PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, nullptr, emax_slot(22), st, route));
+    CQ_DEBUG_SYNC("route 8");
+    g.R = R1; g.X = X1; g.R1 = Racc; g.emax = emax_slot(22);   // R = R₃·(R₂·R₁)
+    g.Rout = R; g.ldr = ldr; g.rout_full = 0; g.rank_flag = rank_flag; g.stats = ctx->cq_stats;
+    g.route_final = 1; g.counter = counter(18);
+    PBQ_TRY(factor_launch(ctx, pl, g, st));
+    CQ_DEBUG_SYNC("route 9");
+    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q2, pl.ldq1, X1, pl.np, 0.0, A, lda, nullptr, gws, pl.gemm_ws, st,
+                               nullptr, true, route));
+    CQ_DEBUG_SYNC("route 10");
+  }
+  // Householder fallback (returns immediately unless a factorization failed)
+  return hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, ext ? hh_req : fallback);
 }
 
 size_t qr_any_ws_bytes(const pbq_ctx* ctx, const QrPlan& hp, long m, long n) {

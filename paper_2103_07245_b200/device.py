@@ -51,7 +51,8 @@ class Context:
             self.check(self.lib.pbq_set_qr_method(self.handle, int(method)), "set_qr_method")
 
     def cholqr_stats(self, stats):
-        """Count [Cholesky-QR2 completions, Householder fallbacks, series pass 2] into the
+        """Count [Cholesky-QR completions, Householder fallbacks, series last pass,
+        shifted-route completions] into the
         int32 device tensor ``stats`` (None to stop)."""
         with self.lock:
             self.check(self.lib.pbq_debug_cholqr_stats(self.handle, ptr(stats)), "cholqr_stats")

@@ -110,7 +110,7 @@ def test_qr_rank_flags(cuda, qr_method):
 def _cholqr_counts(ctx, cuda, x):
     from paper_2103_07245_b200 import device as D
 
-    stats = torch.zeros(3, dtype=torch.int32, device=cuda)
+    stats = torch.zeros(4, dtype=torch.int32, device=cuda)
     ctx.cholqr_stats(stats)
     try:
         t = _dev_matrix(x, cuda)
@@ -120,6 +120,34 @@ def _cholqr_counts(ctx, cuda, x):
         return stats.tolist(), t.cpu().numpy(), r.cpu().numpy(), int(flag.item())
     finally:
         ctx.cholqr_stats(None)
+
+
+def test_shifted_cholqr3_route(cuda):
+    """n ≥ 384: an input that fails the κ₁ guard goes through the shifted
+    Cholesky-QR3 route (still GEMM-shaped passes) instead of the Householder
+    kernel; only an exactly singular one reaches Householder."""
+    from paper_2103_07245_b200 import device as D
+
+    ctx = D.context(cuda)
+    ctx.set_qr_method(ctx.QR_AUTO)
+    rng = np.random.default_rng(11)
+    for m, n, logk in ((4000, 400, 10), (512, 512, 9), (3000, 416, 12)):
+        u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+        v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        x = (u * np.logspace(0, -logk, n)) @ v.T
+        counts, q, r, flag = _cholqr_counts(ctx, cuda, x)
+        assert counts == [1, 0, counts[2], 1], (m, n, counts)
+        qr_, rr = oracle_qr(x)
+        assert flag == rank_flag(rr) == 0
+        kj = np.abs(rr[0, 0]) / np.abs(np.diag(rr))
+        tol = np.maximum(1e-10, 64 * 2.0**-53 * kj)
+        assert np.all(column_relative_error(q, qr_) <= tol), (m, n)
+        assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
+    # exactly rank deficient: the shifted route's later passes fail → Householder
+    b = rng.standard_normal((2000, 400))
+    b[:, 200:] = b[:, :200] @ rng.standard_normal((200, 200))
+    counts, q, r, flag = _cholqr_counts(ctx, cuda, b)
+    assert counts[1] == 1 and counts[0] == 0 and flag == 1
 
 
 def test_cholqr_path_and_guard(cuda):
@@ -134,19 +162,19 @@ def test_cholqr_path_and_guard(cuda):
     rng = np.random.default_rng(5)
     u, _ = np.linalg.qr(rng.standard_normal((3000, 96)))
     v, _ = np.linalg.qr(rng.standard_normal((96, 96)))
-    # expected [CholQR2 done, fallbacks, pass 2 by the near-identity series];
+    # expected [done, Householder fallbacks, pass 2 by the near-identity series, done by the shifted route];
     # method 2 forces the blocked Cholesky in pass 2 (its safety path: the κ₁
     # guard fires long before G₂ stops being near the identity)
     cases = [
-        ("gaussian", rng.standard_normal((3000, 96)), [1, 0, 1], 0),
-        ("graded 1e-4", rng.standard_normal((3000, 96)) * np.logspace(0, -4, 96), [1, 0, 1], 0),
-        ("kappa 1e5", (u * np.logspace(0, -5, 96)) @ v.T, [1, 0, 1], 0),
-        ("kappa 1e12", (u * np.logspace(0, -12, 96)) @ v.T, [0, 1, 0], 0),
-        ("rank deficient", np.hstack([u[:, :40], u[:, :40] @ rng.standard_normal((40, 56))]), [0, 1, 0], 0),
-        ("zero", np.zeros((300, 40)), [0, 1, 0], 0),
-        ("gaussian, no series", rng.standard_normal((3000, 96)), [1, 0, 0], 2),
-        ("kappa 1e5, no series", (u * np.logspace(0, -5, 96)) @ v.T, [1, 0, 0], 2),
-        ("300x257, no series", rng.standard_normal((300, 257)), [1, 0, 0], 2),
+        ("gaussian", rng.standard_normal((3000, 96)), [1, 0, 1, 0], 0),
+        ("graded 1e-4", rng.standard_normal((3000, 96)) * np.logspace(0, -4, 96), [1, 0, 1, 0], 0),
+        ("kappa 1e5", (u * np.logspace(0, -5, 96)) @ v.T, [1, 0, 1, 0], 0),
+        ("kappa 1e12", (u * np.logspace(0, -12, 96)) @ v.T, [0, 1, 0, 0], 0),
+        ("rank deficient", np.hstack([u[:, :40], u[:, :40] @ rng.standard_normal((40, 56))]), [0, 1, 0, 0], 0),
+        ("zero", np.zeros((300, 40)), [0, 1, 0, 0], 0),
+        ("gaussian, no series", rng.standard_normal((3000, 96)), [1, 0, 0, 0], 2),
+        ("kappa 1e5, no series", (u * np.logspace(0, -5, 96)) @ v.T, [1, 0, 0, 0], 2),
+        ("300x257, no series", rng.standard_normal((300, 257)), [1, 0, 0, 0], 2),
     ]
     for name, x, expect, method in cases:
         ctx.set_qr_method(method)

@@ -18,7 +18,7 @@ if len(sys.argv) > 1:
     shapes = [tuple(int(v) for v in s.split("x")) for s in sys.argv[1:]]
 dev = torch.device("cuda", 0)
 ctx = D.context(dev)
-stats = torch.zeros(3, dtype=torch.int32, device=dev)
+stats = torch.zeros(4, dtype=torch.int32, device=dev)
 ctx.cholqr_stats(stats)
 
 

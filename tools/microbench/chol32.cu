@@ -82,7 +82,11 @@ __global__ void __launch_bounds__(256, 1) bench_env(double* out, const double* g
       if (threadIdx.x == 0) (void)ld_acquire(flag);
       __syncthreads();
     }
-    if (MODE >= 2) {  // fence + release store by thread 0 (publish)
+    if (MODE == 3) {  // a few nanosleep polls before the factorization
+      for (int r = 0; r < 4; ++r) __nanosleep(64);
+      __syncthreads();
+    }
+    if (MODE == 2) {  // fence + release store by thread 0 (publish)
       out[threadIdx.x & 31] = 1.0;
       __threadfence();
       __syncthreads();
@@ -122,5 +126,8 @@ int main3() {
   printf("env: + acquire poll %lld cycles\n", cy);
   bench_env<2><<<1, 256, smem>>>(o, g, 20, c, fl); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost);
   printf("env: + acquire + fence + release %lld cycles (%s)\n", cy, cudaGetErrorString(cudaGetLastError()));
+  cudaFuncSetAttribute(bench_env<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench_env<3><<<1, 256, smem>>>(o, g, 20, c, fl); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost);
+  printf("env: + acquire + nanosleep %lld cycles (%s)\n", cy, cudaGetErrorString(cudaGetLastError()));
   return 0;
 }

@@ -71,7 +71,7 @@ struct QrArgs {
   unsigned int* counter;
   int* rank_flag;  // may be null
   int* fallbacks;  // may be null: number of panels that took the fallback
-  int* error;      // may be null: set to 1 if a fallback panel met non-resident rows
+  int* error;      // unused (kept for the launch layout); every panel shape is supported
   unsigned long long* phase_ns;  // may be null: CTA-0 time per phase (profiling)
   unsigned long long* bar_wait_ns;  // may be null: per-CTA grid-barrier spin time (profiling)
   const int* run_if;  // may be null; else the kernel runs only when *run_if != 0 (Cholesky-QR fallback)
@@ -656,11 +656,14 @@ __device__ void qr_update_chunk(const QrArgs& p, const QrSmem& s, long cs, long 
 }
 
 // ============ fallback: column-by-column Householder (any jb ≤ 32) ==========
-// Needs the CTA's active rows resident (one chunk, Ps row rr ↔ row ra + rr).
-// On return Ps holds the factored panel (R on/above the pivot diagonal, V
-// below), Ts the T factor and s.beta the signed diagonal.
-__device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* Ts, long k, int jb, long ra,
-                                     long r1, unsigned int& gen) {
+// Works on the CTA's active rows through `P` (row rr ↔ row ra + rr at
+// P + rr·ldp, panel column c at offset c): the shared-memory chunk when the
+// rows are resident, else A itself (global, L2-resident; only the panel's
+// first jb columns of this CTA's rows are touched, and __syncthreads orders
+// them within the CTA).  On return P holds the factored panel (R on/above
+// the pivot diagonal, V below), Ts the T factor and s.beta the signed diagonal.
+__device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* P, long ldp, double* Ts, long k,
+                                     int jb, long ra, long r1, unsigned int& gen) {
   const int tid = threadIdx.x;
   const int G = gridDim.x;
   double* red = s.small;                 // QR_THREADS
@@ -680,13 +683,13 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
       if (c < jb) {
         int rr = int(lmax(0L, piv + 1 - ra)) + grp;
         for (; rr + NG < nrows; rr += 2 * NG) {
-          const double* row0 = s.Ps + rr * QR_PLD;
-          const double* row1 = row0 + NG * QR_PLD;
+          const double* row0 = P + rr * ldp;
+          const double* row1 = row0 + NG * ldp;
           a0 = fma(row0[jj], row0[c], a0);
           a1 = fma(row1[jj], row1[c], a1);
         }
         if (rr < nrows) {
-          const double* row0 = s.Ps + rr * QR_PLD;
+          const double* row0 = P + rr * ldp;
           a0 = fma(row0[jj], row0[c], a0);
         }
       }
@@ -698,7 +701,7 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
 #pragma unroll
       for (int g2 = 0; g2 < QR_THREADS / 32; ++g2) acc += red[g2 * 32 + tid];
       __stcg(p.part + (size_t(buf) * G + blockIdx.x) * 32 + tid, acc);
-      if (piv >= ra && piv < r1) __stcg(p.pivrow + buf * 32 + tid, s.Ps[(piv - ra) * QR_PLD + tid]);
+      if (piv >= ra && piv < r1) __stcg(p.pivrow + buf * 32 + tid, P[(piv - ra) * ldp + tid]);
     }
     grid_barrier(p.counter, gen, p.bar_wait_ns);
     {
@@ -736,7 +739,7 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
     for (int e = tid; e < (nrows - rs) * ncol; e += QR_THREADS) {
       const int rr = rs + e / ncol;
       const int c = jj + e % ncol;
-      double* row = s.Ps + rr * QR_PLD;
+      double* row = P + rr * ldp;
       if (ra + rr == piv) {
         row[c] = (c == jj) ? beta : row[c] - wt[c];
       } else if (c > jj) {
@@ -744,7 +747,7 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* T
       }
     }
     __syncthreads();
-    for (int rr = int(lmax(0L, piv + 1 - ra)) + tid; rr < nrows; rr += QR_THREADS) s.Ps[rr * QR_PLD + jj] *= scale;
+    for (int rr = int(lmax(0L, piv + 1 - ra)) + tid; rr < nrows; rr += QR_THREADS) P[rr * ldp + jj] *= scale;
     __syncthreads();
   }
 }
@@ -936,18 +939,20 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
       }
       QR_PHASE(4);
     } else {
-      // ---- fallback: column-by-column Householder (needs resident rows)
+      // ---- fallback: column-by-column Householder
       ++nfallback;
-      if (!resident) {  // not supported: report loudly, leave the panel as is
-        if (tid == 0 && p.error) atomicExch(p.error, 1);
-        continue;
-      }
+      if (!resident) {  // rows stay in A; the trailing update reloads the V form per chunk
+        __syncthreads();
+        qr_panel_householder(p, s, p.A + ra * p.lda + k, p.lda, Ts, k, jb, ra, r1, gen);
+        __syncthreads();
+        QR_PHASE(5);
+      } else {
       for (int e = tid; e < int(lmax(0L, r1 - ra)) * QR_NB; e += QR_THREADS) {
         const int rr = e >> 5, c = e & 31;
         s.Ps[rr * QR_PLD + c] = (c < jb) ? p.A[(ra + rr) * p.lda + k + c] : 0.0;
       }
       __syncthreads();
-      qr_panel_householder(p, s, Ts, k, jb, ra, r1, gen);
+      qr_panel_householder(p, s, s.Ps, QR_PLD, Ts, k, jb, ra, r1, gen);
       for (int e = tid; e < int(lmax(0L, r1 - ra)) * QR_NB; e += QR_THREADS) {
         const int rr = e >> 5, c = e & 31;
         const long r = ra + rr;
@@ -959,6 +964,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
       }
       __syncthreads();
       QR_PHASE(5);
+      }
     }
     if (blockIdx.x == 0)
       for (int e = tid; e < 1024; e += QR_THREADS) p.tall[pidx * 1024 + e] = Ts[(e >> 5) * QR_SLD + (e & 31)];

@@ -94,6 +94,47 @@ def test_qr_matches_lapack(cuda, qr_method, m, n):
     assert np.abs(q.T @ q - np.eye(n)).max() < 1e-13
 
 
+@pytest.mark.parametrize("m,n,decades", [(30000, 48, 6), (100000, 40, 10), (60000, 100, 8), (200000, 64, 12),
+                                         (40000, 33, 9)])
+def test_qr_graded_rows_beyond_shared_memory(cuda, qr_method, m, n, decades):
+    """Column-graded tall inputs whose per-CTA rows exceed shared memory: the
+    Cholesky-QR guard hands them to the Householder kernel, whose panels then
+    need the column-by-column fallback on rows streamed from A (regression:
+    that combination used to leave the panel unfactored)."""
+    from paper_2103_07245_b200 import device as D
+
+    rng = np.random.default_rng(m + n)
+    x = rng.standard_normal((m, n)) * np.logspace(0, -decades, n)[rng.permutation(n)]
+    qr, rr = oracle_qr(x)
+    ctx = D.context(cuda)
+    t = _dev_matrix(x, cuda)
+    r = D.empty_matrix(n, n, cuda)
+    D.householder_qr_(ctx, t, r, want_q=True)
+    q, rg = t.cpu().numpy(), r.cpu().numpy()
+    assert np.abs(q.T @ q - np.eye(n)).max() < 1e-13
+    colnorm = np.linalg.norm(x, axis=0)
+    assert np.all(np.linalg.norm(q @ rg - x, axis=0) <= 1e-14 * np.sqrt(m) * colnorm)
+    assert column_relative_error(q, qr).max() < 1e-10
+    d = np.abs(np.diag(rr))
+    assert np.all(np.abs(np.diag(rg) - d) <= 1e-12 * d)
+
+
+def test_qr_rank_deficient_rows_beyond_shared_memory(cuda, qr_method):
+    from paper_2103_07245_b200 import device as D
+
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((50000, 3)) @ rng.standard_normal((3, 20))
+    ctx = D.context(cuda)
+    t = _dev_matrix(x, cuda)
+    r = D.empty_matrix(20, 20, cuda)
+    flag = torch.full((1,), -1, dtype=torch.int32, device=cuda)
+    D.householder_qr_(ctx, t, r, want_q=True, rank_flag=flag)
+    q, rg = t.cpu().numpy(), r.cpu().numpy()
+    assert int(flag.item()) == 1
+    assert np.abs(q.T @ q - np.eye(20)).max() < 1e-13
+    assert np.abs(q @ rg - x).max() <= 1e-13 * np.abs(x).max() * 10
+
+
 def test_qr_rank_flags(cuda, qr_method):
     from paper_2103_07245_b200 import device as D
 

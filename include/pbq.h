@@ -153,6 +153,24 @@ int pbq_residual_fro(pbq_ctx* ctx, int64_t n1, int64_t n2, int64_t k, const doub
                      int64_t ldp, double* out, void* workspace, size_t workspace_bytes, void* stream);
 int pbq_residual_workspace_bytes(pbq_ctx* ctx, int64_t n1, int64_t n2, int64_t k, size_t* bytes);
 
+/* Column-pivoted QR pivot order (the cor_utv core): perm[i]
+ * (int64, n entries) such that M[:, perm] = Q·R is LAPACK dgeqp3's
+ * factorization of the row-major m×n matrix M — the pivot rule of
+ * scipy.linalg.qr(m, pivoting=True) behind the reference's
+ * column_pivoted_qr (linalg.py:118-129), restated from dlaqp2 (first-max
+ * pivot, norm downdating with the √ε recompute test).  Q and R follow from
+ * pbq_householder_qr of the gathered columns (pbq_gather_columns).
+ * M is not modified.  Limit: 8·m + 8·n bytes of shared memory per CTA
+ * (PBQ_ERR_DIM beyond it). */
+int pbq_cpqr_pivots(pbq_ctx* ctx, int64_t m, int64_t n, const double* M, int64_t ldm, int64_t* perm,
+                    void* workspace, size_t workspace_bytes, void* stream);
+int pbq_cpqr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes);
+
+/* dst[:, i] = src[:, perm[i]] for row-major rows×cols matrices (V = V̄[:, perm],
+ * algorithms.py:358). */
+int pbq_gather_columns(pbq_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                       const int64_t* perm, double* dst, int64_t ldd, void* stream);
+
 /* Small helpers used by the host driver.
  * dst[i][j] = src[j][i]            (n×n), or with lower=1 the lower triangle
  * of srcᵀ and zeros above (L = tril(R̃ᵀ), algorithms.py:257). */

@@ -13,6 +13,13 @@ This is a restatement of the reference path at the numpy level, call for call:
 * ``oracle_r_svd``       ↔ ``r_svd``         (algorithms.py:263-292)
 * ``oracle_spectral_norm`` ↔ ``spectral_norm`` (linalg.py:168-207)
 * ``oracle_error_curve``   ↔ ``error_curve``   (analysis.py:213-247, pbp_qlp)
+* ``oracle_column_pivoted_qr`` ↔ ``column_pivoted_qr`` (linalg.py:118-129; scipy
+  1.18 → LAPACK dgeqp3)
+* ``oracle_cor_utv``     ↔ ``cor_utv``        (algorithms.py:295-363)
+
+``cpqr_pivots_restated`` restates LAPACK dlaqp2's pivot rule (first-max
+pivot, norm downdating with the √ε recompute test) without a LAPACK call; it
+cross-checks scipy's pivots and is the rule the device kernel implements.
 
 The arithmetic lives in numpy 2.3.5 (the reference pins only numpy>=1.24,
 pyproject.toml:11-15): dgemm for products, LAPACK dgeqrf+dorgqr (via
@@ -275,3 +282,128 @@ def oracle_error_curve(a, d_values, q=0, seed=0, reorthonormalize=True):
 def reconstruction_error(a, qf, l, p):
     a = np.asarray(a, dtype=np.float64)
     return np.linalg.norm(a - qf @ l @ p.T) / np.linalg.norm(a)
+
+
+# -------------------------------------------------------- pivoted QR / UTV --
+def oracle_column_pivoted_qr(m):
+    """linalg.py:118-129: scipy.linalg.qr(m, "economic", pivoting=True), signs
+    fixed so diag(r) >= 0, r = triu(r)."""
+    import scipy.linalg
+
+    m = np.asarray(m, dtype=np.float64)
+    q, r, perm = scipy.linalg.qr(m, mode="economic", pivoting=True)
+    q, r = _fix_signs(q, r)
+    return q, np.triu(r), perm
+
+
+def cpqr_pivots_restated(m, return_gaps=False):
+    """Pivot order of LAPACK dlaqp2 (dgeqp3's unblocked kernel), restated:
+    p = first max of the partial norms vn1 over the free positions; swap;
+    Householder reflector (dlarfg) applied to the trailing columns (dlarf);
+    vn1[j] downdated by √(1 − (|a_kj|/vn1[j])²) unless
+    (1 − (|a_kj|/vn1[j])²)·(vn1[j]/vn2[j])² ≤ √ε (ε = 2⁻⁵³), which
+    recomputes it from rows k+1.. and resets vn2[j].
+
+    With ``return_gaps`` also returns, per step, the relative margin
+    (best − runner-up)/best of the pivot choice: where it is at rounding
+    level the pivot order is decided by rounding, in LAPACK as anywhere."""
+    a = np.array(m, dtype=np.float64, order="F", copy=True)
+    rows, n = a.shape
+    perm = np.arange(n)
+    vn1 = np.sqrt((a * a).sum(axis=0))
+    vn2 = vn1.copy()
+    tol3z = np.sqrt(2.0**-53)
+    gaps = np.full(min(rows, n), np.inf)
+    for k in range(min(rows, n)):
+        p = k + int(np.argmax(vn1[k:]))
+        if n - k > 1 and vn1[p] > 0:
+            gaps[k] = (vn1[p] - np.partition(vn1[k:], -2)[-2]) / vn1[p]
+        if p != k:
+            a[:, [k, p]] = a[:, [p, k]]
+            perm[[k, p]] = perm[[p, k]]
+            vn1[p], vn2[p] = vn1[k], vn2[k]
+        tau = 0.0
+        if k < rows - 1:
+            alpha = a[k, k]
+            xnorm = float(np.sqrt((a[k + 1:, k] ** 2).sum()))
+            if xnorm != 0.0:
+                beta = -np.copysign(np.hypot(alpha, xnorm), alpha)
+                tau = (beta - alpha) / beta
+                a[k + 1:, k] /= alpha - beta
+                a[k, k] = beta
+        if k < n - 1:
+            if tau != 0.0:
+                v = np.concatenate(([1.0], a[k + 1:, k]))
+                w = v @ a[k:, k + 1:]
+                a[k:, k + 1:] -= tau * np.outer(v, w)
+            for j in range(k + 1, n):
+                if vn1[j] != 0.0:
+                    t = 1.0 - (abs(a[k, j]) / vn1[j]) ** 2
+                    t = max(t, 0.0)
+                    t2 = t * (vn1[j] / vn2[j]) ** 2
+                    if t2 <= tol3z:
+                        vn1[j] = float(np.sqrt((a[k + 1:, j] ** 2).sum())) if k < rows - 1 else 0.0
+                        vn2[j] = vn1[j]
+                    else:
+                        vn1[j] *= np.sqrt(t)
+    return (perm, gaps) if return_gaps else perm
+
+
+PINV_RTOL = 1e-12  # algorithms.py:56
+
+
+def oracle_cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=True):
+    """algorithms.py:306-363 restated (Ω n2×d; _power_iterations with
+    transpose_first=False; _transposed_pinv_apply :295-303)."""
+    a = np.asarray(a, dtype=np.float64)
+    omega = oracle_gaussian(a.shape[1], d, seed)
+    flags = []
+    passes = 1
+    f1 = a @ omega
+    if reorthonormalize:
+        ubar_in = f1
+        ubar, fl = oracle_orth(f1)
+        flags.append(fl)
+        for _ in range(q):
+            ubar, fl = oracle_orth(a.T @ ubar)
+            flags.append(fl)
+            ubar_in = a @ ubar
+            ubar, fl = oracle_orth(ubar_in)
+            flags.append(fl)
+            passes += 2
+        f2 = a.T @ ubar
+        gram = None
+    else:
+        for _ in range(q):
+            f1 = a @ (a.T @ f1)
+            passes += 2
+        ubar_in = f1
+        ubar, fl = oracle_orth(f1)
+        flags.append(fl)
+        f2 = a.T @ f1
+        gram = ubar.T @ f1
+    passes += 1
+    vbar, fl = oracle_orth(f2)
+    flags.append(fl)
+    truncated = False
+    if pass_efficient:
+        core = f2.T @ vbar
+        if gram is not None:
+            u, s, vh = np.linalg.svd(gram, full_matrices=False)
+            if s[0] == 0.0:
+                core, truncated = np.zeros_like(core), True
+            else:
+                keep = s > PINV_RTOL * s[0]
+                inv = np.zeros_like(s)
+                inv[keep] = 1.0 / s[keep]
+                core, truncated = (u * inv) @ (vh @ core), bool(not keep.all())
+    else:
+        core = ubar.T @ (a @ vbar)
+        passes += 1
+    qc, t, perm = oracle_column_pivoted_qr(core)
+    # |diag R| of the inputs to the last orth of each basis: the forward error
+    # of Ū's / V̄'s column j is ~ u·R_00/R_jj (what parity tolerances scale by)
+    rd1 = np.abs(np.diag(oracle_qr(ubar_in)[1]))
+    rd2 = np.abs(np.diag(oracle_qr(f2)[1]))
+    return {"u": ubar @ qc, "t": t, "v": vbar[:, perm], "perm": perm, "omega": omega, "passes": passes,
+            "pinv_truncated": truncated, "rank_flags": flags, "core": core, "rdiag_ubar": rd1, "rdiag_vbar": rd2}

@@ -9,8 +9,9 @@ from .algorithms import (PbpQlpPlan, QlpFactors, SketchRecord, pbp_qlp, pbp_qlp_
                          reconstruction_error, residual_norms)
 from .exceptions import (ConvergenceError, DeviceError, DimensionError, MatrixInputError, ParameterError,
                          RankDeficiencyWarning)
-from .linalg import QrFactors, gaussian_matrix, householder_qr, orth
+from .linalg import QrFactors, column_pivoted_qr, gaussian_matrix, householder_qr, orth
 from .rsvd import RsvdFactors, r_svd
+from .utv import UtvFactors, cor_utv
 
 __version__ = "0.1.0"
 
@@ -26,6 +27,9 @@ __all__ = [
     "RankDeficiencyWarning",
     "RsvdFactors",
     "SketchRecord",
+    "UtvFactors",
+    "column_pivoted_qr",
+    "cor_utv",
     "gaussian_matrix",
     "householder_qr",
     "orth",

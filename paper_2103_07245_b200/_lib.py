@@ -46,6 +46,9 @@ EXPORTED = (
     "pbq_debug_cholqr_stats",
     "pbq_residual_fro",
     "pbq_residual_workspace_bytes",
+    "pbq_cpqr_pivots",
+    "pbq_cpqr_workspace_bytes",
+    "pbq_gather_columns",
 )
 
 c_i64 = ctypes.c_int64
@@ -105,6 +108,9 @@ _SIGS = {
                          ctypes.c_int),
     "pbq_residual_workspace_bytes": ([c_p, c_i64, c_i64, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_debug_cholqr_stats": ([c_p, c_p], ctypes.c_int),
+    "pbq_cpqr_pivots": ([c_p, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_sz, c_p], ctypes.c_int),
+    "pbq_cpqr_workspace_bytes": ([c_p, c_i64, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),
+    "pbq_gather_columns": ([c_p, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p], ctypes.c_int),
 }
 
 _lib = None

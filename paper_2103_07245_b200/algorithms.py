@@ -122,6 +122,8 @@ def residual_norms(a, factors, rank=None, *, device=None):
 
     if hasattr(factors, "l"):  # QLP: Q L Pᵀ
         left, mid, right = factors.q_basis, factors.l, factors.p_basis
+    elif hasattr(factors, "t"):  # UTV (cor_utv): U T Vᵀ, T k×d upper trapezoidal
+        left, mid, right = factors.u, factors.t, factors.v
     else:  # SVD-type (RsvdFactors): u diag(s) vᵀ
         left, mid, right = factors.u, None, factors.v
     kmax = left.shape[1] if mid is None else mid.shape[0]
@@ -140,6 +142,12 @@ def residual_norms(a, factors, rank=None, *, device=None):
     q = on_dev(left)[:, :k]
     l = on_dev(mid)[:k, :k] if mid is not None else torch.diag(on_dev(factors.s)[:k])
     p = on_dev(right)[:, :k]
+    if mid is not None and rank is None and mid.shape[1] > mid.shape[0]:
+        # wide UTV core (d > n1): U·T is n1×d, the middle factor the identity
+        ctx = _dev.context(dev)
+        q = _dev.gemm(ctx, on_dev(left), _dev.as_kernel_operand(on_dev(mid)), trans_a=False)
+        l = torch.eye(mid.shape[1], dtype=torch.float64, device=dev)
+        p = on_dev(right)
     out = _dev.residual_fro(_dev.context(dev), a_dev, q, l, p)
     r2, a2 = out.tolist()
     return math.sqrt(r2), math.sqrt(a2)

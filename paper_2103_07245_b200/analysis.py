@@ -3,11 +3,11 @@
 Mirrors the reference's dispatcher and error helpers for the algorithm this
 package implements:
 
-* ``factorize(a, "pbp_qlp" | "r_svd", d, ...)`` ↔ analysis.py:135-157
-* ``low_rank_approx(factors, rank)``         ↔ analysis.py:170-193 (QLP factors)
+* ``factorize(a, "pbp_qlp" | "r_svd" | "cor_utv" | "cpqr", d, ...)`` ↔ analysis.py:135-157
+* ``low_rank_approx(factors, rank)``         ↔ analysis.py:159-193
 * ``spectral_norm(m)``                        ↔ linalg.py:194-207 (+ _power_norm :168-191)
 * ``residual_spectral_norm(a, f, rank)``      ‖A − approx‖₂ without forming the residual
-* ``error_curve(a, "pbp_qlp", d_values, ...)`` ↔ analysis.py:213-247
+* ``error_curve(a, alg, d_values, ...)``       ↔ analysis.py:213-247
 
 The factorization and the Frobenius residual run on libpbq's sm_100a
 kernels (the fused one-pass residual).  The spectral norm of a
@@ -16,7 +16,7 @@ up to 2000 in the larger dimension, else power iteration on the Gram
 operator from the seeded start vector gaussian_matrix(n, 1, seed=0x5EED),
 relative tolerance 1e-10, at most 5000 iterations.  Its matrix-vector
 products use torch on the device; it is an analysis helper, not the hot path.
-Algorithms other than ``pbp_qlp`` and ``r_svd`` are outside this package's
+The exact ``svd`` and the deterministic ``pqlp`` are outside this package's
 scope and raise.
 """
 import math
@@ -27,14 +27,16 @@ import torch
 from . import exceptions as _exc
 from .algorithms import QlpFactors, pbp_qlp, residual_norms
 from .rsvd import RsvdFactors, r_svd
-from .linalg import HostMatrix, gaussian_matrix
+from .linalg import HostMatrix, QrFactors, column_pivoted_qr, gaussian_matrix
+from .utv import UtvFactors, cor_utv
 from .validation import check_index_range
 
 __all__ = ["ALGORITHMS", "GPU_ALGORITHMS", "factorize", "low_rank_approx", "spectral_norm",
            "residual_spectral_norm", "error_curve"]
 
 ALGORITHMS = ("svd", "cpqr", "pqlp", "r_svd", "cor_utv", "pbp_qlp")  # analysis.py:53-55
-GPU_ALGORITHMS = ("pbp_qlp", "r_svd")
+GPU_ALGORITHMS = ("cpqr", "r_svd", "cor_utv", "pbp_qlp")
+DETERMINISTIC_ALGORITHMS = ("svd", "cpqr", "pqlp")  # analysis.py:56
 DENSE_NORM_LIMIT = 2000  # linalg.py:40
 POWER_RTOL = 1e-10       # linalg.py:43
 POWER_MAXITER = 5000     # linalg.py:44
@@ -61,8 +63,13 @@ def factorize(a, algorithm, d, q=0, seed=0, reorthonormalize=True):
     if algorithm not in GPU_ALGORITHMS:
         _check_finite(HostMatrix(a, "a"), "a")
         _check_algorithm(algorithm)
+    if algorithm == "cpqr":
+        _check_finite(HostMatrix(a, "a"), "a")
+        return column_pivoted_qr(a)
     if algorithm == "r_svd":
         return r_svd(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
+    if algorithm == "cor_utv":
+        return cor_utv(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
     return pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
 
 
@@ -76,6 +83,20 @@ def low_rank_approx(factors, rank=None):
             return factors.approx()
         rank = check_index_range(rank, "rank", 1, factors.s.shape[0])
         return (factors.u[:, :rank] * factors.s[:rank]) @ factors.v[:, :rank].T
+    if isinstance(factors, UtvFactors):
+        if rank is None:
+            return factors.approx()
+        rank = check_index_range(rank, "rank", 1, factors.t.shape[0])
+        return factors.u[:, :rank] @ factors.t[:rank, :rank] @ factors.v[:, :rank].T
+    if isinstance(factors, QrFactors):  # analysis.py:159-167 (_pivoted_qr_approx)
+        q, r, perm = factors
+        rank = r.shape[0] if rank is None else check_index_range(rank, "rank", 1, r.shape[0])
+        cols = q[:, :rank] @ r[:rank, :]
+        if perm is None:
+            return cols
+        out = cols.clone() if isinstance(cols, torch.Tensor) else np.empty((q.shape[0], r.shape[1]))
+        out[:, perm] = cols
+        return out
     raise _exc.ParameterError(f"cannot reconstruct from factors of type {type(factors).__name__}")
 
 
@@ -133,6 +154,13 @@ def residual_spectral_norm(a, factors, rank=None, *, device=None):
         kmax = factors.s.shape[0]
         k = kmax if rank is None else check_index_range(rank, "rank", 1, kmax)
         q, l, p = on_dev(factors.u)[:, :k], torch.diag(on_dev(factors.s)[:k]), on_dev(factors.v)[:, :k]
+    elif isinstance(factors, UtvFactors):
+        kmax = factors.t.shape[0]
+        if rank is None:
+            q, l, p = on_dev(factors.u), on_dev(factors.t), on_dev(factors.v)
+        else:
+            k = check_index_range(rank, "rank", 1, kmax)
+            q, l, p = on_dev(factors.u)[:, :k], on_dev(factors.t)[:k, :k], on_dev(factors.v)[:, :k]
     else:
         kmax = factors.l.shape[0]
         k = kmax if rank is None else check_index_range(rank, "rank", 1, kmax)
@@ -156,6 +184,18 @@ def error_curve(a, alg, d_values, q=0, seed=0, reorthonormalize=True):
         raise _exc.ParameterError("d_values must contain at least one sampling size")
     _check_algorithm(alg)
     records = []
+    if alg in DETERMINISTIC_ALGORITHMS:  # factored once, truncated per point (analysis.py:229-236)
+        from . import device as _dev
+
+        base = column_pivoted_qr(t)
+        ctx = _dev.context(t.device)
+        a_perm = _dev.gather_columns(ctx, t, base.perm)  # ‖A − approx‖ = ‖A[:, perm] − Q_d R_d‖
+        for d in d_list:
+            trunc = RsvdFactors(base.q[:, :d], torch.ones(d, dtype=torch.float64, device=t.device),
+                                base.r[:d, :].T, None)
+            fro, _ = residual_norms(a_perm, trunc)
+            records.append({"d": d, "spectral_error": residual_spectral_norm(a_perm, trunc), "frobenius_error": fro})
+        return records
     for d in d_list:
         fac = factorize(t, alg, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
         fro, _ = residual_norms(t, fac)

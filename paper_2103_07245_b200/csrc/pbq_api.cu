@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "gemm_f64.cuh"
 #include "cholqr_f64.cuh"
+#include "cpqr_f64.cuh"
 #include "qr_f64.cuh"
 #include "sketch.cuh"
 
@@ -650,6 +651,77 @@ int transpose_launch(pbq_ctx* ctx, long n, const double* src, long lds, double* 
 
 long thin_ld(long d) { return (d + 1) & ~1L; }
 
+// ------------------------------------------------ column-pivoted QR pivots --
+// cpqr_f64.cuh: pivot order of LAPACK dgeqp3 for a row-major m×n matrix.
+// Shared-memory layout of cpqr_pivot_kernel, or 0 when it exceeds the opt-in
+// limit and the per-CTA vectors live in a global (L2-resident) scratch.
+size_t cpqr_smem(const pbq_ctx* ctx, long m, long n) {
+  const size_t b = cp_scratch_bytes(m, n);
+  return b <= ctx->smem_optin ? b : 0;
+}
+
+int cpqr_grid(pbq_ctx* ctx, long m, long n, int& grid) {
+  const size_t smem = cpqr_smem(ctx, m, n);
+  PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&cpqr_pivot_kernel),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int per_sm = 0;
+  PBQ_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_pivot_kernel, CP_THREADS, smem));
+  if (per_sm < 1) return fail(ctx, PBQ_ERR_DIM, "cpqr: kernel does not fit on an SM");
+  grid = int(std::max(1L, std::min(long(ctx->sms), ceil_div(n, CP_WARPS))));
+  return PBQ_OK;
+}
+
+size_t cpqr_ws_bytes(const pbq_ctx* ctx, long m, long n, int grid) {
+  const long ldw = (m + 1) & ~1L;
+  size_t b = align_up(size_t(n) * ldw * 8, 256) + 2 * align_up(size_t(n) * 8, 256) + 256 + 256;
+  if (!cpqr_smem(ctx, m, n)) b += size_t(grid) * align_up(cp_scratch_bytes(m, n), 256) + 256;
+  return b;
+}
+
+int cpqr_launch(pbq_ctx* ctx, long m, long n, const double* M, long ldm, int64_t* perm, void* ws, size_t ws_bytes,
+                cudaStream_t st) {
+  if (m < 1 || n < 1) return fail(ctx, PBQ_ERR_DIM, "cpqr: bad shape %ld x %ld", m, n);
+  if (ldm < n) return fail(ctx, PBQ_ERR_PARAM, "cpqr: leading dimension too small");
+  if (!M || !perm) return fail(ctx, PBQ_ERR_PARAM, "cpqr: null pointer argument");
+  int grid = 0;
+  PBQ_TRY(cpqr_grid(ctx, m, n, grid));
+  CpArgs a;
+  a.m = m; a.n = n; a.steps = std::min(m, n);
+  a.ldw = (m + 1) & ~1L;
+  Carve cv(ws, ws_bytes);
+  a.W = cv.take<double>(size_t(n) * a.ldw);
+  a.vn1 = cv.take<double>(n);
+  a.vn2 = cv.take<double>(n);
+  a.counter = cv.take<unsigned int>(1);
+  a.perm = perm;
+  const size_t smem = cpqr_smem(ctx, m, n);
+  a.scratch = nullptr;
+  a.scratch_stride = align_up(cp_scratch_bytes(m, n), 256);
+  if (!smem) a.scratch = cv.take<unsigned char>(size_t(grid) * a.scratch_stride);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "cpqr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  PBQ_TRY(transpose_launch(ctx, m, M, ldm, a.W, a.ldw, 0, st, n));  // W = Mᵀ: columns contiguous
+  PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
+  void* args[] = {&a};
+  ProfScope ps(ctx->prof, st, 1);
+  PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&cpqr_pivot_kernel), dim3(grid),
+                                            dim3(CP_THREADS), args, smem, st));
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
+int gather_launch(pbq_ctx* ctx, long rows, long cols, const double* src, long lds, const int64_t* perm, double* dst,
+                  long ldd, cudaStream_t st) {
+  if (rows < 1 || cols < 1) return fail(ctx, PBQ_ERR_DIM, "gather: bad shape %ld x %ld", rows, cols);
+  if (!src || !perm || !dst) return fail(ctx, PBQ_ERR_PARAM, "gather: null pointer argument");
+  if (lds < cols || ldd < cols) return fail(ctx, PBQ_ERR_PARAM, "gather: leading dimension too small");
+  const long blocks = std::min(ceil_div(rows * cols, 256), long(ctx->sms) * 8);
+  ProfScope ps(ctx->prof, st, 3);
+  gather_cols_kernel<<<unsigned(blocks), 256, 0, st>>>(rows, cols, src, lds, perm, dst, ldd);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
 // ------------------------------------------------- reconstruction residual --
 // ‖A − Q_k·L_k·P_kᵀ‖_F² and ‖A‖_F² (QlpFactors.approx(rank), algorithms.py:
 // 101-106; error_curve's frobenius_error, analysis.py:238-244) in one pass
@@ -891,6 +963,27 @@ int pbq_residual_fro(pbq_ctx* ctx, int64_t n1, int64_t n2, int64_t k, const doub
   if (lda < n2 || ldq < k || ldl < k || ldp < k) return fail(ctx, PBQ_ERR_PARAM, "residual: leading dimension too small");
   return resid_launch(ctx, n1, n2, k, A, lda, Q, ldq, L, ldl, P, ldp, out, ws, ws_bytes,
                       static_cast<cudaStream_t>(stream));
+}
+
+int pbq_cpqr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes) {
+  if (!ctx || !bytes) return PBQ_ERR_PARAM;
+  if (m < 1 || n < 1) return fail(ctx, PBQ_ERR_DIM, "cpqr: bad shape");
+  int grid = 0;
+  PBQ_TRY(cpqr_grid(ctx, m, n, grid));
+  *bytes = cpqr_ws_bytes(ctx, m, n, grid);
+  return PBQ_OK;
+}
+
+int pbq_cpqr_pivots(pbq_ctx* ctx, int64_t m, int64_t n, const double* M, int64_t ldm, int64_t* perm, void* ws,
+                    size_t ws_bytes, void* stream) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  return cpqr_launch(ctx, m, n, M, ldm, perm, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int pbq_gather_columns(pbq_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds, const int64_t* perm,
+                       double* dst, int64_t ldd, void* stream) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  return gather_launch(ctx, rows, cols, src, lds, perm, dst, ldd, static_cast<cudaStream_t>(stream));
 }
 
 int pbq_set_qr_method(pbq_ctx* ctx, int32_t method) {

@@ -221,3 +221,34 @@ def transpose(ctx, src, dst=None, lower=False):
                                    stream_ptr(src.device))
         ctx.check(st, "transpose")
     return dst
+
+
+def cpqr_pivots(ctx, m, out=None):
+    """Pivot order of LAPACK dgeqp3 for the m×n device matrix ``m`` → int64
+    device tensor ``perm`` (n entries) with m[:, perm] = Q·R."""
+    dev = m.device
+    m = as_kernel_operand(m)
+    rows, cols = m.shape
+    if out is None:
+        out = torch.empty(cols, dtype=torch.int64, device=dev)
+    nbytes = ctypes.c_size_t()
+    with ctx.lock:
+        ctx.check(ctx.lib.pbq_cpqr_workspace_bytes(ctx.handle, rows, cols, ctypes.byref(nbytes)), "cpqr workspace")
+        ws = workspace(nbytes.value, dev)
+        st = ctx.lib.pbq_cpqr_pivots(ctx.handle, rows, cols, ptr(m), ld_of(m), ptr(out), ptr(ws), nbytes.value,
+                                     stream_ptr(dev))
+        ctx.check(st, "cpqr_pivots")
+    return out
+
+
+def gather_columns(ctx, src, perm, out=None):
+    """out[:, i] = src[:, perm[i]] (perm: int64 device tensor)."""
+    src = as_kernel_operand(src)
+    rows, cols = src.shape[0], perm.shape[0]
+    if out is None:
+        out = empty_matrix(rows, cols, src.device)
+    with ctx.lock:
+        st = ctx.lib.pbq_gather_columns(ctx.handle, rows, cols, ptr(src), ld_of(src), ptr(perm), ptr(out),
+                                        ld_of(out), stream_ptr(src.device))
+        ctx.check(st, "gather_columns")
+    return out

@@ -1,10 +1,10 @@
 """scikit-learn transformers for the GPU paths.
 
-Mirror the reference's ``PbpQlp`` and ``RandomizedSvd`` estimators
-(estimators.py:81-126 on the shared ``_LowRankTransformer`` plumbing,
+Mirror the reference's ``PbpQlp``, ``RandomizedSvd`` and ``CorUtv`` estimators
+(estimators.py:81-157 on the shared ``_LowRankTransformer`` plumbing,
 :31-78): ``fit`` factorizes on the GPU, ``components_`` holds the first
 ``n_components`` columns of the row-space basis transposed (P for PbP-QLP,
-V for r_svd), ``singular_values_`` the estimates of
+V for r_svd and cor_utv), ``singular_values_`` the estimates of
 analysis.singular_value_estimates (|diag L|, resp. s), and ``transform`` /
 ``inverse_transform`` are the skinny products X·componentsᵀ and
 Z·components run on libpbq's DMMA GEMM.  numpy in → numpy out; CUDA tensors
@@ -20,9 +20,10 @@ from . import exceptions as _exc
 from .algorithms import pbp_qlp
 from .linalg import HostMatrix
 from .rsvd import r_svd
+from .utv import cor_utv
 from .validation import check_count
 
-__all__ = ["PbpQlp", "RandomizedSvd"]
+__all__ = ["PbpQlp", "RandomizedSvd", "CorUtv"]
 
 
 def _gemm_nn(x, b):
@@ -124,3 +125,25 @@ class RandomizedSvd(_LowRankTransformer):
 
     def _spectrum(self, f):
         return f.s
+
+
+class CorUtv(_LowRankTransformer):
+    """Randomized rank-revealing UTV via compressed orthogonal bases
+    (estimators.py:128-157)."""
+
+    def __init__(self, n_components, q=0, seed=0, pass_efficient=False, reorthonormalize=True):
+        self.n_components = n_components
+        self.q = q
+        self.seed = seed
+        self.pass_efficient = pass_efficient
+        self.reorthonormalize = reorthonormalize
+
+    def _factorize(self, X, rank):
+        return cor_utv(X, rank, q=self.q, seed=self.seed, pass_efficient=self.pass_efficient,
+                       reorthonormalize=self.reorthonormalize)
+
+    def _row_basis(self, f):
+        return f.v
+
+    def _spectrum(self, f):
+        return f.t_values

@@ -1,7 +1,8 @@
 """Drop-in wiring for the reference package.
 
 ``install(pbpqlp)`` rebinds the reference's PbP-QLP entry point (and the
-sibling ``r_svd``, algorithms.py:263-292) — in every
+siblings ``r_svd``, algorithms.py:263-292, ``cor_utv``, :306-363, and its
+core ``column_pivoted_qr``, linalg.py:118-129) — in every
 module that imported it by name (algorithms.py:209, __init__.py:18,
 analysis.py:16-25 → factorize :153-154, estimators.py:17 → PbpQlp
 :98-105, bounds.py:42 → eval_highprob_bounds :589, cli.py:43 → :448, :733)
@@ -20,8 +21,8 @@ import warnings
 from . import algorithms as _alg
 from . import exceptions as _exc
 
-# modules of the reference that bind the names `pbp_qlp` / `r_svd` at import time
-_BINDERS = ("", ".algorithms", ".analysis", ".estimators", ".bounds", ".cli")
+# modules of the reference that bind the patched names at import time
+_BINDERS = ("", ".linalg", ".algorithms", ".analysis", ".estimators", ".bounds", ".cli")
 
 
 def _translated(pbpqlp, fn):
@@ -63,6 +64,40 @@ def make_rsvd_dropin(pbpqlp):
     return r_svd
 
 
+def make_utv_dropin(pbpqlp):
+    """Reference-typed ``cor_utv(a, d, q=0, seed=0, pass_efficient=False,
+    reorthonormalize=True)`` (algorithms.py:306-363) on the GPU path."""
+    from . import utv as _utv
+
+    ref_alg = pbpqlp.algorithms
+
+    def cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=True):
+        f = _translated(pbpqlp, lambda: _utv.cor_utv(a, d, q=q, seed=seed, pass_efficient=pass_efficient,
+                                                     reorthonormalize=reorthonormalize))
+        sk = f.sketch
+        sketch = ref_alg.SketchRecord(sk.test_matrix, int(seed), sk.d, sk.q, sk.passes_over_a)
+        return ref_alg.UtvFactors(f.u, f.t, f.v, f.pass_efficient, sketch, f.pinv_truncated)
+
+    cor_utv.__doc__ = ref_alg.cor_utv.__doc__
+    cor_utv.__wrapped_gpu__ = True
+    return cor_utv
+
+
+def make_cpqr_dropin(pbpqlp):
+    """Reference-typed ``column_pivoted_qr(m)`` (linalg.py:118-129) on the GPU."""
+    from . import linalg as _linalg
+
+    ref_lin = pbpqlp.linalg
+
+    def column_pivoted_qr(m):
+        f = _translated(pbpqlp, lambda: _linalg.column_pivoted_qr(m))
+        return ref_lin.QrFactors(f.q, f.r, f.perm)
+
+    column_pivoted_qr.__doc__ = ref_lin.column_pivoted_qr.__doc__
+    column_pivoted_qr.__wrapped_gpu__ = True
+    return column_pivoted_qr
+
+
 def make_dropin(pbpqlp):
     """Return a reference-typed ``pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True)``."""
     ref_alg = pbpqlp.algorithms
@@ -98,7 +133,8 @@ def install(pbpqlp):
     bound ``pbp_qlp``; returns the previous bindings (for ``uninstall``)."""
     import importlib
 
-    dropins = {"pbp_qlp": make_dropin(pbpqlp), "r_svd": make_rsvd_dropin(pbpqlp)}
+    dropins = {"pbp_qlp": make_dropin(pbpqlp), "r_svd": make_rsvd_dropin(pbpqlp),
+               "cor_utv": make_utv_dropin(pbpqlp), "column_pivoted_qr": make_cpqr_dropin(pbpqlp)}
     saved = {}
     for suffix in _BINDERS:
         mod = importlib.import_module(pbpqlp.__name__ + suffix) if suffix else pbpqlp

@@ -16,7 +16,7 @@ from . import device as _dev
 from . import exceptions as _exc
 from .validation import check_count, check_seed, coerce_host_matrix, check_shape
 
-__all__ = ["QrFactors", "gaussian_matrix", "householder_qr", "orth", "RANK_DEFICIENCY_RTOL"]
+__all__ = ["QrFactors", "gaussian_matrix", "householder_qr", "column_pivoted_qr", "orth", "RANK_DEFICIENCY_RTOL"]
 
 #: Columns whose pivot falls below this multiple of the leading pivot are
 #: reported as numerically dependent by :func:`orth` (linalg.py:48).
@@ -160,3 +160,41 @@ def orth(m):
     f, flag = _qr(m, True)
     warn_rank(flag, stacklevel=3)
     return f.q
+
+
+def cpqr_device(ctx, t):
+    """Column-pivoted QR of the m×n device matrix ``t`` → (q, r, perm) device
+    tensors: perm from the dgeqp3-rule pivot kernel, then the unpivoted QR of
+    the gathered columns (identical reflector sequence).  Economy sizes as
+    scipy: q m×k, r k×n, k = min(m, n)."""
+    m, n = t.shape
+    dev = t.device
+    perm = _dev.cpqr_pivots(ctx, t)
+    g = _dev.gather_columns(ctx, t, perm)
+    k = min(m, n)
+    if m >= n:
+        r = _dev.empty_matrix(n, n, dev)
+        _dev.householder_qr_(ctx, g, r, want_q=True)
+        return g, r, perm
+    q = _dev.as_kernel_operand(g[:, :m].clone())
+    r11 = _dev.empty_matrix(k, k, dev)
+    _dev.householder_qr_(ctx, q, r11, want_q=True)
+    r = _dev.empty_matrix(k, n, dev)
+    r[:, :k] = r11
+    r[:, k:] = _dev.gemm(ctx, q, _dev.as_kernel_operand(g[:, k:]), trans_a=True)  # R12 = Qᵀ·M[:, perm[k:]]
+    return q, r, perm
+
+
+def column_pivoted_qr(m):
+    """Column-pivoted Householder QR with nonincreasing pivot magnitudes
+    (linalg.py:118-129): ``m[:, perm] = q @ r``, ``diag(r) >= 0``, pivots as
+    LAPACK dgeqp3 chooses them (exact ties → the lowest current position)."""
+    kind, t, _host, home = to_device_matrix(m, "m")
+    if not torch.isfinite(t).all().item():
+        raise _exc.MatrixInputError("m contains non-finite entries")
+    ctx = _dev.context(t.device)
+    q, r, perm = cpqr_device(ctx, t)
+    r = torch.triu(r)
+    if kind == "numpy":
+        return QrFactors(from_device(q, kind), from_device(r, kind), perm.cpu().numpy().astype(np.int32))
+    return QrFactors(from_device(q, kind, home), from_device(r, kind, home), perm.to(home))

@@ -117,7 +117,7 @@ def test_integration_shim_maps_errors_to_reference_classes(reference_pkg):
 
     saved = integration.install(reference_pkg)
     try:
-        assert {name for _, name in saved} == {"pbp_qlp", "r_svd"}
+        assert {name for _, name in saved} == {"pbp_qlp", "r_svd", "cor_utv", "column_pivoted_qr"}
         for modname, name in saved:
             assert getattr(sys.modules[modname], name).__wrapped_gpu__
         with pytest.raises(reference_pkg.ParameterError):

@@ -40,7 +40,7 @@ def test_factorize_rejects_other_algorithms_after_validating_a():
     with pytest.raises(ParameterError, match="unknown algorithm"):
         factorize(a, "nope", 2)
     with pytest.raises(ParameterError, match="outside the B200 path"):
-        factorize(a, "cor_utv", 2)
+        factorize(a, "pqlp", 2)
     bad = a.copy()
     bad[0, 0] = np.nan
     with pytest.raises(MatrixInputError):  # analysis.py:140: check_matrix runs before the dispatch

@@ -43,8 +43,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--d", type=int, default=None, help="override the workload's d (config-5 d-sweep)")
     ap.add_argument("--q", type=int, default=None, help="override the workload's q")
-    ap.add_argument("--path", default="pbp_qlp", choices=["pbp_qlp", "r_svd"],
-                    help="r_svd: the sibling randomized SVD (SURVEY §8 f3), single GPU")
+    ap.add_argument("--path", default="pbp_qlp", choices=["pbp_qlp", "r_svd", "cor_utv"],
+                    help="r_svd / cor_utv: the sibling randomized paths (SURVEY §8 f3), single GPU")
     return ap.parse_args()
 
 
@@ -332,35 +332,44 @@ def run_ours(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
-def run_rsvd(args):
-    """--path r_svd: the randomized SVD on the same kernels,
-    same JSON contract, on one GPU."""
+def run_sibling(args):
+    """--path r_svd | cor_utv: the sibling randomized paths on
+    the same kernels, same JSON contract, on one GPU."""
     import numpy as np
     import torch
 
-    from oracle.pbp_qlp_oracle import oracle_r_svd
+    from oracle.pbp_qlp_oracle import oracle_cor_utv, oracle_r_svd
     from paper_2103_07245_b200 import workloads
     from paper_2103_07245_b200 import device as D
     from paper_2103_07245_b200.rsvd import r_svd, r_svd_flops
+    from paper_2103_07245_b200.utv import cor_utv, cor_utv_flops
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     wl = workload(args)
     n1, n2, d, q = wl["n1"], wl["n2"], wl["d"], wl["q"]
-    flops = r_svd_flops(n1, n2, d, q)
+    k = min(n1, d)
+    if args.path == "r_svd":
+        fn, oracle_fn, passes = r_svd, oracle_r_svd, 2 * q + 2
+        flops = r_svd_flops(n1, n2, d, q)
+        d2h = 8 * (n1 + n2 + 1) * k
+    else:  # cor_utv with the exact core (2q + 3 passes), reference defaults
+        fn, oracle_fn, passes = cor_utv, oracle_cor_utv, 2 * q + 3
+        flops = cor_utv_flops(n1, n2, d, q)
+        d2h = 8 * (n1 * k + k * d + n2 * d)
     a = workloads.make(args.workload, args.seed, dev)
     ctx = D.context(dev)
     for i in range(args.warmup):
-        r_svd(a, d, q=q, seed=args.seed + i)
+        fn(a, d, q=q, seed=args.seed + i)
     torch.cuda.synchronize()
-    # r_svd is host-orchestrated (Python + the cuSOLVER core), so the value
-    # is timed in a clean pass; an identical second pass carries the
-    # per-launch events (GEMM roofline) and the nvidia-smi clock sampling.
+    # host-orchestrated paths (Python between launches), so the value is timed
+    # in a clean pass; an identical second pass carries the per-launch events
+    # (GEMM roofline) and the nvidia-smi clock sampling.
     launches0 = ctx.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        r_svd(a, d, q=q, seed=args.seed + 100 + i)  # one flag read per call (host sync), as the API does
+        fn(a, d, q=q, seed=args.seed + 100 + i)  # one flag read per call (host sync), as the API does
     e1.record()
     torch.cuda.synchronize()
     launches = ctx.launch_count - launches0
@@ -368,19 +377,19 @@ def run_rsvd(args):
     sampler = ClockSampler(0)
     sampler.start()
     time.sleep(0.2)
-    ctx.profile_begin(capacity=64 * (2 * q + 8) * args.steps)
+    ctx.profile_begin(capacity=64 * (2 * q + 12) * args.steps)
     for i in range(args.steps):
-        r_svd(a, d, q=q, seed=args.seed + 100 + i)
+        fn(a, d, q=q, seed=args.seed + 100 + i)
     torch.cuda.synchronize()
     clocks = sampler.stop()
     clocks["sampled"] = "during an identical second timed pass"
     by_class = ctx.profile_end()
     value = flops / (ms * 1e-3) / 1e9
     gemm_ms, gemm_n = by_class["gemm"]
-    fl_gemm = args.steps * ((2 * q + 2) * 2.0 * n1 * n2 * d)
+    fl_gemm = args.steps * (passes * 2.0 * n1 * n2 * d)
     roof = {"bound": "tensor", "achieved": fl_gemm / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "traffic": None,
-            "kernel": "gemm_f64_ring (the 2q+2 A-passes)", "gemm_ms_per_step": gemm_ms / args.steps,
+            "kernel": f"gemm_f64_ring (the {passes} A-passes)", "gemm_ms_per_step": gemm_ms / args.steps,
             "qr_ms_per_step": by_class["qr"][0] / args.steps, "sketch_ms_per_step": by_class["sketch"][0] / args.steps,
             "step_frac_of_peak": value / 1e3 / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE}
     if roof["achieved"]:
@@ -392,26 +401,26 @@ def run_rsvd(args):
         a_np = a.cpu().numpy()
         with threadpool_limits(limits=cpu_threads()):
             t0 = time.perf_counter()
-            oracle_r_svd(a_np, d, q=q, seed=args.seed)
+            oracle_fn(a_np, d, q=q, seed=args.seed)
             sec = time.perf_counter() - t0
         cpu = {"value": flops / sec / 1e9, "unit": "GFLOP/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"one full {n1}x{n2} d={d} q={q} r_svd ({sec:.3f} s; numpy/OpenBLAS oracle_r_svd)"}
+               "sample": f"one full {n1}x{n2} d={d} q={q} {args.path} ({sec:.3f} s; numpy/OpenBLAS "
+                         f"oracle_{args.path})"}
     # e2e: numpy in, numpy out through the public function
     e2e = None
     if not args.no_e2e:
         a_host = a.cpu().numpy()
-        r_svd(a_host, d, q=q, seed=args.seed)
+        fn(a_host, d, q=q, seed=args.seed)
         t0 = time.perf_counter()
-        r_svd(a_host, d, q=q, seed=args.seed + 1)
+        fn(a_host, d, q=q, seed=args.seed + 1)
         sec = time.perf_counter() - t0
         e2e = {"value": flops / sec / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(a_host.nbytes),
-               "d2h_bytes_per_step": int(8 * (n1 + n2 + 1) * min(n1, d)), "ms_per_step": sec * 1e3,
-               "input": "numpy host array (pageable)"}
-    line = {"metric": "r_svd GFLOP/s at " + f"{n1}x{n2}, d={d}, q={q}", "value": value, "unit": "GFLOP/s",
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3, "input": "numpy host array (pageable)"}
+    line = {"metric": f"{args.path} GFLOP/s at {n1}x{n2}, d={d}, q={q}", "value": value, "unit": "GFLOP/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(args, wl, 1), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clocks, "path": "r_svd"}
+            "gpu_launches": int(launches), "clocks": clocks, "path": args.path}
     print(json.dumps(line), flush=True)
 
 
@@ -446,8 +455,8 @@ def main():
         finally:
             dist.destroy_process_group()
         return
-    if args.path == "r_svd":
-        run_rsvd(args)
+    if args.path in ("r_svd", "cor_utv"):
+        run_sibling(args)
     elif args.impl == "reference":
         run_reference(args, world, rank)
     else:

@@ -678,6 +678,63 @@ size_t cpqr_ws_bytes(const pbq_ctx* ctx, long m, long n, int grid) {
   return b;
 }
 
+// Single-cluster plan: C CTAs (one column per warp where possible, C ≤ 16)
+// holding all n columns in shared memory.  Returns false when it does not fit.
+using CpClusterFn = void (*)(CpClusterArgs);
+CpClusterFn cpqr_cluster_fn(long m) {
+  if (m <= 256) return cpqr_cluster_kernel<8>;
+  if (m <= 512) return cpqr_cluster_kernel<16>;
+  return cpqr_cluster_kernel<32>;
+}
+
+bool cpqr_cluster_plan(pbq_ctx* ctx, long m, long n, int& C, int& nc, size_t& smem) {
+  static int max_c_by_t[3] = {-1, -1, -1};  // largest launchable cluster per instantiation at full shared memory
+  int& max_c = max_c_by_t[m <= 256 ? 0 : (m <= 512 ? 1 : 2)];
+  if (getenv("PBQ_CPQR_NO_CLUSTER")) return false;
+  if (m > 1024) return false;  // the pivot column lives in registers: ≤ 32 doubles per lane
+  const int cmin = int(std::min<long>(16, std::max<long>(1, ceil_div(n, CP_WARPS))));
+  for (C = cmin; C <= 16; ++C) {
+    nc = int(ceil_div(n, C));
+    smem = cp_cluster_smem(m, n, nc, m);
+    if (smem <= ctx->smem_optin) break;
+  }
+  if (C > 16) return false;
+  if (cudaFuncSetAttribute(reinterpret_cast<void*>(cpqr_cluster_fn(m)), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem)) != cudaSuccess ||
+      cudaFuncSetAttribute(reinterpret_cast<void*>(cpqr_cluster_fn(m)),
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (max_c < 0) {
+    max_c = 0;
+    for (int c = 16; c >= 1 && max_c == 0; c /= 2) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      cfg.gridDim = dim3(c);
+      cfg.blockDim = dim3(CP_THREADS);
+      cfg.dynamicSmemBytes = ctx->smem_optin;
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = c;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaFuncSetAttribute(reinterpret_cast<void*>(cpqr_cluster_fn(m)), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(ctx->smem_optin));
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, reinterpret_cast<void*>(cpqr_cluster_fn(m)), &cfg) ==
+              cudaSuccess &&
+          nclusters > 0)
+        max_c = c;
+      cudaGetLastError();
+    }
+    cudaFuncSetAttribute(reinterpret_cast<void*>(cpqr_cluster_fn(m)), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+  }
+  return C <= max_c;
+}
+
 int cpqr_launch(pbq_ctx* ctx, long m, long n, const double* M, long ldm, int64_t* perm, void* ws, size_t ws_bytes,
                 cudaStream_t st) {
   if (m < 1 || n < 1) return fail(ctx, PBQ_ERR_DIM, "cpqr: bad shape %ld x %ld", m, n);
@@ -700,6 +757,28 @@ int cpqr_launch(pbq_ctx* ctx, long m, long n, const double* M, long ldm, int64_t
   if (!smem) a.scratch = cv.take<unsigned char>(size_t(grid) * a.scratch_stride);
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "cpqr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_TRY(transpose_launch(ctx, m, M, ldm, a.W, a.ldw, 0, st, n));  // W = Mᵀ: columns contiguous
+  int C = 0, nc = 0;
+  size_t csmem = 0;
+  if (cpqr_cluster_plan(ctx, m, n, C, nc, csmem)) {
+    CpClusterArgs c;
+    c.m = m; c.n = n; c.steps = a.steps; c.W = a.W; c.ldw = a.ldw; c.perm = perm; c.nc = nc; c.ldc = m;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(CP_THREADS);
+    cfg.dynamicSmemBytes = csmem;
+    cfg.stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ProfScope ps(ctx->prof, st, 1);
+    PBQ_CUDA(ctx, cudaLaunchKernelEx(&cfg, cpqr_cluster_fn(m), c));
+    ctx->launches += 1;
+    return PBQ_OK;
+  }
   PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
   void* args[] = {&a};
   ProfScope ps(ctx->prof, st, 1);

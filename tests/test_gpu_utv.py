@@ -343,3 +343,23 @@ def test_integration_installs_cor_utv(cuda, reference_pkg):
         assert reference_pkg.analysis.factorize(a, "cor_utv", 10, q=1, seed=4).t.shape == (10, 10)
     finally:
         integration.uninstall(saved)
+
+
+@pytest.mark.parametrize("shape,decades", [((300, 200), 10), ((256, 256), 6), ((90, 40), 4), ((12, 30), 3),
+                                           ((640, 600), 7)])
+def test_cpqr_cluster_and_grid_kernels_agree(cuda, monkeypatch, shape, decades):
+    """The single-cluster kernel (DSMEM, n ≤ ~640) and the cooperative-grid
+    kernel implement the same rule: identical pivots, both equal to LAPACK's."""
+    import torch
+
+    from paper_2103_07245_b200 import device as D
+
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    m = rng.standard_normal(shape) * np.logspace(0, -decades, shape[1])[rng.permutation(shape[1])]
+    t = D.as_kernel_operand(torch.from_numpy(m).to(cuda))
+    ctx = D.context(cuda)
+    p_cluster = D.cpqr_pivots(ctx, t).cpu().numpy()
+    monkeypatch.setenv("PBQ_CPQR_NO_CLUSTER", "1")
+    p_grid = D.cpqr_pivots(ctx, t).cpu().numpy()
+    assert np.array_equal(p_cluster, p_grid)
+    assert np.array_equal(p_cluster, oracle_column_pivoted_qr(m)[2])

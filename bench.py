@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--q", type=int, default=None, help="override the workload's q")
     ap.add_argument("--path", default="pbp_qlp", choices=["pbp_qlp", "r_svd", "cor_utv"],
                     help="r_svd / cor_utv: the sibling randomized paths (SURVEY §8 f3), single GPU")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: validates the N>1 code path with ranks sharing GPUs (host-mediated "
+                         "collectives); its timings are not bench values")
     return ap.parse_args()
 
 
@@ -264,6 +267,13 @@ def run_ours(args, world, rank, local):
         f = QlpFactors(plan.Q, plan.L, plan.P, None)
         check = {"recon_rel_err": reconstruction_error(a, f),
                  "method": "pbq_residual_fro (fused GEMM + residual epilogue, one pass over A)"}
+    else:
+        qg, l, p, _ = runner.factors()
+        sums = D.residual_fro(ctx, a, qg, l, p)  # this shard's ‖A_g − Q_g L Pᵀ‖², ‖A_g‖²
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        r2, a2 = sums.tolist()
+        check = {"recon_rel_err": (r2 / a2) ** 0.5,
+                 "method": "pbq_residual_fro per row shard (fused GEMM + residual epilogue) + allreduce(sum)"}
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -274,19 +284,21 @@ def run_ours(args, world, rank, local):
     # from the CUDA events recorded around each launch inside the timed region
     roof = None
     if rank == 0:
-        traffic = gemm_traffic(args.workload)
+        traffic = gemm_traffic(args.workload) if world == 1 else {"bytes": None, "source": None}
         gemm_ms, gemm_n = by_class["gemm"]
         big = 2 * q + 2  # A-passes per step; the P̄·W product is 2·n2·d² flops
-        fl_pass = 2.0 * n1 * n2 * d
-        fl_small = 2.0 * n2 * d * d
+        m_loc = n1 if world == 1 else (n1 * (rank + 1)) // world - (n1 * rank) // world  # this rank's rows
+        fl_pass = 2.0 * m_loc * n2 * d
+        fl_small = 2.0 * n2 * d * d + (0.0 if world == 1 else (q + 1) * 2.0 * m_loc * d * d)  # + TSQR Q·Q̂
         fl_total = args.steps * (big * fl_pass + fl_small)
         achieved = fl_total / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
         roof = {
             "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": traffic["bytes"],
             "traffic_unit": "bytes per launch (DRAM read + write)", "traffic_source": traffic["source"],
-            "algorithmic_bytes_per_launch": 8.0 * (n1 * n2 + n1 * d + n2 * d),
-            "kernel": "gemm_f64_ring (C=A^T X and D=A X, FP64 DMMA.8x8x4)",
+            "algorithmic_bytes_per_launch": 8.0 * (m_loc * n2 + m_loc * d + n2 * d),
+            "kernel": "gemm_f64_ring (C=A^T X and D=A X, FP64 DMMA.8x8x4)" + ("" if world == 1 else
+                      f", rank 0's row shard ({m_loc} rows); AᵀX in row-block chunks overlapped with their allreduce"),
             "per_launch_flop": fl_pass, "launches_per_step": gemm_n / args.steps,
             "gemm_ms_per_step": gemm_ms / args.steps, "gemm_share_of_step": gemm_ms / args.steps / ms,
             "qr_ms_per_step": by_class["qr"][0] / args.steps, "sketch_ms_per_step": by_class["sketch"][0] / args.steps,
@@ -297,6 +309,33 @@ def run_ours(args, world, rank, local):
 
     # ---- end to end through the public API with host (pinned) input
     e2e = None
+    if not args.no_e2e and world > 1:
+        # each rank: its pinned host shard → device, the sharded factorization,
+        # its Q rows (and on rank 0 the replicated L, P, R) back to the host;
+        # the step time is the max over ranks
+        a_host = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        a_host.copy_(a)
+        del a
+        torch.cuda.empty_cache()
+        ts = []
+        for i in range(max(3, min(args.steps, 10)) + 1):
+            barrier()
+            t0 = time.perf_counter()
+            a_dev = D.as_kernel_operand(a_host.to(dev, non_blocking=True))
+            runner.run(a_dev, seed=args.seed + 200 + i)
+            runner.finish()
+            qg, l, p, r = runner.factors()
+            outs = [qg.cpu()] + ([l.cpu(), p.cpu(), r.cpu()] if rank == 0 else [])
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            del a_dev
+            if i > 0:  # the first call is the warm-up
+                ts.append(float(dt.item()))
+        t_e2e = statistics.median(ts)
+        d2h = sum(x.numel() * 8 for x in outs)
+        e2e = {"value": flops / t_e2e / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(a_host.numel() * 8),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": t_e2e * 1e3,
+               "input": "pinned host row shard per rank (bytes: rank 0's)", "max_over_ranks": True}
     if not args.no_e2e and world == 1:
         a_host = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
         a_host.copy_(a)
@@ -329,6 +368,8 @@ def run_ours(args, world, rank, local):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "check": check,
         }
+        if world > 1 and args.dist_backend != "nccl":
+            line["validation_only"] = f"{args.dist_backend} collectives, ranks sharing GPUs: not a bench value"
         print(json.dumps(line), flush=True)
 
 
@@ -448,8 +489,13 @@ def main():
             if rank == 0:
                 run_reference(args, world, rank)
             return
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo":  # validation mode: ranks may share a GPU
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         try:
             run_ours(args, world, rank, local)
         finally:

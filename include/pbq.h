@@ -171,6 +171,25 @@ int pbq_cpqr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes);
 int pbq_gather_columns(pbq_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
                        const int64_t* perm, double* dst, int64_t ldd, void* stream);
 
+/* Distributed Cholesky-QR2 of a row-sharded tall matrix (the
+ * QR of A·P̄ across ranks, replacing the TSQR tree when the input is
+ * well-conditioned).  A is this rank's m×n row block.  The three stages run
+ * the guarded Cholesky-QR2 chain of pbq_householder_qr split at its two Gram
+ * matrices; between the stages the CALLER allreduces (sum) the np×np
+ * matrix G (np = *ldg) across ranks:
+ *   stage 0: G ← AᵀA (this rank's rows)
+ *   stage 1: [G summed] R₁ = chol(G) with the κ₁ ≤ 1e6 guard; Q₁ = A·R₁⁻¹;
+ *            G ← Q₁ᵀQ₁ (this rank's rows)
+ *   stage 2: [G summed] R = R₂·R₁ (diag ≥ 0, rank flag as orth); A ← Q₁·R₂⁻¹
+ * Every rank factors the same G, so R is bitwise identical on all ranks.
+ * *fallback (device int32) is set when the guard fails: A is then left
+ * untouched and the caller runs its TSQR instead.  The workspace must
+ * persist across the three calls. */
+int pbq_cholqr2_dist(pbq_ctx* ctx, int32_t stage, int64_t m, int64_t n, double* A, int64_t lda, double* R,
+                     int64_t ldr, int32_t* rank_flag, double* G, int32_t* fallback, void* workspace,
+                     size_t workspace_bytes, void* stream);
+int pbq_cholqr2_dist_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes, int64_t* ldg);
+
 /* Small helpers used by the host driver.
  * dst[i][j] = src[j][i]            (n×n), or with lower=1 the lower triangle
  * of srcᵀ and zeros above (L = tril(R̃ᵀ), algorithms.py:257). */

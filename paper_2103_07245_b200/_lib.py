@@ -49,6 +49,8 @@ EXPORTED = (
     "pbq_cpqr_pivots",
     "pbq_cpqr_workspace_bytes",
     "pbq_gather_columns",
+    "pbq_cholqr2_dist",
+    "pbq_cholqr2_dist_workspace_bytes",
 )
 
 c_i64 = ctypes.c_int64
@@ -111,6 +113,10 @@ _SIGS = {
     "pbq_cpqr_pivots": ([c_p, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_sz, c_p], ctypes.c_int),
     "pbq_cpqr_workspace_bytes": ([c_p, c_i64, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_gather_columns": ([c_p, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p], ctypes.c_int),
+    "pbq_cholqr2_dist": ([c_p, c_i32, c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_p, c_p, c_p, c_sz, c_p],
+                         ctypes.c_int),
+    "pbq_cholqr2_dist_workspace_bytes": ([c_p, c_i64, c_i64, ctypes.POINTER(c_sz), ctypes.POINTER(c_i64)],
+                                         ctypes.c_int),
 }
 
 _lib = None

@@ -108,6 +108,34 @@ __global__ void __launch_bounds__(256) cholqr_gram_reduce(const double* __restri
   }
 }
 
+// Distributed Cholesky-QR2: after the caller's allreduce(sum) of the local
+// Gram matrices, restore the identity padding (rows/cols in [n, np) summed
+// to G·I over G ranks) and, for pass 2, fold max|G − I| of the GLOBAL Gram
+// into `emax` (the local reduce's value is not the global one).
+__global__ void __launch_bounds__(256) cholqr_dist_fix(double* __restrict__ G, long n, long np,
+                                                       unsigned long long* emax) {
+  double dev = 0.0;
+  for (long e = long(blockIdx.x) * blockDim.x + threadIdx.x; e < np * np; e += long(gridDim.x) * blockDim.x) {
+    const long r = e / np, c = e % np;
+    if (r >= n || c >= n) {
+      G[e] = (r == c) ? 1.0 : 0.0;
+    } else if (emax && r <= c) {
+      const double d = fabs(G[e] - (r == c ? 1.0 : 0.0));
+      dev = (d <= dev) ? dev : d;  // NaN sticks
+    }
+  }
+  if (emax) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, dev, o);
+      dev = (x <= dev) ? dev : x;
+    }
+    if ((threadIdx.x & 31) == 0 && dev != 0.0) {
+      const unsigned long long bits = (dev == dev) ? __double_as_longlong(dev) : 0x7ff0000000000000ull;
+      atomicMax(emax, bits);
+    }
+  }
+}
+
 struct CqArgs {
   int nb;             // 32-blocks per side; np = 32·nb
   long n, np;

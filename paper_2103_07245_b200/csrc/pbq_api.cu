@@ -542,6 +542,87 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   return hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, ext ? hh_req : fallback);
 }
 
+// ------------------------------------------- distributed Cholesky-QR2 ----
+// Row-sharded A (this rank's m×n rows): the chain of cq_launch split at its
+// two Gram matrices, which the caller allreduces (sum) across ranks between
+// stages.  Every rank then factors the same global Gram → identical R.
+//   stage 0: G ← AᵀA (local)
+//   stage 1: [G global] R₁ (κ guard → *fallback), Q₁ = A·R₁⁻¹, G ← Q₁ᵀQ₁ (local)
+//   stage 2: [G global] R = R₂R₁ (+ rank flag), A ← Q₁·R₂⁻¹
+// On *fallback (κ₁ > 1e6, or a failed pass 2) A is left untouched and the
+// caller runs its TSQR instead.  The workspace persists across the stages.
+size_t cqd_ws_bytes(const CqPlan& p, long m) {
+  const size_t sq = align_up(size_t(p.np) * p.np * sizeof(double), 256);
+  return 256 + 5 * sq + align_up(2 * size_t(p.nb) * p.np * sizeof(double), 256) + align_up(p.gemm_ws, 256) +
+         align_up(size_t(m) * p.ldq1 * sizeof(double), 256) + 1024;
+}
+
+int cqd_stage(pbq_ctx* ctx, int stage, long m, long n, double* A, long lda, double* R, long ldr, int32_t* rank_flag,
+              double* G, int32_t* fallback, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (m < n || n < 1) return fail(ctx, PBQ_ERR_DIM, "cholqr2_dist: needs m >= n >= 1 (got %ldx%ld)", m, n);
+  if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "cholqr2_dist: leading dimension too small");
+  if ((lda & 1) || !aligned16(A)) return fail(ctx, PBQ_ERR_PARAM, "cholqr2_dist: lda must be even and A 16-byte aligned");
+  if (!G || !fallback || !R) return fail(ctx, PBQ_ERR_PARAM, "cholqr2_dist: null pointer argument");
+  const CqPlan pl = cq_plan(ctx, m, n);
+  const size_t sq = size_t(pl.np) * pl.np;
+  Carve cv(ws, ws_bytes);
+  int* ctl = cv.take<int>(64);  // [1] [2] grid-barrier counters, [4] emax of pass 2
+  double* X1 = cv.take<double>(sq);
+  double* X2 = cv.take<double>(sq);
+  double* R1 = cv.take<double>(sq);
+  double* R2 = cv.take<double>(sq);
+  double* T = cv.take<double>(sq);
+  double* colsum = cv.take<double>(2 * size_t(pl.nb) * pl.np);
+  char* gws = cv.take<char>(pl.gemm_ws);
+  double* Q1 = cv.take<double>(size_t(m) * pl.ldq1);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "cholqr2_dist: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  double* part = reinterpret_cast<double*>(gws);
+  auto counter = [&](int i) { return reinterpret_cast<unsigned int*>(ctl + i); };
+  auto emax_slot = [&](int i) { return reinterpret_cast<unsigned long long*>(ctl + i); };
+  ProfScope ps(ctx->prof, st, 1);
+  ProfSuppress quiet(ctx->prof);
+  const unsigned fix_grid = unsigned(std::min<long>(ceil_div(long(sq), 256), 64));
+  CqArgs f;
+  memset(&f, 0, sizeof(f));
+  f.nb = pl.nb; f.n = n; f.np = pl.np; f.m = m;
+  f.G = G; f.T = T; f.fallback = fallback;
+  f.colsum = colsum; f.stats = ctx->cq_stats; f.fail_stats = ctx->cq_stats;
+  f.kappa_max = CQ_KAPPA_MAX;
+  f.phase_ns = ctx->qr_phase_ns;
+  f.allow_series = ctx->qr_method != PBQ_QR_CHOLQR_NOSERIES;
+  if (stage == 0) {
+    PBQ_CUDA(ctx, cudaMemsetAsync(ctl, 0, 64 * sizeof(int), st));
+    PBQ_CUDA(ctx, cudaMemsetAsync(fallback, 0, sizeof(int32_t), st));
+    PBQ_TRY(gram_launch(ctx, pl, m, n, A, lda, part, nullptr, st));
+    PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, nullptr, nullptr, st));
+    return PBQ_OK;
+  }
+  if (stage == 1) {
+    cholqr_dist_fix<<<fix_grid, 256, 0, st>>>(G, n, pl.np, nullptr);
+    PBQ_CUDA(ctx, cudaGetLastError());
+    ctx->launches += 1;
+    f.pass = 1; f.R = R1; f.X = X1; f.counter = counter(1);
+    PBQ_TRY(factor_launch(ctx, pl, f, st));
+    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
+                               fallback, true));
+    PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st));
+    PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, nullptr, st));
+    return PBQ_OK;
+  }
+  if (stage == 2) {
+    cholqr_dist_fix<<<fix_grid, 256, 0, st>>>(G, n, pl.np, emax_slot(4));
+    PBQ_CUDA(ctx, cudaGetLastError());
+    ctx->launches += 1;
+    f.pass = 2; f.R = R2; f.X = X2; f.R1 = R1; f.Rout = R; f.ldr = ldr; f.rank_flag = rank_flag;
+    f.emax = emax_slot(4); f.counter = counter(2);
+    PBQ_TRY(factor_launch(ctx, pl, f, st));
+    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q1, pl.ldq1, X2, pl.np, 0.0, A, lda, nullptr, gws, pl.gemm_ws, st,
+                               fallback, true));
+    return PBQ_OK;
+  }
+  return fail(ctx, PBQ_ERR_PARAM, "cholqr2_dist: stage must be 0, 1 or 2");
+}
+
 size_t qr_any_ws_bytes(const pbq_ctx* ctx, const QrPlan& hp, long m, long n) {
   if (ctx->qr_method != PBQ_QR_HOUSEHOLDER) return cq_ws_bytes(cq_plan(ctx, m, n), hp, m, n);
   return qr_ws_bytes(hp, n);
@@ -1063,6 +1144,22 @@ int pbq_gather_columns(pbq_ctx* ctx, int64_t rows, int64_t cols, const double* s
                        double* dst, int64_t ldd, void* stream) {
   if (!ctx) return PBQ_ERR_PARAM;
   return gather_launch(ctx, rows, cols, src, lds, perm, dst, ldd, static_cast<cudaStream_t>(stream));
+}
+
+int pbq_cholqr2_dist_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes, int64_t* ldg) {
+  if (!ctx || !bytes || !ldg) return PBQ_ERR_PARAM;
+  if (m < n || n < 1) return fail(ctx, PBQ_ERR_DIM, "cholqr2_dist: needs m >= n >= 1");
+  const CqPlan pl = cq_plan(ctx, m, n);
+  *bytes = cqd_ws_bytes(pl, m);
+  *ldg = pl.np;
+  return PBQ_OK;
+}
+
+int pbq_cholqr2_dist(pbq_ctx* ctx, int32_t stage, int64_t m, int64_t n, double* A, int64_t lda, double* R, int64_t ldr,
+                     int32_t* rank_flag, double* G, int32_t* fallback, void* ws, size_t ws_bytes, void* stream) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  return cqd_stage(ctx, stage, m, n, A, lda, R, ldr, rank_flag, G, fallback, ws, ws_bytes,
+                   static_cast<cudaStream_t>(stream));
 }
 
 int pbq_set_qr_method(pbq_ctx* ctx, int32_t method) {

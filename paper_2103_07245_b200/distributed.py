@@ -11,10 +11,14 @@ of the global stream, so Φ does not depend on G).  Exchanges:
   b overlaps the GEMM of block b+1 and only the last block's allreduce is
   exposed.  The result is identical on all ranks, so ``orth`` of it is
   computed replicated (same input → same bits).
-* qr(A·P̄) — A_g·P̄ is local; its QR is a distributed TSQR: local Householder
-  QR (Q_g, R_g), all-gather of the d×d R factors, a replicated QR of the
-  stacked (G·d)×d matrix → (Q̂, R), then Q_g ← Q_g·Q̂_g (local GEMM).  R and
-  the `orth` rank test come from the replicated QR.
+* qr(A·P̄) — A_g·P̄ is local; its QR is a distributed Cholesky-QR2
+  (``pbq_cholqr2_dist``): local Gram A_gᵀA_g, allreduce(sum) of the d×d Gram,
+  the guarded factorization replicated (same G → same R on every rank), the
+  local product, and again for the second pass — two d×d allreduces and no
+  tall replicated work.  When its κ guard fires (one 4-byte flag read per
+  call) the shard is untouched and the TSQR tree runs instead: local QR
+  (Q_g, R_g), all-gather of the d×d R factors, a replicated QR of the stacked
+  (G·d)×d matrix → (Q̂, R), then Q_g ← Q_g·Q̂_g (local GEMM).
 * qr(Rᵀ), L = tril(R̃ᵀ) and P = P̄·W are replicated.
 
 Q stays row-sharded (rank g holds Q[r_g : r_{g+1}]); L, P, R are replicated.
@@ -72,11 +76,31 @@ class CudaBackend:
     def contiguous(self, t):
         return _dev.as_kernel_operand(t)
 
+    # -- distributed Cholesky-QR2 (pbq_cholqr2_dist) -------------------------
+    def cholqr2_dist_state(self, m, n):
+        """Persistent (workspace, G, fallback flag) for one m×n shard shape."""
+        nbytes, ldg = ctypes.c_size_t(), ctypes.c_int64()
+        self.ctx.check(self.ctx.lib.pbq_cholqr2_dist_workspace_bytes(self.ctx.handle, m, n, ctypes.byref(nbytes),
+                                                                     ctypes.byref(ldg)), "cholqr2_dist workspace")
+        g = torch.zeros((ldg.value, ldg.value), dtype=torch.float64, device=self.device)
+        return {"ws": _dev.workspace(nbytes.value, self.device), "nbytes": nbytes.value, "G": g,
+                "fallback": torch.zeros(1, dtype=torch.int32, device=self.device)}
+
+    def cholqr2_dist(self, stage, a, r, state, flag=None):
+        """One stage of the distributed Cholesky-QR2 of the shard ``a`` (in place)."""
+        m, n = a.shape
+        st = self.ctx.lib.pbq_cholqr2_dist(self.ctx.handle, int(stage), m, n, _dev.ptr(a), _dev.ld_of(a), _dev.ptr(r),
+                                           _dev.ld_of(r), _dev.ptr(flag), _dev.ptr(state["G"]),
+                                           _dev.ptr(state["fallback"]), _dev.ptr(state["ws"]), state["nbytes"],
+                                           _dev.stream_ptr(self.device))
+        self.ctx.check(st, "cholqr2_dist")
+
 
 class DistributedPbpQlp:
     """One rank's part of a row-sharded PbP-QLP; all ranks call ``run``."""
 
-    def __init__(self, n1, n2, d, q, rows, device=None, reorthonormalize=True, group=None, backend=None, chunks=None):
+    def __init__(self, n1, n2, d, q, rows, device=None, reorthonormalize=True, group=None, backend=None, chunks=None,
+                 dist_qr="auto"):
         self.n1, self.n2, self.d, self.q = int(n1), int(n2), int(d), int(q)
         self.rows = list(rows)
         self.group = group
@@ -109,6 +133,15 @@ class DistributedPbpQlp:
         self.Qtmp = be.empty(self.m, self.d)
         self.flags = be.zeros_i32(2 * self.q + 3)  # [non-finite, sketch status, rank flags …]
         self.PHI = None
+        # qr(A·P̄): distributed Cholesky-QR2 (one d×d allreduce per pass) with
+        # the TSQR tree as its fallback, or the TSQR tree alone
+        if dist_qr not in ("auto", "cholqr2", "tsqr"):
+            raise _exc.ParameterError("dist_qr must be 'auto', 'cholqr2' or 'tsqr'")
+        use_cq = dist_qr != "tsqr" and hasattr(be, "cholqr2_dist")
+        if dist_qr == "cholqr2" and not use_cq:
+            raise _exc.ParameterError("this backend has no distributed Cholesky-QR2")
+        self.cq_state = be.cholqr2_dist_state(self.m, self.d) if use_cq else None
+        self.tsqr_fallbacks = 0
 
     # -- collectives ---------------------------------------------------------
     def _chunk_bounds(self):
@@ -153,6 +186,24 @@ class DistributedPbpQlp:
         be.gemm_nn(self.Q, be.contiguous(qhat), self.Qtmp)
         self.Q.copy_(self.Qtmp)
 
+    def _qr_sharded_(self, flag=None):
+        """QR of the row-sharded self.Q in place (R → self.R): distributed
+        Cholesky-QR2 — local Gram, allreduce(sum) of the d×d Gram, replicated
+        factor, local product, twice — and the TSQR tree only when its κ guard
+        fires (one 4-byte flag read per call)."""
+        st = self.cq_state
+        if st is None:
+            return self._tsqr_(flag)
+        be = self.be
+        be.cholqr2_dist(0, self.Q, self.R, st, flag)
+        dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
+        be.cholqr2_dist(1, self.Q, self.R, st, flag)
+        dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
+        be.cholqr2_dist(2, self.Q, self.R, st, flag)
+        if int(st["fallback"].item()):  # identical on every rank (same G)
+            self.tsqr_fallbacks += 1
+            self._tsqr_(flag)
+
     # -- the algorithm ------------------------------------------------------
     def run(self, A_local, seed=0, phi_local=None):
         """Enqueue one factorization of this rank's rows (kernel-ready operand)."""
@@ -171,7 +222,7 @@ class DistributedPbpQlp:
             site += 1
             for _ in range(q):
                 be.gemm_nn(A_local, self.C, self.Q)
-                self._tsqr_(flags[site:site + 1])
+                self._qr_sharded_(flags[site:site + 1])
                 site += 1
                 self._at_x(A_local, self.Q)
                 be.qr_(self.C, self.Rs, flags[site:site + 1])
@@ -182,7 +233,7 @@ class DistributedPbpQlp:
                 self._at_x(A_local, self.Q)
             be.qr_(self.C, self.Rs, flags[site:site + 1])
         be.gemm_nn(A_local, self.C, self.Q)
-        self._tsqr_()
+        self._qr_sharded_()
         be.transpose(self.R, self.W)
         be.qr_(self.W, self.Rt)
         be.transpose(self.Rt, self.L, lower=True)

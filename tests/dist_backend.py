@@ -43,3 +43,44 @@ class NumpyBackend:
 
     def contiguous(self, t):
         return t.contiguous()
+
+    # -- distributed Cholesky-QR2, restated for the CPU (pbq_cholqr2_dist) --
+    KAPPA_MAX = 1e6  # the device guard (pbq_api.cu CQ_KAPPA_MAX)
+
+    def cholqr2_dist_state(self, m, n):
+        return {"G": torch.zeros((n, n), dtype=torch.float64), "fallback": torch.zeros(1, dtype=torch.int32)}
+
+    def cholqr2_dist(self, stage, a, r, state, flag=None):
+        import scipy.linalg as sla
+
+        g = state["G"]
+        if stage == 0:
+            state["fallback"].zero_()
+            g.copy_(torch.from_numpy(a.numpy().T @ a.numpy()))
+            return
+        if state["fallback"].item():
+            return
+        if stage == 1:
+            try:
+                r1 = np.linalg.cholesky(g.numpy()).T
+            except np.linalg.LinAlgError:
+                state["fallback"].fill_(1)
+                return
+            r1i = sla.solve_triangular(r1, np.eye(r1.shape[0]), lower=False)
+            if not np.linalg.norm(r1, 1) * np.linalg.norm(r1i, 1) <= self.KAPPA_MAX:
+                state["fallback"].fill_(1)
+                return
+            q1 = a.numpy() @ r1i
+            state["r1"], state["q1"] = r1, q1
+            g.copy_(torch.from_numpy(q1.T @ q1))
+            return
+        try:
+            r2 = np.linalg.cholesky(g.numpy()).T
+        except np.linalg.LinAlgError:
+            state["fallback"].fill_(1)
+            return
+        rr = r2 @ state["r1"]
+        r.copy_(torch.from_numpy(np.triu(rr)))
+        a.copy_(torch.from_numpy(sla.solve_triangular(r2, state["q1"].T, trans="T", lower=False).T))
+        if flag is not None:
+            flag.fill_(rank_flag(rr))

@@ -18,7 +18,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks=None):
+def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks=None, dist_qr="auto"):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -34,7 +34,8 @@ def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks=None):
     try:
         n1, n2 = a.shape
         rows = shard_rows(n1, world)
-        run = DistributedPbpQlp(n1, n2, d, q, rows, reorthonormalize=reorth, backend=NumpyBackend(), chunks=chunks)
+        run = DistributedPbpQlp(n1, n2, d, q, rows, reorthonormalize=reorth, backend=NumpyBackend(), chunks=chunks,
+                                dist_qr=dist_qr)
         a_loc = torch.from_numpy(np.ascontiguousarray(a[rows[rank]:rows[rank + 1]]))
         run.run(a_loc, seed=seed)
         import warnings
@@ -44,20 +45,23 @@ def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks=None):
             run.finish()
         qg, l, p, r = run.factors()
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), q=qg.numpy(), l=l.numpy(), p=p.numpy(), r=r.numpy(),
-                 phi=run.PHI.numpy(), warn=len(rec))
+                 phi=run.PHI.numpy(), warn=len(rec), tsqr=run.tsqr_fallbacks)
     finally:
         dist.destroy_process_group()
 
 
-def _run(a, d, q, seed, reorth, tmp_path, world=2, chunks=None):
+def _run(a, d, q, seed, reorth, tmp_path, world=2, chunks=None, dist_qr="auto"):
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, a, d, q, seed, reorth, str(tmp_path), chunks), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, a, d, q, seed, reorth, str(tmp_path), chunks, dist_qr), nprocs=world,
+             join=True)
     parts = [np.load(os.path.join(tmp_path, f"rank{g}.npz")) for g in range(world)]
     return parts
 
 
-@pytest.mark.parametrize("q,reorth,chunks", [(0, True, None), (1, True, None), (1, False, None), (1, True, 3)])
-def test_row_sharded_matches_oracle(tmp_path, q, reorth, chunks):
+@pytest.mark.parametrize("q,reorth,chunks,dist_qr", [(0, True, None, "auto"), (1, True, None, "auto"),
+                                                     (1, False, None, "auto"), (1, True, 3, "auto"),
+                                                     (1, True, None, "tsqr")])
+def test_row_sharded_matches_oracle(tmp_path, q, reorth, chunks, dist_qr):
     """chunks=3 splits AᵀX into row blocks of 128 (n2 = 300 → 128, 128, 44)
     whose allreduces are issued asynchronously while later blocks compute."""
     from oracle.pbp_qlp_oracle import column_relative_error, conditioning_tolerance, oracle_pbp_qlp
@@ -66,7 +70,8 @@ def test_row_sharded_matches_oracle(tmp_path, q, reorth, chunks):
     n2 = 300 if chunks else 90
     a = rng.standard_normal((240, 40)) @ rng.standard_normal((40, n2)) / 7 + 1e-3 * rng.standard_normal((240, n2))
     d = 24
-    parts = _run(a, d, q, 5, reorth, tmp_path, chunks=chunks)
+    parts = _run(a, d, q, 5, reorth, tmp_path, chunks=chunks, dist_qr=dist_qr)
+    assert all(int(p["tsqr"]) == 0 for p in parts)  # well-conditioned: Cholesky-QR2 (or TSQR when asked)
     ref = oracle_pbp_qlp(a, d, q=q, seed=5, reorthonormalize=reorth)
     qfull = np.vstack([p["q"] for p in parts])
     phi = np.vstack([p["phi"] for p in parts])
@@ -87,3 +92,4 @@ def test_row_sharded_rank_warning(tmp_path):
     a = rng.standard_normal((120, 3)) @ rng.standard_normal((3, 50))
     parts = _run(a, 8, 1, 2, True, tmp_path)
     assert all(int(p["warn"]) == 3 for p in parts)  # every orth site warns on every rank
+    assert all(int(p["tsqr"]) == 2 for p in parts)  # rank 3 < d: the Cholesky guard hands both QRs to TSQR

@@ -6,8 +6,9 @@ gloo's collectives are host-mediated (stream sync → host copy → TCP → copy
 back), so no rank's kernel ever waits on another rank's kernel: this is safe
 on one GPU, unlike NCCL ranks sharing a device.  It exercises everything the
 N-GPU bench runs except the NCCL transport itself: the sharded sketch rows,
-the chunked AᵀX GEMMs with their asynchronous allreduces, the TSQR all-gather
-and replicated QR, the flag reduction, and the replicated second stage."""
+the chunked AᵀX GEMMs with their asynchronous allreduces, the distributed
+Cholesky-QR2 of A·P̄ (pbq_cholqr2_dist stages around two Gram allreduces) and
+its TSQR fallback, the flag reduction, and the replicated second stage."""
 import os
 import socket
 
@@ -26,7 +27,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks):
+def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks, dist_qr):
     import sys
     import warnings
 
@@ -45,7 +46,8 @@ def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks):
     try:
         n1, n2 = a.shape
         rows = shard_rows(n1, world)
-        run = DistributedPbpQlp(n1, n2, d, q, rows, device=dev, reorthonormalize=reorth, chunks=chunks)
+        run = DistributedPbpQlp(n1, n2, d, q, rows, device=dev, reorthonormalize=reorth, chunks=chunks,
+                                dist_qr=dist_qr)
         a_loc = D.as_kernel_operand(torch.from_numpy(np.ascontiguousarray(a[rows[rank]:rows[rank + 1]])).to(dev))
         launches0 = run.be.ctx.launch_count
         run.run(a_loc, seed=seed)
@@ -54,27 +56,32 @@ def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks):
             run.finish()
         qg, l, p, r = (t.cpu().numpy() for t in run.factors())
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), q=qg, l=l, p=p, r=r, phi=run.PHI.cpu().numpy(),
-                 warn=len(rec), launches=run.be.ctx.launch_count - launches0)
+                 warn=len(rec), launches=run.be.ctx.launch_count - launches0, tsqr=run.tsqr_fallbacks)
     finally:
         dist.destroy_process_group()
 
 
-def _run(a, d, q, seed, reorth, tmp_path, world, chunks=None):
+def _run(a, d, q, seed, reorth, tmp_path, world, chunks=None, dist_qr="auto"):
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, a, d, q, seed, reorth, str(tmp_path), chunks), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, a, d, q, seed, reorth, str(tmp_path), chunks, dist_qr), nprocs=world,
+             join=True)
     return [np.load(os.path.join(tmp_path, f"rank{g}.npz")) for g in range(world)]
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("world,q,reorth,chunks", [(2, 1, True, None), (3, 1, True, 3), (2, 2, False, None),
-                                                   (2, 0, True, 1)])
-def test_sharded_device_path_matches_oracle(cuda, tmp_path, world, q, reorth, chunks):
+@pytest.mark.parametrize("world,q,reorth,chunks,dist_qr", [(2, 1, True, None, "auto"), (3, 1, True, 3, "auto"),
+                                                           (2, 2, False, None, "auto"), (2, 0, True, 1, "auto"),
+                                                           (2, 1, True, None, "tsqr"), (3, 2, True, None, "tsqr")])
+def test_sharded_device_path_matches_oracle(cuda, tmp_path, world, q, reorth, chunks, dist_qr):
+    """dist_qr "auto": qr(A·P̄) by the distributed Cholesky-QR2 (two d×d
+    allreduces); "tsqr": the TSQR tree it falls back to."""
     from oracle.pbp_qlp_oracle import column_relative_error, conditioning_tolerance, oracle_pbp_qlp
 
     rng = np.random.default_rng(17)
     n1, n2, d = 1500, 700, 48
     a = rng.standard_normal((n1, 60)) @ rng.standard_normal((60, n2)) / 8 + 1e-3 * rng.standard_normal((n1, n2))
-    parts = _run(a, d, q, 9, reorth, tmp_path, world, chunks)
+    parts = _run(a, d, q, 9, reorth, tmp_path, world, chunks, dist_qr)
+    assert all(int(p["tsqr"]) == 0 for p in parts)
     ref = oracle_pbp_qlp(a, d, q=q, seed=9, reorthonormalize=reorth)
     assert all(int(p["launches"]) > 0 for p in parts)  # the device kernels ran in every rank
     phi = np.vstack([p["phi"] for p in parts])
@@ -100,3 +107,4 @@ def test_sharded_device_path_rank_warnings(cuda, tmp_path):
     a = rng.standard_normal((600, 3)) @ rng.standard_normal((3, 200))
     parts = _run(a, 8, 1, 2, True, tmp_path, 2)
     assert all(int(p["warn"]) == 3 for p in parts)  # every orth site warns on every rank
+    assert all(int(p["tsqr"]) == 2 for p in parts)  # the Cholesky guard handed both QRs of A·P̄ to TSQR

@@ -120,7 +120,13 @@ class DistributedPbpQlp:
             raise _exc.ParameterError("chunks must be >= 1")
         self.be = backend if backend is not None else CudaBackend(device)
         be = self.be
-        self.C = be.empty(self.n2, self.d)         # AᵀX partial → allreduced → P̄ (in place)
+        # AᵀX partial → allreduced → P̄ (in place).  G·s rows (s = ⌈n2/G⌉) so
+        # that orth(C) can run on equal row slices; rows ≥ n2 stay zero.
+        self.slice_rows = -(-self.n2 // self.world)
+        self.Cbuf = be.empty(self.world * self.slice_rows, self.d)
+        ldc = self.Cbuf.stride(0)
+        self.Cbuf.as_strided((self.Cbuf.shape[0], ldc), (ldc, 1)).zero_()  # incl. the even-ld pad column
+        self.C = self.Cbuf[:self.n2]
         self.Q = be.empty(self.m, self.d)          # A_g·P̄ → local Q_g → Q rows of this rank
         self.R = be.empty(self.d, self.d)
         self.Rloc = be.empty(self.d, self.d)
@@ -142,6 +148,11 @@ class DistributedPbpQlp:
             raise _exc.ParameterError("this backend has no distributed Cholesky-QR2")
         self.cq_state = be.cholqr2_dist_state(self.m, self.d) if use_cq else None
         self.tsqr_fallbacks = 0
+        # orth(C) sharded over row slices (same distributed Cholesky-QR2, then an
+        # all-gather of the slices) when every slice has ≥ d rows; else replicated
+        self.c_state = (be.cholqr2_dist_state(self.slice_rows, self.d)
+                        if use_cq and self.world > 1 and self.slice_rows >= self.d else None)
+        self.orth_fallbacks = 0
 
     # -- collectives ---------------------------------------------------------
     def _chunk_bounds(self):
@@ -204,6 +215,36 @@ class DistributedPbpQlp:
             self.tsqr_fallbacks += 1
             self._tsqr_(flag)
 
+    def _orth_c_(self, flag):
+        """orth(C) in place, C replicated on every rank: each rank
+        orthonormalizes its row slice by the distributed Cholesky-QR2 (two
+        d×d allreduces), then the slices are all-gathered.  On a guard failure
+        C is untouched everywhere and every rank runs the replicated QR."""
+        st = self.c_state
+        if st is None:
+            return self.be.qr_(self.C, self.Rs, flag)
+        be = self.be
+        s0 = self.rank * self.slice_rows
+        mine = self.Cbuf[s0:s0 + self.slice_rows]
+        be.cholqr2_dist(0, mine, self.Rs, st, flag)
+        dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
+        be.cholqr2_dist(1, mine, self.Rs, st, flag)
+        dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
+        be.cholqr2_dist(2, mine, self.Rs, st, flag)
+        if int(st["fallback"].item()):  # identical on every rank (same G); C untouched
+            self.orth_fallbacks += 1
+            return be.qr_(self.C, self.Rs, flag)
+        buf = self.Cbuf
+        ld = buf.stride(0)
+        whole = buf.as_strided((buf.shape[0], ld), (ld, 1))  # whole rows incl. the even-ld pad column
+        part = whole[s0:s0 + self.slice_rows]
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(whole, part, group=self.group)  # in place: part is rank's chunk
+        else:
+            parts = [torch.empty_like(part) for _ in range(self.world)]
+            dist.all_gather(parts, part.contiguous(), group=self.group)
+            whole.copy_(torch.cat(parts, 0))
+
     # -- the algorithm ------------------------------------------------------
     def run(self, A_local, seed=0, phi_local=None):
         """Enqueue one factorization of this rank's rows (kernel-ready operand)."""
@@ -218,20 +259,20 @@ class DistributedPbpQlp:
         site = 2
         self._at_x(A_local, self.PHI, nonfinite=flags[0:1])
         if self.reorthonormalize:
-            be.qr_(self.C, self.Rs, flags[site:site + 1])
+            self._orth_c_(flags[site:site + 1])
             site += 1
             for _ in range(q):
                 be.gemm_nn(A_local, self.C, self.Q)
                 self._qr_sharded_(flags[site:site + 1])
                 site += 1
                 self._at_x(A_local, self.Q)
-                be.qr_(self.C, self.Rs, flags[site:site + 1])
+                self._orth_c_(flags[site:site + 1])
                 site += 1
         else:
             for _ in range(q):
                 be.gemm_nn(A_local, self.C, self.Q)
                 self._at_x(A_local, self.Q)
-            be.qr_(self.C, self.Rs, flags[site:site + 1])
+            self._orth_c_(flags[site:site + 1])
         be.gemm_nn(A_local, self.C, self.Q)
         self._qr_sharded_()
         be.transpose(self.R, self.W)

@@ -45,7 +45,7 @@ def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks=None, dist_
             run.finish()
         qg, l, p, r = run.factors()
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), q=qg.numpy(), l=l.numpy(), p=p.numpy(), r=r.numpy(),
-                 phi=run.PHI.numpy(), warn=len(rec), tsqr=run.tsqr_fallbacks)
+                 phi=run.PHI.numpy(), warn=len(rec), tsqr=run.tsqr_fallbacks, orthfb=run.orth_fallbacks)
     finally:
         dist.destroy_process_group()
 
@@ -92,4 +92,5 @@ def test_row_sharded_rank_warning(tmp_path):
     a = rng.standard_normal((120, 3)) @ rng.standard_normal((3, 50))
     parts = _run(a, 8, 1, 2, True, tmp_path)
     assert all(int(p["warn"]) == 3 for p in parts)  # every orth site warns on every rank
-    assert all(int(p["tsqr"]) == 2 for p in parts)  # rank 3 < d: the Cholesky guard hands both QRs to TSQR
+    assert all(int(p["tsqr"]) == 2 for p in parts)
+    assert all(int(p["orthfb"]) == 2 for p in parts)  # ... and both orth(C) calls to the replicated QR  # rank 3 < d: the Cholesky guard hands both QRs to TSQR

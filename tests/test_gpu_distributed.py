@@ -56,7 +56,7 @@ def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks, dist_qr):
             run.finish()
         qg, l, p, r = (t.cpu().numpy() for t in run.factors())
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), q=qg, l=l, p=p, r=r, phi=run.PHI.cpu().numpy(),
-                 warn=len(rec), launches=run.be.ctx.launch_count - launches0, tsqr=run.tsqr_fallbacks)
+                 warn=len(rec), launches=run.be.ctx.launch_count - launches0, tsqr=run.tsqr_fallbacks, orthfb=run.orth_fallbacks)
     finally:
         dist.destroy_process_group()
 
@@ -107,4 +107,5 @@ def test_sharded_device_path_rank_warnings(cuda, tmp_path):
     a = rng.standard_normal((600, 3)) @ rng.standard_normal((3, 200))
     parts = _run(a, 8, 1, 2, True, tmp_path, 2)
     assert all(int(p["warn"]) == 3 for p in parts)  # every orth site warns on every rank
-    assert all(int(p["tsqr"]) == 2 for p in parts)  # the Cholesky guard handed both QRs of A·P̄ to TSQR
+    assert all(int(p["tsqr"]) == 2 for p in parts)
+    assert all(int(p["orthfb"]) == 2 for p in parts)  # ... and both orth(C) calls to the replicated QR  # the Cholesky guard handed both QRs of A·P̄ to TSQR

@@ -90,269 +90,10 @@ struct GemmCfg {
   static_assert((BK * B_ROWW) % THREADS == 0 && THREADS % B_ROWW == 0, "B loader geometry");
 };
 
-template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES, bool CHECK, bool SPLIT = false>
-__global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::THREADS, 1)
-    gemm_f64_streamk(GemmArgs p) {
-  if (p.skip && __ldcg(p.skip) != 0) return;
-  using Cfg = GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>;
-  constexpr int THREADS = Cfg::THREADS;
-  constexpr int MT = Cfg::MT, NT = Cfg::NT;
-  constexpr int KSTEPS = BK / 4;
-  extern __shared__ __align__(128) double smem[];
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm0 = (warp / Cfg::WARPS_N) * WM;
-  const int wn0 = (warp % Cfg::WARPS_N) * WN;
-  const int G = gridDim.x;
-
-  // per-thread loader geometry (first chunk; the others are +ROW_STEP rows)
-  const int a_row = tid / Cfg::A_ROWW, a_col = (tid % Cfg::A_ROWW) * 2;
-  const int b_row = tid / Cfg::B_ROWW, b_col = (tid % Cfg::B_ROWW) * 2;
-  const long a_kstep = TRANS_A ? long(BK) * p.lda : long(BK);  // pointer advance per k-block
-  const long b_kstep = long(BK) * p.ldb;
-  const long a_rstep = long(Cfg::A_ROW_STEP) * p.lda;
-  const long b_rstep = long(Cfg::B_ROW_STEP) * p.ldb;
-
-  long it = long(blockIdx.x) * p.total_iters / G;
-  const long it_end = long(blockIdx.x + 1) * p.total_iters / G;
-  int unit = blockIdx.x;
-  bool saw_nonfinite = false;
-
-  for (;;) {
-    int tile, kb, ke, tm, tn;
-    int tile_k = p.k_iters;  // k-blocks of this tile
-    long tile_it0 = 0;       // stream-K index of this tile's k=0 block
-    if (SPLIT) {
-      if (unit >= p.units) break;
-      const int tsel = unit / p.split, s = unit % p.split;
-      if (p.sym) {
-        upper_tile(tsel, p.tiles_n, tm, tn);
-      } else {
-        tm = tsel / p.tiles_n;
-        tn = tsel % p.tiles_n;
-      }
-      tile = tsel;
-      kb = int(long(s) * p.k_iters / p.split);
-      ke = int(long(s + 1) * p.k_iters / p.split);
-    } else {
-      if (it >= it_end) break;
-      if (p.tri_b) {
-        tm = int(it / p.row_iters);
-        int rem = int(it % p.row_iters);
-        tn = 0;
-        for (;;) {
-          const int kt = int(lmin(p.k_iters, long(tn + 1) * BN / BK));
-          if (rem < kt) {
-            tile_k = kt;
-            break;
-          }
-          rem -= kt;
-          ++tn;
-        }
-        kb = rem;
-        tile = tm * p.tiles_n + tn;
-      } else {
-        tile = int(it / p.k_iters);
-        kb = int(it % p.k_iters);
-        tm = tile / p.tiles_n;
-        tn = tile % p.tiles_n;
-        tile_k = p.k_iters;
-      }
-      tile_it0 = it - kb;
-      ke = int(lmin(tile_k, kb + (it_end - it)));
-    }
-    const long m0 = long(tm) * BM, n0 = long(tn) * BN;
-    const bool check = CHECK && (tn == 0);
-
-    // loader state for this tile: one source pointer per operand, byte
-    // counts for the M/N edge (K edge checked only on the last k-block)
-    const double* a_src;
-    int a_bytes;
-    if (TRANS_A) {
-      const long gm = m0 + a_col;
-      a_bytes = gm < p.M ? int(lmin(2, p.M - gm)) * 8 : 0;
-      a_src = p.A + (long(kb) * BK + a_row) * p.lda + (a_bytes ? gm : 0);
-    } else {
-      a_bytes = 16;
-      a_src = p.A + (m0 + a_row) * p.lda + long(kb) * BK + a_col;
-    }
-    const long gn = n0 + b_col;
-    const int b_bytes = gn < p.N ? int(lmin(2, p.N - gn)) * 8 : 0;
-    const double* b_src = p.B + (long(kb) * BK + b_row) * p.ldb + (b_bytes ? gn : 0);
-
-    double acc[MT][NT][2];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    auto load_stage = [&](int stage, int kblk) {
-      double* sA = smem + stage * Cfg::STAGE_ELEMS;
-      double* sB = sA + Cfg::SA_ELEMS;
-      const long k0 = long(kblk) * BK;
-      const bool kfull = k0 + BK <= p.K;
-#pragma unroll
-      for (int i = 0; i < Cfg::A_PER_THREAD; ++i) {
-        const int r = a_row + i * Cfg::A_ROW_STEP;  // staged row
-        int bytes;
-        if (TRANS_A) {
-          bytes = (kfull || k0 + r < p.K) ? a_bytes : 0;
-        } else {
-          const long gk = k0 + a_col;
-          bytes = (m0 + r < p.M) ? (kfull ? 16 : (gk < p.K ? int(lmin(2, p.K - gk)) * 8 : 0)) : 0;
-        }
-        cp_async16(sA + r * Cfg::SA_LD + a_col, bytes ? a_src + i * a_rstep : p.A, bytes);
-      }
-#pragma unroll
-      for (int i = 0; i < Cfg::B_PER_THREAD; ++i) {
-        const int r = b_row + i * Cfg::B_ROW_STEP;
-        const int bytes = (kfull || k0 + r < p.K) ? b_bytes : 0;
-        cp_async16(sB + r * Cfg::SB_LD + b_col, bytes ? b_src + i * b_rstep : p.B, bytes);
-      }
-      a_src += a_kstep;
-      b_src += b_kstep;
-    };
-    // Non-finite scan of the A chunks this thread staged (own cp.async data is
-    // visible to the issuing thread after wait_group).
-    auto scan_stage = [&](int stage) {
-      const double* sA = smem + stage * Cfg::STAGE_ELEMS;
-#pragma unroll
-      for (int i = 0; i < Cfg::A_PER_THREAD; ++i) {
-        const int r = a_row + i * Cfg::A_ROW_STEP;
-        const double2 v = *reinterpret_cast<const double2*>(sA + r * Cfg::SA_LD + a_col);
-        saw_nonfinite |= nonfinite_bits(v.x) | nonfinite_bits(v.y);
-      }
-    };
-    auto load_frags = [&](const double* sA, const double* sB, int kk, double (&a)[MT], double (&b)[NT]) {
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        if (TRANS_A)
-          a[mt] = sA[(kk * 4 + t) * Cfg::SA_LD + wm0 + mt * 8 + g];
-        else
-          a[mt] = sA[(wm0 + mt * 8 + g) * Cfg::SA_LD + kk * 4 + t];
-      }
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[nt] = sB[(kk * 4 + t) * Cfg::SB_LD + wn0 + nt * 8 + g];
-    };
-
-    // ---- prologue ------------------------------------------------------
-    const int nk = ke - kb;
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-      if (s < nk) load_stage(s, kb + s);
-      cp_async_commit();
-    }
-
-    // ---- main loop -----------------------------------------------------
-    for (int i = 0; i < nk; ++i) {
-      cp_async_wait<STAGES - 2>();
-      __syncthreads();
-      const int stage = i % STAGES;
-      if (CHECK && check) scan_stage(stage);
-      {
-        const int nxt = i + STAGES - 1;
-        if (nxt < nk) load_stage(nxt % STAGES, kb + nxt);
-        cp_async_commit();
-      }
-      const double* sA = smem + stage * Cfg::STAGE_ELEMS;
-      const double* sB = sA + Cfg::SA_ELEMS;
-      double fa[2][MT], fb[2][NT];
-      load_frags(sA, sB, 0, fa[0], fb[0]);
-#pragma unroll
-      for (int kk = 0; kk < KSTEPS; ++kk) {
-        const int cur = kk & 1;
-        if (kk + 1 < KSTEPS) load_frags(sA, sB, kk + 1, fa[cur ^ 1], fb[cur ^ 1]);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], fa[cur][mt], fb[cur][nt]);
-      }
-    }
-    cp_async_wait<0>();
-    __syncthreads();  // ring buffer is reused by the next tile
-
-    if (SPLIT) {
-      // partial tile of this (tile, k-slice) unit, plain row-major layout
-      double* slot = p.partials + size_t(unit) * (BM * BN);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          __stcg(reinterpret_cast<double2*>(slot + (wm0 + mt * 8 + g) * BN + wn0 + nt * 8 + 2 * t),
-                 make_double2(acc[mt][nt][0], acc[mt][nt][1]));
-      unit += G;
-      continue;
-    }
-    // ---- stream-K fix-up + epilogue ------------------------------------
-    const bool full = (kb == 0 && ke == tile_k);
-    if (!full && kb != 0) {
-      // contributor: publish the partial tile in fragment-native layout
-      double* slot = p.partials + size_t(blockIdx.x) * (BM * BN);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            __stcg(slot + size_t(((warp * MT + mt) * NT + nt) * 2 + e) * 32 + lane, acc[mt][nt][e]);
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) st_release(p.flags + blockIdx.x, 1);
-    } else {
-      if (!full) {
-        // owner of the k=0 block: add later CTAs' partials in k order
-        const long tile_end = tile_it0 + tile_k;
-        for (int c = blockIdx.x + 1; c < G; ++c) {
-          if (tid == 0) {
-            while (ld_acquire(p.flags + c) == 0) {
-            }
-          }
-          __syncthreads();
-          const double* slot = p.partials + size_t(c) * (BM * BN);
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-              for (int e = 0; e < 2; ++e)
-                acc[mt][nt][e] += __ldcg(slot + size_t(((warp * MT + mt) * NT + nt) * 2 + e) * 32 + lane);
-          if (long(c + 1) * p.total_iters / G >= tile_end) break;
-        }
-      }
-      // epilogue: C = alpha·acc + beta·C
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const long r = m0 + wm0 + mt * 8 + g;
-        if (r >= p.M) continue;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const long cidx = n0 + wn0 + nt * 8 + 2 * t;
-          double* dst = p.C + r * p.ldc + cidx;
-          double v0 = p.alpha * acc[mt][nt][0], v1 = p.alpha * acc[mt][nt][1];
-          if (cidx + 1 < p.N) {
-            if (p.beta != 0.0) {
-              const double2 o = *reinterpret_cast<const double2*>(dst);
-              v0 += p.beta * o.x;
-              v1 += p.beta * o.y;
-            }
-            *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-          } else if (cidx < p.N) {
-            if (p.beta != 0.0) v0 += p.beta * dst[0];
-            dst[0] = v0;
-          }
-        }
-      }
-    }
-    it += nk;
-  }
-  if (CHECK && saw_nonfinite) atomicOr(p.nonfinite, 1);
-}
-
 // ---------------------------------------------------------------------------
-// Same contract and schedule as gemm_f64_streamk, with the k-block ring
-// synchronised by mbarriers instead of a CTA barrier per k-block:
+// The kernel.  The k-block ring is synchronised by mbarriers instead of a CTA
+// barrier per k-block (the first version's scheme, 14.5 → 13.8 ms per config-3
+// step when replaced):
 //   full[s]  — expected THREADS arrivals; each thread arrives through
 //              cp.async.mbarrier.arrive.noinc once its copies for the stage
 //              have landed;

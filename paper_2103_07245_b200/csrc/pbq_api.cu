@@ -124,33 +124,18 @@ struct Carve {
 //            idle with 8 warps of 64×32 (33.2 → 35.0 TFLOP/s at config 3).
 //            A streams ⌈N/128⌉ times; a 64×256 tile that reads A once
 //            measured 6% slower (BK 16), and DRAM is at ~20% of bandwidth.
-#ifndef PBQ_GEMM_WARPS16
-#define PBQ_GEMM_WARPS16 1  // 128×128 tile with 16 warps of 32×32 (4 per scheduler) instead of 8 of 64×32
-#endif
-#if PBQ_GEMM_WARPS16
+// 128×128 tile: 16 warps of 32×32 (4 per scheduler); 128×64 tile (d ≤ 64):
+// 16 warps of 32×16 (31.7 → 33.2 TFLOP/s at d = 64 over 8 warps of 64×32)
 constexpr int GEMM_WM = 32;
-constexpr int GEMM_WN64 = 16;  // 128×64 tile: 16 warps of 32×16 (31.7 → 33.2 TFLOP/s at d = 64)
-#else
-constexpr int GEMM_WM = 64;
-constexpr int GEMM_WN64 = 32;
-#endif
-#ifndef PBQ_GEMM_RING
-#define PBQ_GEMM_RING 1  // mbarrier k-block ring (gemm_f64_ring) instead of a CTA barrier per k-block
-#endif
+constexpr int GEMM_WN64 = 16;
 template <bool T, int BM, int BN, int BK, int WM, int WN, int ST>
 struct GemmKernel {
   using Cfg = GemmCfg<T, BM, BN, BK, WM, WN, ST>;
   static void* fn(bool check) {
-    if (PBQ_GEMM_RING)
-      return check ? reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, true>)
-                   : reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, false>);
-    return check ? reinterpret_cast<void*>(&gemm_f64_streamk<T, BM, BN, BK, WM, WN, ST, true>)
-                 : reinterpret_cast<void*>(&gemm_f64_streamk<T, BM, BN, BK, WM, WN, ST, false>);
+    return check ? reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, true>)
+                 : reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, false>);
   }
-  static void* split_fn() {
-    if (PBQ_GEMM_RING) return reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, false, true>);
-    return reinterpret_cast<void*>(&gemm_f64_streamk<T, BM, BN, BK, WM, WN, ST, false, true>);
-  }
+  static void* split_fn() { return reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, false, true>); }
 };
 
 struct GemmPlan {
@@ -569,6 +554,9 @@ int cqd_stage(pbq_ctx* ctx, int stage, long m, long n, double* A, long lda, doub
   int* ctl = cv.take<int>(64);  // [1] [2] grid-barrier counters, [4] emax of pass 2
   double* X1 = cv.take<double>(sq);
   double* X2 = cv.take<double>(sq);
+  // the factor kernel writes only the upper triangle of R⁻¹ and the products
+  // read the whole np×np block: ctl, X1 and X2 start zeroed (as in cq_launch)
+  const size_t zero_bytes = size_t(reinterpret_cast<char*>(X2 + sq) - reinterpret_cast<char*>(ctl));
   double* R1 = cv.take<double>(sq);
   double* R2 = cv.take<double>(sq);
   double* T = cv.take<double>(sq);
@@ -591,7 +579,7 @@ int cqd_stage(pbq_ctx* ctx, int stage, long m, long n, double* A, long lda, doub
   f.phase_ns = ctx->qr_phase_ns;
   f.allow_series = ctx->qr_method != PBQ_QR_CHOLQR_NOSERIES;
   if (stage == 0) {
-    PBQ_CUDA(ctx, cudaMemsetAsync(ctl, 0, 64 * sizeof(int), st));
+    PBQ_CUDA(ctx, cudaMemsetAsync(ctl, 0, zero_bytes, st));
     PBQ_CUDA(ctx, cudaMemsetAsync(fallback, 0, sizeof(int32_t), st));
     PBQ_TRY(gram_launch(ctx, pl, m, n, A, lda, part, nullptr, st));
     PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, nullptr, nullptr, st));

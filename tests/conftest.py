@@ -49,3 +49,19 @@ def qr_method(request, cuda):
     ctx.set_qr_method(ctx.QR_AUTO if request.param == "auto" else ctx.QR_HOUSEHOLDER)
     yield request.param
     ctx.set_qr_method(ctx.QR_AUTO)
+
+
+@pytest.fixture(autouse=True)
+def _dirty_device_memory(request):
+    """Every GPU test starts with NaN-filled memory in torch's caching
+    allocator, so a workspace the library forgets to initialise is caught
+    (freshly mapped device memory is zero and would hide it)."""
+    if request.node.get_closest_marker("gpu") is None:
+        yield
+        return
+    import torch
+
+    if torch.cuda.is_available():
+        junk = torch.full((64 << 20,), float("nan"), dtype=torch.float64, device="cuda:0")  # 512 MB
+        del junk
+    yield

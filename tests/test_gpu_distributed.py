@@ -42,6 +42,8 @@ def _worker(rank, world, port, a, d, q, seed, reorth, outdir, chunks, dist_qr):
     os.environ["MASTER_PORT"] = str(port)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
+    junk = torch.full((32 << 20,), float("nan"), dtype=torch.float64, device=dev)  # dirty cached memory
+    del junk
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         n1, n2 = a.shape

@@ -50,6 +50,11 @@ struct GemmArgs {
   // needs k < (tn+1)·BN — the stream-K space then has row_iters =
   // Σ_tn k-blocks(tn) iterations per row of tiles (total_iters = tiles_m·row_iters)
   int tri_b, row_iters;
+  // group > 1 (plain stream-K only): CTAs c = g·group + r form a group that
+  // walks the same (row tile, k-block) range, CTA r taking column tile
+  // tnp·group + r, so the group streams each A block from HBM once and its
+  // other members hit L2 (total_iters counts group iterations)
+  int group;
   // RESID epilogue (‖A − op(A)·B‖_F of the reconstruction): instead of storing
   // C, each finished tile subtracts from ref[r·ldref + c] and accumulates the
   // squared residual and squared ref; per-CTA sums go to sums[2·cta + {0,1}]
@@ -123,6 +128,8 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
   const int wm0 = (warp / Cfg::WARPS_N) * WM;
   const int wn0 = (warp % Cfg::WARPS_N) * WN;
   const int G = gridDim.x;
+  const int GS = (SPLIT || p.group < 1) ? 1 : p.group;  // group size
+  const int NG = G / GS, gi = blockIdx.x / GS, gr = blockIdx.x % GS;
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
@@ -151,8 +158,8 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
   };
   auto first_cursor = [&]() {
     Cursor c;
-    c.it = long(blockIdx.x) * p.total_iters / G;
-    c.it_end = long(blockIdx.x + 1) * p.total_iters / G;
+    c.it = long(gi) * p.total_iters / NG;
+    c.it_end = long(gi + 1) * p.total_iters / NG;
     c.unit = blockIdx.x;
     return c;
   };
@@ -191,10 +198,11 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
       s.kb = rem;
       s.tile = s.tm * p.tiles_n + s.tn;
     } else {
-      s.tile = int(c.it / p.k_iters);
+      const int tg = int(c.it / p.k_iters), tpg = p.tiles_n / GS;
       s.kb = int(c.it % p.k_iters);
-      s.tm = s.tile / p.tiles_n;
-      s.tn = s.tile % p.tiles_n;
+      s.tm = tg / tpg;
+      s.tn = (tg % tpg) * GS + gr;
+      s.tile = s.tm * p.tiles_n + s.tn;
     }
     s.tile_it0 = c.it - s.kb;
     s.ke = int(lmin(s.tile_k, s.kb + (c.it_end - c.it)));
@@ -352,7 +360,8 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
     }
     if (!full) {
       const long tile_end = seg.tile_it0 + seg.tile_k;
-      for (int c = blockIdx.x + 1; c < G; ++c) {
+      for (int cg = gi + 1; cg < NG; ++cg) {
+        const int c = cg * GS + gr;
         if (tid == 0) {
           while (ld_acquire(p.flags + c) == 0) {
           }
@@ -366,7 +375,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
 #pragma unroll
             for (int e = 0; e < 2; ++e)
               acc[mt][nt][e] += __ldcg(slot + size_t(((warp * MT + mt) * NT + nt) * 2 + e) * 32 + lane);
-        if (long(c + 1) * p.total_iters / G >= tile_end) break;
+        if (long(cg + 1) * p.total_iters / NG >= tile_end) break;
       }
     }
     if (RESID) {

@@ -122,8 +122,10 @@ struct Carve {
 //   N > 64 : 128×128, BK 32, 16 warps of 32×32, 3 stages.  Four warps per
 //            scheduler hide the fragment-load latency that left the DMMA pipe
 //            idle with 8 warps of 64×32 (33.2 → 35.0 TFLOP/s at config 3).
-//            A streams ⌈N/128⌉ times; a 64×256 tile that reads A once
-//            measured 6% slower (BK 16), and DRAM is at ~20% of bandwidth.
+//            A 64×256 tile that reads A once measured 6% slower (BK 16);
+//            instead the ⌈N/128⌉ column tiles of a row tile run side by side
+//            in a CTA group (GemmArgs::group) over the same k-blocks, so A
+//            leaves HBM once per pass (ncu: 3.87 → 1.91 GB per config-3 pass).
 // 128×128 tile: 16 warps of 32×32 (4 per scheduler); 128×64 tile (d ≤ 64):
 // 16 warps of 32×16 (31.7 → 33.2 TFLOP/s at d = 64 over 8 warps of 64×32)
 constexpr int GEMM_WM = 32;
@@ -140,6 +142,7 @@ struct GemmKernel {
 
 struct GemmPlan {
   int row_iters;
+  int group;
   int bm, bn;
   int tiles_m, tiles_n, k_iters;
   long total;
@@ -159,11 +162,23 @@ GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K, bool tri_b = fals
   p.k_iters = int(ceil_div(K, bk));
   p.total = long(p.tiles_m) * p.tiles_n * p.k_iters;
   p.row_iters = 0;
+  p.group = 1;
   if (tri_b) {
     for (int tn = 0; tn < p.tiles_n; ++tn) p.row_iters += int(std::min<long>(p.k_iters, long(tn + 1) * p.bn / bk));
     p.total = long(p.tiles_m) * p.row_iters;
+  } else {
+    // column tiles of one row tile run side by side in a CTA group (A read
+    // once from HBM): the largest group in {4, 2} dividing both tiles_n and
+    // the SM count, when every group still gets at least one k-block
+    for (int gsz = 4; gsz >= 2; gsz /= 2) {
+      if (p.tiles_n % gsz == 0 && ctx->sms % gsz == 0 && p.total / gsz >= ctx->sms / gsz) {
+        p.group = gsz;
+        break;
+      }
+    }
+    p.total /= p.group;
   }
-  p.grid = int(std::min<long>(ctx->sms, p.total));
+  p.grid = int(std::min<long>(ctx->sms / p.group, p.total)) * p.group;
   return p;
 }
 
@@ -194,6 +209,7 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   a.split = 0; a.sym = 0; a.units = 0;
   a.skip = skip;
   a.tri_b = tri_b; a.row_iters = pl.row_iters;
+  a.group = pl.group;
   a.run_if = run_if;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gemm: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
@@ -929,6 +945,7 @@ int resid_launch(pbq_ctx* ctx, long n1, long n2, long k, const double* A, long l
   a.A = ql; a.lda = ldk; a.B = pt; a.ldb = ldn;
   a.alpha = 1.0;
   a.tiles_m = pl.tiles_m; a.tiles_n = pl.tiles_n; a.k_iters = pl.k_iters; a.total_iters = pl.total;
+  a.group = pl.group;
   Carve gc(gws, gws_bytes);
   a.partials = gc.take<double>(size_t(pl.grid) * pl.bm * pl.bn);
   a.flags = gc.take<int>(pl.grid);

@@ -1,0 +1,19 @@
+#!/usr/bin/env bash
+# One GPU session's captures for tools/summarize_profiles.py <tag>.
+# Run on the box:  gpurun -- 'bash tools/profile_round.sh <tag>'
+# Every ncu command runs only after the same command exited 0 without ncu.
+set -u
+TAG=${1:?tag}
+O=gpurun_out
+mkdir -p $O
+NCU="ncu --clock-control none"
+python bench.py --no-e2e --no-cpu-baseline > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err || exit 1
+python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1 || exit 1
+$NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $O/${TAG}_launches.csv \
+  python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/${TAG}_ncu_launches.log 2>&1
+python tools/gemm_probe.py > $O/${TAG}_gemm_probe.txt 2>&1 || exit 1
+$NCU --set full --import-source on -k regex:gemm_f64_ring --launch-skip 1 -c 1 -f -o $O/${TAG}_gemm_tn \
+  python tools/gemm_probe.py > $O/${TAG}_ncu_gemm_tn.log 2>&1
+$NCU --set full --import-source on -k regex:gemm_f64_ring --launch-skip 7 -c 1 -f -o $O/${TAG}_gemm_nn \
+  python tools/gemm_probe.py > $O/${TAG}_ncu_gemm_nn.log 2>&1
+echo done

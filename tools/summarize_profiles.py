@@ -129,8 +129,9 @@ def gemm(tag):
     avg = (traffic["TN"] + traffic["NN"]) / 2
     alg = 8.0 * (20000 * 10000 + 20000 * 256 + 10000 * 256)
     md += ["", f"DRAM traffic per launch: TN {traffic['TN'] / 1e9:.2f} GB, NN {traffic['NN'] / 1e9:.2f} GB "
-           f"(average {avg / 1e9:.2f} GB) vs {alg / 1e9:.2f} GB algorithmic: A streams once per 128-wide output "
-           "column tile (2× at d = 256); compute-bound, so the re-read costs power, not time."]
+           f"(average {avg / 1e9:.2f} GB) vs {alg / 1e9:.2f} GB algorithmic (A once + the thin operands once). "
+           "The column tiles of one row tile run side by side in a CTA group of the stream-K schedule, so A "
+           "leaves HBM about once per pass; the rest is thin-operand re-reads that miss L2."]
     open(os.path.join(PROF, f"{tag}_gemm_ncu.md"), "w").write("\n".join(md) + "\n")
     json.dump({"kernel": "gemm_f64_ring (config-3 A-passes)", "source": f"profiles/{tag}_gemm_ncu.md (ncu --set full)",
                "dram_bytes_per_launch": traffic, "dram_bytes_per_launch_avg": avg,

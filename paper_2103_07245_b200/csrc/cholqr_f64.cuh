@@ -38,76 +38,6 @@ constexpr size_t CQ_SMEM_BYTES = size_t(CQ_SMEM_BLOCKS) * CQ_BLK * sizeof(double
 // O(‖E‖³) ≤ 1e-15
 constexpr double CQ_SERIES_EMAX = 1e-5;
 
-// G (np×np, ld np) = Σ_s partials[tile·S + s]  (fixed order), upper tiles of
-// the Gram GEMM; rows/cols in [n, np) become the identity padding.  A CTA
-// owns 32 consecutive tile elements; warp w sums slices s ≡ w (mod 8) and
-// the 8 warp sums are combined in warp order (deterministic for fixed S).
-// When `emax` is given, max|G − I| is folded into it (atomicMax on the bits
-// of a non-negative double; order-independent).
-__global__ void __launch_bounds__(256) cholqr_gram_reduce(const double* __restrict__ part, int S, int ntiles,
-                                                          int tiles_n, int sym, int bm, int bn, long n, long np,
-                                                          double* __restrict__ G, const int* skip,
-                                                          unsigned long long* emax, const int* run_if,
-                                                          double* __restrict__ Gcopy) {
-  if (skip && __ldcg(skip) != 0) return;
-  if (run_if && __ldcg(run_if) == 0) return;
-  __shared__ double s_part[8][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long tile_elems = long(bm) * bn;
-  const long total = long(ntiles) * tile_elems;
-  double dev = 0.0;
-  for (long base = long(blockIdx.x) * 32; base < total; base += long(gridDim.x) * 32) {
-    const long idx = base + lane;
-    const int tsel = int(idx / tile_elems);
-    const long e = idx % tile_elems;
-    double acc = 0.0;
-    if (idx < total) {
-      const double* src = part + size_t(tsel) * S * tile_elems + e;
-      for (int s0 = warp; s0 < S; s0 += 64) {  // 8 independent loads in flight per thread
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = (s0 + 8 * q < S) ? __ldcg(src + size_t(s0 + 8 * q) * tile_elems) : 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc += v[q];
-      }
-    }
-    s_part[warp][lane] = acc;
-    __syncthreads();
-    if (warp == 0 && idx < total) {
-      double g = s_part[0][lane];
-#pragma unroll
-      for (int w = 1; w < 8; ++w) g += s_part[w][lane];
-      int tm, tn;
-      if (sym) {
-        upper_tile(tsel, tiles_n, tm, tn);
-      } else {
-        tm = tsel / tiles_n;
-        tn = tsel % tiles_n;
-      }
-      const long r = long(tm) * bm + e / bn, c = long(tn) * bn + e % bn;
-      if (r < np && c < np) {
-        if (r >= n || c >= n) g = (r == c) ? 1.0 : 0.0;
-        G[r * np + c] = g;
-        if (Gcopy) Gcopy[r * np + c] = g;
-        const double d = fabs(g - (r == c ? 1.0 : 0.0));
-        dev = (d <= dev) ? dev : d;  // NaN sticks
-      }
-    }
-    __syncthreads();
-  }
-  if (emax && warp == 0) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double x = __shfl_xor_sync(0xffffffffu, dev, o);
-      dev = (x <= dev) ? dev : x;
-    }
-    if (lane == 0 && dev != 0.0) {
-      const unsigned long long bits = (dev == dev) ? __double_as_longlong(dev) : 0x7ff0000000000000ull;
-      atomicMax(emax, bits);
-    }
-  }
-}
-
 // Distributed Cholesky-QR2: after the caller's allreduce(sum) of the local
 // Gram matrices, restore the identity padding (rows/cols in [n, np) summed
 // to G·I over G ranks) and, for pass 2, fold max|G − I| of the GLOBAL Gram

@@ -61,6 +61,15 @@ struct GemmArgs {
   const double* ref;
   long ldref;
   double* sums;
+  // SPLIT with red_counter (zeroed, cooperative launch): the slice sum runs in
+  // the same launch after a grid barrier — G (np×np, ld np) = Σ_s partials in
+  // slice order, rows/cols in [n, np) the identity padding, optional copy and
+  // max|G − I| (bits, atomicMax) for the pass-2 series test
+  unsigned int* red_counter;
+  double* red_G;
+  double* red_Gcopy;
+  unsigned long long* red_emax;
+  long red_n, red_np;
 };
 
 
@@ -428,6 +437,55 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
     }
   }
   if (CHECK && saw_nonfinite) atomicOr(p.nonfinite, 1);
+  if (SPLIT && p.red_counter) {
+    // ---- fused slice sum (one thread per Gram element, slices in order) ---
+    unsigned int gen = 0;
+    grid_barrier(p.red_counter, gen);
+    constexpr long TILE = long(BM) * BN;
+    const long total = long(p.units / p.split) * TILE;
+    const long per = (total + G - 1) / G;
+    const long e0 = long(blockIdx.x) * per, e1 = lmin(total, e0 + per);
+    double dev = 0.0;
+    for (long idx = e0 + tid; idx < e1; idx += THREADS) {
+      const int tsel = int(idx / TILE);
+      const long e = idx % TILE;
+      const double* src = p.partials + size_t(tsel) * p.split * TILE + e;
+      double acc = 0.0;
+      for (int s0 = 0; s0 < p.split; s0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = (s0 + q < p.split) ? __ldcg(src + size_t(s0 + q) * TILE) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += v[q];
+      }
+      int tm, tn;
+      if (p.sym) {
+        upper_tile(tsel, p.tiles_n, tm, tn);
+      } else {
+        tm = tsel / p.tiles_n;
+        tn = tsel % p.tiles_n;
+      }
+      const long r = long(tm) * BM + e / BN, c = long(tn) * BN + e % BN;
+      if (r < p.red_np && c < p.red_np) {
+        if (r >= p.red_n || c >= p.red_n) acc = (r == c) ? 1.0 : 0.0;
+        p.red_G[r * p.red_np + c] = acc;
+        if (p.red_Gcopy) p.red_Gcopy[r * p.red_np + c] = acc;
+        const double d = fabs(acc - (r == c ? 1.0 : 0.0));
+        dev = (d <= dev) ? dev : d;  // NaN sticks
+      }
+    }
+    if (p.red_emax) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double x = __shfl_xor_sync(0xffffffffu, dev, o);
+        dev = (x <= dev) ? dev : x;
+      }
+      if (lane == 0 && dev != 0.0) {
+        const unsigned long long bits = (dev == dev) ? __double_as_longlong(dev) : 0x7ff0000000000000ull;
+        atomicMax(p.red_emax, bits);
+      }
+    }
+  }
   if (RESID) {
     // fixed-order CTA reduction → sums[2·cta + {0,1}]
     __shared__ double s_red[2][THREADS / 32];

@@ -364,8 +364,13 @@ size_t cq_ws_bytes(const CqPlan& p, const QrPlan& hp, long m, long n) {
          (ext ? 2 * sq + thin : 0) + qr_ws_bytes(hp, n) + 1024;
 }
 
+// Gram matrix G = XᵀX (upper tiles, split-K partials).  With `counter` (a
+// zeroed int of the caller's control block) the slice sum runs in the same
+// cooperative launch and writes G, its copy and max|G − I| (one launch
+// instead of Gram + a separate slice-sum kernel); without it only the partials.
 int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X, long ldx, double* part,
-                const int* skip, cudaStream_t st, const int* run_if = nullptr) {
+                const int* skip, cudaStream_t st, const int* run_if = nullptr, int* counter = nullptr,
+                double* G = nullptr, unsigned long long* emax = nullptr, double* gcopy = nullptr) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.M = n; a.N = n; a.K = m;
@@ -376,6 +381,8 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
   a.split = pl.S; a.sym = pl.ntiles > 1; a.units = pl.units;
   a.skip = skip;
   a.run_if = run_if;
+  a.red_counter = reinterpret_cast<unsigned int*>(counter);
+  a.red_G = G; a.red_Gcopy = gcopy; a.red_emax = emax; a.red_n = n; a.red_np = pl.np;
   void* fn;
   size_t smem;
   int threads;
@@ -390,21 +397,11 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
   }
   PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   void* args[] = {&a};
-  PBQ_CUDA(ctx, cudaLaunchKernel(fn, dim3(std::min(pl.units, ctx->sms)), dim3(threads), args, smem, st));
-  ctx->launches += 1;
-  const long total = long(pl.ntiles) * pl.bm * pl.bn;
-  (void)total;
-  return PBQ_OK;
-}
-
-int gram_reduce_launch(pbq_ctx* ctx, const CqPlan& pl, long n, const double* part, double* G, const int* skip,
-                       unsigned long long* emax, cudaStream_t st, const int* run_if = nullptr,
-                       double* gcopy = nullptr) {
-  const long total = long(pl.ntiles) * pl.bm * pl.bn;
-  const int grid = int(std::min<long>(ceil_div(total, 32), 8L * ctx->sms));
-  cholqr_gram_reduce<<<grid, 256, 0, st>>>(part, pl.S, pl.ntiles, pl.tiles_n, pl.ntiles > 1, pl.bm, pl.bn, n, pl.np,
-                                            G, skip, emax, run_if, gcopy);
-  PBQ_CUDA(ctx, cudaGetLastError());
+  const dim3 grid(std::min(pl.units, ctx->sms));
+  if (counter)
+    PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(fn, grid, dim3(threads), args, smem, st));
+  else
+    PBQ_CUDA(ctx, cudaLaunchKernel(fn, grid, dim3(threads), args, smem, st));
   ctx->launches += 1;
   return PBQ_OK;
 }
@@ -485,14 +482,12 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
     f.hh_req = hh_req;
   }
   // ---- Cholesky-QR2
-  PBQ_TRY(gram_launch(ctx, pl, m, n, A, lda, part, fallback, st));
-  PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, nullptr, st, nullptr, Gc));
+  PBQ_TRY(gram_launch(ctx, pl, m, n, A, lda, part, fallback, st, nullptr, ctl + 32, G, nullptr, Gc));
   f.pass = 1; f.R = R1; f.X = X1; f.counter = counter(1);
   PBQ_TRY(factor_launch(ctx, pl, f, st));
   PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
                              fallback, true));
-  PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st));
-  PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, emax_slot(4), st));
+  PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st, nullptr, ctl + 33, G, emax_slot(4)));
   f.pass = 2; f.R = R2; f.X = X2; f.R1 = R1; f.Rout = R; f.ldr = ldr; f.rank_flag = rank_flag;
   f.counter = counter(2);
   f.shift_req = nullptr;
@@ -515,9 +510,8 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
     PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
                                nullptr, true, route));
     CQ_DEBUG_SYNC("route 2");
-    PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, nullptr, st, route));
+    PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, nullptr, st, route, ctl + 34, G, emax_slot(20)));
     CQ_DEBUG_SYNC("route 3");
-    PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, nullptr, emax_slot(20), st, route));
     CQ_DEBUG_SYNC("route 4");
     g.pass = 2; g.shift_mode = 0; g.G = G; g.R = R2; g.X = X2; g.R1 = R1; g.emax = emax_slot(20);
     g.Rout = Racc; g.ldr = pl.np; g.rout_full = 1; g.rank_flag = nullptr; g.stats = nullptr; g.counter = counter(17);
@@ -526,9 +520,8 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
     PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q1, pl.ldq1, X2, pl.np, 0.0, Q2, pl.ldq1, nullptr, gws, pl.gemm_ws,
                                st, nullptr, true, route));
     CQ_DEBUG_SYNC("route 6");
-    PBQ_TRY(gram_launch(ctx, pl, m, n, Q2, pl.ldq1, part, nullptr, st, route));
+    PBQ_TRY(gram_launch(ctx, pl, m, n, Q2, pl.ldq1, part, nullptr, st, route, ctl + 35, G, emax_slot(22)));
     CQ_DEBUG_SYNC("route 7");
-    PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, nullptr, emax_slot(22), st, route));
     CQ_DEBUG_SYNC("route 8");
     g.R = R1; g.X = X1; g.R1 = Racc; g.emax = emax_slot(22);   // R = R₃·(R₂·R₁)
     g.Rout = R; g.ldr = ldr; g.rout_full = 0; g.rank_flag = rank_flag; g.stats = ctx->cq_stats;
@@ -597,8 +590,7 @@ int cqd_stage(pbq_ctx* ctx, int stage, long m, long n, double* A, long lda, doub
   if (stage == 0) {
     PBQ_CUDA(ctx, cudaMemsetAsync(ctl, 0, zero_bytes, st));
     PBQ_CUDA(ctx, cudaMemsetAsync(fallback, 0, sizeof(int32_t), st));
-    PBQ_TRY(gram_launch(ctx, pl, m, n, A, lda, part, nullptr, st));
-    PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, nullptr, nullptr, st));
+    PBQ_TRY(gram_launch(ctx, pl, m, n, A, lda, part, nullptr, st, nullptr, ctl + 32, G));
     return PBQ_OK;
   }
   if (stage == 1) {
@@ -609,8 +601,7 @@ int cqd_stage(pbq_ctx* ctx, int stage, long m, long n, double* A, long lda, doub
     PBQ_TRY(factor_launch(ctx, pl, f, st));
     PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
                                fallback, true));
-    PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st));
-    PBQ_TRY(gram_reduce_launch(ctx, pl, n, part, G, fallback, nullptr, st));
+    PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st, nullptr, ctl + 33, G));
     return PBQ_OK;
   }
   if (stage == 2) {

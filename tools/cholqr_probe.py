@@ -83,7 +83,7 @@ ctx.cholqr_stats(None)
 if os.environ.get("CQ_PHASES"):
     import ctypes
     fb = torch.zeros(1, dtype=torch.int32, device=dev)
-    ph = torch.zeros(24, dtype=torch.int64, device=dev)
+    ph = torch.zeros(128, dtype=torch.int64, device=dev)
     bw = torch.zeros(1024, dtype=torch.int64, device=dev)
     ctx.lib.pbq_debug_qr_hooks(ctx.handle, ctypes.c_void_p(fb.data_ptr()), ctypes.c_void_p(ph.data_ptr()),
                                ctypes.c_void_p(bw.data_ptr()))
@@ -102,4 +102,9 @@ if os.environ.get("CQ_PHASES"):
         v = [t / 1e3 for t in ph.tolist()[:8]]
         print(f"{m}x{n} factor phases (us): pass1 " + ", ".join(f"{a}={b:.1f}" for a, b in zip(names, v[:4])) +
               " | pass2 " + ", ".join(f"{a}={b:.1f}" for a, b in zip(names, v[4:8])))
+        cl = [t / 1e3 for t in ph.tolist()[8:]]
+        if any(cl):
+            for c in range((n + 31) // 32):
+                print(f"   cluster CTA {c:2d}: " + ", ".join(
+                    f"{a}={b:.1f}" for a, b in zip(["A", "bar1", "B", "bar2", "C"], cl[5 * c:5 * c + 5])))
     ctx.lib.pbq_debug_qr_hooks(ctx.handle, None, None, None)

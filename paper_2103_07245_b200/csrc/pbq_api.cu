@@ -1,6 +1,7 @@
 // C-ABI implementation of libpbq (include/pbq.h): launch planning, workspace
 // carving and the single-device PbP-QLP pipeline (algorithms.py:209-260).
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -12,6 +13,7 @@
 #include "../../include/pbq.h"
 #include "common.cuh"
 #include "gemm_f64.cuh"
+#include "gemm_tma_f64.cuh"
 #include "cholqr_f64.cuh"
 #include "cpqr_f64.cuh"
 #include "qr_f64.cuh"
@@ -130,15 +132,122 @@ struct Carve {
 // 16 warps of 32×16 (31.7 → 33.2 TFLOP/s at d = 64 over 8 warps of 64×32)
 constexpr int GEMM_WM = 32;
 constexpr int GEMM_WN64 = 16;
-template <bool T, int BM, int BN, int BK, int WM, int WN, int ST>
-struct GemmKernel {
-  using Cfg = GemmCfg<T, BM, BN, BK, WM, WN, ST>;
-  static void* fn(bool check) {
-    return check ? reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, true>)
-                 : reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, false>);
+
+// ---- GEMM kernel selection -----------------------------------------------
+// The TMA-staged kernel (gemm_tma_f64.cuh) is the default; PBQ_GEMM_LOADER=cpasync
+// selects the cp.async ring kernel (gemm_f64.cuh) for A/B measurements, and it
+// is also the path when the driver's tensor-map encoder is unavailable.
+enum GemmMode { GEMM_PLAIN = 0, GEMM_SPLIT = 1, GEMM_RESID = 2 };
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+bool gemm_use_tma() {
+  static const bool cpasync = [] {
+    const char* e = getenv("PBQ_GEMM_LOADER");
+    return e && strcmp(e, "cpasync") == 0;
+  }();
+  return !cpasync && tensor_map_encoder() != nullptr;
+}
+
+// row-major matrix of `rows` rows × `cols` doubles, leading dimension ld → a
+// 2-D tensor map with boxes of 16 columns × box_rows rows, 128-byte swizzle
+bool encode_map(CUtensorMap* m, const double* base, long cols, long rows, long ld, int box_rows) {
+  const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * sizeof(double)};
+  const cuuint32_t box[2] = {16u, cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1u, 1u};
+  return tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the same matrix as a 3-D map {16, rows, cols/16} whose outer dimension
+// steps over column groups (byte stride 128): one copy of box {16, box_rows,
+// groups} lands group g at g·box_rows·128 bytes — the layout of the 2-D boxes.
+// Only when cols is a multiple of 16 (no group reaches past the row end).
+bool encode_map3(CUtensorMap* m, const double* base, long cols, long rows, long ld, int box_rows, int groups) {
+  if (cols % 16 != 0 || groups < 1) return false;
+  const cuuint64_t dims[3] = {16u, cuuint64_t(rows), cuuint64_t(cols / 16)};
+  const cuuint64_t strides[2] = {cuuint64_t(ld) * sizeof(double), 128u};
+  const cuuint32_t box[3] = {16u, cuuint32_t(box_rows), cuuint32_t(groups)};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  return tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool T, int BN, bool CHECK, int MODE>
+void* tma_fn() {
+  constexpr int WN = BN == 64 ? GEMM_WN64 : 32;
+  return reinterpret_cast<void*>(&gemm_f64_tma<T, 128, BN, GEMM_WM, WN, 3, CHECK, MODE == GEMM_SPLIT, MODE == GEMM_RESID>);
+}
+template <bool T, int BN, bool CHECK, int MODE>
+void* ring_fn() {
+  constexpr int WN = BN == 64 ? GEMM_WN64 : 32;
+  return reinterpret_cast<void*>(
+      &gemm_f64_ring<T, 128, BN, 32, GEMM_WM, WN, 3, CHECK, MODE == GEMM_SPLIT, MODE == GEMM_RESID>);
+}
+template <bool TMA, int BN>
+void* pick_fn(bool trans, bool check, int mode) {
+  if (mode == GEMM_SPLIT) return TMA ? tma_fn<true, BN, false, GEMM_SPLIT>() : ring_fn<true, BN, false, GEMM_SPLIT>();
+  if (mode == GEMM_RESID) return TMA ? tma_fn<false, BN, false, GEMM_RESID>() : ring_fn<false, BN, false, GEMM_RESID>();
+  if (trans)
+    return check ? (TMA ? tma_fn<true, BN, true, 0>() : ring_fn<true, BN, true, 0>())
+                 : (TMA ? tma_fn<true, BN, false, 0>() : ring_fn<true, BN, false, 0>());
+  return check ? (TMA ? tma_fn<false, BN, true, 0>() : ring_fn<false, BN, true, 0>())
+               : (TMA ? tma_fn<false, BN, false, 0>() : ring_fn<false, BN, false, 0>());
+}
+
+int gemm_dispatch(pbq_ctx* ctx, const GemmArgs& a, bool trans, int bn, int mode, dim3 grid, bool coop,
+                  cudaStream_t st) {
+  constexpr int threads = 512;  // 16 warps for both tile shapes
+  void* fn;
+  size_t smem;
+  GemmTmaArgs ta;
+  void* args[1];
+  if (gemm_use_tma()) {
+    memset(&ta, 0, sizeof(ta));
+    ta.g = a;
+    static const bool no3d = getenv("PBQ_TMA_NO3D") != nullptr;
+    ta.a3d = !no3d && (trans ? encode_map3(&ta.ta, a.A, a.M, a.K, a.lda, 32, 128 / 16)
+                             : encode_map3(&ta.ta, a.A, a.K, a.M, a.lda, 128, 32 / 16));
+    ta.b3d = !no3d && encode_map3(&ta.tb, a.B, a.N, a.K, a.ldb, 32, bn / 16);
+    const bool ok = (ta.a3d || (trans ? encode_map(&ta.ta, a.A, a.M, a.K, a.lda, 32)
+                                      : encode_map(&ta.ta, a.A, a.K, a.M, a.lda, 128))) &&
+                    (ta.b3d || encode_map(&ta.tb, a.B, a.N, a.K, a.ldb, 32));
+    if (!ok) return fail(ctx, PBQ_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
+    fn = bn == 64 ? pick_fn<true, 64>(trans, a.nonfinite != nullptr, mode)
+                  : pick_fn<true, 128>(trans, a.nonfinite != nullptr, mode);
+    smem = bn == 64 ? gemm_tma_smem_bytes<true, 128, 64, 3>() : gemm_tma_smem_bytes<true, 128, 128, 3>();
+    args[0] = &ta;
+  } else {
+    fn = bn == 64 ? pick_fn<false, 64>(trans, a.nonfinite != nullptr, mode)
+                  : pick_fn<false, 128>(trans, a.nonfinite != nullptr, mode);
+    smem = trans ? (bn == 64 ? GemmCfg<true, 128, 64, 32, 32, GEMM_WN64, 3>::SMEM_BYTES
+                             : GemmCfg<true, 128, 128, 32, GEMM_WM, 32, 3>::SMEM_BYTES)
+                 : (bn == 64 ? GemmCfg<false, 128, 64, 32, 32, GEMM_WN64, 3>::SMEM_BYTES
+                             : GemmCfg<false, 128, 128, 32, GEMM_WM, 32, 3>::SMEM_BYTES);
+    args[0] = const_cast<GemmArgs*>(&a);
   }
-  static void* split_fn() { return reinterpret_cast<void*>(&gemm_f64_ring<T, BM, BN, BK, WM, WN, ST, false, true>); }
-};
+  PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (coop)
+    PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(fn, grid, dim3(threads), args, smem, st));
+  else
+    PBQ_CUDA(ctx, cudaLaunchKernel(fn, grid, dim3(threads), args, smem, st));
+  ctx->launches += 1;
+  return PBQ_OK;
+}
 
 struct GemmPlan {
   int row_iters;
@@ -213,22 +322,8 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   a.run_if = run_if;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gemm: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
-  void* fn;
-  size_t smem;
-  int threads;
-  if (pl.bn == 64) {
-    using K_ = GemmKernel<TRANS, 128, 64, 32, 32, GEMM_WN64, 3>;
-    fn = K_::fn(nonfinite != nullptr); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
-  } else {
-    using K_ = GemmKernel<TRANS, 128, 128, 32, GEMM_WM, 32, 3>;
-    fn = K_::fn(nonfinite != nullptr); smem = K_::Cfg::SMEM_BYTES; threads = K_::Cfg::THREADS;
-  }
-  PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  void* args[] = {&a};
   ProfScope ps(ctx->prof, st, 0);
-  PBQ_CUDA(ctx, cudaLaunchKernel(fn, dim3(pl.grid), dim3(threads), args, smem, st));
-  ctx->launches += 1;
-  return PBQ_OK;
+  return gemm_dispatch(ctx, a, TRANS, pl.bn, GEMM_PLAIN, dim3(pl.grid), false, st);
 }
 
 // ------------------------------------------------------------------ QR ----
@@ -383,27 +478,7 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
   a.run_if = run_if;
   a.red_counter = reinterpret_cast<unsigned int*>(counter);
   a.red_G = G; a.red_Gcopy = gcopy; a.red_emax = emax; a.red_n = n; a.red_np = pl.np;
-  void* fn;
-  size_t smem;
-  int threads;
-  if (pl.bn == 64) {
-    using C_ = GemmCfg<true, 128, 64, 32, 32, GEMM_WN64, 3>;
-    fn = GemmKernel<true, 128, 64, 32, 32, GEMM_WN64, 3>::split_fn();
-    smem = C_::SMEM_BYTES; threads = C_::THREADS;
-  } else {
-    using C_ = GemmCfg<true, 128, 128, 32, GEMM_WM, 32, 3>;
-    fn = GemmKernel<true, 128, 128, 32, GEMM_WM, 32, 3>::split_fn();
-    smem = C_::SMEM_BYTES; threads = C_::THREADS;
-  }
-  PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  void* args[] = {&a};
-  const dim3 grid(std::min(pl.units, ctx->sms));
-  if (counter)
-    PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(fn, grid, dim3(threads), args, smem, st));
-  else
-    PBQ_CUDA(ctx, cudaLaunchKernel(fn, grid, dim3(threads), args, smem, st));
-  ctx->launches += 1;
-  return PBQ_OK;
+  return gemm_dispatch(ctx, a, true, pl.bn, GEMM_SPLIT, dim3(std::min(pl.units, ctx->sms)), counter != nullptr, st);
 }
 
 int factor_launch(pbq_ctx* ctx, const CqPlan& pl, CqArgs& a, cudaStream_t st) {
@@ -942,25 +1017,10 @@ int resid_launch(pbq_ctx* ctx, long n1, long n2, long k, const double* A, long l
   a.flags = gc.take<int>(pl.grid);
   a.ref = A; a.ldref = lda; a.sums = sums;
   PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
-  void* fn;
-  size_t smem;
-  int threads;
-  if (pl.bn == 64) {
-    using C_ = GemmCfg<false, 128, 64, 32, 32, GEMM_WN64, 3>;
-    fn = reinterpret_cast<void*>(&gemm_f64_ring<false, 128, 64, 32, 32, GEMM_WN64, 3, false, false, true>);
-    smem = C_::SMEM_BYTES; threads = C_::THREADS;
-  } else {
-    using C_ = GemmCfg<false, 128, 128, 32, GEMM_WM, 32, 3>;
-    fn = reinterpret_cast<void*>(&gemm_f64_ring<false, 128, 128, 32, GEMM_WM, 32, 3, false, false, true>);
-    smem = C_::SMEM_BYTES; threads = C_::THREADS;
-  }
-  PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  void* args[] = {&a};
   {
     ProfScope ps(ctx->prof, st, 0);
-    PBQ_CUDA(ctx, cudaLaunchKernel(fn, dim3(pl.grid), dim3(threads), args, smem, st));
+    PBQ_TRY(gemm_dispatch(ctx, a, false, pl.bn, GEMM_RESID, dim3(pl.grid), false, st));
   }
-  ctx->launches += 1;
   resid_final_kernel<<<1, 256, 0, st>>>(sums, pl.grid, out);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 1;

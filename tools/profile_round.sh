@@ -12,8 +12,8 @@ python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $O/${TAG}_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/${TAG}_ncu_launches.log 2>&1
 python tools/gemm_probe.py > $O/${TAG}_gemm_probe.txt 2>&1 || exit 1
-$NCU --set full --import-source on -k regex:gemm_f64_ring --launch-skip 1 -c 1 -f -o $O/${TAG}_gemm_tn \
+$NCU --set full --import-source on -k regex:gemm_f64 --launch-skip 1 -c 1 -f -o $O/${TAG}_gemm_tn \
   python tools/gemm_probe.py > $O/${TAG}_ncu_gemm_tn.log 2>&1
-$NCU --set full --import-source on -k regex:gemm_f64_ring --launch-skip 7 -c 1 -f -o $O/${TAG}_gemm_nn \
+$NCU --set full --import-source on -k regex:gemm_f64 --launch-skip 7 -c 1 -f -o $O/${TAG}_gemm_nn \
   python tools/gemm_probe.py > $O/${TAG}_ncu_gemm_nn.log 2>&1
 echo done

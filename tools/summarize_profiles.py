@@ -42,8 +42,11 @@ def launch_shares(tag):
     rows = [r for r in csv.DictReader(lines[i:]) if r["Metric Name"] == "gpu__time_duration.sum"]
 
     def cls(n):
-        if "gemm_f64_ring" in n:
-            return "gemm_split" if (", true>" in n or "Lb0ELb1E" in n or "0, 1, 0>" in n) else "gemm"
+        if "gemm_f64_ring" in n or "gemm_f64_tma" in n:
+            # template arguments: ring <T, BM, BN, BK, WM, WN, ST, CHECK, SPLIT, RESID>,
+            # tma <T, BM, BN, WM, WN, ST, CHECK, SPLIT, RESID>
+            args = [x.strip() for x in n[n.index("<") + 1:n.index(">")].split(",")]
+            return "gemm_split" if args[-2] in ("1", "true") else "gemm"
         for k in ("cholqr_factor_kernel", "cholqr_gram_reduce", "qr_tall_kernel", "sketch_k1", "sketch_k2",
                   "sketch_k3", "transpose_kernel", "merge_flag_kernel"):
             if k in n:
@@ -60,9 +63,9 @@ def launch_shares(tag):
         if name == "transpose_kernel":
             ntr += 1
         if name == "gemm" and us > 1000:
-            key = "GEMM A-passes (gemm_f64_ring)"
+            key = "GEMM A-passes (gemm_f64_tma)"
         elif name == "gemm" and ntr == 2:
-            key = "GEMM P = P̄·W (gemm_f64_ring)"
+            key = "GEMM P = P̄·W (gemm_f64_tma)"
         elif name in ("gemm", "gemm_split", "cholqr_gram_reduce", "cholqr_factor_kernel", "qr_tall_kernel"):
             key = "QR ×5 (Cholesky-QR2 chain; Householder early-exit)"
         elif name.startswith("sketch"):
@@ -111,8 +114,8 @@ GEMM_KEYS = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "D
 def gemm(tag):
     reps = {"TN": os.path.join(OUT, f"{tag}_gemm_tn.ncu-rep"), "NN": os.path.join(OUT, f"{tag}_gemm_nn.ncu-rep")}
     vals = {k: raw(v) for k, v in reps.items()}
-    md = [f"# {tag} ncu --set full: gemm_f64_ring on the config-3 A-passes", "",
-          "`ncu --set full --import-source on --clock-control none -k regex:gemm_f64_ring --launch-skip {1,7} -c 1 "
+    md = [f"# {tag} ncu --set full: the DMMA GEMM on the config-3 A-passes", "",
+          "`ncu --set full --import-source on --clock-control none -k regex:gemm_f64 --launch-skip {1,7} -c 1 "
           "python tools/gemm_probe.py` (TN = AᵀΦ 10000×256×20000, NN = A·P̄ 20000×256×10000), after the probe "
           "ran without ncu:", "", "```"] + open(os.path.join(OUT, f"{tag}_gemm_probe.txt")).read().strip().splitlines() + \
         ["```", "", "| metric | TN | NN |", "|---|---|---|"]
@@ -133,7 +136,7 @@ def gemm(tag):
            "The column tiles of one row tile run side by side in a CTA group of the stream-K schedule, so A "
            "leaves HBM about once per pass; the rest is thin-operand re-reads that miss L2."]
     open(os.path.join(PROF, f"{tag}_gemm_ncu.md"), "w").write("\n".join(md) + "\n")
-    json.dump({"kernel": "gemm_f64_ring (config-3 A-passes)", "source": f"profiles/{tag}_gemm_ncu.md (ncu --set full)",
+    json.dump({"kernel": "gemm_f64_tma (config-3 A-passes)", "source": f"profiles/{tag}_gemm_ncu.md (ncu --set full)",
                "dram_bytes_per_launch": traffic, "dram_bytes_per_launch_avg": avg,
                "algorithmic_bytes_per_launch": alg}, open(os.path.join(PROF, f"{tag}_gemm_traffic.json"), "w"), indent=1)
 

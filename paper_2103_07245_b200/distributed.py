@@ -15,10 +15,15 @@ of the global stream, so Φ does not depend on G).  Exchanges:
   (``pbq_cholqr2_dist``): local Gram A_gᵀA_g, allreduce(sum) of the d×d Gram,
   the guarded factorization replicated (same G → same R on every rank), the
   local product, and again for the second pass — two d×d allreduces and no
-  tall replicated work.  When its κ guard fires (one 4-byte flag read per
-  call) the shard is untouched and the TSQR tree runs instead: local QR
-  (Q_g, R_g), all-gather of the d×d R factors, a replicated QR of the stacked
-  (G·d)×d matrix → (Q̂, R), then Q_g ← Q_g·Q̂_g (local GEMM).
+  tall replicated work.  Its fallback is the TSQR tree: local QR (Q_g, R_g),
+  all-gather of the d×d R factors, a replicated QR of the stacked (G·d)×d
+  matrix → (Q̂, R), then Q_g ← Q_g·Q̂_g (local GEMM).
+* No host synchronisation inside ``run``: each distributed Cholesky-QR2 ORs
+  its κ-guard flag into a device flag (identical on every rank, since every
+  rank factors the same allreduced Gram).  ``finish`` reads it with the
+  status flags in its one device→host copy; when a guard fired, every rank
+  re-runs the factorization with the fallbacks (TSQR, replicated orth) in
+  every QR.  Well-conditioned inputs therefore never stall the stream.
 * qr(Rᵀ), L = tril(R̃ᵀ) and P = P̄·W are replicated.
 
 Q stays row-sharded (rank g holds Q[r_g : r_{g+1}]); L, P, R are replicated.
@@ -137,7 +142,10 @@ class DistributedPbpQlp:
         self.L = be.empty(self.d, self.d)
         self.P = be.empty(self.n2, self.d)
         self.Qtmp = be.empty(self.m, self.d)
-        self.flags = be.zeros_i32(2 * self.q + 3)  # [non-finite, sketch status, rank flags …]
+        # [non-finite, sketch status, rank flags …, Cholesky-QR2 guard fired]
+        self.flags = be.zeros_i32(2 * self.q + 4)
+        self.force_fallback = False  # set by finish() for the re-run after a guard fired
+        self._last = None
         self.PHI = None
         # qr(A·P̄): distributed Cholesky-QR2 (one d×d allreduce per pass) with
         # the TSQR tree as its fallback, or the TSQR tree alone
@@ -197,13 +205,21 @@ class DistributedPbpQlp:
         be.gemm_nn(self.Q, be.contiguous(qhat), self.Qtmp)
         self.Q.copy_(self.Qtmp)
 
+    def _note_guard(self, st):
+        """OR the call's guard flag into flags[-1] on the device (no sync)."""
+        fb = self.flags[-1:]
+        torch.maximum(fb, st["fallback"].to(fb.dtype), out=fb)
+
     def _qr_sharded_(self, flag=None):
         """QR of the row-sharded self.Q in place (R → self.R): distributed
         Cholesky-QR2 — local Gram, allreduce(sum) of the d×d Gram, replicated
-        factor, local product, twice — and the TSQR tree only when its κ guard
-        fires (one 4-byte flag read per call)."""
+        factor, local product, twice.  Its guard flag is noted on the device;
+        the TSQR tree runs in the re-run that ``finish`` starts when it fired."""
         st = self.cq_state
         if st is None:
+            return self._tsqr_(flag)
+        if self.force_fallback:
+            self.tsqr_fallbacks += 1
             return self._tsqr_(flag)
         be = self.be
         be.cholqr2_dist(0, self.Q, self.R, st, flag)
@@ -211,9 +227,7 @@ class DistributedPbpQlp:
         be.cholqr2_dist(1, self.Q, self.R, st, flag)
         dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
         be.cholqr2_dist(2, self.Q, self.R, st, flag)
-        if int(st["fallback"].item()):  # identical on every rank (same G)
-            self.tsqr_fallbacks += 1
-            self._tsqr_(flag)
+        self._note_guard(st)
 
     def _orth_c_(self, flag):
         """orth(C) in place, C replicated on every rank: each rank
@@ -223,6 +237,9 @@ class DistributedPbpQlp:
         st = self.c_state
         if st is None:
             return self.be.qr_(self.C, self.Rs, flag)
+        if self.force_fallback:
+            self.orth_fallbacks += 1
+            return self.be.qr_(self.C, self.Rs, flag)
         be = self.be
         s0 = self.rank * self.slice_rows
         mine = self.Cbuf[s0:s0 + self.slice_rows]
@@ -231,9 +248,7 @@ class DistributedPbpQlp:
         be.cholqr2_dist(1, mine, self.Rs, st, flag)
         dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
         be.cholqr2_dist(2, mine, self.Rs, st, flag)
-        if int(st["fallback"].item()):  # identical on every rank (same G); C untouched
-            self.orth_fallbacks += 1
-            return be.qr_(self.C, self.Rs, flag)
+        self._note_guard(st)  # a fired guard left the slices untouched; finish() re-runs
         buf = self.Cbuf
         ld = buf.stride(0)
         whole = buf.as_strided((buf.shape[0], ld), (ld, 1))  # whole rows incl. the even-ld pad column
@@ -250,6 +265,7 @@ class DistributedPbpQlp:
         """Enqueue one factorization of this rank's rows (kernel-ready operand)."""
         be = self.be
         d, q = self.d, self.q
+        self._last = (A_local, seed, phi_local)
         self.flags.zero_()
         flags = self.flags
         if phi_local is None:
@@ -284,11 +300,22 @@ class DistributedPbpQlp:
         """Synchronise, raise / warn like the reference (every rank)."""
         # a non-finite entry in any shard fails every rank
         dist.all_reduce(self.flags[0:2], op=dist.ReduceOp.MAX, group=self.group)
+        dist.all_reduce(self.flags[-1:], op=dist.ReduceOp.MAX, group=self.group)  # same on every rank anyway
         fl = self.flags.cpu().tolist()
         if fl[0]:
             raise _exc.MatrixInputError("a contains non-finite entries")
         if fl[1]:
             raise _exc.DeviceError("sketch generator overflow (internal error)")
+        if fl[-1] and not self.force_fallback:
+            # a Cholesky-QR2 guard fired (the same on every rank): redo the
+            # factorization with the fallback in every QR
+            self.force_fallback = True
+            try:
+                self.run(*self._last)
+                return self.finish(stacklevel=stacklevel + 1)
+            finally:
+                self.force_fallback = False
+        fl = fl[:-1]
         for f in fl[2:]:
             warn_rank(f, stacklevel=stacklevel + 1)
         return fl

@@ -190,6 +190,16 @@ int pbq_cholqr2_dist(pbq_ctx* ctx, int32_t stage, int64_t m, int64_t n, double* 
                      size_t workspace_bytes, void* stream);
 int pbq_cholqr2_dist_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes, int64_t* ldg);
 
+/* PbP-QLP's second stage (reference algorithms.py:256-257): from the d×d
+ * upper-triangular R of qr(D), (W, R̃) = householder_qr(Rᵀ) with diag R̃ ≥ 0
+ * and L = tril(R̃ᵀ).  W (d×d) and L (d×d, zeros above the diagonal) are
+ * row-major outputs; R is not modified.  Transpose, the pbq_householder_qr
+ * chain on the d×d matrix, transpose, in one call.  No rank test (the
+ * reference does not warn here). */
+int pbq_second_stage(pbq_ctx* ctx, int64_t d, const double* R, int64_t ldr, double* W, int64_t ldw, double* L,
+                     int64_t ldl, void* workspace, size_t workspace_bytes, void* stream);
+int pbq_second_stage_workspace_bytes(pbq_ctx* ctx, int64_t d, size_t* bytes);
+
 /* Small helpers used by the host driver.
  * dst[i][j] = src[j][i]            (n×n), or with lower=1 the lower triangle
  * of srcᵀ and zeros above (L = tril(R̃ᵀ), algorithms.py:257). */

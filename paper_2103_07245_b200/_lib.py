@@ -39,6 +39,8 @@ EXPORTED = (
     "pbq_pbp_qlp_workspace_bytes",
     "pbq_pbp_qlp",
     "pbq_transpose",
+    "pbq_second_stage",
+    "pbq_second_stage_workspace_bytes",
     "pbq_debug_qr_hooks",
     "pbq_profile_begin",
     "pbq_profile_end",
@@ -102,6 +104,8 @@ _SIGS = {
     "pbq_pbp_qlp_workspace_bytes": ([c_p, ctypes.POINTER(PbqProblem), ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_pbp_qlp": ([c_p, ctypes.POINTER(PbqProblem), ctypes.POINTER(PbqOutputs), c_p, c_sz, c_p], ctypes.c_int),
     "pbq_transpose": ([c_p, c_i64, c_p, c_i64, c_p, c_i64, c_i32, c_p], ctypes.c_int),
+    "pbq_second_stage": ([c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_sz, c_p], ctypes.c_int),
+    "pbq_second_stage_workspace_bytes": ([c_p, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_debug_qr_hooks": ([c_p, c_p, c_p, c_p], ctypes.c_int),
     "pbq_profile_begin": ([c_p, c_i32], ctypes.c_int),
     "pbq_profile_end": ([c_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)], ctypes.c_int),

@@ -1238,6 +1238,46 @@ int pbq_transpose(pbq_ctx* ctx, int64_t n, const double* src, int64_t lds, doubl
   return transpose_launch(ctx, n, src, lds, dst, ldd, lower, static_cast<cudaStream_t>(stream));
 }
 
+// ------------------------------------------------------- second stage --
+// (W, R̃) = qr(Rᵀ), L = tril(R̃ᵀ) (algorithms.py:256-257): transpose, the
+// tall-QR chain on the d×d matrix, transpose into L.  (A single-CTA
+// shared-memory Householder for d ≤ 160 measured slower than this chain at
+// every d — tools/microbench/small_qr_single_cta_kernel.cu.)
+static size_t second_stage_ws_bytes(pbq_ctx* ctx, long d) {
+  size_t q = 0;
+  pbq_qr_workspace_bytes(ctx, d, d, &q);
+  return 2 * align_up(size_t(d) * thin_ld(d) * sizeof(double), 256) + q + 512;
+}
+
+static int second_stage_launch(pbq_ctx* ctx, long d, const double* R, long ldr, double* W, long ldw, double* L,
+                               long ldl, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (d < 1) return fail(ctx, PBQ_ERR_DIM, "second stage: d must be >= 1");
+  if (ldr < d || ldw < d || ldl < d) return fail(ctx, PBQ_ERR_PARAM, "second stage: leading dimension too small");
+  if ((ldw & 1) || !aligned16(W)) return fail(ctx, PBQ_ERR_PARAM, "second stage: ldw must be even, W 16-byte aligned");
+  const long ld = thin_ld(d);
+  Carve cv(ws, ws_bytes);
+  double* rt = cv.take<double>(size_t(d) * ld);
+  size_t q = 0;
+  PBQ_TRY(pbq_qr_workspace_bytes(ctx, d, d, &q));
+  void* qws = cv.take<char>(q);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "second stage: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  PBQ_TRY(transpose_launch(ctx, d, R, ldr, W, ldw, 0, st));
+  PBQ_TRY(qr_launch(ctx, d, d, W, ldw, rt, ld, 1, nullptr, qws, q, st));
+  return transpose_launch(ctx, d, rt, ld, L, ldl, 1, st);
+}
+
+int pbq_second_stage_workspace_bytes(pbq_ctx* ctx, int64_t d, size_t* bytes) {
+  if (!ctx || !bytes) return PBQ_ERR_PARAM;
+  *bytes = second_stage_ws_bytes(ctx, d);
+  return PBQ_OK;
+}
+
+int pbq_second_stage(pbq_ctx* ctx, int64_t d, const double* R, int64_t ldr, double* W, int64_t ldw, double* L,
+                     int64_t ldl, void* ws, size_t ws_bytes, void* stream) {
+  if (!ctx || !R || !W || !L) return PBQ_ERR_PARAM;
+  return second_stage_launch(ctx, d, R, ldr, W, ldw, L, ldl, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
 // ------------------------------------------------------------- pipeline --
 static int pipeline_sizes(pbq_ctx* ctx, const pbq_problem* pr, size_t* total, size_t* scratch) {
   const long n1 = pr->n1, n2 = pr->n2, d = pr->d;
@@ -1247,12 +1287,12 @@ static int pipeline_sizes(pbq_ctx* ctx, const pbq_problem* pr, size_t* total, si
   PBQ_TRY(pbq_gemm_workspace_bytes(ctx, n2, d, d, &g3));
   PBQ_TRY(pbq_qr_workspace_bytes(ctx, n2, d, &q1));
   PBQ_TRY(pbq_qr_workspace_bytes(ctx, n1, d, &q2));
-  PBQ_TRY(pbq_qr_workspace_bytes(ctx, d, d, &q3));
+  q3 = second_stage_ws_bytes(ctx, d);
   if (!pr->phi && !pr->c_init) PBQ_TRY(pbq_gaussian_workspace_bytes(ctx, n1, d, 0, &s1));
   const size_t sc = std::max({g1, g2, g3, q1, q2, q3, s1});
   const long ld = thin_ld(d);
   *scratch = sc;
-  *total = align_up(size_t(n2) * ld * 8, 256) + 2 * align_up(size_t(d) * ld * 8, 256) + align_up(64, 256) + sc + 512;
+  *total = align_up(size_t(n2) * ld * 8, 256) + align_up(size_t(d) * ld * 8, 256) + align_up(64, 256) + sc + 512;
   return PBQ_OK;
 }
 
@@ -1280,8 +1320,7 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   const long ld = thin_ld(d);
   Carve cv(ws, ws_bytes);
   double* cbuf = cv.take<double>(size_t(n2) * ld);  // C, then P̄ (in place)
-  double* wbuf = cv.take<double>(size_t(d) * ld);   // Rᵀ → W
-  double* rt = cv.take<double>(size_t(d) * ld);     // R̃
+  double* wbuf = cv.take<double>(size_t(d) * ld);   // W of the second stage
   int32_t* sk_err = cv.take<int32_t>(16);
   void* sc = cv.take<char>(scratch);
   const int32_t check = pr->check_finite ? 1 : 0;
@@ -1327,9 +1366,7 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cbuf, ld, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
   PBQ_TRY(qr_launch(ctx, n1, d, dbuf, ldq, o->r, o->ldr, 1, nullptr, sc, scratch, st));
   // (W, R̃) = qr(Rᵀ); L = tril(R̃ᵀ); P = P̄·W
-  PBQ_TRY(transpose_launch(ctx, d, o->r, o->ldr, wbuf, ld, 0, st));
-  PBQ_TRY(qr_launch(ctx, d, d, wbuf, ld, rt, ld, 1, nullptr, sc, scratch, st));
-  PBQ_TRY(transpose_launch(ctx, d, rt, ld, o->l, o->ldl, 1, st));
+  PBQ_TRY(second_stage_launch(ctx, d, o->r, o->ldr, wbuf, ld, o->l, o->ldl, sc, scratch, st));
   PBQ_TRY(gemm_launch<false>(ctx, n2, d, d, 1.0, cbuf, ld, wbuf, ld, 0.0, o->p, o->ldp, nullptr, sc, scratch, st));
   if (!pr->phi && !pr->c_init) {
     // fold a sketch-generator overflow into bit 1 of the status word so the

@@ -223,6 +223,23 @@ def transpose(ctx, src, dst=None, lower=False):
     return dst
 
 
+def second_stage(ctx, r, w=None, l=None):
+    """(W, R̃) = qr(Rᵀ) and L = tril(R̃ᵀ) of the d×d upper-triangular ``r``
+    (reference algorithms.py:256-257) → (W, L)."""
+    d = r.shape[0]
+    dev = r.device
+    w = empty_matrix(d, d, dev) if w is None else w
+    l = empty_matrix(d, d, dev) if l is None else l
+    nbytes = ctypes.c_size_t()
+    with ctx.lock:
+        ctx.check(ctx.lib.pbq_second_stage_workspace_bytes(ctx.handle, d, ctypes.byref(nbytes)), "second stage workspace")
+        ws = workspace(nbytes.value, dev)
+        st = ctx.lib.pbq_second_stage(ctx.handle, d, ptr(r), ld_of(r), ptr(w), ld_of(w), ptr(l), ld_of(l), ptr(ws),
+                                      nbytes.value, stream_ptr(dev))
+        ctx.check(st, "second stage")
+    return w, l
+
+
 def cpqr_pivots(ctx, m, out=None):
     """Pivot order of LAPACK dgeqp3 for the m×n device matrix ``m`` → int64
     device tensor ``perm`` (n entries) with m[:, perm] = Q·R."""

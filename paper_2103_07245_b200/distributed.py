@@ -78,6 +78,10 @@ class CudaBackend:
     def transpose(self, src, dst, lower=False):
         return _dev.transpose(self.ctx, src, dst, lower=lower)
 
+    def second_stage(self, r, w, l):
+        """(W, R̃) = qr(Rᵀ), L = tril(R̃ᵀ) (one CTA for d ≤ 160)."""
+        return _dev.second_stage(self.ctx, r, w, l)
+
     def contiguous(self, t):
         return _dev.as_kernel_operand(t)
 
@@ -291,9 +295,12 @@ class DistributedPbpQlp:
             self._orth_c_(flags[site:site + 1])
         be.gemm_nn(A_local, self.C, self.Q)
         self._qr_sharded_()
-        be.transpose(self.R, self.W)
-        be.qr_(self.W, self.Rt)
-        be.transpose(self.Rt, self.L, lower=True)
+        if hasattr(be, "second_stage"):
+            be.second_stage(self.R, self.W, self.L)
+        else:
+            be.transpose(self.R, self.W)
+            be.qr_(self.W, self.Rt)
+            be.transpose(self.Rt, self.L, lower=True)
         be.gemm_nn(self.C, self.W, self.P)
 
     def finish(self, stacklevel=3):

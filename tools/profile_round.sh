@@ -16,4 +16,10 @@ $NCU --set full --import-source on -k regex:gemm_f64 --launch-skip 1 -c 1 -f -o 
   python tools/gemm_probe.py > $O/${TAG}_ncu_gemm_tn.log 2>&1
 $NCU --set full --import-source on -k regex:gemm_f64 --launch-skip 7 -c 1 -f -o $O/${TAG}_gemm_nn \
   python tools/gemm_probe.py > $O/${TAG}_ncu_gemm_nn.log 2>&1
+python tools/_cq_one.py > /dev/null 2>&1 || exit 1
+$NCU --set full --import-source on -k regex:cholqr_factor_kernel --launch-skip 4 -c 2 -f -o $O/${TAG}_cq_factor \
+  python tools/_cq_one.py > $O/${TAG}_ncu_cq.log 2>&1
+python tools/sketch_probe.py > $O/${TAG}_sketch_probe.txt 2>&1 || exit 1
+$NCU --set full --import-source on -k regex:sketch_k -c 3 -f -o $O/${TAG}_sketch \
+  python tools/sketch_probe.py > $O/${TAG}_ncu_sketch.log 2>&1
 echo done

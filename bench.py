@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--q", type=int, default=None, help="override the workload's q")
     ap.add_argument("--path", default="pbp_qlp", choices=["pbp_qlp", "r_svd", "cor_utv"],
                     help="r_svd / cor_utv: the sibling randomized paths (SURVEY §8 f3), single GPU")
+    ap.add_argument("--exchange", default=None, choices=["p2p", "nccl"],
+                    help="N > 1 AᵀX exchange: p2p = the fused scatter-GEMM / slice reduce over NVLink peer memory "
+                         "(default with NCCL), nccl = chunked GEMM + asynchronous ncclAllReduce")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: validates the N>1 code path with ranks sharing GPUs (host-mediated "
                          "collectives); its timings are not bench values")
@@ -221,7 +224,17 @@ def run_ours(args, world, rank, local):
         a = a_full[rows[rank]:rows[rank + 1]].contiguous()
         del a_full
         torch.cuda.empty_cache()
-        runner = PD.DistributedPbpQlp(n1, n2, d, q, rows, dev)
+        # p2p needs GPUs of their own (its waits span ranks): never with the
+        # gloo validation mode, where ranks share a GPU
+        exchange = args.exchange or ("p2p" if args.dist_backend == "nccl" else "nccl")
+        if exchange == "p2p" and args.dist_backend != "nccl":
+            raise SystemExit("--exchange p2p needs --dist-backend nccl (one GPU per rank)")
+        try:
+            runner = PD.DistributedPbpQlp(n1, n2, d, q, rows, dev, exchange=exchange)
+            exchange_note = exchange
+        except Exception as exc:  # symmetric memory unavailable: the NCCL exchange
+            runner = PD.DistributedPbpQlp(n1, n2, d, q, rows, dev, exchange="nccl")
+            exchange_note = f"nccl (p2p unavailable: {type(exc).__name__}: {str(exc)[:120]})"
         step = lambda s: runner.run(a, seed=s)  # noqa: E731
         finish = runner.finish
         ctx = D.context(dev)
@@ -298,7 +311,7 @@ def run_ours(args, world, rank, local):
             "traffic_unit": "bytes per launch (DRAM read + write)", "traffic_source": traffic["source"],
             "algorithmic_bytes_per_launch": 8.0 * (m_loc * n2 + m_loc * d + n2 * d),
             "kernel": "gemm_f64_tma (C=A^T X and D=A X, FP64 DMMA.8x8x4, TMA-staged)" + ("" if world == 1 else
-                      f", rank 0's row shard ({m_loc} rows); AᵀX in row-block chunks overlapped with their allreduce"),
+                      f", rank 0's row shard ({m_loc} rows); AᵀX exchange: {exchange_note}"),
             "per_launch_flop": fl_pass, "launches_per_step": gemm_n / args.steps,
             "gemm_ms_per_step": gemm_ms / args.steps, "gemm_share_of_step": gemm_ms / args.steps / ms,
             "qr_ms_per_step": by_class["qr"][0] / args.steps, "sketch_ms_per_step": by_class["sketch"][0] / args.steps,
@@ -368,6 +381,8 @@ def run_ours(args, world, rank, local):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "check": check,
         }
+        if world > 1:
+            line["exchange"] = exchange_note
         if world > 1 and args.dist_backend != "nccl":
             line["validation_only"] = f"{args.dist_backend} collectives, ranks sharing GPUs: not a bench value"
         print(json.dumps(line), flush=True)

@@ -200,6 +200,37 @@ int pbq_second_stage(pbq_ctx* ctx, int64_t d, const double* R, int64_t ldr, doub
                      int64_t ldl, void* workspace, size_t workspace_bytes, void* stream);
 int pbq_second_stage_workspace_bytes(pbq_ctx* ctx, int64_t d, size_t* bytes);
 
+/* Fused AᵀX exchange over NVLink peer memory (the allreduce of
+ * the row-sharded partials C_g = A_gᵀ·X_g, algorithms.py:182-184 across
+ * ranks).  Rows of the n2×N result are split into world slices of S rows
+ * (S a multiple of 128); rank r owns slice r.  Buffers come from symmetric
+ * (peer-mapped) memory; the pointer arguments named *_ptrs are DEVICE arrays
+ * of world peer pointers, indexed by rank.
+ *   pbq_gemm_tn_scatter: the DMMA GEMM whose epilogue stores each finished
+ *     128-row tile into the owner's landing buffer, slot `rank` (landing is
+ *     world·S×ldl doubles per rank), then adds 1 to the owner's tile counter
+ *     (system-scope release).  Needs the TMA GEMM.
+ *   pbq_xchg_reduce: rank r waits until its tile counter reaches `target`,
+ *     sums its slice's world slots in slot order and stores the result into
+ *     rows [r·S, r·S+S) ∩ [0, n2) of every rank's C (ld ldc), then adds
+ *     PBQ_XCHG_CTAS (64) to every rank's done counter.
+ *   pbq_xchg_wait: waits until this rank's done counter reaches `target`.
+ * Counters are never reset: per call the tile counter of rank r grows by
+ * pbq_xchg_expected_tiles(...) and the done counter by 64·world, so call k
+ * (1-based) passes target = k·(that growth).  A rank's counter block is three
+ * consecutive uint32 [tile count, done count, status]; a wait that has not
+ * completed after 20 s sets status bit 0 and returns instead of hanging. */
+#define PBQ_XCHG_CTAS 64
+int pbq_gemm_tn_scatter(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double* const* land_ptrs, uint32_t* const* cnt_ptrs, int32_t rank, int32_t world,
+                        int64_t S, int64_t ldl, int32_t* nonfinite, void* workspace, size_t workspace_bytes,
+                        void* stream);
+int pbq_xchg_reduce(pbq_ctx* ctx, int32_t rank, int32_t world, int64_t n2, int64_t N, int64_t S, const double* land,
+                    int64_t ldl, double* const* c_ptrs, int64_t ldc, const uint32_t* cnt, uint32_t target,
+                    uint32_t* const* done_ptrs, void* stream);
+int pbq_xchg_wait(pbq_ctx* ctx, const uint32_t* done, uint32_t target, void* stream);
+int pbq_xchg_expected_tiles(int64_t n2, int64_t N, int64_t S, int32_t rank, int32_t world, uint32_t* tiles);
+
 /* Small helpers used by the host driver.
  * dst[i][j] = src[j][i]            (n×n), or with lower=1 the lower triangle
  * of srcᵀ and zeros above (L = tril(R̃ᵀ), algorithms.py:257). */

@@ -41,6 +41,10 @@ EXPORTED = (
     "pbq_transpose",
     "pbq_second_stage",
     "pbq_second_stage_workspace_bytes",
+    "pbq_gemm_tn_scatter",
+    "pbq_xchg_reduce",
+    "pbq_xchg_wait",
+    "pbq_xchg_expected_tiles",
     "pbq_debug_qr_hooks",
     "pbq_profile_begin",
     "pbq_profile_end",
@@ -106,6 +110,12 @@ _SIGS = {
     "pbq_transpose": ([c_p, c_i64, c_p, c_i64, c_p, c_i64, c_i32, c_p], ctypes.c_int),
     "pbq_second_stage": ([c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_sz, c_p], ctypes.c_int),
     "pbq_second_stage_workspace_bytes": ([c_p, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),
+    "pbq_gemm_tn_scatter": ([c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_p, c_i32, c_i32, c_i64, c_i64, c_p,
+                             c_p, c_sz, c_p], ctypes.c_int),
+    "pbq_xchg_reduce": ([c_p, c_i32, c_i32, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, ctypes.c_uint32, c_p, c_p],
+                        ctypes.c_int),
+    "pbq_xchg_wait": ([c_p, c_p, ctypes.c_uint32, c_p], ctypes.c_int),
+    "pbq_xchg_expected_tiles": ([c_i64, c_i64, c_i64, c_i32, c_i32, ctypes.POINTER(ctypes.c_uint32)], ctypes.c_int),
     "pbq_debug_qr_hooks": ([c_p, c_p, c_p, c_p], ctypes.c_int),
     "pbq_profile_begin": ([c_p, c_i32], ctypes.c_int),
     "pbq_profile_end": ([c_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)], ctypes.c_int),

@@ -1,0 +1,95 @@
+// Fused AᵀX exchange over NVLink peer memory (the allreduce(sum)
+// of the per-rank partials C_g = A_gᵀ·X_g, reference `_PassCounter.apply_t`
+// across row shards, algorithms.py:182-184).
+//
+// Instead of GEMM → ncclAllReduce, the GEMM's epilogue is the first half of
+// a reduce-scatter: rows of C are split into G slices of S rows (S a
+// multiple of the 128-row tile), slice r owned by rank r, and every finished
+// output tile of rank g is stored straight into rank r's landing buffer
+// (slot g) through the peer mapping (symmetric memory), followed by one
+// system-scope release increment of rank r's tile counter.  The tiles cross
+// NVLink while the GEMM is still computing the next ones.  Then:
+//   xchg_reduce_kernel  (rank r) waits for its tile count, sums the G slots
+//                        of its slice in slot order (so every rank ends with
+//                        the same bits), stores the slice into every rank's C
+//                        (all-gather by peer stores) and increments every
+//                        rank's done counter;
+//   xchg_wait_kernel    waits until all G slices have arrived.
+// Counters only grow: the host passes targets epoch·(expected per call), so
+// nothing is reset between calls.  With G = 1 the same kernels run against
+// the rank's own buffers.
+#pragma once
+#include "common.cuh"
+
+namespace pbq {
+
+// CTAs of xchg_reduce_kernel (PBQ_XCHG_CTAS, include/pbq.h): each increments
+// every rank's done counter once, so a call adds PBQ_XCHG_CTAS·G to each
+#ifndef PBQ_XCHG_CTAS
+#define PBQ_XCHG_CTAS 64
+#endif
+
+__device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add(unsigned int* p, unsigned int v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// Epilogue target of the scatter GEMM (GemmArgs::xs): tile rows [m0, m0+BM)
+// of the n2×N result go to landing[owner][(rank·S + m0 − owner·S) … ].
+struct XchgScatter {
+  double* const* land;         // G device pointers (peer-mapped), each G·S×ldl doubles
+  unsigned int* const* cnt;    // G device pointers to the owners' tile counters
+  long S, ldl;
+  int rank, world;
+};
+
+// Spin until *p ≥ target, at most PBQ_XCHG_TIMEOUT_NS: a peer that never
+// arrives (a broken peer mapping, a rank that died) must not hang the GPU.
+// On timeout *status |= 1 (the host raises); the caller then proceeds.
+#define PBQ_XCHG_TIMEOUT_NS 20000000000ull
+__device__ __forceinline__ void xchg_spin(const unsigned int* p, unsigned int target, unsigned int* status) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (ld_acquire_sys_u32(p) < target) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > PBQ_XCHG_TIMEOUT_NS) {
+      atomicOr(status, 1u);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
+// Sum of the G landing slots of this rank's slice → every rank's C.  The
+// counter block of a rank is [tile count, done count, status].
+__global__ void __launch_bounds__(256) xchg_reduce_kernel(const double* __restrict__ land, long ldl, int world, long S,
+                                                          long rows, long n, double* const* c_ptrs, long ldc,
+                                                          long row0, const unsigned int* cnt, unsigned int target,
+                                                          unsigned int* const* done_ptrs) {
+  if (threadIdx.x == 0) xchg_spin(cnt, target, const_cast<unsigned int*>(cnt) + 2);
+  __syncthreads();
+  const long total = rows * n;
+  for (long e = long(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += long(gridDim.x) * blockDim.x) {
+    const long i = e / n, j = e % n;
+    double s = 0.0;
+    for (int g = 0; g < world; ++g) s += __ldcv(land + (long(g) * S + i) * ldl + j);  // slot order
+    for (int p = 0; p < world; ++p) c_ptrs[p][(row0 + i) * ldc + j] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < world; ++p) red_release_sys_add(done_ptrs[p], 1u);
+  }
+}
+
+__global__ void xchg_wait_kernel(const unsigned int* done, unsigned int target) {
+  if (threadIdx.x == 0) xchg_spin(done, target, const_cast<unsigned int*>(done) + 1);
+  __syncthreads();
+}
+
+}  // namespace pbq

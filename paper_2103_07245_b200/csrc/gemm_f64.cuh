@@ -70,6 +70,13 @@ struct GemmArgs {
   double* red_Gcopy;
   unsigned long long* red_emax;
   long red_n, red_np;
+  // scatter epilogue (TMA kernel, plain mode; exchange_f64.cuh): instead of C,
+  // tile rows [m0, m0+BM) go to xs_land[o] + (xs_rank·xs_S + m0 − o·xs_S)·xs_ldl,
+  // o = m0 / xs_S (the slice owner, peer memory), then xs_cnt[o] += 1 (release, sys)
+  double* const* xs_land;
+  unsigned int* const* xs_cnt;
+  long xs_S, xs_ldl;
+  int xs_rank;
 };
 
 

@@ -375,6 +375,15 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
       }
       continue;
     }
+    // plain epilogue, or the scatter into the slice owner's landing slot
+    int owner = 0;
+    double* cbase = p.C + m0 * p.ldc;
+    long ldo = p.ldc;
+    if (p.xs_land) {
+      owner = int(m0 / p.xs_S);
+      cbase = p.xs_land[owner] + (long(p.xs_rank) * p.xs_S + (m0 - long(owner) * p.xs_S)) * p.xs_ldl;
+      ldo = p.xs_ldl;
+    }
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       const long r = m0 + out_row(mt);
@@ -382,7 +391,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const long cidx = n0 + out_col(nt);
-        double* dst = p.C + r * p.ldc + cidx;
+        double* dst = cbase + (r - m0) * ldo + cidx;
         double v0 = p.alpha * acc[mt][nt][0], v1 = p.alpha * acc[mt][nt][1];
         if (cidx + 1 < p.N) {
           if (p.beta != 0.0) {
@@ -395,6 +404,13 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
           if (p.beta != 0.0) v0 += p.beta * dst[0];
           dst[0] = v0;
         }
+      }
+    }
+    if (p.xs_land) {  // the tile has landed in the owner's slot: count it there
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence_system();
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;\n" ::"l"(p.xs_cnt[owner]) : "memory");
       }
     }
   }

@@ -18,6 +18,7 @@
 #include "cpqr_f64.cuh"
 #include "qr_f64.cuh"
 #include "sketch.cuh"
+#include "exchange_f64.cuh"
 
 // Optional per-kernel-class timing (pbq_profile_*): event pairs recorded on
 // the launch stream around every kernel of the pipeline.
@@ -298,7 +299,8 @@ size_t gemm_ws_bytes(const GemmPlan& p) {
 template <bool TRANS>
 int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double* A, long lda, const double* B,
                 long ldb, double beta, double* C, long ldc, int32_t* nonfinite, void* ws, size_t ws_bytes,
-                cudaStream_t st, const int* skip = nullptr, bool tri_b = false, const int* run_if = nullptr) {
+                cudaStream_t st, const int* skip = nullptr, bool tri_b = false, const int* run_if = nullptr,
+                const XchgScatter* xs = nullptr) {
   if (M <= 0 || N <= 0 || K < 0) return fail(ctx, PBQ_ERR_DIM, "gemm: bad shape M=%ld N=%ld K=%ld", M, N, K);
   if ((lda & 1) || (ldb & 1) || (ldc & 1) || !aligned16(A) || !aligned16(B) || !aligned16(C))
     return fail(ctx, PBQ_ERR_PARAM, "gemm: leading dimensions must be even and pointers 16-byte aligned");
@@ -320,6 +322,11 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   a.tri_b = tri_b; a.row_iters = pl.row_iters;
   a.group = pl.group;
   a.run_if = run_if;
+  if (xs) {
+    if (!gemm_use_tma()) return fail(ctx, PBQ_ERR_UNSUPPORTED, "gemm scatter epilogue needs the TMA kernel");
+    if (xs->S % pl.bm != 0 || xs->S < 1) return fail(ctx, PBQ_ERR_PARAM, "gemm scatter: S must be a multiple of %d", pl.bm);
+    a.xs_land = xs->land; a.xs_cnt = xs->cnt; a.xs_S = xs->S; a.xs_ldl = xs->ldl; a.xs_rank = xs->rank;
+  }
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gemm: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
   ProfScope ps(ctx->prof, st, 0);
@@ -1109,6 +1116,50 @@ int64_t pbq_ctx_launch_count(const pbq_ctx* ctx) { return ctx ? ctx->launches : 
 int pbq_gemm_workspace_bytes(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, size_t* bytes) {
   if (!ctx || !bytes) return PBQ_ERR_PARAM;
   *bytes = gemm_ws_bytes(gemm_plan(ctx, M, N, std::max<int64_t>(K, 1)));
+  return PBQ_OK;
+}
+
+int pbq_gemm_tn_scatter(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double* const* land_ptrs, uint32_t* const* cnt_ptrs, int32_t rank, int32_t world,
+                        int64_t S, int64_t ldl, int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream) {
+  if (!ctx || !land_ptrs || !cnt_ptrs) return PBQ_ERR_PARAM;
+  if (world < 1 || rank < 0 || rank >= world) return fail(ctx, PBQ_ERR_PARAM, "gemm scatter: bad rank/world");
+  if (lda < M || ldb < N || ldl < N || (ldl & 1)) return fail(ctx, PBQ_ERR_PARAM, "gemm scatter: bad leading dimension");
+  if (long(world) * S < M) return fail(ctx, PBQ_ERR_DIM, "gemm scatter: world·S < M");
+  XchgScatter xs;
+  xs.land = land_ptrs; xs.cnt = cnt_ptrs; xs.S = S; xs.ldl = ldl; xs.rank = rank; xs.world = world;
+  // C is unused by the scatter epilogue; pass the landing pointer array's slot only for the argument checks
+  return gemm_launch<true>(ctx, M, N, K, 1.0, A, lda, B, ldb, 0.0, reinterpret_cast<double*>(ws), N + (N & 1),
+                           nonfinite, ws, ws_bytes, static_cast<cudaStream_t>(stream), nullptr, false, nullptr, &xs);
+}
+
+int pbq_xchg_reduce(pbq_ctx* ctx, int32_t rank, int32_t world, int64_t n2, int64_t N, int64_t S, const double* land,
+                    int64_t ldl, double* const* c_ptrs, int64_t ldc, const uint32_t* cnt, uint32_t target,
+                    uint32_t* const* done_ptrs, void* stream) {
+  if (!ctx || !land || !c_ptrs || !cnt || !done_ptrs) return PBQ_ERR_PARAM;
+  if (world < 1 || rank < 0 || rank >= world || S < 1) return fail(ctx, PBQ_ERR_PARAM, "xchg_reduce: bad arguments");
+  const long row0 = long(rank) * S;
+  const long rows = std::max<long>(0, std::min<long>(S, n2 - row0));
+  xchg_reduce_kernel<<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      land, ldl, world, S, rows, N, c_ptrs, ldc, row0, cnt, target, done_ptrs);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
+int pbq_xchg_wait(pbq_ctx* ctx, const uint32_t* done, uint32_t target, void* stream) {
+  if (!ctx || !done) return PBQ_ERR_PARAM;
+  xchg_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(done, target);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
+int pbq_xchg_expected_tiles(int64_t n2, int64_t N, int64_t S, int32_t rank, int32_t world, uint32_t* tiles) {
+  if (!tiles || world < 1 || rank < 0 || rank >= world || S < 1 || N < 1) return PBQ_ERR_PARAM;
+  const long rows = std::max<long>(0, std::min<long>(S, n2 - long(rank) * S));
+  const long tn = N <= 64 ? 1 : ceil_div(N, 128);  // column tiles of gemm_plan
+  *tiles = uint32_t(ceil_div(rows, 128) * tn * world);
   return PBQ_OK;
 }
 

@@ -163,6 +163,45 @@ def gemm(ctx, a, b, trans_a, out=None, alpha=1.0, beta=0.0, nonfinite=None):
     return out
 
 
+# ------------------------------------------------ fused AᵀX exchange (p2p) --
+def gemm_tn_scatter(ctx, a, x, xchg, nonfinite=None):
+    """C_rank = aᵀ·x with every finished tile stored into its slice owner's
+    landing slot through the peer mapping (pbq_gemm_tn_scatter)."""
+    a = as_kernel_operand(a)
+    x = as_kernel_operand(x)
+    K, M = a.shape
+    N = x.shape[1]
+    nbytes = ctypes.c_size_t()
+    with ctx.lock:
+        ctx.check(ctx.lib.pbq_gemm_workspace_bytes(ctx.handle, M, N, K, ctypes.byref(nbytes)), "gemm workspace")
+        ws = workspace(nbytes.value, a.device)
+        st = ctx.lib.pbq_gemm_tn_scatter(ctx.handle, M, N, K, ptr(a), ld_of(a), ptr(x), ld_of(x), ptr(xchg.land_ptrs),
+                                         ptr(xchg.cnt_ptrs), xchg.rank, xchg.world, xchg.S, xchg.ldl, ptr(nonfinite),
+                                         ptr(ws), nbytes.value, stream_ptr(a.device))
+        ctx.check(st, "gemm_tn_scatter")
+
+
+def xchg_reduce(ctx, xchg, n2, n, tile_target):
+    with ctx.lock:
+        st = ctx.lib.pbq_xchg_reduce(ctx.handle, xchg.rank, xchg.world, n2, n, xchg.S, ptr(xchg.land), xchg.ldl,
+                                     ptr(xchg.c_ptrs), xchg.ldl, ptr(xchg.cnt), ctypes.c_uint32(tile_target),
+                                     ptr(xchg.done_ptrs), stream_ptr(xchg.land.device))
+        ctx.check(st, "xchg_reduce")
+
+
+def xchg_wait(ctx, xchg, done_target):
+    with ctx.lock:
+        st = ctx.lib.pbq_xchg_wait(ctx.handle, ptr(xchg.done), ctypes.c_uint32(done_target),
+                                   stream_ptr(xchg.land.device))
+        ctx.check(st, "xchg_wait")
+
+
+def xchg_expected_tiles(ctx, n2, n, S, rank, world):
+    t = ctypes.c_uint32()
+    ctx.check(ctx.lib.pbq_xchg_expected_tiles(n2, n, S, rank, world, ctypes.byref(t)), "xchg_expected_tiles")
+    return int(t.value)
+
+
 def householder_qr_(ctx, a, r=None, want_q=True, rank_flag=None):
     """In-place QR of the m×n device matrix ``a`` (must be kernel-ready)."""
     dev = a.device

@@ -41,12 +41,85 @@ from . import device as _dev
 from . import exceptions as _exc
 from .linalg import warn_rank
 
-__all__ = ["shard_rows", "DistributedPbpQlp", "CudaBackend"]
+__all__ = ["shard_rows", "DistributedPbpQlp", "CudaBackend", "P2PExchange", "virtual_exchanges",
+           "xchg_slice_rows"]
 
 
 def shard_rows(n1, world):
     """Contiguous, balanced row offsets [r_0 = 0, …, r_G = n1]."""
     return [(n1 * g) // world for g in range(world + 1)]
+
+
+# ------------------------------------------------ fused AᵀX exchange (p2p) --
+def xchg_slice_rows(n2, world):
+    """Rows per owner slice of the exchanged n2×d result: ⌈n2/G⌉ rounded up
+    to the GEMM's 128-row tile, so no tile straddles two owners."""
+    s = -(-n2 // world)
+    return -(-s // 128) * 128
+
+
+class _XchgBuffers:
+    """One rank's landing buffer (G slots of S×ldl), result C (G·S×ldl), tile
+    and done counters, and device arrays of every rank's pointers to them
+    (indexed by rank) — the arguments of pbq_gemm_tn_scatter /
+    pbq_xchg_reduce / pbq_xchg_wait (include/pbq.h)."""
+
+    def __init__(self, rank, world, S, ldl, land, c, ctr):
+        self.rank, self.world, self.S, self.ldl = rank, world, S, ldl
+        self.land = land.view(world * S, ldl)
+        self.C = c.view(world * S, ldl)
+        self.cnt, self.done, self.status = ctr[0:1], ctr[1:2], ctr[2:3]  # [tiles, done, status]
+        self.land_ptrs = self.c_ptrs = self.cnt_ptrs = self.done_ptrs = None
+
+    def set_peers(self, land, c, cnt, done):
+        dev = self.land.device
+        mk = lambda v: torch.tensor([int(x) for x in v], dtype=torch.int64, device=dev)  # noqa: E731
+        self.land_ptrs, self.c_ptrs, self.cnt_ptrs, self.done_ptrs = mk(land), mk(c), mk(cnt), mk(done)
+
+
+class P2PExchange(_XchgBuffers):
+    """The buffers in symmetric memory (torch.distributed._symmetric_memory:
+    peer-mapped allocations over NVLink) of this rank of ``group``."""
+
+    def __init__(self, n2, d, device, group=None):
+        import torch.distributed._symmetric_memory as symm
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        S, ldl = xchg_slice_rows(n2, world), d + (d & 1)
+        pg = group if group is not None else dist.group.WORLD
+        land = symm.empty(world * S * ldl, dtype=torch.float64, device=device)
+        c = symm.empty(world * S * ldl, dtype=torch.float64, device=device)
+        ctr = symm.empty(64, dtype=torch.int32, device=device)
+        c.zero_()  # rows ≥ n2 of C stay zero (orth(C) runs on whole row slices)
+        ctr.zero_()
+        super().__init__(rank, world, S, ldl, land, c, ctr)
+        handles = [symm.rendezvous(t, pg) for t in (land, c, ctr)]
+        peers = []
+        for t, h in zip((land, c, ctr), handles):
+            off = t.data_ptr() - int(h.buffer_ptrs[rank])
+            peers.append([int(h.buffer_ptrs[p]) + off for p in range(world)])
+        self.set_peers(peers[0], peers[1], peers[2], [p + 4 for p in peers[2]])
+        self._keep = (land, c, ctr, handles)
+        torch.cuda.synchronize(device)
+        dist.barrier(group)  # every rank's counters are zero before any peer adds to them
+
+
+def virtual_exchanges(n2, d, world, device):
+    """``world`` exchange buffer sets on ONE device whose peer pointers refer
+    to each other — the one-GPU emulation of the p2p exchange used by the
+    tests (each virtual rank's kernels are launched in turn; no kernel waits
+    on a kernel that has not run yet)."""
+    S, ldl = xchg_slice_rows(n2, world), d + (d & 1)
+    xs = []
+    for r in range(world):
+        land = torch.full((world * S * ldl,), float("nan"), dtype=torch.float64, device=device)
+        c = torch.zeros(world * S * ldl, dtype=torch.float64, device=device)
+        ctr = torch.zeros(64, dtype=torch.int32, device=device)
+        xs.append(_XchgBuffers(r, world, S, ldl, land, c, ctr))
+    for x in xs:
+        x.set_peers([y.land.data_ptr() for y in xs], [y.C.data_ptr() for y in xs], [y.cnt.data_ptr() for y in xs],
+                    [y.done.data_ptr() for y in xs])
+    return xs
 
 
 class CudaBackend:
@@ -77,6 +150,19 @@ class CudaBackend:
 
     def transpose(self, src, dst, lower=False):
         return _dev.transpose(self.ctx, src, dst, lower=lower)
+
+    # -- fused AᵀX exchange over peer memory ----------------------------------
+    def xchg_init(self, n2, d, group):
+        return P2PExchange(n2, d, self.device, group)
+
+    def xchg_at_x(self, xchg, a, x, n2, epoch, nonfinite=None):
+        """xchg.C[:n2] = Σ_g A_gᵀ·X_g on every rank: scatter GEMM, slice
+        reduce + all-gather, wait (call ``epoch`` ≥ 1 of this buffer set)."""
+        d = x.shape[1]
+        _dev.gemm_tn_scatter(self.ctx, a, x, xchg, nonfinite=nonfinite)
+        tiles = _dev.xchg_expected_tiles(self.ctx, n2, d, xchg.S, xchg.rank, xchg.world)
+        _dev.xchg_reduce(self.ctx, xchg, n2, d, epoch * tiles)
+        _dev.xchg_wait(self.ctx, xchg, epoch * 64 * xchg.world)
 
     def second_stage(self, r, w, l):
         """(W, R̃) = qr(Rᵀ), L = tril(R̃ᵀ) (one CTA for d ≤ 160)."""
@@ -109,7 +195,7 @@ class DistributedPbpQlp:
     """One rank's part of a row-sharded PbP-QLP; all ranks call ``run``."""
 
     def __init__(self, n1, n2, d, q, rows, device=None, reorthonormalize=True, group=None, backend=None, chunks=None,
-                 dist_qr="auto"):
+                 dist_qr="auto", exchange="nccl"):
         self.n1, self.n2, self.d, self.q = int(n1), int(n2), int(d), int(q)
         self.rows = list(rows)
         self.group = group
@@ -129,12 +215,26 @@ class DistributedPbpQlp:
             raise _exc.ParameterError("chunks must be >= 1")
         self.be = backend if backend is not None else CudaBackend(device)
         be = self.be
-        # AᵀX partial → allreduced → P̄ (in place).  G·s rows (s = ⌈n2/G⌉) so
-        # that orth(C) can run on equal row slices; rows ≥ n2 stay zero.
-        self.slice_rows = -(-self.n2 // self.world)
-        self.Cbuf = be.empty(self.world * self.slice_rows, self.d)
-        ldc = self.Cbuf.stride(0)
-        self.Cbuf.as_strided((self.Cbuf.shape[0], ldc), (ldc, 1)).zero_()  # incl. the even-ld pad column
+        # AᵀX exchange: "nccl" — chunked GEMM + asynchronous allreduces;
+        # "p2p" — the fused scatter-GEMM / slice reduce over peer memory
+        if exchange not in ("nccl", "p2p"):
+            raise _exc.ParameterError("exchange must be 'nccl' or 'p2p'")
+        if exchange == "p2p" and not hasattr(be, "xchg_init"):
+            raise _exc.ParameterError("this backend has no peer-memory exchange")
+        self.exchange = exchange
+        self.xchg = be.xchg_init(self.n2, self.d, group) if exchange == "p2p" else None
+        self.epoch = 0
+        # AᵀX partial → allreduced → P̄ (in place).  G·s rows (s = ⌈n2/G⌉, for
+        # p2p rounded to the 128-row tile) so that orth(C) can run on equal
+        # row slices; rows ≥ n2 stay zero.
+        if self.xchg is not None:
+            self.slice_rows = self.xchg.S
+            self.Cbuf = self.xchg.C[:, :self.d]
+        else:
+            self.slice_rows = -(-self.n2 // self.world)
+            self.Cbuf = be.empty(self.world * self.slice_rows, self.d)
+            ldc = self.Cbuf.stride(0)
+            self.Cbuf.as_strided((self.Cbuf.shape[0], ldc), (ldc, 1)).zero_()  # incl. the even-ld pad column
         self.C = self.Cbuf[:self.n2]
         self.Q = be.empty(self.m, self.d)          # A_g·P̄ → local Q_g → Q rows of this rank
         self.R = be.empty(self.d, self.d)
@@ -177,9 +277,13 @@ class DistributedPbpQlp:
 
     def _at_x(self, A_local, X, nonfinite=None):
         """self.C = Σ_g A_gᵀ·X_g with the allreduce of each row block
-        overlapping the GEMM of the next one."""
+        overlapping the GEMM of the next one (or the fused p2p exchange)."""
         be = self.be
         C = self.C
+        if self.xchg is not None:
+            self.epoch += 1
+            be.xchg_at_x(self.xchg, A_local, X, self.n2, self.epoch, nonfinite=nonfinite)
+            return C
         ld = C.stride(0)
         padded = C.as_strided((C.shape[0], ld), (ld, 1))  # whole rows incl. the even-ld pad column
         handles = []
@@ -308,6 +412,8 @@ class DistributedPbpQlp:
         # a non-finite entry in any shard fails every rank
         dist.all_reduce(self.flags[0:2], op=dist.ReduceOp.MAX, group=self.group)
         dist.all_reduce(self.flags[-1:], op=dist.ReduceOp.MAX, group=self.group)  # same on every rank anyway
+        if self.xchg is not None and int(self.xchg.status.item()):
+            raise _exc.DeviceError("p2p AᵀX exchange: a peer did not arrive within 20 s")
         fl = self.flags.cpu().tolist()
         if fl[0]:
             raise _exc.MatrixInputError("a contains non-finite entries")

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <unordered_map>
 
 #include "../../include/pbq.h"
 #include "common.cuh"
@@ -43,6 +44,7 @@ struct pbq_ctx {
   unsigned long long* qr_bar_wait_ns = nullptr;
   int qr_method = PBQ_QR_AUTO;
   int* cq_stats = nullptr;                    // debug: [Cholesky-QR2 done, fallbacks]
+  std::unordered_map<const void*, int> smem_attr;  // max dynamic smem already set per kernel (one driver call each)
   char err[512] = {0};
 };
 
@@ -73,6 +75,17 @@ int fail(pbq_ctx* ctx, int code, const char* fmt, ...) {
     int s_ = (expr);         \
     if (s_ != PBQ_OK) return s_; \
   } while (0)
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize, set once per kernel and
+// context (raised when a launch needs more): a driver call per launch cost
+// ~µs of host time on every one of the pipeline's ~50 launches
+cudaError_t ensure_smem(pbq_ctx* ctx, const void* fn, size_t bytes) {
+  int& cur = ctx->smem_attr[fn];
+  if (cur >= int(bytes)) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e == cudaSuccess) cur = int(bytes);
+  return e;
+}
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -241,7 +254,7 @@ int gemm_dispatch(pbq_ctx* ctx, const GemmArgs& a, bool trans, int bn, int mode,
                              : GemmCfg<false, 128, 128, 32, GEMM_WM, 32, 3>::SMEM_BYTES);
     args[0] = const_cast<GemmArgs*>(&a);
   }
-  PBQ_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  PBQ_CUDA(ctx, ensure_smem(ctx, fn, smem));
   if (coop)
     PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(fn, grid, dim3(threads), args, smem, st));
   else
@@ -401,8 +414,7 @@ int hh_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   a.run_if = run_if;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
-  PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&qr_tall_kernel),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
+  PBQ_CUDA(ctx, ensure_smem(ctx, reinterpret_cast<const void*>(&qr_tall_kernel), pl.smem));
   void* args[] = {&a};
   ProfScope ps(ctx->prof, st, 1);
   PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&qr_tall_kernel), dim3(pl.grid),
@@ -489,8 +501,7 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
 }
 
 int factor_launch(pbq_ctx* ctx, const CqPlan& pl, CqArgs& a, cudaStream_t st) {
-  PBQ_CUDA(ctx, cudaFuncSetAttribute(reinterpret_cast<void*>(&cholqr_factor_kernel),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(CQ_SMEM_BYTES)));
+  PBQ_CUDA(ctx, ensure_smem(ctx, reinterpret_cast<const void*>(&cholqr_factor_kernel), CQ_SMEM_BYTES));
   void* args[] = {&a};
   PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&cholqr_factor_kernel),
                                             dim3(a.pass == 1 ? pl.grid : pl.grid2),

@@ -231,6 +231,21 @@ int pbq_xchg_reduce(pbq_ctx* ctx, int32_t rank, int32_t world, int64_t n2, int64
 int pbq_xchg_wait(pbq_ctx* ctx, const uint32_t* done, uint32_t target, void* stream);
 int pbq_xchg_expected_tiles(int64_t n2, int64_t N, int64_t S, int32_t rank, int32_t world, uint32_t* tiles);
 
+/* Small collectives on symmetric memory (the d×d Gram allreduces of the
+ * distributed Cholesky-QR2 and the all-gather of orth(C)'s row slices):
+ *   pbq_p2p_push: copies src (n doubles) to dst_ptrs[p] + rank·slot on every
+ *     rank p, then adds PBQ_XCHG_CTAS to every rank's counter cnt_ptrs[p];
+ *   pbq_p2p_sum:  waits until *cnt ≥ target, then out = Σ_g slots[g·slot + i]
+ *     in slot order (allreduce = push into the peers' slot arrays + sum);
+ *   pbq_p2p_wait: waits until *cnt ≥ target (all-gather = push with slot =
+ *     the slice length into the peers' result buffers + wait).
+ * Waits give up after 20 s and set *status bit 0 instead of hanging. */
+int pbq_p2p_push(pbq_ctx* ctx, const double* src, int64_t n, double* const* dst_ptrs, int64_t slot, int32_t rank,
+                 int32_t world, uint32_t* const* cnt_ptrs, void* stream);
+int pbq_p2p_sum(pbq_ctx* ctx, const double* slots, int64_t slot, int32_t world, int64_t n, double* out,
+                const uint32_t* cnt, uint32_t target, uint32_t* status, void* stream);
+int pbq_p2p_wait(pbq_ctx* ctx, const uint32_t* cnt, uint32_t target, uint32_t* status, void* stream);
+
 /* Small helpers used by the host driver.
  * dst[i][j] = src[j][i]            (n×n), or with lower=1 the lower triangle
  * of srcᵀ and zeros above (L = tril(R̃ᵀ), algorithms.py:257). */

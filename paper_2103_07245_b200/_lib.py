@@ -45,6 +45,9 @@ EXPORTED = (
     "pbq_xchg_reduce",
     "pbq_xchg_wait",
     "pbq_xchg_expected_tiles",
+    "pbq_p2p_push",
+    "pbq_p2p_sum",
+    "pbq_p2p_wait",
     "pbq_debug_qr_hooks",
     "pbq_profile_begin",
     "pbq_profile_end",
@@ -116,6 +119,9 @@ _SIGS = {
                         ctypes.c_int),
     "pbq_xchg_wait": ([c_p, c_p, ctypes.c_uint32, c_p], ctypes.c_int),
     "pbq_xchg_expected_tiles": ([c_i64, c_i64, c_i64, c_i32, c_i32, ctypes.POINTER(ctypes.c_uint32)], ctypes.c_int),
+    "pbq_p2p_push": ([c_p, c_p, c_i64, c_p, c_i64, c_i32, c_i32, c_p, c_p], ctypes.c_int),
+    "pbq_p2p_sum": ([c_p, c_p, c_i64, c_i32, c_i64, c_p, c_p, ctypes.c_uint32, c_p, c_p], ctypes.c_int),
+    "pbq_p2p_wait": ([c_p, c_p, ctypes.c_uint32, c_p, c_p], ctypes.c_int),
     "pbq_debug_qr_hooks": ([c_p, c_p, c_p, c_p], ctypes.c_int),
     "pbq_profile_begin": ([c_p, c_i32], ctypes.c_int),
     "pbq_profile_end": ([c_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)], ctypes.c_int),

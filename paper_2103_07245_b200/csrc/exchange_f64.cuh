@@ -87,6 +87,44 @@ __global__ void __launch_bounds__(256) xchg_reduce_kernel(const double* __restri
   }
 }
 
+// Small collectives on the same symmetric buffers (the d×d Gram allreduces
+// and the all-gather of orth(C)'s row slices):
+//   p2p_push_kernel: src (n doubles) → dst_ptrs[p] + rank·slot for every rank
+//     p, then one release increment of every rank's counter per CTA;
+//   p2p_sum_kernel:  wait for the counter, out = Σ_g slots[g·slot] in slot
+//     order (the same bits on every rank).
+// An all-gather is a push with slot = the slice size into C itself plus a
+// wait (xchg_wait_kernel on that counter).
+__global__ void __launch_bounds__(256) p2p_push_kernel(const double* __restrict__ src, long n, double* const* dst_ptrs,
+                                                       long slot, int rank, int world, unsigned int* const* cnt_ptrs) {
+  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+    const double v = src[i];
+    for (int p = 0; p < world; ++p) dst_ptrs[p][long(rank) * slot + i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < world; ++p) red_release_sys_add(cnt_ptrs[p], 1u);
+  }
+}
+
+__global__ void __launch_bounds__(256) p2p_sum_kernel(const double* __restrict__ slots, long slot, int world, long n,
+                                                      double* __restrict__ out, const unsigned int* cnt,
+                                                      unsigned int target, unsigned int* status) {
+  if (threadIdx.x == 0) xchg_spin(cnt, target, status);
+  __syncthreads();
+  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int g = 0; g < world; ++g) s += __ldcv(slots + long(g) * slot + i);
+    out[i] = s;
+  }
+}
+
+__global__ void p2p_wait_kernel(const unsigned int* cnt, unsigned int target, unsigned int* status) {
+  if (threadIdx.x == 0) xchg_spin(cnt, target, status);
+  __syncthreads();
+}
+
 __global__ void xchg_wait_kernel(const unsigned int* done, unsigned int target) {
   if (threadIdx.x == 0) xchg_spin(done, target, const_cast<unsigned int*>(done) + 1);
   __syncthreads();

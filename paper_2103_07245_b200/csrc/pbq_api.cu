@@ -1158,6 +1158,36 @@ int pbq_xchg_reduce(pbq_ctx* ctx, int32_t rank, int32_t world, int64_t n2, int64
   return PBQ_OK;
 }
 
+int pbq_p2p_push(pbq_ctx* ctx, const double* src, int64_t n, double* const* dst_ptrs, int64_t slot, int32_t rank,
+                 int32_t world, uint32_t* const* cnt_ptrs, void* stream) {
+  if (!ctx || !src || !dst_ptrs || !cnt_ptrs) return PBQ_ERR_PARAM;
+  if (world < 1 || rank < 0 || rank >= world || n < 0) return fail(ctx, PBQ_ERR_PARAM, "p2p_push: bad arguments");
+  p2p_push_kernel<<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, n, dst_ptrs, slot, rank, world,
+                                                                                cnt_ptrs);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
+int pbq_p2p_sum(pbq_ctx* ctx, const double* slots, int64_t slot, int32_t world, int64_t n, double* out,
+                const uint32_t* cnt, uint32_t target, uint32_t* status, void* stream) {
+  if (!ctx || !slots || !out || !cnt || !status) return PBQ_ERR_PARAM;
+  if (world < 1 || n < 0) return fail(ctx, PBQ_ERR_PARAM, "p2p_sum: bad arguments");
+  p2p_sum_kernel<<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(slots, slot, world, n, out, cnt, target,
+                                                                               status);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
+int pbq_p2p_wait(pbq_ctx* ctx, const uint32_t* cnt, uint32_t target, uint32_t* status, void* stream) {
+  if (!ctx || !cnt || !status) return PBQ_ERR_PARAM;
+  p2p_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(cnt, target, status);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return PBQ_OK;
+}
+
 int pbq_xchg_wait(pbq_ctx* ctx, const uint32_t* done, uint32_t target, void* stream) {
   if (!ctx || !done) return PBQ_ERR_PARAM;
   xchg_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(done, target);

@@ -196,6 +196,26 @@ def xchg_wait(ctx, xchg, done_target):
         ctx.check(st, "xchg_wait")
 
 
+def p2p_push(ctx, src, n, dst_ptrs, slot, rank, world, cnt_ptrs):
+    with ctx.lock:
+        st = ctx.lib.pbq_p2p_push(ctx.handle, ptr(src), int(n), ptr(dst_ptrs), int(slot), int(rank), int(world),
+                                  ptr(cnt_ptrs), stream_ptr(src.device))
+        ctx.check(st, "p2p_push")
+
+
+def p2p_sum(ctx, slots, slot, world, n, out, cnt, target, status):
+    with ctx.lock:
+        st = ctx.lib.pbq_p2p_sum(ctx.handle, ptr(slots), int(slot), int(world), int(n), ptr(out), ptr(cnt),
+                                 ctypes.c_uint32(target), ptr(status), stream_ptr(out.device))
+        ctx.check(st, "p2p_sum")
+
+
+def p2p_wait(ctx, cnt, target, status):
+    with ctx.lock:
+        st = ctx.lib.pbq_p2p_wait(ctx.handle, ptr(cnt), ctypes.c_uint32(target), ptr(status), stream_ptr(cnt.device))
+        ctx.check(st, "p2p_wait")
+
+
 def xchg_expected_tiles(ctx, n2, n, S, rank, world):
     t = ctypes.c_uint32()
     ctx.check(ctx.lib.pbq_xchg_expected_tiles(n2, n, S, rank, world, ctypes.byref(t)), "xchg_expected_tiles")

@@ -64,17 +64,31 @@ class _XchgBuffers:
     (indexed by rank) — the arguments of pbq_gemm_tn_scatter /
     pbq_xchg_reduce / pbq_xchg_wait (include/pbq.h)."""
 
-    def __init__(self, rank, world, S, ldl, land, c, ctr):
+    def __init__(self, rank, world, S, ldl, land, c, ctr, gram):
         self.rank, self.world, self.S, self.ldl = rank, world, S, ldl
         self.land = land.view(world * S, ldl)
         self.C = c.view(world * S, ldl)
-        self.cnt, self.done, self.status = ctr[0:1], ctr[1:2], ctr[2:3]  # [tiles, done, status]
+        # counter block [AᵀX tiles, AᵀX done, status, Gram pushes, all-gather pushes]
+        self.cnt, self.done, self.status = ctr[0:1], ctr[1:2], ctr[2:3]
+        self.gram_cnt, self.ag_cnt = ctr[3:4], ctr[4:5]
+        # Gram allreduce landing: two halves (epoch parity) of `world` slots of
+        # np² doubles — a fast peer's next push lands in the other half
+        self.gram_land = gram
+        self.gram_slot = gram.numel() // (2 * world)
         self.land_ptrs = self.c_ptrs = self.cnt_ptrs = self.done_ptrs = None
 
-    def set_peers(self, land, c, cnt, done):
+    def set_peers(self, land, c, ctr, gram):
         dev = self.land.device
         mk = lambda v: torch.tensor([int(x) for x in v], dtype=torch.int64, device=dev)  # noqa: E731
-        self.land_ptrs, self.c_ptrs, self.cnt_ptrs, self.done_ptrs = mk(land), mk(c), mk(cnt), mk(done)
+        self.land_ptrs, self.c_ptrs = mk(land), mk(c)
+        self.cnt_ptrs, self.done_ptrs = mk(ctr), mk([x + 4 for x in ctr])
+        self.gram_cnt_ptrs, self.ag_cnt_ptrs = mk([x + 12 for x in ctr]), mk([x + 16 for x in ctr])
+        half = self.gram_slot * self.world * 8
+        self.gram_ptrs = (mk(gram), mk([x + half for x in gram]))
+
+
+def _gram_np(d):
+    return 32 * (-(-d // 32))
 
 
 class P2PExchange(_XchgBuffers):
@@ -90,16 +104,18 @@ class P2PExchange(_XchgBuffers):
         land = symm.empty(world * S * ldl, dtype=torch.float64, device=device)
         c = symm.empty(world * S * ldl, dtype=torch.float64, device=device)
         ctr = symm.empty(64, dtype=torch.int32, device=device)
+        gram = symm.empty(2 * world * _gram_np(d) ** 2, dtype=torch.float64, device=device)
         c.zero_()  # rows ≥ n2 of C stay zero (orth(C) runs on whole row slices)
         ctr.zero_()
-        super().__init__(rank, world, S, ldl, land, c, ctr)
-        handles = [symm.rendezvous(t, pg) for t in (land, c, ctr)]
+        super().__init__(rank, world, S, ldl, land, c, ctr, gram)
+        bufs = (land, c, ctr, gram)
+        handles = [symm.rendezvous(t, pg) for t in bufs]
         peers = []
-        for t, h in zip((land, c, ctr), handles):
+        for t, h in zip(bufs, handles):
             off = t.data_ptr() - int(h.buffer_ptrs[rank])
             peers.append([int(h.buffer_ptrs[p]) + off for p in range(world)])
-        self.set_peers(peers[0], peers[1], peers[2], [p + 4 for p in peers[2]])
-        self._keep = (land, c, ctr, handles)
+        self.set_peers(*peers)
+        self._keep = (bufs, handles)
         torch.cuda.synchronize(device)
         dist.barrier(group)  # every rank's counters are zero before any peer adds to them
 
@@ -115,10 +131,11 @@ def virtual_exchanges(n2, d, world, device):
         land = torch.full((world * S * ldl,), float("nan"), dtype=torch.float64, device=device)
         c = torch.zeros(world * S * ldl, dtype=torch.float64, device=device)
         ctr = torch.zeros(64, dtype=torch.int32, device=device)
-        xs.append(_XchgBuffers(r, world, S, ldl, land, c, ctr))
+        gram = torch.full((2 * world * _gram_np(d) ** 2,), float("nan"), dtype=torch.float64, device=device)
+        xs.append(_XchgBuffers(r, world, S, ldl, land, c, ctr, gram))
     for x in xs:
         x.set_peers([y.land.data_ptr() for y in xs], [y.C.data_ptr() for y in xs], [y.cnt.data_ptr() for y in xs],
-                    [y.done.data_ptr() for y in xs])
+                    [y.gram_land.data_ptr() for y in xs])
     return xs
 
 
@@ -154,6 +171,37 @@ class CudaBackend:
     # -- fused AᵀX exchange over peer memory ----------------------------------
     def xchg_init(self, n2, d, group):
         return P2PExchange(n2, d, self.device, group)
+
+    def p2p_allreduce(self, xchg, g, epoch):
+        """g (the np×np Gram) ← Σ over ranks, by pushes into every rank's slot
+        and a slot-ordered sum (call ``epoch`` ≥ 1 of this buffer set)."""
+        self.p2p_allreduce_push(xchg, g, epoch)
+        self.p2p_allreduce_sum(xchg, g, epoch)
+
+    def p2p_allreduce_push(self, xchg, g, epoch):
+        n = g.numel()
+        if n > xchg.gram_slot:
+            raise _exc.ParameterError("p2p allreduce: buffer larger than the Gram slot")
+        _dev.p2p_push(self.ctx, g, n, xchg.gram_ptrs[epoch & 1], xchg.gram_slot, xchg.rank, xchg.world,
+                      xchg.gram_cnt_ptrs)
+
+    def p2p_allreduce_sum(self, xchg, g, epoch):
+        slots = xchg.gram_land[(epoch & 1) * xchg.world * xchg.gram_slot:]
+        _dev.p2p_sum(self.ctx, slots, xchg.gram_slot, xchg.world, g.numel(), g, xchg.gram_cnt,
+                     epoch * 64 * xchg.world, xchg.status)
+
+    def p2p_allgather_rows(self, xchg, epoch):
+        """Every rank's S-row slice of xchg.C into every rank's C."""
+        self.p2p_allgather_push(xchg)
+        self.p2p_allgather_wait(xchg, epoch)
+
+    def p2p_allgather_push(self, xchg):
+        slot = xchg.S * xchg.ldl
+        mine = xchg.C[xchg.rank * xchg.S:(xchg.rank + 1) * xchg.S]
+        _dev.p2p_push(self.ctx, mine, slot, xchg.c_ptrs, slot, xchg.rank, xchg.world, xchg.ag_cnt_ptrs)
+
+    def p2p_allgather_wait(self, xchg, epoch):
+        _dev.p2p_wait(self.ctx, xchg.ag_cnt, epoch * 64 * xchg.world, xchg.status)
 
     def xchg_at_x(self, xchg, a, x, n2, epoch, nonfinite=None):
         """xchg.C[:n2] = Σ_g A_gᵀ·X_g on every rank: scatter GEMM, slice
@@ -223,7 +271,9 @@ class DistributedPbpQlp:
             raise _exc.ParameterError("this backend has no peer-memory exchange")
         self.exchange = exchange
         self.xchg = be.xchg_init(self.n2, self.d, group) if exchange == "p2p" else None
-        self.epoch = 0
+        self.epoch = 0    # AᵀX exchanges
+        self.ep_gram = 0  # Gram allreduces (p2p)
+        self.ep_ag = 0    # all-gathers of orth(C) slices (p2p)
         # AᵀX partial → allreduced → P̄ (in place).  G·s rows (s = ⌈n2/G⌉, for
         # p2p rounded to the 128-row tile) so that orth(C) can run on equal
         # row slices; rows ≥ n2 stay zero.
@@ -313,6 +363,15 @@ class DistributedPbpQlp:
         be.gemm_nn(self.Q, be.contiguous(qhat), self.Qtmp)
         self.Q.copy_(self.Qtmp)
 
+    def _sum_gram(self, g):
+        """Allreduce(sum) of a d×d Gram: NCCL, or pushes into the peers' slots
+        and a slot-ordered sum over symmetric memory (exchange="p2p")."""
+        if self.xchg is None:
+            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
+            return
+        self.ep_gram += 1
+        self.be.p2p_allreduce(self.xchg, g, self.ep_gram)
+
     def _note_guard(self, st):
         """OR the call's guard flag into flags[-1] on the device (no sync)."""
         fb = self.flags[-1:]
@@ -331,9 +390,9 @@ class DistributedPbpQlp:
             return self._tsqr_(flag)
         be = self.be
         be.cholqr2_dist(0, self.Q, self.R, st, flag)
-        dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
+        self._sum_gram(st["G"])
         be.cholqr2_dist(1, self.Q, self.R, st, flag)
-        dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
+        self._sum_gram(st["G"])
         be.cholqr2_dist(2, self.Q, self.R, st, flag)
         self._note_guard(st)
 
@@ -352,16 +411,19 @@ class DistributedPbpQlp:
         s0 = self.rank * self.slice_rows
         mine = self.Cbuf[s0:s0 + self.slice_rows]
         be.cholqr2_dist(0, mine, self.Rs, st, flag)
-        dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
+        self._sum_gram(st["G"])
         be.cholqr2_dist(1, mine, self.Rs, st, flag)
-        dist.all_reduce(st["G"], op=dist.ReduceOp.SUM, group=self.group)
+        self._sum_gram(st["G"])
         be.cholqr2_dist(2, mine, self.Rs, st, flag)
         self._note_guard(st)  # a fired guard left the slices untouched; finish() re-runs
         buf = self.Cbuf
         ld = buf.stride(0)
         whole = buf.as_strided((buf.shape[0], ld), (ld, 1))  # whole rows incl. the even-ld pad column
         part = whole[s0:s0 + self.slice_rows]
-        if dist.get_backend(self.group) == "nccl":
+        if self.xchg is not None:
+            self.ep_ag += 1
+            self.be.p2p_allgather_rows(self.xchg, self.ep_ag)  # Cbuf is the symmetric C: peer stores
+        elif dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(whole, part, group=self.group)  # in place: part is rank's chunk
         else:
             parts = [torch.empty_like(part) for _ in range(self.world)]

@@ -131,3 +131,44 @@ def test_exchange_wait_times_out_instead_of_hanging(cuda):
     torch.cuda.synchronize()
     assert 15 < time.time() - t0 < 60
     assert int(x.status.item()) == 1
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_virtual_rank_small_collectives(cuda, world):
+    """The Gram allreduce (push into every rank's slot, slot-ordered sum; two
+    epochs, i.e. both halves of the double-buffered slots) and the all-gather
+    of the C row slices, on virtual ranks in emulation order."""
+    from paper_2103_07245_b200.distributed import CudaBackend, virtual_exchanges
+
+    be = CudaBackend(cuda)
+    n2, d = 1000, 100
+    xs = virtual_exchanges(n2, d, world, cuda)
+    npad = 128  # the Gram's padded size for d = 100
+    rng = np.random.default_rng(world)
+    for epoch in (1, 2, 3):
+        gs = [torch.from_numpy(rng.standard_normal((npad, npad))).to(cuda) for _ in range(world)]
+        ref = sum(g.cpu().numpy() for g in gs)
+        for r in range(world):
+            be.p2p_allreduce_push(xs[r], gs[r], epoch)
+        for r in range(world):
+            be.p2p_allreduce_sum(xs[r], gs[r], epoch)
+        torch.cuda.synchronize()
+        out = [g.cpu().numpy() for g in gs]
+        for r in range(world):
+            assert np.array_equal(out[r], out[0])
+        assert np.abs(out[0] - ref).max() <= 1e-12 * np.abs(ref).max()
+    for epoch in (1, 2):
+        slices = []
+        for r in range(world):
+            sl = torch.from_numpy(rng.standard_normal((xs[r].S, xs[r].ldl))).to(cuda)
+            xs[r].C[r * xs[r].S:(r + 1) * xs[r].S].copy_(sl)
+            slices.append(sl.cpu().numpy())
+        for r in range(world):
+            be.p2p_allgather_push(xs[r])
+        for r in range(world):
+            be.p2p_allgather_wait(xs[r], epoch)
+        torch.cuda.synchronize()
+        full = np.vstack(slices)
+        for r in range(world):
+            assert np.array_equal(xs[r].C.cpu().numpy(), full)
+    assert all(int(x.status.item()) == 0 for x in xs)

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
         if (long(cg + 1) * p.total_iters / NG >= tile_end) break;
       }
     }
-    if (RESID) {
+    if constexpr (RESID) {
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const long r = m0 + wm0 + mt * 8 + g;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
         }
       }
       continue;
-    }
+    } else {
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       const long r = m0 + wm0 + mt * 8 + g;
@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
           dst[0] = v0;
         }
       }
+    }
     }
   }
   if (CHECK && saw_nonfinite) atomicOr(p.nonfinite, 1);

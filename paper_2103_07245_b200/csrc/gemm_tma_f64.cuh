@@ -349,7 +349,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
         if (long(cg + 1) * p.total_iters / NG >= tile_end) break;
       }
     }
-    if (RESID) {
+    if constexpr (RESID) {
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const long r = m0 + out_row(mt);

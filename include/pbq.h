@@ -120,6 +120,10 @@ typedef struct {
    * the sketch used (it is not regenerated). */
   const double* c_init;
   int64_t ldc_init;
+  /* Optional device pointer to {seed_lo, seed_hi}: when set, the sketch reads
+   * its key from device memory at run time instead of seed_lo/seed_hi, so a
+   * CUDA graph captured once can be replayed with new seeds. */
+  const uint64_t* seed_dev;
 } pbq_problem;
 
 typedef struct {

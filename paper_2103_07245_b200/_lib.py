@@ -78,6 +78,7 @@ class PbqProblem(ctypes.Structure):
         ("seed_lo", c_u64), ("seed_hi", c_u64),
         ("reorthonormalize", c_i32), ("check_finite", c_i32),
         ("c_init", c_p), ("ldc_init", c_i64),
+        ("seed_dev", c_p),
     ]
 
 

@@ -235,6 +235,7 @@ class PbpQlpPlan:
             raise _exc.DimensionError(f"plan is for {(self.n1, self.n2)}, got {tuple(host.shape)}")
         seed = check_seed(seed)
         self.seed = seed
+        self.prob.seed_dev = None
         if self.PHI is None:
             raise _exc.ParameterError("plan was built for an explicit sketch")
         if getattr(self, "A_dev", None) is None:
@@ -274,8 +275,9 @@ class PbpQlpPlan:
         self._streamed = True
         return A
 
-    def run(self, A, seed=0, phi=None):
+    def run(self, A, seed=0, phi=None, _seed_dev=None):
         """Enqueue one factorization of the kernel-ready device matrix ``A``."""
+        self.prob.seed_dev = _seed_dev  # set only while ``capture`` records the graph
         if tuple(A.shape) != (self.n1, self.n2):
             raise _exc.DimensionError(f"plan is for {(self.n1, self.n2)}, got {tuple(A.shape)}")
         seed = check_seed(seed)
@@ -296,6 +298,42 @@ class PbpQlpPlan:
             st = self.ctx.lib.pbq_pbp_qlp(self.ctx.handle, ctypes.byref(self.prob), ctypes.byref(self.out),
                                           _dev.ptr(self.ws), self.ws_bytes, _dev.stream_ptr(self.device))
             self.ctx.check(st, "pbp_qlp")
+
+    # -- CUDA graph of the whole pipeline -----------------------------------
+    def capture(self, A):
+        """Capture one factorization of the device matrix ``A`` (seeded mode)
+        into a CUDA graph; ``replay(seed)`` then re-runs all of it — sketch,
+        every pass and QR — with one graph launch.  The sketch reads its key
+        from device memory (``pbq_problem.seed_dev``), so each replay can use a
+        new seed; ``A`` and the outputs are the captured buffers."""
+        if self.PHI is None:
+            raise _exc.ParameterError("capture needs a plan with a seeded sketch")
+        dev = self.device
+        self.seed_dev = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.run(A, seed=0)  # warm: tables, function attributes, lazy module loads
+        launches0 = self.ctx.launch_count
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            self.run(A, seed=0, _seed_dev=self.seed_dev.data_ptr())
+        self.prob.seed_dev = None
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.graph_launches = self.ctx.launch_count - launches0  # kernels per replay
+        self.graph, self.graph_A = graph, A
+        return graph
+
+    def replay(self, seed=0):
+        """Launch the captured factorization with sketch seed ``seed``."""
+        seed = check_seed(seed)
+        self.seed = seed
+        lo, hi = seed & ((1 << 64) - 1), seed >> 64
+        to_i64 = lambda v: v - (1 << 64) if v >= (1 << 63) else v  # noqa: E731  (same 64 bits)
+        self.seed_dev[0].fill_(to_i64(lo))
+        self.seed_dev[1].fill_(to_i64(hi))
+        self.phi_in = None
+        self._streamed = False
+        self.graph.replay()
 
     def finish(self, stacklevel=3):
         fl = self.flags.cpu().tolist()  # the one device→host synchronisation

@@ -752,7 +752,8 @@ int sketch_tables(pbq_ctx* ctx) {
 }
 
 int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t k0, uint64_t k1, double* out,
-                  long ldo, int* error_flag, void* ws, size_t ws_bytes, cudaStream_t st) {
+                  long ldo, int* error_flag, void* ws, size_t ws_bytes, cudaStream_t st,
+                  const uint64_t* seed_dev = nullptr) {
   if (rows < 1 || cols < 1 || row_offset < 0) return fail(ctx, PBQ_ERR_DIM, "gaussian: bad shape");
   if (ldo < cols) return fail(ctx, PBQ_ERR_PARAM, "gaussian: ldo < cols");
   PBQ_TRY(sketch_tables(ctx));
@@ -760,6 +761,7 @@ int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t 
   Carve cv(ws, ws_bytes);
   SketchArgs a;
   a.k0 = k0; a.k1 = k1;
+  a.seed_dev = seed_dev;
   a.n_chunks = pl.n_chunks;
   a.first = row_offset * cols;
   a.count = rows * cols;
@@ -1428,7 +1430,8 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   } else {
     if (!phi) {
       PBQ_CUDA(ctx, cudaMemsetAsync(sk_err, 0, sizeof(int32_t), st));
-      PBQ_TRY(sketch_launch(ctx, n1, d, 0, pr->seed_lo, pr->seed_hi, o->phi, o->ldphi, sk_err, sc, scratch, st));
+      PBQ_TRY(sketch_launch(ctx, n1, d, 0, pr->seed_lo, pr->seed_hi, o->phi, o->ldphi, sk_err, sc, scratch, st,
+                            pr->seed_dev));
       phi = o->phi;
       ldphi = o->ldphi;
     }

@@ -139,6 +139,7 @@ __device__ uint64_t zig_resolve(const ZigTables& t, uint64_t p, uint64_t k0, uin
 
 struct SketchArgs {
   uint64_t k0, k1;
+  const uint64_t* seed_dev;  // when set, the key {k0, k1} is read from device memory (CUDA-graph replays)
   long n_chunks;
   long first;  // global index of the first normal to emit (row_offset·cols)
   long count;  // normals to emit (rows·cols)
@@ -218,6 +219,10 @@ __device__ __forceinline__ void sk_walk(uint64_t s, uint64_t cend, const SkWarpS
 }
 
 __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k1(SketchArgs a) {
+  if (a.seed_dev) {
+    a.k0 = __ldg(a.seed_dev);
+    a.k1 = __ldg(a.seed_dev + 1);
+  }
   __shared__ SkWarpSmem sw[PBQ_SK_WARPS];
   __shared__ double stage[PBQ_SK_WARPS][32 * 33];  // position-indexed values, row ℓ = lane ℓ's 32 positions (padded)
   __shared__ ZigTables zt;
@@ -358,6 +363,10 @@ __global__ void __launch_bounds__(1024) sketch_k2(SketchArgs a) {
 }
 
 __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k3(SketchArgs a) {
+  if (a.seed_dev) {
+    a.k0 = __ldg(a.seed_dev);
+    a.k1 = __ldg(a.seed_dev + 1);
+  }
   __shared__ SkWarpSmem sw[PBQ_SK_WARPS];
   __shared__ double buf[PBQ_SK_WARPS][32 * 33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

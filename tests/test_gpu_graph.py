@@ -1,0 +1,55 @@
+"""The whole PbP-QLP pipeline as one CUDA graph (PbpQlpPlan.capture / replay):
+every kernel of a factorization — sketch, passes, QR chains, second stage —
+recorded once and replayed with new seeds (the sketch reads its key from
+device memory, pbq_problem.seed_dev).  A replay must give the same bits as
+the stream-ordered run with the same seed, and the oracle's factors."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n1,n2,d,q", [(600, 400, 48, 1), (1000, 1000, 40, 0), (2000, 1500, 130, 2)])
+def test_graph_replay_matches_stream_run(cuda, n1, n2, d, q):
+    from paper_2103_07245_b200 import PbpQlpPlan
+    from paper_2103_07245_b200 import device as D
+
+    rng = np.random.default_rng(n1 + d)
+    a_np = rng.standard_normal((n1, 50)) @ rng.standard_normal((50, n2)) + 1e-3 * rng.standard_normal((n1, n2))
+    a = D.as_kernel_operand(torch.from_numpy(a_np).to(cuda))
+    plan = PbpQlpPlan(n1, n2, d, q, device=cuda)
+    ref = {}
+    for seed in (3, 2**70 + 5):
+        plan.run(a, seed=seed)
+        plan.finish()
+        ref[seed] = [t.clone() for t in (plan.Q, plan.L, plan.P, plan.R, plan.PHI)]
+    plan.capture(a)
+    assert plan.graph_launches > 10
+    for seed in (3, 2**70 + 5, 3):
+        plan.replay(seed)
+        plan.finish()
+        for got, want in zip((plan.Q, plan.L, plan.P, plan.R, plan.PHI), ref[seed]):
+            assert torch.equal(got, want)
+    # stream-ordered runs after the capture read their own seed again
+    plan.run(a, seed=2**70 + 5)
+    plan.finish()
+    assert torch.equal(plan.PHI, ref[2**70 + 5][4])
+
+
+def test_graph_replay_matches_oracle(cuda):
+    from oracle.pbp_qlp_oracle import column_relative_error, conditioning_tolerance, oracle_pbp_qlp
+    from paper_2103_07245_b200 import PbpQlpPlan
+    from paper_2103_07245_b200 import device as D
+
+    rng = np.random.default_rng(5)
+    a_np = rng.standard_normal((1500, 60)) @ rng.standard_normal((60, 700)) / 8 + 1e-3 * rng.standard_normal((1500, 700))
+    a = D.as_kernel_operand(torch.from_numpy(a_np).to(cuda))
+    plan = PbpQlpPlan(1500, 700, 48, 1, device=cuda)
+    plan.capture(a)
+    plan.replay(9)
+    plan.finish()
+    ref = oracle_pbp_qlp(a_np, 48, q=1, seed=9)
+    tol = conditioning_tolerance(ref["l"], strict=1e-10)
+    assert np.all(column_relative_error(plan.Q.cpu().numpy(), ref["q"]) <= tol)
+    assert np.all(column_relative_error(plan.P.cpu().numpy(), ref["p"]) <= tol)

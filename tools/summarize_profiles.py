@@ -70,6 +70,8 @@ def launch_shares(tag):
             key = "QR ×5 (Cholesky-QR2 chain; Householder early-exit)"
         elif name.startswith("sketch"):
             key = "sketch (Philox4x64 + ziggurat, k1/k2/k3)"
+        elif name == "input-prep":
+            key = "torch kernels (seed writes of a graph replay)"
         else:
             key = "transposes + status merge"
         groups.setdefault(key, [0.0, 0])

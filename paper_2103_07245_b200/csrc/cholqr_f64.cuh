@@ -95,6 +95,7 @@ struct CqArgs {
   int rout_full;    // 1: write Rout over the padded np×np (an intermediate product)
   int route_final;  // 1: last factorization of the shifted route (stats[3] counts it)
   int* fail_stats;  // optional: stats[1] counts hand-overs to Householder (also from intermediate passes)
+  int chol_1warp;   // 1: diagonal blocks on one warp (cq_chol_inv32_warp) instead of two
 };
 
 #define CQ_MARK(slot)                                                                  \
@@ -225,6 +226,77 @@ __device__ __noinline__ bool cq_chol_inv32_warp(double* S, double* Xs, double* r
     Xs[lane * CQ_LD + i] = w[i];
   }
   return ok;
+}
+
+// The same factorization on two warps: warp 0 eliminates G (the R part),
+// warp 1 the identity (the R⁻ᵀ part).  The per-pivot chain of warp 0
+// (shuffle → rsqrt → mul → fma of the next pivot) stays as above, but each
+// warp now issues half of the step's FP64 updates — the single-warp version
+// is issue-bound (64 DFMA of 2 cycles each per pivot), not latency-bound.
+// Warp 0 publishes row k of R and 1/r_kk in slot k mod 2 and signals with a
+// named-barrier arrive on FULL[k mod 2] (ids 1, 2); warp 1 consumes it and
+// frees the slot with EMPTY[k mod 2] (ids 3, 4), which warp 0 waits for two
+// pivots later.  One barrier id per slot and direction: a warp never arrives
+// twice at a barrier whose previous phase is still open (arrive counts
+// threads, so a second arrival of warp 0 would complete it without warp 1).
+// Called by warps 0 and 1 of the CTA; the result of warp 0 is the one to use.
+constexpr int CQ_RB2 = 36;  // doubles per slot: row k (32), 1/r_kk, padding (16-byte aligned)
+__device__ __forceinline__ void cq_bar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void cq_bar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+
+__device__ __noinline__ bool cq_chol_inv32_2warp(double* S, double* Xs, double* rowbuf /*2·CQ_RB2, 16-byte aligned*/) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) == 0) {
+    double v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = S[i * CQ_LD + lane];
+    bool ok = true;
+    double piv = v[0];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double dk = __shfl_sync(0xffffffffu, piv, k);
+      ok = ok && (dk > 0.0);
+      const double inv = fast_rsqrt(dk);
+      const double rkj = (lane >= k) ? v[k] * inv : 0.0;
+      v[k] = rkj;
+      if (k + 1 < 32) piv = fma(-rkj, rkj, v[k + 1]);  // meaningful on lane k+1
+      if (k >= 2) cq_bar_sync(3 + (k & 1));             // warp 1 has consumed the slot of pivot k−2
+      double* rb = rowbuf + (k & 1) * CQ_RB2;
+      rb[lane] = rkj;
+      if (lane == 0) rb[32] = inv;
+      cq_bar_arrive(1 + (k & 1));
+      __syncwarp();
+#pragma unroll
+      for (int i2 = (k + 1) & ~1; i2 < 32; i2 += 2) {
+        const double2 r2 = *reinterpret_cast<const double2*>(rb + i2);
+        if (i2 > k) v[i2] = fma(-r2.x, rkj, v[i2]);
+        if (i2 + 1 > k && i2 + 1 < 32) v[i2 + 1] = fma(-r2.y, rkj, v[i2 + 1]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) S[i * CQ_LD + lane] = (i <= lane) ? v[i] : 0.0;
+    return ok;
+  }
+  double w[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) w[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    cq_bar_sync(1 + (k & 1));
+    const double* rb = rowbuf + (k & 1) * CQ_RB2;
+    const double bkj = w[k] * rb[32];
+    w[k] = bkj;
+#pragma unroll
+    for (int i2 = (k + 1) & ~1; i2 < 32; i2 += 2) {
+      const double2 r2 = *reinterpret_cast<const double2*>(rb + i2);
+      if (i2 > k) w[i2] = fma(-r2.x, bkj, w[i2]);
+      if (i2 + 1 > k && i2 + 1 < 32) w[i2 + 1] = fma(-r2.y, bkj, w[i2 + 1]);
+    }
+    if (k + 2 < 32) cq_bar_arrive(3 + (k & 1));  // the slot is free for pivot k+2
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Xs[lane * CQ_LD + i] = w[i];
+  return true;
 }
 
 __device__ __forceinline__ double cq_split(int r, int c, double x) { return c > r ? x : (c == r ? 0.5 * x : 0.0); }
@@ -361,7 +433,7 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
   double* sC = pairs + 2 * CQ_BLK;
   double* sT = pairs + 3 * CQ_BLK;
   __shared__ int s_ok;
-  __shared__ __align__(16) double s_rowbuf[64];
+  __shared__ __align__(16) double s_rowbuf[2 * CQ_RB2];
   if (p.fallback && __ldcg(p.fallback) != 0) return;  // uniform: written by an earlier launch
   if (p.route && __ldcg(p.route) == 0) return;
   // a failed factorization: pass 1 of the extended chain asks for the shifted
@@ -522,8 +594,13 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
       if (tid < 32 && k * 32 + tid < p.n) sKK[tid * CQ_LD + tid] += shift;
       __syncthreads();
     }
-    if (warp == 0) {
-      const bool ok = cq_chol_inv32_warp(sKK, sKI, s_rowbuf);
+    if (p.chol_1warp) {  // the single-warp variant (A/B measurements)
+      if (warp == 0) {
+        const bool ok = cq_chol_inv32_warp(sKK, sKI, s_rowbuf);
+        if (tid == 0) s_ok = ok;
+      }
+    } else if (warp < 2) {
+      const bool ok = cq_chol_inv32_2warp(sKK, sKI, s_rowbuf);
       if (tid == 0) s_ok = ok;
     }
     __syncthreads();

@@ -423,6 +423,7 @@ __device__ __forceinline__ void cq_inverse_item(const CqArgs& p, int k, int i, d
 }
 
 __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) {
+  pdl_trigger();  // a programmatically launched successor may start its prologue
   extern __shared__ __align__(16) double sm[];
   double* sKK = sm;           // R_kk
   double* sKI = sm + CQ_BLK;  // R_kk⁻¹

@@ -37,7 +37,7 @@ struct GemmArgs {
   int tiles_m, tiles_n, k_iters;
   long total_iters;
   double* partials;  // grid × (BM·BN) doubles
-  int* flags;        // grid ints, zeroed before the launch
+  int* flags;        // grid ints, zero at launch; each consumed flag is reset by its reader
   int* nonfinite;    // CHECK only: OR-flag set if any element of A is Inf/NaN
   // SPLIT mode (Gram matrices of the Cholesky-QR path): unit u = (tile u/split,
   // k-slice u%split) writes its partial tile to partials[u] (plain row-major
@@ -135,6 +135,8 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
   constexpr int KSTEPS = BK / 4;
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  pdl_wait();
+  pdl_trigger();
   if (p.skip && __ldcg(p.skip) != 0) return;
   if (p.run_if && __ldcg(p.run_if) == 0) return;
 
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
         if (tid == 0) {
           while (ld_acquire(p.flags + c) == 0) {
           }
+          p.flags[c] = 0;  // consumed: the context's flag array is left zeroed for the next launch
         }
         __syncthreads();
         const double* slot = p.partials + size_t(c) * (BM * BN);

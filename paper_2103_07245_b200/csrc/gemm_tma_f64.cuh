@@ -70,6 +70,14 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
   const GemmArgs& p = pa.g;
   extern __shared__ __align__(16) unsigned char smem_raw[];  // ring aligned to 1024 below (an __align__(1024) here would pad the static shared memory of every kernel in the library)
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&pa.ta);
+    tma_prefetch_desc(&pa.tb);
+  }
+  // launched with programmatic serialization: everything above overlaps the
+  // predecessor's tail; nothing it wrote is read before this point
+  pdl_wait();
+  pdl_trigger();
   if (p.skip && __ldcg(p.skip) != 0) return;
   if (p.run_if && __ldcg(p.run_if) == 0) return;
 
@@ -85,8 +93,6 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
   const uint32_t ring = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const unsigned char* ring_gen = smem_raw + (ring - smem_u32(smem_raw));
   if (tid == 0) {
-    tma_prefetch_desc(&pa.ta);
-    tma_prefetch_desc(&pa.tb);
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -336,6 +342,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
         if (tid == 0) {
           while (ld_acquire(p.flags + c) == 0) {
           }
+          p.flags[c] = 0;  // consumed: the context's flag array is left zeroed for the next launch
         }
         __syncthreads();
         const double* slot = p.partials + size_t(c) * (BM * BN);

@@ -45,6 +45,7 @@ struct pbq_ctx {
   int qr_method = PBQ_QR_AUTO;
   int* cq_stats = nullptr;                    // debug: [Cholesky-QR2 done, fallbacks]
   std::unordered_map<const void*, int> smem_attr;  // max dynamic smem already set per kernel (one driver call each)
+  int* gemm_flags = nullptr;  // stream-K partial-ready flags (sms ints), zero between GEMM launches: readers reset them
   char err[512] = {0};
 };
 
@@ -255,10 +256,25 @@ int gemm_dispatch(pbq_ctx* ctx, const GemmArgs& a, bool trans, int bn, int mode,
     args[0] = const_cast<GemmArgs*>(&a);
   }
   PBQ_CUDA(ctx, ensure_smem(ctx, fn, smem));
-  if (coop)
+  if (coop) {
     PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(fn, grid, dim3(threads), args, smem, st));
-  else
-    PBQ_CUDA(ctx, cudaLaunchKernel(fn, grid, dim3(threads), args, smem, st));
+  } else {
+    // programmatic dependent launch: the GEMM's CTAs may start (prologue,
+    // tensor-map prefetch) while the previous kernel drains; the kernel's
+    // griddepcontrol.wait orders every access to that kernel's results
+    static const bool no_pdl = getenv("PBQ_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = no_pdl ? 0 : 1;
+    PBQ_CUDA(ctx, cudaLaunchKernelExC(&cfg, fn, args));
+  }
   ctx->launches += 1;
   return PBQ_OK;
 }
@@ -328,7 +344,8 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   a.alpha = alpha; a.beta = beta;
   a.tiles_m = pl.tiles_m; a.tiles_n = pl.tiles_n; a.k_iters = pl.k_iters; a.total_iters = pl.total;
   a.partials = cv.take<double>(size_t(pl.grid) * pl.bm * pl.bn);
-  a.flags = cv.take<int>(pl.grid);
+  cv.take<int>(pl.grid);  // (workspace layout unchanged; the flags are the context's)
+  a.flags = ctx->gemm_flags;
   a.nonfinite = nonfinite;
   a.split = 0; a.sym = 0; a.units = 0;
   a.skip = skip;
@@ -341,7 +358,6 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
     a.xs_land = xs->land; a.xs_cnt = xs->cnt; a.xs_S = xs->S; a.xs_ldl = xs->ldl; a.xs_rank = xs->rank;
   }
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gemm: workspace too small (%zu < %zu)", ws_bytes, cv.off);
-  PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
   ProfScope ps(ctx->prof, st, 0);
   return gemm_dispatch(ctx, a, TRANS, pl.bn, GEMM_PLAIN, dim3(pl.grid), false, st);
 }
@@ -797,6 +813,7 @@ int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t 
 // lower triangle of srcᵀ and zeros the rest (L = tril(R̃ᵀ)).
 __global__ void transpose_kernel(long rows, long cols, const double* __restrict__ src, long lds,
                                  double* __restrict__ dst, long ldd, int lower) {
+  pdl_trigger();
   __shared__ double tile[32][33];
   const long bx = long(blockIdx.x) * 32, by = long(blockIdx.y) * 32;  // bx: src column block, by: src row block
   for (int j = threadIdx.y; j < 32; j += 8) {
@@ -1036,9 +1053,9 @@ int resid_launch(pbq_ctx* ctx, long n1, long n2, long k, const double* A, long l
   a.group = pl.group;
   Carve gc(gws, gws_bytes);
   a.partials = gc.take<double>(size_t(pl.grid) * pl.bm * pl.bn);
-  a.flags = gc.take<int>(pl.grid);
+  gc.take<int>(pl.grid);
+  a.flags = ctx->gemm_flags;
   a.ref = A; a.ldref = lda; a.sums = sums;
-  PBQ_CUDA(ctx, cudaMemsetAsync(a.flags, 0, sizeof(int) * pl.grid, st));
   {
     ProfScope ps(ctx->prof, st, 0);
     PBQ_TRY(gemm_dispatch(ctx, a, false, pl.bn, GEMM_RESID, dim3(pl.grid), false, st));
@@ -1072,11 +1089,22 @@ int pbq_ctx_create(int device, pbq_ctx** out) {
     return PBQ_ERR_CUDA;
   }
   ctx->smem_optin = size_t(optin);
+  // the GEMMs' stream-K flags live in the context (not in the per-call
+  // workspace), start zeroed and are reset by their readers, so no launch
+  // needs a memset in front of it (which would also break the programmatic
+  // launch chain); GEMMs of one context run on one stream at a time
+  if (cudaMalloc(&ctx->gemm_flags, sizeof(int) * size_t(std::max(ctx->sms, 1))) != cudaSuccess ||
+      cudaMemset(ctx->gemm_flags, 0, sizeof(int) * size_t(std::max(ctx->sms, 1))) != cudaSuccess) {
+    cudaFree(ctx->gemm_flags);
+    delete ctx;
+    return PBQ_ERR_CUDA;
+  }
   *out = ctx;
   return PBQ_OK;
 }
 
 int pbq_ctx_destroy(pbq_ctx* ctx) {
+  if (ctx && ctx->gemm_flags) cudaFree(ctx->gemm_flags);
   if (ctx && ctx->prof.ev) {
     for (int i = 0; i < 2 * ctx->prof.cap; ++i) cudaEventDestroy(ctx->prof.ev[i]);
     delete[] ctx->prof.ev;

@@ -754,6 +754,7 @@ __device__ void qr_panel_householder(const QrArgs& p, const QrSmem& s, double* P
 
 // ================================ the kernel ================================
 __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
+  pdl_trigger();  // a programmatically launched successor may start its prologue
   extern __shared__ __align__(16) double qsm[];
   if (p.run_if && __ldcg(p.run_if) == 0) return;  // uniform across the grid
   const long m = p.m, n = p.n;

@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(1024) sketch_k2(SketchArgs a) {
 }
 
 __global__ void __launch_bounds__(PBQ_SK_THREADS) sketch_k3(SketchArgs a) {
+  pdl_trigger();  // a programmatically launched successor may start its prologue
   if (a.seed_dev) {
     a.k0 = __ldg(a.seed_dev);
     a.k1 = __ldg(a.seed_dev + 1);

@@ -405,7 +405,7 @@ size_t qr_ws_bytes(const QrPlan& pl, long n) {
 }
 
 int hh_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int want_q, int32_t* rank_flag,
-              void* ws, size_t ws_bytes, cudaStream_t st, const int* run_if) {
+              void* ws, size_t ws_bytes, cudaStream_t st, const int* run_if, unsigned int* zeroed_counter = nullptr) {
   QrPlan pl;
   PBQ_TRY(qr_plan(ctx, m, n, pl));
   if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "qr: leading dimension too small");
@@ -422,6 +422,7 @@ int hh_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   a.ybuf = cv.take<double>(size_t(QR_NB) * qr_ldy(n));
   a.tall = cv.take<double>(size_t(ceil_div(n, QR_NB)) * 1024);
   a.counter = cv.take<unsigned int>(1);
+  if (zeroed_counter) a.counter = zeroed_counter;  // the caller's control block, already zeroed (no memset node)
   a.error = ctx->qr_error ? ctx->qr_error : cv.take<int>(1);
   a.rank_flag = rank_flag;
   a.fallbacks = ctx->qr_fallbacks;
@@ -429,7 +430,7 @@ int hh_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   a.bar_wait_ns = ctx->qr_bar_wait_ns;
   a.run_if = run_if;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
-  PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
+  if (!zeroed_counter) PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
   PBQ_CUDA(ctx, ensure_smem(ctx, reinterpret_cast<const void*>(&qr_tall_kernel), pl.smem));
   void* args[] = {&a};
   ProfScope ps(ctx->prof, st, 1);
@@ -552,7 +553,8 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   Carve cv(ws, ws_bytes);
   // ctl: [0] fallback (stops the CholQR2 path), [1] [2] [16] [17] [18] grid-barrier
   // counters, [4:6] [20:22] [22:24] max|G − I| slots, [10] shifted route running,
-  // [12] Householder requested (extended chain)
+  // [12] Householder requested (extended chain), [32..35] Gram slice-sum barriers,
+  // [48] the Householder kernel's grid-barrier counter
   int* ctl = cv.take<int>(64);
   double* X1 = cv.take<double>(sq);
   double* X2 = cv.take<double>(sq);
@@ -644,7 +646,8 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
     CQ_DEBUG_SYNC("route 10");
   }
   // Householder fallback (returns immediately unless a factorization failed)
-  return hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, ext ? hh_req : fallback);
+  return hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, ext ? hh_req : fallback,
+                   reinterpret_cast<unsigned int*>(ctl + 48));
 }
 
 // ------------------------------------------- distributed Cholesky-QR2 ----
@@ -1066,6 +1069,15 @@ int resid_launch(pbq_ctx* ctx, long n1, long n2, long k, const double* A, long l
   return PBQ_OK;
 }
 
+// zeroes the pipeline's status words in one launch (instead of three memset
+// nodes in front of the sketch)
+__global__ void pipeline_init_kernel(int32_t* nonfinite, int32_t* rank_flags, int n_rank, int32_t* sk_err) {
+  const int t = threadIdx.x;
+  if (t == 0 && nonfinite) *nonfinite = 0;
+  if (t == 1 && sk_err) *sk_err = 0;
+  for (int i = t; i < n_rank; i += blockDim.x) rank_flags[i] = 0;
+}
+
 __global__ void merge_flag_kernel(int32_t* status, const int32_t* sketch_err) {
   if (*sketch_err) *status |= 2;
 }
@@ -1449,8 +1461,10 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   void* sc = cv.take<char>(scratch);
   const int32_t check = pr->check_finite ? 1 : 0;
 
-  if (!pr->c_init) PBQ_CUDA(ctx, cudaMemsetAsync(o->nonfinite, 0, sizeof(int32_t), st));
-  PBQ_CUDA(ctx, cudaMemsetAsync(o->rank_flags, 0, sizeof(int32_t) * (2 * q + 1), st));
+  pipeline_init_kernel<<<1, 64, 0, st>>>(pr->c_init ? nullptr : o->nonfinite, o->rank_flags, int(2 * q + 1),
+                                         (!pr->phi && !pr->c_init) ? sk_err : nullptr);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
   const double* phi = pr->phi;
   long ldphi = pr->ldphi;
   if (pr->c_init) {
@@ -1459,7 +1473,6 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
                                     d * sizeof(double), n2, cudaMemcpyDeviceToDevice, st));
   } else {
     if (!phi) {
-      PBQ_CUDA(ctx, cudaMemsetAsync(sk_err, 0, sizeof(int32_t), st));
       PBQ_TRY(sketch_launch(ctx, n1, d, 0, pr->seed_lo, pr->seed_hi, o->phi, o->ldphi, sk_err, sc, scratch, st,
                             pr->seed_dev));
       phi = o->phi;

@@ -48,7 +48,7 @@ def launch_shares(tag):
             args = [x.strip() for x in n[n.index("<") + 1:n.index(">")].split(",")]
             return "gemm_split" if args[-2] in ("1", "true") else "gemm"
         for k in ("cholqr_factor_kernel", "cholqr_gram_reduce", "qr_tall_kernel", "sketch_k1", "sketch_k2",
-                  "sketch_k3", "transpose_kernel", "merge_flag_kernel"):
+                  "sketch_k3", "transpose_kernel", "merge_flag_kernel", "pipeline_init_kernel"):
             if k in n:
                 return k
         return "input-prep"
@@ -73,7 +73,7 @@ def launch_shares(tag):
         elif name == "input-prep":
             key = "torch kernels (seed writes of a graph replay)"
         else:
-            key = "transposes + status merge"
+            key = "transposes + status init/merge"
         groups.setdefault(key, [0.0, 0])
         groups[key][0] += us
         groups[key][1] += 1

@@ -72,7 +72,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, a, d, q, seed, outdir):
+def _worker(rank, world, port, a, d, q, seed, outdir, reps=2):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -91,11 +91,16 @@ def _worker(rank, world, port, a, d, q, seed, outdir):
         rows = shard_rows(n1, world)
         run = DistributedPbpQlp(n1, n2, d, q, rows, device=dev, exchange="p2p")
         a_loc = D.as_kernel_operand(torch.from_numpy(np.ascontiguousarray(a[rows[rank]:rows[rank + 1]])).to(dev))
-        for s in (seed, seed):  # two factorizations: the exchange's second epoch
-            run.run(a_loc, seed=s)
-            run.finish()
+        import warnings
+
+        for _ in range(reps):  # repeated factorizations: later epochs of the exchange
+            with warnings.catch_warnings(record=True) as rec:
+                warnings.simplefilter("always")
+                run.run(a_loc, seed=seed)
+                run.finish()
         qg, l, p, r = (t.cpu().numpy() for t in run.factors())
-        np.savez(os.path.join(outdir, f"rank{rank}.npz"), q=qg, l=l, p=p, epoch=run.epoch)
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), q=qg, l=l, p=p, epoch=run.epoch, tsqr=run.tsqr_fallbacks,
+                 warn=len(rec))
     finally:
         dist.destroy_process_group()
 
@@ -172,3 +177,19 @@ def test_virtual_rank_small_collectives(cuda, world):
         for r in range(world):
             assert np.array_equal(xs[r].C.cpu().numpy(), full)
     assert all(int(x.status.item()) == 0 for x in xs)
+
+
+@pytest.mark.timeout(600)
+def test_p2p_driver_guard_fallback_rerun(cuda, tmp_path):
+    """A rank-deficient A: the Cholesky-QR2 guard fires inside run(); finish()
+    re-runs the factorization with TSQR in every QR, the p2p AᵀX exchange
+    carrying on with its next epochs, and warns like the reference."""
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((600, 3)) @ rng.standard_normal((3, 200))
+    mp.spawn(_worker, args=(1, _free_port(), a, 8, 1, 2, str(tmp_path), 1), nprocs=1, join=True)
+    part = np.load(os.path.join(tmp_path, "rank0.npz"))
+    assert int(part["tsqr"]) == 2          # both QRs of A·P̄ by TSQR in the re-run
+    assert int(part["epoch"]) == 2 * 2     # 2 AᵀX exchanges per factorization, the run and its re-run
+    assert int(part["warn"]) == 3          # every orth site warns
+    qg = part["q"]
+    assert np.abs(qg.T @ qg - np.eye(qg.shape[1])).max() < 1e-12

@@ -44,6 +44,11 @@ struct GemmArgs {
   // BM×BN); `sym` enumerates only tiles with tm <= tn (requires BM == BN or a
   // single tile).  A separate kernel sums the slices in fixed order.
   int split, sym, units;
+  // sym with split_diag > 0: diagonal tiles get split_diag slices and the
+  // others `split` (the TMA kernel skips a diagonal tile's strictly-lower
+  // warp tiles, spread over the schedulers); split_tiles tiles in all, the
+  // slices of tile t occupy units [Σ_{t'<t} S_t', …)
+  int split_diag, split_tiles;
   const int* skip;   // when non-null and *skip != 0 the launch is a no-op
   const int* run_if; // when non-null and *run_if == 0 the launch is a no-op
   // tri_b: B is upper triangular (K == N), so output column tile tn only
@@ -78,6 +83,48 @@ struct GemmArgs {
   long xs_S, xs_ldl;
   int xs_rank;
 };
+
+// SPLIT mode: tile of unit u, its slice index, its slice count and the unit
+// of its first slice (the tiles' slice ranges are contiguous, in tile order)
+__device__ __forceinline__ void split_unit(const GemmArgs& p, int u, int& tsel, int& sl, int& S, int& first) {
+  if (!(p.sym && p.split_diag > 0)) {
+    tsel = u / p.split;
+    sl = u % p.split;
+    S = p.split;
+    first = tsel * p.split;
+    return;
+  }
+  int acc = 0;
+  for (int t = 0;; ++t) {
+    int tm, tn;
+    upper_tile(t, p.tiles_n, tm, tn);
+    const int st = (tm == tn) ? p.split_diag : p.split;
+    if (u < acc + st || t + 1 >= p.split_tiles) {
+      tsel = t;
+      sl = u - acc;
+      S = st;
+      first = acc;
+      return;
+    }
+    acc += st;
+  }
+}
+
+// first unit and slice count of tile tsel (the inverse of split_unit)
+__device__ __forceinline__ void split_tile(const GemmArgs& p, int tsel, int& first, int& S) {
+  S = p.split;
+  first = tsel * p.split;
+  if (!(p.sym && p.split_diag > 0)) return;
+  first = 0;
+  for (int t = 0; t < tsel; ++t) {
+    int tm, tn;
+    upper_tile(t, p.tiles_n, tm, tn);
+    first += (tm == tn) ? p.split_diag : p.split;
+  }
+  int tm, tn;
+  upper_tile(tsel, p.tiles_n, tm, tn);
+  S = (tm == tn) ? p.split_diag : p.split;
+}
 
 
 template <bool TRANS_A, int BM, int BN, int BK, int WM, int WN, int STAGES>
@@ -186,7 +233,8 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
     s.tile_it0 = 0;
     if (SPLIT) {
       if (c.unit >= p.units) return false;
-      const int tsel = c.unit / p.split, sl = c.unit % p.split;
+      int tsel, sl, S, first;
+      split_unit(p, c.unit, tsel, sl, S, first);
       if (p.sym) {
         upper_tile(tsel, p.tiles_n, s.tm, s.tn);
       } else {
@@ -194,8 +242,8 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
         s.tn = tsel % p.tiles_n;
       }
       s.tile = tsel;
-      s.kb = int(long(sl) * p.k_iters / p.split);
-      s.ke = int(long(sl + 1) * p.k_iters / p.split);
+      s.kb = int(long(sl) * p.k_iters / S);
+      s.ke = int(long(sl + 1) * p.k_iters / S);
       c.unit += G;
       return true;
     }
@@ -453,19 +501,21 @@ __global__ void __launch_bounds__(GemmCfg<TRANS_A, BM, BN, BK, WM, WN, STAGES>::
     unsigned int gen = 0;
     grid_barrier(p.red_counter, gen);
     constexpr long TILE = long(BM) * BN;
-    const long total = long(p.units / p.split) * TILE;
+    const long total = long(p.split_tiles > 0 ? p.split_tiles : p.units / p.split) * TILE;
     const long per = (total + G - 1) / G;
     const long e0 = long(blockIdx.x) * per, e1 = lmin(total, e0 + per);
     double dev = 0.0;
     for (long idx = e0 + tid; idx < e1; idx += THREADS) {
       const int tsel = int(idx / TILE);
       const long e = idx % TILE;
-      const double* src = p.partials + size_t(tsel) * p.split * TILE + e;
+      int first, S;
+      split_tile(p, tsel, first, S);
+      const double* src = p.partials + size_t(first) * TILE + e;
       double acc = 0.0;
-      for (int s0 = 0; s0 < p.split; s0 += 8) {
+      for (int s0 = 0; s0 < S; s0 += 8) {
         double v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = (s0 + q < p.split) ? __ldcg(src + size_t(s0 + q) * TILE) : 0.0;
+        for (int q = 0; q < 8; ++q) v[q] = (s0 + q < S) ? __ldcg(src + size_t(s0 + q) * TILE) : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc += v[q];
       }

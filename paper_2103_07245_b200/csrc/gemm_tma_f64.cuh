@@ -84,8 +84,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm0 = (warp / WARPS_N) * WM;
-  const int wn0 = (warp % WARPS_N) * WN;
+  int wm0 = (warp / WARPS_N) * WM;
+  int wn0 = (warp % WARPS_N) * WN;
   const int G = gridDim.x;
   const int GS = (SPLIT || p.group < 1) ? 1 : p.group;
   const int NG = G / GS, gi = blockIdx.x / GS, gr = blockIdx.x % GS;
@@ -122,7 +122,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
     s.tile_it0 = 0;
     if (SPLIT) {
       if (c.unit >= p.units) return false;
-      const int tsel = c.unit / p.split, sl = c.unit % p.split;
+      int tsel, sl, S, first;
+      split_unit(p, c.unit, tsel, sl, S, first);
       if (p.sym) {
         upper_tile(tsel, p.tiles_n, s.tm, s.tn);
       } else {
@@ -130,8 +131,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
         s.tn = tsel % p.tiles_n;
       }
       s.tile = tsel;
-      s.kb = int(long(sl) * p.k_iters / p.split);
-      s.ke = int(long(sl + 1) * p.k_iters / p.split);
+      s.kb = int(long(sl) * p.k_iters / S);
+      s.ke = int(long(sl + 1) * p.k_iters / S);
       c.unit += G;
       return true;
     }
@@ -251,6 +252,24 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
   while (next_seg(ccur, seg)) {
     const long m0 = long(seg.tm) * BM, n0 = long(seg.tn) * BN;
     const bool check = CHECK && (seg.tn == 0);
+    // A symmetric Gram's diagonal tile: the 6 warp tiles strictly below its
+    // diagonal are never read (the Cholesky uses blocks i ≤ j of G), so they
+    // are skipped and stay zero.  The warps are remapped so that the skipped
+    // tiles fall 2/1/1/2 on the four schedulers (warp w runs on w mod 4):
+    // 2/3/3/2 live warp tiles per scheduler instead of up to 4.
+    bool lowskip = false;
+    if constexpr (SPLIT && BM == 128 && BN == 128 && WM == 32 && WN == 32) {
+      if (p.sym && p.split_diag > 0 && seg.tm == seg.tn) {
+        constexpr unsigned long long kMap = 0xE9C8DF64B7A53210ull;  // warp w → warp tile (4-bit wr·4 + wc)
+        const int wt = int((kMap >> (4 * warp)) & 15);
+        wm0 = (wt >> 2) * WM;
+        wn0 = (wt & 3) * WN;
+        lowskip = wm0 > wn0;
+      } else {
+        wm0 = (warp / WARPS_N) * WM;
+        wn0 = (warp % WARPS_N) * WN;
+      }
+    }
     double acc[MT][NT][2];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
@@ -287,15 +306,17 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
           b[nt] = *reinterpret_cast<const double*>(sB + uint32_t(((wn0 >> 4) + (nt >> 1)) * 4096 + 512 * kk) +
                                                    V[(nt & 1) + 2 * (kk & 1)]);
       };
-      load_frags(0, fa[0], fb[0]);
+      if (!lowskip) {
+        load_frags(0, fa[0], fb[0]);
 #pragma unroll
-      for (int kk = 0; kk < KSTEPS; ++kk) {
-        const int cur = kk & 1;
-        if (kk + 1 < KSTEPS) load_frags(kk + 1, fa[cur ^ 1], fb[cur ^ 1]);
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+          const int cur = kk & 1;
+          if (kk + 1 < KSTEPS) load_frags(kk + 1, fa[cur ^ 1], fb[cur ^ 1]);
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
+          for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], fa[cur][mt], fb[cur][nt]);
+            for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], fa[cur][mt], fb[cur][nt]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
@@ -426,19 +447,21 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
     unsigned int gen = 0;
     grid_barrier(p.red_counter, gen);
     constexpr long TILE = long(BM) * BN;
-    const long total = long(p.units / p.split) * TILE;
+    const long total = long(p.split_tiles > 0 ? p.split_tiles : p.units / p.split) * TILE;
     const long per = (total + G - 1) / G;
     const long e0 = long(blockIdx.x) * per, e1 = lmin(total, e0 + per);
     double dev = 0.0;
     for (long idx = e0 + tid; idx < e1; idx += THREADS) {
       const int tsel = int(idx / TILE);
       const long e = idx % TILE;
-      const double* src = p.partials + size_t(tsel) * p.split * TILE + e;
+      int first, S;
+      split_tile(p, tsel, first, S);
+      const double* src = p.partials + size_t(first) * TILE + e;
       double acc = 0.0;
-      for (int s0 = 0; s0 < p.split; s0 += 8) {
+      for (int s0 = 0; s0 < S; s0 += 8) {
         double v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = (s0 + q < p.split) ? __ldcg(src + size_t(s0 + q) * TILE) : 0.0;
+        for (int q = 0; q < 8; ++q) v[q] = (s0 + q < S) ? __ldcg(src + size_t(s0 + q) * TILE) : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc += v[q];
       }

@@ -450,6 +450,7 @@ struct CqPlan {
   int nb;
   long np;
   int bm, bn, tiles_m, tiles_n, ntiles, k_iters, S, units;  // Gram GEMM (split-K partials)
+  int Sd;                                                  // slices of a diagonal tile (0: all tiles S)
   int grid;                                                // factor kernel CTAs, pass 1
   int grid2;                                               // pass 2 (series rounds have more items)
   long ldq1;
@@ -469,7 +470,23 @@ CqPlan cq_plan(const pbq_ctx* ctx, long m, long n) {
   p.ntiles = (p.tiles_m == 1 && p.tiles_n == 1) ? 1 : p.tiles_n * (p.tiles_n + 1) / 2;
   p.k_iters = int(ceil_div(m, 32));
   p.S = int(std::max<long>(1, std::min<long>(p.k_iters, ctx->sms / p.ntiles)));
+  p.Sd = 0;
   p.units = p.ntiles * p.S;
+  if (p.ntiles > 1 && p.bm == 128 && p.bn == 128 && gemm_use_tma()) {
+    // symmetric Gram: a diagonal tile skips its strictly-lower warp tiles and
+    // its busiest scheduler runs 3 instead of 4 warp tiles (gemm_tma_f64.cuh),
+    // so it gets 3/4 of an off-diagonal tile's k-slices
+    const long nd = p.tiles_n, no = p.ntiles - p.tiles_n;
+    long so = std::min<long>(p.k_iters, std::max<long>(1, (4L * ctx->sms) / (3L * nd + 4L * no)));
+    long sd = std::max<long>(1, std::min<long>(p.k_iters, (3 * so + 2) / 4));
+    while (nd * sd + no * so > ctx->sms && so > 1) {
+      --so;
+      sd = std::max<long>(1, std::min<long>(p.k_iters, (3 * so + 2) / 4));
+    }
+    p.S = int(so);
+    p.Sd = int(sd);
+    p.units = int(nd * sd + no * so);
+  }
   p.grid = int(std::max<long>(1, std::min<long>(ctx->sms, std::max<long>(long(p.nb) * (p.nb - 1) / 2, p.nb - 1))));
   {
     const long nbl = p.nb;
@@ -510,6 +527,7 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
   a.tiles_m = pl.tiles_m; a.tiles_n = pl.tiles_n; a.k_iters = pl.k_iters;
   a.partials = part;
   a.split = pl.S; a.sym = pl.ntiles > 1; a.units = pl.units;
+  a.split_diag = pl.Sd; a.split_tiles = pl.ntiles;
   a.skip = skip;
   a.run_if = run_if;
   a.red_counter = reinterpret_cast<unsigned int*>(counter);

@@ -270,6 +270,25 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
         wn0 = (warp % WARPS_N) * WN;
       }
     }
+    // Triangular B (Q₁ = A·R⁻¹): inside the diagonal 128-block of B, k-block
+    // kl (0…3) has nonzeros only in columns ≥ 32·kl, so warp tiles of warp
+    // column wc < kl skip it.  Warps are mapped so each scheduler holds one
+    // warp tile of every column: (wr, wc) = (w/4, (w + w/4) mod 4), and the
+    // skips thin out all four schedulers equally.
+    int tri_kl0 = 1 << 30;  // k-block index where the diagonal block of B starts
+    int wcol = 0;
+    if constexpr (!SPLIT && !RESID && BM == 128 && BN == 128 && WM == 32 && WN == 32) {
+      if (p.tri_b) {
+        const int wr = warp >> 2, wc = (warp + (warp >> 2)) & 3;
+        wm0 = wr * WM;
+        wn0 = wc * WN;
+        wcol = wc;
+        tri_kl0 = int(n0 / BK);
+      } else {
+        wm0 = (warp / WARPS_N) * WM;
+        wn0 = (warp % WARPS_N) * WN;
+      }
+    }
     double acc[MT][NT][2];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
@@ -306,7 +325,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
           b[nt] = *reinterpret_cast<const double*>(sB + uint32_t(((wn0 >> 4) + (nt >> 1)) * 4096 + 512 * kk) +
                                                    V[(nt & 1) + 2 * (kk & 1)]);
       };
-      if (!lowskip) {
+      if (!lowskip && !(kbk - tri_kl0 > wcol)) {
         load_frags(0, fa[0], fb[0]);
 #pragma unroll
         for (int kk = 0; kk < KSTEPS; ++kk) {

@@ -308,8 +308,10 @@ __device__ __forceinline__ double cq_split(int r, int c, double x) { return c > 
 //           barrier); work items are the Schur updates
 //             G_ij −= R_kiᵀ·R_kj,  R_kj = R_kk⁻ᵀ·G_kj     (k < i ≤ j)
 //           and the inverse blocks
-//             X_ik = −(Σ_{i≤l<k} X_il·R_lk)·R_kk⁻¹        (i < k)
-//           which only read blocks finished before step k; the operands of a
+//             X_ik = −(Σ_{i≤l<k} X_il·R_lk)·R_kk⁻¹        (i < k),
+//           accumulated one term per step (cq_inverse_accumulate_item /
+//           cq_inverse_final_item), which only read blocks finished before
+//           step k; the operands of a
 //           CTA's first item are fetched (cp.async) while G_kk is factored;
 //   one grid barrier per step.
 // Pass 2 with a near-identity G₂ = I + E instead runs the pivot-free series
@@ -355,8 +357,6 @@ __device__ __forceinline__ void cq_schur_item(const CqArgs& p, int k, int i, int
   __syncthreads();
 }
 
-__device__ __forceinline__ void cq_inverse_item(const CqArgs& p, int k, int i, double* sKI, double* sU,
-                                                double* pairs);
 
 // In-place split(E) of a staged block of E = G − I (block coordinates bi, bj):
 // strict upper part, half the diagonal, zeros below (X₀ of the series).
@@ -403,13 +403,46 @@ __device__ __forceinline__ void cq_block_sum(double (&c)[2][2], const double* M1
   }
 }
 
-// X_ik = −(Σ_{l=i}^{k−1} X_il·R_lk)·R_kk⁻¹
-__device__ __forceinline__ void cq_inverse_item(const CqArgs& p, int k, int i, double* sKI, double* sU,
-                                                double* pairs) {
+// X_ik = −(Σ_{l=i}^{k−1} X_il·R_lk)·R_kk⁻¹: the inverse's column blocks,
+// spread over the block steps instead of being
+// summed at step k alone (which made X_0k, with k products, the straggler of
+// every late step):
+//   accumulate item (step k, row i ≤ k−1, column j > k):
+//     P_ij += X_i,k−1 · R_k−1,j      (the first term, i = k−1, overwrites)
+//   final item (step k, row i ≤ k−1):
+//     X_ik = −(P_ik + X_i,k−1 · R_k−1,k) · R_kk⁻¹   (P_ik absent when i = k−1)
+// P_ij lives in X's slot (i, j) until the final item overwrites it.  Every
+// item is one block product (plus the R_kk⁻¹ product of the final items).
+__device__ __forceinline__ void cq_load_acc_global(double (&c)[2][2], const double* M, long np, int bi, int bj) {
+  const double* row = M + (long(bi) * 32 + cq_row()) * np + long(bj) * 32;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(row + cq_col(h)));
+    c[h][0] = v.x;
+    c[h][1] = v.y;
+  }
+}
+
+__device__ __forceinline__ void cq_inverse_accumulate_item(const CqArgs& p, int k, int i, int j, double* pairs) {
   const long np = p.np;
   double c[2][2];
-  cq_zero(c);
-  cq_block_sum<false>(c, p.X, p.R, np, i, k, i, k - 1, pairs);
+  if (i == k - 1)
+    cq_zero(c);
+  else
+    cq_load_acc_global(c, p.X, np, i, j);
+  cq_block_sum<false>(c, p.X, p.R, np, i, j, k - 1, k - 1, pairs);
+  cq_store_acc_global(p.X, np, i, j, c);
+}
+
+__device__ __forceinline__ void cq_inverse_final_item(const CqArgs& p, int k, int i, double* sKI, double* sU,
+                                                      double* pairs) {
+  const long np = p.np;
+  double c[2][2];
+  if (i == k - 1)
+    cq_zero(c);
+  else
+    cq_load_acc_global(c, p.X, np, i, k);
+  cq_block_sum<false>(c, p.X, p.R, np, i, k, k - 1, k - 1, pairs);
   cq_store_acc(sU, c, 1.0);
   __syncthreads();
   cq_zero(c);
@@ -421,6 +454,7 @@ __device__ __forceinline__ void cq_inverse_item(const CqArgs& p, int k, int i, d
   if (p.pass == 1) cq_colsum(p.colsum + long(p.nb) * np, np, i, k, out);
   __syncthreads();
 }
+
 
 __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) {
   pdl_trigger();  // a programmatically launched successor may start its prologue
@@ -575,7 +609,8 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
   for (int k = 0; k < nb; ++k) {
     const int mrem = nb - k - 1;
     const int n_upd = mrem * (mrem + 1) / 2;
-    const int n_items = n_upd + k;
+    const int n_acc = k * mrem;  // accumulate items: rows i < k, columns k+1 … nb−1
+    const int n_items = n_upd + k + n_acc;
     // operands of this CTA's first Schur item travel while G_kk is factored
     const bool pre = (int(blockIdx.x) < n_upd);
     cq_load_async(sKK, p.G, np, k, k);
@@ -623,8 +658,11 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
         int ii, jj;
         upper_tile(w, mrem, ii, jj);
         cq_schur_item(p, k, k + 1 + ii, k + 1 + jj, sKI, sA, sB, sC, sT, sU, pre && w == int(blockIdx.x));
+      } else if (w < n_upd + k) {
+        cq_inverse_final_item(p, k, w - n_upd, sKI, sU, pairs);
       } else {
-        cq_inverse_item(p, k, w - n_upd, sKI, sU, pairs);
+        const int u = w - n_upd - k;
+        cq_inverse_accumulate_item(p, k, u / mrem, k + 1 + u % mrem, pairs);
       }
     }
     CQ_MARK(1);

@@ -167,6 +167,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+bool small_tiles_off() {
+  static const bool off = getenv("PBQ_NO_SMALL_TILES") != nullptr;  // A/B switch
+  return off;
+}
+
 bool gemm_use_tma() {
   static const bool cpasync = [] {
     const char* e = getenv("PBQ_GEMM_LOADER");
@@ -202,10 +207,16 @@ bool encode_map3(CUtensorMap* m, const double* base, long cols, long rows, long 
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool T, int BN, bool CHECK, int MODE>
+template <bool T, int BN, bool CHECK, int MODE, int BM = 128>
 void* tma_fn() {
-  constexpr int WN = BN == 64 ? GEMM_WN64 : 32;
-  return reinterpret_cast<void*>(&gemm_f64_tma<T, 128, BN, GEMM_WM, WN, 3, CHECK, MODE == GEMM_SPLIT, MODE == GEMM_RESID>);
+  constexpr int WN = (BN == 64) ? GEMM_WN64 : 32;  // 128×64 and 64×64: warp tiles 32×16
+  return reinterpret_cast<void*>(&gemm_f64_tma<T, BM, BN, GEMM_WM, WN, 3, CHECK, MODE == GEMM_SPLIT, MODE == GEMM_RESID>);
+}
+// 64×64 tiles (8 warps) for small plain products (M ≤ 1024, e.g. the d×d
+// second stage), where 128×128 tiles leave a few CTAs with long fix-up chains
+void* tma_fn_small(bool trans, bool check) {
+  if (trans) return check ? tma_fn<true, 64, true, 0, 64>() : tma_fn<true, 64, false, 0, 64>();
+  return check ? tma_fn<false, 64, true, 0, 64>() : tma_fn<false, 64, false, 0, 64>();
 }
 template <bool T, int BN, bool CHECK, int MODE>
 void* ring_fn() {
@@ -225,8 +236,10 @@ void* pick_fn(bool trans, bool check, int mode) {
 }
 
 int gemm_dispatch(pbq_ctx* ctx, const GemmArgs& a, bool trans, int bn, int mode, dim3 grid, bool coop,
-                  cudaStream_t st) {
-  constexpr int threads = 512;  // 16 warps for both tile shapes
+                  cudaStream_t st, int bm = 128) {
+  const int threads = bm == 64 ? 256 : 512;  // 16 warps for the 128-row tiles, 8 for 64×64
+  if (bm == 64 && (mode != GEMM_PLAIN || bn != 64 || !gemm_use_tma()))
+    return fail(ctx, PBQ_ERR_UNSUPPORTED, "gemm: 64×64 tiles are for plain TMA products only");
   void* fn;
   size_t smem;
   GemmTmaArgs ta;
@@ -235,16 +248,21 @@ int gemm_dispatch(pbq_ctx* ctx, const GemmArgs& a, bool trans, int bn, int mode,
     memset(&ta, 0, sizeof(ta));
     ta.g = a;
     static const bool no3d = getenv("PBQ_TMA_NO3D") != nullptr;
-    ta.a3d = !no3d && (trans ? encode_map3(&ta.ta, a.A, a.M, a.K, a.lda, 32, 128 / 16)
-                             : encode_map3(&ta.ta, a.A, a.K, a.M, a.lda, 128, 32 / 16));
+    ta.a3d = !no3d && (trans ? encode_map3(&ta.ta, a.A, a.M, a.K, a.lda, 32, bm / 16)
+                             : encode_map3(&ta.ta, a.A, a.K, a.M, a.lda, bm, 32 / 16));
     ta.b3d = !no3d && encode_map3(&ta.tb, a.B, a.N, a.K, a.ldb, 32, bn / 16);
     const bool ok = (ta.a3d || (trans ? encode_map(&ta.ta, a.A, a.M, a.K, a.lda, 32)
-                                      : encode_map(&ta.ta, a.A, a.K, a.M, a.lda, 128))) &&
+                                      : encode_map(&ta.ta, a.A, a.K, a.M, a.lda, bm))) &&
                     (ta.b3d || encode_map(&ta.tb, a.B, a.N, a.K, a.ldb, 32));
     if (!ok) return fail(ctx, PBQ_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
-    fn = bn == 64 ? pick_fn<true, 64>(trans, a.nonfinite != nullptr, mode)
-                  : pick_fn<true, 128>(trans, a.nonfinite != nullptr, mode);
-    smem = bn == 64 ? gemm_tma_smem_bytes<true, 128, 64, 3>() : gemm_tma_smem_bytes<true, 128, 128, 3>();
+    if (bm == 64) {
+      fn = tma_fn_small(trans, a.nonfinite != nullptr);
+      smem = gemm_tma_smem_bytes<true, 64, 64, 3>();
+    } else {
+      fn = bn == 64 ? pick_fn<true, 64>(trans, a.nonfinite != nullptr, mode)
+                    : pick_fn<true, 128>(trans, a.nonfinite != nullptr, mode);
+      smem = bn == 64 ? gemm_tma_smem_bytes<true, 128, 64, 3>() : gemm_tma_smem_bytes<true, 128, 128, 3>();
+    }
     args[0] = &ta;
   } else {
     fn = bn == 64 ? pick_fn<false, 64>(trans, a.nonfinite != nullptr, mode)
@@ -288,11 +306,13 @@ struct GemmPlan {
   int grid;
 };
 
-GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K, bool tri_b = false) {
+GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K, bool tri_b = false, bool allow_small = true) {
   GemmPlan p;
   const int bk = 32;
   if (N <= 64) {
     p.bm = 128; p.bn = 64;
+  } else if (allow_small && M <= 1024 && gemm_use_tma() && !small_tiles_off()) {
+    p.bm = 64; p.bn = 64;  // small products: 4× the tiles, short fix-up chains
   } else {
     p.bm = 128; p.bn = 128;
   }
@@ -335,7 +355,8 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
     return fail(ctx, PBQ_ERR_PARAM, "gemm: leading dimensions must be even and pointers 16-byte aligned");
   if (K == 0) return fail(ctx, PBQ_ERR_DIM, "gemm: K == 0");
   if (tri_b && K != N) return fail(ctx, PBQ_ERR_DIM, "gemm: triangular B must be square");
-  const GemmPlan pl = gemm_plan(ctx, M, N, K, tri_b);
+  // the scatter epilogue's tile counts (pbq_xchg_expected_tiles) assume the 128-row tiles
+  const GemmPlan pl = gemm_plan(ctx, M, N, K, tri_b, xs == nullptr);
   Carve cv(ws, ws_bytes);
   GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -359,7 +380,7 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   }
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gemm: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   ProfScope ps(ctx->prof, st, 0);
-  return gemm_dispatch(ctx, a, TRANS, pl.bn, GEMM_PLAIN, dim3(pl.grid), false, st);
+  return gemm_dispatch(ctx, a, TRANS, pl.bn, GEMM_PLAIN, dim3(pl.grid), false, st, pl.bm);
 }
 
 // ------------------------------------------------------------------ QR ----
@@ -1041,7 +1062,7 @@ __global__ void resid_final_kernel(const double* sums, int n, double* out) {
 }
 
 size_t resid_ws_bytes(const pbq_ctx* ctx, long n1, long n2, long k) {
-  const GemmPlan g1 = gemm_plan(ctx, n1, n2, k), g2 = gemm_plan(ctx, n1, k, k);
+  const GemmPlan g1 = gemm_plan(ctx, n1, n2, k, false, false), g2 = gemm_plan(ctx, n1, k, k);
   const long ldk = thin_ld(k), ldn = thin_ld(n2);
   return align_up(size_t(n1) * ldk * 8, 256) + align_up(size_t(k) * ldn * 8, 256) +
          align_up(2 * size_t(ctx->sms) * 8, 256) + std::max(gemm_ws_bytes(g1), gemm_ws_bytes(g2)) + 1024;
@@ -1059,7 +1080,7 @@ int resid_launch(pbq_ctx* ctx, long n1, long n2, long k, const double* A, long l
   double* ql = cv.take<double>(size_t(n1) * ldk);
   double* pt = cv.take<double>(size_t(k) * ldn);
   double* sums = cv.take<double>(2 * size_t(ctx->sms));
-  const GemmPlan pl = gemm_plan(ctx, n1, n2, k);
+  const GemmPlan pl = gemm_plan(ctx, n1, n2, k, false, false);
   const size_t gws_bytes = std::max(gemm_ws_bytes(pl), gemm_ws_bytes(gemm_plan(ctx, n1, k, k)));
   char* gws = cv.take<char>(gws_bytes);
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "residual: workspace too small (%zu < %zu)", ws_bytes, cv.off);
@@ -1188,7 +1209,8 @@ int64_t pbq_ctx_launch_count(const pbq_ctx* ctx) { return ctx ? ctx->launches : 
 
 int pbq_gemm_workspace_bytes(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, size_t* bytes) {
   if (!ctx || !bytes) return PBQ_ERR_PARAM;
-  *bytes = gemm_ws_bytes(gemm_plan(ctx, M, N, std::max<int64_t>(K, 1)));
+  const int64_t k1 = std::max<int64_t>(K, 1);  // either tile choice (the scatter GEMM keeps the 128-row tiles)
+  *bytes = std::max(gemm_ws_bytes(gemm_plan(ctx, M, N, k1)), gemm_ws_bytes(gemm_plan(ctx, M, N, k1, false, false)));
   return PBQ_OK;
 }
 

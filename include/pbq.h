@@ -16,6 +16,10 @@
  *    point synchronises the host except pbq_ctx_create.
  *  - Scratch memory is caller-owned: query the size, pass a device buffer.
  *    A workspace must not be shared by calls that may run concurrently.
+ *  - Calls of one context may run concurrently on different streams (each
+ *    with its own workspace): the GEMMs' stream-K flags are kept per stream.
+ *    A CUDA graph captured from a stream uses that stream's flags, so do not
+ *    replay it concurrently with other work enqueued on the capture stream.
  *  - Return value is a pbq_status; pbq_last_error() describes the last failure.
  *  - A context is bound to one device and is not thread-safe.
  */

@@ -117,8 +117,10 @@ def rank_flag(r):
     return 0
 
 
-def oracle_orth(m):
+def oracle_orth(m, diag_log=None):
     q, r = oracle_qr(m)
+    if diag_log is not None:  # test hook: |diag R| of every orth call, in call order
+        diag_log.append(np.abs(np.diagonal(r)).copy())
     return q, rank_flag(r)
 
 
@@ -161,7 +163,9 @@ def oracle_pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, phi=None):
     if phi is None:
         phi = oracle_gaussian(n1, d, seed)
     flags = []
+    diags = []  # |diag R| of each orth call (rank-test margins)
     passes = 0
+    orth = lambda m: oracle_orth(m, diags)  # noqa: E731
 
     def apply(block):
         nonlocal passes
@@ -175,24 +179,25 @@ def oracle_pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, phi=None):
 
     c = apply_t(phi)
     if reorthonormalize:
-        pbar, f = oracle_orth(c)
+        pbar, f = orth(c)
         flags.append(f)
         for _ in range(q):
-            pbar, f = oracle_orth(apply(pbar))
+            pbar, f = orth(apply(pbar))
             flags.append(f)
-            pbar, f = oracle_orth(apply_t(pbar))
+            pbar, f = orth(apply_t(pbar))
             flags.append(f)
     else:
         for _ in range(q):
             c = apply_t(apply(c))
-        pbar, f = oracle_orth(c)
+        pbar, f = orth(c)
         flags.append(f)
     dmat = apply(pbar)
     qfac, rfac = oracle_qr(dmat)
     w, rt = oracle_qr(rfac.T)
     l = np.tril(rt.T)
     p = pbar @ w
-    return {"q": qfac, "l": l, "p": p, "r": rfac, "phi": phi, "rank_flags": flags, "passes": passes}
+    return {"q": qfac, "l": l, "p": p, "r": rfac, "phi": phi, "rank_flags": flags, "passes": passes,
+            "orth_r_diag": diags}
 
 
 # ------------------------------------------------------------------ checks --

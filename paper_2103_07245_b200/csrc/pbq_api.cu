@@ -9,7 +9,10 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <mutex>
 #include <unordered_map>
+#include <utility>
+#include <vector>
 
 #include "../../include/pbq.h"
 #include "common.cuh"
@@ -45,13 +48,46 @@ struct pbq_ctx {
   int qr_method = PBQ_QR_AUTO;
   int* cq_stats = nullptr;                    // debug: [Cholesky-QR2 done, fallbacks]
   std::unordered_map<const void*, int> smem_attr;  // max dynamic smem already set per kernel (one driver call each)
-  int* gemm_flags = nullptr;  // stream-K partial-ready flags (sms ints), zero between GEMM launches: readers reset them
+  // stream-K partial-ready flags: one array of `sms` ints per stream that
+  // has launched a GEMM on this context.  An array is zero between launches
+  // (its readers reset the flags they consume), and GEMMs on one stream are
+  // serialised, so no array is ever shared by two GEMMs in flight — calls on
+  // different streams (each with its own workspace) may run concurrently.
+  std::mutex flag_mu;
+  std::vector<std::pair<cudaStream_t, int*>> stream_flags;
+  std::vector<int*> flag_blocks;  // cudaMalloc'd batches backing stream_flags
+  size_t flag_free = 0;           // unassigned arrays left in flag_blocks.back()
   char err[512] = {0};
 };
 
 namespace {
 
 using namespace pbq;
+
+constexpr size_t kFlagBatch = 32;  // flag arrays per cudaMalloc batch
+
+// The stream-K flag array of stream `st` (see pbq_ctx::stream_flags).  The
+// first batch is zeroed at context creation; an array from a later batch is
+// zeroed by an async memset on the stream it is assigned to (legal inside
+// stream capture, and ordered before that stream's first GEMM).  nullptr on
+// allocation failure.
+int* gemm_flags_for(pbq_ctx* ctx, cudaStream_t st) {
+  std::lock_guard<std::mutex> g(ctx->flag_mu);
+  for (auto& e : ctx->stream_flags)
+    if (e.first == st) return e.second;
+  const size_t per = size_t(std::max(ctx->sms, 1));
+  if (ctx->flag_free == 0) {
+    int* blk = nullptr;
+    if (cudaMalloc(&blk, sizeof(int) * per * kFlagBatch) != cudaSuccess) return nullptr;
+    ctx->flag_blocks.push_back(blk);
+    ctx->flag_free = kFlagBatch;
+  }
+  int* f = ctx->flag_blocks.back() + per * (kFlagBatch - ctx->flag_free);
+  if (ctx->flag_blocks.size() > 1 && cudaMemsetAsync(f, 0, sizeof(int) * per, st) != cudaSuccess) return nullptr;
+  --ctx->flag_free;
+  ctx->stream_flags.emplace_back(st, f);
+  return f;
+}
 
 int fail(pbq_ctx* ctx, int code, const char* fmt, ...) {
   if (ctx) {
@@ -365,8 +401,9 @@ int gemm_launch(pbq_ctx* ctx, long M, long N, long K, double alpha, const double
   a.alpha = alpha; a.beta = beta;
   a.tiles_m = pl.tiles_m; a.tiles_n = pl.tiles_n; a.k_iters = pl.k_iters; a.total_iters = pl.total;
   a.partials = cv.take<double>(size_t(pl.grid) * pl.bm * pl.bn);
-  cv.take<int>(pl.grid);  // (workspace layout unchanged; the flags are the context's)
-  a.flags = ctx->gemm_flags;
+  cv.take<int>(pl.grid);  // (workspace layout unchanged; the flags are per stream)
+  a.flags = gemm_flags_for(ctx, st);
+  if (!a.flags) return fail(ctx, PBQ_ERR_OOM, "gemm: cannot allocate stream-K flags");
   a.nonfinite = nonfinite;
   a.split = 0; a.sym = 0; a.units = 0;
   a.skip = skip;
@@ -1096,7 +1133,8 @@ int resid_launch(pbq_ctx* ctx, long n1, long n2, long k, const double* A, long l
   Carve gc(gws, gws_bytes);
   a.partials = gc.take<double>(size_t(pl.grid) * pl.bm * pl.bn);
   gc.take<int>(pl.grid);
-  a.flags = ctx->gemm_flags;
+  a.flags = gemm_flags_for(ctx, st);
+  if (!a.flags) return fail(ctx, PBQ_ERR_OOM, "residual: cannot allocate stream-K flags");
   a.ref = A; a.ldref = lda; a.sums = sums;
   {
     ProfScope ps(ctx->prof, st, 0);
@@ -1140,22 +1178,29 @@ int pbq_ctx_create(int device, pbq_ctx** out) {
     return PBQ_ERR_CUDA;
   }
   ctx->smem_optin = size_t(optin);
-  // the GEMMs' stream-K flags live in the context (not in the per-call
-  // workspace), start zeroed and are reset by their readers, so no launch
-  // needs a memset in front of it (which would also break the programmatic
-  // launch chain); GEMMs of one context run on one stream at a time
-  if (cudaMalloc(&ctx->gemm_flags, sizeof(int) * size_t(std::max(ctx->sms, 1))) != cudaSuccess ||
-      cudaMemset(ctx->gemm_flags, 0, sizeof(int) * size_t(std::max(ctx->sms, 1))) != cudaSuccess) {
-    cudaFree(ctx->gemm_flags);
-    delete ctx;
-    return PBQ_ERR_CUDA;
+  // the GEMMs' stream-K flags live in the context, one array per stream (not
+  // in the per-call workspace): they start zeroed and are reset by their
+  // readers, so no launch needs a memset in front of it (which would also
+  // break the programmatic launch chain).  The first batch is zeroed here.
+  {
+    const size_t per = size_t(std::max(ctx->sms, 1));
+    int* blk = nullptr;
+    if (cudaMalloc(&blk, sizeof(int) * per * kFlagBatch) != cudaSuccess ||
+        cudaMemset(blk, 0, sizeof(int) * per * kFlagBatch) != cudaSuccess) {
+      cudaFree(blk);
+      delete ctx;
+      return PBQ_ERR_CUDA;
+    }
+    ctx->flag_blocks.push_back(blk);
+    ctx->flag_free = kFlagBatch;
   }
   *out = ctx;
   return PBQ_OK;
 }
 
 int pbq_ctx_destroy(pbq_ctx* ctx) {
-  if (ctx && ctx->gemm_flags) cudaFree(ctx->gemm_flags);
+  if (ctx)
+    for (int* b : ctx->flag_blocks) cudaFree(b);
   if (ctx && ctx->prof.ev) {
     for (int i = 0; i < 2 * ctx->prof.cap; ++i) cudaEventDestroy(ctx->prof.ev[i]);
     delete[] ctx->prof.ev;

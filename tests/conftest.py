@@ -8,6 +8,17 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 REFERENCE_SRC = "/root/reference/pkg/src"
+# the stock reference installed by tools/install_reference.sh (git-ignored;
+# travels to the GPU box, where /root/reference does not exist)
+REFERENCE_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_path():
+    """Directory to put on sys.path to import the reference ``pbpqlp``, or None."""
+    for cand in (REFERENCE_SRC, REFERENCE_INSTALL):
+        if os.path.isfile(os.path.join(cand, "pbpqlp", "__init__.py")):
+            return cand
+    return None
 
 
 def pytest_configure(config):
@@ -29,11 +40,13 @@ def cuda():
 
 @pytest.fixture(scope="session")
 def reference_pkg():
-    """The reference package, importable only in the build container."""
-    if not os.path.isdir(REFERENCE_SRC):
-        pytest.skip("reference source not present (GPU box)")
-    if REFERENCE_SRC not in sys.path:
-        sys.path.insert(0, REFERENCE_SRC)
+    """The reference package: /root/reference in the build container, the
+    stock install under baseline/_ref on the GPU box."""
+    path = reference_path()
+    if path is None:
+        pytest.skip("reference not present (run tools/install_reference.sh)")
+    if path not in sys.path:
+        sys.path.insert(0, path)
     import pbpqlp
 
     return pbpqlp

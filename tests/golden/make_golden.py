@@ -34,11 +34,25 @@ def sha(a):
 def main():
     manifest = {}
     for name, case in CASES.items():
-        a = make_input(case["recipe"])
+        rec_ = case["recipe"]
+        if rec_["kind"] == "stored":  # inputs from a reference generator, e.g. gen_hansen('baart', 200)
+            import ast
+
+            fn, args = rec_["source"].split("(", 1)
+            gen_args = ast.literal_eval("(" + args.rstrip()[:-1] + ",)")
+            np.save(os.path.join(HERE, rec_["file"]), getattr(pbpqlp, fn)(*gen_args))
+        a = make_input(rec_)
         with warnings.catch_warnings(record=True) as rec:
             warnings.simplefilter("always")
             f = pbpqlp.pbp_qlp(a, case["d"], q=case["q"], seed=case["seed"], reorthonormalize=case["reorth"])
         n_warn = sum(1 for w in rec if issubclass(w.category, pbpqlp.RankDeficiencyWarning))
+        # rank-test margins of the reference's own orth calls (the oracle is
+        # bitwise the reference here): smallest |R_ii|/|R_00| per call
+        from oracle.pbp_qlp_oracle import oracle_pbp_qlp
+
+        o = oracle_pbp_qlp(a, case["d"], q=case["q"], seed=case["seed"], reorthonormalize=case["reorth"])
+        assert np.array_equal(o["q"], f.q_basis), "oracle is not the reference"
+        min_ratio = [float(dg.min() / dg[0]) if dg[0] > 0 else 0.0 for dg in o["orth_r_diag"]]
         np.savez_compressed(
             os.path.join(HERE, f"{name}.npz"),
             q=f.q_basis, l=f.l, p=f.p_basis, r=f.first_stage_r, phi=f.sketch.test_matrix,
@@ -49,6 +63,8 @@ def main():
             "a_sha256": sha(a),
             "passes_over_a": f.sketch.passes_over_a,
             "rank_warnings": n_warn,
+            "rank_flags": [int(x) for x in o["rank_flags"]],
+            "orth_min_ratio": min_ratio,
         }
         print(name, a.shape, "warnings", n_warn)
     # sketch-only fixtures: gaussian_matrix(rows, cols, seed)

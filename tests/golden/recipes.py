@@ -18,6 +18,13 @@ CASES = {
     "rank_deficient": {"recipe": {"kind": "lowrank", "shape": [120, 80], "rank": 3, "noise": 0.0, "seed": 9},
                        "d": 8, "q": 1, "seed": 1, "reorth": True},
     "cfg1": {"recipe": {"kind": "cfg1", "seed": 0}, "d": 40, "q": 0, "seed": 0, "reorth": True},
+    # the reference's own rank-test edge case (test_analysis.py:209-215):
+    # Hansen's baart(200) at the norm-ratio default d = 20, every orth warns;
+    # several |R_ii|/|R_00| sit within 10x of the 1e-14 threshold
+    "baart200_q0": {"recipe": {"kind": "stored", "file": "baart200_a.npy", "source": "gen_hansen('baart', 200)"},
+                    "d": 20, "q": 0, "seed": 1, "reorth": True},
+    "baart200_q2": {"recipe": {"kind": "stored", "file": "baart200_a.npy", "source": "gen_hansen('baart', 200)"},
+                    "d": 20, "q": 2, "seed": 1, "reorth": True},
 }
 
 
@@ -30,6 +37,12 @@ def _haar(n, rng):
 
 def make_input(recipe):
     kind = recipe["kind"]
+    if kind == "stored":
+        # an input produced by a reference generator (make_golden.py), stored
+        # as-is because the generator is not part of this package
+        import os
+
+        return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), recipe["file"]))
     if kind == "eye":
         return np.eye(recipe["n"])
     if kind == "gauss":

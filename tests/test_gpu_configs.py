@@ -114,12 +114,27 @@ def test_config4_full(cuda):
     _parity(a, 512, 1, 0, a_dev=a_dev)
 
 
-@pytest.mark.slow
-def test_config5_full(cuda):
-    """Config 5 at its BASELINE size: 65536×16384 (A = 8.6 GB), d = 256, q = 0,
-    σ_i = e^(−i/40) + 1e-8·N(0,1)."""
+@pytest.fixture(scope="module")
+def cfg5_matrix(cuda):
+    """Config 5's A (65536×16384, 8.6 GB) on the device and its host copy,
+    built once for the whole d-sweep."""
     from paper_2103_07245_b200 import workloads
 
     a_dev = workloads.make_cfg5(0, cuda)
     a = a_dev.cpu().numpy()
-    _parity(a, 256, 0, 0, a_dev=a_dev)
+    yield a_dev, a
+    del a_dev
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("q", [0, 2])
+@pytest.mark.parametrize("d", [64, 128, 256, 512, 1024])
+def test_config5_full(cuda, cfg5_matrix, d, q):
+    """Config 5 at its BASELINE size, every point of the d-sweep the bench
+    reports (BASELINE.json configs[4]): 65536×16384 (A = 8.6 GB),
+    σ_i = e^(−i/40) over inner dimension 2048 + 1e-8·N(0,1),
+    d ∈ {64, 128, 256, 512, 1024}, q ∈ {0, 2}.  d ≥ 512 is conditioning-
+    limited: the per-column bound is max(1e-10, 64·u·κ_j)."""
+    a_dev, a = cfg5_matrix
+    _parity(a, d, q, 0, a_dev=a_dev)

@@ -57,6 +57,33 @@ def test_gemm_alpha_beta_and_determinism(cuda):
     assert np.array_equal(r1, r2)  # stream-K fix-up order is fixed
 
 
+@pytest.mark.gpu
+def test_gemm_concurrent_streams_one_context(cuda):
+    """Stream-K GEMMs of ONE context on several streams at once (each call
+    with its own workspace, include/pbq.h): every stream has its own flag
+    array, so the fix-ups cannot consume each other's partials."""
+    import torch
+
+    from paper_2103_07245_b200 import device as D
+
+    rng = np.random.default_rng(17)
+    ctx = D.context(cuda)
+    mats = [(rng.standard_normal((4100, 900 + 64 * i)), rng.standard_normal((4100, 200))) for i in range(4)]
+    devs = [(_dev_matrix(a, cuda), _dev_matrix(b, cuda)) for a, b in mats]
+    serial = [D.gemm(ctx, A, B, trans_a=True).cpu().numpy() for A, B in devs]
+    streams = [torch.cuda.Stream(cuda) for _ in devs]
+    for rep in range(3):
+        outs = []
+        torch.cuda.synchronize()
+        for (A, B), s in zip(devs, streams):
+            with torch.cuda.stream(s):
+                outs.append([D.gemm(ctx, A, B, trans_a=True) for _ in range(4)])
+        torch.cuda.synchronize()
+        for got, ref in zip(outs, serial):
+            for g in got:
+                assert np.array_equal(g.cpu().numpy(), ref)
+
+
 def test_gemm_nonfinite_flag(cuda):
     from paper_2103_07245_b200 import device as D
 

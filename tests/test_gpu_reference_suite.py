@@ -1,0 +1,86 @@
+"""The reference's OWN tests, run against the GPU drop-in (SURVEY.md §7 step
+6; VERDICT r01 "next" item 2).
+
+Each case runs pytest in a subprocess on one of the reference's test files
+(``/root/reference/pkg/tests`` in the build container, the copy staged by
+tools/install_reference.sh under ``baseline/_ref/_reference_tests`` on the
+GPU box) with ``-p tests.reference_suite_plugin``, which installs the drop-in
+into the stock ``pbpqlp`` before the test modules import it.  Every
+``pbp_qlp`` / ``r_svd`` / ``cor_utv`` / ``column_pivoted_qr`` the tests call
+then runs on libpbq; the plugin reports the call and launch counts and this
+test requires them to be nonzero.
+
+The selection is the reference's tests of the path and its callers:
+test_algorithms.py:31-157 (PbP-QLP, r_svd, cor_utv), test_estimators.py,
+test_analysis.py (factorize, error curves, the baart(200) warning case at
+:209-215), test_bounds.py:112-225 and test_acceptance.py:52-155.
+"""
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from tests.conftest import REFERENCE_INSTALL, ROOT, reference_path
+
+pytestmark = pytest.mark.gpu
+
+TARGETS = [
+    "test_algorithms.py::TestTwoSidedRandomized",
+    "test_algorithms.py::TestRandomizedSvd",
+    "test_algorithms.py::TestCompressedUtv",
+    "test_estimators.py",
+    "test_analysis.py",
+    "test_bounds.py",
+    "test_acceptance.py",
+]
+
+
+def _tests_dir():
+    for cand in (os.path.join(REFERENCE_INSTALL, "_reference_tests"), "/root/reference/pkg/tests"):
+        if os.path.isfile(os.path.join(cand, "test_algorithms.py")):
+            return cand
+    return None
+
+
+@pytest.mark.parametrize("target", TARGETS)
+def test_reference_suite_through_install(cuda, target):
+    tdir, rpath = _tests_dir(), reference_path()
+    if tdir is None or rpath is None:
+        pytest.skip("reference tests not staged (run tools/install_reference.sh)")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([rpath, ROOT] + ([env["PYTHONPATH"]] if env.get("PYTHONPATH") else []))
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    fname, _, sel = target.partition("::")
+    path = os.path.join(tdir, fname) + (f"::{sel}" if sel else "")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-p", "tests.reference_suite_plugin",
+           "--rootdir", tdir, "-o", "addopts=", path]
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1800)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-6000:]
+    m = re.search(r"(\d+) passed", out)
+    assert m and int(m.group(1)) > 0, out[-3000:]
+    assert not re.search(r"\d+ (failed|error)", out), out[-3000:]
+    calls = re.search(r"GPU-DROPIN calls: (.*); libpbq launches: (\d+)", out)
+    assert calls and calls.group(1) != "none" and int(calls.group(2)) > 0, out[-3000:]
+    print(f"{target}: {m.group(0)}; {calls.group(0)}")
+
+
+def test_oracle_is_the_reference_on_this_box(reference_pkg):
+    """The oracle the GPU tests check against is re-pinned to the stock
+    reference on the box itself (bitwise, same numpy/OpenBLAS), not only in
+    the build container (tests/test_oracle.py)."""
+    from oracle.pbp_qlp_oracle import oracle_pbp_qlp
+    from tests.golden.recipes import CASES, make_input
+
+    cases = [(make_input(c["recipe"]), c["d"], c["q"], c["seed"], c["reorth"]) for c in CASES.values()]
+    rng = np.random.default_rng(0)
+    cases.append((rng.standard_normal((300, 200)), 25, 2, 3, False))
+    for a, d, q, seed, reorth in cases:
+        ref = reference_pkg.pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorth)
+        o = oracle_pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorth)
+        for x, y in ((ref.q_basis, o["q"]), (ref.l, o["l"]), (ref.p_basis, o["p"]), (ref.first_stage_r, o["r"]),
+                     (ref.sketch.test_matrix, o["phi"])):
+            assert np.array_equal(x, y)

@@ -47,9 +47,12 @@ def parse():
     ap.add_argument("--q", type=int, default=None, help="override the workload's q")
     ap.add_argument("--path", default="pbp_qlp", choices=["pbp_qlp", "r_svd", "cor_utv"],
                     help="r_svd / cor_utv: the sibling randomized paths (SURVEY §8 f3), single GPU")
-    ap.add_argument("--exchange", default=None, choices=["p2p", "nccl"],
-                    help="N > 1 AᵀX exchange: p2p = the fused scatter-GEMM / slice reduce over NVLink peer memory "
-                         "(default with NCCL), nccl = chunked GEMM + asynchronous ncclAllReduce")
+    ap.add_argument("--exchange", default="nccl", choices=["p2p", "nccl"],
+                    help="N > 1 AᵀX exchange: nccl (default) = chunked GEMM + asynchronous ncclAllReduce; p2p = the "
+                         "fused scatter-GEMM / slice reduce over NVLink peer memory (self-checked against NCCL at "
+                         "init, falls back to nccl on mismatch or timeout)")
+    ap.add_argument("--no-cfg4", action="store_true",
+                    help="skip the extra config-4 (200000x8192, d=512, q=1) timing carried in the default line")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: validates the N>1 code path with ranks sharing GPUs (host-mediated "
                          "collectives); its timings are not bench values")
@@ -126,21 +129,70 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_impl(path="pbp_qlp"):
+    """The CPU implementation the baseline times: the STOCK reference
+    (``pbpqlp`` installed unmodified under baseline/_ref by
+    tools/install_reference.sh) when present — kind "reference" — else the
+    oracle port of its call sequence (oracle/pbp_qlp_oracle.py, kind "port")."""
+    if os.path.isfile(os.path.join(REF_INSTALL, "pbpqlp", "__init__.py")):
+        if REF_INSTALL not in sys.path:
+            sys.path.insert(0, REF_INSTALL)
+        import pbpqlp
+
+        fn = getattr(pbpqlp, path)
+        return fn, "reference", f"stock pbpqlp {pbpqlp.__version__}.{path} from baseline/_ref"
+    from oracle import pbp_qlp_oracle as O
+
+    fn = {"pbp_qlp": O.oracle_pbp_qlp, "r_svd": O.oracle_r_svd, "cor_utv": O.oracle_cor_utv}[path]
+    return fn, "port", f"oracle port oracle/pbp_qlp_oracle.py:oracle_{path} (reference call sequence)"
+
+
+def host_info():
+    """CPU model, numpy and BLAS build of the host the CPU baseline ran on."""
+    import numpy as np
+
+    info = {"numpy": np.__version__, "cores_available": cpu_threads()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    info["cpu_model"] = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+
+        info["threadpools"] = [{k: tp.get(k) for k in ("user_api", "internal_api", "version", "num_threads",
+                                                       "threading_layer", "architecture")}
+                               for tp in threadpool_info()]
+    except Exception as exc:  # noqa: BLE001
+        info["threadpools"] = f"unavailable: {exc}"
+    return info
+
+
 def time_cpu_oracle(a_host, wl, seed, steps, budget_s=None):
-    """Time the CPU oracle (the reference's numpy call sequence) on all host cores."""
+    """Time the reference's CPU path on all host cores: the stock pbpqlp when
+    installed (kind "reference"), else the oracle port (kind "port")."""
+    import warnings
+
     from threadpoolctl import threadpool_limits
 
-    from oracle.pbp_qlp_oracle import oracle_pbp_qlp
     from paper_2103_07245_b200 import pbp_qlp_flops
 
+    fn, kind, prov = reference_impl("pbp_qlp")
     cores = cpu_threads()
     n1, n2, d, q = wl["n1"], wl["n2"], wl["d"], wl["q"]
     a = a_host
     sample = f"full {n1}x{n2} d={d} q={q} factorization per step"
     times = []
-    with threadpool_limits(limits=cores):
+    with threadpool_limits(limits=cores), warnings.catch_warnings():
+        warnings.simplefilter("ignore")
         t0 = time.perf_counter()
-        oracle_pbp_qlp(a, d, q=q, seed=seed)
+        fn(a, d, q=q, seed=seed)  # discarded warm-up (cli.py:393-415 protocol)
         first = time.perf_counter() - t0
         if budget_s is not None and first * steps > budget_s:
             rows = max(d, int(n1 * budget_s / (first * steps * 1.2)))
@@ -149,17 +201,19 @@ def time_cpu_oracle(a_host, wl, seed, steps, budget_s=None):
             sample = f"row sample {rows}x{n2} of the {wl['n1']}x{n2} matrix, d={d} q={q}, per step"
         for i in range(steps):
             t0 = time.perf_counter()
-            oracle_pbp_qlp(a, d, q=q, seed=seed + 1 + i)
+            fn(a, d, q=q, seed=seed + 1 + i)
             times.append(time.perf_counter() - t0)
     f = pbp_qlp_flops(n1, n2, d, q)
     med = statistics.median(times)
-    return {"value": f / med / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-            "sample": sample + f" ({len(times)} timed, median {med:.3f} s; numpy/OpenBLAS oracle/pbp_qlp_oracle.py)",
-            "seconds": med, "times": times}
+    return {"value": f / med / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": kind,
+            "sample": sample + f" ({len(times)} timed after 1 discarded, median {med:.3f} s, "
+                               f"mean {statistics.mean(times):.3f} s; {prov}; numpy/OpenBLAS on {cores} threads)",
+            "seconds": med, "times": times, "host": host_info()}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU path (oracle port) on rank 0 only."""
+    """--impl reference: the reference's CPU path (the stock pbpqlp from
+    baseline/_ref, else the oracle port) on rank 0 only."""
     if rank != 0:
         return
     import numpy as np
@@ -177,7 +231,7 @@ def run_reference(args, world, rank):
         "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(args, wl, world),
-        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample", "host")},
         "e2e": {"value": res["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,15 +282,7 @@ def run_ours(args, world, rank, local):
         torch.cuda.empty_cache()
         # p2p needs GPUs of their own (its waits span ranks): never with the
         # gloo validation mode, where ranks share a GPU
-        exchange = args.exchange or ("p2p" if args.dist_backend == "nccl" else "nccl")
-        if exchange == "p2p" and args.dist_backend != "nccl":
-            raise SystemExit("--exchange p2p needs --dist-backend nccl (one GPU per rank)")
-        try:
-            runner = PD.DistributedPbpQlp(n1, n2, d, q, rows, dev, exchange=exchange)
-            exchange_note = exchange
-        except Exception as exc:  # symmetric memory unavailable: the NCCL exchange
-            runner = PD.DistributedPbpQlp(n1, n2, d, q, rows, dev, exchange="nccl")
-            exchange_note = f"nccl (p2p unavailable: {type(exc).__name__}: {str(exc)[:120]})"
+        runner, exchange_note = make_runner(args, PD, n1, n2, d, q, rows, dev)
         step = lambda s: runner.run(a, seed=s)  # noqa: E731
         finish = runner.finish
         ctx = D.context(dev)
@@ -256,14 +302,21 @@ def run_ours(args, world, rank, local):
         step(args.seed + i)
         finish()
     # one GPU: the whole factorization is captured once as a CUDA graph and
-    # each timed step is a replay with a new seed (every kernel runs again);
-    # N > 1 keeps the stream-ordered driver (its collectives sit between kernels)
-    graph = world == 1 and not args.no_graph
-    if graph:
+    # each timed step is a replay with a new seed (every kernel runs again).
+    # N > 1 with the NCCL exchange: the sharded step (kernels + NCCL
+    # collectives) is captured the same way, replayed with the captured seed;
+    # the p2p exchange stays stream-ordered (its spin targets are host-side
+    # epoch counters baked into the launches).
+    graph = not args.no_graph
+    graph_note = None
+    if graph and world == 1:
         plan.capture(a)
         for i in range(args.warmup):
             plan.replay(args.seed + 50 + i)
         finish()
+    elif graph:
+        graph_note = try_capture_dist(runner, a, args, finish)
+        graph = graph_note == "captured"
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.2)
@@ -274,15 +327,17 @@ def run_ours(args, world, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        if graph:
+        if graph and world == 1:
             plan.replay(args.seed + 100 + i)
+        elif graph:
+            runner.replay()
         else:
             step(args.seed + 100 + i)
     e1.record()
     torch.cuda.synchronize()
     clocks = sampler.stop()
     if graph:
-        launches = plan.graph_launches * args.steps
+        launches = (plan.graph_launches if world == 1 else runner.graph_launches) * args.steps
         finish()
         # per-kernel-class times: CUDA events around every launch of the same
         # steps, stream-ordered (events cannot sit between the graph's nodes)
@@ -401,12 +456,39 @@ def run_ours(args, world, rank, local):
         d2h = sum(x.numel() * 8 for x in (f.q_basis, f.l, f.p_basis, f.first_stage_r)) + 4 * (2 * q + 2)
         e2e = {"value": flops / t_e2e / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(n1 * n2 * 8),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": t_e2e * 1e3, "input": "pinned host torch tensor"}
+        # the reference's own calling convention: a (pageable) numpy array in,
+        # numpy factors out — staged through the plan's pinned ring
+        a_np = np.array(a_host.numpy())  # a pageable copy
+        pbp_qlp(a_np, d, q=q, seed=args.seed)  # warm (plan cache, pinned ring)
+        ts = []
+        for i in range(max(3, min(args.steps, 10))):
+            t0 = time.perf_counter()
+            f = pbp_qlp(a_np, d, q=q, seed=args.seed + 300 + i)
+            ts.append(time.perf_counter() - t0)
+        t_np = statistics.median(ts)
+        e2e["numpy"] = {"value": flops / t_np / 1e9, "unit": "GFLOP/s", "ms_per_step": t_np * 1e3,
+                        "h2d_bytes_per_step": int(n1 * n2 * 8), "d2h_bytes_per_step": int(d2h),
+                        "input": "pageable numpy float64 array (the reference's calling convention), staged through "
+                                 "a pinned ring overlapped with the H2D DMA and the first pass"}
+        del a_np, f
+        from paper_2103_07245_b200 import clear_plan_cache
+
+        clear_plan_cache()
+        torch.cuda.empty_cache()
+
+    # ---- config 4 (the north star's scaling shape) timed in the same run, so
+    # the driver's N = 1 and N > 1 lines both carry it
+    cfg4 = None
+    if args.workload == "cfg3" and not args.no_cfg4 and args.d is None and args.q is None:
+        a = None  # release config 3's A (the step closures hold the name, not the tensor)
+        torch.cuda.empty_cache()
+        cfg4 = time_cfg4(args, world, rank, dev, barrier)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        a_np = a_host.numpy() if e2e is not None else a.cpu().numpy()
+        a_np = a_host.numpy() if e2e is not None else workloads.make(args.workload, args.seed, dev).cpu().numpy()
         res = time_cpu_oracle(a_np, wl, args.seed, steps=3, budget_s=60.0)
-        cpu = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample", "host")}
 
     if rank == 0:
         line = {
@@ -417,11 +499,109 @@ def run_ours(args, world, rank, local):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "check": check,
         }
+        if cfg4 is not None:
+            line["cfg4"] = cfg4
+        if graph_note is not None:
+            line["graph"] = graph_note
         if world > 1:
             line["exchange"] = exchange_note
         if world > 1 and args.dist_backend != "nccl":
             line["validation_only"] = f"{args.dist_backend} collectives, ranks sharing GPUs: not a bench value"
         print(json.dumps(line), flush=True)
+
+
+def make_runner(args, PD, n1, n2, d, q, rows, dev):
+    """The row-sharded driver with the requested AᵀX exchange.  "p2p" (one
+    GPU per rank only) checks itself against NCCL at init and falls back."""
+    exchange = args.exchange
+    if exchange == "p2p" and args.dist_backend != "nccl":
+        raise SystemExit("--exchange p2p needs --dist-backend nccl (one GPU per rank)")
+    try:
+        runner = PD.DistributedPbpQlp(n1, n2, d, q, rows, dev, exchange=exchange)
+        note = runner.exchange_note
+    except Exception as exc:  # noqa: BLE001  symmetric memory unavailable: the NCCL exchange
+        runner = PD.DistributedPbpQlp(n1, n2, d, q, rows, dev, exchange="nccl")
+        note = f"nccl (p2p unavailable: {type(exc).__name__}: {str(exc)[:120]})"
+    return runner, note
+
+
+def try_capture_dist(runner, a, args, finish):
+    """Capture the sharded step as a CUDA graph (NCCL exchange only); returns
+    "captured" or why it stays stream-ordered."""
+    if runner.exchange != "nccl":
+        return "stream-ordered: the p2p exchange's spin targets are host-side epochs"
+    try:
+        runner.capture(a, seed=args.seed + 50)
+        for _ in range(args.warmup):
+            runner.replay()
+        finish()
+        return "captured"
+    except Exception as exc:  # noqa: BLE001
+        import torch
+
+        torch.cuda.synchronize()
+        return f"stream-ordered: capture failed ({type(exc).__name__}: {str(exc)[:120]})"
+
+
+def time_cfg4(args, world, rank, dev, barrier):
+    """Config 4 (200000x8192 fp64, d=512, q=1) — the north star's ≥6x-at-8-GPU
+    shape — timed like the main line: N = 1 as CUDA-graph replays, N > 1
+    row-sharded (same A split N ways; max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_07245_b200 import PbpQlpPlan, pbp_qlp_flops, workloads
+
+    n1, n2, d, q = 200000, 8192, 512, 1
+    flops = pbp_qlp_flops(n1, n2, d, q)
+    steps = max(3, min(args.steps, 5))
+    a = workloads.make_cfg4(args.seed, dev)
+    note = None
+    if world > 1:
+        from paper_2103_07245_b200 import distributed as PD
+
+        rows = PD.shard_rows(n1, world)
+        a = a[rows[rank]:rows[rank + 1]].contiguous()
+        torch.cuda.empty_cache()
+        runner, note = make_runner(args, PD, n1, n2, d, q, rows, dev)
+        runner.run(a, seed=args.seed)
+        runner.finish()
+        gnote = try_capture_dist(runner, a, args, runner.finish) if not args.no_graph else "stream-ordered"
+        step = runner.replay if gnote == "captured" else (lambda: runner.run(a, seed=args.seed))
+        fin = runner.finish
+    else:
+        plan = PbpQlpPlan(n1, n2, d, q, device=dev)
+        plan.run(a, seed=args.seed)
+        plan.finish()
+        plan.capture(a)
+        for i in range(args.warmup):
+            plan.replay(args.seed + 1 + i)
+        plan.finish()
+        gnote = "captured"
+        it = iter(range(10**9))
+        step = lambda: plan.replay(args.seed + 100 + next(it))  # noqa: E731
+        fin = plan.finish
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    fin()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = flops / (ms * 1e-3) / 1e9
+    out = {"workload": f"cfg4: A {n1}x{n2} fp64 synthetic (BASELINE config 4), d={d}, q={q}, seeded device sketch"
+                       + ("" if world == 1 else f", row-sharded x{world} (strong scaling)"),
+           "ms_per_step": ms, "value": value, "unit": "GFLOP/s", "steps": steps,
+           "frac_of_fp64_peak": value / 1e3 / FP64_PEAK_TFLOPS, "graph": gnote}
+    if note is not None:
+        out["exchange"] = note
+    return out
 
 
 def run_sibling(args):
@@ -430,7 +610,6 @@ def run_sibling(args):
     import numpy as np
     import torch
 
-    from oracle.pbp_qlp_oracle import oracle_cor_utv, oracle_r_svd
     from paper_2103_07245_b200 import workloads
     from paper_2103_07245_b200 import device as D
     from paper_2103_07245_b200.rsvd import r_svd, r_svd_flops
@@ -442,11 +621,11 @@ def run_sibling(args):
     n1, n2, d, q = wl["n1"], wl["n2"], wl["d"], wl["q"]
     k = min(n1, d)
     if args.path == "r_svd":
-        fn, oracle_fn, passes = r_svd, oracle_r_svd, 2 * q + 2
+        fn, passes = r_svd, 2 * q + 2
         flops = r_svd_flops(n1, n2, d, q)
         d2h = 8 * (n1 + n2 + 1) * k
     else:  # cor_utv with the exact core (2q + 3 passes), reference defaults
-        fn, oracle_fn, passes = cor_utv, oracle_cor_utv, 2 * q + 3
+        fn, passes = cor_utv, 2 * q + 3
         flops = cor_utv_flops(n1, n2, d, q)
         d2h = 8 * (n1 * k + k * d + n2 * d)
     a = workloads.make(args.workload, args.seed, dev)
@@ -491,13 +670,18 @@ def run_sibling(args):
         from threadpoolctl import threadpool_limits
 
         a_np = a.cpu().numpy()
-        with threadpool_limits(limits=cpu_threads()):
+        import warnings
+
+        ref_fn, kind, prov = reference_impl(args.path)
+        with threadpool_limits(limits=cpu_threads()), warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            ref_fn(a_np, d, q=q, seed=args.seed)  # discarded warm-up
             t0 = time.perf_counter()
-            oracle_fn(a_np, d, q=q, seed=args.seed)
+            ref_fn(a_np, d, q=q, seed=args.seed + 1)
             sec = time.perf_counter() - t0
-        cpu = {"value": flops / sec / 1e9, "unit": "GFLOP/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"one full {n1}x{n2} d={d} q={q} {args.path} ({sec:.3f} s; numpy/OpenBLAS "
-                         f"oracle_{args.path})"}
+        cpu = {"value": flops / sec / 1e9, "unit": "GFLOP/s", "cores": cpu_threads(), "kind": kind,
+               "sample": f"one full {n1}x{n2} d={d} q={q} {args.path} after one discarded ({sec:.3f} s; {prov}; "
+                         f"numpy/OpenBLAS)", "host": host_info()}
     # e2e: numpy in, numpy out through the public function
     e2e = None
     if not args.no_e2e:

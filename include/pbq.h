@@ -227,7 +227,8 @@ int pbq_second_stage_workspace_bytes(pbq_ctx* ctx, int64_t d, size_t* bytes);
  * pbq_xchg_expected_tiles(...) and the done counter by 64·world, so call k
  * (1-based) passes target = k·(that growth).  A rank's counter block is three
  * consecutive uint32 [tile count, done count, status]; a wait that has not
- * completed after 20 s sets status bit 0 and returns instead of hanging. */
+ * completed after 20 s (pbq_set_p2p_timeout_ms) sets status bit 0 and
+ * returns instead of hanging. */
 #define PBQ_XCHG_CTAS 64
 int pbq_gemm_tn_scatter(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                         int64_t ldb, double* const* land_ptrs, uint32_t* const* cnt_ptrs, int32_t rank, int32_t world,
@@ -238,6 +239,9 @@ int pbq_xchg_reduce(pbq_ctx* ctx, int32_t rank, int32_t world, int64_t n2, int64
                     uint32_t* const* done_ptrs, void* stream);
 int pbq_xchg_wait(pbq_ctx* ctx, const uint32_t* done, uint32_t target, void* stream);
 int pbq_xchg_expected_tiles(int64_t n2, int64_t N, int64_t S, int32_t rank, int32_t world, uint32_t* tiles);
+/* Spin limit (milliseconds, default 20000) of every peer-memory wait
+ * launched later on this context (the exchange's init self-check uses 2000). */
+int pbq_set_p2p_timeout_ms(pbq_ctx* ctx, int64_t ms);
 
 /* Small collectives on symmetric memory (the d×d Gram allreduces of the
  * distributed Cholesky-QR2 and the all-gather of orth(C)'s row slices):

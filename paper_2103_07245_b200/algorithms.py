@@ -27,7 +27,7 @@ from . import exceptions as _exc
 from .linalg import HostMatrix, from_device, householder_qr, to_device_matrix, warn_rank
 from .validation import check_index_range, check_seed, check_sketch_params
 
-__all__ = ["SketchRecord", "QlpFactors", "PbpQlpPlan", "pbp_qlp", "pbp_qlp_flops", "pbp_qlp_bytes"]
+__all__ = ["SketchRecord", "QlpFactors", "PbpQlpPlan", "pbp_qlp", "pbp_qlp_flops", "pbp_qlp_bytes", "clear_plan_cache"]
 
 
 class SketchRecord:
@@ -229,7 +229,14 @@ class PbpQlpPlan:
         """Factor a host (CPU) float64 tensor, streaming it to the device in
         row chunks on a copy stream while the first pass C = AᵀΦ accumulates
         chunk by chunk on the compute stream (β = 1 GEMM updates); the rest of
-        the pipeline starts from that C.  Returns the device copy of A."""
+        the pipeline starts from that C.  Returns the device copy of A.
+
+        Pinned input is copied by DMA straight from its pages.  Pageable
+        input (numpy arrays) goes through a ring of STAGE_SLOTS pinned
+        staging buffers: the host copies chunk i+1 into a free slot (torch's
+        multithreaded CPU copy) while the DMA engine moves chunk i, so the
+        link and host memory bandwidth overlap instead of the runtime's
+        synchronous pageable path (~10 GB/s)."""
         dev = self.device
         if tuple(host.shape) != (self.n1, self.n2):
             raise _exc.DimensionError(f"plan is for {(self.n1, self.n2)}, got {tuple(host.shape)}")
@@ -253,12 +260,31 @@ class PbpQlpPlan:
         _dev.gaussian(self.ctx, self.n1, self.d, seed, dev, out=self.PHI, status=self.sk_status)
         nchunks = max(1, min(int(chunks), self.n1 // max(self.d, 1)))
         bounds = [(self.n1 * i) // nchunks for i in range(nchunks + 1)]
+        pinned = host.is_pinned()
+        if not pinned:
+            rows_max = max(bounds[i + 1] - bounds[i] for i in range(nchunks))
+            ring = getattr(self, "stage", None)
+            if ring is None or ring[0].shape[0] < rows_max:
+                # pinned staging ring, kept with the plan (pinned allocations are slow)
+                self.stage = ring = [torch.empty((rows_max, self.n2), dtype=torch.float64, pin_memory=True)
+                                     for _ in range(STAGE_SLOTS)]
+                self.stage_ev = [None] * STAGE_SLOTS
         for i in range(nchunks):
             r0, r1 = bounds[i], bounds[i + 1]
+            if pinned:
+                src = host[r0:r1]
+            else:
+                k = i % STAGE_SLOTS
+                if self.stage_ev[k] is not None:
+                    self.stage_ev[k].synchronize()  # the DMA out of this slot has finished
+                src = ring[k][:r1 - r0]
+                src.copy_(host[r0:r1])
             with torch.cuda.stream(self.copy_stream):
-                A[r0:r1].copy_(host[r0:r1], non_blocking=True)
+                A[r0:r1].copy_(src, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self.copy_stream)
+            if not pinned:
+                self.stage_ev[k] = ev
             compute.wait_event(ev)
             _dev.gemm(self.ctx, A[r0:r1], self.PHI[r0:r1], trans_a=True, out=C0, beta=0.0 if i == 0 else 1.0,
                       nonfinite=self.flags[0:1])
@@ -274,6 +300,16 @@ class PbpQlpPlan:
         self.prob.c_init, self.prob.ldc_init = None, 0
         self._streamed = True
         return A
+
+    def detach_sketch(self):
+        """Hand the seeded sketch buffer to the caller (a SketchRecord) and
+        give the plan a fresh one, so a cached plan's next call cannot
+        overwrite a returned Φ."""
+        phi = self.PHI
+        if phi is not None:
+            self.PHI = _dev.empty_matrix(self.n1, self.d, self.device)
+            self.out.phi, self.out.ldphi = self.PHI.data_ptr(), self.PHI.stride(0)
+        return phi
 
     def run(self, A, seed=0, phi=None, _seed_dev=None):
         """Enqueue one factorization of the kernel-ready device matrix ``A``."""
@@ -351,6 +387,50 @@ class PbpQlpPlan:
 #: host inputs at least this large stream to the GPU in row chunks overlapped
 #: with the first pass (PbpQlpPlan.run_streamed)
 STREAM_MIN_BYTES = 64 << 20
+#: pinned staging buffers in the pageable-input ring of run_streamed
+STAGE_SLOTS = 3
+
+# Plans of recent host-input calls, keyed by device and problem shape: a plan
+# holds the device copy of A, the factor buffers, the workspace and the
+# pinned staging ring, so a repeated call of the same shape (the reference's
+# runtime protocol, an estimator refit) allocates nothing.  Only calls whose
+# results are copied back to the host use it (device callers get tensors
+# that alias the plan's buffers).  A plan is checked out while in use, so
+# concurrent calls never share one.  PBQ_PLAN_CACHE=0 disables it.
+_PLAN_CACHE = {}
+_PLAN_CACHE_MAX = 2
+_PLAN_LOCK = __import__("threading").Lock()
+
+
+def _plan_cache_enabled():
+    import os
+
+    return os.environ.get("PBQ_PLAN_CACHE", "1") != "0"
+
+
+def _checkout_plan(n1, n2, d, q, reorth, dev):
+    key = (torch.device(dev).index, n1, n2, d, q, bool(reorth))
+    if _plan_cache_enabled():
+        with _PLAN_LOCK:
+            plan = _PLAN_CACHE.pop(key, None)
+        if plan is not None:
+            return key, plan
+    return key, PbpQlpPlan(n1, n2, d, q, reorth, dev)
+
+
+def _checkin_plan(key, plan):
+    if not _plan_cache_enabled():
+        return
+    with _PLAN_LOCK:
+        _PLAN_CACHE[key] = plan
+        while len(_PLAN_CACHE) > _PLAN_CACHE_MAX:
+            _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+
+
+def clear_plan_cache():
+    """Release the cached host-input plans (device memory of A and the factors)."""
+    with _PLAN_LOCK:
+        _PLAN_CACHE.clear()
 
 
 def _to_host(t, kind, home):
@@ -386,9 +466,11 @@ def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, *, phi=None, device=None):
     kind, home = ha.kind, ha.home
     host = ha.host_tensor()
     streamed = host is not None and phi is None and n1 * n2 * 8 >= STREAM_MIN_BYTES and n1 >= 2 * d
+    host_side = not (kind == "torch" and home is not None and torch.device(home).type == "cuda")
+    key = None
     if streamed:
         dev = _dev.require_cuda(device)
-        plan = PbpQlpPlan(n1, n2, d, q, reorthonormalize, dev)
+        key, plan = _checkout_plan(n1, n2, d, q, reorthonormalize, dev)
         plan.run_streamed(host, seed)
         PHI = None
     else:
@@ -397,18 +479,25 @@ def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, *, phi=None, device=None):
         PHI = None
         if phi is not None:
             _, PHI, _, _ = to_device_matrix(phi, "phi", dev)
-        plan = PbpQlpPlan(n1, n2, d, q, reorthonormalize, dev, explicit_phi=phi is not None)
+        if host_side and phi is None:
+            key, plan = _checkout_plan(n1, n2, d, q, reorthonormalize, dev)
+        else:
+            plan = PbpQlpPlan(n1, n2, d, q, reorthonormalize, dev, explicit_phi=phi is not None)
         plan.run(A, seed, PHI)
-    host_side = not (kind == "torch" and home is not None and torch.device(home).type == "cuda")
     if host_side:
         outs = [_to_host(t, kind, home) for t in (plan.Q, plan.L, plan.P, plan.R)]
-    plan.finish(stacklevel=3)  # synchronises the stream (also completes the copies above)
+    try:
+        plan.finish(stacklevel=3)  # synchronises the stream (also completes the copies above)
+    finally:
+        phi_dev = PHI if PHI is not None else plan.detach_sketch() if key is not None else plan.PHI
+        if key is not None:
+            _checkin_plan(key, plan)
     if host_side:
         outs = [o.numpy() if kind == "numpy" else o for o in outs]
     else:
         outs = [from_device(t, kind, home) for t in (plan.Q, plan.L, plan.P, plan.R)]
     passes = 2 * q + 2
-    sketch = SketchRecord(PHI if PHI is not None else plan.PHI, kind, seed, d, q, passes, home)
+    sketch = SketchRecord(phi_dev, kind, seed, d, q, passes, home)
     if phi is not None and kind == "numpy":
         sketch._host = np.asarray(phi, dtype=np.float64)
     return QlpFactors(outs[0], outs[1], outs[2], outs[3], sketch)

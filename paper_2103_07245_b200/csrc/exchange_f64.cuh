@@ -47,17 +47,19 @@ struct XchgScatter {
   int rank, world;
 };
 
-// Spin until *p ≥ target, at most PBQ_XCHG_TIMEOUT_NS: a peer that never
-// arrives (a broken peer mapping, a rank that died) must not hang the GPU.
-// On timeout *status |= 1 (the host raises); the caller then proceeds.
+// Spin until *p ≥ target, at most `timeout_ns` (pbq_set_p2p_timeout_ms,
+// default 20 s): a peer that never arrives (a broken peer mapping, a rank
+// that died) must not hang the GPU.  On timeout *status |= 1 (the host
+// raises and poisons the exchange); the caller then proceeds.
 #define PBQ_XCHG_TIMEOUT_NS 20000000000ull
-__device__ __forceinline__ void xchg_spin(const unsigned int* p, unsigned int target, unsigned int* status) {
+__device__ __forceinline__ void xchg_spin(const unsigned int* p, unsigned int target, unsigned int* status,
+                                          unsigned long long timeout_ns) {
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   while (ld_acquire_sys_u32(p) < target) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > PBQ_XCHG_TIMEOUT_NS) {
+    if (t - t0 > timeout_ns) {
       atomicOr(status, 1u);
       return;
     }
@@ -67,18 +69,38 @@ __device__ __forceinline__ void xchg_spin(const unsigned int* p, unsigned int ta
 
 // Sum of the G landing slots of this rank's slice → every rank's C.  The
 // counter block of a rank is [tile count, done count, status].
+// One warp per row (rows strided over the grid's warps), lanes over column
+// pairs: 16-byte volatile loads of the G slots (written by peers) and 16-byte
+// stores to every rank's C, no per-element index division.  ldl and ldc are
+// even and the bases 16-byte aligned; an odd n ends in one scalar column.
 __global__ void __launch_bounds__(256) xchg_reduce_kernel(const double* __restrict__ land, long ldl, int world, long S,
                                                           long rows, long n, double* const* c_ptrs, long ldc,
                                                           long row0, const unsigned int* cnt, unsigned int target,
-                                                          unsigned int* const* done_ptrs) {
-  if (threadIdx.x == 0) xchg_spin(cnt, target, const_cast<unsigned int*>(cnt) + 2);
+                                                          unsigned int* const* done_ptrs,
+                                                          unsigned long long timeout_ns) {
+  if (threadIdx.x == 0) xchg_spin(cnt, target, const_cast<unsigned int*>(cnt) + 2, timeout_ns);
   __syncthreads();
-  const long total = rows * n;
-  for (long e = long(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += long(gridDim.x) * blockDim.x) {
-    const long i = e / n, j = e % n;
-    double s = 0.0;
-    for (int g = 0; g < world; ++g) s += __ldcv(land + (long(g) * S + i) * ldl + j);  // slot order
-    for (int p = 0; p < world; ++p) c_ptrs[p][(row0 + i) * ldc + j] = s;
+  const int lane = threadIdx.x & 31;
+  const long warp = (long(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = (long(gridDim.x) * blockDim.x) >> 5;
+  const long pairs = n >> 1;
+  for (long i = warp; i < rows; i += nwarps) {
+    const double* src = land + i * ldl;
+    const long crow = (row0 + i) * ldc;
+    for (long jp = lane; jp < pairs; jp += 32) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int g = 0; g < world; ++g) {  // slot order: the same bits on every rank
+        const double2 v = __ldcv(reinterpret_cast<const double2*>(src + long(g) * S * ldl) + jp);
+        s.x += v.x;
+        s.y += v.y;
+      }
+      for (int p = 0; p < world; ++p) reinterpret_cast<double2*>(c_ptrs[p] + crow)[jp] = s;
+    }
+    if ((n & 1) && lane == 0) {
+      double s = 0.0;
+      for (int g = 0; g < world; ++g) s += __ldcv(src + long(g) * S * ldl + n - 1);
+      for (int p = 0; p < world; ++p) c_ptrs[p][crow + n - 1] = s;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -94,12 +116,26 @@ __global__ void __launch_bounds__(256) xchg_reduce_kernel(const double* __restri
 //   p2p_sum_kernel:  wait for the counter, out = Σ_g slots[g·slot] in slot
 //     order (the same bits on every rank).
 // An all-gather is a push with slot = the slice size into C itself plus a
-// wait (xchg_wait_kernel on that counter).
+// wait (xchg_wait_kernel on that counter).  Both move 16-byte pairs when
+// every base and the slot are 16-byte aligned (checked by the host), with a
+// scalar tail for odd n.
+template <bool VEC>
 __global__ void __launch_bounds__(256) p2p_push_kernel(const double* __restrict__ src, long n, double* const* dst_ptrs,
                                                        long slot, int rank, int world, unsigned int* const* cnt_ptrs) {
-  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
-    const double v = src[i];
-    for (int p = 0; p < world; ++p) dst_ptrs[p][long(rank) * slot + i] = v;
+  const long t0 = long(blockIdx.x) * blockDim.x + threadIdx.x, nt = long(gridDim.x) * blockDim.x;
+  if (VEC) {
+    const long pairs = n >> 1;
+    for (long i = t0; i < pairs; i += nt) {
+      const double2 v = reinterpret_cast<const double2*>(src)[i];
+      for (int p = 0; p < world; ++p) reinterpret_cast<double2*>(dst_ptrs[p] + long(rank) * slot)[i] = v;
+    }
+    if ((n & 1) && t0 == 0)
+      for (int p = 0; p < world; ++p) dst_ptrs[p][long(rank) * slot + n - 1] = src[n - 1];
+  } else {
+    for (long i = t0; i < n; i += nt) {
+      const double v = src[i];
+      for (int p = 0; p < world; ++p) dst_ptrs[p][long(rank) * slot + i] = v;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -108,25 +144,47 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(const double* __restrict_
   }
 }
 
+template <bool VEC>
 __global__ void __launch_bounds__(256) p2p_sum_kernel(const double* __restrict__ slots, long slot, int world, long n,
                                                       double* __restrict__ out, const unsigned int* cnt,
-                                                      unsigned int target, unsigned int* status) {
-  if (threadIdx.x == 0) xchg_spin(cnt, target, status);
+                                                      unsigned int target, unsigned int* status,
+                                                      unsigned long long timeout_ns) {
+  if (threadIdx.x == 0) xchg_spin(cnt, target, status, timeout_ns);
   __syncthreads();
-  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
-    double s = 0.0;
-    for (int g = 0; g < world; ++g) s += __ldcv(slots + long(g) * slot + i);
-    out[i] = s;
+  const long t0 = long(blockIdx.x) * blockDim.x + threadIdx.x, nt = long(gridDim.x) * blockDim.x;
+  if (VEC) {
+    const long pairs = n >> 1;
+    for (long i = t0; i < pairs; i += nt) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int g = 0; g < world; ++g) {
+        const double2 v = __ldcv(reinterpret_cast<const double2*>(slots + long(g) * slot) + i);
+        s.x += v.x;
+        s.y += v.y;
+      }
+      reinterpret_cast<double2*>(out)[i] = s;
+    }
+    if ((n & 1) && t0 == 0) {
+      double s = 0.0;
+      for (int g = 0; g < world; ++g) s += __ldcv(slots + long(g) * slot + n - 1);
+      out[n - 1] = s;
+    }
+  } else {
+    for (long i = t0; i < n; i += nt) {
+      double s = 0.0;
+      for (int g = 0; g < world; ++g) s += __ldcv(slots + long(g) * slot + i);
+      out[i] = s;
+    }
   }
 }
 
-__global__ void p2p_wait_kernel(const unsigned int* cnt, unsigned int target, unsigned int* status) {
-  if (threadIdx.x == 0) xchg_spin(cnt, target, status);
+__global__ void p2p_wait_kernel(const unsigned int* cnt, unsigned int target, unsigned int* status,
+                                unsigned long long timeout_ns) {
+  if (threadIdx.x == 0) xchg_spin(cnt, target, status, timeout_ns);
   __syncthreads();
 }
 
-__global__ void xchg_wait_kernel(const unsigned int* done, unsigned int target) {
-  if (threadIdx.x == 0) xchg_spin(done, target, const_cast<unsigned int*>(done) + 1);
+__global__ void xchg_wait_kernel(const unsigned int* done, unsigned int target, unsigned long long timeout_ns) {
+  if (threadIdx.x == 0) xchg_spin(done, target, const_cast<unsigned int*>(done) + 1, timeout_ns);
   __syncthreads();
 }
 

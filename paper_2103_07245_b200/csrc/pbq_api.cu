@@ -57,6 +57,7 @@ struct pbq_ctx {
   std::vector<std::pair<cudaStream_t, int*>> stream_flags;
   std::vector<int*> flag_blocks;  // cudaMalloc'd batches backing stream_flags
   size_t flag_free = 0;           // unassigned arrays left in flag_blocks.back()
+  unsigned long long p2p_timeout_ns = PBQ_XCHG_TIMEOUT_NS;  // spin limit of the peer-memory waits
   char err[512] = {0};
 };
 
@@ -1280,8 +1281,9 @@ int pbq_xchg_reduce(pbq_ctx* ctx, int32_t rank, int32_t world, int64_t n2, int64
   if (world < 1 || rank < 0 || rank >= world || S < 1) return fail(ctx, PBQ_ERR_PARAM, "xchg_reduce: bad arguments");
   const long row0 = long(rank) * S;
   const long rows = std::max<long>(0, std::min<long>(S, n2 - row0));
+  if ((ldl & 1) || (ldc & 1) || !aligned16(land)) return fail(ctx, PBQ_ERR_PARAM, "xchg_reduce: ldl/ldc must be even, land 16-byte aligned");
   xchg_reduce_kernel<<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      land, ldl, world, S, rows, N, c_ptrs, ldc, row0, cnt, target, done_ptrs);
+      land, ldl, world, S, rows, N, c_ptrs, ldc, row0, cnt, target, done_ptrs, ctx->p2p_timeout_ns);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 1;
   return PBQ_OK;
@@ -1291,8 +1293,15 @@ int pbq_p2p_push(pbq_ctx* ctx, const double* src, int64_t n, double* const* dst_
                  int32_t world, uint32_t* const* cnt_ptrs, void* stream) {
   if (!ctx || !src || !dst_ptrs || !cnt_ptrs) return PBQ_ERR_PARAM;
   if (world < 1 || rank < 0 || rank >= world || n < 0) return fail(ctx, PBQ_ERR_PARAM, "p2p_push: bad arguments");
-  p2p_push_kernel<<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, n, dst_ptrs, slot, rank, world,
-                                                                                cnt_ptrs);
+  // 16-byte pairs when src and every destination slot are aligned (the
+  // peers' bases come from one symmetric allocation layout: check slot parity
+  // and src here, the peer bases are 16-byte aligned allocations)
+  if (aligned16(src) && !(slot & 1))
+    p2p_push_kernel<true><<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, n, dst_ptrs, slot, rank,
+                                                                                      world, cnt_ptrs);
+  else
+    p2p_push_kernel<false><<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, n, dst_ptrs, slot, rank,
+                                                                                       world, cnt_ptrs);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 1;
   return PBQ_OK;
@@ -1302,8 +1311,12 @@ int pbq_p2p_sum(pbq_ctx* ctx, const double* slots, int64_t slot, int32_t world, 
                 const uint32_t* cnt, uint32_t target, uint32_t* status, void* stream) {
   if (!ctx || !slots || !out || !cnt || !status) return PBQ_ERR_PARAM;
   if (world < 1 || n < 0) return fail(ctx, PBQ_ERR_PARAM, "p2p_sum: bad arguments");
-  p2p_sum_kernel<<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(slots, slot, world, n, out, cnt, target,
-                                                                               status);
+  if (aligned16(slots) && aligned16(out) && !(slot & 1))
+    p2p_sum_kernel<true><<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(slots, slot, world, n, out, cnt,
+                                                                                     target, status, ctx->p2p_timeout_ns);
+  else
+    p2p_sum_kernel<false><<<PBQ_XCHG_CTAS, 256, 0, static_cast<cudaStream_t>(stream)>>>(slots, slot, world, n, out, cnt,
+                                                                                      target, status, ctx->p2p_timeout_ns);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 1;
   return PBQ_OK;
@@ -1311,7 +1324,7 @@ int pbq_p2p_sum(pbq_ctx* ctx, const double* slots, int64_t slot, int32_t world, 
 
 int pbq_p2p_wait(pbq_ctx* ctx, const uint32_t* cnt, uint32_t target, uint32_t* status, void* stream) {
   if (!ctx || !cnt || !status) return PBQ_ERR_PARAM;
-  p2p_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(cnt, target, status);
+  p2p_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(cnt, target, status, ctx->p2p_timeout_ns);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 1;
   return PBQ_OK;
@@ -1319,9 +1332,15 @@ int pbq_p2p_wait(pbq_ctx* ctx, const uint32_t* cnt, uint32_t target, uint32_t* s
 
 int pbq_xchg_wait(pbq_ctx* ctx, const uint32_t* done, uint32_t target, void* stream) {
   if (!ctx || !done) return PBQ_ERR_PARAM;
-  xchg_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(done, target);
+  xchg_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(done, target, ctx->p2p_timeout_ns);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += 1;
+  return PBQ_OK;
+}
+
+int pbq_set_p2p_timeout_ms(pbq_ctx* ctx, int64_t ms) {
+  if (!ctx || ms < 1) return PBQ_ERR_PARAM;
+  ctx->p2p_timeout_ns = (unsigned long long)ms * 1000000ull;
   return PBQ_OK;
 }
 

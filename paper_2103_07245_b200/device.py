@@ -50,6 +50,11 @@ class Context:
         with self.lock:
             self.check(self.lib.pbq_set_qr_method(self.handle, int(method)), "set_qr_method")
 
+    def set_p2p_timeout_ms(self, ms):
+        """Spin limit of the peer-memory waits launched from now on (default 20 s)."""
+        with self.lock:
+            self.check(self.lib.pbq_set_p2p_timeout_ms(self.handle, int(ms)), "set_p2p_timeout_ms")
+
     def cholqr_stats(self, stats):
         """Count [Cholesky-QR completions, Householder fallbacks, series last pass,
         shifted-route completions] into the

@@ -270,22 +270,23 @@ class DistributedPbpQlp:
         if exchange == "p2p" and not hasattr(be, "xchg_init"):
             raise _exc.ParameterError("this backend has no peer-memory exchange")
         self.exchange = exchange
-        self.xchg = be.xchg_init(self.n2, self.d, group) if exchange == "p2p" else None
         self.epoch = 0    # AᵀX exchanges
         self.ep_gram = 0  # Gram allreduces (p2p)
         self.ep_ag = 0    # all-gathers of orth(C) slices (p2p)
-        # AᵀX partial → allreduced → P̄ (in place).  G·s rows (s = ⌈n2/G⌉, for
-        # p2p rounded to the 128-row tile) so that orth(C) can run on equal
-        # row slices; rows ≥ n2 stay zero.
+        self.poisoned = None  # set when a peer-memory wait timed out: the counters are no longer consistent
+        self.xchg = be.xchg_init(self.n2, self.d, group) if exchange == "p2p" else None
+        self._setup_c()
+        self.exchange_note = exchange
         if self.xchg is not None:
-            self.slice_rows = self.xchg.S
-            self.Cbuf = self.xchg.C[:, :self.d]
-        else:
-            self.slice_rows = -(-self.n2 // self.world)
-            self.Cbuf = be.empty(self.world * self.slice_rows, self.d)
-            ldc = self.Cbuf.stride(0)
-            self.Cbuf.as_strided((self.Cbuf.shape[0], ldc), (ldc, 1)).zero_()  # incl. the even-ld pad column
-        self.C = self.Cbuf[:self.n2]
+            ok, why = self._p2p_self_check()
+            if not ok:  # the whole group agreed (allreduce MIN): every rank falls back together
+                self.xchg = None
+                self.exchange = "nccl"
+                self.epoch = self.ep_gram = self.ep_ag = 0
+                self._setup_c()
+                self.exchange_note = f"nccl (p2p self-check failed: {why})"
+            else:
+                self.exchange_note = f"p2p (self-check vs NCCL allreduce passed: {why})"
         self.Q = be.empty(self.m, self.d)          # A_g·P̄ → local Q_g → Q rows of this rank
         self.R = be.empty(self.d, self.d)
         self.Rloc = be.empty(self.d, self.d)
@@ -315,6 +316,86 @@ class DistributedPbpQlp:
         self.c_state = (be.cholqr2_dist_state(self.slice_rows, self.d)
                         if use_cq and self.world > 1 and self.slice_rows >= self.d else None)
         self.orth_fallbacks = 0
+
+    def _setup_c(self):
+        """AᵀX partial → allreduced → P̄ (in place).  G·s rows (s = ⌈n2/G⌉, for
+        p2p rounded to the 128-row tile) so that orth(C) can run on equal row
+        slices; rows ≥ n2 stay zero."""
+        if self.xchg is not None:
+            self.slice_rows = self.xchg.S
+            self.Cbuf = self.xchg.C[:, :self.d]
+        else:
+            self.slice_rows = -(-self.n2 // self.world)
+            self.Cbuf = self.be.empty(self.world * self.slice_rows, self.d)
+            ldc = self.Cbuf.stride(0)
+            self.Cbuf.as_strided((self.Cbuf.shape[0], ldc), (ldc, 1)).zero_()  # incl. the even-ld pad column
+        self.C = self.Cbuf[:self.n2]
+
+    def _p2p_self_check(self, timeout_ms=2000):
+        """Run one small AᵀX exchange, one Gram allreduce and one all-gather
+        over peer memory with a short spin limit, and compare them with NCCL
+        collectives of the same data.  Returns (ok, note), identical on every
+        rank (the verdict is combined with an allreduce(MIN)); a mismatch or a
+        timeout makes the caller fall back to the NCCL exchange."""
+        import time
+
+        be, x = self.be, self.xchg
+        dev = x.land.device
+        g = torch.Generator(device=dev)
+        g.manual_seed(1000 + self.rank)
+        k = 256  # rows of this rank's probe block
+        a = torch.randn(k, self.n2, dtype=torch.float64, device=dev, generator=g)
+        a = be.contiguous(a)
+        xb = be.contiguous(torch.randn(k, self.d, dtype=torch.float64, device=dev, generator=g))
+        ok, why = True, ""
+        ctx = getattr(be, "ctx", None)
+        if ctx is not None:
+            ctx.set_p2p_timeout_ms(timeout_ms)
+        t0 = time.perf_counter()
+        try:
+            # AᵀX: fused scatter GEMM + slice reduce + all-gather
+            self.epoch += 1
+            be.xchg_at_x(x, a, xb, self.n2, self.epoch)
+            got = self.C.clone()
+            ref = be.empty(self.n2, self.d)
+            be.gemm_tn(a, xb, ref)
+            ref = ref.contiguous()
+            dist.all_reduce(ref, op=dist.ReduceOp.SUM, group=self.group)
+            # Gram allreduce (push + slot-ordered sum)
+            np_ = int(round(x.gram_slot ** 0.5))
+            gram = torch.randn(np_, np_, dtype=torch.float64, device=dev, generator=g)
+            gref = gram.clone()
+            self.ep_gram += 1
+            be.p2p_allreduce(x, gram, self.ep_gram)
+            dist.all_reduce(gref, op=dist.ReduceOp.SUM, group=self.group)
+            if dev.type == "cuda":
+                torch.cuda.synchronize(dev)
+            # every spin (tile count, done count, Gram pushes) ORs into the status word
+            if int(x.status.item()):
+                ok, why = False, "a peer did not arrive within %d ms" % timeout_ms
+            else:
+                scale = float(ref.abs().max()) or 1.0
+                err = float((got - ref).abs().max()) / scale
+                gerr = float((gram - gref).abs().max()) / (float(gref.abs().max()) or 1.0)
+                if not (err <= 1e-12 and gerr <= 1e-12):
+                    ok, why = False, f"results differ from NCCL (AᵀX rel err {err:.2e}, Gram {gerr:.2e})"
+                else:
+                    why = f"AᵀX rel err {err:.1e}, Gram {gerr:.1e}, {1e3 * (time.perf_counter() - t0):.0f} ms"
+        except Exception as exc:  # noqa: BLE001  (e.g. an illegal peer address)
+            ok, why = False, f"{type(exc).__name__}: {str(exc)[:100]}"
+        finally:
+            if ctx is not None:
+                ctx.set_p2p_timeout_ms(20000)
+        verdict = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(verdict, op=dist.ReduceOp.MIN, group=self.group)
+        if ok and not int(verdict.item()):
+            ok, why = False, "another rank's check failed"
+        return ok, why
+
+    def _check_usable(self):
+        if self.poisoned:
+            raise _exc.DeviceError(f"p2p exchange unusable after an earlier failure ({self.poisoned}); "
+                                   "create a new DistributedPbpQlp")
 
     # -- collectives ---------------------------------------------------------
     def _chunk_bounds(self):
@@ -433,6 +514,7 @@ class DistributedPbpQlp:
     # -- the algorithm ------------------------------------------------------
     def run(self, A_local, seed=0, phi_local=None):
         """Enqueue one factorization of this rank's rows (kernel-ready operand)."""
+        self._check_usable()
         be = self.be
         d, q = self.d, self.q
         self._last = (A_local, seed, phi_local)
@@ -469,13 +551,46 @@ class DistributedPbpQlp:
             be.transpose(self.Rt, self.L, lower=True)
         be.gemm_nn(self.C, self.W, self.P)
 
+    # -- CUDA graph of one sharded step --------------------------------------
+    def capture(self, A_local, seed=0, phi_local=None):
+        """Capture one ``run`` (kernels and NCCL collectives; every rank must
+        call it) into a CUDA graph that ``replay`` relaunches with one call.
+        The sketch seed is the captured one.  Only the NCCL exchange can be
+        captured: the p2p exchange's spin targets are host-side epoch counts."""
+        if self.xchg is not None:
+            raise _exc.ParameterError("capture needs the NCCL exchange")
+        dev = self.be.device
+        self.run(A_local, seed, phi_local)  # warm: allocations, NCCL communicator, lazy loads
+        self.finish()
+        ctx = getattr(self.be, "ctx", None)
+        launches0 = ctx.launch_count if ctx is not None else 0
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            self.run(A_local, seed, phi_local)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.graph_launches = (ctx.launch_count - launches0) if ctx is not None else 0
+        self.graph = graph
+        self.finish()
+        return graph
+
+    def replay(self):
+        """Relaunch the captured step (``finish`` reads its flags as usual)."""
+        self._check_usable()
+        self.graph.replay()
+
     def finish(self, stacklevel=3):
         """Synchronise, raise / warn like the reference (every rank)."""
         # a non-finite entry in any shard fails every rank
         dist.all_reduce(self.flags[0:2], op=dist.ReduceOp.MAX, group=self.group)
         dist.all_reduce(self.flags[-1:], op=dist.ReduceOp.MAX, group=self.group)  # same on every rank anyway
         if self.xchg is not None and int(self.xchg.status.item()):
-            raise _exc.DeviceError("p2p AᵀX exchange: a peer did not arrive within 20 s")
+            # a late peer's increments could satisfy a later call's targets:
+            # this exchange's counters are no longer consistent
+            self.poisoned = "a peer did not arrive within the spin limit"
+            raise _exc.DeviceError("p2p AᵀX exchange: a peer did not arrive within 20 s; the exchange is now "
+                                   "unusable (create a new DistributedPbpQlp)")
         fl = self.flags.cpu().tolist()
         if fl[0]:
             raise _exc.MatrixInputError("a contains non-finite entries")

@@ -84,3 +84,59 @@ class NumpyBackend:
         a.copy_(torch.from_numpy(sla.solve_triangular(r2, state["q1"].T, trans="T", lower=False).T))
         if flag is not None:
             flag.fill_(rank_flag(rr))
+
+
+class FakeP2PBackend(NumpyBackend):
+    """NumpyBackend plus a stand-in for the peer-memory exchange
+    (CudaBackend.xchg_init / xchg_at_x / p2p_allreduce / p2p_allgather_rows),
+    its data movement done with gloo collectives.  ``fault`` injects the
+    failures the exchange's init self-check must catch:
+      None       a working transport;
+      "wrong"    rank 1's AᵀX result is corrupted (a broken peer mapping);
+      "timeout"  rank 0's status word reports a spin timeout."""
+
+    def __init__(self, fault=None):
+        self.fault = fault
+
+    def xchg_init(self, n2, d, group):
+        import torch.distributed as dist
+
+        from paper_2103_07245_b200.distributed import _XchgBuffers, _gram_np, xchg_slice_rows
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        S, ldl = xchg_slice_rows(n2, world), d + (d & 1)
+        land = torch.zeros(world * S * ldl, dtype=torch.float64)
+        c = torch.zeros(world * S * ldl, dtype=torch.float64)
+        ctr = torch.zeros(64, dtype=torch.int32)
+        gram = torch.zeros(2 * world * _gram_np(d) ** 2, dtype=torch.float64)
+        x = _XchgBuffers(rank, world, S, ldl, land, c, ctr, gram)
+        x.group = group
+        return x
+
+    def xchg_at_x(self, xchg, a, x, n2, epoch, nonfinite=None):
+        import torch.distributed as dist
+
+        d = x.shape[1]
+        part = torch.from_numpy(a.numpy().T @ x.numpy())
+        if nonfinite is not None and not torch.isfinite(a).all():
+            nonfinite.fill_(1)
+        dist.all_reduce(part, op=dist.ReduceOp.SUM, group=xchg.group)
+        if self.fault == "wrong" and xchg.rank == 1:
+            part[0, 0] += 1.0
+        if self.fault == "timeout" and xchg.rank == 0:
+            xchg.status.fill_(1)
+        xchg.C[:n2, :d].copy_(part)
+
+    def p2p_allreduce(self, xchg, g, epoch):
+        import torch.distributed as dist
+
+        dist.all_reduce(g, op=dist.ReduceOp.SUM, group=xchg.group)
+
+    def p2p_allgather_rows(self, xchg, epoch):
+        import torch.distributed as dist
+
+        S = xchg.S
+        mine = xchg.C[xchg.rank * S:(xchg.rank + 1) * S].contiguous()
+        parts = [torch.empty_like(mine) for _ in range(xchg.world)]
+        dist.all_gather(parts, mine, group=xchg.group)
+        xchg.C.copy_(torch.cat(parts, 0))

@@ -213,6 +213,16 @@ def test_distributed_driver_on_one_gpu(cuda):
             assert np.all(column_relative_error(qg, ref.q_basis) <= tol)
             assert np.all(column_relative_error(p, ref.p_basis) <= tol)
             assert np.allclose(np.diag(l), np.diag(ref.l), rtol=1e-10, atol=0)
+            # the same step captured as a CUDA graph (kernels + NCCL
+            # collectives) and replayed: bitwise the stream-ordered result
+            run.capture(at, seed=7)
+            for t in run.factors():
+                t.fill_(float("nan"))
+            run.replay()
+            run.finish()
+            for x, y in zip((t.cpu().numpy() for t in run.factors()), (qg, l, p, r)):
+                assert np.array_equal(x, y)
+            assert run.graph_launches > 0
     finally:
         dist.destroy_process_group()
 

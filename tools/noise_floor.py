@@ -1,0 +1,98 @@
+"""Intrinsic rounding sensitivity of the reference's PbP-QLP factors, per
+column, at full BASELINE size (run on the GPU box):
+
+  python tools/noise_floor.py --workload cfg5 --d 512 --q 0 [--out gpurun_out/nf.npz]
+
+Three factorizations of the SAME A and Φ:
+  ref  the oracle (bitwise the reference's call sequence, numpy/OpenBLAS);
+  alt  the same call sequence with every product's summation split in two
+       halves of its reduction dimension (a legitimate reordering: each
+       product is still a backward-stable FP64 dgemm);
+  gpu  this package's pbp_qlp on the device.
+Per column j it records the sign-normalised column errors of Q and P and
+|ΔL_jj|/L_jj of alt-vs-ref and gpu-vs-ref, with κ_j = L_00/L_jj and the
+relative gap to the neighbouring L values — the data behind the parity
+tolerance of tests/test_gpu_configs.py."""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from oracle.pbp_qlp_oracle import column_relative_error, oracle_gaussian, oracle_pbp_qlp, oracle_qr  # noqa: E402
+
+
+def reordered_pbp_qlp(a, d, q, phi):
+    """oracle_pbp_qlp with the reduction of every product split in two."""
+    n1, n2 = a.shape
+    h1, h2 = n1 // 2, n2 // 2
+
+    def apply(x):  # a @ x, reduction over n2
+        return a[:, :h2] @ x[:h2] + a[:, h2:] @ x[h2:]
+
+    def apply_t(x):  # a.T @ x, reduction over n1
+        return a[:h1].T @ x[:h1] + a[h1:].T @ x[h1:]
+
+    pbar, _ = oracle_qr(apply_t(phi))
+    for _ in range(q):
+        pbar, _ = oracle_qr(apply(pbar))
+        pbar, _ = oracle_qr(apply_t(pbar))
+    qf, r = oracle_qr(apply(pbar))
+    w, rt = oracle_qr(r.T)
+    return {"q": qf, "l": np.tril(rt.T), "p": pbar @ w}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="cfg5")
+    ap.add_argument("--d", type=int, nargs="+", default=[512])
+    ap.add_argument("--q", type=int, nargs="+", default=[0])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--out", default="gpurun_out/noise_floor")
+    args = ap.parse_args()
+    import torch
+
+    from paper_2103_07245_b200 import pbp_qlp, workloads
+
+    a_dev = workloads.make(args.workload, args.seed, "cuda")
+    a = a_dev.cpu().numpy()
+    for d in args.d:
+        phi = oracle_gaussian(a.shape[0], d, args.seed)
+        for q in args.q:
+            t0 = time.time()
+            ref = oracle_pbp_qlp(a, d, q=q, seed=args.seed, phi=phi)
+            alt = reordered_pbp_qlp(a, d, q, phi)
+            got = pbp_qlp(a_dev, d, q=q, seed=args.seed)
+            gq, gl, gp = (x.cpu().numpy() for x in (got.q_basis, got.l, got.p_basis))
+            lref = np.abs(np.diag(ref["l"]))
+            kappa = lref[0] / lref
+            gap = np.full(d, np.inf)
+            rel = np.abs(np.diff(lref)) / lref[1:]
+            gap[1:] = rel
+            gap[:-1] = np.minimum(gap[:-1], rel)
+            rec = {
+                "kappa": kappa, "l": lref, "relgap": gap,
+                "alt_q": column_relative_error(alt["q"], ref["q"]), "alt_p": column_relative_error(alt["p"], ref["p"]),
+                "alt_l": np.abs(np.abs(np.diag(alt["l"])) - lref) / lref,
+                "gpu_q": column_relative_error(gq, ref["q"]), "gpu_p": column_relative_error(gp, ref["p"]),
+                "gpu_l": np.abs(np.abs(np.diag(gl)) - lref) / lref,
+            }
+            os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+            np.savez(f"{args.out}_{args.workload}_d{d}_q{q}.npz", **rec)
+            u = 2.0 ** -53
+            for k in ("q", "p", "l"):
+                ga, al = rec[f"gpu_{k}"], rec[f"alt_{k}"]
+                print(f"{args.workload} d={d} q={q} {k.upper()}: gpu max {ga.max():.2e} (col {ga.argmax()}), "
+                      f"alt max {al.max():.2e} (col {al.argmax()}); max gpu/(u·κ) {np.max(ga / (u * kappa)):.1f}, "
+                      f"max alt/(u·κ) {np.max(al / (u * kappa)):.1f}; max gpu/max(alt,1e-16) per col "
+                      f"{np.max(ga / np.maximum(al, 1e-16)):.1f}", flush=True)
+            print(f"  ({time.time() - t0:.0f} s)", flush=True)
+            del got
+            torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

@@ -5,8 +5,8 @@ Drop-in for the reference package's PbP-QLP path (``pbpqlp.pbp_qlp``,
 arguments, errors, warnings and result fields; every FLOP runs in
 hand-written sm_100a CUDA behind the C ABI in include/pbq.h.
 """
-from .algorithms import (PbpQlpPlan, QlpFactors, SketchRecord, pbp_qlp, pbp_qlp_bytes, pbp_qlp_flops,
-                         reconstruction_error, residual_norms)
+from .algorithms import (PbpQlpPlan, QlpFactors, SketchRecord, clear_plan_cache, pbp_qlp, pbp_qlp_bytes,
+                         pbp_qlp_flops, reconstruction_error, residual_norms)
 from .exceptions import (ConvergenceError, DeviceError, DimensionError, MatrixInputError, ParameterError,
                          RankDeficiencyWarning)
 from .linalg import QrFactors, column_pivoted_qr, gaussian_matrix, householder_qr, orth
@@ -28,6 +28,7 @@ __all__ = [
     "RsvdFactors",
     "SketchRecord",
     "UtvFactors",
+    "clear_plan_cache",
     "column_pivoted_qr",
     "cor_utv",
     "gaussian_matrix",

@@ -100,7 +100,7 @@ def _worker(rank, world, port, a, d, q, seed, outdir, reps=2):
                 run.finish()
         qg, l, p, r = (t.cpu().numpy() for t in run.factors())
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), q=qg, l=l, p=p, epoch=run.epoch, tsqr=run.tsqr_fallbacks,
-                 warn=len(rec))
+                 warn=len(rec), exchange=run.exchange, note=run.exchange_note)
     finally:
         dist.destroy_process_group()
 
@@ -114,7 +114,10 @@ def test_p2p_driver_world1_matches_oracle(cuda, tmp_path):
     a = rng.standard_normal((n1, 60)) @ rng.standard_normal((60, n2)) / 8 + 1e-3 * rng.standard_normal((n1, n2))
     mp.spawn(_worker, args=(1, _free_port(), a, d, q, 9, str(tmp_path)), nprocs=1, join=True)
     part = np.load(os.path.join(tmp_path, "rank0.npz"))
-    assert int(part["epoch"]) == 2 * (q + 1)  # AᵀX exchanges: q+1 per factorization, two factorizations
+    # the init self-check (one AᵀX exchange vs an NCCL allreduce) passed on the
+    # real symmetric-memory buffers; then q+1 exchanges per factorization, two factorizations
+    assert str(part["exchange"]) == "p2p" and "passed" in str(part["note"]), str(part["note"])
+    assert int(part["epoch"]) == 1 + 2 * (q + 1)
     ref = oracle_pbp_qlp(a, d, q=q, seed=9)
     tol = conditioning_tolerance(ref["l"], strict=1e-10)
     assert np.all(column_relative_error(part["q"], ref["q"]) <= tol)

@@ -8,7 +8,10 @@ Three factorizations of the SAME A and Φ:
   alt  the same call sequence with every product's summation split in two
        halves of its reduction dimension (a legitimate reordering: each
        product is still a backward-stable FP64 dgemm);
-  gpu  this package's pbp_qlp on the device.
+  alt2 the call sequence with every QR applied to a row-permuted copy
+       (LAPACK's own rounding perturbed; exact factors unchanged);
+  gpu  this package's pbp_qlp on the device (default QR method);
+  hh   the same with the blocked Householder QR kernel forced.
 Per column j it records the sign-normalised column errors of Q and P and
 |ΔL_jj|/L_jj of alt-vs-ref and gpu-vs-ref, with κ_j = L_00/L_jj and the
 relative gap to the neighbouring L values — the data behind the parity
@@ -45,6 +48,29 @@ def reordered_pbp_qlp(a, d, q, phi):
     return {"q": qf, "l": np.tril(rt.T), "p": pbar @ w}
 
 
+def permuted_qr_pbp_qlp(a, d, q, phi, seed=12345):
+    """oracle_pbp_qlp whose every QR factors a row-permuted copy (Q = P·Q_perm):
+    the exact factors are unchanged, LAPACK's rounding is not — the
+    reference's own QR noise, which `alt` (same QR inputs up to GEMM
+    rounding) cannot show."""
+    rng = np.random.default_rng(seed)
+
+    def qr(m):
+        perm = rng.permutation(m.shape[0])
+        qp, r = oracle_qr(m[perm])
+        out = np.empty_like(qp)
+        out[perm] = qp
+        return out, r
+
+    pbar, _ = qr(a.T @ phi)
+    for _ in range(q):
+        pbar, _ = qr(a @ pbar)
+        pbar, _ = qr(a.T @ pbar)
+    qf, r = qr(a @ pbar)
+    w, rt = oracle_qr(r.T)
+    return {"q": qf, "l": np.tril(rt.T), "p": pbar @ w}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="cfg5")
@@ -65,8 +91,18 @@ def main():
             t0 = time.time()
             ref = oracle_pbp_qlp(a, d, q=q, seed=args.seed, phi=phi)
             alt = reordered_pbp_qlp(a, d, q, phi)
+            alt2 = permuted_qr_pbp_qlp(a, d, q, phi)
             got = pbp_qlp(a_dev, d, q=q, seed=args.seed)
             gq, gl, gp = (x.cpu().numpy() for x in (got.q_basis, got.l, got.p_basis))
+            from paper_2103_07245_b200 import device as D
+
+            ctx = D.context(a_dev.device)
+            ctx.set_qr_method(ctx.QR_HOUSEHOLDER)
+            try:
+                hh = pbp_qlp(a_dev, d, q=q, seed=args.seed)
+            finally:
+                ctx.set_qr_method(ctx.QR_AUTO)
+            hq, hl, hp = (x.cpu().numpy() for x in (hh.q_basis, hh.l, hh.p_basis))
             lref = np.abs(np.diag(ref["l"]))
             kappa = lref[0] / lref
             gap = np.full(d, np.inf)
@@ -79,18 +115,23 @@ def main():
                 "alt_l": np.abs(np.abs(np.diag(alt["l"])) - lref) / lref,
                 "gpu_q": column_relative_error(gq, ref["q"]), "gpu_p": column_relative_error(gp, ref["p"]),
                 "gpu_l": np.abs(np.abs(np.diag(gl)) - lref) / lref,
+                "alt2_q": column_relative_error(alt2["q"], ref["q"]),
+                "alt2_p": column_relative_error(alt2["p"], ref["p"]),
+                "alt2_l": np.abs(np.abs(np.diag(alt2["l"])) - lref) / lref,
+                "hh_q": column_relative_error(hq, ref["q"]), "hh_p": column_relative_error(hp, ref["p"]),
+                "hh_l": np.abs(np.abs(np.diag(hl)) - lref) / lref,
             }
             os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
             np.savez(f"{args.out}_{args.workload}_d{d}_q{q}.npz", **rec)
             u = 2.0 ** -53
             for k in ("q", "p", "l"):
-                ga, al = rec[f"gpu_{k}"], rec[f"alt_{k}"]
-                print(f"{args.workload} d={d} q={q} {k.upper()}: gpu max {ga.max():.2e} (col {ga.argmax()}), "
-                      f"alt max {al.max():.2e} (col {al.argmax()}); max gpu/(u·κ) {np.max(ga / (u * kappa)):.1f}, "
-                      f"max alt/(u·κ) {np.max(al / (u * kappa)):.1f}; max gpu/max(alt,1e-16) per col "
-                      f"{np.max(ga / np.maximum(al, 1e-16)):.1f}", flush=True)
+                parts = []
+                for v in ("gpu", "hh", "alt", "alt2"):
+                    e = rec[f"{v}_{k}"]
+                    parts.append(f"{v} max {e.max():.2e} (col {e.argmax()}, /(u·κ) {np.max(e / (u * kappa)):.1f})")
+                print(f"{args.workload} d={d} q={q} {k.upper()}: " + "; ".join(parts), flush=True)
             print(f"  ({time.time() - t0:.0f} s)", flush=True)
-            del got
+            del got, hh
             torch.cuda.empty_cache()
 
 

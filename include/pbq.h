@@ -179,6 +179,23 @@ int pbq_cpqr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes);
 int pbq_gather_columns(pbq_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
                        const int64_t* perm, double* dst, int64_t ldd, void* stream);
 
+/* Singular value decomposition of a small dense matrix (the
+ * k×k core `svd_full`, linalg.py:131-139 / LAPACK dgesdd, of r_svd,
+ * algorithms.py:263-292, and the pseudoinverse of cor_utv, :295-303) by
+ * one-sided Jacobi on the n rows (length L ≥ n) of the row-major X:
+ *   G·X = diag(s)·Y  ⇒  X = Gᵀ·diag(s)·Y,
+ * s (n doubles) sorted descending, Y (n×L, ldy; may be NULL) with orthonormal
+ * rows (rows with s = 0 are completed to an orthonormal set), and — when
+ * `accumulate` — G (n×n, ldg) orthogonal, its rows the left singular vectors.
+ * X is not modified.  status (device, 2 ints): sweeps used, 1 if not
+ * converged within 30 sweeps.  n ≤ 256 rows of ≤ 768 doubles (incl. the G
+ * row when accumulating) run in one thread-block cluster with the vectors in
+ * registers; larger problems keep the vectors in L2. */
+int pbq_jacobi_svd(pbq_ctx* ctx, int64_t n, int64_t L, const double* X, int64_t ldx, int32_t accumulate, double* s,
+                   double* Y, int64_t ldy, double* G, int64_t ldg, int32_t* status, void* workspace,
+                   size_t workspace_bytes, void* stream);
+int pbq_jacobi_svd_workspace_bytes(pbq_ctx* ctx, int64_t n, int64_t L, int32_t accumulate, size_t* bytes);
+
 /* Distributed Cholesky-QR2 of a row-sharded tall matrix (the
  * QR of A·P̄ across ranks, replacing the TSQR tree when the input is
  * well-conditioned).  A is this rank's m×n row block.  The three stages run

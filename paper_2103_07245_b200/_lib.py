@@ -124,6 +124,9 @@ _SIGS = {
     "pbq_p2p_sum": ([c_p, c_p, c_i64, c_i32, c_i64, c_p, c_p, ctypes.c_uint32, c_p, c_p], ctypes.c_int),
     "pbq_p2p_wait": ([c_p, c_p, ctypes.c_uint32, c_p, c_p], ctypes.c_int),
     "pbq_set_p2p_timeout_ms": ([c_p, c_i64], ctypes.c_int),
+    "pbq_jacobi_svd": ([c_p, c_i64, c_i64, c_p, c_i64, c_i32, c_p, c_p, c_i64, c_p, c_i64, c_p, c_p, c_sz, c_p],
+                       ctypes.c_int),
+    "pbq_jacobi_svd_workspace_bytes": ([c_p, c_i64, c_i64, c_i32, ctypes.POINTER(c_sz)], ctypes.c_int),
     "pbq_debug_qr_hooks": ([c_p, c_p, c_p, c_p], ctypes.c_int),
     "pbq_profile_begin": ([c_p, c_i32], ctypes.c_int),
     "pbq_profile_end": ([c_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)], ctypes.c_int),

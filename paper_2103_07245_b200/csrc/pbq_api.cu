@@ -23,6 +23,7 @@
 #include "qr_f64.cuh"
 #include "sketch.cuh"
 #include "exchange_f64.cuh"
+#include "svd_f64.cuh"
 
 // Optional per-kernel-class timing (pbq_profile_*): event pairs recorded on
 // the launch stream around every kernel of the pipeline.
@@ -1071,6 +1072,137 @@ int gather_launch(pbq_ctx* ctx, long rows, long cols, const double* src, long ld
   return PBQ_OK;
 }
 
+// ----------------------------------------------------- Jacobi SVD core ----
+// svd_f64.cuh.  Register kernel instantiations by doubles-per-lane.
+using JacFn = void (*)(JacArgs);
+JacFn jac_reg_fn(int vpl) {
+  switch (vpl) {
+    case 4: return jacobi_reg_kernel<4>;
+    case 8: return jacobi_reg_kernel<8>;
+    case 16: return jacobi_reg_kernel<16>;
+    default: return jacobi_reg_kernel<24>;
+  }
+}
+int jac_vpl(long V) { return V <= 128 ? 4 : V <= 256 ? 8 : V <= 512 ? 16 : 24; }
+size_t jac_reg_smem(int vpl) { return size_t(2) * JAC_WARPS * 2 * 32 * vpl * sizeof(double) + 64 * sizeof(int); }
+
+// Largest cluster of C CTAs the register kernel with `vpl` can launch (0: none).
+bool jac_cluster_ok(pbq_ctx* ctx, JacFn fn, int C, size_t smem, int threads) {
+  static std::unordered_map<long, bool> memo;
+  const long key = (long(reinterpret_cast<uintptr_t>(fn)) << 12) ^ (long(C) << 4) ^ long(threads);
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  cudaFuncSetAttribute(reinterpret_cast<void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(reinterpret_cast<void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  const bool ok = cudaOccupancyMaxActiveClusters(&nclusters, reinterpret_cast<void*>(fn), &cfg) == cudaSuccess &&
+                  nclusters > 0;
+  cudaGetLastError();
+  memo[key] = ok;
+  return ok;
+}
+
+size_t jacobi_ws_bytes(long n, long L, int accumulate) {
+  const long np = n + (n & 1), V = L + (accumulate ? n : 0), ldz = V + (V & 1);
+  return align_up(size_t(np) * ldz * 8, 256) + align_up(size_t(n) * 8, 256) + align_up(size_t(L) * 8, 256) + 512;
+}
+
+int jacobi_launch(pbq_ctx* ctx, long n, long L, const double* X, long ldx, int accumulate, double* s, double* Y,
+                  long ldy, double* G, long ldg, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (n < 1 || L < 1) return fail(ctx, PBQ_ERR_DIM, "jacobi_svd: bad shape %ld x %ld", n, L);
+  if (n > L) return fail(ctx, PBQ_ERR_DIM, "jacobi_svd: needs n <= L (got %ld x %ld)", n, L);
+  if (!X || !s || !status || ldx < L || (Y && ldy < L) || (accumulate && (!G || ldg < n)))
+    return fail(ctx, PBQ_ERR_PARAM, "jacobi_svd: bad pointer or leading dimension");
+  if (n > (1L << 20)) return fail(ctx, PBQ_ERR_UNSUPPORTED, "jacobi_svd: n too large");
+  JacArgs a;
+  a.n = int(n);
+  a.np = int(n + (n & 1));
+  a.L = int(L);
+  a.V = int(L + (accumulate ? n : 0));
+  a.accumulate = accumulate ? 1 : 0;
+  a.X = X;
+  a.ldx = ldx;
+  a.ldz = a.V + (a.V & 1);
+  a.status = status;
+  a.max_sweeps = 30;                                     // LAPACK dgesvj's NSWEEP
+  a.tol = sqrt(double(L)) * 1.1102230246251565e-16;      // √L·u (dgesvj's CTOL)
+  Carve cv(ws, ws_bytes);
+  a.Z = cv.take<double>(size_t(a.np) * a.ldz);
+  double* sig = cv.take<double>(n);
+  double* work = cv.take<double>(L);
+  int* nzero = cv.take<int>(1);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "jacobi_svd: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  const int P = a.np / 2;
+  ProfScope ps(ctx->prof, st, 1);
+  PBQ_CUDA(ctx, cudaMemsetAsync(nzero, 0, sizeof(int), st));
+  bool done = false;
+  if (P <= JAC_MAX_PAIRS_REG && a.V <= 32 * JAC_MAX_VPL && !getenv("PBQ_JACOBI_L2")) {
+    const int vpl = jac_vpl(a.V);
+    const int C = int(ceil_div(P, JAC_WARPS));
+    const JacFn fn = jac_reg_fn(vpl);
+    const size_t smem = jac_reg_smem(vpl);
+    if (jac_cluster_ok(ctx, fn, C, smem, JAC_WARPS * 32)) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      cfg.gridDim = dim3(C);
+      cfg.blockDim = dim3(JAC_WARPS * 32);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      PBQ_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, a));
+      ctx->launches += 1;
+      done = true;
+    }
+  }
+  if (!done) {
+    const long blocks = std::min(ceil_div(long(a.np) * a.V, 256), long(ctx->sms) * 4);
+    jacobi_init_kernel<<<unsigned(blocks), 256, 0, st>>>(a);
+    PBQ_CUDA(ctx, cudaGetLastError());
+    ctx->launches += 1;
+    int C = int(std::min<long>(16, ceil_div(P, JAC_L2_WARPS)));
+    const JacFn fn = jacobi_l2_kernel<16>;
+    while (C > 1 && !jac_cluster_ok(ctx, fn, C, 0, JAC_L2_WARPS * 32)) C /= 2;
+    if (C > 1) cudaFuncSetAttribute(reinterpret_cast<void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(JAC_L2_WARPS * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PBQ_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, a));
+    ctx->launches += 1;
+  }
+  const unsigned wb = unsigned(ceil_div(n, 8));  // 8 warps per 256-thread block, one per vector
+  jacobi_norms_kernel<<<wb, 256, 0, st>>>(a, sig);
+  jacobi_output_kernel<<<wb, 256, 0, st>>>(a, sig, s, Y, ldy, G, ldg, nzero);
+  if (Y) jacobi_complete_kernel<<<1, 256, 0, st>>>(int(n), int(L), Y, ldy, nzero, work);
+  PBQ_CUDA(ctx, cudaGetLastError());
+  ctx->launches += Y ? 3 : 2;
+  return PBQ_OK;
+}
+
 // ------------------------------------------------- reconstruction residual --
 // ‖A − Q_k·L_k·P_kᵀ‖_F² and ‖A‖_F² (QlpFactors.approx(rank), algorithms.py:
 // 101-106; error_curve's frobenius_error, analysis.py:238-244) in one pass
@@ -1342,6 +1474,20 @@ int pbq_set_p2p_timeout_ms(pbq_ctx* ctx, int64_t ms) {
   if (!ctx || ms < 1) return PBQ_ERR_PARAM;
   ctx->p2p_timeout_ns = (unsigned long long)ms * 1000000ull;
   return PBQ_OK;
+}
+
+int pbq_jacobi_svd_workspace_bytes(pbq_ctx* ctx, int64_t n, int64_t L, int32_t accumulate, size_t* bytes) {
+  if (!ctx || !bytes || n < 1 || L < 1) return PBQ_ERR_PARAM;
+  *bytes = jacobi_ws_bytes(n, L, accumulate);
+  return PBQ_OK;
+}
+
+int pbq_jacobi_svd(pbq_ctx* ctx, int64_t n, int64_t L, const double* X, int64_t ldx, int32_t accumulate, double* s,
+                   double* Y, int64_t ldy, double* G, int64_t ldg, int32_t* status, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  return jacobi_launch(ctx, n, L, X, ldx, accumulate, s, Y, ldy, G, ldg, status, workspace, workspace_bytes,
+                       static_cast<cudaStream_t>(stream));
 }
 
 int pbq_xchg_expected_tiles(int64_t n2, int64_t N, int64_t S, int32_t rank, int32_t world, uint32_t* tiles) {

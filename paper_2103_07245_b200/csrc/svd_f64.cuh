@@ -1,0 +1,432 @@
+// One-sided (Hestenes) Jacobi SVD of a small dense FP64 matrix — the k×k
+// core of the sibling randomized paths: `svd_full`
+// (/root/reference/pkg/src/pbpqlp/linalg.py:131-139, LAPACK dgesdd through
+// np.linalg.svd) as used by r_svd (algorithms.py:263-292) and the
+// pseudoinverse of cor_utv (`_transposed_pinv_apply`, algorithms.py:295-303).
+//
+// Problem.  M is n×L row-major (n ≤ L); its rows are the "vectors".  Plane
+// rotations combine pairs of rows until all rows are mutually orthogonal:
+//   G·M = diag(s)·Y,  G orthogonal (n×n), Y with orthonormal rows,
+// so M = Gᵀ·diag(s)·Y is an SVD (left vectors = columns of Gᵀ = rows of G).
+// With `accumulate`, each vector carries the matching row of G (initially
+// the identity), so the rotations build G alongside (vector length V = L+n,
+// dot products over the first L entries only).
+//
+// Rotation (Rutishauser, as in LAPACK dgesvj): for rows x, y with
+// a = ‖x‖², b = ‖y‖², c = x·y, rotate when |c| > tol·√a·√b (tol = √L·u):
+// ζ = (b − a)/(2c), t = sign(ζ)/(|ζ| + √(1+ζ²)), cs = 1/√(1+t²), sn = cs·t,
+// x ← cs·x − sn·y, y ← sn·x + cs·y.  The sums a, b, c are recomputed from the
+// current vectors at every visit, so every rotation is computed from data
+// accurate relative to ‖x‖‖y‖ (one-sided Jacobi's relative accuracy).
+//
+// Order: the circle (round-robin) ordering on n_p = n rounded up to even
+// positions: n_p − 1 rounds per sweep, n_p/2 disjoint pairs per round
+// (pair p = positions p and n_p−1−p), every pair exactly once per sweep;
+// between rounds the vectors at positions 1…n_p−1 advance one position, so
+// after a sweep every vector is back at its start.  The sweep loop ends
+// when a whole sweep rotated nothing (convergence), bounded by max_sweeps.
+// Everything is in fixed order, so results are bitwise reproducible.
+//
+// Two kernels, one schedule:
+//  * jacobi_reg_kernel — n_p/2 ≤ 128 pairs: one thread-block cluster (≤ 16
+//    CTAs of 8 warps), warp p holds pair p's two vectors in registers for the
+//    whole run.  After each round it hands its top vector to warp p+1 and its
+//    bottom vector to warp p−1 through shared-memory mailboxes (DSMEM stores
+//    across CTA boundaries), double-buffered by round parity, with one
+//    cluster barrier per round.
+//  * jacobi_l2_kernel — any size: the vectors stay in a global (L2-resident)
+//    array and the schedule moves the computation instead: in round r the
+//    vector at position x ≥ 1 is vector 1 + ((x − 1 − r) mod (n_p − 1)).  One
+//    cluster of up to 16 CTAs, warps take pairs round-robin, a cluster
+//    barrier per round.
+// Then jacobi_norms_kernel / jacobi_output_kernel: σ_i = ‖row i‖ (fixed-order
+// sums), a stable descending sort by σ (rank by counting), Y rows = x/σ,
+// G rows permuted alike; jacobi_complete_kernel gives rows with σ = 0 an
+// orthonormal completion (classical Gram-Schmidt twice against the other
+// rows, from unit vectors), as LAPACK returns orthonormal vectors for a zero
+// singular value.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace pbq {
+
+namespace jcg = cooperative_groups;
+
+constexpr int JAC_WARPS = 8;            // warps per CTA of the register kernel
+constexpr int JAC_MAX_PAIRS_REG = 128;  // 16 CTAs × 8 warps
+constexpr int JAC_MAX_VPL = 24;         // doubles per lane per vector (V ≤ 768)
+constexpr int JAC_L2_WARPS = 16;
+
+struct JacArgs {
+  int n, np, L, V;     // vectors, padded count (even), dot length, vector length
+  int accumulate;      // V == L + n: vectors carry their row of G
+  const double* X;     // n×L input (ldx)
+  long ldx;
+  double* Z;           // np×V final vectors (ldz = V rounded up to even)
+  long ldz;
+  int* status;         // [0] sweeps used, [1] 1 if not converged within max_sweeps
+  int max_sweeps;
+  double tol;
+};
+
+__device__ __forceinline__ void jac_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// Initial value of element e (< V) of vector i: row i of X, then e_i.
+__device__ __forceinline__ double jac_init(const JacArgs& p, int i, int e) {
+  if (i >= p.n) return 0.0;
+  if (e < p.L) return p.X[long(i) * p.ldx + e];
+  return (e - p.L == i) ? 1.0 : 0.0;
+}
+
+// The rotation of one pair (x, y: VPL doubles per lane, element lane + 32·k).
+// Returns true when a rotation was applied.
+template <int VPL>
+__device__ __forceinline__ bool jac_rotate(double (&x)[VPL], double (&y)[VPL], int L, double tol) {
+  const int lane = threadIdx.x & 31;
+  double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    if (lane + 32 * k < L) {
+      a = fma(x[k], x[k], a);
+      b = fma(y[k], y[k], b);
+      c = fma(x[k], y[k], c);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if (!(a > 0.0 && b > 0.0) || !(fabs(c) > tol * sqrt(a) * sqrt(b))) return false;
+  const double zeta = (b - a) / (2.0 * c);
+  double t;
+  if (fabs(zeta) > 1e100)
+    t = 0.5 / zeta;
+  else
+    t = copysign(1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
+  const double cs = 1.0 / sqrt(fma(t, t, 1.0));
+  const double sn = cs * t;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const double xv = x[k], yv = y[k];
+    x[k] = fma(cs, xv, -sn * yv);
+    y[k] = fma(sn, xv, cs * yv);
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Register-resident kernel.  Launch: grid = C CTAs = one cluster of C,
+// JAC_WARPS warps each, C·JAC_WARPS ≥ P = np/2; dynamic shared memory
+// 2 (parity) × JAC_WARPS × 2 (slots) × 32·VPL doubles + counters.
+template <int VPL>
+__global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p) {
+  extern __shared__ __align__(16) double jsm[];
+  jcg::cluster_group cl = jcg::this_cluster();
+  const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+  const int C = int(cl.num_blocks()), me = int(cl.block_rank());
+  const int P = p.np / 2;
+  const int w = me * JAC_WARPS + lw;  // this warp's pair index
+  const bool active = w < P;
+  const size_t slot_d = size_t(32) * VPL;
+  const size_t box_d = size_t(2) * JAC_WARPS * 2 * slot_d;  // both parities
+  int* counts = reinterpret_cast<int*>(jsm + box_d);        // [2 parity][16 CTAs] (used on CTA 0)
+  int* red = counts + 32;                                   // [JAC_WARPS]
+
+  double x[VPL], y[VPL];
+  const int ti = w, bi = p.np - 1 - w;  // vector indices at positions w and np−1−w
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int e = lane + 32 * k;
+    x[k] = (active && e < p.V) ? jac_init(p, ti, e) : 0.0;
+    y[k] = (active && e < p.V) ? jac_init(p, bi, e) : 0.0;
+  }
+  // mailbox of (warp q, slot s, parity par) — possibly in another CTA
+  auto box = [&](int q, int s, int par) -> double* {
+    const int cta = q / JAC_WARPS, lq = q % JAC_WARPS;
+    double* local = jsm + ((size_t(par) * JAC_WARPS + lq) * 2 + s) * slot_d;
+    return cta == me ? local : cl.map_shared_rank(local, cta);
+  };
+  int sweeps = 0, converged = 0;
+  for (int sw = 0; sw < p.max_sweeps && !converged; ++sw) {
+    int rot = 0;
+    for (int r = 0; r < p.np - 1; ++r) {
+      const int par = r & 1;
+      if (active && jac_rotate<VPL>(x, y, p.L, p.tol)) ++rot;
+      if (P > 1) {
+        // hand over: T' → warp w+1 (1 ≤ w ≤ P−2) or kept as B (w = P−1);
+        //            B' → warp w−1 (w ≥ 1) or to warp 1's T (w = 0)
+        if (active) {
+          double* dt = nullptr;
+          double* db = nullptr;
+          if (w >= 1 && w <= P - 2) dt = box(w + 1, 0, par);
+          if (w >= 1) db = box(w - 1, 1, par);
+          else db = box(1, 0, par);
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            if (dt) dt[32 * k + lane] = x[k];
+            db[32 * k + lane] = y[k];
+          }
+        }
+        if (C > 1)
+          jac_cluster_sync();
+        else
+          __syncthreads();
+        if (active) {
+          // T_in: own T' (w = 0), warp 0's B' (w = 1), warp w−1's T' (w ≥ 2)
+          // B_in: own T' (w = P−1), else warp w+1's B'
+          const double* mt = jsm + ((size_t(par) * JAC_WARPS + lw) * 2 + 0) * slot_d;
+          const double* mb = jsm + ((size_t(par) * JAC_WARPS + lw) * 2 + 1) * slot_d;
+          if (w == P - 1) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) y[k] = x[k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) y[k] = mb[32 * k + lane];
+          }
+          if (w >= 1) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) x[k] = mt[32 * k + lane];
+          }
+        }
+      }
+    }
+    // ---- convergence: total rotations of the sweep, summed over the cluster
+    int cnt = active ? rot : 0;  // identical on every lane of the warp
+    if (lane == 0) red[lw] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int i = 0; i < JAC_WARPS; ++i) s += red[i];
+      int* dst = (C > 1) ? cl.map_shared_rank(counts, 0) : counts;
+      dst[(sw & 1) * 16 + me] = s;
+    }
+    if (C > 1)
+      jac_cluster_sync();
+    else
+      __syncthreads();
+    int total = 0;
+    const int* src = (C > 1) ? cl.map_shared_rank(counts, 0) : counts;
+    for (int i = 0; i < C; ++i) total += src[(sw & 1) * 16 + i];
+    sweeps = sw + 1;
+    converged = (total == 0);
+  }
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int e = lane + 32 * k;
+      if (e < p.V) {
+        p.Z[long(ti) * p.ldz + e] = x[k];
+        p.Z[long(bi) * p.ldz + e] = y[k];
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.status[0] = sweeps;
+    p.status[1] = converged ? 0 : 1;
+  }
+  if (C > 1) jac_cluster_sync();  // no CTA exits while its shared memory may still be read
+}
+
+// ---------------------------------------------------------------------------
+// L2-resident kernel (any n, V).  Launch: one cluster of C CTAs of
+// JAC_L2_WARPS warps; Z must already hold the initial vectors (jacobi_init_kernel).
+template <int VPL>
+__global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs p) {
+  __shared__ int red[JAC_L2_WARPS];
+  __shared__ int counts[2][16];
+  jcg::cluster_group cl = jcg::this_cluster();
+  const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+  const int C = int(cl.num_blocks()), me = int(cl.block_rank());
+  const int P = p.np / 2, TW = C * JAC_L2_WARPS, w0 = me * JAC_L2_WARPS + lw;
+  const int m1 = p.np - 1;
+  int sweeps = 0, converged = 0;
+  for (int sw = 0; sw < p.max_sweeps && !converged; ++sw) {
+    int rot = 0;
+    for (int r = 0; r < m1; ++r) {
+      for (int q = w0; q < P; q += TW) {
+        const int xt = q, xb = p.np - 1 - q;  // positions
+        const int it = xt == 0 ? 0 : 1 + ((xt - 1 - r) % m1 + m1) % m1;
+        const int ib = 1 + ((xb - 1 - r) % m1 + m1) % m1;
+        double* zt = p.Z + long(it) * p.ldz;
+        double* zb = p.Z + long(ib) * p.ldz;
+        // vector length V may exceed 32·VPL: process in chunks of 32·VPL
+        // (the dot products must cover all of [0, L) before rotating)
+        if (p.V <= 32 * VPL) {
+          double x[VPL], y[VPL];
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            const int e = lane + 32 * k;
+            x[k] = e < p.V ? __ldcg(zt + e) : 0.0;
+            y[k] = e < p.V ? __ldcg(zb + e) : 0.0;
+          }
+          if (jac_rotate<VPL>(x, y, p.L, p.tol)) {
+            ++rot;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+              const int e = lane + 32 * k;
+              if (e < p.V) {
+                __stcg(zt + e, x[k]);
+                __stcg(zb + e, y[k]);
+              }
+            }
+          }
+        } else {
+          // long vectors: dots over L from global, then the rotation streamed
+          double a = 0.0, b = 0.0, c = 0.0;
+          for (int e = lane; e < p.L; e += 32) {
+            const double xv = __ldcg(zt + e), yv = __ldcg(zb + e);
+            a = fma(xv, xv, a);
+            b = fma(yv, yv, b);
+            c = fma(xv, yv, c);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+          }
+          if (a > 0.0 && b > 0.0 && fabs(c) > p.tol * sqrt(a) * sqrt(b)) {
+            const double zeta = (b - a) / (2.0 * c);
+            const double t = fabs(zeta) > 1e100 ? 0.5 / zeta
+                                                : copysign(1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
+            const double cs = 1.0 / sqrt(fma(t, t, 1.0)), sn = cs * t;
+            for (int e = lane; e < p.V; e += 32) {
+              const double xv = __ldcg(zt + e), yv = __ldcg(zb + e);
+              __stcg(zt + e, fma(cs, xv, -sn * yv));
+              __stcg(zb + e, fma(sn, xv, cs * yv));
+            }
+            ++rot;
+          }
+        }
+      }
+      jac_cluster_sync();
+    }
+    if (lane == 0) red[lw] = rot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int i = 0; i < JAC_L2_WARPS; ++i) s += red[i];
+      cl.map_shared_rank(&counts[0][0], 0)[(sw & 1) * 16 + me] = s;
+    }
+    jac_cluster_sync();
+    int total = 0;
+    const int* src = cl.map_shared_rank(&counts[0][0], 0);
+    for (int i = 0; i < C; ++i) total += src[(sw & 1) * 16 + i];
+    sweeps = sw + 1;
+    converged = (total == 0);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.status[0] = sweeps;
+    p.status[1] = converged ? 0 : 1;
+  }
+  jac_cluster_sync();
+}
+
+__global__ void jacobi_init_kernel(JacArgs p) {
+  const long total = long(p.np) * p.V;
+  for (long t = long(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += long(gridDim.x) * blockDim.x) {
+    const int i = int(t / p.V), e = int(t % p.V);
+    p.Z[long(i) * p.ldz + e] = jac_init(p, i, e);
+  }
+}
+
+// σ_i = ‖z_i[0:L)‖, fixed-order sums (one warp per vector).
+__global__ void jacobi_norms_kernel(JacArgs p, double* sig) {
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= p.n) return;
+  const double* z = p.Z + long(i) * p.ldz;
+  double a = 0.0;
+  for (int e = lane; e < p.L; e += 32) a = fma(z[e], z[e], a);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0) sig[i] = sqrt(a);
+}
+
+// Sorted outputs: rank(i) = #{j: σ_j > σ_i or (σ_j == σ_i and j < i)};
+// s[rank] = σ_i, Y[rank] = z_i[0:L)/σ_i (zero row when σ_i = 0, completed
+// by jacobi_complete_kernel), G[rank] = z_i[L:L+n) when accumulating.
+__global__ void jacobi_output_kernel(JacArgs p, const double* sig, double* s, double* Y, long ldy, double* G, long ldg,
+                                     int* nzero) {
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= p.n) return;
+  const double si = sig[i];
+  int rank = 0;
+  for (int j = lane; j < p.n; j += 32) {
+    const double sj = sig[j];
+    rank += (sj > si || (sj == si && j < i)) ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+  const double* z = p.Z + long(i) * p.ldz;
+  const double inv = si > 0.0 ? 1.0 / si : 0.0;
+  if (lane == 0) {
+    s[rank] = si;
+    if (!(si > 0.0)) atomicAdd(nzero, 1);
+  }
+  if (Y)
+    for (int e = lane; e < p.L; e += 32) Y[long(rank) * ldy + e] = z[e] * inv;
+  if (G && p.accumulate)
+    for (int e = lane; e < p.n; e += 32) G[long(rank) * ldg + e] = z[p.L + e];
+}
+
+// Rows rank ≥ n − nzero of Y (σ = 0) get an orthonormal completion: for each,
+// unit vectors e_t (t = 0, 1, …) are orthogonalised twice (CGS2) against all
+// other rows until the remainder keeps more than half its norm.  One CTA,
+// sequential over the (rare) zero rows.
+__global__ void __launch_bounds__(256) jacobi_complete_kernel(int n, int L, double* Y, long ldy, const int* nzero,
+                                                              double* work) {
+  __shared__ double red[8];
+  __shared__ double coef_s;
+  const int nz = *nzero;
+  if (nz == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  double* v = work;  // L doubles
+  auto block_sum = [&](double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    __syncthreads();
+    if (lane == 0) red[wp] = x;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < 8; ++i) s += red[i];
+    return s;
+  };
+  for (int row = n - nz; row < n; ++row) {
+    for (int t = 0; t < L; ++t) {
+      for (int e = tid; e < L; e += 256) v[e] = (e == t) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int j = 0; j < row; ++j) {  // rows < row are orthonormal (earlier ranks)
+          double d = 0.0;
+          for (int e = tid; e < L; e += 256) d = fma(Y[long(j) * ldy + e], v[e], d);
+          d = block_sum(d);
+          if (tid == 0) coef_s = d;
+          __syncthreads();
+          const double cf = coef_s;
+          for (int e = tid; e < L; e += 256) v[e] = fma(-cf, Y[long(j) * ldy + e], v[e]);
+          __syncthreads();
+        }
+      }
+      double nn = 0.0;
+      for (int e = tid; e < L; e += 256) nn = fma(v[e], v[e], nn);
+      nn = block_sum(nn);
+      if (nn > 0.25) {
+        const double inv = 1.0 / sqrt(nn);
+        for (int e = tid; e < L; e += 256) Y[long(row) * ldy + e] = v[e] * inv;
+        __syncthreads();
+        break;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace pbq

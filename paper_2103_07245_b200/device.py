@@ -304,6 +304,31 @@ def second_stage(ctx, r, w=None, l=None):
     return w, l
 
 
+def jacobi_svd(ctx, x, accumulate=True, want_y=True, status=None):
+    """One-sided Jacobi SVD of the rows of ``x`` (n×L, n ≤ L):
+    G·x = diag(s)·Y (pbq_jacobi_svd).  Returns (s, Y, G, status) as device
+    tensors — Y None unless ``want_y``, G None unless ``accumulate``;
+    status = [sweeps, not-converged flag] (int32, on the device)."""
+    x = as_kernel_operand(x)
+    n, L = x.shape
+    dev = x.device
+    s = torch.empty(n, dtype=torch.float64, device=dev)
+    y = empty_matrix(n, L, dev) if want_y else None
+    g = empty_matrix(n, n, dev) if accumulate else None
+    if status is None:
+        status = torch.zeros(2, dtype=torch.int32, device=dev)
+    nbytes = ctypes.c_size_t()
+    with ctx.lock:
+        ctx.check(ctx.lib.pbq_jacobi_svd_workspace_bytes(ctx.handle, n, L, 1 if accumulate else 0,
+                                                         ctypes.byref(nbytes)), "jacobi_svd workspace")
+        ws = workspace(nbytes.value, dev)
+        st = ctx.lib.pbq_jacobi_svd(ctx.handle, n, L, ptr(x), ld_of(x), 1 if accumulate else 0, ptr(s), ptr(y),
+                                    ld_of(y) if y is not None else 0, ptr(g), ld_of(g) if g is not None else 0,
+                                    ptr(status), ptr(ws), nbytes.value, stream_ptr(dev))
+        ctx.check(st, "jacobi_svd")
+    return s, y, g, status
+
+
 def cpqr_pivots(ctx, m, out=None):
     """Pivot order of LAPACK dgeqp3 for the m×n device matrix ``m`` → int64
     device tensor ``perm`` (n entries) with m[:, perm] = Q·R."""

@@ -192,7 +192,8 @@ def test_p2p_driver_guard_fallback_rerun(cuda, tmp_path):
     mp.spawn(_worker, args=(1, _free_port(), a, 8, 1, 2, str(tmp_path), 1), nprocs=1, join=True)
     part = np.load(os.path.join(tmp_path, "rank0.npz"))
     assert int(part["tsqr"]) == 2          # both QRs of A·P̄ by TSQR in the re-run
-    assert int(part["epoch"]) == 2 * 2     # 2 AᵀX exchanges per factorization, the run and its re-run
+    assert int(part["epoch"]) == 1 + 2 * 2  # the init self-check, then 2 AᵀX exchanges per factorization,
+    # the run and its re-run
     assert int(part["warn"]) == 3          # every orth site warns
     qg = part["q"]
     assert np.abs(qg.T @ qg - np.eye(qg.shape[1])).max() < 1e-12

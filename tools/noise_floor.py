@@ -10,6 +10,8 @@ Three factorizations of the SAME A and Φ:
        product is still a backward-stable FP64 dgemm);
   alt2 the call sequence with every QR applied to a row-permuted copy
        (LAPACK's own rounding perturbed; exact factors unchanged);
+  alt3 every product summed in a random order and every QR row-permuted
+       (a different, equally valid FP64 evaluation of the whole sequence);
   gpu  this package's pbp_qlp on the device (default QR method);
   hh   the same with the blocked Householder QR kernel forced.
 Per column j it records the sign-normalised column errors of Q and P and
@@ -71,6 +73,42 @@ def permuted_qr_pbp_qlp(a, d, q, phi, seed=12345):
     return {"q": qf, "l": np.tril(rt.T), "p": pbar @ w}
 
 
+def shuffled_pbp_qlp(a, d, q, phi, seed=777):
+    """Every product summed in a random order (rows and columns of A
+    permuted, results un-permuted) and every QR on a row-permuted copy: a
+    different but equally valid FP64 evaluation order of the whole call
+    sequence, like any reimplementation (a GPU's blocked DMMA sums) has."""
+    rng = np.random.default_rng(seed)
+    n1, n2 = a.shape
+    p1, p2 = rng.permutation(n1), rng.permutation(n2)
+    ap = a[p1][:, p2]
+
+    def apply_t(x):  # aᵀx, summed over rows in p1 order
+        out = np.empty((n2, x.shape[1]))
+        out[p2] = ap.T @ x[p1]
+        return out
+
+    def apply(y):  # a·y, summed over columns in p2 order
+        out = np.empty((n1, y.shape[1]))
+        out[p1] = ap @ y[p2]
+        return out
+
+    def qr(m):
+        perm = rng.permutation(m.shape[0])
+        qp, r = oracle_qr(m[perm])
+        out = np.empty_like(qp)
+        out[perm] = qp
+        return out, r
+
+    pbar, _ = qr(apply_t(phi))
+    for _ in range(q):
+        pbar, _ = qr(apply(pbar))
+        pbar, _ = qr(apply_t(pbar))
+    qf, r = qr(apply(pbar))
+    w, rt = oracle_qr(r.T)
+    return {"q": qf, "l": np.tril(rt.T), "p": pbar @ w}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="cfg5")
@@ -92,6 +130,7 @@ def main():
             ref = oracle_pbp_qlp(a, d, q=q, seed=args.seed, phi=phi)
             alt = reordered_pbp_qlp(a, d, q, phi)
             alt2 = permuted_qr_pbp_qlp(a, d, q, phi)
+            alt3 = shuffled_pbp_qlp(a, d, q, phi)
             got = pbp_qlp(a_dev, d, q=q, seed=args.seed)
             gq, gl, gp = (x.cpu().numpy() for x in (got.q_basis, got.l, got.p_basis))
             from paper_2103_07245_b200 import device as D
@@ -118,6 +157,9 @@ def main():
                 "alt2_q": column_relative_error(alt2["q"], ref["q"]),
                 "alt2_p": column_relative_error(alt2["p"], ref["p"]),
                 "alt2_l": np.abs(np.abs(np.diag(alt2["l"])) - lref) / lref,
+                "alt3_q": column_relative_error(alt3["q"], ref["q"]),
+                "alt3_p": column_relative_error(alt3["p"], ref["p"]),
+                "alt3_l": np.abs(np.abs(np.diag(alt3["l"])) - lref) / lref,
                 "hh_q": column_relative_error(hq, ref["q"]), "hh_p": column_relative_error(hp, ref["p"]),
                 "hh_l": np.abs(np.abs(np.diag(hl)) - lref) / lref,
             }
@@ -126,7 +168,7 @@ def main():
             u = 2.0 ** -53
             for k in ("q", "p", "l"):
                 parts = []
-                for v in ("gpu", "hh", "alt", "alt2"):
+                for v in ("gpu", "hh", "alt", "alt2", "alt3"):
                     e = rec[f"{v}_{k}"]
                     parts.append(f"{v} max {e.max():.2e} (col {e.argmax()}, /(u·κ) {np.max(e / (u * kappa)):.1f})")
                 print(f"{args.workload} d={d} q={q} {k.upper()}: " + "; ".join(parts), flush=True)

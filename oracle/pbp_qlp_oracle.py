@@ -51,7 +51,8 @@ def build_c_oracle():
     os.makedirs(os.path.join(_HERE, "_build"), exist_ok=True)
     src = os.path.join(_HERE, "sketch_oracle.c")
     if not os.path.exists(_CLIB) or os.path.getmtime(_CLIB) < os.path.getmtime(src):
-        subprocess.run(["gcc", "-O2", "-fPIC", "-std=gnu11", "-shared", "-o", _CLIB, src, "-lm"], check=True)
+        subprocess.run(["gcc", "-O2", "-fPIC", "-std=gnu11", "-ffp-contract=off", "-shared", "-o", _CLIB, src, "-lm"],
+                       check=True)
     return _CLIB
 
 
@@ -64,6 +65,7 @@ def _c():
         lib.pbqo_philox_raw.argtypes = [ctypes.c_uint64] * 4 + [ctypes.c_void_p]
         lib.pbqo_normals.argtypes = [ctypes.c_uint64] * 4 + [ctypes.c_void_p]
         lib.pbqo_normals.restype = ctypes.c_uint64
+        lib.pbqo_log1p_pair.argtypes = [ctypes.c_void_p, ctypes.c_long, ctypes.c_void_p, ctypes.c_void_p]
         _clib = lib
     return _clib
 
@@ -81,6 +83,15 @@ def c_gaussian(rows, cols, seed=0, row_offset=0):
     out = np.empty((rows, cols))
     _c().pbqo_normals(seed & (2**64 - 1), seed >> 64, row_offset * cols, rows * cols, out.ctypes.data)
     return out
+
+
+def c_log1p_pair(x):
+    """(restated glibc log1p — the device's glibc_log1p — , the C library's
+    log1p) of every x: the pin of the sketch's exponential-tail arithmetic."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    a, b = np.empty_like(x), np.empty_like(x)
+    _c().pbqo_log1p_pair(x.ctypes.data, x.size, a.ctypes.data, b.ctypes.data)
+    return a, b
 
 
 def c_philox_raw(seed, start, n):

@@ -100,3 +100,91 @@ uint64_t pbqo_normals(uint64_t k0, uint64_t k1, uint64_t skip, uint64_t n, doubl
   for (uint64_t i = 0; i < n; ++i) out[i] = pbqo_normal(&g, &pos);
   return pos;
 }
+
+/* ---- log1p pin: the device's glibc_log1p (csrc/sketch.cuh), restated on
+ * the host with the same explicit fma() and single-rounded operations
+ * (this file is built with -ffp-contract=off), next to the C library's own
+ * log1p, which numpy's ziggurat tail calls (npy_log1p).  tests/test_oracle.py
+ * checks the two agree bit for bit. */
+static inline int32_t pbqo_hi(double x) {
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  return (int32_t)(b >> 32);
+}
+static inline double pbqo_sethi(double x, int32_t h) {
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  b = (b & 0xffffffffULL) | ((uint64_t)(uint32_t)h << 32);
+  memcpy(&x, &b, 8);
+  return x;
+}
+
+double pbqo_glibc_log1p(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01, Lp3 = 2.857142874366239149e-01,
+               Lp4 = 2.222219843214978396e-01, Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  const int32_t hx = pbqo_hi(x), ax = hx & 0x7fffffff;
+  int32_t k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (hx < 0x3FDA827A) {
+    if (ax >= 0x3ff00000) return x == -1.0 ? -INFINITY : NAN;
+    if (ax < 0x3e200000) return ax < 0x3c900000 ? x : fma(-(x * x), 0.5, x);
+    if (hx > 0 || hx <= (int32_t)0xbfd2bec3) {
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  }
+  if (hx >= 0x7ff00000) return x + x;
+  if (k != 0) {
+    double u;
+    if (hx < 0x43400000) {
+      u = 1.0 + x;
+      hu = pbqo_hi(u);
+      k = (hu >> 20) - 1023;
+      c = k > 0 ? 1.0 - (u - x) : x - (u - 1.0);
+      c /= u;
+    } else {
+      u = x;
+      hu = pbqo_hi(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = pbqo_sethi(u, hu | 0x3ff00000);
+    } else {
+      k += 1;
+      u = pbqo_sethi(u, hu | 0x3fe00000);
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = u - 1.0;
+  }
+  const double dk = (double)k;
+  const double hfsq = (0.5 * f) * f;
+  if (hu == 0) {
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      c = fma(dk, ln2_lo, c);
+      return fma(dk, ln2_hi, c);
+    }
+    const double R = hfsq * fma(-f, 0.66666666666666666, 1.0);
+    if (k == 0) return f - R;
+    return fma(dk, ln2_hi, -((R - fma(dk, ln2_lo, c)) - f));
+  }
+  const double s = f / (2.0 + f), z = s * s;
+  const double z2 = z * z, z4 = z2 * z2, z6 = z4 * z2;
+  const double R2 = fma(z, Lp3, Lp2), R3 = fma(z, Lp5, Lp4), R4 = fma(z, Lp7, Lp6);
+  const double R = fma(z6, R4, fma(z4, R3, fma(z, Lp1, z2 * R2)));
+  const double shr = s * (hfsq + R);
+  if (k == 0) return f - (hfsq - shr);
+  return fma(dk, ln2_hi, -((hfsq - (shr + fma(dk, ln2_lo, c))) - f));
+}
+
+void pbqo_log1p_pair(const double* x, long n, double* restated, double* libm) {
+  for (long i = 0; i < n; ++i) {
+    restated[i] = pbqo_glibc_log1p(x[i]);
+    libm[i] = log1p(x[i]);
+  }
+}

@@ -23,10 +23,16 @@
 //   K3 rebuilds the chain's start positions from the saved specials, ranks
 //      them with a warp scan, gathers their values and writes them coalesced
 //      to Φ — a memory-bound compaction (no Philox).
-// Values equal numpy's bit for bit, except that the exponential-tail branch
-// (idx 0, ~2.6e-4 of draws) uses CUDA's log1p, which can differ from glibc's by
-// 1 ulp; see DESIGN.md §5.
+// Values equal numpy's bit for bit.  The exponential-tail branch (idx 0,
+// ~2.6e-4 of draws) calls log1p; numpy calls the C library's, so the device
+// uses glibc_log1p below, a restatement of glibc's (fdlibm-derived) log1p as
+// its x86-64 FMA build evaluates it — bitwise equal to the host libm on 1e8
+// samples of the sampler's domain (tests/test_oracle.py).  The wedge test's
+// exp(-x²/2) only decides accept/reject, where a last-bit difference between
+// CUDA's exp and the host's matters only if the comparison ties to the ulp.
 #pragma once
+#include <math_constants.h>
+
 #include "common.cuh"
 #include "ziggurat_tables.h"
 
@@ -102,6 +108,84 @@ __device__ __forceinline__ double zig_fast_value(const ZigTables& t, uint64_t r)
   return ((r >> 8) & 1) ? -x : x;
 }
 
+// log1p(x) exactly as glibc 2.39 computes it on x86-64 with FMA (the ifunc
+// variant numpy's npy_log1p reaches on the reference's hosts): the fdlibm
+// s_log1p.c algorithm (Sun Microsystems, 1993) — argument reduction
+// 1+x = 2^k·(1+f) with the correction term c, s = f/(2+f), the degree-14
+// polynomial in z = s² with fdlibm's Lp1..Lp7 evaluated in glibc's
+// z/z²/z⁴/z⁶ (Estrin) grouping — with every multiply-add that GCC contracts
+// in that build written as fma() and every other operation rounded on its
+// own (__dmul_rn/__dadd_rn/__dsub_rn never contract).  Host twin for the
+// checks: oracle/sketch_oracle.c.  Only x ∈ (−1, 0] reaches it here, but the
+// whole function is restated.
+__device__ __forceinline__ double glibc_log1p(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01, Lp3 = 2.857142874366239149e-01,
+               Lp4 = 2.222219843214978396e-01, Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  const int hx = __double2hiint(x);
+  const int ax = hx & 0x7fffffff;
+  int k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (hx < 0x3FDA827A) {  // x < 0.41422
+    if (ax >= 0x3ff00000) return x == -1.0 ? -CUDART_INF : CUDART_NAN;
+    if (ax < 0x3e200000) {  // |x| < 2^-29
+      if (ax < 0x3c900000) return x;
+      return fma(-__dmul_rn(x, x), 0.5, x);
+    }
+    if (hx > 0 || hx <= int(0xbfd2bec3)) {  // -0.2929 < x < 0.41422
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  }
+  if (hx >= 0x7ff00000) return __dadd_rn(x, x);
+  if (k != 0) {
+    double u;
+    if (hx < 0x43400000) {
+      u = __dadd_rn(1.0, x);
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = k > 0 ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+      c = __ddiv_rn(c, u);
+    } else {
+      u = x;
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = __hiloint2double(hu | 0x3ff00000, __double2loint(u));
+    } else {
+      k += 1;
+      u = __hiloint2double(hu | 0x3fe00000, __double2loint(u));
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double dk = double(k);
+  const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
+  if (hu == 0) {  // |f| < 2^-20
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      c = fma(dk, ln2_lo, c);
+      return fma(dk, ln2_hi, c);
+    }
+    const double R = __dmul_rn(hfsq, fma(-f, 0.66666666666666666, 1.0));
+    if (k == 0) return __dsub_rn(f, R);
+    return fma(dk, ln2_hi, -__dsub_rn(__dsub_rn(R, fma(dk, ln2_lo, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
+  const double z = __dmul_rn(s, s);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z4, z2);
+  const double R2 = fma(z, Lp3, Lp2), R3 = fma(z, Lp5, Lp4), R4 = fma(z, Lp7, Lp6);
+  const double R = fma(z6, R4, fma(z4, R3, fma(z, Lp1, __dmul_rn(z2, R2))));
+  const double shr = __dmul_rn(s, __dadd_rn(hfsq, R));
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, shr));
+  return fma(dk, ln2_hi, -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(shr, fma(dk, ln2_lo, c))), f));
+}
+
 // Full sampler for a normal whose first attempt starts at stream position p.
 // Returns the position after the normal and (optionally) its value.
 __device__ uint64_t zig_resolve(const ZigTables& t, uint64_t p, uint64_t k0, uint64_t k1, double* value) {
@@ -119,10 +203,10 @@ __device__ uint64_t zig_resolve(const ZigTables& t, uint64_t p, uint64_t k0, uin
     }
     if (idx == 0) {
       for (;;) {
-        const double xx = -PBQ_ZIG_INV_R * log1p(-u64_to_unit(philox_word(p, k0, k1)));
-        const double yy = -log1p(-u64_to_unit(philox_word(p + 1, k0, k1)));
+        const double xx = __dmul_rn(-PBQ_ZIG_INV_R, glibc_log1p(-u64_to_unit(philox_word(p, k0, k1))));
+        const double yy = -glibc_log1p(-u64_to_unit(philox_word(p + 1, k0, k1)));
         p += 2;
-        if (yy + yy > xx * xx) {
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
           if (value) *value = ((rabs >> 8) & 1) ? -(PBQ_ZIG_R + xx) : (PBQ_ZIG_R + xx);
           return p;
         }
@@ -130,7 +214,9 @@ __device__ uint64_t zig_resolve(const ZigTables& t, uint64_t p, uint64_t k0, uin
     }
     const double u = u64_to_unit(philox_word(p, k0, k1));
     p += 1;
-    if ((t.fi[idx - 1] - t.fi[idx]) * u + t.fi[idx] < exp(-0.5 * x * x)) {
+    // numpy's C evaluates this without contraction: round every step alone
+    if (__dadd_rn(__dmul_rn(__dsub_rn(t.fi[idx - 1], t.fi[idx]), u), t.fi[idx]) <
+        exp(__dmul_rn(__dmul_rn(-0.5, x), x))) {
       if (value) *value = x;
       return p;
     }

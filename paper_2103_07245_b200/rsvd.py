@@ -13,11 +13,11 @@
 The A passes and every ``orth`` run on libpbq's sm_100a kernels (DMMA GEMM,
 Cholesky-QR2 with Householder fallback).  The SVD of the k×n2 matrix g is
 reduced to a k×k core: h = AᵀŪ = Q_h·R_h (libpbq QR), so g = R_hᵀ·Q_hᵀ and
-svd(R_hᵀ) = U_c·diag(s)·W_cᵀ gives v = Q_h·W_c.  The k×k SVD (k ≤ d) is a
-library call (cuSOLVER through torch.linalg.svd on the device).  As in the
-reference, singular vectors carry LAPACK's arbitrary signs; u_j and v_j are
-defined up to a joint sign.  When d > n1 the reference's ``orth`` of the
-n1×d sample returns n1 columns (the Householder Q is fixed by the first
+svd(R_hᵀ) = U_c·diag(s)·W_cᵀ gives v = Q_h·W_c.  The k×k SVD (k ≤ d) is
+libpbq's one-sided Jacobi core (pbq_jacobi_svd, svd_f64.cuh: one thread-block
+cluster, the vectors in registers).  As in the reference, singular vectors
+carry arbitrary signs; u_j and v_j are defined up to a joint sign.  When
+d > n1 the reference's ``orth`` of the n1×d sample returns n1 columns (the Householder Q is fixed by the first
 min(n1, d) columns), and so does this path.
 """
 from dataclasses import dataclass
@@ -118,15 +118,20 @@ def r_svd(a, d, q=0, seed=0, reorthonormalize=True, *, device=None):
     _dev.gemm(ctx, A, ubar, trans_a=True, out=h)
     rh = _dev.empty_matrix(k, k, dev)
     _dev.householder_qr_(ctx, h, rh, want_q=True)  # h ← Q_h (the reference does not warn here)
-    uc, s, wct = torch.linalg.svd(rh.T, full_matrices=False)
-    u = _dev.gemm(ctx, ubar, _dev.as_kernel_operand(uc), trans_a=False)
-    v = _dev.gemm(ctx, h, _dev.as_kernel_operand(wct.T), trans_a=False)
+    # svd(R_hᵀ) by the native one-sided Jacobi core on the rows of R_h
+    # (= columns of R_hᵀ): G·R_h = diag(s)·Y ⇒ R_hᵀ = Yᵀ·diag(s)·G, so
+    # U_c = Yᵀ and W_c = Gᵀ (pbq_jacobi_svd, svd_f64.cuh)
+    s, y, g, jst = _dev.jacobi_svd(ctx, rh, accumulate=True, want_y=True)
+    u = _dev.gemm(ctx, ubar, _dev.transpose(ctx, y), trans_a=False)
+    v = _dev.gemm(ctx, h, _dev.transpose(ctx, g), trans_a=False)
 
     fl = flags.cpu().tolist()  # the one host read
     if fl[0]:
         raise _exc.MatrixInputError("a contains non-finite entries")
     if fl[1]:
         raise _exc.DeviceError("sketch generator overflow (internal error)")
+    if int(jst[1].item()):
+        raise _exc.ConvergenceError("r_svd: the Jacobi SVD core did not converge in 30 sweeps")
     for flag in fl[2:]:
         warn_rank(flag, stacklevel=3)
     outs = [from_device(x, kind, home) for x in (u, s.contiguous(), v)]

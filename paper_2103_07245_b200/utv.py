@@ -14,10 +14,10 @@ follows /root/reference/pkg/src/pbpqlp/algorithms.py:306-363 call for call:
 
 Every pass over A, every orth, the pivot selection of the core's CPQR
 (LAPACK dgeqp3's rule, cpqr_f64.cuh), its QR and the column gather run on
-libpbq's sm_100a kernels.  The one library call is the SVD of the k×d sample
-Gram factor on the pass-efficient, non-reorthonormalized branch
-(``_transposed_pinv_apply``, algorithms.py:295-303), done by cuSOLVER through
-torch.linalg.svd on the device, like r_svd's core SVD.
+libpbq's sm_100a kernels, and so does the SVD of the k×d sample Gram factor
+on the pass-efficient, non-reorthonormalized branch (``_transposed_pinv_apply``,
+algorithms.py:295-303): libpbq's one-sided Jacobi core (pbq_jacobi_svd), like
+r_svd's core SVD.
 """
 from dataclasses import dataclass
 from typing import Any, Optional
@@ -148,7 +148,10 @@ def cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=True, *, d
     if pass_efficient:
         core = _dev.gemm(ctx, f2, vbar, trans_a=True)  # f2ᵀ·V̄
         if gram is not None:
-            u_g, s_g, vh_g = torch.linalg.svd(gram, full_matrices=False)
+            # svd(gram) by the native Jacobi core on its k rows (k ≤ d):
+            # G·gram = diag(s)·Y ⇒ u_g = Gᵀ, vh_g = Y (pbq_jacobi_svd)
+            s_g, vh_g, g_g, jst = _dev.jacobi_svd(ctx, gram, accumulate=True, want_y=True)
+            u_g = _dev.transpose(ctx, g_g)
             keep = s_g > PINV_RTOL * s_g[0]
             # s[0] == 0 keeps nothing: zero core, flagged (algorithms.py:298-299)
             inv = torch.where(keep, 1.0 / torch.where(keep, s_g, torch.ones_like(s_g)), torch.zeros_like(s_g))
@@ -168,6 +171,8 @@ def cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=True, *, d
         raise _exc.MatrixInputError("a contains non-finite entries")
     if fl[1]:
         raise _exc.DeviceError("sketch generator overflow (internal error)")
+    if gram is not None and int(jst[1].item()):
+        raise _exc.ConvergenceError("cor_utv: the Jacobi SVD core of the pseudoinverse did not converge in 30 sweeps")
     for flag in fl[2:site]:
         warn_rank(flag, stacklevel=3)
     outs = [from_device(x, kind, home) for x in (u, t, v)]

@@ -87,8 +87,7 @@ def test_sharded_device_path_matches_oracle(cuda, tmp_path, world, q, reorth, ch
     ref = oracle_pbp_qlp(a, d, q=q, seed=9, reorthonormalize=reorth)
     assert all(int(p["launches"]) > 0 for p in parts)  # the device kernels ran in every rank
     phi = np.vstack([p["phi"] for p in parts])
-    diff = phi != ref["phi"]  # device sketch: bit-exact but for ≤ 1-ulp exponential-tail draws
-    assert np.count_nonzero(diff) <= 2
+    assert np.array_equal(phi, ref["phi"])  # device sketch: bit-exact
     for p in parts[1:]:  # replicated factors are bitwise identical across ranks
         for k in ("l", "p", "r"):
             assert np.array_equal(p[k], parts[0][k])

@@ -29,8 +29,7 @@ def test_matches_reference_fixture(cuda, name):
     assert sum(1 for w in rec if issubclass(w.category, RankDeficiencyWarning)) == case["rank_warnings"]
     assert f.sketch.passes_over_a == case["passes_over_a"]
     phi = f.sketch.test_matrix
-    diff = phi != g["phi"]
-    assert np.count_nonzero(diff) <= 2 and np.all(np.abs(phi[diff] - g["phi"][diff]) <= 2 * np.spacing(np.abs(g["phi"][diff])))
+    assert np.array_equal(phi, g["phi"])  # the reference's own sketch, bit for bit
     assert f.q_basis.shape == g["q"].shape and f.p_basis.shape == g["p"].shape
     assert np.array_equal(f.l, np.tril(f.l)) and np.all(np.diag(f.l) >= 0)
     assert np.array_equal(f.first_stage_r, np.triu(f.first_stage_r)) and np.all(np.diag(f.first_stage_r) >= 0)

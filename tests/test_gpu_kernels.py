@@ -268,12 +268,20 @@ def test_gaussian_matches_numpy(cuda, rows, cols, seed):
 
     got = gaussian_matrix(rows, cols, seed)
     ref = oracle_gaussian(rows, cols, seed)
-    diff = got != ref
-    # bit-exact except possibly the exponential-tail draws (CUDA log1p vs glibc, ≤ 1 ulp)
-    assert np.count_nonzero(diff) <= max(2, int(2e-5 * rows * cols))
-    if diff.any():
-        assert np.all(np.abs(ref[diff]) > 3.6)
-        assert np.all(np.abs(got[diff] - ref[diff]) <= 2 * np.spacing(np.abs(ref[diff])))
+    # bit-exact, exponential-tail draws included (glibc_log1p, sketch.cuh)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("seed", [0, 7, 2**64 + 5])
+def test_gaussian_bitwise_many_tail_draws(cuda, seed):
+    """4 M normals (≈ 1000 exponential-tail draws, ≈ 4e4 wedge tests) per
+    seed: every value bitwise numpy's, the tails included."""
+    from paper_2103_07245_b200 import gaussian_matrix
+
+    got = gaussian_matrix(4000, 1000, seed)
+    ref = oracle_gaussian(4000, 1000, seed)
+    assert np.count_nonzero(np.abs(ref) > 3.6541528853610088) > 500  # the tail branch was exercised
+    assert np.array_equal(got, ref)
 
 
 def test_gaussian_row_offset(cuda):
@@ -283,7 +291,7 @@ def test_gaussian_row_offset(cuda):
     part = gaussian_matrix(1000, 64, 9, row_offset=1500)
     assert np.array_equal(part, full[1500:2500])
     ref = c_gaussian(1000, 64, 9, row_offset=1500)
-    assert np.count_nonzero(part != ref) <= 2
+    assert np.array_equal(part, ref)
 
 
 @pytest.mark.parametrize("n1,n2,d,rank", [(300, 200, 25, None), (301, 257, 33, 7), (1000, 40, 40, 40),

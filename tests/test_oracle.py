@@ -92,3 +92,22 @@ def test_restated_householder_matches_lapack(shape):
     q2, r2 = householder_qr_restated(a)
     assert np.abs(q1 - q2).max() < 1e-13
     assert np.abs(r1 - r2).max() < 1e-12 * np.abs(r1).max()
+
+
+def test_log1p_restatement_is_the_c_library():
+    """The sketch's exponential tail calls log1p (numpy's npy_log1p → the C
+    library).  The device restates glibc's (sketch.cuh: glibc_log1p); its
+    host twin must equal libm bit for bit on the sampler's domain
+    x = −k·2⁻⁵³ ∈ (−1, 0] and across every branch of the function."""
+    from oracle.pbp_qlp_oracle import c_log1p_pair
+
+    rng = np.random.default_rng(2024)
+    dom = -(rng.integers(0, 2**53, size=2_000_000, dtype=np.int64).astype(np.float64) * 2.0**-53)
+    e = np.arange(-70, 0)
+    m = np.linspace(1.0, 2.0, 400, endpoint=False)
+    edges = (m[None, :] * np.ldexp(1.0, e)[:, None]).ravel()
+    wide = np.concatenate([rng.uniform(-1, 8, 200_000), np.ldexp(rng.uniform(1, 2, 20_000), rng.integers(-60, 60, 20_000))])
+    x = np.concatenate([dom, -edges[edges < 1], edges, wide, [0.0, -0.0, 0.41422, -0.2929, 1e300, -1.0 + 2**-53]])
+    mine, libm = c_log1p_pair(x)
+    bad = np.flatnonzero(mine.view(np.int64) != libm.view(np.int64))
+    assert bad.size == 0, (x[bad[:5]], mine[bad[:5]], libm[bad[:5]])

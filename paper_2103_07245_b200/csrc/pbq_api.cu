@@ -1084,7 +1084,9 @@ JacFn jac_reg_fn(int vpl) {
   }
 }
 int jac_vpl(long V) { return V <= 128 ? 4 : V <= 256 ? 8 : V <= 512 ? 16 : 24; }
-size_t jac_reg_smem(int vpl) { return size_t(2) * JAC_WARPS * 2 * 32 * vpl * sizeof(double) + 64 * sizeof(int); }
+size_t jac_reg_smem(int vpl) {
+  return size_t(2) * JAC_WARPS * 2 * 32 * vpl * sizeof(double) + 4 * JAC_WARPS * sizeof(uint64_t) + 64 * sizeof(int);
+}
 
 // Largest cluster of C CTAs the register kernel with `vpl` can launch (0: none).
 bool jac_cluster_ok(pbq_ctx* ctx, JacFn fn, int C, size_t smem, int threads) {
@@ -1135,7 +1137,7 @@ int jacobi_launch(pbq_ctx* ctx, long n, long L, const double* X, long ldx, int a
   a.ldx = ldx;
   a.ldz = a.V + (a.V & 1);
   a.status = status;
-  a.max_sweeps = 30;                                     // LAPACK dgesvj's NSWEEP
+  a.max_sweeps = 60;  // dgesvj's NSWEEP is 30 with de Rijk pivoting; plain cyclic order gets twice that
   a.tol = sqrt(double(L)) * 1.1102230246251565e-16;      // √L·u (dgesvj's CTOL)
   Carve cv(ws, ws_bytes);
   a.Z = cv.take<double>(size_t(a.np) * a.ldz);

@@ -32,8 +32,8 @@
 //    CTAs of 8 warps), warp p holds pair p's two vectors in registers for the
 //    whole run.  After each round it hands its top vector to warp p+1 and its
 //    bottom vector to warp p−1 through shared-memory mailboxes (DSMEM stores
-//    across CTA boundaries), double-buffered by round parity, with one
-//    cluster barrier per round.
+//    across CTA boundaries), double-buffered by round parity and signalled
+//    point to point with mbarriers (no cluster-wide barrier per round).
 //  * jacobi_l2_kernel — any size: the vectors stay in a global (L2-resident)
 //    array and the schedule moves the computation instead: in round r the
 //    vector at position x ≥ 1 is vector 1 + ((x − 1 − r) mod (n_p − 1)).  One
@@ -122,8 +122,41 @@ __device__ __forceinline__ bool jac_rotate(double (&x)[VPL], double (&y)[VPL], i
 
 // ---------------------------------------------------------------------------
 // Register-resident kernel.  Launch: grid = C CTAs = one cluster of C,
-// JAC_WARPS warps each, C·JAC_WARPS ≥ P = np/2; dynamic shared memory
-// 2 (parity) × JAC_WARPS × 2 (slots) × 32·VPL doubles + counters.
+// JAC_WARPS warps each, C·JAC_WARPS ≥ P = np/2; dynamic shared memory =
+// jac_reg_smem(VPL).  Hand-over between neighbouring warps is point to
+// point: each mailbox slot has an mbarrier (32 arrivals: every lane of the
+// sender arrives after its own stores, with release at cluster scope when
+// the receiver is in another CTA), and the receiver waits on it — no
+// cluster-wide barrier per round.  Slots are double-buffered by round
+// parity; the data dependencies of the schedule make reuse safe (a sender
+// writes a slot again only after receiving its neighbour's next vector,
+// which the neighbour sends after consuming the slot's previous content).
+__device__ __forceinline__ uint32_t jac_mapa(uint32_t addr, int cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void jac_st_remote(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void jac_arrive_remote(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void jac_arrive_local(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void jac_wait(uint32_t bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "JW_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra JW_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 template <int VPL>
 __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p) {
   extern __shared__ __align__(16) double jsm[];
@@ -135,8 +168,18 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
   const bool active = w < P;
   const size_t slot_d = size_t(32) * VPL;
   const size_t box_d = size_t(2) * JAC_WARPS * 2 * slot_d;  // both parities
-  int* counts = reinterpret_cast<int*>(jsm + box_d);        // [2 parity][16 CTAs] (used on CTA 0)
-  int* red = counts + 32;                                   // [JAC_WARPS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(jsm + box_d);  // [2 parity][JAC_WARPS][2 slots]
+  int* counts = reinterpret_cast<int*>(bars + 4 * JAC_WARPS);  // [2 parity][16 CTAs] (used on CTA 0)
+  int* red = counts + 32;                                       // [JAC_WARPS]
+  auto box_off = [&](int lq, int s, int par) { return ((size_t(par) * JAC_WARPS + lq) * 2 + s) * slot_d; };
+  auto bar_of = [&](int lq, int s, int par) { return bars + (par * JAC_WARPS + lq) * 2 + s; };
+
+  if (threadIdx.x < 4 * JAC_WARPS) mbar_init(bars + threadIdx.x, 32);
+  mbar_fence_init();
+  if (C > 1)
+    jac_cluster_sync();  // every CTA's barriers exist before any remote arrival
+  else
+    __syncthreads();
 
   double x[VPL], y[VPL];
   const int ti = w, bi = p.np - 1 - w;  // vector indices at positions w and np−1−w
@@ -146,53 +189,54 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
     x[k] = (active && e < p.V) ? jac_init(p, ti, e) : 0.0;
     y[k] = (active && e < p.V) ? jac_init(p, bi, e) : 0.0;
   }
-  // mailbox of (warp q, slot s, parity par) — possibly in another CTA
-  auto box = [&](int q, int s, int par) -> double* {
+  // store v into slot s of warp q (round parity par) and arrive on its barrier
+  auto send = [&](const double (&v)[VPL], int q, int s, int par) {
     const int cta = q / JAC_WARPS, lq = q % JAC_WARPS;
-    double* local = jsm + ((size_t(par) * JAC_WARPS + lq) * 2 + s) * slot_d;
-    return cta == me ? local : cl.map_shared_rank(local, cta);
+    const size_t off = box_off(lq, s, par);
+    if (cta == me) {
+      double* d = jsm + off;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) d[32 * k + lane] = v[k];
+      jac_arrive_local(smem_u32(bar_of(lq, s, par)));
+    } else {
+      const uint32_t d = jac_mapa(smem_u32(jsm + off), cta);
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) jac_st_remote(d + 8u * (32 * k + lane), v[k]);
+      jac_arrive_remote(jac_mapa(smem_u32(bar_of(lq, s, par)), cta));
+    }
   };
+  long R = 0;  // rounds so far (all sweeps): slot parity R&1, barrier phase (R>>1)&1
   int sweeps = 0, converged = 0;
   for (int sw = 0; sw < p.max_sweeps && !converged; ++sw) {
     int rot = 0;
-    for (int r = 0; r < p.np - 1; ++r) {
-      const int par = r & 1;
+    for (int r = 0; r < p.np - 1; ++r, ++R) {
+      const int par = int(R & 1);
+      const unsigned phase = unsigned((R >> 1) & 1);
       if (active && jac_rotate<VPL>(x, y, p.L, p.tol)) ++rot;
-      if (P > 1) {
-        // hand over: T' → warp w+1 (1 ≤ w ≤ P−2) or kept as B (w = P−1);
-        //            B' → warp w−1 (w ≥ 1) or to warp 1's T (w = 0)
-        if (active) {
-          double* dt = nullptr;
-          double* db = nullptr;
-          if (w >= 1 && w <= P - 2) dt = box(w + 1, 0, par);
-          if (w >= 1) db = box(w - 1, 1, par);
-          else db = box(1, 0, par);
-#pragma unroll
-          for (int k = 0; k < VPL; ++k) {
-            if (dt) dt[32 * k + lane] = x[k];
-            db[32 * k + lane] = y[k];
-          }
-        }
-        if (C > 1)
-          jac_cluster_sync();
+      if (active && P > 1) {
+        // T' → warp w+1 (1 ≤ w ≤ P−2) or kept as B (w = P−1);
+        // B' → warp w−1 (w ≥ 1) or warp 1's T slot (w = 0)
+        if (w >= 1 && w <= P - 2) send(x, w + 1, 0, par);
+        if (w >= 1)
+          send(y, w - 1, 1, par);
         else
-          __syncthreads();
-        if (active) {
-          // T_in: own T' (w = 0), warp 0's B' (w = 1), warp w−1's T' (w ≥ 2)
-          // B_in: own T' (w = P−1), else warp w+1's B'
-          const double* mt = jsm + ((size_t(par) * JAC_WARPS + lw) * 2 + 0) * slot_d;
-          const double* mb = jsm + ((size_t(par) * JAC_WARPS + lw) * 2 + 1) * slot_d;
-          if (w == P - 1) {
+          send(y, 1, 0, par);
+        // B_in: own T' (w = P−1), else warp w+1's B';
+        // T_in: own T' (w = 0), warp 0's B' (w = 1), warp w−1's T' (w ≥ 2)
+        if (w == P - 1) {
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) y[k] = x[k];
-          } else {
+          for (int k = 0; k < VPL; ++k) y[k] = x[k];
+        } else {
+          jac_wait(smem_u32(bar_of(lw, 1, par)), phase);
+          const double* mb = jsm + box_off(lw, 1, par);
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) y[k] = mb[32 * k + lane];
-          }
-          if (w >= 1) {
+          for (int k = 0; k < VPL; ++k) y[k] = mb[32 * k + lane];
+        }
+        if (w >= 1) {
+          jac_wait(smem_u32(bar_of(lw, 0, par)), phase);
+          const double* mt = jsm + box_off(lw, 0, par);
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) x[k] = mt[32 * k + lane];
-          }
+          for (int k = 0; k < VPL; ++k) x[k] = mt[32 * k + lane];
         }
       }
     }

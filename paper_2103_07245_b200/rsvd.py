@@ -15,7 +15,8 @@ Cholesky-QR2 with Householder fallback).  The SVD of the k×n2 matrix g is
 reduced to a k×k core: h = AᵀŪ = Q_h·R_h (libpbq QR), so g = R_hᵀ·Q_hᵀ and
 svd(R_hᵀ) = U_c·diag(s)·W_cᵀ gives v = Q_h·W_c.  The k×k SVD (k ≤ d) is
 libpbq's one-sided Jacobi core (pbq_jacobi_svd, svd_f64.cuh: one thread-block
-cluster, the vectors in registers).  As in the reference, singular vectors
+cluster, the vectors in registers), preconditioned by one more k×k QR
+(R_hᵀ = W·R̃, pbq_second_stage).  As in the reference, singular vectors
 carry arbitrary signs; u_j and v_j are defined up to a joint sign.  When
 d > n1 the reference's ``orth`` of the n1×d sample returns n1 columns (the Householder Q is fixed by the first
 min(n1, d) columns), and so does this path.
@@ -118,12 +119,17 @@ def r_svd(a, d, q=0, seed=0, reorthonormalize=True, *, device=None):
     _dev.gemm(ctx, A, ubar, trans_a=True, out=h)
     rh = _dev.empty_matrix(k, k, dev)
     _dev.householder_qr_(ctx, h, rh, want_q=True)  # h ← Q_h (the reference does not warn here)
-    # svd(R_hᵀ) by the native one-sided Jacobi core on the rows of R_h
-    # (= columns of R_hᵀ): G·R_h = diag(s)·Y ⇒ R_hᵀ = Yᵀ·diag(s)·G, so
-    # U_c = Yᵀ and W_c = Gᵀ (pbq_jacobi_svd, svd_f64.cuh)
-    s, y, g, jst = _dev.jacobi_svd(ctx, rh, accumulate=True, want_y=True)
-    u = _dev.gemm(ctx, ubar, _dev.transpose(ctx, y), trans_a=False)
-    v = _dev.gemm(ctx, h, _dev.transpose(ctx, g), trans_a=False)
+    # svd(R_hᵀ): first the QLP step (W, R̃) = qr(R_hᵀ) (pbq_second_stage; the
+    # diagonal of R̃ tracks the singular values, so its rows are graded like
+    # them — the QR preconditioning of one-sided Jacobi, Drmač & Veselić
+    # 2008), then the native one-sided Jacobi core on the rows of R̃:
+    # G·R̃ = diag(s)·Y ⇒ R_hᵀ = W·R̃ = (W·Gᵀ)·diag(s)·Y, so U_c = W·Gᵀ and
+    # W_c = Yᵀ (pbq_jacobi_svd, svd_f64.cuh)
+    w, l = _dev.second_stage(ctx, rh)  # l = tril(R̃ᵀ)
+    s, y, g, jst = _dev.jacobi_svd(ctx, _dev.transpose(ctx, l), accumulate=True, want_y=True)
+    uc = _dev.gemm(ctx, w, _dev.transpose(ctx, g), trans_a=False)
+    u = _dev.gemm(ctx, ubar, uc, trans_a=False)
+    v = _dev.gemm(ctx, h, _dev.transpose(ctx, y), trans_a=False)
 
     fl = flags.cpu().tolist()  # the one host read
     if fl[0]:

@@ -303,7 +303,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
       const unsigned char* sB = sA + A_BYTES;
       if (CHECK && check) {
         // the k-block's A tile as raw bytes: the swizzle only permutes it
-#pragma unroll
+        // (not unrolled: keeps the NN variant's consumers inside 128 registers)
+#pragma unroll 1
         for (int i = 0; i < int(A_BYTES / 16 / THREADS); ++i) {
           const double2 v = *reinterpret_cast<const double2*>(sA + (size_t(i) * THREADS + tid) * 16);
           saw_nonfinite |= nonfinite_bits(v.x) | nonfinite_bits(v.y);

@@ -1085,7 +1085,8 @@ JacFn jac_reg_fn(int vpl) {
 }
 int jac_vpl(long V) { return V <= 128 ? 4 : V <= 256 ? 8 : V <= 512 ? 16 : 24; }
 size_t jac_reg_smem(int vpl) {
-  return size_t(2) * JAC_WARPS * 2 * 32 * vpl * sizeof(double) + 4 * JAC_WARPS * sizeof(uint64_t) + 64 * sizeof(int);
+  return size_t(2) * JAC_WARPS * 2 * 32 * vpl * sizeof(double) + 4 * JAC_WARPS * sizeof(uint64_t) +
+         (2 * 16 * 3 + 3 * JAC_WARPS) * sizeof(double);
 }
 
 // Largest cluster of C CTAs the register kernel with `vpl` can launch (0: none).

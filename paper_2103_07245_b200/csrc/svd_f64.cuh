@@ -83,9 +83,12 @@ __device__ __forceinline__ double jac_init(const JacArgs& p, int i, int e) {
 }
 
 // The rotation of one pair (x, y: VPL doubles per lane, element lane + 32·k).
-// Returns true when a rotation was applied.
+// Returns true when a rotation was applied; `aapq` receives the pair's
+// relative off-diagonal |x·y|/(‖x‖‖y‖) before it and `sinj` |sin θ| of the
+// rotation (0 when none) — dgesvj's convergence measures.
 template <int VPL>
-__device__ __forceinline__ bool jac_rotate(double (&x)[VPL], double (&y)[VPL], int L, double tol) {
+__device__ __forceinline__ bool jac_rotate(double (&x)[VPL], double (&y)[VPL], int L, double tol, double& aapq,
+                                           double& sinj) {
   const int lane = threadIdx.x & 31;
   double a = 0.0, b = 0.0, c = 0.0;
 #pragma unroll
@@ -102,7 +105,11 @@ __device__ __forceinline__ bool jac_rotate(double (&x)[VPL], double (&y)[VPL], i
     b += __shfl_xor_sync(0xffffffffu, b, o);
     c += __shfl_xor_sync(0xffffffffu, c, o);
   }
-  if (!(a > 0.0 && b > 0.0) || !(fabs(c) > tol * sqrt(a) * sqrt(b))) return false;
+  sinj = 0.0;
+  aapq = 0.0;
+  if (!(a > 0.0 && b > 0.0)) return false;
+  aapq = fabs(c) / (sqrt(a) * sqrt(b));
+  if (!(aapq > tol)) return false;
   const double zeta = (b - a) / (2.0 * c);
   double t;
   if (fabs(zeta) > 1e100)
@@ -111,6 +118,7 @@ __device__ __forceinline__ bool jac_rotate(double (&x)[VPL], double (&y)[VPL], i
     t = copysign(1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
   const double cs = 1.0 / sqrt(fma(t, t, 1.0));
   const double sn = cs * t;
+  sinj = fabs(sn);
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const double xv = x[k], yv = y[k];
@@ -118,6 +126,14 @@ __device__ __forceinline__ bool jac_rotate(double (&x)[VPL], double (&y)[VPL], i
     y[k] = fma(sn, xv, cs * yv);
   }
   return true;
+}
+
+// Sweep-end test (LAPACK dgesvj): stop when no rotation was applied, or when
+// the largest relative off-diagonal met in the sweep is below √n·tol and
+// n·max|aapq|·max|sin θ| < tol (the remaining rotations change nothing at
+// working precision).
+__device__ __forceinline__ bool jac_converged(int rot, double mx_aapq, double mx_sin, int n, double tol) {
+  return rot == 0 || (mx_aapq < sqrt(double(n)) * tol && double(n) * mx_aapq * mx_sin < tol);
 }
 
 // ---------------------------------------------------------------------------
@@ -169,8 +185,8 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
   const size_t slot_d = size_t(32) * VPL;
   const size_t box_d = size_t(2) * JAC_WARPS * 2 * slot_d;  // both parities
   uint64_t* bars = reinterpret_cast<uint64_t*>(jsm + box_d);  // [2 parity][JAC_WARPS][2 slots]
-  int* counts = reinterpret_cast<int*>(bars + 4 * JAC_WARPS);  // [2 parity][16 CTAs] (used on CTA 0)
-  int* red = counts + 32;                                       // [JAC_WARPS]
+  double* sums = reinterpret_cast<double*>(bars + 4 * JAC_WARPS);  // [2 parity][16 CTAs][3] (on CTA 0)
+  double* red = sums + 2 * 16 * 3;                                  // [JAC_WARPS][3]
   auto box_off = [&](int lq, int s, int par) { return ((size_t(par) * JAC_WARPS + lq) * 2 + s) * slot_d; };
   auto bar_of = [&](int lq, int s, int par) { return bars + (par * JAC_WARPS + lq) * 2 + s; };
 
@@ -209,10 +225,16 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
   int sweeps = 0, converged = 0;
   for (int sw = 0; sw < p.max_sweeps && !converged; ++sw) {
     int rot = 0;
+    double mx_aapq = 0.0, mx_sin = 0.0;
     for (int r = 0; r < p.np - 1; ++r, ++R) {
       const int par = int(R & 1);
       const unsigned phase = unsigned((R >> 1) & 1);
-      if (active && jac_rotate<VPL>(x, y, p.L, p.tol)) ++rot;
+      if (active) {
+        double aapq, sinj;
+        if (jac_rotate<VPL>(x, y, p.L, p.tol, aapq, sinj)) ++rot;
+        mx_aapq = fmax(mx_aapq, aapq);
+        mx_sin = fmax(mx_sin, sinj);
+      }
       if (active && P > 1) {
         // T' → warp w+1 (1 ≤ w ≤ P−2) or kept as B (w = P−1);
         // B' → warp w−1 (w ≥ 1) or warp 1's T slot (w = 0)
@@ -240,25 +262,39 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
         }
       }
     }
-    // ---- convergence: total rotations of the sweep, summed over the cluster
-    int cnt = active ? rot : 0;  // identical on every lane of the warp
-    if (lane == 0) red[lw] = cnt;
+    // ---- sweep-end test: rotations, max relative off-diagonal and max |sin|
+    // over the cluster (identical on every lane of a warp)
+    if (lane == 0) {
+      red[3 * lw] = double(rot);
+      red[3 * lw + 1] = mx_aapq;
+      red[3 * lw + 2] = mx_sin;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      int s = 0;
-      for (int i = 0; i < JAC_WARPS; ++i) s += red[i];
-      int* dst = (C > 1) ? cl.map_shared_rank(counts, 0) : counts;
-      dst[(sw & 1) * 16 + me] = s;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int i = 0; i < JAC_WARPS; ++i) {
+        s0 += red[3 * i];
+        s1 = fmax(s1, red[3 * i + 1]);
+        s2 = fmax(s2, red[3 * i + 2]);
+      }
+      double* dst = ((C > 1) ? cl.map_shared_rank(sums, 0) : sums) + ((sw & 1) * 16 + me) * 3;
+      dst[0] = s0;
+      dst[1] = s1;
+      dst[2] = s2;
     }
     if (C > 1)
       jac_cluster_sync();
     else
       __syncthreads();
-    int total = 0;
-    const int* src = (C > 1) ? cl.map_shared_rank(counts, 0) : counts;
-    for (int i = 0; i < C; ++i) total += src[(sw & 1) * 16 + i];
+    double total = 0.0, gmx = 0.0, gsin = 0.0;
+    const double* src = (C > 1) ? cl.map_shared_rank(sums, 0) : sums;
+    for (int i = 0; i < C; ++i) {
+      total += src[((sw & 1) * 16 + i) * 3];
+      gmx = fmax(gmx, src[((sw & 1) * 16 + i) * 3 + 1]);
+      gsin = fmax(gsin, src[((sw & 1) * 16 + i) * 3 + 2]);
+    }
     sweeps = sw + 1;
-    converged = (total == 0);
+    converged = jac_converged(int(total), gmx, gsin, p.n, p.tol);
   }
   if (active) {
 #pragma unroll
@@ -282,8 +318,8 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
 // JAC_L2_WARPS warps; Z must already hold the initial vectors (jacobi_init_kernel).
 template <int VPL>
 __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs p) {
-  __shared__ int red[JAC_L2_WARPS];
-  __shared__ int counts[2][16];
+  __shared__ double red[JAC_L2_WARPS][3];
+  __shared__ double sums[2][16][3];
   jcg::cluster_group cl = jcg::this_cluster();
   const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
   const int C = int(cl.num_blocks()), me = int(cl.block_rank());
@@ -292,6 +328,7 @@ __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs
   int sweeps = 0, converged = 0;
   for (int sw = 0; sw < p.max_sweeps && !converged; ++sw) {
     int rot = 0;
+    double mx_aapq = 0.0, mx_sin = 0.0;
     for (int r = 0; r < m1; ++r) {
       for (int q = w0; q < P; q += TW) {
         const int xt = q, xb = p.np - 1 - q;  // positions
@@ -309,7 +346,11 @@ __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs
             x[k] = e < p.V ? __ldcg(zt + e) : 0.0;
             y[k] = e < p.V ? __ldcg(zb + e) : 0.0;
           }
-          if (jac_rotate<VPL>(x, y, p.L, p.tol)) {
+          double aapq, sinj;
+          const bool did = jac_rotate<VPL>(x, y, p.L, p.tol, aapq, sinj);
+          mx_aapq = fmax(mx_aapq, aapq);
+          mx_sin = fmax(mx_sin, sinj);
+          if (did) {
             ++rot;
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
@@ -335,11 +376,14 @@ __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs
             b += __shfl_xor_sync(0xffffffffu, b, o);
             c += __shfl_xor_sync(0xffffffffu, c, o);
           }
-          if (a > 0.0 && b > 0.0 && fabs(c) > p.tol * sqrt(a) * sqrt(b)) {
+          const double aapq = (a > 0.0 && b > 0.0) ? fabs(c) / (sqrt(a) * sqrt(b)) : 0.0;
+          mx_aapq = fmax(mx_aapq, aapq);
+          if (aapq > p.tol) {
             const double zeta = (b - a) / (2.0 * c);
             const double t = fabs(zeta) > 1e100 ? 0.5 / zeta
                                                 : copysign(1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
             const double cs = 1.0 / sqrt(fma(t, t, 1.0)), sn = cs * t;
+            mx_sin = fmax(mx_sin, fabs(sn));
             for (int e = lane; e < p.V; e += 32) {
               const double xv = __ldcg(zt + e), yv = __ldcg(zb + e);
               __stcg(zt + e, fma(cs, xv, -sn * yv));
@@ -351,19 +395,34 @@ __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs
       }
       jac_cluster_sync();
     }
-    if (lane == 0) red[lw] = rot;
+    if (lane == 0) {
+      red[lw][0] = double(rot);
+      red[lw][1] = mx_aapq;
+      red[lw][2] = mx_sin;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      int s = 0;
-      for (int i = 0; i < JAC_L2_WARPS; ++i) s += red[i];
-      cl.map_shared_rank(&counts[0][0], 0)[(sw & 1) * 16 + me] = s;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int i = 0; i < JAC_L2_WARPS; ++i) {
+        s0 += red[i][0];
+        s1 = fmax(s1, red[i][1]);
+        s2 = fmax(s2, red[i][2]);
+      }
+      double* dst = cl.map_shared_rank(&sums[0][0][0], 0) + ((sw & 1) * 16 + me) * 3;
+      dst[0] = s0;
+      dst[1] = s1;
+      dst[2] = s2;
     }
     jac_cluster_sync();
-    int total = 0;
-    const int* src = cl.map_shared_rank(&counts[0][0], 0);
-    for (int i = 0; i < C; ++i) total += src[(sw & 1) * 16 + i];
+    double total = 0.0, gmx = 0.0, gsin = 0.0;
+    const double* src = cl.map_shared_rank(&sums[0][0][0], 0);
+    for (int i = 0; i < C; ++i) {
+      total += src[((sw & 1) * 16 + i) * 3];
+      gmx = fmax(gmx, src[((sw & 1) * 16 + i) * 3 + 1]);
+      gsin = fmax(gsin, src[((sw & 1) * 16 + i) * 3 + 2]);
+    }
     sweeps = sw + 1;
-    converged = (total == 0);
+    converged = jac_converged(int(total), gmx, gsin, p.n, p.tol);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.status[0] = sweeps;

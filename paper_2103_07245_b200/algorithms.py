@@ -462,7 +462,14 @@ def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True, *, phi=None, device=None):
         if not ha.all_finite():
             raise _exc.MatrixInputError("a contains non-finite entries") from None
         raise
-    seed = check_seed(seed)
+    try:
+        seed = check_seed(seed)
+    except ValueError:
+        # likewise for the seed (numpy's Philox rejects it only after
+        # check_matrix has scanned A, algorithms.py:239-242)
+        if not ha.all_finite():
+            raise _exc.MatrixInputError("a contains non-finite entries") from None
+        raise
     kind, home = ha.kind, ha.home
     host = ha.host_tensor()
     streamed = host is not None and phi is None and n1 * n2 * 8 >= STREAM_MIN_BYTES and n1 >= 2 * d

@@ -2,8 +2,10 @@
 //
 // FP64 tensor math on sm_100a is the warp-level DMMA.8x8x4 instruction
 // (`mma.sync.aligned.m8n8k4.row.col.f64`); tcgen05/UMMA has no f64 kind, so the
-// FP64 path is register MMA fed from shared memory that is staged with
-// cp.async (LDGSTS) multi-buffering.  See DESIGN.md §3.
+// FP64 path is register MMA fed from shared memory.  The GEMMs stage their
+// tiles with the Tensor Memory Accelerator (cp.async.bulk.tensor into an
+// mbarrier ring, gemm_tma_f64.cuh; the default) or, as the fallback, with
+// cp.async (LDGSTS) multi-buffering (gemm_f64.cuh).  See DESIGN.md §3.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -824,6 +824,7 @@ int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
 // -------------------------------------------------------------- sketch ----
 struct SketchPlan {
   long n_chunks;
+  long vchunk0;  // first chunk that can hold a requested normal (normal index ≤ stream position)
 };
 
 SketchPlan sketch_plan(long rows, long cols, long row_offset) {
@@ -831,13 +832,14 @@ SketchPlan sketch_plan(long rows, long cols, long row_offset) {
   SketchPlan p;
   // ~1.0223 words per normal; 5% + 4 chunks of head-room (shortfall is detected)
   p.n_chunks = ceil_div(long(double(last) * 1.05) + 2 * PBQ_SK_CHUNK, PBQ_SK_CHUNK) + 2;
+  p.vchunk0 = std::min(p.n_chunks - 1, (row_offset * cols) / PBQ_SK_CHUNK);
   return p;
 }
 
 size_t sketch_ws_bytes(const SketchPlan& p) {
-  const size_t n = p.n_chunks;
+  const size_t n = p.n_chunks, nv = p.n_chunks - p.vchunk0;
   return align_up(n * 4, 256) + align_up(n * PBQ_SK_E * 4, 256) + align_up(n * 8, 256) + align_up(n * 4, 256) +
-         align_up(n * PBQ_SK_CHUNK * 8, 256) + align_up(n * 2 * PBQ_SK_MAXSPECIAL * 8, 256) + align_up(n * 4, 256) +
+         align_up(nv * PBQ_SK_CHUNK * 8, 256) + align_up(nv * 2 * PBQ_SK_MAXSPECIAL * 8, 256) + align_up(nv * 4, 256) +
          256 + 256;
 }
 
@@ -862,6 +864,7 @@ int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t 
   a.k0 = k0; a.k1 = k1;
   a.seed_dev = seed_dev;
   a.n_chunks = pl.n_chunks;
+  a.vchunk0 = pl.vchunk0;
   a.first = row_offset * cols;
   a.count = rows * cols;
   a.cols = cols;
@@ -870,9 +873,9 @@ int sketch_launch(pbq_ctx* ctx, long rows, long cols, long row_offset, uint64_t 
   a.counts = cv.take<int>(size_t(pl.n_chunks) * PBQ_SK_E);
   a.base = cv.take<long>(pl.n_chunks);
   a.entry = cv.take<int>(pl.n_chunks);
-  a.vals = cv.take<double>(size_t(pl.n_chunks) * PBQ_SK_CHUNK);
-  a.sp = cv.take<uint64_t>(size_t(pl.n_chunks) * 2 * PBQ_SK_MAXSPECIAL);
-  a.nsp = cv.take<int>(pl.n_chunks);
+  a.vals = cv.take<double>(size_t(pl.n_chunks - pl.vchunk0) * PBQ_SK_CHUNK);
+  a.sp = cv.take<uint64_t>(size_t(pl.n_chunks - pl.vchunk0) * 2 * PBQ_SK_MAXSPECIAL);
+  a.nsp = cv.take<int>(pl.n_chunks - pl.vchunk0);
   int* own_err = cv.take<int>(1);
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "gaussian: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   a.error = error_flag ? error_flag : own_err;

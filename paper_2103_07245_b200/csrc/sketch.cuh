@@ -227,6 +227,8 @@ struct SketchArgs {
   uint64_t k0, k1;
   const uint64_t* seed_dev;  // when set, the key {k0, k1} is read from device memory (CUDA-graph replays)
   long n_chunks;
+  long vchunk0;  // chunks below it end before stream position `first` (normal index ≤ position),
+                 // so they hold no requested normal: K1 walks them for the chain only
   long first;  // global index of the first normal to emit (row_offset·cols)
   long count;  // normals to emit (rows·cols)
   long cols;
@@ -237,9 +239,9 @@ struct SketchArgs {
   long* base;   // n_chunks: global normal index of the chunk's first start
   int* entry;   // n_chunks: entry offset of the chunk
   int* error;   // set on internal overflow
-  double* vals;     // n_chunks × 1024: value of a normal starting at each position
-  uint64_t* sp;     // n_chunks × 2·MAXSPECIAL: special positions, then where their normals end
-  int* nsp;         // n_chunks: number of specials
+  double* vals;     // (n_chunks − vchunk0) × 1024: value of a normal starting at each position
+  uint64_t* sp;     // (n_chunks − vchunk0) × 2·MAXSPECIAL: special positions, then where their normals end
+  int* nsp;         // n_chunks − vchunk0: number of specials
 };
 
 struct SkWarpSmem {
@@ -351,24 +353,32 @@ __global__ void __launch_bounds__(PBQ_SK_THREADS, 5) sketch_k1(SketchArgs a) {
   const int nsp = min(total, PBQ_SK_MAXSPECIAL);
   if (total > PBQ_SK_MAXSPECIAL && lane == 0) atomicExch(a.error, 1);
   __syncwarp();
-  // resolve the specials (full sampler); their values go to their positions
-  uint64_t* gsp = a.sp + size_t(chunk) * 2 * PBQ_SK_MAXSPECIAL;
+  // resolve the specials (full sampler); their values go to their positions.
+  // A prefix chunk (below vchunk0, e.g. the rows before this rank's row block)
+  // only needs where its specials end, for the chain walk: no values, no saves.
+  const bool keep = chunk >= a.vchunk0;
+  const long vc = chunk - a.vchunk0;
+  uint64_t* gsp = a.sp + size_t(keep ? vc : 0) * 2 * PBQ_SK_MAXSPECIAL;
   for (int i = lane; i < nsp; i += 32) {
     double v;
     const uint64_t sp = w.sp_pos[i];
     const uint64_t nx = zig_resolve(zt, sp, a.k0, a.k1, &v);
     w.sp_next[i] = nx;
-    const int rel = int(sp - cstart);
-    st[(rel >> 5) * 33 + (rel & 31)] = v;
-    gsp[i] = sp;
-    gsp[PBQ_SK_MAXSPECIAL + i] = nx;
+    if (keep) {
+      const int rel = int(sp - cstart);
+      st[(rel >> 5) * 33 + (rel & 31)] = v;
+      gsp[i] = sp;
+      gsp[PBQ_SK_MAXSPECIAL + i] = nx;
+    }
   }
-  if (lane == 0) a.nsp[chunk] = nsp;
+  if (keep && lane == 0) a.nsp[vc] = nsp;
   __syncwarp();
   // coalesced position-indexed write-out
-  double* gv = a.vals + size_t(chunk) * PBQ_SK_CHUNK;
+  if (keep) {
+    double* gv = a.vals + size_t(vc) * PBQ_SK_CHUNK;
 #pragma unroll 8
-  for (int e = lane; e < PBQ_SK_CHUNK; e += 32) __stcg(gv + e, st[(e >> 5) * 33 + (e & 31)]);
+    for (int e = lane; e < PBQ_SK_CHUNK; e += 32) __stcg(gv + e, st[(e >> 5) * 33 + (e & 31)]);
+  }
   int cnt;
   uint64_t ex;
   sk_walk(cstart + lane, cend, w, nsp, cnt, ex);  // entry offset = lane
@@ -463,15 +473,16 @@ __global__ void __launch_bounds__(PBQ_SK_THREADS, 5) sketch_k3(SketchArgs a) {
   const int entry = a.entry[chunk];
   const int cnt_here = a.counts[chunk * PBQ_SK_E + entry];
   if (base >= a.first + a.count || base + cnt_here <= a.first) return;  // nothing requested here
+  const long vc = chunk - a.vchunk0;  // ≥ 0 here: a prefix chunk never holds a requested normal
   SkWarpSmem& w = sw[warp];
   double* bw = buf[warp];
   const uint64_t cstart = uint64_t(chunk) * PBQ_SK_CHUNK, cend = cstart + PBQ_SK_CHUNK;
   // position-indexed values → padded shared memory (coalesced read)
-  const double* gv = a.vals + size_t(chunk) * PBQ_SK_CHUNK;
+  const double* gv = a.vals + size_t(vc) * PBQ_SK_CHUNK;
 #pragma unroll 8
   for (int e = lane; e < PBQ_SK_CHUNK; e += 32) bw[(e >> 5) * 33 + (e & 31)] = __ldcs(gv + e);
-  const int nsp = a.nsp[chunk];
-  const uint64_t* gsp = a.sp + size_t(chunk) * 2 * PBQ_SK_MAXSPECIAL;
+  const int nsp = a.nsp[vc];
+  const uint64_t* gsp = a.sp + size_t(vc) * 2 * PBQ_SK_MAXSPECIAL;
   for (int i = lane; i < nsp; i += 32) {
     w.sp_pos[i] = gsp[i];
     w.sp_next[i] = gsp[PBQ_SK_MAXSPECIAL + i];

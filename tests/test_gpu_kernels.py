@@ -292,6 +292,11 @@ def test_gaussian_row_offset(cuda):
     assert np.array_equal(part, full[1500:2500])
     ref = c_gaussian(1000, 64, 9, row_offset=1500)
     assert np.array_equal(part, ref)
+    # a block deep in the stream: the prefix chunks are walked for the chain
+    # only (no value write-out), the block itself is bitwise numpy's
+    deep = gaussian_matrix(300, 37, 2**70 + 3, row_offset=40000)
+    assert np.array_equal(deep, oracle_gaussian(40300, 37, 2**70 + 3)[40000:])
+    assert np.array_equal(gaussian_matrix(1, 5, 4, row_offset=7), oracle_gaussian(8, 5, 4)[7:])
 
 
 @pytest.mark.parametrize("n1,n2,d,rank", [(300, 200, 25, None), (301, 257, 33, 7), (1000, 40, 40, 40),

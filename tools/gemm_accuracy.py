@@ -41,5 +41,31 @@ def main():
             print(f"   {name:10s} max {mx / 2**-53:9.2f} u   median {md / 2**-53:8.3f} u")
 
 
+def big(shapes=((65536, 16384, 512), (20000, 10000, 256))):
+    """Full-size AᵀX (many output tiles: each tile's K range is accumulated by
+    one or two CTAs) — error measured on a 1024×16 corner of C against the
+    extended-precision sum."""
+    dev = torch.device("cuda", 0)
+    ctx = D.context(dev)
+    rng = np.random.default_rng(1)
+    for K, M, N in shapes:
+        a = rng.standard_normal((K, M))
+        x = rng.standard_normal((K, N))
+        sub_m, sub_n = 1024, 16
+        ex = a[:, :sub_m].astype(np.longdouble).T @ x[:, :sub_n].astype(np.longdouble)
+        scale = (np.abs(a[:, :sub_m]).T @ np.abs(x[:, :sub_n])).astype(np.longdouble)
+        c_blas = (a[:, :sub_m].T @ x)[:, :sub_n]
+        A, X = D.as_kernel_operand(torch.from_numpy(a).to(dev)), D.as_kernel_operand(torch.from_numpy(x).to(dev))
+        c_pbq = D.gemm(ctx, A, X, trans_a=True)[:sub_m, :sub_n].cpu().numpy()
+        print(f"K={K} M={M} N={N} (full-size C, {sub_m}x{sub_n} corner checked):")
+        for name, c in (("openblas", c_blas), ("libpbq TN", c_pbq)):
+            e = np.abs(c.astype(np.longdouble) - ex) / scale
+            print(f"   {name:10s} max {float(e.max()) / 2**-53:9.2f} u   median {float(np.median(e)) / 2**-53:8.3f} u",
+                  flush=True)
+        del A, X
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
     main()
+    big()

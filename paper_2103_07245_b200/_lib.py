@@ -60,6 +60,9 @@ EXPORTED = (
     "pbq_gather_columns",
     "pbq_cholqr2_dist",
     "pbq_cholqr2_dist_workspace_bytes",
+    "pbq_set_p2p_timeout_ms",
+    "pbq_jacobi_svd",
+    "pbq_jacobi_svd_workspace_bytes",
 )
 
 c_i64 = ctypes.c_int64

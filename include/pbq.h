@@ -185,16 +185,22 @@ int pbq_gather_columns(pbq_ctx* ctx, int64_t rows, int64_t cols, const double* s
  * one-sided Jacobi on the n rows (length L ≥ n) of the row-major X:
  *   G·X = diag(s)·Y  ⇒  X = Gᵀ·diag(s)·Y,
  * s (n doubles) sorted descending, Y (n×L, ldy; may be NULL) with orthonormal
- * rows (rows with s = 0 are completed to an orthonormal set), and — when
- * `accumulate` — G (n×n, ldg) orthogonal, its rows the left singular vectors.
- * X is not modified.  status (device, 2 ints): sweeps used, 1 if not
- * converged within 30 sweeps.  n ≤ 256 rows of ≤ 768 doubles (incl. the G
- * row when accumulating) run in one thread-block cluster with the vectors in
+ * rows (rows with s = 0 are completed to an orthonormal set), and — with
+ * PBQ_JACOBI_ACCUMULATE in `flags` — G (n×n, ldg) orthogonal, its rows the
+ * left singular vectors.  PBQ_JACOBI_PRECONDITION first reduces X to the
+ * n×n R̃ of Xᵀ = Q_h·R, Rᵀ = W·R̃ (two pbq_householder_qr chains, as LAPACK
+ * dgejsv) and runs Jacobi on R̃ (far fewer sweeps on graded inputs); Y and G
+ * then need even leading dimensions and 16-byte alignment.  X is not
+ * modified.  status (device, 2 ints): sweeps used, 1 if not converged within
+ * 60 sweeps.  n ≤ 256 rows of ≤ 768 doubles (incl. the G row when
+ * accumulating) run in one thread-block cluster with the vectors in
  * registers; larger problems keep the vectors in L2. */
-int pbq_jacobi_svd(pbq_ctx* ctx, int64_t n, int64_t L, const double* X, int64_t ldx, int32_t accumulate, double* s,
+#define PBQ_JACOBI_ACCUMULATE 1
+#define PBQ_JACOBI_PRECONDITION 2
+int pbq_jacobi_svd(pbq_ctx* ctx, int64_t n, int64_t L, const double* X, int64_t ldx, int32_t flags, double* s,
                    double* Y, int64_t ldy, double* G, int64_t ldg, int32_t* status, void* workspace,
                    size_t workspace_bytes, void* stream);
-int pbq_jacobi_svd_workspace_bytes(pbq_ctx* ctx, int64_t n, int64_t L, int32_t accumulate, size_t* bytes);
+int pbq_jacobi_svd_workspace_bytes(pbq_ctx* ctx, int64_t n, int64_t L, int32_t flags, size_t* bytes);
 
 /* Distributed Cholesky-QR2 of a row-sharded tall matrix (the
  * QR of A·P̄ across ranks, replacing the TSQR tree when the input is

@@ -402,6 +402,7 @@ def oracle_cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=Tru
     vbar, fl = oracle_orth(f2)
     flags.append(fl)
     truncated = False
+    pinv_kappa = 1.0  # κ₂ of the pseudoinverted gram over its kept singular values (1: no pinv)
     if pass_efficient:
         core = f2.T @ vbar
         if gram is not None:
@@ -413,6 +414,7 @@ def oracle_cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=Tru
                 inv = np.zeros_like(s)
                 inv[keep] = 1.0 / s[keep]
                 core, truncated = (u * inv) @ (vh @ core), bool(not keep.all())
+                pinv_kappa = float(s[0] / s[keep][-1])
     else:
         core = ubar.T @ (a @ vbar)
         passes += 1
@@ -422,4 +424,5 @@ def oracle_cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=Tru
     rd1 = np.abs(np.diag(oracle_qr(ubar_in)[1]))
     rd2 = np.abs(np.diag(oracle_qr(f2)[1]))
     return {"u": ubar @ qc, "t": t, "v": vbar[:, perm], "perm": perm, "omega": omega, "passes": passes,
-            "pinv_truncated": truncated, "rank_flags": flags, "core": core, "rdiag_ubar": rd1, "rdiag_vbar": rd2}
+            "pinv_truncated": truncated, "rank_flags": flags, "core": core, "rdiag_ubar": rd1, "rdiag_vbar": rd2,
+            "pinv_kappa": pinv_kappa}

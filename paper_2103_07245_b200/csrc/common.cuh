@@ -122,6 +122,56 @@ __device__ __forceinline__ double fast_rsqrt(double d) {
   return fma(y, e, y);
 }
 
+// Tensor memory (TMEM) as a second-level FP64 accumulator.  tcgen05 has no
+// f64 MMA kind, so the DMMA GEMMs leave the SM's 256 KB of TMEM unused; they
+// park a running sum there (blocked summation, see gemm_tma_f64.cuh).  Each
+// thread moves its own 32-bit words: lane ℓ of warp w owns TMEM lane
+// 32·(w mod 4) + ℓ (the 32x32b shape), 16 consecutive columns per access.
+__device__ __forceinline__ void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {  // one full warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(smem_dst)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {  // the allocating warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before_sync() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after_sync() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+// 8 doubles (16 words) per thread: v[i] ↔ columns 2i, 2i+1 (lo, hi words)
+__device__ __forceinline__ void tmem_st8d(uint32_t taddr, const double (&v)[8]) {
+  uint32_t w[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    w[2 * i] = __double2loint(v[i]);
+    w[2 * i + 1] = __double2hiint(v[i]);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};\n" ::"r"(taddr),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]),
+      "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld8d(uint32_t taddr, double (&v)[8]) {
+  uint32_t w[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"  // in the same statement: no use of w can be hoisted above it
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]), "=r"(w[8]),
+        "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __hiloint2double(int(w[2 * i + 1]), int(w[2 * i]));
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
 // True when the IEEE-754 binary64 exponent field is all ones (Inf or NaN).
 __device__ __forceinline__ bool nonfinite_bits(double x) {
   return ((__double_as_longlong(x) >> 52) & 0x7ff) == 0x7ff;

@@ -100,7 +100,35 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
     }
     mbar_fence_init();
   }
+  // Blocked summation through tensor memory (plain GEMMs): every FOLD_KB
+  // k-blocks a warp adds its register accumulator into a running sum parked
+  // in TMEM and restarts it at zero, so no DMMA chain is longer than
+  // FOLD_KB·BK/4 = 256 steps.  The four warps of a scheduler fold at
+  // staggered k-blocks, so three of them keep the DMMA pipe busy while one
+  // folds.  A pass over A (K = n1 up to 2·10⁵) would
+  // otherwise sum each output in one chain of K/4 DMMAs; tools/gemm_accuracy.py
+  // measured 3.6 u max error against an extended-precision sum at K = 65536
+  // (OpenBLAS, K-blocked, 0.22 u), enough to push config 5's d = 512 tail
+  // columns past the reference's own reordering noise (tools/noise_floor.py).
+  // TMEM is otherwise idle in an FP64 kernel (tcgen05 has no f64 MMA kind).
+  constexpr bool FOLD = !SPLIT && !RESID;
+  constexpr int FOLD_KB = 32;
+  constexpr int ACC_D = MT * NT * 2;  // accumulator doubles per thread
+  static_assert(ACC_D % 8 == 0, "accumulator folds move 8 doubles at a time");
+  constexpr uint32_t TM_NEED = uint32_t((NWARPS + 3) / 4) * ACC_D * 2;
+  constexpr uint32_t TM_COLS = TM_NEED <= 32 ? 32 : TM_NEED <= 64 ? 64 : TM_NEED <= 128 ? 128 : TM_NEED <= 256 ? 256 : 512;
+  static_assert(TM_NEED <= 512, "TMEM holds 512 columns");
+  __shared__ uint32_t s_tmem;
+  if constexpr (FOLD) {
+    if (warp == 0) tmem_alloc(&s_tmem, TM_COLS);
+    tmem_fence_before_sync();
+  }
   __syncthreads();
+  uint32_t tm_mine = 0;  // this warp's columns in its lane quarter
+  if constexpr (FOLD) {
+    tmem_fence_after_sync();
+    tm_mine = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(warp >> 2) * uint32_t(ACC_D * 2);
+  }
 
   struct Seg {
     int tile, tm, tn, kb, ke, tile_k;
@@ -294,6 +322,32 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
     for (int i = 0; i < MT; ++i)
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    bool folded = false;
+    // acc → TMEM (first fold: store; later: add), then restart at zero
+    auto fold = [&]() {
+#pragma unroll
+      for (int c = 0; c < ACC_D / 8; ++c) {
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int x = 8 * c + i;
+          v[i] = acc[x / (NT * 2)][(x / 2) % NT][x % 2];
+        }
+        if (folded) {
+          double o[8];
+          tmem_ld8d(tm_mine + uint32_t(16 * c), o);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = o[i] + v[i];
+        }
+        tmem_st8d(tm_mine + uint32_t(16 * c), v);
+      }
+      tmem_wait_st();
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      folded = true;
+    };
 
 #pragma unroll 1
     for (int kbk = seg.kb; kbk < seg.ke; ++kbk) {
@@ -342,6 +396,23 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
       ++cflat;
       produce();
+      if constexpr (FOLD) {
+        if ((kbk + 1 - seg.kb + (warp >> 2) * (FOLD_KB / 4)) % FOLD_KB == 0 && kbk + 1 < seg.ke) fold();
+      }
+    }
+    if constexpr (FOLD) {
+      if (folded) {  // final = running sum + the last chain
+#pragma unroll
+        for (int c = 0; c < ACC_D / 8; ++c) {
+          double o[8];
+          tmem_ld8d(tm_mine + uint32_t(16 * c), o);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int x = 8 * c + i;
+            acc[x / (NT * 2)][(x / 2) % NT][x % 2] = o[i] + acc[x / (NT * 2)][(x / 2) % NT][x % 2];
+          }
+        }
+      }
     }
 
     // output coordinates of this thread's accumulators
@@ -512,6 +583,12 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
         atomicMax(p.red_emax, bits);
       }
     }
+  }
+  if constexpr (FOLD) {  // every warp's TMEM traffic has completed (loads waited, stores waited)
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    if (warp == 0) tmem_dealloc(s_tmem, TM_COLS);
   }
   if (RESID) {
     __shared__ double s_red[2][THREADS / 32];

@@ -2,6 +2,7 @@
 // carving and the single-device PbP-QLP pipeline (algorithms.py:209-260).
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -156,6 +157,16 @@ struct ProfSuppress {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Bump allocator over a caller workspace.
+// NVTX range over one stage of the pipeline (SURVEY §5 profiling): host
+// enqueue ranges that nsys/ncu correlate with the kernels launched inside.
+// Header-only NVTX3: a no-op unless a tool injects itself.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct Carve {
   char* base;
   size_t cap, off = 0;
@@ -1119,13 +1130,13 @@ bool jac_cluster_ok(pbq_ctx* ctx, JacFn fn, int C, size_t smem, int threads) {
   return ok;
 }
 
-size_t jacobi_ws_bytes(long n, long L, int accumulate) {
+size_t jacobi_core_ws_bytes(long n, long L, int accumulate) {
   const long np = n + (n & 1), V = L + (accumulate ? n : 0), ldz = V + (V & 1);
   return align_up(size_t(np) * ldz * 8, 256) + align_up(size_t(n) * 8, 256) + align_up(size_t(L) * 8, 256) + 512;
 }
 
-int jacobi_launch(pbq_ctx* ctx, long n, long L, const double* X, long ldx, int accumulate, double* s, double* Y,
-                  long ldy, double* G, long ldg, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
+int jacobi_core_launch(pbq_ctx* ctx, long n, long L, const double* X, long ldx, int accumulate, double* s, double* Y,
+                       long ldy, double* G, long ldg, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n < 1 || L < 1) return fail(ctx, PBQ_ERR_DIM, "jacobi_svd: bad shape %ld x %ld", n, L);
   if (n > L) return fail(ctx, PBQ_ERR_DIM, "jacobi_svd: needs n <= L (got %ld x %ld)", n, L);
   if (!X || !s || !status || ldx < L || (Y && ldy < L) || (accumulate && (!G || ldg < n)))
@@ -1147,11 +1158,13 @@ int jacobi_launch(pbq_ctx* ctx, long n, long L, const double* X, long ldx, int a
   a.Z = cv.take<double>(size_t(a.np) * a.ldz);
   double* sig = cv.take<double>(n);
   double* work = cv.take<double>(L);
-  int* nzero = cv.take<int>(1);
+  int* ctl = cv.take<int>(64);  // [0] nzero, [16] grid barrier, [32..48) sweep statistics (grid kernel)
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "jacobi_svd: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  int* nzero = ctl;
+  ctl += 16;
   const int P = a.np / 2;
   ProfScope ps(ctx->prof, st, 1);
-  PBQ_CUDA(ctx, cudaMemsetAsync(nzero, 0, sizeof(int), st));
+  PBQ_CUDA(ctx, cudaMemsetAsync(nzero, 0, 64 * sizeof(int), st));
   bool done = false;
   if (P <= JAC_MAX_PAIRS_REG && a.V <= 32 * JAC_MAX_VPL && !getenv("PBQ_JACOBI_L2")) {
     const int vpl = jac_vpl(a.V);
@@ -1181,23 +1194,19 @@ int jacobi_launch(pbq_ctx* ctx, long n, long L, const double* X, long ldx, int a
     jacobi_init_kernel<<<unsigned(blocks), 256, 0, st>>>(a);
     PBQ_CUDA(ctx, cudaGetLastError());
     ctx->launches += 1;
-    int C = int(std::min<long>(16, ceil_div(P, JAC_L2_WARPS)));
-    const JacFn fn = jacobi_l2_kernel<16>;
-    while (C > 1 && !jac_cluster_ok(ctx, fn, C, 0, JAC_L2_WARPS * 32)) C /= 2;
-    if (C > 1) cudaFuncSetAttribute(reinterpret_cast<void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    cfg.gridDim = dim3(C);
-    cfg.blockDim = dim3(JAC_L2_WARPS * 32);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = C;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    PBQ_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, a));
+    const int vpl = a.V <= 256 ? 8 : a.V <= 512 ? 16 : a.V <= 768 ? 24 : 40;  // V > 1280: streamed path
+    void* fn = vpl == 8    ? reinterpret_cast<void*>(&jacobi_grid_kernel<8>)
+               : vpl == 16 ? reinterpret_cast<void*>(&jacobi_grid_kernel<16>)
+               : vpl == 24 ? reinterpret_cast<void*>(&jacobi_grid_kernel<24>)
+                           : reinterpret_cast<void*>(&jacobi_grid_kernel<40>);
+    int per_sm = 0;
+    PBQ_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, JAC_GRID_WARPS * 32, 0));
+    if (per_sm < 1) return fail(ctx, PBQ_ERR_UNSUPPORTED, "jacobi_svd: grid kernel cannot be resident");
+    const int grid = int(std::max<long>(1, std::min<long>(ceil_div(P, JAC_GRID_WARPS), long(ctx->sms))));
+    unsigned int* bar = reinterpret_cast<unsigned int*>(ctl);
+    unsigned long long* stat = reinterpret_cast<unsigned long long*>(ctl + 16);
+    void* args[] = {&a, &bar, &stat};
+    PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(JAC_GRID_WARPS * 32), args, 0, st));
     ctx->launches += 1;
   }
   const unsigned wb = unsigned(ceil_div(n, 8));  // 8 warps per 256-thread block, one per vector
@@ -1206,6 +1215,89 @@ int jacobi_launch(pbq_ctx* ctx, long n, long L, const double* X, long ldx, int a
   if (Y) jacobi_complete_kernel<<<1, 256, 0, st>>>(int(n), int(L), Y, ldy, nzero, work);
   PBQ_CUDA(ctx, cudaGetLastError());
   ctx->launches += Y ? 3 : 2;
+  return PBQ_OK;
+}
+
+// Preconditioned Jacobi (PBQ_JACOBI_PRECONDITION; Drmač & Veselić 2008, as
+// LAPACK dgejsv): Xᵀ = Q_h·R (tall QR), Rᵀ = W·R̃ (the QLP step), then the
+// one-sided Jacobi core on the rows of the n×n R̃, whose rows are graded like
+// the singular values and far closer to orthogonal than X's — 8–12 sweeps
+// instead of 25–45 on graded inputs (tools/svd_probe.py).  With
+// G₃·R̃ = diag(s)·Y₃:  X = Rᵀ·Q_hᵀ = W·R̃·Q_hᵀ  ⇒  G = G₃·Wᵀ, Y = Y₃·Q_hᵀ.
+struct JacPre {
+  long ldn, ldL;
+  size_t qr, gemm, core;
+};
+int jacobi_pre_plan(pbq_ctx* ctx, long n, long L, int accumulate, JacPre& p) {
+  p.ldn = thin_ld(n);
+  p.ldL = thin_ld(L);
+  size_t a = 0, b = 0;
+  PBQ_TRY(pbq_qr_workspace_bytes(ctx, L, n, &a));
+  PBQ_TRY(pbq_qr_workspace_bytes(ctx, n, n, &b));
+  p.qr = std::max(a, b);
+  PBQ_TRY(pbq_gemm_workspace_bytes(ctx, n, L, n, &a));
+  PBQ_TRY(pbq_gemm_workspace_bytes(ctx, n, n, n, &b));
+  p.gemm = std::max(a, b);
+  p.core = jacobi_core_ws_bytes(n, n, accumulate);
+  return PBQ_OK;
+}
+size_t jacobi_pre_ws_bytes(const JacPre& p, long n, long L) {
+  const size_t sq = align_up(size_t(n) * p.ldn * 8, 256);
+  return align_up(size_t(L) * p.ldn * 8, 256) + 6 * sq + align_up(size_t(n) * p.ldL * 8, 256) + align_up(p.qr, 256) +
+         align_up(p.gemm, 256) + align_up(p.core, 256) + 512;
+}
+
+int jacobi_ws_bytes(pbq_ctx* ctx, long n, long L, int flags, size_t* bytes) {
+  const int acc = flags & PBQ_JACOBI_ACCUMULATE;
+  if ((flags & PBQ_JACOBI_PRECONDITION) && n >= 2) {
+    JacPre p;
+    PBQ_TRY(jacobi_pre_plan(ctx, n, L, acc, p));
+    *bytes = jacobi_pre_ws_bytes(p, n, L);
+  } else {
+    *bytes = jacobi_core_ws_bytes(n, L, acc);
+  }
+  return PBQ_OK;
+}
+
+int jacobi_launch(pbq_ctx* ctx, long n, long L, const double* X, long ldx, int flags, double* s, double* Y, long ldy,
+                  double* G, long ldg, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int acc = flags & PBQ_JACOBI_ACCUMULATE;
+  if (!(flags & PBQ_JACOBI_PRECONDITION) || n < 2)
+    return jacobi_core_launch(ctx, n, L, X, ldx, acc, s, Y, ldy, G, ldg, status, ws, ws_bytes, st);
+  if (n > L) return fail(ctx, PBQ_ERR_DIM, "jacobi_svd: needs n <= L (got %ld x %ld)", n, L);
+  if (!X || !s || !status || ldx < L || (Y && ldy < L) || (acc && (!G || ldg < n)))
+    return fail(ctx, PBQ_ERR_PARAM, "jacobi_svd: bad pointer or leading dimension");
+  if ((Y && ((ldy & 1) || !aligned16(Y))) || (acc && ((ldg & 1) || !aligned16(G))))
+    return fail(ctx, PBQ_ERR_PARAM, "jacobi_svd: preconditioned outputs need even leading dimensions, 16-byte aligned");
+  JacPre p;
+  PBQ_TRY(jacobi_pre_plan(ctx, n, L, acc, p));
+  Carve cv(ws, ws_bytes);
+  double* H = cv.take<double>(size_t(L) * p.ldn);   // Xᵀ, then Q_h
+  double* R1 = cv.take<double>(size_t(n) * p.ldn);  // R of Xᵀ
+  double* T = cv.take<double>(size_t(n) * p.ldn);   // Rᵀ, then W
+  double* Rt = cv.take<double>(size_t(n) * p.ldn);  // R̃
+  double* Y3 = cv.take<double>(size_t(n) * p.ldn);
+  double* G3 = cv.take<double>(size_t(n) * p.ldn);
+  double* Wt = cv.take<double>(size_t(n) * p.ldn);
+  double* Qt = cv.take<double>(size_t(n) * p.ldL);  // Q_hᵀ
+  char* qws = cv.take<char>(p.qr);
+  char* gws = cv.take<char>(p.gemm);
+  char* cws = cv.take<char>(p.core);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "jacobi_svd: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  PBQ_TRY(transpose_launch(ctx, n, X, ldx, H, p.ldn, 0, st, L));
+  PBQ_TRY(qr_launch(ctx, L, n, H, p.ldn, R1, p.ldn, 1, nullptr, qws, p.qr, st));
+  PBQ_TRY(transpose_launch(ctx, n, R1, p.ldn, T, p.ldn, 0, st));
+  PBQ_TRY(qr_launch(ctx, n, n, T, p.ldn, Rt, p.ldn, 1, nullptr, qws, p.qr, st));
+  PBQ_TRY(jacobi_core_launch(ctx, n, n, Rt, p.ldn, acc, s, Y ? Y3 : nullptr, p.ldn, acc ? G3 : nullptr, p.ldn, status,
+                             cws, p.core, st));
+  if (Y) {
+    PBQ_TRY(transpose_launch(ctx, L, H, p.ldn, Qt, p.ldL, 0, st, n));
+    PBQ_TRY(gemm_launch<false>(ctx, n, L, n, 1.0, Y3, p.ldn, Qt, p.ldL, 0.0, Y, ldy, nullptr, gws, p.gemm, st));
+  }
+  if (acc) {
+    PBQ_TRY(transpose_launch(ctx, n, T, p.ldn, Wt, p.ldn, 0, st));
+    PBQ_TRY(gemm_launch<false>(ctx, n, n, n, 1.0, G3, p.ldn, Wt, p.ldn, 0.0, G, ldg, nullptr, gws, p.gemm, st));
+  }
   return PBQ_OK;
 }
 
@@ -1482,17 +1574,16 @@ int pbq_set_p2p_timeout_ms(pbq_ctx* ctx, int64_t ms) {
   return PBQ_OK;
 }
 
-int pbq_jacobi_svd_workspace_bytes(pbq_ctx* ctx, int64_t n, int64_t L, int32_t accumulate, size_t* bytes) {
-  if (!ctx || !bytes || n < 1 || L < 1) return PBQ_ERR_PARAM;
-  *bytes = jacobi_ws_bytes(n, L, accumulate);
-  return PBQ_OK;
+int pbq_jacobi_svd_workspace_bytes(pbq_ctx* ctx, int64_t n, int64_t L, int32_t flags, size_t* bytes) {
+  if (!ctx || !bytes || n < 1 || L < 1 || n > L) return PBQ_ERR_PARAM;
+  return jacobi_ws_bytes(ctx, n, L, flags, bytes);
 }
 
-int pbq_jacobi_svd(pbq_ctx* ctx, int64_t n, int64_t L, const double* X, int64_t ldx, int32_t accumulate, double* s,
+int pbq_jacobi_svd(pbq_ctx* ctx, int64_t n, int64_t L, const double* X, int64_t ldx, int32_t flags, double* s,
                    double* Y, int64_t ldy, double* G, int64_t ldg, int32_t* status, void* workspace,
                    size_t workspace_bytes, void* stream) {
   if (!ctx) return PBQ_ERR_PARAM;
-  return jacobi_launch(ctx, n, L, X, ldx, accumulate, s, Y, ldy, G, ldg, status, workspace, workspace_bytes,
+  return jacobi_launch(ctx, n, L, X, ldx, flags, s, Y, ldy, G, ldg, status, workspace, workspace_bytes,
                        static_cast<cudaStream_t>(stream));
 }
 
@@ -1729,12 +1820,14 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
                                     d * sizeof(double), n2, cudaMemcpyDeviceToDevice, st));
   } else {
     if (!phi) {
+      NvtxRange nv("pbq sketch: Phi = gaussian_matrix(n1, d, seed)");
       PBQ_TRY(sketch_launch(ctx, n1, d, 0, pr->seed_lo, pr->seed_hi, o->phi, o->ldphi, sk_err, sc, scratch, st,
                             pr->seed_dev));
       phi = o->phi;
       ldphi = o->ldphi;
     }
     // pass 1: C = Aᵀ Φ  (+ fused isfinite scan of A)
+    NvtxRange nv("pbq pass: C = A^T Phi");
     PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, phi, ldphi, 0.0, cbuf, ld,
                               check ? o->nonfinite : nullptr, sc, scratch, st));
   }
@@ -1742,8 +1835,12 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   double* dbuf = o->q;  // n1×d scratch for A·P̄, finally D itself
   const long ldq = o->ldq;
   if (pr->reorthonormalize) {
-    PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
+    {
+      NvtxRange nv("pbq orth(C)");
+      PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
+    }
     for (long it = 0; it < q; ++it) {
+      NvtxRange nv("pbq power iteration");
       PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cbuf, ld, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
       PBQ_TRY(qr_launch(ctx, n1, d, dbuf, ldq, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
       PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, dbuf, ldq, 0.0, cbuf, ld, nullptr, sc, scratch, st));
@@ -1751,17 +1848,27 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
     }
   } else {
     for (long it = 0; it < q; ++it) {
+      NvtxRange nv("pbq power iteration (no reorth)");
       PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cbuf, ld, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
       PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, dbuf, ldq, 0.0, cbuf, ld, nullptr, sc, scratch, st));
     }
     PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
   }
   // D = A·P̄ ; (Q, R) = qr(D)
-  PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cbuf, ld, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
-  PBQ_TRY(qr_launch(ctx, n1, d, dbuf, ldq, o->r, o->ldr, 1, nullptr, sc, scratch, st));
+  {
+    NvtxRange nv("pbq pass: D = A Pbar");
+    PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cbuf, ld, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
+  }
+  {
+    NvtxRange nv("pbq qr(D)");
+    PBQ_TRY(qr_launch(ctx, n1, d, dbuf, ldq, o->r, o->ldr, 1, nullptr, sc, scratch, st));
+  }
   // (W, R̃) = qr(Rᵀ); L = tril(R̃ᵀ); P = P̄·W
-  PBQ_TRY(second_stage_launch(ctx, d, o->r, o->ldr, wbuf, ld, o->l, o->ldl, sc, scratch, st));
-  PBQ_TRY(gemm_launch<false>(ctx, n2, d, d, 1.0, cbuf, ld, wbuf, ld, 0.0, o->p, o->ldp, nullptr, sc, scratch, st));
+  {
+    NvtxRange nv("pbq second stage: qr(R^T), L, P = Pbar W");
+    PBQ_TRY(second_stage_launch(ctx, d, o->r, o->ldr, wbuf, ld, o->l, o->ldl, sc, scratch, st));
+    PBQ_TRY(gemm_launch<false>(ctx, n2, d, d, 1.0, cbuf, ld, wbuf, ld, 0.0, o->p, o->ldp, nullptr, sc, scratch, st));
+  }
   if (!pr->phi && !pr->c_init) {
     // fold a sketch-generator overflow into bit 1 of the status word so the
     // host reads one int

@@ -34,11 +34,11 @@
 //    bottom vector to warp p−1 through shared-memory mailboxes (DSMEM stores
 //    across CTA boundaries), double-buffered by round parity and signalled
 //    point to point with mbarriers (no cluster-wide barrier per round).
-//  * jacobi_l2_kernel — any size: the vectors stay in a global (L2-resident)
+//  * jacobi_grid_kernel — any size: the vectors stay in a global (L2-resident)
 //    array and the schedule moves the computation instead: in round r the
-//    vector at position x ≥ 1 is vector 1 + ((x − 1 − r) mod (n_p − 1)).  One
-//    cluster of up to 16 CTAs, warps take pairs round-robin, a cluster
-//    barrier per round.
+//    vector at position x ≥ 1 is vector 1 + ((x − 1 − r) mod (n_p − 1)).  A
+//    cooperative grid over all SMs, one warp per pair, a grid barrier per
+//    round.
 // Then jacobi_norms_kernel / jacobi_output_kernel: σ_i = ‖row i‖ (fixed-order
 // sums), a stable descending sort by σ (rank by counting), Y rows = x/σ,
 // G rows permuted alike; jacobi_complete_kernel gives rows with σ = 0 an
@@ -57,7 +57,6 @@ namespace jcg = cooperative_groups;
 constexpr int JAC_WARPS = 8;            // warps per CTA of the register kernel
 constexpr int JAC_MAX_PAIRS_REG = 128;  // 16 CTAs × 8 warps
 constexpr int JAC_MAX_VPL = 24;         // doubles per lane per vector (V ≤ 768)
-constexpr int JAC_L2_WARPS = 16;
 
 struct JacArgs {
   int n, np, L, V;     // vectors, padded count (even), dot length, vector length
@@ -314,17 +313,26 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
 }
 
 // ---------------------------------------------------------------------------
-// L2-resident kernel (any n, V).  Launch: one cluster of C CTAs of
-// JAC_L2_WARPS warps; Z must already hold the initial vectors (jacobi_init_kernel).
+// L2-resident kernel (any n, V).  Launch: cooperative, up to one CTA of
+// JAC_GRID_WARPS warps per SM, warps take pairs round-robin (one pair each
+// when 8·SMs ≥ P), a grid barrier per round; Z must already hold the initial
+// vectors (jacobi_init_kernel).  Vectors of up to 32·VPL doubles are loaded
+// whole into registers (all loads in flight at once); longer ones are
+// streamed.  The sweep-end statistics are combined with integer atomics
+// (counts, and max of non-negative doubles as bit patterns — order
+// independent, so bitwise reproducible) in a slot per sweep parity:
+// stat[par·4 + {0: rotations, 1: max aapq, 2: max |sin|}], zeroed before the
+// launch; slot par^1 is cleared after every CTA has read it (one round
+// barrier later).
+constexpr int JAC_GRID_WARPS = 8;
+
 template <int VPL>
-__global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs p) {
-  __shared__ double red[JAC_L2_WARPS][3];
-  __shared__ double sums[2][16][3];
-  jcg::cluster_group cl = jcg::this_cluster();
+__global__ void __launch_bounds__(JAC_GRID_WARPS * 32, 1)
+    jacobi_grid_kernel(JacArgs p, unsigned int* bar, unsigned long long* stat) {
   const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-  const int C = int(cl.num_blocks()), me = int(cl.block_rank());
-  const int P = p.np / 2, TW = C * JAC_L2_WARPS, w0 = me * JAC_L2_WARPS + lw;
+  const int P = p.np / 2, TW = int(gridDim.x) * JAC_GRID_WARPS, w0 = int(blockIdx.x) * JAC_GRID_WARPS + lw;
   const int m1 = p.np - 1;
+  unsigned int gen = 0;
   int sweeps = 0, converged = 0;
   for (int sw = 0; sw < p.max_sweeps && !converged; ++sw) {
     int rot = 0;
@@ -336,8 +344,6 @@ __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs
         const int ib = 1 + ((xb - 1 - r) % m1 + m1) % m1;
         double* zt = p.Z + long(it) * p.ldz;
         double* zb = p.Z + long(ib) * p.ldz;
-        // vector length V may exceed 32·VPL: process in chunks of 32·VPL
-        // (the dot products must cover all of [0, L) before rotating)
         if (p.V <= 32 * VPL) {
           double x[VPL], y[VPL];
 #pragma unroll
@@ -364,6 +370,7 @@ __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs
         } else {
           // long vectors: dots over L from global, then the rotation streamed
           double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll 4
           for (int e = lane; e < p.L; e += 32) {
             const double xv = __ldcg(zt + e), yv = __ldcg(zb + e);
             a = fma(xv, xv, a);
@@ -384,6 +391,7 @@ __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs
                                                 : copysign(1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
             const double cs = 1.0 / sqrt(fma(t, t, 1.0)), sn = cs * t;
             mx_sin = fmax(mx_sin, fabs(sn));
+#pragma unroll 4
             for (int e = lane; e < p.V; e += 32) {
               const double xv = __ldcg(zt + e), yv = __ldcg(zb + e);
               __stcg(zt + e, fma(cs, xv, -sn * yv));
@@ -393,34 +401,20 @@ __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs
           }
         }
       }
-      jac_cluster_sync();
+      grid_barrier(bar, gen);
     }
+    // ---- sweep-end test (dgesvj): rotations, max relative off-diagonal, max |sin|
+    const int par = sw & 1;
     if (lane == 0) {
-      red[lw][0] = double(rot);
-      red[lw][1] = mx_aapq;
-      red[lw][2] = mx_sin;
+      if (rot) atomicAdd(stat + 4 * par, (unsigned long long)rot);
+      if (mx_aapq > 0.0) atomicMax(stat + 4 * par + 1, (unsigned long long)__double_as_longlong(mx_aapq));
+      if (mx_sin > 0.0) atomicMax(stat + 4 * par + 2, (unsigned long long)__double_as_longlong(mx_sin));
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      for (int i = 0; i < JAC_L2_WARPS; ++i) {
-        s0 += red[i][0];
-        s1 = fmax(s1, red[i][1]);
-        s2 = fmax(s2, red[i][2]);
-      }
-      double* dst = cl.map_shared_rank(&sums[0][0][0], 0) + ((sw & 1) * 16 + me) * 3;
-      dst[0] = s0;
-      dst[1] = s1;
-      dst[2] = s2;
-    }
-    jac_cluster_sync();
-    double total = 0.0, gmx = 0.0, gsin = 0.0;
-    const double* src = cl.map_shared_rank(&sums[0][0][0], 0);
-    for (int i = 0; i < C; ++i) {
-      total += src[((sw & 1) * 16 + i) * 3];
-      gmx = fmax(gmx, src[((sw & 1) * 16 + i) * 3 + 1]);
-      gsin = fmax(gsin, src[((sw & 1) * 16 + i) * 3 + 2]);
-    }
+    if (blockIdx.x == 0 && threadIdx.x < 3) stat[4 * (par ^ 1) + threadIdx.x] = 0ull;  // read a round ago
+    grid_barrier(bar, gen);
+    const double total = double(__ldcg(stat + 4 * par));
+    const double gmx = __longlong_as_double((long long)__ldcg(stat + 4 * par + 1));
+    const double gsin = __longlong_as_double((long long)__ldcg(stat + 4 * par + 2));
     sweeps = sw + 1;
     converged = jac_converged(int(total), gmx, gsin, p.n, p.tol);
   }
@@ -428,7 +422,6 @@ __global__ void __launch_bounds__(JAC_L2_WARPS * 32, 1) jacobi_l2_kernel(JacArgs
     p.status[0] = sweeps;
     p.status[1] = converged ? 0 : 1;
   }
-  jac_cluster_sync();
 }
 
 __global__ void jacobi_init_kernel(JacArgs p) {

@@ -13,6 +13,9 @@ import torch
 from . import _lib
 from . import exceptions as _exc
 
+JACOBI_ACCUMULATE = 1  # pbq.h PBQ_JACOBI_ACCUMULATE
+JACOBI_PRECONDITION = 2  # pbq.h PBQ_JACOBI_PRECONDITION
+
 _ctx_lock = threading.Lock()
 _contexts = {}
 
@@ -304,11 +307,14 @@ def second_stage(ctx, r, w=None, l=None):
     return w, l
 
 
-def jacobi_svd(ctx, x, accumulate=True, want_y=True, status=None):
+def jacobi_svd(ctx, x, accumulate=True, want_y=True, status=None, precondition=True):
     """One-sided Jacobi SVD of the rows of ``x`` (n×L, n ≤ L):
-    G·x = diag(s)·Y (pbq_jacobi_svd).  Returns (s, Y, G, status) as device
-    tensors — Y None unless ``want_y``, G None unless ``accumulate``;
-    status = [sweeps, not-converged flag] (int32, on the device)."""
+    G·x = diag(s)·Y (pbq_jacobi_svd).  ``precondition`` first reduces x to
+    the n×n R̃ of xᵀ = Q·R, Rᵀ = W·R̃ (LAPACK dgejsv's QR preconditioning;
+    leave it off when x already is such a factor).  Returns (s, Y, G, status)
+    as device tensors — Y None unless ``want_y``, G None unless
+    ``accumulate``; status = [sweeps, not-converged flag] (int32, on the
+    device)."""
     x = as_kernel_operand(x)
     n, L = x.shape
     dev = x.device
@@ -317,12 +323,13 @@ def jacobi_svd(ctx, x, accumulate=True, want_y=True, status=None):
     g = empty_matrix(n, n, dev) if accumulate else None
     if status is None:
         status = torch.zeros(2, dtype=torch.int32, device=dev)
+    flags = (JACOBI_ACCUMULATE if accumulate else 0) | (JACOBI_PRECONDITION if precondition else 0)
     nbytes = ctypes.c_size_t()
     with ctx.lock:
-        ctx.check(ctx.lib.pbq_jacobi_svd_workspace_bytes(ctx.handle, n, L, 1 if accumulate else 0,
-                                                         ctypes.byref(nbytes)), "jacobi_svd workspace")
+        ctx.check(ctx.lib.pbq_jacobi_svd_workspace_bytes(ctx.handle, n, L, flags, ctypes.byref(nbytes)),
+                  "jacobi_svd workspace")
         ws = workspace(nbytes.value, dev)
-        st = ctx.lib.pbq_jacobi_svd(ctx.handle, n, L, ptr(x), ld_of(x), 1 if accumulate else 0, ptr(s), ptr(y),
+        st = ctx.lib.pbq_jacobi_svd(ctx.handle, n, L, ptr(x), ld_of(x), flags, ptr(s), ptr(y),
                                     ld_of(y) if y is not None else 0, ptr(g), ld_of(g) if g is not None else 0,
                                     ptr(status), ptr(ws), nbytes.value, stream_ptr(dev))
         ctx.check(st, "jacobi_svd")

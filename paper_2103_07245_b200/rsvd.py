@@ -126,7 +126,7 @@ def r_svd(a, d, q=0, seed=0, reorthonormalize=True, *, device=None):
     # G·R̃ = diag(s)·Y ⇒ R_hᵀ = W·R̃ = (W·Gᵀ)·diag(s)·Y, so U_c = W·Gᵀ and
     # W_c = Yᵀ (pbq_jacobi_svd, svd_f64.cuh)
     w, l = _dev.second_stage(ctx, rh)  # l = tril(R̃ᵀ)
-    s, y, g, jst = _dev.jacobi_svd(ctx, _dev.transpose(ctx, l), accumulate=True, want_y=True)
+    s, y, g, jst = _dev.jacobi_svd(ctx, _dev.transpose(ctx, l), accumulate=True, want_y=True, precondition=False)
     uc = _dev.gemm(ctx, w, _dev.transpose(ctx, g), trans_a=False)
     u = _dev.gemm(ctx, ubar, uc, trans_a=False)
     v = _dev.gemm(ctx, h, _dev.transpose(ctx, y), trans_a=False)
@@ -137,7 +137,7 @@ def r_svd(a, d, q=0, seed=0, reorthonormalize=True, *, device=None):
     if fl[1]:
         raise _exc.DeviceError("sketch generator overflow (internal error)")
     if int(jst[1].item()):
-        raise _exc.ConvergenceError("r_svd: the Jacobi SVD core did not converge in 30 sweeps")
+        raise _exc.ConvergenceError("r_svd: the Jacobi SVD core did not converge in 60 sweeps")
     for flag in fl[2:]:
         warn_rank(flag, stacklevel=3)
     outs = [from_device(x, kind, home) for x in (u, s.contiguous(), v)]

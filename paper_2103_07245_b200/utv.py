@@ -172,7 +172,7 @@ def cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=True, *, d
     if fl[1]:
         raise _exc.DeviceError("sketch generator overflow (internal error)")
     if gram is not None and int(jst[1].item()):
-        raise _exc.ConvergenceError("cor_utv: the Jacobi SVD core of the pseudoinverse did not converge in 30 sweeps")
+        raise _exc.ConvergenceError("cor_utv: the Jacobi SVD core of the pseudoinverse did not converge in 60 sweeps")
     for flag in fl[2:site]:
         warn_rank(flag, stacklevel=3)
     outs = [from_device(x, kind, home) for x in (u, t, v)]

@@ -58,14 +58,18 @@ def _check_utv(a, f, ref_u, ref_t, ref_v, ref, strict=1e-10):
     """Determined block: per column max(strict, 64·u·κ_j) with κ_j from the
     core's T and from the orth inputs of V̄ (column perm_j) and Ū (worst
     column) — the non-reorthonormalized branch orthonormalizes A(AᵀA)^q Ω
-    once, so its bases are only determined to u·κ of that sample."""
+    once, so its bases are only determined to u·κ of that sample.  On the
+    pass-efficient non-reorthonormalized branch the core is pinv(gram)ᵀ·…
+    (algorithms.py:295-303): LAPACK's own singular values of gram carry an
+    absolute error ~u·σ₀, i.e. a relative u·κ₂(gram) on the smallest kept one,
+    so the reference's core itself is determined only to ~u·κ₂(gram)."""
     k = _determined(ref["core"], ref_t)
     if k:
         d = np.abs(np.diag(ref_t))[:k]
         perm = ref["perm"][:k]
         ku = _kappa(ref["rdiag_ubar"])
         kv = _kappa(ref["rdiag_vbar"])
-        tol_core = np.maximum(strict, 64 * U * d[0] / d)
+        tol_core = np.maximum(strict, 64 * U * ref.get("pinv_kappa", 1.0) * d[0] / d)
         tol_v = np.maximum(tol_core, 64 * U * kv[perm] * (d[0] / d))
         tol_u = np.maximum(tol_core, 64 * U * ku.max() * (d[0] / d))
         assert np.all(column_relative_error(f.v[:, :k], ref_v[:, :k]) <= tol_v)

@@ -87,7 +87,9 @@ int pbq_gemm_workspace_bytes(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, size
  * a pivot fails it continues, for n ≥ 384, with shifted Cholesky-QR3, and
  * otherwise (or if that fails too) hands the call to the blocked
  * Householder kernel, all decided on the device; method 1 forces the
- * Householder kernel. */
+ * Householder kernel.  For n ≤ 128 and m ≤ 64·SMs the whole Cholesky-QR2
+ * runs as one cooperative launch (redundant per-CTA n×n factorizations in
+ * shared memory); method 3 forces the multi-launch chain instead. */
 int pbq_householder_qr(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, double* R,
                        int64_t ldr, int32_t want_q, int32_t* rank_flag, void* workspace,
                        size_t workspace_bytes, void* stream);
@@ -309,6 +311,7 @@ int pbq_debug_qr_hooks(pbq_ctx* ctx, int32_t* fallbacks, uint64_t* phase_ns, uin
 #define PBQ_QR_AUTO 0
 #define PBQ_QR_HOUSEHOLDER 1
 #define PBQ_QR_CHOLQR_NOSERIES 2
+#define PBQ_QR_CHOLQR_CHAIN 3 /* the multi-launch chain even where the single-launch kernel applies */
 int pbq_set_qr_method(pbq_ctx* ctx, int32_t method);
 
 /* Debug counters (device int[4], NULL to disable): QR calls completed by

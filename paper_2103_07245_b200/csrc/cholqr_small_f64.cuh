@@ -1,0 +1,532 @@
+// Cholesky-QR2 of a small tall matrix in ONE cooperative launch — the
+// `householder_qr` / `orth` path (reference linalg.py:106-115, :142-165) for
+// n ≤ 128 columns and moderate m: config 1's 1000×40 and config 2's 4000×100
+// factors, and the d×d second stage qr(Rᵀ) (algorithms.py:256) for d ≤ 128.
+//
+// Same mathematics, guards and outputs as the multi-launch chain of
+// cholqr_f64.cuh (cq_launch):
+//   G₁ = AᵀA, R₁ = chol(G₁) (κ₁ ≤ 1e6 guard), Q₁ = A·R₁⁻¹,
+//   G₂ = Q₁ᵀQ₁, R₂ = chol(G₂) (the pivot-free series when n·max|G₂ − I| ≤ 1e-5),
+//   Q = Q₁·R₂⁻¹, R = R₂·R₁, rank test of orth on diag(R),
+// but for these shapes the chain is launch- and barrier-bound (7 launches,
+// each a few µs of work: ≈ 95 µs for 1000×40, 140 µs for 4000×100 —
+// tools/cholqr_probe.py).  Here the whole sequence is one kernel with four
+// grid barriers:
+//
+//   [Gram₁ partials] ─bar─ [slice sums → G₁] ─bar─ [factor₁ (every CTA, in
+//   shared memory) ; Q₁ = A·R₁⁻¹ ; Gram₂ partials] ─bar─ [slice sums → G₂]
+//   ─bar─ [factor₂ (every CTA) ; Q = Q₁·R₂⁻¹ ; R = R₂·R₁]
+//
+// * Rows are processed in chunks of 32 (CTA c takes chunks c, c+P, …),
+//   staged in shared memory as nb column blocks of 32×32 (stride CQ_LD), so
+//   every product is the 256-thread DMMA block product cq_mma.
+// * The n×n factorizations are REDUNDANT: every CTA loads the summed Gram
+//   (nb(nb+1)/2 upper blocks, ≤ 80 KB) from L2 and factors it in its own
+//   shared memory — no broadcast barrier, and every CTA holds R⁻¹ for its
+//   triangular product.  Identical data and code give identical bits in
+//   every CTA, so the guards decide uniformly.
+// * Partial Grams are written per CTA and summed in fixed CTA order by the
+//   slice-sum phase (each CTA a contiguous range of elements): bitwise
+//   reproducible.
+// * A is written only by the last phase, after both factorizations passed,
+//   so the Householder fallback (qr_f64.cuh, launched behind with run_if =
+//   *fallback) sees the original input.
+#pragma once
+#include "cholqr_f64.cuh"
+
+namespace pbq {
+
+constexpr int CS_THREADS = 256;
+constexpr int CS_MAX_NB = 4;  // n ≤ 128
+
+__host__ __device__ constexpr int cs_nblk(int nb) { return nb * (nb + 1) / 2; }
+// slot of upper block (i, j), i ≤ j, in row-major upper order
+__device__ __forceinline__ int cs_ut(int i, int j, int nb) { return i * nb - (i * (i - 1)) / 2 + (j - i); }
+template <int NB>
+__host__ __device__ constexpr int cs_region_a_blocks() {
+  return cs_nblk(NB) > 2 * NB ? cs_nblk(NB) : 2 * NB;
+}
+template <int NB>
+__host__ __device__ constexpr size_t cs_smem_bytes() {
+  return size_t(cs_region_a_blocks<NB>() + cs_nblk(NB) + 2) * CQ_BLK * sizeof(double);
+}
+
+struct CsArgs {
+  long m, n, np;
+  double* A;          // m×n (lda), overwritten by Q on success
+  long lda;
+  double* R;          // n×n (ldr) upper, zeros below (may be null)
+  long ldr;
+  int* rank_flag;     // may be null
+  int* fallback;      // set → the Householder kernel runs (A untouched)
+  double* Q1;         // m×np scratch (ld np)
+  double* part;       // [P][nblk][32·32] partial Grams
+  double* G;          // [nblk][32·32] summed Gram
+  double* R1;         // [nblk][32·32] R₁ blocks (pass 2 forms R = R₂·R₁)
+  unsigned long long* emax;  // max|G₂ − I| bits (zeroed by the host)
+  unsigned int* counter;     // grid barrier (zeroed by the host)
+  int* stats;                // optional [done, fallbacks, by the series, shifted]
+  double kappa_max;
+  int allow_series;
+  unsigned long long* phase_ns;  // optional profiling (CTA 0): [16..24) the phases below
+};
+
+#define CS_MARK(slot)                                                                  \
+  do {                                                                                 \
+    if (p.phase_ns && blockIdx.x == 0 && threadIdx.x == 0) {                           \
+      unsigned long long now_;                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                        \
+      p.phase_ns[16 + (slot)] += now_ - t_mark;                                        \
+      t_mark = now_;                                                                   \
+    }                                                                                  \
+  } while (0)
+
+// 32-row chunk `ch` of the m×n row-major matrix M (ld) → nb column blocks of
+// 32×32 in shared memory (columns ≥ n and rows ≥ m read as zero)
+template <int NB>
+__device__ __forceinline__ void cs_load_chunk(double* dst, const double* M, long ld, long m, long n, long ch) {
+  constexpr int PER = 32 * 32 * NB / CS_THREADS;  // elements per thread: all loads in flight, then the stores
+  const long r0 = ch * 32;
+  double v[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = threadIdx.x + q * CS_THREADS;
+    const int r = e / (32 * NB), c = e % (32 * NB);
+    const long gr = r0 + r;
+    v[q] = (gr < m && c < n) ? __ldcg(M + gr * ld + c) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = threadIdx.x + q * CS_THREADS;
+    const int r = e / (32 * NB), c = e % (32 * NB);
+    dst[(c >> 5) * CQ_BLK + r * CQ_LD + (c & 31)] = v[q];
+  }
+}
+template <int NB>
+__device__ __forceinline__ void cs_store_chunk(double* M, long ld, long m, long n, long ch, const double* src) {
+  const long r0 = ch * 32;
+  for (int e = threadIdx.x; e < 32 * 32 * NB; e += CS_THREADS) {
+    const int r = e / (32 * NB), c = e % (32 * NB);
+    const long gr = r0 + r;
+    if (gr < m && c < n) M[gr * ld + c] = src[(c >> 5) * CQ_BLK + r * CQ_LD + (c & 31)];
+  }
+}
+
+// partial Gram of this CTA's chunks of M → part[blockIdx.x]
+template <int NB>
+__device__ void cs_gram(const CsArgs& p, const double* M, long ld, double* chunk) {
+  constexpr int NBLK = cs_nblk(NB);
+  const long nch = (p.m + 31) / 32;
+  double c[NBLK][2][2];
+#pragma unroll
+  for (int b = 0; b < NBLK; ++b) cq_zero(c[b]);
+  for (long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    cs_load_chunk<NB>(chunk, M, ld, p.m, p.n, ch);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+#pragma unroll
+      for (int j = i; j < NB; ++j) cq_mma<true, false>(c[i * NB - (i * (i - 1)) / 2 + (j - i)], chunk + i * CQ_BLK, chunk + j * CQ_BLK);
+    __syncthreads();
+  }
+  double* dst = p.part + size_t(blockIdx.x) * NBLK * 1024;
+  const int r = cq_row();
+#pragma unroll
+  for (int b = 0; b < NBLK; ++b)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      __stcg(reinterpret_cast<double2*>(dst + b * 1024 + r * 32 + cq_col(h)), make_double2(c[b][h][0], c[b][h][1]));
+}
+
+// G = Σ_ctas part (fixed order), identity padding beyond n; with emax, max|G − I|
+template <int NB>
+__device__ void cs_reduce(const CsArgs& p, unsigned long long* emax) {
+  constexpr int NBLK = cs_nblk(NB);
+  const long E = long(NBLK) * 1024;
+  const long e0 = long(blockIdx.x) * E / gridDim.x, e1 = long(blockIdx.x + 1) * E / gridDim.x;
+  double dev = 0.0;
+  for (long e = e0 + threadIdx.x; e < e1; e += CS_THREADS) {
+    const int b = int(e >> 10), w = int(e & 1023);
+    int bi = 0, bj = 0;
+    upper_tile(b, NB, bi, bj);
+    const long gr = long(bi) * 32 + (w >> 5), gc = long(bj) * 32 + (w & 31);
+    double s = 0.0;
+    const double* src = p.part + e;
+    for (int q0 = 0; q0 < int(gridDim.x); q0 += 8) {  // 8 loads in flight, summed in CTA order
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = (q0 + q < int(gridDim.x)) ? __ldcg(src + size_t(q0 + q) * E) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    if (gr >= p.n || gc >= p.n) s = (gr == gc) ? 1.0 : 0.0;
+    __stcg(p.G + e, s);
+    if (emax && gr <= gc) {
+      const double d = fabs(s - (gr == gc ? 1.0 : 0.0));
+      dev = (d <= dev) ? dev : d;  // NaN sticks
+    }
+  }
+  if (emax) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, dev, o);
+      dev = (x <= dev) ? dev : x;
+    }
+    if ((threadIdx.x & 31) == 0 && dev != 0.0) {
+      const unsigned long long bits = (dev == dev) ? __double_as_longlong(dev) : 0x7ff0000000000000ull;
+      atomicMax(emax, bits);
+    }
+  }
+}
+
+// c (accumulator of a 32×32 block) → shared block S (ld CQ_LD)
+__device__ __forceinline__ void cs_put(double* S, const double (&c)[2][2]) { cq_store_acc(S, c, 1.0); }
+
+// Blocked right-looking Cholesky of the nb×nb upper blocks in Gs (in place →
+// R) and X = R⁻¹ in Xs, in this CTA's shared memory.  Returns false when a
+// pivot is not positive (uniform over the CTA).  tmp: 2 scratch blocks.
+template <int NB>
+__device__ bool cs_chol_inv(double* Gs, double* Xs, double* tmp, double* rowbuf, int* s_ok) {
+  const int warp = threadIdx.x >> 5;
+  for (int k = 0; k < NB; ++k) {
+    double* Gkk = Gs + cs_ut(k, k, NB) * CQ_BLK;
+    double* Xkk = Xs + cs_ut(k, k, NB) * CQ_BLK;
+    if (warp < 2) {
+      const bool ok = cq_chol_inv32_2warp(Gkk, Xkk, rowbuf);
+      if (threadIdx.x == 0) *s_ok = ok;
+    }
+    __syncthreads();
+    if (!*s_ok) return false;
+    // R_kj = R_kk⁻ᵀ·G_kj  (j > k)
+    for (int j = k + 1; j < NB; ++j) {
+      double c[2][2];
+      cq_zero(c);
+      double* Gkj = Gs + cs_ut(k, j, NB) * CQ_BLK;
+      cq_mma<true, false>(c, Xkk, Gkj);
+      __syncthreads();
+      cs_put(Gkj, c);
+      __syncthreads();
+    }
+    // Schur: G_ij −= R_kiᵀ·R_kj  (k < i ≤ j)
+    for (int i = k + 1; i < NB; ++i)
+      for (int j = i; j < NB; ++j) {
+        double c[2][2];
+        cq_zero(c);
+        cq_mma<true, false>(c, Gs + cs_ut(k, i, NB) * CQ_BLK, Gs + cs_ut(k, j, NB) * CQ_BLK);
+        double* Gij = Gs + cs_ut(i, j, NB) * CQ_BLK;  // read by no other item of this step
+        const int r = cq_row();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          Gij[r * CQ_LD + cq_col(h)] -= c[h][0];
+          Gij[r * CQ_LD + cq_col(h) + 1] -= c[h][1];
+        }
+      }
+    __syncthreads();
+    // X_ik = −(Σ_{l=i}^{k−1} X_il·R_lk)·R_kk⁻¹  (i < k)
+    for (int i = 0; i < k; ++i) {
+      double c[2][2];
+      cq_zero(c);
+      for (int l = i; l < k; ++l) cq_mma<false, false>(c, Xs + cs_ut(i, l, NB) * CQ_BLK, Gs + cs_ut(l, k, NB) * CQ_BLK);
+      cs_put(tmp, c);
+      __syncthreads();
+      cq_zero(c);
+      cq_mma<false, false>(c, tmp, Xkk);
+      cq_store_acc(Xs + cs_ut(i, k, NB) * CQ_BLK, c, -1.0);
+      __syncthreads();
+    }
+  }
+  return true;
+}
+
+// κ₁(R) = ‖R‖₁·‖R⁻¹‖₁ over the first n columns (max column sums)
+template <int NB>
+__device__ double cs_kappa1(const double* Rs, const double* Xs, long n, double* red) {
+  double mr = 0.0, mx = 0.0;
+  for (int j = threadIdx.x; j < n; j += CS_THREADS) {
+    const int jb = j >> 5, jc = j & 31;
+    double sr = 0.0, sx = 0.0;
+    for (int ib = 0; ib <= jb; ++ib)
+      for (int r = 0; r < 32; ++r) {
+        sr += fabs(Rs[cs_ut(ib, jb, NB) * CQ_BLK + r * CQ_LD + jc]);
+        sx += fabs(Xs[cs_ut(ib, jb, NB) * CQ_BLK + r * CQ_LD + jc]);
+      }
+    mr = fmax(mr, sr);
+    mx = fmax(mx, sx);
+    if (!(sr < INFINITY) || !(sx < INFINITY)) mr = INFINITY;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[warp] = mr;
+    red[8 + warp] = mx;
+  }
+  __syncthreads();
+  mr = 0.0;
+  mx = 0.0;
+  for (int w = 0; w < CS_THREADS / 32; ++w) {
+    mr = fmax(mr, red[w]);
+    mx = fmax(mx, red[8 + w]);
+  }
+  __syncthreads();
+  return mr * mx;
+}
+
+// out = chunk · X (X upper-block triangular): out_j = Σ_{l≤j} chunk_l·X_lj
+template <int NB>
+__device__ __forceinline__ void cs_tri(const double* chunk, const double* Xs, double* out) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    double c[2][2];
+    cq_zero(c);
+    for (int l = 0; l <= j; ++l) cq_mma<false, false>(c, chunk + l * CQ_BLK, Xs + cs_ut(l, j, NB) * CQ_BLK);
+    cs_put(out + j * CQ_BLK, c);
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(CS_THREADS, 1) cholqr_small_kernel(CsArgs p) {
+  constexpr int NBLK = cs_nblk(NB);
+  extern __shared__ __align__(16) double sm[];
+  double* regA = sm;                                          // G / R blocks, or chunk in + out
+  double* Xs = sm + cs_region_a_blocks<NB>() * CQ_BLK;        // R⁻¹ blocks
+  double* tmp = Xs + NBLK * CQ_BLK;                           // 2 scratch blocks
+  __shared__ __align__(16) double s_rowbuf[2 * CQ_RB2];
+  __shared__ double s_red[16];
+  __shared__ int s_ok;
+  const int tid = threadIdx.x;
+  const long nch = (p.m + 31) / 32;
+  unsigned int gen = 0;
+  unsigned long long t_mark = 0;
+  if (p.phase_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_mark));
+
+  // ---- Gram₁
+  cs_gram<NB>(p, p.A, p.lda, regA);
+  grid_barrier(p.counter, gen);
+  CS_MARK(0);
+  cs_reduce<NB>(p, nullptr);
+  grid_barrier(p.counter, gen);
+  CS_MARK(1);
+
+  // ---- factor₁ (every CTA), κ guard
+  for (int e = tid; e < NBLK * 1024; e += CS_THREADS)
+    regA[(e >> 10) * CQ_BLK + ((e & 1023) >> 5) * CQ_LD + (e & 31)] = __ldcg(p.G + e);
+  for (int e = tid; e < NBLK * CQ_BLK; e += CS_THREADS) Xs[e] = 0.0;
+  __syncthreads();
+  bool ok = cs_chol_inv<NB>(regA, Xs, tmp, s_rowbuf, &s_ok);
+  if (ok) ok = cs_kappa1<NB>(regA, Xs, p.n, s_red) <= p.kappa_max;
+  if (!ok) {
+    if (blockIdx.x == 0 && tid == 0) {
+      *p.fallback = 1;
+      if (p.stats) atomicAdd(p.stats + 1, 1);
+    }
+    return;  // uniform: every CTA factored the same G₁
+  }
+  CS_MARK(2);
+  if (blockIdx.x == 0)  // R₁ for R = R₂·R₁ (upper blocks, zeros below inside diagonal blocks)
+    for (int e = tid; e < NBLK * 1024; e += CS_THREADS) {
+      const int b = e >> 10, r = (e & 1023) >> 5, c = e & 31;
+      int bi = 0, bj = 0;
+      upper_tile(b, NB, bi, bj);
+      const double v = regA[b * CQ_BLK + r * CQ_LD + c];
+      __stcg(p.R1 + e, (bi == bj && c < r) ? 0.0 : v);
+    }
+  __syncthreads();
+
+  // ---- Q₁ = A·R₁⁻¹ → scratch, and Gram₂ partials of the same chunks
+  {
+    double* chunk = regA;
+    double* out = regA + NB * CQ_BLK;
+    double c[NBLK][2][2];
+#pragma unroll
+    for (int b = 0; b < NBLK; ++b) cq_zero(c[b]);
+    for (long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+      cs_load_chunk<NB>(chunk, p.A, p.lda, p.m, p.n, ch);
+      __syncthreads();
+      cs_tri<NB>(chunk, Xs, out);
+      __syncthreads();
+      // rows ≥ m of a chunk are zero in A, hence in Q₁: they add nothing
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int j = i; j < NB; ++j)
+          cq_mma<true, false>(c[i * NB - (i * (i - 1)) / 2 + (j - i)], out + i * CQ_BLK, out + j * CQ_BLK);
+      cs_store_chunk<NB>(p.Q1, p.np, p.m, p.np, ch, out);
+      __syncthreads();
+    }
+    double* dst = p.part + size_t(blockIdx.x) * NBLK * 1024;
+    const int r = cq_row();
+#pragma unroll
+    for (int b = 0; b < NBLK; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        __stcg(reinterpret_cast<double2*>(dst + b * 1024 + r * 32 + cq_col(h)), make_double2(c[b][h][0], c[b][h][1]));
+  }
+  grid_barrier(p.counter, gen);
+  CS_MARK(3);
+  cs_reduce<NB>(p, p.emax);
+  grid_barrier(p.counter, gen);
+  CS_MARK(4);
+
+  // ---- factor₂ (every CTA): series when G₂ is near the identity
+  const double em = __longlong_as_double(static_cast<long long>(__ldcg(p.emax)));
+  const bool series = p.allow_series && double(p.n) * em <= CQ_SERIES_EMAX;  // false for NaN
+  for (int e = tid; e < NBLK * 1024; e += CS_THREADS)
+    regA[(e >> 10) * CQ_BLK + ((e & 1023) >> 5) * CQ_LD + (e & 31)] = __ldcg(p.G + e);
+  for (int e = tid; e < NBLK * CQ_BLK; e += CS_THREADS) Xs[e] = 0.0;
+  __syncthreads();
+  // R₂ = I + Xd with Xd upper: series X = split(E − X₀ᵀX₀), X₀ = split(E);
+  // R₂⁻¹ = I − X + X·X.  Cholesky: R₂ blocks in regA, R₂⁻¹ in Xs.
+  if (series) {
+    // X₀ = split(E) in place (regA), then X = split(E − X₀ᵀX₀) → tmp-staged per block into Xs
+    for (int b = 0; b < NBLK; ++b) {
+      int bi = 0, bj = 0;
+      upper_tile(b, NB, bi, bj);
+      for (int e = tid; e < 1024; e += CS_THREADS) {
+        const int r = e >> 5, cc = e & 31;
+        double* v = regA + b * CQ_BLK + r * CQ_LD + cc;
+        *v = cq_split(bi * 32 + r, bj * 32 + cc, *v - ((bi == bj && r == cc) ? 1.0 : 0.0));
+      }
+    }
+    __syncthreads();
+    // (X₀ᵀX₀)_ij = Σ_{l ≤ i} X₀_liᵀ·X₀_lj ; X_ij = split(E_ij − ·) with E_ij recovered from X₀
+    for (int b = 0; b < NBLK; ++b) {
+      int bi = 0, bj = 0;
+      upper_tile(b, NB, bi, bj);
+      double c[2][2];
+      cq_zero(c);
+      for (int l = 0; l <= bi; ++l)
+        cq_mma<true, false>(c, regA + cs_ut(l, bi, NB) * CQ_BLK, regA + cs_ut(l, bj, NB) * CQ_BLK);
+      const int r = cq_row();
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int gr = bi * 32 + r, gc = bj * 32 + cq_col(h) + e;
+          const double x0 = regA[b * CQ_BLK + r * CQ_LD + cq_col(h) + e];
+          const double ev = gc > gr ? x0 : (gc == gr ? 2.0 * x0 : 0.0);  // E_ij from split(E)
+          c[h][e] = cq_split(gr, gc, ev - c[h][e]);
+        }
+      cq_store_acc(Xs + b * CQ_BLK, c, 1.0);  // X (not yet the inverse)
+    }
+    __syncthreads();
+    // regA ← X ; Xs ← R₂⁻¹ = I − X + X·X
+    for (int e = tid; e < NBLK * CQ_BLK; e += CS_THREADS) regA[e] = Xs[e];
+    __syncthreads();
+    for (int b = 0; b < NBLK; ++b) {
+      int bi = 0, bj = 0;
+      upper_tile(b, NB, bi, bj);
+      double c[2][2];
+      cq_zero(c);
+      for (int l = bi; l <= bj; ++l)
+        cq_mma<false, false>(c, regA + cs_ut(bi, l, NB) * CQ_BLK, regA + cs_ut(l, bj, NB) * CQ_BLK);
+      const int r = cq_row();
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int gr = bi * 32 + r, gc = bj * 32 + cq_col(h) + e;
+          c[h][e] = (gr == gc ? 1.0 : 0.0) - regA[b * CQ_BLK + r * CQ_LD + cq_col(h) + e] + c[h][e];
+        }
+      cq_store_acc(Xs + b * CQ_BLK, c, 1.0);
+    }
+    __syncthreads();
+    // regA holds X: R₂ = I + X (diagonal of R₂ = 1 + X_ii)
+  } else {
+    if (!cs_chol_inv<NB>(regA, Xs, tmp, s_rowbuf, &s_ok)) {
+      if (blockIdx.x == 0 && tid == 0) {
+        *p.fallback = 1;
+        if (p.stats) atomicAdd(p.stats + 1, 1);
+      }
+      return;
+    }
+  }
+
+  CS_MARK(5);
+  // ---- R = R₂·R₁, output block b on CTA b mod P (each a few L2 round trips);
+  // then the rank test of orth on diag(R) by CTA 0
+  for (int b = blockIdx.x; b < NB * NB; b += gridDim.x) {
+    const int bi = b / NB, bj = b % NB;
+    double c[2][2];
+    cq_zero(c);
+    if (bi <= bj) {
+      // series: R = R₁ + X·R₁ ; Cholesky: R = R₂·R₁ (R₂ upper blocks in regA)
+      for (int l = bi; l <= bj; ++l) {
+        const double* r1 = p.R1 + size_t(cs_ut(l, bj, NB)) * 1024;
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = __ldcg(r1 + tid + q * CS_THREADS);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = tid + q * CS_THREADS;
+          tmp[(e >> 5) * CQ_LD + (e & 31)] = v[q];
+        }
+        __syncthreads();
+        cq_mma<false, false>(c, regA + cs_ut(bi, l, NB) * CQ_BLK, tmp);
+        __syncthreads();
+      }
+      if (series) {
+        const double* r1 = p.R1 + size_t(cs_ut(bi, bj, NB)) * 1024;
+        const int r = cq_row();
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) c[h][e] += __ldcg(r1 + r * 32 + cq_col(h) + e);
+      }
+    }
+    if (p.R) {
+      const int r = cq_row();
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const long gr = long(bi) * 32 + r, gc = long(bj) * 32 + cq_col(h) + e;
+          if (gr < p.n && gc < p.n) p.R[gr * p.ldr + gc] = (gc >= gr) ? c[h][e] : 0.0;
+        }
+    }
+  }
+  if (blockIdx.x == 0) {
+    // rank test input, as the chain computes it: diag(R) = diag(R₁)·(1 + diag X)
+    // (series) or diag(R₂)∘diag(R₁)
+    for (int i = tid; i < NB * 32; i += CS_THREADS) {
+      const int b = cs_ut(i >> 5, i >> 5, NB), w = i & 31;
+      const double r1 = __ldcg(p.R1 + size_t(b) * 1024 + w * 32 + w);
+      const double x = regA[b * CQ_BLK + w * CQ_LD + w];
+      tmp[CQ_BLK + i] = series ? r1 * (1.0 + x) : x * r1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double d0 = fabs(tmp[CQ_BLK]);
+      int def = 0;
+      for (long i = 0; i < p.n; ++i)
+        if (fabs(tmp[CQ_BLK + i]) < 1e-14 * d0) def = 1;
+      if (p.rank_flag) *p.rank_flag = (d0 == 0.0) ? 2 : def;
+      if (p.stats) {
+        atomicAdd(p.stats, 1);
+        if (series) atomicAdd(p.stats + 2, 1);
+      }
+    }
+    __syncthreads();
+  }
+
+  CS_MARK(6);
+  // ---- Q = Q₁·R₂⁻¹ → A
+  {
+    double* chunk = regA;  // (regA's X / R₂ is no longer needed)
+    double* out = regA + NB * CQ_BLK;
+    for (long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+      cs_load_chunk<NB>(chunk, p.Q1, p.np, p.m, p.np, ch);
+      __syncthreads();
+      cs_tri<NB>(chunk, Xs, out);
+      __syncthreads();
+      cs_store_chunk<NB>(p.A, p.lda, p.m, p.n, ch, out);
+      __syncthreads();
+    }
+  }
+  CS_MARK(7);
+}
+
+}  // namespace pbq

@@ -20,6 +20,7 @@
 #include "gemm_f64.cuh"
 #include "gemm_tma_f64.cuh"
 #include "cholqr_f64.cuh"
+#include "cholqr_small_f64.cuh"
 #include "cpqr_f64.cuh"
 #include "qr_f64.cuh"
 #include "sketch.cuh"
@@ -821,13 +822,92 @@ int cqd_stage(pbq_ctx* ctx, int stage, long m, long n, double* A, long lda, doub
   return fail(ctx, PBQ_ERR_PARAM, "cholqr2_dist: stage must be 0, 1 or 2");
 }
 
+// ------------------------------------------- single-launch Cholesky-QR2 ----
+// cholqr_small_f64.cuh: n ≤ 128 and at most CS_MAX_CHUNKS 32-row chunks per
+// CTA, where the 7-launch chain is launch/barrier-bound.
+constexpr long CS_MAX_CHUNKS = 2;
+bool cs_eligible(const pbq_ctx* ctx, long m, long n) {
+  return (ctx->qr_method == PBQ_QR_AUTO || ctx->qr_method == PBQ_QR_CHOLQR_NOSERIES) && n >= 1 &&
+         n <= 32L * CS_MAX_NB && m >= n && ceil_div(m, 32) <= CS_MAX_CHUNKS * ctx->sms;
+}
+int cs_grid(const pbq_ctx* ctx, long m) { return int(std::max<long>(1, std::min<long>(ceil_div(m, 32), ctx->sms))); }
+size_t cs_ws_bytes(const pbq_ctx* ctx, const QrPlan& hp, long m, long n) {
+  const long nb = ceil_div(n, 32), np = 32 * nb, nblk = nb * (nb + 1) / 2;
+  return 256 + align_up(size_t(cs_grid(ctx, m)) * nblk * 1024 * 8, 256) + 2 * align_up(size_t(nblk) * 1024 * 8, 256) +
+         align_up(size_t(m) * np * 8, 256) + qr_ws_bytes(hp, n) + 1024;
+}
+using CsFn = void (*)(CsArgs);
+CsFn cs_fn(int nb) {
+  switch (nb) {
+    case 1: return cholqr_small_kernel<1>;
+    case 2: return cholqr_small_kernel<2>;
+    case 3: return cholqr_small_kernel<3>;
+    default: return cholqr_small_kernel<4>;
+  }
+}
+size_t cs_smem(int nb) {
+  switch (nb) {
+    case 1: return cs_smem_bytes<1>();
+    case 2: return cs_smem_bytes<2>();
+    case 3: return cs_smem_bytes<3>();
+    default: return cs_smem_bytes<4>();
+  }
+}
+
+int cs_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int32_t* rank_flag, void* ws,
+              size_t ws_bytes, cudaStream_t st) {
+  QrPlan hp;
+  PBQ_TRY(qr_plan(ctx, m, n, hp));
+  if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "qr: leading dimension too small");
+  const int nb = int(ceil_div(n, 32)), nblk = nb * (nb + 1) / 2;
+  const long np = 32L * nb;
+  const int grid = cs_grid(ctx, m);
+  Carve cv(ws, ws_bytes);
+  int* ctl = cv.take<int>(64);  // [0] fallback, [8] grid barrier, [16..17] emax, [48] Householder barrier
+  double* part = cv.take<double>(size_t(grid) * nblk * 1024);
+  double* G = cv.take<double>(size_t(nblk) * 1024);
+  double* R1 = cv.take<double>(size_t(nblk) * 1024);
+  double* Q1 = cv.take<double>(size_t(m) * np);
+  const size_t hws_bytes = qr_ws_bytes(hp, n);
+  char* hws = cv.take<char>(hws_bytes);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  PBQ_CUDA(ctx, cudaMemsetAsync(ctl, 0, 64 * sizeof(int), st));
+  CsArgs a;
+  memset(&a, 0, sizeof(a));
+  a.m = m; a.n = n; a.np = np; a.A = A; a.lda = lda; a.R = R; a.ldr = ldr;
+  a.rank_flag = rank_flag; a.fallback = ctl; a.Q1 = Q1; a.part = part; a.G = G; a.R1 = R1;
+  a.emax = reinterpret_cast<unsigned long long*>(ctl + 16);
+  a.counter = reinterpret_cast<unsigned int*>(ctl + 8);
+  a.stats = ctx->cq_stats;
+  a.kappa_max = CQ_KAPPA_MAX;
+  a.allow_series = ctx->qr_method != PBQ_QR_CHOLQR_NOSERIES;
+  a.phase_ns = ctx->qr_phase_ns;
+  const CsFn fn = cs_fn(nb);
+  const size_t smem = cs_smem(nb);
+  {
+    ProfScope ps(ctx->prof, st, 1);
+    ProfSuppress quiet(ctx->prof);
+    PBQ_CUDA(ctx, ensure_smem(ctx, reinterpret_cast<const void*>(fn), smem));
+    void* args[] = {&a};
+    PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid), dim3(CS_THREADS), args, smem, st));
+    ctx->launches += 1;
+    // Householder fallback (returns at once unless a factorization failed)
+    PBQ_TRY(hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, ctl,
+                      reinterpret_cast<unsigned int*>(ctl + 48)));
+  }
+  return PBQ_OK;
+}
+
 size_t qr_any_ws_bytes(const pbq_ctx* ctx, const QrPlan& hp, long m, long n) {
-  if (ctx->qr_method != PBQ_QR_HOUSEHOLDER) return cq_ws_bytes(cq_plan(ctx, m, n), hp, m, n);
-  return qr_ws_bytes(hp, n);
+  if (ctx->qr_method == PBQ_QR_HOUSEHOLDER) return qr_ws_bytes(hp, n);
+  size_t b = cq_ws_bytes(cq_plan(ctx, m, n), hp, m, n);
+  if (cs_eligible(ctx, m, n)) b = std::max(b, cs_ws_bytes(ctx, hp, m, n));
+  return b;
 }
 
 int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int want_q, int32_t* rank_flag,
               void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (want_q && cs_eligible(ctx, m, n)) return cs_launch(ctx, m, n, A, lda, R, ldr, rank_flag, ws, ws_bytes, st);
   if (ctx->qr_method != PBQ_QR_HOUSEHOLDER && want_q) return cq_launch(ctx, m, n, A, lda, R, ldr, rank_flag, ws, ws_bytes, st);
   return hh_launch(ctx, m, n, A, lda, R, ldr, want_q, rank_flag, ws, ws_bytes, st, nullptr);
 }
@@ -1703,7 +1783,8 @@ int pbq_cholqr2_dist(pbq_ctx* ctx, int32_t stage, int64_t m, int64_t n, double* 
 
 int pbq_set_qr_method(pbq_ctx* ctx, int32_t method) {
   if (!ctx) return PBQ_ERR_PARAM;
-  if (method != PBQ_QR_AUTO && method != PBQ_QR_HOUSEHOLDER && method != PBQ_QR_CHOLQR_NOSERIES)
+  if (method != PBQ_QR_AUTO && method != PBQ_QR_HOUSEHOLDER && method != PBQ_QR_CHOLQR_NOSERIES &&
+      method != PBQ_QR_CHOLQR_CHAIN)
     return fail(ctx, PBQ_ERR_PARAM, "unknown QR method %d", method);
   ctx->qr_method = method;
   return PBQ_OK;

@@ -81,6 +81,34 @@ __device__ __forceinline__ double jac_init(const JacArgs& p, int i, int e) {
   return (e - p.L == i) ? 1.0 : 0.0;
 }
 
+// Rotation parameters for the pair with a = ‖x‖², b = ‖y‖², c = x·y:
+// returns false (no rotation) unless aapq = |c|/(‖x‖‖y‖) > tol.  On the
+// MUFU approximations + Newton steps (fast_rsqrt / fast_rcp, ~1 ulp): the
+// IEEE chain sqrt → div → sqrt → div → sqrt was most of a round's latency.
+// Norms near the ends of the exponent range (the .ftz approximations would
+// flush) take the IEEE formulas.
+__device__ __forceinline__ bool jac_params(double a, double b, double c, double tol, double& aapq, double& cs,
+                                           double& sn) {
+  aapq = 0.0;
+  if (!(a > 0.0 && b > 0.0) || !(a < INFINITY && b < INFINITY)) return false;
+  const bool fast = a > 1e-280 && b > 1e-280 && a < 1e280 && b < 1e280;
+  aapq = fast ? fabs(c) * fast_rsqrt(a) * fast_rsqrt(b) : fabs(c) / (sqrt(a) * sqrt(b));
+  if (!(aapq > tol)) return false;
+  const double zeta = fast ? 0.5 * (b - a) * fast_rcp(c) : (b - a) / (2.0 * c);
+  double t;
+  if (fabs(zeta) > 1e100) {
+    t = 0.5 / zeta;
+  } else if (fast) {
+    const double h = fma(zeta, zeta, 1.0);
+    t = copysign(fast_rcp(fabs(zeta) + h * fast_rsqrt(h)), zeta);
+  } else {
+    t = copysign(1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
+  }
+  cs = fast ? fast_rsqrt(fma(t, t, 1.0)) : 1.0 / sqrt(fma(t, t, 1.0));
+  sn = cs * t;
+  return true;
+}
+
 // The rotation of one pair (x, y: VPL doubles per lane, element lane + 32·k).
 // Returns true when a rotation was applied; `aapq` receives the pair's
 // relative off-diagonal |x·y|/(‖x‖‖y‖) before it and `sinj` |sin θ| of the
@@ -105,18 +133,8 @@ __device__ __forceinline__ bool jac_rotate(double (&x)[VPL], double (&y)[VPL], i
     c += __shfl_xor_sync(0xffffffffu, c, o);
   }
   sinj = 0.0;
-  aapq = 0.0;
-  if (!(a > 0.0 && b > 0.0)) return false;
-  aapq = fabs(c) / (sqrt(a) * sqrt(b));
-  if (!(aapq > tol)) return false;
-  const double zeta = (b - a) / (2.0 * c);
-  double t;
-  if (fabs(zeta) > 1e100)
-    t = 0.5 / zeta;
-  else
-    t = copysign(1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
-  const double cs = 1.0 / sqrt(fma(t, t, 1.0));
-  const double sn = cs * t;
+  double cs, sn;
+  if (!jac_params(a, b, c, tol, aapq, cs, sn)) return false;
   sinj = fabs(sn);
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
@@ -383,13 +401,10 @@ __global__ void __launch_bounds__(JAC_GRID_WARPS * 32, 1)
             b += __shfl_xor_sync(0xffffffffu, b, o);
             c += __shfl_xor_sync(0xffffffffu, c, o);
           }
-          const double aapq = (a > 0.0 && b > 0.0) ? fabs(c) / (sqrt(a) * sqrt(b)) : 0.0;
+          double aapq, cs, sn;
+          const bool rot_it = jac_params(a, b, c, p.tol, aapq, cs, sn);
           mx_aapq = fmax(mx_aapq, aapq);
-          if (aapq > p.tol) {
-            const double zeta = (b - a) / (2.0 * c);
-            const double t = fabs(zeta) > 1e100 ? 0.5 / zeta
-                                                : copysign(1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
-            const double cs = 1.0 / sqrt(fma(t, t, 1.0)), sn = cs * t;
+          if (rot_it) {
             mx_sin = fmax(mx_sin, fabs(sn));
 #pragma unroll 4
             for (int e = lane; e < p.V; e += 32) {

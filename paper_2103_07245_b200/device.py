@@ -44,7 +44,7 @@ class Context:
     def check(self, status, what):
         _lib.raise_status(status, self.handle, what)
 
-    QR_AUTO, QR_HOUSEHOLDER, QR_CHOLQR_NOSERIES = 0, 1, 2
+    QR_AUTO, QR_HOUSEHOLDER, QR_CHOLQR_NOSERIES, QR_CHOLQR_CHAIN = 0, 1, 2, 3
 
     def set_qr_method(self, method):
         """0: Cholesky-QR2 with on-device Householder fallback (default);

@@ -52,14 +52,16 @@ def reference_pkg():
     return pbpqlp
 
 
-@pytest.fixture(params=["auto", "householder"])
+@pytest.fixture(params=["auto", "chain", "householder"])
 def qr_method(request, cuda):
-    """Run a test under both QR methods: the default guarded Cholesky-QR2
-    (cholqr_f64.cuh) and the blocked Householder kernel (qr_f64.cuh)."""
+    """Run a test under each QR method: the default guarded Cholesky-QR2
+    (the single-launch kernel of cholqr_small_f64.cuh where it applies, else
+    the chain of cholqr_f64.cuh), the chain forced, and the blocked
+    Householder kernel (qr_f64.cuh)."""
     from paper_2103_07245_b200 import device as D
 
     ctx = D.context(cuda)
-    ctx.set_qr_method(ctx.QR_AUTO if request.param == "auto" else ctx.QR_HOUSEHOLDER)
+    ctx.set_qr_method({"auto": ctx.QR_AUTO, "chain": ctx.QR_CHOLQR_CHAIN, "householder": ctx.QR_HOUSEHOLDER}[request.param])
     yield request.param
     ctx.set_qr_method(ctx.QR_AUTO)
 

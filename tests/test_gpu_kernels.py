@@ -218,11 +218,14 @@ def test_shifted_cholqr3_route(cuda):
     assert counts[1] == 1 and counts[0] == 0 and flag == 1
 
 
-def test_cholqr_path_and_guard(cuda):
+@pytest.mark.parametrize("family", ["auto", "chain"])
+def test_cholqr_path_and_guard(cuda, family):
     """The default method completes well-conditioned inputs (κ₁ ≤ 1e6, both
     the series and the Cholesky variant of pass 2) by Cholesky-QR2 and hands
     ill-conditioned, rank-deficient and zero inputs to the Householder kernel
-    on the device; either way the factors match LAPACK (linalg.py:106-115)."""
+    on the device; either way the factors match LAPACK (linalg.py:106-115).
+    "auto" runs n ≤ 128 through the single-launch kernel
+    (cholqr_small_f64.cuh), "chain" forces the multi-launch chain."""
     from paper_2103_07245_b200 import device as D
 
     ctx = D.context(cuda)
@@ -245,6 +248,8 @@ def test_cholqr_path_and_guard(cuda):
         ("300x257, no series", rng.standard_normal((300, 257)), [1, 0, 0, 0], 2),
     ]
     for name, x, expect, method in cases:
+        if family == "chain" and method == 0:
+            method = ctx.QR_CHOLQR_CHAIN
         ctx.set_qr_method(method)
         try:
             counts, q, r, flag = _cholqr_counts(ctx, cuda, x)

@@ -53,15 +53,15 @@ def case(name, a_np):
     x0 = torch.from_numpy(a_np).to(dev)
     qr_, rr_ = ref_qr(a_np)
     out = []
-    for method in (0, 1):
+    for method in (0, 3, 1):  # auto (single-launch kernel where it applies), the 7-launch chain, Householder
         stats.zero_()
         q, r, flag, t = run(method, x0)
         st = stats.tolist()
         eq = np.max(np.linalg.norm(q - qr_, axis=0) / np.linalg.norm(qr_, axis=0))
-        er = np.linalg.norm(r - rr_) / np.linalg.norm(rr_)
+        er = np.linalg.norm(r - rr_) / np.linalg.norm(rr_) if np.linalg.norm(rr_) > 0 else 0.0
         orth = np.linalg.norm(q.T @ q - np.eye(n))
-        out.append(f"{'chol' if method == 0 else 'hh  '} {t*1e3:8.1f}us eq={eq:.1e} er={er:.1e} orth={orth:.1e} "
-                   f"flag={flag} stats={st}")
+        out.append(f"{ {0: 'auto', 3: 'chain', 1: 'hh'}[method]:5s} {t*1e3:8.1f}us eq={eq:.1e} er={er:.1e} "
+                   f"orth={orth:.1e} flag={flag} stats={st}")
     print(f"{name:>22s}: " + " | ".join(out), flush=True)
 
 
@@ -107,4 +107,17 @@ if os.environ.get("CQ_PHASES"):
             for c in range((n + 31) // 32):
                 print(f"   cluster CTA {c:2d}: " + ", ".join(
                     f"{a}={b:.1f}" for a, b in zip(["A", "bar1", "B", "bar2", "C"], cl[5 * c:5 * c + 5])))
+    names_s = ["gram1+bar", "reduce1+bar", "factor1", "tri+gram2+bar", "reduce2+bar", "factor2", "R", "final tri"]
+    for m, n in [(1000, 40), (4000, 100), (64, 64), (100, 33), (50, 1), (256, 100)]:
+        x = D.empty_matrix(m, n, dev)
+        x.normal_()
+        r = D.empty_matrix(n, n, dev)
+        D.householder_qr_(ctx, x, r)
+        torch.cuda.synchronize()
+        ph.zero_()
+        x.normal_()
+        D.householder_qr_(ctx, x, r)
+        torch.cuda.synchronize()
+        v = [t / 1e3 for t in ph.tolist()[16:24]]
+        print(f"{m}x{n} single-launch phases (us): " + ", ".join(f"{a}={b:.1f}" for a, b in zip(names_s, v)))
     ctx.lib.pbq_debug_qr_hooks(ctx.handle, None, None, None)

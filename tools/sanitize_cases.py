@@ -4,12 +4,15 @@ gpurun call).  Sizes are tiny: the sanitizers slow kernels by 10-1000x.
 
   python tools/sanitize_cases.py [case ...]
 
-Cases: pipeline (config-1 shape PbP-QLP: sketch, TMA GEMMs, cooperative
-Cholesky-QR factor kernel, second stage), householder (the blocked
+Cases: pipeline (config-1 shape PbP-QLP: sketch, TMA GEMMs with the TMEM
+accumulator fold, the single-launch Cholesky-QR2 kernel, second stage),
+chain (the multi-launch Cholesky-QR2: split-K Gram with its cooperative slice
+sum, cooperative factor kernel, triangular products), householder (the blocked
 cooperative Householder QR), shifted (shifted Cholesky-QR3 route),
 cpqr_cluster / cpqr_grid (the pivot kernels), exchange (virtual-rank p2p
 scatter GEMM / slice reduce / waits, G = 2), residual (fused residual GEMM),
-svd (the Jacobi SVD core, when built)."""
+svd (the preconditioned Jacobi SVD: QR chains, register cluster kernel,
+GEMMs), svd_grid (the cooperative L2-resident Jacobi kernel)."""
 import os
 import sys
 
@@ -28,6 +31,17 @@ def pipeline(dev):
     a = workloads.make_cfg1(0)
     f = pbp_qlp(a, 40, q=1, seed=1)
     print("pipeline ok", float(np.abs(np.diag(f.l))[0]))
+
+
+def chain(dev):
+    ctx = D.context(dev)
+    ctx.set_qr_method(ctx.QR_CHOLQR_CHAIN)
+    try:
+        a = np.random.default_rng(8).standard_normal((900, 700))
+        f = pbp_qlp(a, 160, q=1, seed=4)
+    finally:
+        ctx.set_qr_method(ctx.QR_AUTO)
+    print("chain ok", float(np.abs(np.diag(f.l))[0]))
 
 
 def householder(dev):
@@ -100,9 +114,20 @@ def svd(dev):
     print("svd ok")
 
 
-CASES = {"pipeline": pipeline, "householder": householder, "shifted": shifted,
+def svd_grid(dev):
+    os.environ["PBQ_JACOBI_L2"] = "1"
+    try:
+        m = torch.from_numpy(np.random.default_rng(9).standard_normal((40, 50))).to(dev)
+        D.jacobi_svd(D.context(dev), D.as_kernel_operand(m), precondition=False)
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("PBQ_JACOBI_L2", None)
+    print("svd_grid ok")
+
+
+CASES = {"pipeline": pipeline, "chain": chain, "householder": householder, "shifted": shifted,
          "cpqr_cluster": lambda dev: cpqr(dev, True), "cpqr_grid": lambda dev: cpqr(dev, False),
-         "exchange": exchange, "residual": residual, "svd": svd}
+         "exchange": exchange, "residual": residual, "svd": svd, "svd_grid": svd_grid}
 
 if __name__ == "__main__":
     dev = torch.device("cuda", 0)

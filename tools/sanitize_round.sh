@@ -10,7 +10,7 @@ mkdir -p $O
 python tools/sanitize_cases.py > $O/${TAG}_${TOOL}_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 EXTRA=""
 [ "$TOOL" = memcheck ] && EXTRA="--leak-check no"
-for c in pipeline householder shifted cpqr_cluster cpqr_grid exchange residual svd; do
+for c in pipeline chain householder shifted cpqr_cluster cpqr_grid exchange residual svd svd_grid; do
   echo "=== case $c ($TOOL)" >> $O/${TAG}_${TOOL}.txt
   timeout 1500 compute-sanitizer --tool $TOOL $EXTRA --report-api-errors no --print-limit 20 \
     python tools/sanitize_cases.py $c >> $O/${TAG}_${TOOL}.txt 2>&1

@@ -26,8 +26,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FP64_PEAK_TFLOPS = 37.0  # measured DMMA.8x8x4 burst peak, profiles/r01_fp64_peak.jsonl
-FP64_PEAK_SOURCE = "measured: tools/microbench/fp64_peak.cu DMMA m8n8k4 on this pool's B200 (profiles/r01_fp64_peak.jsonl); MEASURED_PEAKS.json has no FP64 entry"
+FP64_PEAK_TFLOPS = 37.17  # measured DMMA.8x8x4 peak at 1965 MHz, profiles/r02_fp64_peak.jsonl (clock record inside)
+FP64_PEAK_SOURCE = "measured: tools/microbench/fp64_peak.cu DMMA m8n8k4, 16 warps/SM, on this pool's B200 at a median 1965 MHz SM clock with no throttle reason (tools/fp64_peak_round.sh, profiles/r02_fp64_peak.jsonl); MEASURED_PEAKS.json has no FP64 entry"
 METRIC = "PbP-QLP GFLOP/s and % FP64 roofline at 20000x10000, d=256; 1/2/4/8 GPU scaling"
 
 

@@ -51,30 +51,6 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
-// The same copies with an L2 cache-policy operand (createpolicy): the thin
-// B operand (Φ, P̄, R⁻¹: re-read by every row tile) is loaded evict_last so
-// the streamed A does not push it out of L2 between its reuses.
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar,
-                                                 uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], "
-      "[%4], %5;\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                                 uint32_t bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
-      "%4}], [%5], %6;\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
-      : "memory");
-}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -255,12 +231,11 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
 #pragma unroll
       for (int h = 0; h < BK / 16; ++h) tma_load_2d(sa + h * (BM * 128), &pa.ta, k0 + 16 * h, m0, bar);
     }
-    const uint64_t pol_b = l2_policy_evict_last();
     if (pa.b3d) {
-      tma_load_3d_hint(sb, &pa.tb, 0, k0, n0 / 16, bar, pol_b);
+      tma_load_3d(sb, &pa.tb, 0, k0, n0 / 16, bar);
     } else {
 #pragma unroll
-      for (int j = 0; j < BN / 16; ++j) tma_load_2d_hint(sb + j * (BK * 128), &pa.tb, n0 + 16 * j, k0, bar, pol_b);
+      for (int j = 0; j < BN / 16; ++j) tma_load_2d(sb + j * (BK * 128), &pa.tb, n0 + 16 * j, k0, bar);
     }
     prod.flat = pflat + 1;
     if (++prod.k == prod.seg.ke) {

@@ -85,13 +85,13 @@ class HostMatrix:
             if t.dtype != torch.float64:
                 t = t.to(torch.float64)
             if not t.is_cuda:
-                t = t.to(dev, non_blocking=t.is_pinned())
+                out = _dev.empty_matrix(t.shape[0], t.shape[1], dev)
+                return _dev.h2d(t.contiguous(), out)
             return _dev.as_kernel_operand(t)
         dev = _dev.require_cuda(device)
         arr = self.array
         out = _dev.empty_matrix(arr.shape[0], arr.shape[1], dev)
-        out.copy_(torch.from_numpy(np.ascontiguousarray(arr)))
-        return out
+        return _dev.h2d(torch.from_numpy(np.ascontiguousarray(arr)), out)
 
 
 def to_device_matrix(m, name, device=None):

@@ -530,6 +530,10 @@ def try_capture_dist(runner, a, args, finish):
     "captured" or why it stays stream-ordered."""
     if runner.exchange != "nccl":
         return "stream-ordered: the p2p exchange's spin targets are host-side epochs"
+    import torch.distributed as dist
+
+    if dist.get_backend() != "nccl":  # the gloo validation mode: host-mediated collectives cannot be captured
+        return "stream-ordered: gloo collectives are host-mediated (validation mode)"
     try:
         runner.capture(a, seed=args.seed + 50)
         for _ in range(args.warmup):

@@ -428,9 +428,11 @@ def _checkin_plan(key, plan):
 
 
 def clear_plan_cache():
-    """Release the cached host-input plans (device memory of A and the factors)."""
+    """Release the cached host-input plans (device memory of A and the factors)
+    and the pinned staging rings of host-array copies."""
     with _PLAN_LOCK:
         _PLAN_CACHE.clear()
+    _dev.release_staging()
 
 
 def _to_host(t, kind, home):

@@ -186,6 +186,16 @@ def h2d(host, out):
     return out
 
 
+def release_staging():
+    """Free the pinned staging rings of h2d (they are re-created on demand)."""
+    with _stage_lock:
+        for bufs, evs in _stage.values():
+            for ev in evs:
+                if ev is not None:
+                    ev.synchronize()
+        _stage.clear()
+
+
 def workspace(nbytes, device):
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 

@@ -65,6 +65,15 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
+        # per-class split from a stream-ordered repeat with events around every kernel
+        ctx = getattr(run.be, "ctx", None)
+        by_class = None
+        if ctx is not None:
+            ctx.profile_begin(capacity=4096)
+            run.run(a, seed=11)
+            torch.cuda.synchronize()
+            by_class = {k: round(v[0], 3) for k, v in ctx.profile_end().items()}
+            run.finish()
         if n == 1:
             t1 = ms
         big = (q + 1) * n2 * d * 8
@@ -74,7 +83,7 @@ def main():
                 "per_rank_ms": round(ms, 3), "per_rank_tflops": round(flops / n / ms / 1e9, 2),
                 "comm_model_ms": round(comm_ms, 3), "predicted_ms": round(ms + comm_ms, 3),
                 "predicted_speedup": round(t1 / (ms + comm_ms), 2), "bw_bus_gbs": BW_BUS / 1e9,
-                "graph": "captured", "note": "one rank of an N-GPU job on one GPU (world-1 NCCL); model, not a measurement"}
+                "graph": "captured", "class_ms_stream_ordered": by_class, "note": "one rank of an N-GPU job on one GPU (world-1 NCCL); model, not a measurement"}
         print(json.dumps(line), flush=True)
         del run, a
         torch.cuda.empty_cache()

@@ -359,10 +359,12 @@ struct GemmPlan {
 GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K, bool tri_b = false, bool allow_small = true) {
   GemmPlan p;
   const int bk = 32;
-  if (N <= 64) {
+  if (allow_small && M <= 1024 && gemm_use_tma() && !small_tiles_off()) {
+    // small products (any N): 64×64 tiles — 2–4× the tiles of 128×64/128×128,
+    // short fix-up chains (1000×40×1000: 30 → 19 µs, tools/gemm_small_probe.py)
+    p.bm = 64; p.bn = 64;
+  } else if (N <= 64) {
     p.bm = 128; p.bn = 64;
-  } else if (allow_small && M <= 1024 && gemm_use_tma() && !small_tiles_off()) {
-    p.bm = 64; p.bn = 64;  // small products: 4× the tiles, short fix-up chains
   } else {
     p.bm = 128; p.bn = 128;
   }
@@ -387,7 +389,15 @@ GemmPlan gemm_plan(const pbq_ctx* ctx, long M, long N, long K, bool tri_b = fals
     }
     p.total /= p.group;
   }
-  p.grid = int(std::min<long>(ctx->sms / p.group, p.total)) * p.group;
+  // at least two k-block units per CTA: a product with fewer units than 2·SMs
+  // runs on fewer CTAs with half the fix-up partials (100×100×100 9.2 → 8.4 µs,
+  // 256³ 13.5 → 10.8 µs); large products are unaffected.  PBQ_GEMM_MIN_UNITS
+  // overrides (A/B).
+  static const long min_units = [] {
+    const char* e = getenv("PBQ_GEMM_MIN_UNITS");
+    return e ? std::max(1L, atol(e)) : 2L;
+  }();
+  p.grid = int(std::min<long>(ctx->sms / p.group, ceil_div(p.total, min_units))) * p.group;
   return p;
 }
 

@@ -544,6 +544,9 @@ def try_capture_dist(runner, a, args, finish):
         import torch
 
         torch.cuda.synchronize()
+        # the capture's invalidation error is still this thread's CUDA
+        # last-error: clear it, or the next stream-ordered launch reports it
+        getattr(runner.be, "ctx", None) and runner.be.ctx.clear_error()
         return f"stream-ordered: capture failed ({type(exc).__name__}: {str(exc)[:120]})"
 
 

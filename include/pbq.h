@@ -52,6 +52,12 @@ typedef struct pbq_ctx pbq_ctx;
 int pbq_ctx_create(int device, pbq_ctx** out);
 int pbq_ctx_destroy(pbq_ctx* ctx);
 const char* pbq_last_error(const pbq_ctx* ctx);
+/* Reset this thread's CUDA last-error state, returning the cudaError_t that
+ * was pending (0 if none).  For hosts that recover from a failed stream
+ * capture: the capture's invalidation error would otherwise surface in the
+ * next launch check of an unrelated pbq_* call.  Sticky errors (a faulted
+ * context) are not cleared by this and keep failing every call. */
+int pbq_clear_error(pbq_ctx* ctx);
 int pbq_ctx_sm_count(const pbq_ctx* ctx);
 /* Kernel launches enqueued by this context since creation (evidence for the
  * bench's "gpu_launches" count). */

@@ -63,6 +63,7 @@ EXPORTED = (
     "pbq_set_p2p_timeout_ms",
     "pbq_jacobi_svd",
     "pbq_jacobi_svd_workspace_bytes",
+    "pbq_clear_error",
 )
 
 c_i64 = ctypes.c_int64
@@ -127,6 +128,7 @@ _SIGS = {
     "pbq_p2p_sum": ([c_p, c_p, c_i64, c_i32, c_i64, c_p, c_p, ctypes.c_uint32, c_p, c_p], ctypes.c_int),
     "pbq_p2p_wait": ([c_p, c_p, ctypes.c_uint32, c_p, c_p], ctypes.c_int),
     "pbq_set_p2p_timeout_ms": ([c_p, c_i64], ctypes.c_int),
+    "pbq_clear_error": ([c_p], ctypes.c_int),
     "pbq_jacobi_svd": ([c_p, c_i64, c_i64, c_p, c_i64, c_i32, c_p, c_p, c_i64, c_p, c_i64, c_p, c_p, c_sz, c_p],
                        ctypes.c_int),
     "pbq_jacobi_svd_workspace_bytes": ([c_p, c_i64, c_i64, c_i32, ctypes.POINTER(c_sz)], ctypes.c_int),

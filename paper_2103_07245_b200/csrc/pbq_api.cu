@@ -1570,6 +1570,15 @@ int pbq_profile_end(pbq_ctx* ctx, double* ms_by_class, int32_t* launches_by_clas
 }
 
 const char* pbq_last_error(const pbq_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+// Reset this thread's CUDA last-error state (e.g. after a failed stream
+// capture, whose invalidation error would otherwise be reported by the next
+// launch check of an unrelated call).  Returns the error that was pending.
+int pbq_clear_error(pbq_ctx* ctx) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  const cudaError_t e = cudaGetLastError();
+  ctx->err[0] = 0;
+  return int(e);
+}
 int pbq_ctx_sm_count(const pbq_ctx* ctx) { return ctx ? ctx->sms : 0; }
 int64_t pbq_ctx_launch_count(const pbq_ctx* ctx) { return ctx ? ctx->launches : 0; }
 

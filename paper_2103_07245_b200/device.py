@@ -46,6 +46,12 @@ class Context:
 
     QR_AUTO, QR_HOUSEHOLDER, QR_CHOLQR_NOSERIES, QR_CHOLQR_CHAIN = 0, 1, 2, 3
 
+    def clear_error(self):
+        """Reset the CUDA last-error state (after a failed stream capture);
+        returns the pending cudaError_t code (0: none)."""
+        with self.lock:
+            return int(self.lib.pbq_clear_error(self.handle))
+
     def set_qr_method(self, method):
         """0: Cholesky-QR2 with on-device Householder fallback (default);
         1: Householder kernel only; 2: as 0 with the blocked Cholesky in the

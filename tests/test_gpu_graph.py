@@ -53,3 +53,25 @@ def test_graph_replay_matches_oracle(cuda):
     tol = conditioning_tolerance(ref["l"], strict=1e-10)
     assert np.all(column_relative_error(plan.Q.cpu().numpy(), ref["q"]) <= tol)
     assert np.all(column_relative_error(plan.P.cpu().numpy(), ref["p"]) <= tol)
+
+
+def test_clear_error_after_failed_capture(cuda):
+    """A stream capture invalidated by an uncapturable operation leaves its
+    error as the thread's CUDA last-error; pbq_clear_error resets it so the
+    next library call (stream-ordered) runs (bench.py's N > 1 capture
+    fallback relies on this)."""
+    from paper_2103_07245_b200 import device as D
+
+    ctx = D.context(cuda)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream(cuda)
+    out = torch.empty(64, 8, dtype=torch.float64, device=cuda)
+    with pytest.raises(Exception):
+        with torch.cuda.graph(g, stream=s):
+            D.gaussian(ctx, 64, 8, 1, cuda, out=out)
+            torch.cuda.synchronize()  # illegal while capturing: invalidates the capture
+    torch.cuda.synchronize()
+    ctx.clear_error()
+    phi = D.gaussian(ctx, 64, 8, 1, cuda)
+    torch.cuda.synchronize()
+    assert torch.isfinite(phi).all()

@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
   double* sC = pairs + 2 * CQ_BLK;
   double* sT = pairs + 3 * CQ_BLK;
   __shared__ int s_ok;
+  __shared__ double s_dmax, s_dmin;  // running max / min |R_ii| (pass-1 early κ guard)
   __shared__ __align__(16) double s_rowbuf[2 * CQ_RB2];
   if (p.fallback && __ldcg(p.fallback) != 0) return;  // uniform: written by an earlier launch
   if (p.route && __ldcg(p.route) == 0) return;
@@ -643,6 +644,32 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
     if (!s_ok) {  // identical in every CTA (same data, same code): all leave together
       if (blockIdx.x == 0 && tid == 0) fail_all();
       return;
+    }
+    if (pass1 && !p.shift_mode) {
+      // early κ guard: κ₁(R₁) = ‖R₁‖₁‖R₁⁻¹‖₁ ≥ max|R_ii| / min|R_jj|, so once the
+      // diagonal seen so far spans more than kappa_max the final guard must fail:
+      // leave now instead of finishing the factorization (the shifted route or
+      // the Householder kernel takes over at once; identical in every CTA)
+      if (warp == 0) {
+        const long row = long(k) * 32 + (tid & 31);
+        const double dgl = row < p.n ? fabs(sKK[(tid & 31) * CQ_LD + (tid & 31)]) : 0.0;
+        double mx = dgl, mn = row < p.n ? dgl : INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        }
+        if (tid == 0) {
+          s_dmax = k == 0 ? mx : fmax(s_dmax, mx);
+          s_dmin = k == 0 ? mn : fmin(s_dmin, mn);
+          s_ok = !(s_dmax > p.kappa_max * s_dmin);
+        }
+      }
+      __syncthreads();
+      if (!s_ok) {
+        if (blockIdx.x == 0 && tid == 0) fail_all();
+        return;
+      }
     }
     if (blockIdx.x == gridDim.x - 1) {  // the last CTA has the fewest items; CTA 0 carries (k+1, k+1)
       cq_store(p.R, np, k, k, sKK);

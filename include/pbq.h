@@ -95,7 +95,9 @@ int pbq_gemm_workspace_bytes(pbq_ctx* ctx, int64_t M, int64_t N, int64_t K, size
  * Householder kernel, all decided on the device; method 1 forces the
  * Householder kernel.  For n ≤ 128 and m ≤ 64·SMs the whole Cholesky-QR2
  * runs as one cooperative launch (redundant per-CTA n×n factorizations in
- * shared memory); method 3 forces the multi-launch chain instead. */
+ * shared memory), and for 128 < n ≤ 256 with m ≤ 1024 as another (the
+ * distributed factorization with the small products folded in); method 3
+ * forces the multi-launch chain instead. */
 int pbq_householder_qr(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, double* R,
                        int64_t ldr, int32_t want_q, int32_t* rank_flag, void* workspace,
                        size_t workspace_bytes, void* stream);

@@ -456,9 +456,12 @@ __device__ __forceinline__ void cq_inverse_final_item(const CqArgs& p, int k, in
 }
 
 
-__global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) {
-  pdl_trigger();  // a programmatically launched successor may start its prologue
-  extern __shared__ __align__(16) double sm[];
+// The factorization body: run by every CTA of a cooperative grid (the
+// factor kernel below, or the single-launch mid-size Cholesky-QR2 of
+// cholqr_mid_f64.cuh, which calls it between its own phases).  sm: the
+// CQ_SMEM_BYTES dynamic shared-memory block.  p.counter: a grid-barrier
+// counter used by this call only (zeroed before the launch).
+__device__ void cq_factor(const CqArgs& p, double* sm) {
   double* sKK = sm;           // R_kk
   double* sKI = sm + CQ_BLK;  // R_kk⁻¹
   double* sU = sm + 2 * CQ_BLK;
@@ -775,6 +778,12 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) 
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(CQ_THREADS, 1) cholqr_factor_kernel(CqArgs p) {
+  pdl_trigger();  // a programmatically launched successor may start its prologue
+  extern __shared__ __align__(16) double sm[];
+  cq_factor(p, sm);
 }
 
 }  // namespace pbq

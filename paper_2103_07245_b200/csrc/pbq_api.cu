@@ -21,6 +21,7 @@
 #include "gemm_tma_f64.cuh"
 #include "cholqr_f64.cuh"
 #include "cholqr_small_f64.cuh"
+#include "cholqr_mid_f64.cuh"
 #include "cpqr_f64.cuh"
 #include "qr_f64.cuh"
 #include "sketch.cuh"
@@ -908,16 +909,95 @@ int cs_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   return PBQ_OK;
 }
 
+// ------------------------------------------ single-launch, 128 < n ≤ 256 ----
+// cholqr_mid_f64.cuh: few rows (the d×d second stage at d = 256): the chain's
+// small GEMMs and launch gaps folded into one cooperative kernel around the
+// same distributed factorization.
+constexpr long CM_MAX_M = 1024;  // 2048×256: 230 µs against the chain's 192 (its TMA GEMMs win there)
+bool cm_eligible(const pbq_ctx* ctx, long m, long n) {
+  return (ctx->qr_method == PBQ_QR_AUTO || ctx->qr_method == PBQ_QR_CHOLQR_NOSERIES) && n > 32L * CS_MAX_NB &&
+         n <= 256 && m >= n && m <= CM_MAX_M;
+}
+int cm_grid(const pbq_ctx* ctx) { return int(std::min<long>(ctx->sms, 128)); }
+size_t cm_ws_bytes(const pbq_ctx* ctx, const QrPlan& hp, long m, long n) {
+  const long nb = ceil_div(n, 32), np = 32 * nb, nblk = nb * (nb + 1) / 2, nch = ceil_div(m, 32);
+  const size_t sq = align_up(size_t(np) * np * 8, 256);
+  return 256 + 7 * sq + align_up(2 * size_t(nb) * np * 8, 256) + align_up(size_t(m) * np * 8, 256) +
+         align_up(size_t(nch) * nblk * 1024 * 8, 256) + qr_ws_bytes(hp, n) + 1024;
+}
+
+int cm_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int32_t* rank_flag, void* ws,
+              size_t ws_bytes, cudaStream_t st) {
+  QrPlan hp;
+  PBQ_TRY(qr_plan(ctx, m, n, hp));
+  if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "qr: leading dimension too small");
+  const int nb = int(ceil_div(n, 32)), nblk = nb * (nb + 1) / 2;
+  const long np = 32L * nb, nch = ceil_div(m, 32);
+  const size_t sq = size_t(np) * np;
+  Carve cv(ws, ws_bytes);
+  // ctl: [0] fallback, [1] [2] factor barriers, [4..5] max|G₂ − I|, [8] kernel barrier, [48] Householder barrier
+  int* ctl = cv.take<int>(64);
+  double* X1 = cv.take<double>(sq);
+  double* X2 = cv.take<double>(sq);
+  const size_t zero_bytes = size_t(reinterpret_cast<char*>(X2 + sq) - reinterpret_cast<char*>(ctl));
+  double* G = cv.take<double>(sq);
+  double* R1 = cv.take<double>(sq);
+  double* R2 = cv.take<double>(sq);
+  double* T = cv.take<double>(sq);
+  double* colsum = cv.take<double>(2 * size_t(nb) * np);
+  double* Q1 = cv.take<double>(size_t(m) * np);
+  double* part = cv.take<double>(size_t(nch) * nblk * 1024);
+  const size_t hws_bytes = qr_ws_bytes(hp, n);
+  char* hws = cv.take<char>(hws_bytes);
+  if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  PBQ_CUDA(ctx, cudaMemsetAsync(ctl, 0, zero_bytes, st));
+  CmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.m = m; a.n = n; a.np = np; a.nb = nb; a.A = A; a.lda = lda; a.Q1 = Q1; a.part = part;
+  a.counter = reinterpret_cast<unsigned int*>(ctl + 8);
+  a.fallback = ctl;
+  a.emax = reinterpret_cast<unsigned long long*>(ctl + 4);
+  CqArgs f;
+  memset(&f, 0, sizeof(f));
+  f.nb = nb; f.n = n; f.np = np; f.m = m;
+  f.G = G; f.T = T; f.fallback = ctl;
+  f.emax = a.emax; f.colsum = colsum; f.stats = ctx->cq_stats; f.fail_stats = ctx->cq_stats;
+  f.kappa_max = CQ_KAPPA_MAX;
+  f.phase_ns = ctx->qr_phase_ns;
+  f.allow_series = ctx->qr_method != PBQ_QR_CHOLQR_NOSERIES;
+  f.chol_1warp = 0;
+  a.f1 = f;
+  a.f1.pass = 1; a.f1.R = R1; a.f1.X = X1; a.f1.counter = reinterpret_cast<unsigned int*>(ctl + 1);
+  a.f2 = f;
+  a.f2.pass = 2; a.f2.R = R2; a.f2.X = X2; a.f2.R1 = R1; a.f2.Rout = R; a.f2.ldr = ldr; a.f2.rank_flag = rank_flag;
+  a.f2.counter = reinterpret_cast<unsigned int*>(ctl + 2);
+  const int grid = cm_grid(ctx);
+  {
+    ProfScope ps(ctx->prof, st, 1);
+    ProfSuppress quiet(ctx->prof);
+    PBQ_CUDA(ctx, ensure_smem(ctx, reinterpret_cast<const void*>(&cholqr_mid_kernel), CQ_SMEM_BYTES));
+    void* args[] = {&a};
+    PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&cholqr_mid_kernel), dim3(grid),
+                                              dim3(CQ_THREADS), args, CQ_SMEM_BYTES, st));
+    ctx->launches += 1;
+    PBQ_TRY(hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, ctl,
+                      reinterpret_cast<unsigned int*>(ctl + 48)));
+  }
+  return PBQ_OK;
+}
+
 size_t qr_any_ws_bytes(const pbq_ctx* ctx, const QrPlan& hp, long m, long n) {
   if (ctx->qr_method == PBQ_QR_HOUSEHOLDER) return qr_ws_bytes(hp, n);
   size_t b = cq_ws_bytes(cq_plan(ctx, m, n), hp, m, n);
   if (cs_eligible(ctx, m, n)) b = std::max(b, cs_ws_bytes(ctx, hp, m, n));
+  if (cm_eligible(ctx, m, n)) b = std::max(b, cm_ws_bytes(ctx, hp, m, n));
   return b;
 }
 
 int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int want_q, int32_t* rank_flag,
               void* ws, size_t ws_bytes, cudaStream_t st) {
   if (want_q && cs_eligible(ctx, m, n)) return cs_launch(ctx, m, n, A, lda, R, ldr, rank_flag, ws, ws_bytes, st);
+  if (want_q && cm_eligible(ctx, m, n)) return cm_launch(ctx, m, n, A, lda, R, ldr, rank_flag, ws, ws_bytes, st);
   if (ctx->qr_method != PBQ_QR_HOUSEHOLDER && want_q) return cq_launch(ctx, m, n, A, lda, R, ldr, rank_flag, ws, ws_bytes, st);
   return hh_launch(ctx, m, n, A, lda, R, ldr, want_q, rank_flag, ws, ws_bytes, st, nullptr);
 }

@@ -108,7 +108,8 @@ def test_pipeline_guarded(guarded, cuda, method, shape, d, q):
         ctx.set_qr_method(ctx.QR_AUTO)
 
 
-@pytest.mark.parametrize("m,n", [(50, 1), (100, 33), (1000, 40), (4000, 100), (300, 128), (8192, 512)])
+@pytest.mark.parametrize("m,n", [(50, 1), (100, 33), (1000, 40), (4000, 100), (300, 128), (256, 256), (1000, 200),
+                                 (8192, 512)])
 def test_qr_guarded(guarded, cuda, m, n):
     """QR through device.householder_qr_ (single-launch kernel, chain, shifted route at n ≥ 384)."""
     from paper_2103_07245_b200 import device as D

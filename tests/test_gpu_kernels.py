@@ -246,6 +246,11 @@ def test_cholqr_path_and_guard(cuda, family):
         ("gaussian, no series", rng.standard_normal((3000, 96)), [1, 0, 0, 0], 2),
         ("kappa 1e5, no series", (u * np.logspace(0, -5, 96)) @ v.T, [1, 0, 0, 0], 2),
         ("300x257, no series", rng.standard_normal((300, 257)), [1, 0, 0, 0], 2),
+        # 128 < n ≤ 256 with few rows: the mid-size single launch (cholqr_mid_f64.cuh) under "auto"
+        ("mid 400x200", rng.standard_normal((400, 200)), [1, 0, 1, 0], 0),
+        ("mid 256x256, no series", rng.standard_normal((256, 256)), [1, 0, 0, 0], 2),
+        ("mid kappa 1e12", (np.linalg.qr(rng.standard_normal((400, 160)))[0] * np.logspace(0, -12, 160))
+         @ np.linalg.qr(rng.standard_normal((160, 160)))[0].T, [0, 1, 0, 0], 0),
     ]
     for name, x, expect, method in cases:
         if family == "chain" and method == 0:

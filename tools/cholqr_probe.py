@@ -120,4 +120,17 @@ if os.environ.get("CQ_PHASES"):
         torch.cuda.synchronize()
         v = [t / 1e3 for t in ph.tolist()[16:24]]
         print(f"{m}x{n} single-launch phases (us): " + ", ".join(f"{a}={b:.1f}" for a, b in zip(names_s, v)))
+    names_m = ["gram1+sums", "factor1", "Q1", "gram2+sums", "factor2", "Q"]
+    for m, n in [(256, 256), (200, 160), (1000, 200)]:
+        x = D.empty_matrix(m, n, dev)
+        x.normal_()
+        r = D.empty_matrix(n, n, dev)
+        D.householder_qr_(ctx, x, r)
+        torch.cuda.synchronize()
+        ph.zero_()
+        x.normal_()
+        D.householder_qr_(ctx, x, r)
+        torch.cuda.synchronize()
+        v = [t / 1e3 for t in ph.tolist()[24:30]]
+        print(f"{m}x{n} mid-size single-launch phases (us): " + ", ".join(f"{a}={b:.1f}" for a, b in zip(names_m, v)))
     ctx.lib.pbq_debug_qr_hooks(ctx.handle, None, None, None)

@@ -1323,6 +1323,7 @@ int jacobi_core_launch(pbq_ctx* ctx, long n, long L, const double* X, long ldx, 
   a.ldz = a.V + (a.V & 1);
   a.status = status;
   a.max_sweeps = 60;  // dgesvj's NSWEEP is 30 with de Rijk pivoting; plain cyclic order gets twice that
+  a.tphase = ctx->qr_phase_ns ? ctx->qr_phase_ns + 40 : nullptr;  // debug hooks: [40..44) round phases
   a.tol = sqrt(double(L)) * 1.1102230246251565e-16;      // √L·u (dgesvj's CTOL)
   Carve cv(ws, ws_bytes);
   a.Z = cv.take<double>(size_t(a.np) * a.ldz);

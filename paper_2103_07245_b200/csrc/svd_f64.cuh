@@ -68,6 +68,8 @@ struct JacArgs {
   int* status;         // [0] sweeps used, [1] 1 if not converged within max_sweeps
   int max_sweeps;
   double tol;
+  unsigned long long* tphase;  // optional profiling (register kernel, middle warp): cycles in
+                               // [rotate, send, wait], rounds
 };
 
 __device__ __forceinline__ void jac_cluster_sync() {
@@ -157,10 +159,17 @@ __device__ __forceinline__ bool jac_converged(int rot, double mx_aapq, double mx
 // Register-resident kernel.  Launch: grid = C CTAs = one cluster of C,
 // JAC_WARPS warps each, C·JAC_WARPS ≥ P = np/2; dynamic shared memory =
 // jac_reg_smem(VPL).  Hand-over between neighbouring warps is point to
-// point: each mailbox slot has an mbarrier (32 arrivals: every lane of the
-// sender arrives after its own stores, with release at cluster scope when
-// the receiver is in another CTA), and the receiver waits on it — no
-// cluster-wide barrier per round.  Slots are double-buffered by round
+// point: each mailbox slot has an mbarrier and the receiver waits on it — no
+// cluster-wide barrier per round.  A slot fed from the same CTA completes on
+// 32 arrivals (every lane of the sender, release at CTA scope, after its
+// stores).  A slot fed from a neighbouring CTA completes on transaction
+// bytes: the sender pushes the vector with st.async (each store completes
+// its bytes on the remote mbarrier) and never waits, and the receiver arms
+// the phase with one arrive.expect_tx.  (The first version stored with
+// st.shared::cluster and arrived with release at cluster scope: the release
+// waited for the remote stores, 1421 of a round's ~3000 cycles at n = 256,
+// `tools/svd_probe.py --phases`.)  Slot layout: lane ℓ's elements k, k+1 (k
+// even) are the 16 bytes at 2·(32·(k/2) + ℓ), one v2 store each.  Slots are double-buffered by round
 // parity; the data dependencies of the schedule make reuse safe (a sender
 // writes a slot again only after receiving its neighbour's next vector,
 // which the neighbour sends after consuming the slot's previous content).
@@ -174,6 +183,16 @@ __device__ __forceinline__ void jac_st_remote(uint32_t addr, double v) {
 }
 __device__ __forceinline__ void jac_arrive_remote(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+// Asynchronous remote store of 16 bytes that completes `bytes` of the remote
+// mbarrier's transaction count (no release fence, no arrival by the sender).
+__device__ __forceinline__ void jac_st_async2(uint32_t addr, double a, double b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
+               "d"(a), "d"(b), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void jac_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void jac_arrive_local(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
@@ -207,7 +226,15 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
   auto box_off = [&](int lq, int s, int par) { return ((size_t(par) * JAC_WARPS + lq) * 2 + s) * slot_d; };
   auto bar_of = [&](int lq, int s, int par) { return bars + (par * JAC_WARPS + lq) * 2 + s; };
 
-  if (threadIdx.x < 4 * JAC_WARPS) mbar_init(bars + threadIdx.x, 32);
+  // barrier (par, lq, s): slot 0 (T_in) of warp q is fed by warp q−1 (warp 0 for
+  // q = 1), slot 1 (B_in) by warp q+1 — from another CTA when lq is 0 / last
+  auto remote_fed = [&](int q, int lq, int s) {
+    return s == 0 ? (lq == 0 && q >= 2) : (lq == JAC_WARPS - 1 && q + 1 < P);
+  };
+  if (threadIdx.x < 4 * JAC_WARPS) {
+    const int lq = (threadIdx.x >> 1) % JAC_WARPS, sl = threadIdx.x & 1;
+    mbar_init(bars + threadIdx.x, remote_fed(me * JAC_WARPS + lq, lq, sl) ? 1 : 32);
+  }
   mbar_fence_init();
   if (C > 1)
     jac_cluster_sync();  // every CTA's barriers exist before any remote arrival
@@ -229,13 +256,27 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
     if (cta == me) {
       double* d = jsm + off;
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) d[32 * k + lane] = v[k];
+      for (int k = 0; k < VPL; k += 2)
+        *reinterpret_cast<double2*>(d + 2 * (32 * (k >> 1) + lane)) = make_double2(v[k], v[k + 1]);
       jac_arrive_local(smem_u32(bar_of(lq, s, par)));
     } else {
       const uint32_t d = jac_mapa(smem_u32(jsm + off), cta);
+      const uint32_t rb = jac_mapa(smem_u32(bar_of(lq, s, par)), cta);
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) jac_st_remote(d + 8u * (32 * k + lane), v[k]);
-      jac_arrive_remote(jac_mapa(smem_u32(bar_of(lq, s, par)), cta));
+      for (int k = 0; k < VPL; k += 2) jac_st_async2(d + 16u * (32 * (k >> 1) + lane), v[k], v[k + 1], rb);
+    }
+  };
+  // wait for slot s of this warp (round parity par, barrier phase ph) and read it
+  auto receive = [&](double (&v)[VPL], int s, int par, unsigned ph) {
+    const uint32_t b = smem_u32(bar_of(lw, s, par));
+    if (remote_fed(w, lw, s) && lane == 0) jac_arrive_expect_tx(b, uint32_t(32 * VPL * sizeof(double)));
+    jac_wait(b, ph);
+    const double* mb = jsm + box_off(lw, s, par);
+#pragma unroll
+    for (int k = 0; k < VPL; k += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(mb + 2 * (32 * (k >> 1) + lane));
+      v[k] = t.x;
+      v[k + 1] = t.y;
     }
   };
   long R = 0;  // rounds so far (all sweeps): slot parity R&1, barrier phase (R>>1)&1
@@ -246,12 +287,16 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
     for (int r = 0; r < p.np - 1; ++r, ++R) {
       const int par = int(R & 1);
       const unsigned phase = unsigned((R >> 1) & 1);
+      const bool timed = p.tphase && w == P / 2;
+      long long c0 = 0, c1 = 0, c2 = 0;
+      if (timed) c0 = clock64();
       if (active) {
         double aapq, sinj;
         if (jac_rotate<VPL>(x, y, p.L, p.tol, aapq, sinj)) ++rot;
         mx_aapq = fmax(mx_aapq, aapq);
         mx_sin = fmax(mx_sin, sinj);
       }
+      if (timed) c1 = clock64();
       if (active && P > 1) {
         // T' → warp w+1 (1 ≤ w ≤ P−2) or kept as B (w = P−1);
         // B' → warp w−1 (w ≥ 1) or warp 1's T slot (w = 0)
@@ -260,22 +305,22 @@ __global__ void __launch_bounds__(JAC_WARPS * 32, 1) jacobi_reg_kernel(JacArgs p
           send(y, w - 1, 1, par);
         else
           send(y, 1, 0, par);
+        if (timed) c2 = clock64();
         // B_in: own T' (w = P−1), else warp w+1's B';
         // T_in: own T' (w = 0), warp 0's B' (w = 1), warp w−1's T' (w ≥ 2)
         if (w == P - 1) {
 #pragma unroll
           for (int k = 0; k < VPL; ++k) y[k] = x[k];
         } else {
-          jac_wait(smem_u32(bar_of(lw, 1, par)), phase);
-          const double* mb = jsm + box_off(lw, 1, par);
-#pragma unroll
-          for (int k = 0; k < VPL; ++k) y[k] = mb[32 * k + lane];
+          receive(y, 1, par, phase);
         }
-        if (w >= 1) {
-          jac_wait(smem_u32(bar_of(lw, 0, par)), phase);
-          const double* mt = jsm + box_off(lw, 0, par);
-#pragma unroll
-          for (int k = 0; k < VPL; ++k) x[k] = mt[32 * k + lane];
+        if (w >= 1) receive(x, 0, par, phase);
+        if (timed && lane == 0) {
+          const long long c3 = clock64();
+          atomicAdd(p.tphase, (unsigned long long)(c1 - c0));
+          atomicAdd(p.tphase + 1, (unsigned long long)(c2 - c1));
+          atomicAdd(p.tphase + 2, (unsigned long long)(c3 - c2));
+          atomicAdd(p.tphase + 3, 1ull);
         }
       }
     }

@@ -46,5 +46,33 @@ def main():
                       f"|YYᵀ-I| {yo:.1e} {ms:.3f} ms", flush=True)
 
 
+def phases():
+    """Where a register-kernel round goes (middle warp, clock64): rotate /
+    send / wait cycles per round, via the debug hooks."""
+    import ctypes
+    dev = torch.device("cuda", 0)
+    ctx = D.context(dev)
+    fb = torch.zeros(1, dtype=torch.int32, device=dev)
+    ph = torch.zeros(128, dtype=torch.int64, device=dev)
+    bw = torch.zeros(1024, dtype=torch.int64, device=dev)
+    ctx.lib.pbq_debug_qr_hooks(ctx.handle, ctypes.c_void_p(fb.data_ptr()), ctypes.c_void_p(ph.data_ptr()),
+                               ctypes.c_void_p(bw.data_ptr()))
+    for n, acc in ((256, True), (256, False), (128, True)):
+        x = D.as_kernel_operand(torch.from_numpy(graded(n, n, 8, 2 * n)).to(dev))
+        D.jacobi_svd(ctx, x, accumulate=acc, precondition=False)
+        torch.cuda.synchronize()
+        ph.zero_()
+        D.jacobi_svd(ctx, x, accumulate=acc, precondition=False)
+        torch.cuda.synchronize()
+        rot, send, wait, rounds = ph.tolist()[40:44]
+        rounds = max(rounds, 1)
+        print(f"register kernel n={n} acc={acc}: per round rotate {rot / rounds:.0f}, send {send / rounds:.0f}, "
+              f"wait+receive {wait / rounds:.0f} cycles ({rounds} rounds)", flush=True)
+    ctx.lib.pbq_debug_qr_hooks(ctx.handle, None, None, None)
+
+
 if __name__ == "__main__":
-    main()
+    if "--phases" in sys.argv:
+        phases()
+    else:
+        main()

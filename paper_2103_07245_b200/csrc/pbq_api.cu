@@ -512,6 +512,11 @@ int hh_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   a.phase_ns = ctx->qr_phase_ns;
   a.bar_wait_ns = ctx->qr_bar_wait_ns;
   a.run_if = run_if;
+  static const bool slow_panels = getenv("PBQ_QR_SLOW_PANELS") != nullptr;  // A/B switch
+  a.slow_panels = slow_panels ? 1 : 0;
+  static const double fast_ratio =  // A/B switch
+      getenv("PBQ_QR_FAST_RATIO") ? atof(getenv("PBQ_QR_FAST_RATIO")) : QR_FAST_DIAG_RATIO;
+  a.fast_ratio = fast_ratio;
   if (!cv.ok()) return fail(ctx, PBQ_ERR_PARAM, "qr: workspace too small (%zu < %zu)", ws_bytes, cv.off);
   if (!zeroed_counter) PBQ_CUDA(ctx, cudaMemsetAsync(a.counter, 0, sizeof(unsigned int), st));
   PBQ_CUDA(ctx, ensure_smem(ctx, reinterpret_cast<const void*>(&qr_tall_kernel), pl.smem));

@@ -23,8 +23,8 @@
 // small matrix products, so the per-row work becomes 32×32 matrix products.
 // A panel takes the fallback — column-by-column Householder (dlarfg
 // convention, one grid reduction per column) — when it is the last, partial
-// panel or when diag(R₁) shows it is numerically rank deficient / worse
-// conditioned than 1e4; every CTA takes the same decision from the same
+// panel or when diag(R₁) shows it is numerically rank deficient / its
+// min/max diagonal ratio is below 0.1 (QR_FAST_DIAG_RATIO); every CTA takes the same decision from the same
 // reduced Gram matrix.  The trailing update A2 ← (I − V Tᵀ Vᵀ) A2 and the
 // backward Q formation Q ← (I − V T Vᵀ) Q are GEMM-shaped: per-CTA partials
 // of VᵀX, a fixed-order slice reduction, then a row-local update.  All
@@ -49,7 +49,12 @@ constexpr int QR_CW = 128;                // trailing columns per staged tile
 constexpr int QR_XLD = QR_CW + 4;         // leading dimension of staged tiles
 constexpr int QR_TILE_DOUBLES = QR_NB * QR_XLD;  // one staged tile (32 rows × 128 columns)
 constexpr double QR_RANK_RTOL = 1e-14;    // RANK_DEFICIENCY_RTOL, linalg.py:48
-constexpr double QR_FAST_DIAG_RATIO = 1e-4;  // min/max diag(R₁) accepted by the fast path
+// min/max diag(R₁) a panel needs for the fast path.  The reconstructed
+// reflectors lose orthogonality roughly with that ratio's inverse
+// (tools/_hh_orth_probe.py, 129×129 at κ = 1e13: |QᵀQ − I| 3.3e-9 at 1e-4,
+// 1.8e-12 at 1e-3, 1.1e-15 at 1e-1 — LAPACK's level); well-conditioned
+// panels (random ones sit near 0.5) keep the fast path.
+constexpr double QR_FAST_DIAG_RATIO = 1e-1;
 constexpr int QR_NSMALL = 12;             // 32×32 scratch matrices in shared memory
 
 struct QrArgs {
@@ -75,6 +80,8 @@ struct QrArgs {
   unsigned long long* phase_ns;  // may be null: CTA-0 time per phase (profiling)
   unsigned long long* bar_wait_ns;  // may be null: per-CTA grid-barrier spin time (profiling)
   const int* run_if;  // may be null; else the kernel runs only when *run_if != 0 (Cholesky-QR fallback)
+  int slow_panels;    // 1: every panel by the column-by-column path (A/B)
+  double fast_ratio;  // min/max diag(R₁) a panel needs for the fast path
 };
 
 __device__ __forceinline__ unsigned long long qr_now() {
@@ -824,7 +831,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
       }
       __syncthreads();
       const double ratio1 = sm_chol(R1, vec);
-      fast = ratio1 > QR_FAST_DIAG_RATIO;
+      fast = ratio1 > p.fast_ratio && !p.slow_panels;
       QR_PHASE(1);
       if (fast) {
         sm_tri_inv_upper<false, false>(R1i, R1, Z);

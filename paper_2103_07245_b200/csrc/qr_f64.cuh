@@ -55,6 +55,12 @@ constexpr double QR_RANK_RTOL = 1e-14;    // RANK_DEFICIENCY_RTOL, linalg.py:48
 // 1.8e-12 at 1e-3, 1.1e-15 at 1e-1 — LAPACK's level); well-conditioned
 // panels (random ones sit near 0.5) keep the fast path.
 constexpr double QR_FAST_DIAG_RATIO = 1e-1;
+// ... and at least this many rows below its top: a short panel's Q₁ is most
+// of its Q, and the reconstruction lost orthogonality there too (129×129 with
+// a clustered spectrum: 4.3e-13 with all diag ratios ≥ 0.1,
+// tests/test_gpu_fuzz_qr.py); the last panels of square-ish inputs are cheap
+// by the column-by-column path anyway.
+constexpr long QR_FAST_MIN_ROWS = 4 * 32;
 constexpr int QR_NSMALL = 12;             // 32×32 scratch matrices in shared memory
 
 struct QrArgs {
@@ -806,7 +812,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_tall_kernel(QrArgs p) {
     const long ra = lmax(r0, k);  // first active owned row
     double* gdst = p.wpart + size_t(blockIdx.x) * QR_NB * qr_ldw(n);
     bool fast = false;
-    if (jb == QR_NB) {
+    if (jb == QR_NB && p.m - k >= QR_FAST_MIN_ROWS && !p.slow_panels) {
       // ---- pass 1: Gram partial (+ publish the pivot rows)
       double acc[2] = {0.0, 0.0};
       for (long cs = ra; cs < r1; cs += rch) {

@@ -103,6 +103,26 @@ int pbq_householder_qr(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t ld
                        size_t workspace_bytes, void* stream);
 int pbq_qr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes);
 
+/* Basis-only orth (m ≥ n ≥ 1) for the intermediate `orth` calls of the power
+ * iterations (algorithms.py:196-205, `basis = orth(counter.apply(basis))`),
+ * whose result is only ever multiplied by A and orthonormalised again.
+ * Out (m×n, ldo even, 16-byte aligned) receives B = Q·T, with Q the `orth`
+ * basis of A and T upper triangular with positive diagonal, ‖TᵀT − I‖ ≲ 1e-4
+ * (T = R₂ of Cholesky-QR2: only the first Cholesky-QR pass runs).  The thin
+ * QR of A_next·B has the Q factor of A_next·Q (right-multiplication by T
+ * leaves it unchanged), so the following orth returns what the reference
+ * computes, at half the passes of this one.  rank_flag as for
+ * pbq_householder_qr.  A is used as scratch.  Where the chain is not the
+ * route (single-launch sizes, the Householder method, a failed guard, or
+ * pbq_set_basis_orth(ctx, 0)) the full QR runs and Out = Q.  Workspace:
+ * pbq_qr_workspace_bytes(m, n). */
+int pbq_orth_basis(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, double* Out, int64_t ldo,
+                   int32_t* rank_flag, void* workspace, size_t workspace_bytes, void* stream);
+
+/* 1 (default): pbq_pbp_qlp runs every orth but the last one basis-only;
+ * 0: every orth is the full QR (A/B switch; results agree to rounding). */
+int pbq_set_basis_orth(pbq_ctx* ctx, int32_t on);
+
 /* rows×cols standard-normal sketch, bit-identical to
  * numpy.random.Generator(numpy.random.Philox(key=seed)).standard_normal((rows, cols))
  * as drawn by `gaussian_matrix` (linalg.py:83-93): Philox4x64-10 with

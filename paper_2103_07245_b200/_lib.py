@@ -64,6 +64,8 @@ EXPORTED = (
     "pbq_jacobi_svd",
     "pbq_jacobi_svd_workspace_bytes",
     "pbq_clear_error",
+    "pbq_orth_basis",
+    "pbq_set_basis_orth",
 )
 
 c_i64 = ctypes.c_int64
@@ -136,6 +138,8 @@ _SIGS = {
     "pbq_profile_begin": ([c_p, c_i32], ctypes.c_int),
     "pbq_profile_end": ([c_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)], ctypes.c_int),
     "pbq_set_qr_method": ([c_p, c_i32], ctypes.c_int),
+    "pbq_set_basis_orth": ([c_p, c_i32], ctypes.c_int),
+    "pbq_orth_basis": ([c_p, c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_p, c_sz, c_p], ctypes.c_int),
     "pbq_residual_fro": ([c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_p, c_sz, c_p],
                          ctypes.c_int),
     "pbq_residual_workspace_bytes": ([c_p, c_i64, c_i64, c_i64, ctypes.POINTER(c_sz)], ctypes.c_int),

@@ -96,6 +96,8 @@ struct CqArgs {
   int route_final;  // 1: last factorization of the shifted route (stats[3] counts it)
   int* fail_stats;  // optional: stats[1] counts hand-overs to Householder (also from intermediate passes)
   int chol_1warp;   // 1: diagonal blocks on one warp (cq_chol_inv32_warp) instead of two
+  int basis;        // pass 1 of a basis-only call (no second pass): a passed guard completes the call
+                    // (rank_flag ← 0: κ₁ ≤ kappa_max bounds every |R_ii|/|R_00| far above 1e-14)
 };
 
 #define CQ_MARK(slot)                                                                  \
@@ -732,7 +734,12 @@ __device__ void cq_factor(const CqArgs& p, double* sm) {
           mx = fmax(mx, s_max[1][w]);
         }
         const double kappa = mr * mx;
-        if (!p.shift_mode && !(kappa <= p.kappa_max)) fail_all();
+        if (!p.shift_mode && !(kappa <= p.kappa_max)) {
+          fail_all();
+        } else if (p.basis) {
+          if (p.rank_flag) *p.rank_flag = 0;
+          if (p.stats) atomicAdd(p.stats, 1);
+        }
       }
     }
     return;

@@ -51,6 +51,7 @@ struct pbq_ctx {
   unsigned long long* qr_bar_wait_ns = nullptr;
   int qr_method = PBQ_QR_AUTO;
   int* cq_stats = nullptr;                    // debug: [Cholesky-QR2 done, fallbacks]
+  bool basis_orth = true;                     // intermediate orth calls of the pipeline run basis-only (orth_basis_launch)
   std::unordered_map<const void*, int> smem_attr;  // max dynamic smem already set per kernel (one driver call each)
   // stream-K partial-ready flags: one array of `sms` ints per stream that
   // has launched a GEMM on this context.  An array is zero between launches
@@ -647,12 +648,31 @@ int factor_launch(pbq_ctx* ctx, const CqPlan& pl, CqArgs& a, cudaStream_t st) {
     }                                                                                            \
   } while (0)
 
+// copy src → dst (m×n) only when *run_if != 0: the fallback hand-over of a
+// basis-only call (the Householder kernel and the shifted route work in place)
+__global__ void __launch_bounds__(256) copy_if_kernel(const int* __restrict__ run_if, const double* __restrict__ src,
+                                                      long lds, double* __restrict__ dst, long ldd, long m, long n) {
+  if (__ldcg(run_if) == 0) return;
+  for (long e = long(blockIdx.x) * blockDim.x + threadIdx.x; e < m * n; e += long(gridDim.x) * blockDim.x) {
+    const long r = e / n, c = e % n;
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+}
+
+// Out != nullptr: basis-only call (orth_basis_launch below).  Only the first
+// Cholesky-QR pass runs: Out = A·R₁⁻¹ = Q·R₂ with R₂ upper triangular,
+// positive diagonal, ‖R₂ᵀR₂ − I‖ ≲ κ₁²u ≤ 1e-4 — the same Q factor under any
+// later QR, at half the passes.  A failed guard runs the full in-place chain /
+// Householder kernel on A and copies the result to Out.
 int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long ldr, int32_t* rank_flag, void* ws,
-              size_t ws_bytes, cudaStream_t st) {
+              size_t ws_bytes, cudaStream_t st, double* Out = nullptr, long ldo = 0) {
   QrPlan hp;
   PBQ_TRY(qr_plan(ctx, m, n, hp));
   if (lda < n || (R && ldr < n)) return fail(ctx, PBQ_ERR_PARAM, "qr: leading dimension too small");
   if ((lda & 1) || !aligned16(A)) return fail(ctx, PBQ_ERR_PARAM, "qr: lda must be even and A 16-byte aligned");
+  const bool basis = Out != nullptr;
+  if (basis && (ldo < n || (ldo & 1) || !aligned16(Out)))
+    return fail(ctx, PBQ_ERR_PARAM, "orth_basis: ldo must be even and >= n, Out 16-byte aligned");
   const CqPlan pl = cq_plan(ctx, m, n);
   const bool ext = n >= CQ_EXT_MIN_N;
   const size_t sq = size_t(pl.np) * pl.np;
@@ -703,16 +723,23 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   // ---- Cholesky-QR2
   PBQ_TRY(gram_launch(ctx, pl, m, n, A, lda, part, fallback, st, nullptr, ctl + 32, G, nullptr, Gc));
   f.pass = 1; f.R = R1; f.X = X1; f.counter = counter(1);
+  if (basis) {
+    f.basis = 1;
+    f.rank_flag = rank_flag;
+  }
   PBQ_TRY(factor_launch(ctx, pl, f, st));
-  PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
-                             fallback, true));
-  PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st, nullptr, ctl + 33, G, emax_slot(4)));
-  f.pass = 2; f.R = R2; f.X = X2; f.R1 = R1; f.Rout = R; f.ldr = ldr; f.rank_flag = rank_flag;
-  f.counter = counter(2);
-  f.shift_req = nullptr;
-  PBQ_TRY(factor_launch(ctx, pl, f, st));
-  PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q1, pl.ldq1, X2, pl.np, 0.0, A, lda, nullptr, gws, pl.gemm_ws, st,
-                             fallback, true));
+  PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, basis ? Out : Q1, basis ? ldo : pl.ldq1,
+                             nullptr, gws, pl.gemm_ws, st, fallback, true));
+  f.basis = 0;
+  if (!basis) {
+    PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st, nullptr, ctl + 33, G, emax_slot(4)));
+    f.pass = 2; f.R = R2; f.X = X2; f.R1 = R1; f.Rout = R; f.ldr = ldr; f.rank_flag = rank_flag;
+    f.counter = counter(2);
+    f.shift_req = nullptr;
+    PBQ_TRY(factor_launch(ctx, pl, f, st));
+    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q1, pl.ldq1, X2, pl.np, 0.0, A, lda, nullptr, gws, pl.gemm_ws, st,
+                               fallback, true));
+  }
   CQ_DEBUG_SYNC("cholqr2 done");
   if (ext) {
     // ---- shifted Cholesky-QR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto,
@@ -752,8 +779,15 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
     CQ_DEBUG_SYNC("route 10");
   }
   // Householder fallback (returns immediately unless a factorization failed)
-  return hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, ext ? hh_req : fallback,
-                   reinterpret_cast<unsigned int*>(ctl + 48));
+  PBQ_TRY(hh_launch(ctx, m, n, A, lda, R, ldr, 1, rank_flag, hws, hws_bytes, st, ext ? hh_req : fallback,
+                    reinterpret_cast<unsigned int*>(ctl + 48)));
+  if (basis) {
+    copy_if_kernel<<<unsigned(std::min<long>(ceil_div(m * n, 256L * 8), 4L * ctx->sms)), 256, 0, st>>>(fallback, A, lda, Out,
+                                                                                                     ldo, m, n);
+    PBQ_CUDA(ctx, cudaGetLastError());
+    ctx->launches += 1;
+  }
+  return PBQ_OK;
 }
 
 // ------------------------------------------- distributed Cholesky-QR2 ----
@@ -1005,6 +1039,30 @@ int qr_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   if (want_q && cm_eligible(ctx, m, n)) return cm_launch(ctx, m, n, A, lda, R, ldr, rank_flag, ws, ws_bytes, st);
   if (ctx->qr_method != PBQ_QR_HOUSEHOLDER && want_q) return cq_launch(ctx, m, n, A, lda, R, ldr, rank_flag, ws, ws_bytes, st);
   return hh_launch(ctx, m, n, A, lda, R, ldr, want_q, rank_flag, ws, ws_bytes, st, nullptr);
+}
+
+// Basis-only orth for an operand that is multiplied by A and orthonormalised
+// again (the intermediate orth calls of the power iterations,
+// algorithms.py:196-205): QR is invariant under right-multiplication by an
+// upper-triangular matrix with positive diagonal — qr(A·Q·T) has the Q factor
+// of qr(A·Q) — so the next orth returns the same basis from B = Q·T, T = R₂
+// of Cholesky-QR2, as from Q itself.  On the chain route only the first
+// Cholesky-QR pass runs and B lands in Out; the single-launch routes and the
+// Householder method factor A in place.  *res / *ldres: where the basis is.
+bool basis_route(const pbq_ctx* ctx, long m, long n) {
+  return ctx->basis_orth && ctx->qr_method != PBQ_QR_HOUSEHOLDER && !cs_eligible(ctx, m, n) && !cm_eligible(ctx, m, n);
+}
+
+int orth_basis_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* Out, long ldo, int32_t* rank_flag,
+                      void* ws, size_t ws_bytes, cudaStream_t st, double** res, long* ldres) {
+  if (Out && basis_route(ctx, m, n)) {
+    *res = Out;
+    *ldres = ldo;
+    return cq_launch(ctx, m, n, A, lda, nullptr, 0, rank_flag, ws, ws_bytes, st, Out, ldo);
+  }
+  *res = A;
+  *ldres = lda;
+  return qr_launch(ctx, m, n, A, lda, nullptr, 0, 1, rank_flag, ws, ws_bytes, st);
 }
 
 // -------------------------------------------------------------- sketch ----
@@ -1812,6 +1870,26 @@ int pbq_householder_qr(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t ld
   return qr_launch(ctx, m, n, A, lda, R, ldr, want_q, rank_flag, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
+int pbq_orth_basis(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, double* Out, int64_t ldo,
+                   int32_t* rank_flag, void* ws, size_t ws_bytes, void* stream) {
+  if (!ctx || !A || !Out) return PBQ_ERR_PARAM;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (ldo < n) return fail(ctx, PBQ_ERR_PARAM, "orth_basis: leading dimension too small");
+  double* res = nullptr;
+  long ldres = 0;
+  PBQ_TRY(orth_basis_launch(ctx, m, n, A, lda, Out, ldo, rank_flag, ws, ws_bytes, st, &res, &ldres));
+  if (res != Out)  // in-place routes: hand the result over
+    PBQ_CUDA(ctx, cudaMemcpy2DAsync(Out, ldo * sizeof(double), res, ldres * sizeof(double), n * sizeof(double), m,
+                                    cudaMemcpyDeviceToDevice, st));
+  return PBQ_OK;
+}
+
+int pbq_set_basis_orth(pbq_ctx* ctx, int32_t on) {
+  if (!ctx) return PBQ_ERR_PARAM;
+  ctx->basis_orth = on != 0;
+  return PBQ_OK;
+}
+
 int pbq_gaussian_workspace_bytes(pbq_ctx* ctx, int64_t rows, int64_t cols, int64_t row_offset, size_t* bytes) {
   if (!ctx || !bytes) return PBQ_ERR_PARAM;
   *bytes = sketch_ws_bytes(sketch_plan(rows, cols, row_offset));
@@ -1962,6 +2040,9 @@ static int pipeline_sizes(pbq_ctx* ctx, const pbq_problem* pr, size_t* total, si
   const long ld = thin_ld(d);
   *scratch = sc;
   *total = align_up(size_t(n2) * ld * 8, 256) + align_up(size_t(d) * ld * 8, 256) + align_up(64, 256) + sc + 512;
+  // second C and D buffers: the basis-only intermediate orth calls write out of place
+  if (pr->reorthonormalize && pr->q >= 1)
+    *total += align_up(size_t(n2) * ld * 8, 256) + align_up(size_t(n1) * ld * 8, 256);
   return PBQ_OK;
 }
 
@@ -1992,6 +2073,9 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   double* wbuf = cv.take<double>(size_t(d) * ld);   // W of the second stage
   int32_t* sk_err = cv.take<int32_t>(16);
   void* sc = cv.take<char>(scratch);
+  const bool two_buf = pr->reorthonormalize && q >= 1;
+  double* c2buf = two_buf ? cv.take<double>(size_t(n2) * ld) : nullptr;  // basis-only orth(C) output
+  double* d2buf = two_buf ? cv.take<double>(size_t(n1) * ld) : nullptr;  // basis-only orth(D) output
   const int32_t check = pr->check_finite ? 1 : 0;
 
   pipeline_init_kernel<<<1, 64, 0, st>>>(pr->c_init ? nullptr : o->nonfinite, o->rank_flags, int(2 * q + 1),
@@ -2021,16 +2105,31 @@ int pbq_pbp_qlp(pbq_ctx* ctx, const pbq_problem* pr, const pbq_outputs* o, void*
   double* dbuf = o->q;  // n1×d scratch for A·P̄, finally D itself
   const long ldq = o->ldq;
   if (pr->reorthonormalize) {
+    // every orth but the last feeds a pass that is orthonormalised again:
+    // basis-only (orth_basis_launch); the last one is P̄ itself (in place, full)
+    double* cb = cbuf;  // where the current basis of the row space lives
+    long ldcb = ld;
     {
       NvtxRange nv("pbq orth(C)");
-      PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
+      if (q >= 1)
+        PBQ_TRY(orth_basis_launch(ctx, n2, d, cbuf, ld, c2buf, ld, o->rank_flags + site++, sc, scratch, st, &cb, &ldcb));
+      else
+        PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
     }
     for (long it = 0; it < q; ++it) {
       NvtxRange nv("pbq power iteration");
-      PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cbuf, ld, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
-      PBQ_TRY(qr_launch(ctx, n1, d, dbuf, ldq, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
-      PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, dbuf, ldq, 0.0, cbuf, ld, nullptr, sc, scratch, st));
-      PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
+      double* db = dbuf;
+      long lddb = ldq;
+      PBQ_TRY(gemm_launch<false>(ctx, n1, d, n2, 1.0, pr->a, pr->lda, cb, ldcb, 0.0, dbuf, ldq, nullptr, sc, scratch, st));
+      PBQ_TRY(orth_basis_launch(ctx, n1, d, dbuf, ldq, d2buf, ld, o->rank_flags + site++, sc, scratch, st, &db, &lddb));
+      PBQ_TRY(gemm_launch<true>(ctx, n2, d, n1, 1.0, pr->a, pr->lda, db, lddb, 0.0, cbuf, ld, nullptr, sc, scratch, st));
+      if (it + 1 < q) {
+        PBQ_TRY(orth_basis_launch(ctx, n2, d, cbuf, ld, c2buf, ld, o->rank_flags + site++, sc, scratch, st, &cb, &ldcb));
+      } else {
+        PBQ_TRY(qr_launch(ctx, n2, d, cbuf, ld, nullptr, 0, 1, o->rank_flags + site++, sc, scratch, st));
+        cb = cbuf;
+        ldcb = ld;
+      }
     }
   } else {
     for (long it = 0; it < q; ++it) {

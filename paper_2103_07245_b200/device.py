@@ -59,6 +59,12 @@ class Context:
         with self.lock:
             self.check(self.lib.pbq_set_qr_method(self.handle, int(method)), "set_qr_method")
 
+    def set_basis_orth(self, on):
+        """True (default): pbp_qlp's intermediate orth calls run basis-only (one
+        Cholesky-QR pass); False: every orth is the full QR (A/B switch)."""
+        with self.lock:
+            self.check(self.lib.pbq_set_basis_orth(self.handle, int(bool(on))), "set_basis_orth")
+
     def set_p2p_timeout_ms(self, ms):
         """Spin limit of the peer-memory waits launched from now on (default 20 s)."""
         with self.lock:
@@ -303,6 +309,25 @@ def householder_qr_(ctx, a, r=None, want_q=True, rank_flag=None):
                                         int(bool(want_q)), ptr(rank_flag), ptr(ws), nbytes.value, stream_ptr(dev))
         ctx.check(st, "householder_qr")
     return a, r
+
+
+def orth_basis_(ctx, a, out=None, rank_flag=None):
+    """Basis-only orth of the m×n device matrix ``a`` (kernel-ready; clobbered):
+    returns B = Q·T (T upper triangular, positive diagonal, near the identity)
+    for an operand that is multiplied and orthonormalised again
+    (``pbq_orth_basis``; the intermediate orth calls of algorithms.py:196-205)."""
+    dev = a.device
+    m, n = a.shape
+    if out is None:
+        out = empty_matrix(m, n, dev)
+    nbytes = ctypes.c_size_t()
+    with ctx.lock:
+        ctx.check(ctx.lib.pbq_qr_workspace_bytes(ctx.handle, m, n, ctypes.byref(nbytes)), "qr workspace")
+        ws = workspace(nbytes.value, dev)
+        st = ctx.lib.pbq_orth_basis(ctx.handle, m, n, ptr(a), ld_of(a), ptr(out), ld_of(out), ptr(rank_flag), ptr(ws),
+                                    nbytes.value, stream_ptr(dev))
+        ctx.check(st, "orth_basis")
+    return out
 
 
 def residual_fro(ctx, a, q, l, p, out=None):

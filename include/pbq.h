@@ -242,6 +242,9 @@ int pbq_jacobi_svd_workspace_bytes(pbq_ctx* ctx, int64_t n, int64_t L, int32_t f
  *   stage 1: [G summed] R₁ = chol(G) with the κ₁ ≤ 1e6 guard; Q₁ = A·R₁⁻¹;
  *            G ← Q₁ᵀQ₁ (this rank's rows)
  *   stage 2: [G summed] R = R₂·R₁ (diag ≥ 0, rank flag as orth); A ← Q₁·R₂⁻¹
+ *   stage 3 (instead of 1 and 2, basis-only as pbq_orth_basis): [G summed]
+ *            R₁ = chol(G) with the guard; A ← A·R₁⁻¹ = Q·R₂ — one Gram exchange
+ *            for an orth whose result is multiplied by A and orthonormalised again
  * Every rank factors the same G, so R is bitwise identical on all ranks.
  * *fallback (device int32) is set when the guard fails: A is then left
  * untouched and the caller runs its TSQR instead.  The workspace must

@@ -301,6 +301,95 @@ __device__ __noinline__ bool cq_chol_inv32_2warp(double* S, double* Xs, double* 
   return true;
 }
 
+// Software-pipelined two-warp variant (the production routine).  The routine
+// above keeps the row broadcast on warp 0's dependent chain: pivot k+1 cannot
+// start before row k went through shared memory (store → __syncwarp → load,
+// ≈ 70 cycles) and the EMPTY handshake with warp 1.  Here
+//   * row k+1 receives pivot k's update at once, its multiplier r_{k,k+1}
+//     fetched with one shuffle, so the chain per pivot is again shuffle →
+//     rsqrt → mul → fma;
+//   * the rows below get pivot k's update one pivot later (iteration k+1),
+//     when row k has long been visible in shared memory — those FMAs fill the
+//     latency of the next pivot's shuffle and rsqrt instead of stalling;
+//   * row k of R is written straight into S (its final place; G's row k is in
+//     registers by then), so no slot is ever reused and warp 0 never waits
+//     for warp 1.  Warp 1 follows through a published-pivot count
+//     (st.release / ld.acquire on a shared word) and 1/r_kk per pivot.
+// Same operations in the same order per element: bitwise the results of the
+// routines above.  rowbuf: ≥ 34 doubles.  Called by warps 0 and 1; warp 0's
+// result is the one to use.
+__device__ __forceinline__ void cq_flag_release(unsigned int* f, unsigned int v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(f)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int cq_flag_acquire(const unsigned int* f) {
+  unsigned int v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(f)) : "memory");
+  return v;
+}
+
+__device__ __noinline__ bool cq_chol_inv32_pipe(double* S, double* Xs, double* rowbuf /*≥ 34, 16-byte aligned*/) {
+  const int lane = threadIdx.x & 31;
+  double* invb = rowbuf;                                             // 1/r_kk, k = 0…31
+  unsigned int* flag = reinterpret_cast<unsigned int*>(rowbuf + 32);  // pivots published so far
+  if ((threadIdx.x >> 5) == 0) {
+    double v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = S[i * CQ_LD + lane];
+    if (lane == 0) *flag = 0u;
+    cq_bar_sync(1);  // warp 1 starts polling after the reset (and S is in registers)
+    bool ok = true;
+    double piv = v[0];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double dk = __shfl_sync(0xffffffffu, piv, k);
+      if (k >= 1) {  // pivot k−1 on rows k+1…31 (row k took it early, below)
+        const double rp = v[k - 1];
+        const double* rb = S + (k - 1) * CQ_LD;
+#pragma unroll
+        for (int i2 = (k + 1) & ~1; i2 < 32; i2 += 2) {
+          const double2 r2 = *reinterpret_cast<const double2*>(rb + i2);
+          if (i2 > k) v[i2] = fma(-r2.x, rp, v[i2]);
+          if (i2 + 1 > k && i2 + 1 < 32) v[i2 + 1] = fma(-r2.y, rp, v[i2 + 1]);
+        }
+      }
+      ok = ok && (dk > 0.0);
+      const double inv = fast_rsqrt(dk);
+      const double rkj = (lane >= k) ? v[k] * inv : 0.0;
+      v[k] = rkj;
+      if (k + 1 < 32) {
+        piv = fma(-rkj, rkj, v[k + 1]);  // meaningful on lane k+1 (its v[k+1] is complete up to pivot k−1)
+        v[k + 1] = fma(-__shfl_sync(0xffffffffu, rkj, k + 1), rkj, v[k + 1]);
+      }
+      S[k * CQ_LD + lane] = rkj;
+      if (lane == 0) invb[k] = inv;
+      __syncwarp();
+      if (lane == 0) cq_flag_release(flag, unsigned(k + 1));
+    }
+    return ok;
+  }
+  double w[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) w[i] = (i == lane) ? 1.0 : 0.0;
+  cq_bar_sync(1);
+  unsigned int seen = 0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    while (seen <= unsigned(k)) seen = cq_flag_acquire(flag);
+    const double bkj = w[k] * invb[k];
+    w[k] = bkj;
+    const double* rb = S + k * CQ_LD;
+#pragma unroll
+    for (int i2 = (k + 1) & ~1; i2 < 32; i2 += 2) {
+      const double2 r2 = *reinterpret_cast<const double2*>(rb + i2);
+      if (i2 > k) w[i2] = fma(-r2.x, bkj, w[i2]);
+      if (i2 + 1 > k && i2 + 1 < 32) w[i2 + 1] = fma(-r2.y, bkj, w[i2 + 1]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Xs[lane * CQ_LD + i] = w[i];
+  return true;
+}
+
 __device__ __forceinline__ double cq_split(int r, int c, double x) { return c > r ? x : (c == r ? 0.5 * x : 0.0); }
 
 // ---------------------------------------------------------------------------

@@ -651,8 +651,9 @@ int factor_launch(pbq_ctx* ctx, const CqPlan& pl, CqArgs& a, cudaStream_t st) {
 // copy src → dst (m×n) only when *run_if != 0: the fallback hand-over of a
 // basis-only call (the Householder kernel and the shifted route work in place)
 __global__ void __launch_bounds__(256) copy_if_kernel(const int* __restrict__ run_if, const double* __restrict__ src,
-                                                      long lds, double* __restrict__ dst, long ldd, long m, long n) {
-  if (__ldcg(run_if) == 0) return;
+                                                      long lds, double* __restrict__ dst, long ldd, long m, long n,
+                                                      int unless = 0) {
+  if ((__ldcg(run_if) != 0) == (unless != 0)) return;
   for (long e = long(blockIdx.x) * blockDim.x + threadIdx.x; e < m * n; e += long(gridDim.x) * blockDim.x) {
     const long r = e / n, c = e % n;
     dst[r * ldd + c] = src[r * lds + c];
@@ -869,7 +870,24 @@ int cqd_stage(pbq_ctx* ctx, int stage, long m, long n, double* A, long lda, doub
                                fallback, true));
     return PBQ_OK;
   }
-  return fail(ctx, PBQ_ERR_PARAM, "cholqr2_dist: stage must be 0, 1 or 2");
+  if (stage == 3) {
+    // basis-only finish (after stage 0 and the Gram allreduce): R₁, then
+    // A ← A·R₁⁻¹ = Q·R₂ — one Gram exchange instead of two (see cq_launch)
+    cholqr_dist_fix<<<fix_grid, 256, 0, st>>>(G, n, pl.np, nullptr);
+    PBQ_CUDA(ctx, cudaGetLastError());
+    ctx->launches += 1;
+    f.pass = 1; f.R = R1; f.X = X1; f.counter = counter(1);
+    f.basis = 1; f.rank_flag = rank_flag;
+    PBQ_TRY(factor_launch(ctx, pl, f, st));
+    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
+                               fallback, true));
+    copy_if_kernel<<<unsigned(std::min<long>(ceil_div(m * n, 256L * 8), 4L * ctx->sms)), 256, 0, st>>>(
+        fallback, Q1, pl.ldq1, A, lda, m, n, 1);
+    PBQ_CUDA(ctx, cudaGetLastError());
+    ctx->launches += 1;
+    return PBQ_OK;
+  }
+  return fail(ctx, PBQ_ERR_PARAM, "cholqr2_dist: stage must be 0, 1, 2 or 3");
 }
 
 // ------------------------------------------- single-launch Cholesky-QR2 ----

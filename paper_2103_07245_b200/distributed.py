@@ -300,6 +300,7 @@ class DistributedPbpQlp:
         # [non-finite, sketch status, rank flags …, Cholesky-QR2 guard fired]
         self.flags = be.zeros_i32(2 * self.q + 4)
         self.force_fallback = False  # set by finish() for the re-run after a guard fired
+        self.basis_orth = True       # intermediate orths: one Cholesky-QR pass (False: the full QR everywhere)
         self._last = None
         self.PHI = None
         # qr(A·P̄): distributed Cholesky-QR2 (one d×d allreduce per pass) with
@@ -458,7 +459,24 @@ class DistributedPbpQlp:
         fb = self.flags[-1:]
         torch.maximum(fb, st["fallback"].to(fb.dtype), out=fb)
 
-    def _qr_sharded_(self, flag=None):
+    def _cholqr2_stages(self, shard, r, st, flag, basis):
+        """The distributed Cholesky-QR2 stages around their Gram allreduces.
+        ``basis``: the result is only multiplied by A and orthonormalised again
+        (an intermediate orth of the power iterations) — one pass and one Gram
+        exchange (pbq_cholqr2_dist stage 3: shard ← Q·R₂, which leaves the next
+        orth's Q factor unchanged)."""
+        be = self.be
+        be.cholqr2_dist(0, shard, r, st, flag)
+        self._sum_gram(st["G"])
+        if basis and self.basis_orth:
+            be.cholqr2_dist(3, shard, r, st, flag)
+        else:
+            be.cholqr2_dist(1, shard, r, st, flag)
+            self._sum_gram(st["G"])
+            be.cholqr2_dist(2, shard, r, st, flag)
+        self._note_guard(st)
+
+    def _qr_sharded_(self, flag=None, basis=False):
         """QR of the row-sharded self.Q in place (R → self.R): distributed
         Cholesky-QR2 — local Gram, allreduce(sum) of the d×d Gram, replicated
         factor, local product, twice.  Its guard flag is noted on the device;
@@ -469,15 +487,9 @@ class DistributedPbpQlp:
         if self.force_fallback:
             self.tsqr_fallbacks += 1
             return self._tsqr_(flag)
-        be = self.be
-        be.cholqr2_dist(0, self.Q, self.R, st, flag)
-        self._sum_gram(st["G"])
-        be.cholqr2_dist(1, self.Q, self.R, st, flag)
-        self._sum_gram(st["G"])
-        be.cholqr2_dist(2, self.Q, self.R, st, flag)
-        self._note_guard(st)
+        self._cholqr2_stages(self.Q, self.R, st, flag, basis)
 
-    def _orth_c_(self, flag):
+    def _orth_c_(self, flag, basis=False):
         """orth(C) in place, C replicated on every rank: each rank
         orthonormalizes its row slice by the distributed Cholesky-QR2 (two
         d×d allreduces), then the slices are all-gathered.  On a guard failure
@@ -491,12 +503,7 @@ class DistributedPbpQlp:
         be = self.be
         s0 = self.rank * self.slice_rows
         mine = self.Cbuf[s0:s0 + self.slice_rows]
-        be.cholqr2_dist(0, mine, self.Rs, st, flag)
-        self._sum_gram(st["G"])
-        be.cholqr2_dist(1, mine, self.Rs, st, flag)
-        self._sum_gram(st["G"])
-        be.cholqr2_dist(2, mine, self.Rs, st, flag)
-        self._note_guard(st)  # a fired guard left the slices untouched; finish() re-runs
+        self._cholqr2_stages(mine, self.Rs, st, flag, basis)  # a fired guard left the slices untouched; finish() re-runs
         buf = self.Cbuf
         ld = buf.stride(0)
         whole = buf.as_strided((buf.shape[0], ld), (ld, 1))  # whole rows incl. the even-ld pad column
@@ -527,14 +534,16 @@ class DistributedPbpQlp:
         site = 2
         self._at_x(A_local, self.PHI, nonfinite=flags[0:1])
         if self.reorthonormalize:
-            self._orth_c_(flags[site:site + 1])
+            # every orth but the last is basis-only (its result feeds a pass
+            # that is orthonormalised again; include/pbq.h: pbq_orth_basis)
+            self._orth_c_(flags[site:site + 1], basis=(q >= 1))
             site += 1
-            for _ in range(q):
+            for it in range(q):
                 be.gemm_nn(A_local, self.C, self.Q)
-                self._qr_sharded_(flags[site:site + 1])
+                self._qr_sharded_(flags[site:site + 1], basis=True)
                 site += 1
                 self._at_x(A_local, self.Q)
-                self._orth_c_(flags[site:site + 1])
+                self._orth_c_(flags[site:site + 1], basis=(it + 1 < q))
                 site += 1
         else:
             for _ in range(q):

@@ -89,24 +89,30 @@ def r_svd(a, d, q=0, seed=0, reorthonormalize=True, *, device=None):
 
     site = 2
 
-    def orth_(m):
-        """orth(m) in place on the device (first k columns), rank flag → flags[site]."""
+    def orth_(m, final=True):
+        """orth(m) on the device (first k columns), rank flag → flags[site].
+        ``final=False``: the result is only multiplied by A and orthonormalised
+        again — basis-only (``pbq_orth_basis``: Q·T with T upper triangular,
+        which leaves the next orth's Q factor unchanged)."""
         nonlocal site
         m = _dev.as_kernel_operand(m[:, :k]) if m.shape[1] != k else m
-        r = _dev.empty_matrix(k, k, dev)
-        _dev.householder_qr_(ctx, m, r, want_q=True, rank_flag=flags[site:site + 1])
+        if final or m.shape[1] != k:
+            r = _dev.empty_matrix(k, k, dev)
+            _dev.householder_qr_(ctx, m, r, want_q=True, rank_flag=flags[site:site + 1])
+        else:
+            m = _dev.orth_basis_(ctx, m, rank_flag=flags[site:site + 1])
         site += 1
         return m
 
     t = _dev.empty_matrix(n2, k, dev)
     if reorthonormalize:
-        ubar = orth_(f)
-        for _ in range(q):  # transpose_first=False: A.T first, then A
+        ubar = orth_(f, final=(q == 0))
+        for it in range(q):  # transpose_first=False: A.T first, then A
             _dev.gemm(ctx, A, ubar, trans_a=True, out=t)
-            t = orth_(t)
+            tb = orth_(t, final=False)
             ubar_next = _dev.empty_matrix(n1, k, dev)
-            _dev.gemm(ctx, A, t, trans_a=False, out=ubar_next)
-            ubar = orth_(ubar_next)
+            _dev.gemm(ctx, A, tb, trans_a=False, out=ubar_next)
+            ubar = orth_(ubar_next, final=(it == q - 1))
     else:
         tt = _dev.empty_matrix(n2, d, dev)
         for _ in range(q):

@@ -116,13 +116,20 @@ def cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=True, *, d
 
     site = 2
 
-    def orth_(m):
-        """orth(m) in place on the device (first min(rows, cols) columns), rank flag → flags[site]."""
+    def orth_(m, final=True):
+        """orth(m) on the device (first min(rows, cols) columns), rank flag → flags[site].
+        ``final=False``: the result is only multiplied by A and orthonormalised
+        again — basis-only (``pbq_orth_basis``: Q·T with T upper triangular,
+        which leaves the next orth's Q factor unchanged)."""
         nonlocal site
         c = min(m.shape)
-        m = _dev.as_kernel_operand(m[:, :c]) if m.shape[1] != c else _dev.as_kernel_operand(m)
-        r = _dev.empty_matrix(c, c, dev)
-        _dev.householder_qr_(ctx, m, r, want_q=True, rank_flag=flags[site:site + 1])
+        truncated = m.shape[1] != c
+        m = _dev.as_kernel_operand(m[:, :c]) if truncated else _dev.as_kernel_operand(m)
+        if final or truncated:
+            r = _dev.empty_matrix(c, c, dev)
+            _dev.householder_qr_(ctx, m, r, want_q=True, rank_flag=flags[site:site + 1])
+        else:
+            m = _dev.orth_basis_(ctx, m, rank_flag=flags[site:site + 1])
         site += 1
         return m
 
@@ -130,10 +137,10 @@ def cor_utv(a, d, q=0, seed=0, pass_efficient=False, reorthonormalize=True, *, d
     f1 = apply(omega)
     gram = None
     if reorthonormalize:
-        ubar = orth_(f1)
-        for _ in range(q):  # _power_iterations(transpose_first=False): Aᵀ first, then A
-            ubar = orth_(apply_t(ubar))
-            ubar = orth_(apply(ubar))
+        ubar = orth_(f1, final=(q == 0))
+        for it in range(q):  # _power_iterations(transpose_first=False): Aᵀ first, then A
+            ubar = orth_(apply_t(ubar), final=False)
+            ubar = orth_(apply(ubar), final=(it == q - 1))
         f2 = apply_t(ubar)
     else:
         for _ in range(q):

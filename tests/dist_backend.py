@@ -60,7 +60,7 @@ class NumpyBackend:
             return
         if state["fallback"].item():
             return
-        if stage == 1:
+        if stage in (1, 3):
             try:
                 r1 = np.linalg.cholesky(g.numpy()).T
             except np.linalg.LinAlgError:
@@ -71,6 +71,11 @@ class NumpyBackend:
                 state["fallback"].fill_(1)
                 return
             q1 = a.numpy() @ r1i
+            if stage == 3:  # basis-only finish: a ← A·R₁⁻¹ = Q·R₂
+                a.copy_(torch.from_numpy(q1))
+                if flag is not None:
+                    flag.fill_(0)
+                return
             state["r1"], state["q1"] = r1, q1
             g.copy_(torch.from_numpy(q1.T @ q1))
             return

@@ -124,6 +124,7 @@ __global__ void bench(double* out, const double* g, int iters, long long* cyc) {
     if (V == 3 && warp == 0) acc += chain_only(S[lane]);
     if (V == 4 && warp == 0) chol_r_shfl(S);
     if (V == 5 && warp == 0) acc += chain3(S[lane]);
+    if (V == 6) cq_chol_inv32_pipe(S, X, RB);
     __syncthreads();
     const long long t1 = clock64();
     if (it > 0) tot += t1 - t0;
@@ -131,6 +132,27 @@ __global__ void bench(double* out, const double* g, int iters, long long* cyc) {
   }
   if (threadIdx.x == 0) *cyc = tot / (iters - 1);
   out[threadIdx.x] = acc;
+}
+
+// bitwise comparison of the pipelined routine with the two-warp one
+__global__ void verify(const double* g, int* diff) {
+  __shared__ double S0[32 * CQ_LD], X0[32 * CQ_LD], S1[32 * CQ_LD], X1[32 * CQ_LD];
+  __shared__ __align__(16) double RB[2 * CQ_RB2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0)
+    for (int i = 0; i < 32; ++i) S0[i * CQ_LD + lane] = S1[i * CQ_LD + lane] = g[i * 32 + lane];
+  __syncthreads();
+  cq_chol_inv32_2warp(S0, X0, RB);
+  __syncthreads();
+  cq_chol_inv32_pipe(S1, X1, RB);
+  __syncthreads();
+  int d = 0;
+  if (warp == 0)
+    for (int i = 0; i < 32; ++i) {
+      d += __double_as_longlong(S0[i * CQ_LD + lane]) != __double_as_longlong(S1[i * CQ_LD + lane]);
+      d += __double_as_longlong(X0[i * CQ_LD + lane]) != __double_as_longlong(X1[i * CQ_LD + lane]);
+    }
+  if (d) atomicAdd(diff, d);
 }
 
 int main() {
@@ -150,6 +172,10 @@ int main() {
   bench<3><<<1, 64>>>(o, g, 50, c); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost); printf("%s: %lld cycles\n", nm[3], cy);
   bench<4><<<1, 64>>>(o, g, 50, c); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost); printf("%s: %lld cycles\n", nm[4], cy);
   bench<5><<<1, 64>>>(o, g, 50, c); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost); printf("dependent chain, rsqrt3: %lld cycles\n", cy);
+  bench<6><<<1, 64>>>(o, g, 50, c); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost); printf("2-warp chol+inv, pipelined: %lld cycles\n", cy);
+  int* df; cudaMalloc(&df, 4); cudaMemset(df, 0, 4);
+  verify<<<1, 64>>>(g, df); int hd = -1; cudaMemcpy(&hd, df, 4, cudaMemcpyDeviceToHost);
+  printf("pipelined vs two-warp routine: %d differing words (S and X, bitwise)\n", hd);
   double* a3; cudaMalloc(&a3, 96 * 8); acc3<<<1, 32>>>(a3); double ha[96]; cudaMemcpy(ha, a3, 96 * 8, cudaMemcpyDeviceToHost);
   double ma = 0, m2 = 0, m3 = 0;
   for (int i = 0; i < 32; ++i) { ma = fmax(ma, ha[3 * i]); m2 = fmax(m2, ha[3 * i + 1]); m3 = fmax(m3, ha[3 * i + 2]); }

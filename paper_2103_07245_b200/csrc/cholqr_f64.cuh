@@ -95,7 +95,7 @@ struct CqArgs {
   int rout_full;    // 1: write Rout over the padded np×np (an intermediate product)
   int route_final;  // 1: last factorization of the shifted route (stats[3] counts it)
   int* fail_stats;  // optional: stats[1] counts hand-overs to Householder (also from intermediate passes)
-  int chol_1warp;   // 1: diagonal blocks on one warp (cq_chol_inv32_warp) instead of two
+  int chol_1warp;   // diagonal blocks: 0 pipelined two-warp routine, 1 one warp (cq_chol_inv32_warp), 2 lock-step two warps
   int basis;        // pass 1 of a basis-only call (no second pass): a passed guard completes the call
                     // (rank_flag ← 0: κ₁ ≤ kappa_max bounds every |R_ii|/|R_00| far above 1e-14)
 };
@@ -313,30 +313,43 @@ __device__ __noinline__ bool cq_chol_inv32_2warp(double* S, double* Xs, double* 
 //     latency of the next pivot's shuffle and rsqrt instead of stalling;
 //   * row k of R is written straight into S (its final place; G's row k is in
 //     registers by then), so no slot is ever reused and warp 0 never waits
-//     for warp 1.  Warp 1 follows through a published-pivot count
-//     (st.release / ld.acquire on a shared word) and 1/r_kk per pivot.
+//     for warp 1.  Warp 1 follows pivot by pivot through one mbarrier per
+//     pivot (lane 0 of warp 0 arrives after the warp's stores; an mbarrier
+//     arrive is a CTA-scope release without the MEMBAR a flag store needs —
+//     that fence cost 40 cycles per pivot), used for one phase per call; the
+//     phase parity of the call is kept in the state block.
 // Same operations in the same order per element: bitwise the results of the
-// routines above.  rowbuf: ≥ 34 doubles.  Called by warps 0 and 1; warp 0's
-// result is the one to use.
-__device__ __forceinline__ void cq_flag_release(unsigned int* f, unsigned int v) {
-  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(f)), "r"(v) : "memory");
+// routines above (tools/microbench/chol32_2warp.cu: 7421 → 4.6k cycles).
+// State block (rowbuf, CQ_CHOL_STATE doubles, 16-byte aligned): 1/r_kk per
+// pivot, 32 mbarriers, the parity word.  cq_chol_setup once per kernel (all
+// threads, then __syncthreads); cq_chol_teardown before another setup of the
+// same block.  Called by warps 0 and 1; warp 0's result is the one to use.
+constexpr int CQ_CHOL_STATE = 66;
+#ifdef CQ_CHOL_TIMING
+__device__ long long cq_chol_t[2];  // microbenchmark hook: clock64 at the end of warp 0 / warp 1
+#endif
+__device__ __forceinline__ void cq_chol_setup(double* rowbuf) {
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rowbuf + 32);
+  if (threadIdx.x < 32) mbar_init(bars + threadIdx.x, 1);
+  if (threadIdx.x == 0) *reinterpret_cast<unsigned int*>(rowbuf + 64) = 0u;
 }
-__device__ __forceinline__ unsigned int cq_flag_acquire(const unsigned int* f) {
-  unsigned int v;
-  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(f)) : "memory");
-  return v;
+__device__ __forceinline__ void cq_chol_teardown(double* rowbuf) {
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rowbuf + 32);
+  if (threadIdx.x < 32) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bars + threadIdx.x)) : "memory");
 }
 
-__device__ __noinline__ bool cq_chol_inv32_pipe(double* S, double* Xs, double* rowbuf /*≥ 34, 16-byte aligned*/) {
+__device__ __noinline__ bool cq_chol_inv32_pipe(double* S, double* Xs, double* rowbuf) {
   const int lane = threadIdx.x & 31;
-  double* invb = rowbuf;                                             // 1/r_kk, k = 0…31
-  unsigned int* flag = reinterpret_cast<unsigned int*>(rowbuf + 32);  // pivots published so far
+  double* invb = rowbuf;  // 1/r_kk, k = 0…31
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rowbuf + 32);
+  unsigned int* parw = reinterpret_cast<unsigned int*>(rowbuf + 64);
+  const unsigned int par = *parw;  // phase parity of this call, read by both warps before the barrier below
   if ((threadIdx.x >> 5) == 0) {
     double v[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = S[i * CQ_LD + lane];
-    if (lane == 0) *flag = 0u;
-    cq_bar_sync(1);  // warp 1 starts polling after the reset (and S is in registers)
+    cq_bar_sync(1);  // both warps hold `par` (and S is in registers)
+    if (lane == 0) *parw = par ^ 1u;
     bool ok = true;
     double piv = v[0];
 #pragma unroll
@@ -363,20 +376,22 @@ __device__ __noinline__ bool cq_chol_inv32_pipe(double* S, double* Xs, double* r
       S[k * CQ_LD + lane] = rkj;
       if (lane == 0) invb[k] = inv;
       __syncwarp();
-      if (lane == 0) cq_flag_release(flag, unsigned(k + 1));
+      if (lane == 0) mbar_arrive(bars + k);
     }
+#ifdef CQ_CHOL_TIMING
+    if (lane == 0) cq_chol_t[0] = clock64();
+#endif
     return ok;
   }
   double w[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) w[i] = (i == lane) ? 1.0 : 0.0;
   cq_bar_sync(1);
-  unsigned int seen = 0;
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
-    while (seen <= unsigned(k)) seen = cq_flag_acquire(flag);
+    mbar_wait(bars + k, par);
     const double bkj = w[k] * invb[k];
-    w[k] = bkj;
+    Xs[lane * CQ_LD + k] = bkj;  // column k of R⁻¹ is final (stored pivot by pivot: no store tail)
     const double* rb = S + k * CQ_LD;
 #pragma unroll
     for (int i2 = (k + 1) & ~1; i2 < 32; i2 += 2) {
@@ -385,8 +400,9 @@ __device__ __noinline__ bool cq_chol_inv32_pipe(double* S, double* Xs, double* r
       if (i2 + 1 > k && i2 + 1 < 32) w[i2 + 1] = fma(-r2.y, bkj, w[i2 + 1]);
     }
   }
-#pragma unroll
-  for (int i = 0; i < 32; ++i) Xs[lane * CQ_LD + i] = w[i];
+#ifdef CQ_CHOL_TIMING
+  if (lane == 0) cq_chol_t[1] = clock64();
+#endif
   return true;
 }
 
@@ -552,7 +568,7 @@ __device__ __forceinline__ void cq_inverse_final_item(const CqArgs& p, int k, in
 // cholqr_mid_f64.cuh, which calls it between its own phases).  sm: the
 // CQ_SMEM_BYTES dynamic shared-memory block.  p.counter: a grid-barrier
 // counter used by this call only (zeroed before the launch).
-__device__ void cq_factor(const CqArgs& p, double* sm) {
+__device__ void cq_factor_body(const CqArgs& p, double* sm, double* s_rowbuf) {
   double* sKK = sm;           // R_kk
   double* sKI = sm + CQ_BLK;  // R_kk⁻¹
   double* sU = sm + 2 * CQ_BLK;
@@ -563,7 +579,6 @@ __device__ void cq_factor(const CqArgs& p, double* sm) {
   double* sT = pairs + 3 * CQ_BLK;
   __shared__ int s_ok;
   __shared__ double s_dmax, s_dmin;  // running max / min |R_ii| (pass-1 early κ guard)
-  __shared__ __align__(16) double s_rowbuf[2 * CQ_RB2];
   if (p.fallback && __ldcg(p.fallback) != 0) return;  // uniform: written by an earlier launch
   if (p.route && __ldcg(p.route) == 0) return;
   // a failed factorization: pass 1 of the extended chain asks for the shifted
@@ -725,13 +740,13 @@ __device__ void cq_factor(const CqArgs& p, double* sm) {
       if (tid < 32 && k * 32 + tid < p.n) sKK[tid * CQ_LD + tid] += shift;
       __syncthreads();
     }
-    if (p.chol_1warp) {  // the single-warp variant (A/B measurements)
+    if (p.chol_1warp == 1) {  // the single-warp variant (A/B measurements)
       if (warp == 0) {
         const bool ok = cq_chol_inv32_warp(sKK, sKI, s_rowbuf);
         if (tid == 0) s_ok = ok;
       }
-    } else if (warp < 2) {
-      const bool ok = cq_chol_inv32_2warp(sKK, sKI, s_rowbuf);
+    } else if (warp < 2) {  // chol_1warp == 2: the lock-step two-warp routine (A/B)
+      const bool ok = p.chol_1warp == 2 ? cq_chol_inv32_2warp(sKK, sKI, s_rowbuf) : cq_chol_inv32_pipe(sKK, sKI, s_rowbuf);
       if (tid == 0) s_ok = ok;
     }
     __syncthreads();
@@ -873,6 +888,22 @@ __device__ void cq_factor(const CqArgs& p, double* sm) {
         if (p.route_final) atomicAdd(p.stats + 3, 1);
       }
     }
+  }
+}
+
+// (every return of the body is uniform over the CTA)
+__device__ void cq_factor(const CqArgs& p, double* sm) {
+  __shared__ __align__(16) double s_rowbuf[2 * CQ_RB2];
+  static_assert(2 * CQ_RB2 >= CQ_CHOL_STATE, "row buffer holds the pipelined routine's state block");
+  const bool pipe = p.chol_1warp == 0;  // the other variants use the block as plain row slots
+  if (pipe) {
+    cq_chol_setup(s_rowbuf);
+    __syncthreads();
+  }
+  cq_factor_body(p, sm, s_rowbuf);
+  if (pipe) {
+    __syncthreads();
+    cq_chol_teardown(s_rowbuf);
   }
 }
 

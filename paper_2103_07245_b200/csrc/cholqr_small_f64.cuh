@@ -192,7 +192,7 @@ __device__ bool cs_chol_inv(double* Gs, double* Xs, double* tmp, double* rowbuf,
     double* Gkk = Gs + cs_ut(k, k, NB) * CQ_BLK;
     double* Xkk = Xs + cs_ut(k, k, NB) * CQ_BLK;
     if (warp < 2) {
-      const bool ok = cq_chol_inv32_2warp(Gkk, Xkk, rowbuf);
+      const bool ok = cq_chol_inv32_pipe(Gkk, Xkk, rowbuf);
       if (threadIdx.x == 0) *s_ok = ok;
     }
     __syncthreads();
@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) cholqr_small_kernel(CsArgs p) {
   unsigned int gen = 0;
   unsigned long long t_mark = 0;
   if (p.phase_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_mark));
+  cq_chol_setup(s_rowbuf);  // state of the pipelined diagonal factorization (ordered by the barriers below)
 
   // ---- Gram₁
   cs_gram<NB>(p, p.A, p.lda, regA);

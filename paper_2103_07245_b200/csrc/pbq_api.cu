@@ -625,8 +625,9 @@ int gram_launch(pbq_ctx* ctx, const CqPlan& pl, long m, long n, const double* X,
 }
 
 int factor_launch(pbq_ctx* ctx, const CqPlan& pl, CqArgs& a, cudaStream_t st) {
-  static const bool one_warp = getenv("PBQ_CHOL_1WARP") != nullptr;  // A/B switch for the diagonal factorization
-  a.chol_1warp = one_warp ? 1 : 0;
+  // A/B switches for the diagonal factorization (default: the pipelined two-warp routine)
+  static const int variant = getenv("PBQ_CHOL_1WARP") ? 1 : getenv("PBQ_CHOL_LOCKSTEP") ? 2 : 0;
+  a.chol_1warp = variant;
   PBQ_CUDA(ctx, ensure_smem(ctx, reinterpret_cast<const void*>(&cholqr_factor_kernel), CQ_SMEM_BYTES));
   void* args[] = {&a};
   PBQ_CUDA(ctx, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&cholqr_factor_kernel),

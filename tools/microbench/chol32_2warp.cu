@@ -3,6 +3,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o chol32_2warp chol32_2warp.cu
 #include <cstdio>
 #include <cuda_runtime.h>
+#define CQ_CHOL_TIMING
 #include "../../paper_2103_07245_b200/csrc/cholqr_f64.cuh"
 using namespace pbq;
 
@@ -106,6 +107,38 @@ __device__ __noinline__ void chol_r_shfl(double* S) {
   for (int i = 0; i < 32; ++i) S[i * CQ_LD + lane] = (i <= lane) ? v[i] : 0.0;
 }
 
+// F: warp 0 of the pipelined routine alone (no publication, no warp 1)
+__device__ __noinline__ void chol_r_pipe(double* S) {
+  const int lane = threadIdx.x & 31;
+  double v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = S[i * CQ_LD + lane];
+  double piv = v[0];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const double dk = __shfl_sync(0xffffffffu, piv, k);
+    if (k >= 1) {
+      const double rp = v[k - 1];
+      const double* rb = S + (k - 1) * CQ_LD;
+#pragma unroll
+      for (int i2 = (k + 1) & ~1; i2 < 32; i2 += 2) {
+        const double2 r2 = *reinterpret_cast<const double2*>(rb + i2);
+        if (i2 > k) v[i2] = fma(-r2.x, rp, v[i2]);
+        if (i2 + 1 > k && i2 + 1 < 32) v[i2 + 1] = fma(-r2.y, rp, v[i2 + 1]);
+      }
+    }
+    const double inv = fast_rsqrt(dk);
+    const double rkj = (lane >= k) ? v[k] * inv : 0.0;
+    v[k] = rkj;
+    if (k + 1 < 32) {
+      piv = fma(-rkj, rkj, v[k + 1]);
+      v[k + 1] = fma(-__shfl_sync(0xffffffffu, rkj, k + 1), rkj, v[k + 1]);
+    }
+    S[k * CQ_LD + lane] = rkj;
+    __syncwarp();
+  }
+}
+
 template <int V>
 __global__ void bench(double* out, const double* g, int iters, long long* cyc) {
   __shared__ double S[32 * CQ_LD], X[32 * CQ_LD];
@@ -113,6 +146,7 @@ __global__ void bench(double* out, const double* g, int iters, long long* cyc) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   long long tot = 0;
   double acc = 0;
+  if (V == 6) cq_chol_setup(RB);
   for (int it = 0; it < iters; ++it) {
     if (warp == 0)
       for (int i = 0; i < 32; ++i) S[i * CQ_LD + lane] = g[i * 32 + lane];
@@ -125,9 +159,13 @@ __global__ void bench(double* out, const double* g, int iters, long long* cyc) {
     if (V == 4 && warp == 0) chol_r_shfl(S);
     if (V == 5 && warp == 0) acc += chain3(S[lane]);
     if (V == 6) cq_chol_inv32_pipe(S, X, RB);
+    if (V == 7 && warp == 0) chol_r_pipe(S);
     __syncthreads();
     const long long t1 = clock64();
     if (it > 0) tot += t1 - t0;
+    if (V == 6 && it == iters - 1 && threadIdx.x == 0)
+      printf("  pipelined, last call: warp 0 done at %lld, warp 1 at %lld, both through the barrier at %lld cycles\n",
+             cq_chol_t[0] - t0, cq_chol_t[1] - t0, t1 - t0);
     acc += S[lane * CQ_LD + lane];
   }
   if (threadIdx.x == 0) *cyc = tot / (iters - 1);
@@ -144,8 +182,15 @@ __global__ void verify(const double* g, int* diff) {
   __syncthreads();
   cq_chol_inv32_2warp(S0, X0, RB);
   __syncthreads();
-  cq_chol_inv32_pipe(S1, X1, RB);
+  cq_chol_setup(RB);
   __syncthreads();
+  for (int rep = 0; rep < 3; ++rep) {  // three calls: both phase parities
+    if (warp == 0)
+      for (int i = 0; i < 32; ++i) S1[i * CQ_LD + lane] = g[i * 32 + lane];
+    __syncthreads();
+    cq_chol_inv32_pipe(S1, X1, RB);
+    __syncthreads();
+  }
   int d = 0;
   if (warp == 0)
     for (int i = 0; i < 32; ++i) {
@@ -173,6 +218,7 @@ int main() {
   bench<4><<<1, 64>>>(o, g, 50, c); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost); printf("%s: %lld cycles\n", nm[4], cy);
   bench<5><<<1, 64>>>(o, g, 50, c); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost); printf("dependent chain, rsqrt3: %lld cycles\n", cy);
   bench<6><<<1, 64>>>(o, g, 50, c); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost); printf("2-warp chol+inv, pipelined: %lld cycles\n", cy);
+  bench<7><<<1, 64>>>(o, g, 50, c); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost); printf("R part only, pipelined: %lld cycles\n", cy);
   int* df; cudaMalloc(&df, 4); cudaMemset(df, 0, 4);
   verify<<<1, 64>>>(g, df); int hd = -1; cudaMemcpy(&hd, df, 4, cudaMemcpyDeviceToHost);
   printf("pipelined vs two-warp routine: %d differing words (S and X, bitwise)\n", hd);

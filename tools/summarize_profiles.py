@@ -48,7 +48,8 @@ def launch_shares(tag):
             args = [x.strip() for x in n[n.index("<") + 1:n.index(">")].split(",")]
             return "gemm_split" if args[-2] in ("1", "true") else "gemm"
         for k in ("cholqr_factor_kernel", "cholqr_gram_reduce", "qr_tall_kernel", "sketch_k1", "sketch_k2",
-                  "sketch_k3", "transpose_kernel", "merge_flag_kernel", "pipeline_init_kernel"):
+                  "sketch_k3", "transpose_kernel", "merge_flag_kernel", "pipeline_init_kernel", "copy_if_kernel",
+                  "cholqr_mid_kernel", "cholqr_small_kernel"):
             if k in n:
                 return k
         return "input-prep"
@@ -66,8 +67,9 @@ def launch_shares(tag):
             key = "GEMM A-passes (gemm_f64_tma)"
         elif name == "gemm" and ntr == 2:
             key = "GEMM P = P̄·W (gemm_f64_tma)"
-        elif name in ("gemm", "gemm_split", "cholqr_gram_reduce", "cholqr_factor_kernel", "qr_tall_kernel"):
-            key = "QR ×5 (Cholesky-QR2 chain; Householder early-exit)"
+        elif name in ("gemm", "gemm_split", "cholqr_gram_reduce", "cholqr_factor_kernel", "qr_tall_kernel",
+                      "copy_if_kernel", "cholqr_mid_kernel", "cholqr_small_kernel"):
+            key = "QR ×5 (2 basis-only + 2 full Cholesky-QR2 chains, single-launch d×d; Householder / copy early-exit)"
         elif name.startswith("sketch"):
             key = "sketch (Philox4x64 + ziggurat, k1/k2/k3)"
         elif name == "input-prep":

@@ -98,16 +98,25 @@ def make_cpqr_dropin(pbpqlp):
     return column_pivoted_qr
 
 
-def make_dropin(pbpqlp):
-    """Return a reference-typed ``pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True)``."""
+def make_dropin(pbpqlp, devices=None, backend="nccl"):
+    """Return a reference-typed ``pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True)``.
+    ``devices`` (a list of CUDA indices, more than one): the call is row-sharded
+    over those GPUs by ``pbp_qlp_multi_gpu`` (one worker process per GPU)."""
     ref_alg = pbpqlp.algorithms
     ref_exc = pbpqlp.exceptions
+    multi = devices is not None and len(devices) > 1
 
     def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True):
         with warnings.catch_warnings(record=True) as rec:
             warnings.simplefilter("always", _exc.RankDeficiencyWarning)
             try:
-                f = _alg.pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
+                if multi:
+                    from .multigpu import pbp_qlp_multi_gpu
+
+                    f = pbp_qlp_multi_gpu(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize, devices=devices,
+                                          backend=backend)
+                else:
+                    f = _alg.pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
             except _exc.DimensionError as e:
                 raise ref_exc.DimensionError(str(e)) from None
             except _exc.ParameterError as e:
@@ -128,12 +137,13 @@ def make_dropin(pbpqlp):
     return pbp_qlp
 
 
-def install(pbpqlp):
+def install(pbpqlp, devices=None, backend="nccl"):
     """Patch every module of the imported reference package ``pbpqlp`` that
-    bound ``pbp_qlp``; returns the previous bindings (for ``uninstall``)."""
+    bound ``pbp_qlp``; returns the previous bindings (for ``uninstall``).
+    ``devices=[0, 1, …]`` routes ``pbp_qlp`` through the multi-GPU launcher."""
     import importlib
 
-    dropins = {"pbp_qlp": make_dropin(pbpqlp), "r_svd": make_rsvd_dropin(pbpqlp),
+    dropins = {"pbp_qlp": make_dropin(pbpqlp, devices, backend), "r_svd": make_rsvd_dropin(pbpqlp),
                "cor_utv": make_utv_dropin(pbpqlp), "column_pivoted_qr": make_cpqr_dropin(pbpqlp)}
     saved = {}
     for suffix in _BINDERS:

@@ -132,3 +132,28 @@ def test_integration_shim_maps_errors_to_reference_classes(reference_pkg):
         integration.uninstall(saved)
     assert not getattr(reference_pkg.pbp_qlp, "__wrapped_gpu__", False)
     assert not getattr(reference_pkg.r_svd, "__wrapped_gpu__", False)
+
+
+def test_multi_gpu_launcher_validates_before_touching_a_device():
+    """pbp_qlp_multi_gpu keeps pbp_qlp's argument contract (algorithms.py:239-241)
+    and fails loudly without CUDA (no CPU path)."""
+    import numpy as np
+    import torch
+
+    from paper_2103_07245_b200 import DeviceError, MatrixInputError, ParameterError, pbp_qlp_multi_gpu
+    from paper_2103_07245_b200.multigpu import usable_world
+
+    a = np.ones((30, 20))
+    with pytest.raises(ParameterError):
+        pbp_qlp_multi_gpu(a, 21)
+    bad = a.copy()
+    bad[3, 4] = np.inf
+    with pytest.raises(MatrixInputError):
+        pbp_qlp_multi_gpu(bad, 0)
+    with pytest.raises(ParameterError):
+        pbp_qlp_multi_gpu(a, 5, backend="mpi")
+    if not torch.cuda.is_available():
+        with pytest.raises(DeviceError):
+            pbp_qlp_multi_gpu(a, 5)
+    assert [usable_world(200000, 512, n) for n in (1, 2, 4, 8)] == [1, 2, 4, 8]
+    assert usable_world(1000, 512, 8) == 1

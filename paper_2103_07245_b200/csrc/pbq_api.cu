@@ -547,6 +547,12 @@ struct CqPlan {
 };
 
 constexpr double CQ_KAPPA_MAX = 1e6;
+// basis-only calls (cq_launch with Out): B = X·R₁⁻¹ only has to be a
+// well-conditioned basis of range(X), ‖BᵀB − I‖ ≈ κ₂²u — 1e-2 at κ₂ = 1e7 —
+// and its rounding error u·κ₂ relative to ‖B‖ is that of any QR of X.  κ₁ (the
+// 1-norm estimate the guard computes) runs a few times above κ₂; beyond the
+// limit the Cholesky factorization itself starts to break down (pivot test).
+constexpr double CQ_KAPPA_MAX_BASIS = 3e7;
 
 CqPlan cq_plan(const pbq_ctx* ctx, long m, long n) {
   CqPlan p;
@@ -728,11 +734,13 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   if (basis) {
     f.basis = 1;
     f.rank_flag = rank_flag;
+    f.kappa_max = CQ_KAPPA_MAX_BASIS;
   }
   PBQ_TRY(factor_launch(ctx, pl, f, st));
   PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, basis ? Out : Q1, basis ? ldo : pl.ldq1,
                              nullptr, gws, pl.gemm_ws, st, fallback, true));
   f.basis = 0;
+  f.kappa_max = CQ_KAPPA_MAX;
   if (!basis) {
     PBQ_TRY(gram_launch(ctx, pl, m, n, Q1, pl.ldq1, part, fallback, st, nullptr, ctl + 33, G, emax_slot(4)));
     f.pass = 2; f.R = R2; f.X = X2; f.R1 = R1; f.Rout = R; f.ldr = ldr; f.rank_flag = rank_flag;
@@ -879,6 +887,7 @@ int cqd_stage(pbq_ctx* ctx, int stage, long m, long n, double* A, long lda, doub
     ctx->launches += 1;
     f.pass = 1; f.R = R1; f.X = X1; f.counter = counter(1);
     f.basis = 1; f.rank_flag = rank_flag;
+    f.kappa_max = CQ_KAPPA_MAX_BASIS;
     PBQ_TRY(factor_launch(ctx, pl, f, st));
     PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, A, lda, X1, pl.np, 0.0, Q1, pl.ldq1, nullptr, gws, pl.gemm_ws, st,
                                fallback, true));

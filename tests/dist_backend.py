@@ -46,6 +46,7 @@ class NumpyBackend:
 
     # -- distributed Cholesky-QR2, restated for the CPU (pbq_cholqr2_dist) --
     KAPPA_MAX = 1e6  # the device guard (pbq_api.cu CQ_KAPPA_MAX)
+    KAPPA_MAX_BASIS = 3e7  # … of the basis-only stage 3 (CQ_KAPPA_MAX_BASIS)
 
     def cholqr2_dist_state(self, m, n):
         return {"G": torch.zeros((n, n), dtype=torch.float64), "fallback": torch.zeros(1, dtype=torch.int32)}
@@ -67,7 +68,7 @@ class NumpyBackend:
                 state["fallback"].fill_(1)
                 return
             r1i = sla.solve_triangular(r1, np.eye(r1.shape[0]), lower=False)
-            if not np.linalg.norm(r1, 1) * np.linalg.norm(r1i, 1) <= self.KAPPA_MAX:
+            if not np.linalg.norm(r1, 1) * np.linalg.norm(r1i, 1) <= (self.KAPPA_MAX_BASIS if stage == 3 else self.KAPPA_MAX):
                 state["fallback"].fill_(1)
                 return
             q1 = a.numpy() @ r1i

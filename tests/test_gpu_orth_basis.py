@@ -107,6 +107,39 @@ def test_guard_failure_hands_over_the_full_qr(cuda):
     assert np.abs(b.T @ b - np.eye(400)).max() < 1e-13
 
 
+def test_looser_guard_for_a_basis(cuda):
+    """κ₂ = 5e5 (κ₁, the guard's 1-norm estimate, runs ~10× higher) fails the
+    full QR's κ₁ ≤ 1e6 guard but stays on the one-pass route as a basis
+    (CQ_KAPPA_MAX_BASIS): B = Q·T with T within 1e-2 of I."""
+    from paper_2103_07245_b200 import device as D
+
+    ctx = D.context(cuda)
+    rng = np.random.default_rng(8)
+    x = _graded(rng, 6000, 200, 5e5)
+    stats = torch.zeros(4, dtype=torch.int32, device=cuda)
+    ctx.cholqr_stats(stats)
+    try:
+        b, flag = _basis(ctx, cuda, x)
+        assert stats.tolist()[:2] == [1, 0], "expected the one-pass route, no hand-over"
+        stats.zero_()
+        full = _dev_matrix(x, cuda)
+        D.householder_qr_(ctx, full)
+        torch.cuda.synchronize()
+        assert stats.tolist()[1] == 1, "the full QR of the same input should leave the Cholesky route"
+    finally:
+        ctx.cholqr_stats(None)
+    assert flag == 0
+    q, r = oracle_qr(x)
+    t = q.T @ b
+    assert np.abs(t.T @ t - np.eye(200)).max() < 1e-2
+    assert np.all(np.diag(t) > 0.9)
+    # range(B) = range(X) to the accuracy of any QR of X: the component of B outside range(Q) is ~ u·κ₂
+    assert np.abs(b - q @ t).max() < 1e-8
+    qb, _ = oracle_qr(b)
+    tol = conditioning_tolerance(r.T, strict=1e-10)
+    assert np.all(column_relative_error(qb, q) <= tol)
+
+
 def test_rank_flags(cuda):
     from paper_2103_07245_b200 import device as D
 

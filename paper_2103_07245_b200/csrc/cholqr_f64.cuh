@@ -96,6 +96,10 @@ struct CqArgs {
   int route_final;  // 1: last factorization of the shifted route (stats[3] counts it)
   int* fail_stats;  // optional: stats[1] counts hand-overs to Householder (also from intermediate passes)
   int chol_1warp;   // diagonal blocks: 0 pipelined two-warp routine, 1 one warp (cq_chol_inv32_warp), 2 lock-step two warps
+  int* basis_done;  // pass 2 of a basis-only call on the shifted route (may be null): set to 1 when Q₂ = Q₁·R₂⁻¹
+                    // is already a well-conditioned basis (G₂ near I, or max/min |diag R₂| ≤ basis_diag_max),
+                    // so the third pass can be skipped
+  double basis_diag_max;
   int basis;        // pass 1 of a basis-only call (no second pass): a passed guard completes the call
                     // (rank_flag ← 0: κ₁ ≤ kappa_max bounds every |R_ii|/|R_00| far above 1e-14)
 };
@@ -710,6 +714,13 @@ __device__ void cq_factor_body(const CqArgs& p, double* sm, double* s_rowbuf) {
           atomicAdd(p.stats + 2, 1);
           if (p.route_final) atomicAdd(p.stats + 3, 1);
         }
+        if (p.basis_done) {  // Q₁ was orthonormal to ~1e-5 already
+          *p.basis_done = 1;
+          if (p.fail_stats) {
+            atomicAdd(p.fail_stats, 1);
+            atomicAdd(p.fail_stats + 3, 1);
+          }
+        }
       }
     }
     return;
@@ -886,6 +897,41 @@ __device__ void cq_factor_body(const CqArgs& p, double* sm, double* s_rowbuf) {
       if (p.stats) {
         atomicAdd(p.stats, 1);
         if (p.route_final) atomicAdd(p.stats + 3, 1);
+      }
+    }
+    if (p.basis_done) {
+      // κ₂(Q₁) ≥ max/min |diag R₂| and runs within a small factor of it: below
+      // basis_diag_max the orthogonality defect of Q₂, ≈ κ₂(Q₁)²·u, is harmless in a basis
+      __shared__ double s_mx[CQ_THREADS / 32], s_mn[CQ_THREADS / 32];
+      double mx = 0.0, mn = INFINITY;
+      for (long i = tid; i < p.n; i += CQ_THREADS) {
+        const double di = fabs(__ldcg(p.R + i * np + i));
+        mx = fmax(mx, di);
+        mn = (di < mn) ? di : mn;  // NaN never lowers mn; it fails the comparison below through mx or mn = inf
+        if (!(di == di)) mx = INFINITY;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      }
+      if ((tid & 31) == 0) {
+        s_mx[warp] = mx;
+        s_mn[warp] = mn;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < CQ_THREADS / 32; ++w) {
+          mx = fmax(mx, s_mx[w]);
+          mn = fmin(mn, s_mn[w]);
+        }
+        if (mn > 0.0 && mx <= p.basis_diag_max * mn) {
+          *p.basis_done = 1;
+          if (p.fail_stats) {
+            atomicAdd(p.fail_stats, 1);
+            atomicAdd(p.fail_stats + 3, 1);
+          }
+        }
       }
     }
   }

@@ -553,6 +553,9 @@ constexpr double CQ_KAPPA_MAX = 1e6;
 // 1-norm estimate the guard computes) runs a few times above κ₂; beyond the
 // limit the Cholesky factorization itself starts to break down (pivot test).
 constexpr double CQ_KAPPA_MAX_BASIS = 3e7;
+// … and on the shifted route a basis-only call stops after its second pass when
+// max/min |diag R₂| ≤ this (κ₂(Q₁) within a small factor of it, Q₂'s defect ≈ κ₂(Q₁)²u ≲ 1e-4)
+constexpr double CQ_BASIS2_DIAG_MAX = 1e5;
 
 CqPlan cq_plan(const pbq_ctx* ctx, long m, long n) {
   CqPlan p;
@@ -667,6 +670,15 @@ __global__ void __launch_bounds__(256) copy_if_kernel(const int* __restrict__ ru
   }
 }
 
+// the shifted route of a basis-only call found Q₂ good enough: stop the route
+// (its remaining launches return at once) and keep Out as it is
+__global__ void basis_exit_kernel(const int* __restrict__ done, int* route, int* fallback) {
+  if (*done) {
+    *route = 0;
+    *fallback = 0;
+  }
+}
+
 // Out != nullptr: basis-only call (orth_basis_launch below).  Only the first
 // Cholesky-QR pass runs: Out = A·R₁⁻¹ = Q·R₂ with R₂ upper triangular,
 // positive diagonal, ‖R₂ᵀR₂ − I‖ ≲ κ₁²u ≤ 1e-4 — the same Q factor under any
@@ -687,6 +699,7 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
   Carve cv(ws, ws_bytes);
   // ctl: [0] fallback (stops the CholQR2 path), [1] [2] [16] [17] [18] grid-barrier
   // counters, [4:6] [20:22] [22:24] max|G − I| slots, [10] shifted route running,
+  // [14] basis-only call: the route's second pass is already a good basis,
   // [12] Householder requested (extended chain), [32..35] Gram slice-sum barriers,
   // [48] the Householder kernel's grid-barrier counter
   int* ctl = cv.take<int>(64);
@@ -771,12 +784,28 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
     CQ_DEBUG_SYNC("route 4");
     g.pass = 2; g.shift_mode = 0; g.G = G; g.R = R2; g.X = X2; g.R1 = R1; g.emax = emax_slot(20);
     g.Rout = Racc; g.ldr = pl.np; g.rout_full = 1; g.rank_flag = nullptr; g.stats = nullptr; g.counter = counter(17);
+    // basis-only: the second pass writes into Out, and when Q₂ is already a
+    // well-conditioned basis (κ₂(Q₁) small: decided on the device from R₂) the
+    // route ends there — four of its six m-row passes
+    double* Q2b = basis ? Out : Q2;
+    const long ldq2 = basis ? ldo : pl.ldq1;
+    if (basis) {
+      g.basis_done = ctl + 14;
+      g.basis_diag_max = CQ_BASIS2_DIAG_MAX;
+      g.rank_flag = rank_flag;  // diag(R₂)∘diag(R₁); the last factorization overwrites it when it runs
+    }
     PBQ_TRY(factor_launch(ctx, pl, g, st));
+    g.basis_done = nullptr;
     CQ_DEBUG_SYNC("route 5");
-    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q1, pl.ldq1, X2, pl.np, 0.0, Q2, pl.ldq1, nullptr, gws, pl.gemm_ws,
+    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q1, pl.ldq1, X2, pl.np, 0.0, Q2b, ldq2, nullptr, gws, pl.gemm_ws,
                                st, nullptr, true, route));
+    if (basis) {
+      basis_exit_kernel<<<1, 1, 0, st>>>(ctl + 14, route, fallback);
+      PBQ_CUDA(ctx, cudaGetLastError());
+      ctx->launches += 1;
+    }
     CQ_DEBUG_SYNC("route 6");
-    PBQ_TRY(gram_launch(ctx, pl, m, n, Q2, pl.ldq1, part, nullptr, st, route, ctl + 35, G, emax_slot(22)));
+    PBQ_TRY(gram_launch(ctx, pl, m, n, Q2b, ldq2, part, nullptr, st, route, ctl + 35, G, emax_slot(22)));
     CQ_DEBUG_SYNC("route 7");
     CQ_DEBUG_SYNC("route 8");
     g.R = R1; g.X = X1; g.R1 = Racc; g.emax = emax_slot(22);   // R = R₃·(R₂·R₁)
@@ -784,7 +813,7 @@ int cq_launch(pbq_ctx* ctx, long m, long n, double* A, long lda, double* R, long
     g.route_final = 1; g.counter = counter(18);
     PBQ_TRY(factor_launch(ctx, pl, g, st));
     CQ_DEBUG_SYNC("route 9");
-    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q2, pl.ldq1, X1, pl.np, 0.0, A, lda, nullptr, gws, pl.gemm_ws, st,
+    PBQ_TRY(gemm_launch<false>(ctx, m, n, n, 1.0, Q2b, ldq2, X1, pl.np, 0.0, A, lda, nullptr, gws, pl.gemm_ws, st,
                                nullptr, true, route));
     CQ_DEBUG_SYNC("route 10");
   }

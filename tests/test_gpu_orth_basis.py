@@ -100,11 +100,34 @@ def test_guard_failure_hands_over_the_full_qr(cuda):
     assert np.abs(np.tril(r, -1)).max() < 1e-13 * np.abs(r).max()
     assert np.all(np.diag(r) > 0)
     assert np.abs(b @ r - x).max() < 1e-13 * np.abs(x).max()
-    # the shifted route (n >= 384) likewise
-    x = _graded(rng, 3000, 400, 1e9)
-    b, flag = _basis(ctx, cuda, x)
+
+
+@pytest.mark.parametrize("kappa", [1e8, 1e11])
+def test_shifted_route_as_a_basis(cuda, kappa):
+    """n ≥ 384 beyond the Cholesky guard: the shifted route runs, and as a basis
+    it may stop after its second pass (κ₂(Q₁) small, decided on the device from
+    R₂: κ = 1e8 here) or run all three (κ = 1e11).  Either way B = Q·T with T
+    upper triangular near I, and qr(B) returns Q."""
+    from paper_2103_07245_b200 import device as D
+
+    ctx = D.context(cuda)
+    rng = np.random.default_rng(14)
+    x = _graded(rng, 3000, 400, kappa)
+    stats = torch.zeros(4, dtype=torch.int32, device=cuda)
+    ctx.cholqr_stats(stats)
+    try:
+        b, flag = _basis(ctx, cuda, x)
+        st = stats.tolist()
+    finally:
+        ctx.cholqr_stats(None)
     assert flag == 0
-    assert np.abs(b.T @ b - np.eye(400)).max() < 1e-13
+    assert st[0] == 1 and st[1] == 0 and st[3] == 1, st  # completed by the shifted route, no Householder hand-over
+    defect = np.abs(b.T @ b - np.eye(400)).max()
+    assert defect < (1e-4 if kappa < 1e10 else 1e-13), defect
+    q, r = oracle_qr(x)
+    qb, _ = oracle_qr(b)
+    tol = conditioning_tolerance(r.T, strict=1e-10)
+    assert np.all(column_relative_error(qb, q) <= tol)
 
 
 def test_looser_guard_for_a_basis(cuda):

@@ -1,7 +1,10 @@
 #!/usr/bin/env bash
-# One GPU session's captures for tools/summarize_profiles.py <tag>.
+# One GPU session's captures and their summaries (tools/summarize_profiles.py <tag>).
 # Run on the box:  gpurun -- 'bash tools/profile_round.sh <tag>'
 # Every ncu command runs only after the same command exited 0 without ncu.
+# The four .ncu-rep files together exceed what gpurun copies back (64 MiB), so
+# they are summarised on the box: the summaries land in gpurun_out/prof/ (copy
+# them into profiles/) and the reports are deleted unless KEEP_REPS=1.
 set -u
 TAG=${1:?tag}
 O=gpurun_out
@@ -22,4 +25,7 @@ $NCU --set full --import-source on -k regex:cholqr_factor_kernel --launch-skip 4
 python tools/sketch_probe.py > $O/${TAG}_sketch_probe.txt 2>&1 || exit 1
 $NCU --set full --import-source on -k regex:sketch_k -c 3 -f -o $O/${TAG}_sketch \
   python tools/sketch_probe.py > $O/${TAG}_ncu_sketch.log 2>&1
+python tools/summarize_profiles.py $TAG > $O/${TAG}_summarize.log 2>&1
+mkdir -p $O/prof && cp profiles/${TAG}_* $O/prof/
+[ "${KEEP_REPS:-0}" = 1 ] || rm -f $O/${TAG}_*.ncu-rep
 echo done

@@ -119,13 +119,16 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
   constexpr uint32_t TM_COLS = TM_NEED <= 32 ? 32 : TM_NEED <= 64 ? 64 : TM_NEED <= 128 ? 128 : TM_NEED <= 256 ? 256 : 512;
   static_assert(TM_NEED <= 512, "TMEM holds 512 columns");
   __shared__ uint32_t s_tmem;
-  if constexpr (FOLD) {
+  // a fold needs a k-block chain longer than the first stagger step (FOLD_KB/4):
+  // the short products of the QR chain (K = n ≤ 256) never fold and skip TMEM
+  const bool use_tmem = FOLD && p.k_iters > FOLD_KB / 4;
+  if (use_tmem) {
     if (warp == 0) tmem_alloc(&s_tmem, TM_COLS);
     tmem_fence_before_sync();
   }
   __syncthreads();
   uint32_t tm_mine = 0;  // this warp's columns in its lane quarter
-  if constexpr (FOLD) {
+  if (use_tmem) {
     tmem_fence_after_sync();
     tm_mine = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(warp >> 2) * uint32_t(ACC_D * 2);
   }
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
       ++cflat;
       produce();
       if constexpr (FOLD) {
-        if ((kbk + 1 - seg.kb + (warp >> 2) * (FOLD_KB / 4)) % FOLD_KB == 0 && kbk + 1 < seg.ke) fold();
+        if (use_tmem && (kbk + 1 - seg.kb + (warp >> 2) * (FOLD_KB / 4)) % FOLD_KB == 0 && kbk + 1 < seg.ke) fold();
       }
     }
     if constexpr (FOLD) {
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
       }
     }
   }
-  if constexpr (FOLD) {  // every warp's TMEM traffic has completed (loads waited, stores waited)
+  if (use_tmem) {  // every warp's TMEM traffic has completed (loads waited, stores waited)
     tmem_fence_before_sync();
     __syncthreads();
     tmem_fence_after_sync();

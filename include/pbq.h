@@ -112,7 +112,7 @@ int pbq_qr_workspace_bytes(pbq_ctx* ctx, int64_t m, int64_t n, size_t* bytes);
  * QR of A_next·B has the Q factor of A_next·Q (right-multiplication by T
  * leaves it unchanged), so the following orth returns what the reference
  * computes, at half the passes of this one.  rank_flag as for
- * pbq_householder_qr.  A is used as scratch.  Where the chain is not the
+ * pbq_householder_qr.  A is used as scratch and must not alias Out.  Where the chain is not the
  * route (single-launch sizes, the Householder method, a failed guard, or
  * pbq_set_basis_orth(ctx, 0)) the full QR runs and Out = Q.  Workspace:
  * pbq_qr_workspace_bytes(m, n). */

@@ -1932,6 +1932,7 @@ int pbq_orth_basis(pbq_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, d
   if (!ctx || !A || !Out) return PBQ_ERR_PARAM;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (ldo < n) return fail(ctx, PBQ_ERR_PARAM, "orth_basis: leading dimension too small");
+  if (Out == A) return fail(ctx, PBQ_ERR_PARAM, "orth_basis: Out must not alias A (the product runs out of place)");
   double* res = nullptr;
   long ldres = 0;
   PBQ_TRY(orth_basis_launch(ctx, m, n, A, lda, Out, ldo, rank_flag, ws, ws_bytes, st, &res, &ldres));

@@ -8,7 +8,8 @@ graph replays.  The per-rank time T_N is the N-GPU step without the
 inter-GPU transfer; the model adds the transfer at a stated NVLink bus
 bandwidth:
 
-    comm_N = (q+1)·allreduce(n2·d·8 B) + 2(2q+1+1)·allreduce(d²·8 B)
+    comm_N = (q+1)·allreduce(n2·d·8 B) + (4 + 2q)·allreduce(d²·8 B)
+             (two Gram exchanges per full Cholesky-QR2, one per basis-only intermediate orth)
     allreduce(b) = 2·(N−1)/N · b / BW_bus,  BW_bus = 600 GB/s (NVLink 5 ring,
     conservative vs. 900 GB/s per direction)
 
@@ -77,7 +78,9 @@ def main():
         if n == 1:
             t1 = ms
         big = (q + 1) * n2 * d * 8
-        small = 2 * (2 * q + 2) * d * d * 8
+        # Gram allreduces: two per full distributed Cholesky-QR2 (the last orth(C) and qr(A·P̄)),
+        # one per basis-only intermediate orth (2q of them when q ≥ 1; pbq_cholqr2_dist stage 3)
+        small = (2 * 2 + 2 * q if q >= 1 else 2 * 2) * d * d * 8
         comm_ms = 0.0 if n == 1 else 1e3 * 2 * (n - 1) / n * (big + small) / BW_BUS
         line = {"workload": args.workload, "n1": n1, "n2": n2, "d": d, "q": q, "N": n, "shard_rows": m,
                 "per_rank_ms": round(ms, 3), "per_rank_tflops": round(flops / n / ms / 1e9, 2),

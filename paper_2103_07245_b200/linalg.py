@@ -100,9 +100,24 @@ def to_device_matrix(m, name, device=None):
     return h.kind, h.to_device(device), h.array, h.home
 
 
+# device → numpy results of at least this size travel through a pinned host
+# buffer (one DMA at link speed; the runtime's pageable path moves a 41 MB
+# factor in 19 ms, ~2 GB/s, against 1 ms)
+PINNED_D2H_MIN_BYTES = 1 << 20
+
+
 def from_device(t, kind, home=None):
     """Return a device result in the caller's array type."""
     if kind == "numpy":
+        if t.is_cuda and t.numel() * t.element_size() >= PINNED_D2H_MIN_BYTES:
+            try:
+                buf = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+            except RuntimeError:  # no pinned memory left: the pageable path
+                buf = None
+            if buf is not None:
+                buf.copy_(t, non_blocking=True)
+                torch.cuda.current_stream(t.device).synchronize()
+                return buf.numpy()
         return t.cpu().numpy() if t.is_contiguous() else t.contiguous().cpu().numpy()
     t = t.contiguous()
     if home is not None and torch.device(home) != t.device:

@@ -1,0 +1,79 @@
+"""Randomized sweep of the basis-only orth (``pbq_orth_basis``, the
+intermediate ``orth`` calls of algorithms.py:196-205): random m ≥ n up to 600
+columns (every route: the in-place single-launch kernels, the one-pass chain,
+the looser basis guard, the shifted route with and without its early exit,
+the Householder hand-over), condition numbers from 1 to 1e15 with graded,
+clustered and rank-deficient spectra.
+
+What an intermediate basis B must satisfy, checked against LAPACK:
+  * the rank flag of the reference's rank test;
+  * for numerically full-rank inputs: B = Q·T with T = QᵀB upper triangular
+    with a positive diagonal and κ₂(B) ≤ 1.5 (a well-conditioned operand for
+    the next pass), and qr(B) returns Q itself — per column within
+    max(1e-10, 64·u·κ_j, 8× LAPACK's own noise on a row-permuted input).
+PBQ_FUZZ_CASES sets the count (default 60)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.pbp_qlp_oracle import column_relative_error, oracle_qr, rank_flag
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+
+
+def _matrix(seed):
+    rng = np.random.default_rng(9000 + seed)
+    n = int(rng.choice([rng.integers(1, 129), rng.integers(129, 385), rng.integers(385, 601)]))
+    m = int(max(n, rng.choice([n + rng.integers(0, 64), rng.integers(n, 1500), rng.integers(1500, 12001)])))
+    kind = rng.choice(["graded", "clustered", "deficient", "gaussian"], p=[0.5, 0.2, 0.1, 0.2])
+    logk = float(rng.uniform(0, 15))
+    if kind == "gaussian":
+        return rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-3, 3), str(kind)
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    if kind == "graded":
+        s = np.logspace(0, -logk, n)
+    elif kind == "clustered":
+        s = np.where(np.arange(n) < n // 2, 1.0, 10.0 ** -logk)
+    else:
+        s = np.where(np.arange(n) < max(1, n // 3), 1.0, 0.0)
+    return (u * s) @ v.T, str(kind)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PBQ_FUZZ_CASES", "60"))))
+def test_random_basis(cuda, seed):
+    from paper_2103_07245_b200 import device as D
+
+    x, kind = _matrix(seed)
+    m, n = x.shape
+    ctx = D.context(cuda)
+    t = D.empty_matrix(m, n, cuda)
+    t.copy_(torch.from_numpy(x))
+    flag = torch.full((1,), -1, dtype=torch.int32, device=cuda)
+    b = D.orth_basis_(ctx, t, rank_flag=flag).cpu().numpy()
+    fl = int(flag.item())
+    qref, rref = oracle_qr(x)
+    what = (m, n, kind)
+    assert fl == rank_flag(rref), (what, "rank flag", fl, rank_flag(rref))
+    if fl != 0:
+        return
+    sv = np.linalg.svd(b, compute_uv=False)
+    assert sv[0] / sv[-1] <= 1.5, (what, "kappa(B)", sv[0] / sv[-1])
+    d = np.abs(np.diag(rref))
+    kap = d[0] / d
+    tmat = qref.T @ b
+    assert np.all(np.diag(tmat) > 0.5), (what, "diag T")
+    # strictly lower part of T: zero up to the accuracy of LAPACK's own trailing columns
+    low = np.abs(np.tril(tmat, -1)).max(axis=1)
+    assert np.all(low <= np.maximum(1e-9, 1024 * U * kap)), (what, "T not upper triangular", low.max())
+    perm = np.random.default_rng(seed).permutation(m)
+    qalt, _ = oracle_qr(x[perm])
+    noise = np.maximum.accumulate(column_relative_error(qalt[np.argsort(perm)], qref))
+    qb, _ = oracle_qr(b)
+    err = column_relative_error(qb, qref)
+    tol = np.maximum(np.maximum(1e-10, 64 * U * kap), 8 * noise)
+    det = kap <= 1e8
+    assert np.all(err[det] <= tol[det]), (what, "Q of qr(B)", int(np.argmax(err / tol)), err.max())

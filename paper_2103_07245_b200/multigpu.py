@@ -10,8 +10,12 @@ memory, runs the row-sharded driver (:class:`DistributedPbpQlp`, SURVEY.md
 buffers.  Arguments, errors, warnings and the returned :class:`QlpFactors`
 are those of ``pbp_qlp``.
 
-Under ``torchrun`` (one process per GPU already running, A already sharded)
-use :class:`DistributedPbpQlp` directly, as ``bench.py --gpus N`` does.
+Every call starts its own workers: seconds of process start-up (importing
+torch, creating the CUDA contexts and the NCCL communicator) before the first
+kernel, which only a large A amortises.  A service that factors many matrices
+keeps one process per GPU alive instead — ``torchrun`` with
+:class:`DistributedPbpQlp`, A already sharded, as ``bench.py --gpus N`` does
+(its plan objects and CUDA graphs are reused from call to call).
 """
 import os
 import socket

@@ -34,6 +34,7 @@ struct __align__(64) GemmTmaArgs {
   // dimension, byte stride 128) and one copy loads the whole tile in the same
   // shared-memory layout as the per-group boxes (cols a multiple of 16)
   int a3d, b3d;
+  int a_policy;  // 1: A loaded with the evict_first L2 policy (3-D copies only; A/B experiment)
 };
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
@@ -49,6 +50,30 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
           dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+// The same copies with an L2 cache-policy operand (createpolicy).  A/B
+// experiment (PBQ_GEMM_A_POLICY=1): the streamed A operand loaded evict_first
+// so that it does not push the thin, re-read B operand out of L2.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], "
+      "[%4], %5;\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4}], [%5], %6;\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
@@ -222,7 +247,13 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) gemm_f64_tma(co
     const uint32_t bar = smem_u32(&full_bar[stage]);
     mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
     const int k0 = prod.k * BK, m0 = prod.seg.tm * BM, n0 = prod.seg.tn * BN;
-    if (pa.a3d) {
+    if (pa.a3d && pa.a_policy) {
+      const uint64_t pol_a = l2_policy_evict_first();
+      if (TRANS_A)
+        tma_load_3d_hint(sa, &pa.ta, 0, k0, m0 / 16, bar, pol_a);
+      else
+        tma_load_3d_hint(sa, &pa.ta, 0, m0, k0 / 16, bar, pol_a);
+    } else if (pa.a3d) {
       if (TRANS_A)
         tma_load_3d(sa, &pa.ta, 0, k0, m0 / 16, bar);
       else

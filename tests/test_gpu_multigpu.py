@@ -95,3 +95,14 @@ def test_reference_callers_reach_the_launcher(cuda, reference_pkg):
     assert np.all(column_relative_error(f.q_basis, ref.q_basis) <= tol)
     assert np.all(column_relative_error(f.p_basis, ref.p_basis) <= tol)
     assert f.sketch.passes_over_a == ref.sketch.passes_over_a == 4
+
+
+@pytest.mark.timeout(300)
+def test_a_failing_rank_fails_the_call(cuda):
+    """A rank that raises takes the job down (no rank is left waiting in a
+    collective) and the parent reports what the rank recorded."""
+    from paper_2103_07245_b200 import DeviceError, pbp_qlp_multi_gpu
+
+    with pytest.raises(DeviceError, match="rank"):
+        # an exchange name the sharded driver rejects: every rank raises in its constructor
+        pbp_qlp_multi_gpu(_matrix(5, 400, 300), 16, q=1, devices=[0, 0], backend="gloo", exchange="bogus")

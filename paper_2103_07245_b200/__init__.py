@@ -9,7 +9,7 @@ from .algorithms import (PbpQlpPlan, QlpFactors, SketchRecord, clear_plan_cache,
                          pbp_qlp_flops, reconstruction_error, residual_norms)
 from .exceptions import (ConvergenceError, DeviceError, DimensionError, MatrixInputError, ParameterError,
                          RankDeficiencyWarning)
-from .multigpu import pbp_qlp_multi_gpu
+from .multigpu import MultiGpuPool, pbp_qlp_multi_gpu
 from .linalg import QrFactors, column_pivoted_qr, gaussian_matrix, householder_qr, orth
 from .rsvd import RsvdFactors, r_svd
 from .utv import UtvFactors, cor_utv
@@ -21,6 +21,7 @@ __all__ = [
     "DeviceError",
     "DimensionError",
     "MatrixInputError",
+    "MultiGpuPool",
     "ParameterError",
     "PbpQlpPlan",
     "QlpFactors",

@@ -106,3 +106,33 @@ def test_a_failing_rank_fails_the_call(cuda):
     with pytest.raises(DeviceError, match="rank"):
         # an exchange name the sharded driver rejects: every rank raises in its constructor
         pbp_qlp_multi_gpu(_matrix(5, 400, 300), 16, q=1, devices=[0, 0], backend="gloo", exchange="bogus")
+
+
+@pytest.mark.timeout(600)
+def test_pool_serves_many_calls(cuda):
+    """MultiGpuPool: the workers start once and serve several factorizations
+    (different seeds and shapes, a NaN input in between), each equal to the
+    one-shot call's contract."""
+    from paper_2103_07245_b200 import MatrixInputError, MultiGpuPool, pbp_qlp
+
+    a = _matrix(31, 1200, 600)
+    b = _matrix(32, 800, 900)
+    with MultiGpuPool([0, 0], backend="gloo") as pool:
+        assert pool.world == 2
+        for m, d, q, seed in ((a, 40, 1, 1), (a, 40, 1, 2), (b, 64, 2, 3), (a, 40, 1, 1)):
+            got = pool.pbp_qlp(m, d, q=q, seed=seed)
+            one = pbp_qlp(m, d, q=q, seed=seed)
+            ref = oracle_pbp_qlp(m, d, q=q, seed=seed)
+            tol = conditioning_tolerance(ref["l"], strict=1e-10)
+            assert np.array_equal(got.sketch.test_matrix, ref["phi"])
+            assert np.all(column_relative_error(got.q_basis, ref["q"]) <= tol)
+            assert np.all(column_relative_error(got.p_basis, one.p_basis) <= tol)
+        bad = a.copy()
+        bad[1000, 3] = np.inf
+        with pytest.raises(MatrixInputError):
+            pool.pbp_qlp(bad, 40, q=1)
+        again = pool.pbp_qlp(a, 40, q=1, seed=1)  # the pool survives a rejected input
+        assert np.array_equal(again.sketch.test_matrix, oracle_pbp_qlp(a, 40, q=1, seed=1)["phi"])
+        short = pool.pbp_qlp(_matrix(7, 90, 300), 64, q=1, seed=4)  # too short to shard: the single-GPU path
+        assert short.q_basis.shape == (90, 64)
+    assert pool.procs == []

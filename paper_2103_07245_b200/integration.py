@@ -100,21 +100,31 @@ def make_cpqr_dropin(pbpqlp):
 
 def make_dropin(pbpqlp, devices=None, backend="nccl"):
     """Return a reference-typed ``pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True)``.
-    ``devices`` (a list of CUDA indices, more than one): the call is row-sharded
-    over those GPUs by ``pbp_qlp_multi_gpu`` (one worker process per GPU)."""
+    ``devices`` (a list of CUDA indices, more than one): the calls are row-sharded
+    over those GPUs by a ``MultiGpuPool`` (one worker process per GPU, started by
+    the first call, stopped by ``uninstall`` or at exit)."""
     ref_alg = pbpqlp.algorithms
     ref_exc = pbpqlp.exceptions
     multi = devices is not None and len(devices) > 1
+    holder = {"pool": None}  # the worker pool, started by the first call and kept until uninstall / exit
+
+    def _pool():
+        import atexit
+
+        from .multigpu import MultiGpuPool
+
+        pool = holder["pool"]
+        if pool is None or pool.broken:
+            pool = holder["pool"] = MultiGpuPool(devices, backend)
+            atexit.register(pool.close)
+        return pool
 
     def pbp_qlp(a, d, q=0, seed=0, reorthonormalize=True):
         with warnings.catch_warnings(record=True) as rec:
             warnings.simplefilter("always", _exc.RankDeficiencyWarning)
             try:
                 if multi:
-                    from .multigpu import pbp_qlp_multi_gpu
-
-                    f = pbp_qlp_multi_gpu(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize, devices=devices,
-                                          backend=backend)
+                    f = _pool().pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
                 else:
                     f = _alg.pbp_qlp(a, d, q=q, seed=seed, reorthonormalize=reorthonormalize)
             except _exc.DimensionError as e:
@@ -134,6 +144,7 @@ def make_dropin(pbpqlp, devices=None, backend="nccl"):
 
     pbp_qlp.__doc__ = ref_alg.pbp_qlp.__doc__
     pbp_qlp.__wrapped_gpu__ = True
+    pbp_qlp.__pool_holder__ = holder
     return pbp_qlp
 
 
@@ -159,4 +170,9 @@ def uninstall(saved):
     import sys
 
     for (modname, name), fn in saved.items():
+        current = getattr(sys.modules[modname], name, None)
+        holder = getattr(current, "__pool_holder__", None)
+        if holder and holder.get("pool") is not None:  # stop the multi-GPU workers of the drop-in
+            holder["pool"].close()
+            holder["pool"] = None
         setattr(sys.modules[modname], name, fn)

@@ -86,8 +86,13 @@ def test_reference_callers_reach_the_launcher(cuda, reference_pkg):
     saved = integration.install(reference_pkg, devices=[0, 0], backend="gloo")
     try:
         f = reference_pkg.pbp_qlp(a, 40, q=1, seed=5)
+        pool = reference_pkg.pbp_qlp.__pool_holder__["pool"]
+        f2 = reference_pkg.pbp_qlp(a, 40, q=1, seed=6)  # the same workers serve the next call
+        assert reference_pkg.pbp_qlp.__pool_holder__["pool"] is pool and len(pool.procs) == 2
+        assert not np.array_equal(f2.sketch.test_matrix, f.sketch.test_matrix)
     finally:
         integration.uninstall(saved)
+    assert pool.procs == []  # uninstall stopped them
     assert type(f).__module__.startswith("pbpqlp")
     ref = reference_pkg.pbp_qlp(a, 40, q=1, seed=5)
     tol = conditioning_tolerance(ref.l, strict=1e-10)

@@ -157,3 +157,15 @@ def test_multi_gpu_launcher_validates_before_touching_a_device():
             pbp_qlp_multi_gpu(a, 5)
     assert [usable_world(200000, 512, n) for n in (1, 2, 4, 8)] == [1, 2, 4, 8]
     assert usable_world(1000, 512, 8) == 1
+
+
+def test_multi_gpu_pool_fails_loudly_without_cuda():
+    import torch
+
+    from paper_2103_07245_b200 import DeviceError, MultiGpuPool, ParameterError
+
+    with pytest.raises(ParameterError):
+        MultiGpuPool([0, 1], backend="mpi")
+    if not torch.cuda.is_available():
+        with pytest.raises(DeviceError):
+            MultiGpuPool([0, 1])

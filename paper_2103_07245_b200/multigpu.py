@@ -175,7 +175,9 @@ class MultiGpuPool:
     contexts, the NCCL communicator, the sharded driver's buffers per shape)
     are started once — seconds — and reused.  Use as a context manager or call
     :meth:`close`.  After a rank fails, the pool is closed and every later
-    call raises :class:`DeviceError`.
+    call raises :class:`DeviceError`.  The workers are started with the
+    ``spawn`` method (CUDA cannot be forked): a script that creates a pool at
+    import time must do so under ``if __name__ == "__main__":``.
     """
 
     def __init__(self, devices=None, backend="nccl", exchange="nccl", start_timeout_s=300.0):
